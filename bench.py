@@ -1,0 +1,316 @@
+"""Benchmark of the grid max-flow / assignment hot path (one JSON line on rank 0).
+
+Workload (N = 1): BASELINE.json's metric "grid max-flow Medges/s & solve ms at
+4096^2; assignment solve ms at n=4096".  A step = one complete max-flow + min-cut
+solve of a 4096 x 4096 4-connected grid (generator G), inputs
+resident in HBM.  value = Medges/s = E_grid / solve seconds, E_grid =
+2(2HW - H - W) + 2HW.  The n = 4096 assignment solve is reported beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank solves its own 4096^2 instance (seed 4096 +
+rank): independent replicas, weak scaling; time = max over ranks.
+``--impl reference`` times the reference algorithm's CPU port (oracle/, C
+restatement of hybrid_solve with real threads) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid max-flow Medges/s & solve ms at 4096²; assignment solve ms at n=4096"
+UNIT = "Medges/s"
+
+
+def e_grid(H: int, W: int) -> int:
+    return 2 * (2 * H * W - H - W) + 2 * H * W
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (the recipe's clocks line)."""
+
+    def __init__(self, device: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) > 8 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 8 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) > 8:
+                for k, v in zip(names, r[5:9]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline_grid(threads: int):
+    """Reference hybrid_solve restated in C (oracle/), all host threads, bounded sample."""
+    import oracle
+    from paper_1110_6231_b200 import generators as G
+
+    S = 512
+    caps = G.grid_random(S, S, S)
+    t = time.perf_counter()
+    d = oracle.grid_maxflow(*caps, solver="hybrid", worker_count=threads)
+    dt = time.perf_counter() - t
+    t = time.perf_counter()
+    d1 = oracle.grid_maxflow(*caps, solver="seq")
+    dts = time.perf_counter() - t
+    assert d["value"] == d1["value"]
+    return {"value": round(e_grid(S, S) / dt / 1e6, 4), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"generator G {S}x{S} seed {S}: hybrid_solve port (oracle/fm_oracle.c, "
+                      f"{threads} threads, cycle_budget 7000) solve {dt:.2f}s",
+            "seq_port_medges_s": round(e_grid(S, S) / dts / 1e6, 4),
+            "seq_port_sample": f"solve_maxflow_seq port, 1 thread, {dts:.2f}s"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    import oracle
+    from paper_1110_6231_b200 import generators as G
+
+    S = args.ref_size
+    caps = G.grid_random(S, S, S)
+    for _ in range(args.warmup):
+        oracle.grid_maxflow(*caps, solver="hybrid", worker_count=threads)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        d = oracle.grid_maxflow(*caps, solver="hybrid", worker_count=threads)
+        times.append(time.perf_counter() - t)
+    ms = 1000 * statistics.mean(times)
+    v = e_grid(S, S) / (ms / 1000) / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": f"grid max-flow + min-cut, generator G {S}x{S} seed {S} "
+                                   f"(bounded CPU sample of the 4096^2 workload)", "flow": d["value"]},
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"hybrid_solve restated in C (oracle/fm_oracle.c), {threads} threads, "
+                                       f"generator G {S}x{S}"},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=4096)
+    ap.add_argument("--assign-n", type=int, default=4096)
+    ap.add_argument("--ref-size", type=int, default=512)
+    ap.add_argument("--bfs-interval", type=int, default=0)
+    ap.add_argument("--no-assign", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1110_6231_b200 as fmb
+    from paper_1110_6231_b200 import generators as G
+
+    S = args.size
+    seed = S + rank
+    caps_h = [np.ascontiguousarray(c) for c in G.grid_random(S, S, seed)]
+    caps_d = [torch.from_numpy(c).cuda() for c in caps_h]
+    cut_d = torch.empty((S, S), dtype=torch.uint8, device="cuda")
+    solver = fmb.GridSolver(S, S, device=local)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return solver.solve_device(caps_d, 7000, args.bfs_interval, cut_out=cut_d, stream=stream)
+
+    flows = set()
+    for _ in range(args.warmup):
+        f, _ = step()
+        flows.add(f)
+    clocks = Clocks(local)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    agg = {}
+    ev0.record(stream)
+    for _ in range(args.steps):
+        f, st = step()
+        flows.add(f)
+        for k, v in st.items():
+            if isinstance(v, (int, float)):
+                agg[k] = agg.get(k, 0) + v
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    value = ws * e_grid(S, S) / (ms_step / 1000.0) / 1e6
+    assert len(flows) == 1, f"flow changed across steps: {flows}"
+    flow = flows.pop()
+
+    # roofline of the dominant kernel (per launch: algorithmic bytes / mean duration)
+    HW = S * S
+    peak, peak_src = measured_peak_hbm()
+    K = args.steps
+    pr_ms, bfs_ms = agg.get("ms_pr_kern", 0.0), agg.get("ms_bfs_kern", 0.0)
+    if pr_ms >= bfs_ms:
+        launches = max(1, agg.get("pr_launches", 1))
+        bytes_per_launch = (32 * HW * agg.get("pr_sweeps", 0) + 16 * agg.get("pushes", 0)) / launches
+        dur = pr_ms / launches
+        kname = "pr_sweep_kernel"
+    else:
+        launches = max(1, agg.get("bfs_launches", 1))
+        bytes_per_launch = 9 * HW
+        dur = bfs_ms / launches
+        kname = "bfs_tile_kernel"
+    achieved = bytes_per_launch / (dur / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "kernel": kname,
+                "peak_source": peak_src, "bytes_per_launch": int(bytes_per_launch),
+                "launch_ms": round(dur, 5), "kernel_share_of_step": round((pr_ms if kname == 'pr_sweep_kernel' else bfs_ms) / max(1e-9, ms_total), 3)}
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pinned = [torch.from_numpy(c).pin_memory().numpy() for c in caps_h]
+        net = fmb.build_grid_network(*pinned)
+        fmb.hybrid_solve(net)  # warm (workspace allocation)
+        times = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep = fmb.hybrid_solve(net)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            assert rep.objective == flow
+        tt = torch.tensor([statistics.mean(times)], dtype=torch.float64, device="cuda")
+        if ws > 1:
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": round(ws * e_grid(S, S) / float(tt.item()) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": 6 * 4 * HW, "d2h_bytes_per_step": HW + 8,
+               "ms_per_step": round(1000 * float(tt.item()), 3),
+               "api": "paper_1110_6231_b200.hybrid_solve(build_grid_network(*pinned host planes))"}
+
+    # assignment n = 4096 (single GPU; replicas only)
+    assign = None
+    if not args.no_assign and rank == 0:
+        n = args.assign_n
+        assign = {}
+        asolver = fmb.AssignmentSolver(n, device=local)
+        for name, w in (("optical_flow", G.assignment_optical_flow(n, n)),
+                        ("reference_generate_M100", G.assignment_reference(n, 100, n)),
+                        ("reference_generate_M10000", G.assignment_reference(n, 10000, n))):
+            wd = torch.from_numpy(w).cuda()
+            for _ in range(2):
+                asolver.solve_device(wd, stream=stream)
+            ts = []
+            for _ in range(max(1, args.steps)):
+                torch.cuda.synchronize()
+                a0 = torch.cuda.Event(enable_timing=True)
+                a1 = torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                obj, m, _, st = asolver.solve_device(wd, stream=stream)
+                a1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a0.elapsed_time(a1))
+            assert sorted(m.tolist()) == list(range(n))
+            t0 = time.perf_counter()
+            rep, _ = fmb.solve_assignment(w)
+            e2e_ms = 1000 * (time.perf_counter() - t0)
+            assign[name] = {"solve_ms": round(statistics.mean(ts), 3), "objective": obj,
+                            "e2e_ms": round(e2e_ms, 3), "pushes": st["pushes"], "relabels": st["relabels"],
+                            "rounds": st["rounds"], "tail_rounds": st["pr_sweeps"], "refines": st["refines"]}
+        asolver.close()
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and ws == 1:
+            cpu = cpu_baseline_grid(os.cpu_count() or 1)
+        per = {k: round(v / K, 3) if isinstance(v, float) else v // K for k, v in agg.items()
+               if k in ("pushes", "relabels", "rounds", "launches", "pr_sweeps", "bfs_sweeps", "bfs_levels",
+                        "cut_sweeps", "ms_total", "ms_push", "ms_bfs", "ms_cut", "ms_pr_kern", "ms_bfs_kern")}
+        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "config": {"workload": f"grid max-flow + min-cut {S}x{S} 4-connected, generator G "
+                                       f"(numpy PCG64 seed {S}+rank, caps 0..100)",
+                           "E_grid": e_grid(S, S), "flow": flow, "parallelism": f"replicas x{ws}",
+                           "l2": "inputs larger than L2 (6 x 64 MiB planes + 40 B/px state)",
+                           "cycle_budget": 7000, "bfs_interval": args.bfs_interval},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(agg.get("launches", 0)), "clocks": clk,
+                "per_solve": per, "assignment_n4096": assign}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,162 @@
+/*
+ * flowmatch_b200.h -- C ABI of the B200-native grid max-flow / dense assignment
+ * hot path (libfm_b200.so).  Plain pointers and sizes only; no torch types.
+ *
+ * Each entry point replaces one reference interface (reference package
+ * `flowmatch`, /root/reference/pkg/src/flowmatch):
+ *
+ *   fm_grid_solve / fm_grid_solve_host
+ *       replaces hybrid_solve(net, worker_count, cycle_budget, observer=None)
+ *       (maxflow_par.py:157-238) on 4-connected grid networks, which runs
+ *       hybrid_init (maxflow_par.py:44-62), init_preflow (maxflow_seq.py:47-64),
+ *       lockfree_round (maxflow_par.py:65-129), cancel_violations
+ *       (maxflow_par.py:132-154, opt-in flag), global_relabel + gap_relabel
+ *       (maxflow_seq.py:119-160) and the marking / ExcessTotal test
+ *       (maxflow_par.py:195,223-226).  Adds the minimal source-side cut the
+ *       reference does not expose.
+ *   fm_grid_begin / fm_grid_round / fm_grid_export
+ *       the same solve one coordinator round at a time, so the Python mirror
+ *       can honour hybrid_solve's observer(net, hybrid, scanned) hook
+ *       (maxflow_par.py:165-166,228-229).
+ *   fm_assign_solve / fm_assign_solve_host
+ *       replaces solve_assignment(inst, mode="par", ...) (assign_scaling.py:470-497)
+ *       = make_scaling_state (:127-142) + min_cost_loop (:400-467) with
+ *       begin_refine (:145-182), refine_par / lockfree_refine_round
+ *       (assign_par.py:45-237), arc_fix (:185-205), extract_matching (:380-397).
+ *
+ * Grid layout (all int32, H x W row-major, pixel p = r * W + c):
+ *   capR[p]  capacity p -> p+1   (last column must be 0)
+ *   capL[p]  capacity p -> p-1   (first column must be 0)
+ *   capD[p]  capacity p -> p+W   (last row must be 0)
+ *   capU[p]  capacity p -> p-W   (first row must be 0)
+ *   capS[p]  capacity s -> p,    capT[p] capacity p -> t;   all >= 0.
+ * This is the reference network built by the SURVEY.md 8d adapter (s = H*W,
+ * t = H*W + 1) with antiparallel pairs merged; value and minimal cut are equal.
+ *
+ * Status codes (Python mirror maps 1 -> InfeasibleInstanceError, 2 -> ValueError,
+ * 3/4 -> RuntimeError, as the reference raises at assign_scaling.py:44-45,
+ * maxflow_par.py:168-173, maxflow_par.py:213-214).
+ */
+#ifndef FLOWMATCH_B200_H
+#define FLOWMATCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FM_OK 0
+#define FM_INFEASIBLE 1
+#define FM_INVALID_ARG 2
+#define FM_CUDA_ERROR 3
+#define FM_NO_DEVICE 4
+
+/* grid solve flags */
+#define FM_GRID_CANCEL_VIOLATIONS 0x1 /* run the maxflow_par.py:132-154 pass each round */
+#define FM_GRID_NO_PRECANCEL 0x2      /* do not pre-route min(capS, capT) straight to t */
+#define FM_GRID_NO_CUT 0x4            /* skip the min-cut reach */
+
+/* assignment flags (match solve_assignment keyword arguments) */
+#define FM_ASSIGN_PRICE_UPDATE 0x1 /* use_price_update (assign_scaling.py:208-276) */
+#define FM_ASSIGN_ARC_FIX 0x2      /* use_arc_fix (assign_scaling.py:185-205) */
+#define FM_ASSIGN_VALIDATE 0x4     /* validate=True: device-side invariant checks */
+
+/* dense weight marking an absent arc (sparse instance, complete=False) */
+#define FM_ABSENT_WEIGHT INT32_MIN
+
+typedef struct fm_stats {
+    int64_t pushes;        /* SolveReport.pushes */
+    int64_t relabels;      /* SolveReport.relabels */
+    int64_t rounds;        /* SolveReport.rounds: coordinator passes */
+    int64_t launches;      /* kernels launched by this solve */
+    int64_t pr_sweeps;     /* push-relabel sweeps (grid) / refine phases (assign) */
+    int64_t bfs_sweeps;    /* global-relabel tile sweeps (grid) */
+    int64_t bfs_levels;    /* deepest residual distance seen by a global relabel */
+    int64_t cut_sweeps;    /* min-cut reach tile sweeps */
+    int64_t refines;       /* assignment: epsilon phases */
+    int64_t bytes_push;    /* algorithmic bytes moved by the push-relabel kernels */
+    int64_t bytes_bfs;     /* algorithmic bytes moved by global relabel + cut */
+    int64_t pr_tiles;      /* tile visits by the push-relabel kernel */
+    double ms_total;       /* device time of the whole solve (CUDA events) */
+    double ms_push;        /* push-relabel kernels */
+    double ms_bfs;         /* global relabel + gap + mark */
+    double ms_cut;         /* min-cut reach */
+    double ms_h2d;         /* *_host variants only */
+    double ms_d2h;         /* *_host variants only */
+    double ms_pr_kern;     /* push-relabel kernels alone (events around launch batches) */
+    double ms_bfs_kern;    /* global-relabel tile kernels alone */
+    int64_t pr_launches;   /* push-relabel kernel launches */
+    int64_t bfs_launches;  /* global-relabel tile kernel launches */
+    int64_t reserved[4];
+} fm_stats;
+
+/* ----------------------------------------------------------------- common */
+const char *fm_last_error(void);  /* thread-local message for the last failure */
+int fm_device_count(void);
+const char *fm_version(void);
+
+/* ------------------------------------------------------------------- grid */
+typedef struct fm_grid fm_grid;
+
+int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **out);
+void fm_grid_destroy(fm_grid *g);
+
+/* Whole solve on device.  cap* are DEVICE pointers (borrowed for the call).
+ * cycle_budget = max lock-free sweeps per coordinator round (reference
+ * DEFAULT_CYCLE_BUDGET 7000, maxflow_par.py:28).  bfs_interval = sweeps between
+ * global relabels inside a round (0 = library default).  flow_out: host int64.
+ * cut_out: DEVICE uint8[H*W] (1 = source side) or NULL.  stream: cudaStream_t
+ * or NULL for the library's own stream. */
+int fm_grid_solve(fm_grid *g, const int32_t *capR, const int32_t *capL,
+                  const int32_t *capD, const int32_t *capU, const int32_t *capS,
+                  const int32_t *capT, int32_t cycle_budget, int32_t bfs_interval,
+                  int32_t flags, int64_t *flow_out, uint8_t *cut_out,
+                  fm_stats *stats, void *stream);
+
+/* Same, HOST pointers (copies in and out are part of the call; cut_out host). */
+int fm_grid_solve_host(fm_grid *g, const int32_t *capR, const int32_t *capL,
+                       const int32_t *capD, const int32_t *capU, const int32_t *capS,
+                       const int32_t *capT, int32_t cycle_budget, int32_t bfs_interval,
+                       int32_t flags, int64_t *flow_out, uint8_t *cut_out,
+                       fm_stats *stats);
+
+/* Stepwise solve (observer support).  begin copies HOST capacities in and runs
+ * the preflow init + first global relabel; round runs one coordinator round
+ * (lock-free sweeps, then cancel (opt), global relabel, gap, mark) and sets
+ * *done when no unmarked pixel holds excess. */
+int fm_grid_begin(fm_grid *g, const int32_t *capR, const int32_t *capL,
+                  const int32_t *capD, const int32_t *capU, const int32_t *capS,
+                  const int32_t *capT, int32_t flags);
+int fm_grid_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval,
+                  int32_t *done, fm_stats *stats);
+/* Copy the current state to HOST buffers (any may be NULL).  rS = flow on s->p.
+ * marked = pixels written off by the gap step (maxflow_par.py:223-226). */
+int fm_grid_export(fm_grid *g, int32_t *rR, int32_t *rL, int32_t *rD, int32_t *rU,
+                   int32_t *rT, int32_t *rS, int32_t *e, int32_t *h, uint8_t *marked,
+                   int64_t *flow, int64_t *excess_total);
+/* Minimal source-side cut of the current state into a HOST buffer. */
+int fm_grid_cut_host(fm_grid *g, uint8_t *cut_out, fm_stats *stats);
+
+/* ------------------------------------------------------------- assignment */
+typedef struct fm_assign fm_assign;
+
+int fm_assign_create(int32_t n, int32_t device, fm_assign **out);
+void fm_assign_destroy(fm_assign *a);
+
+/* Dense max-weight perfect matching.  weights: DEVICE int32[n*n] row-major,
+ * weights[x*n+y] = w(x, y) or FM_ABSENT_WEIGHT.  alpha >= 2 (DEFAULT_ALPHA 10,
+ * assign_scaling.py:33).  objective_out: host int64.  match_out: HOST int32[n]
+ * (match_out[x] = y).  prices_out: HOST int64[2n] (X then Y) or NULL. */
+int fm_assign_solve(fm_assign *a, const int32_t *weights, int64_t alpha, int32_t flags,
+                    int64_t *objective_out, int32_t *match_out, int64_t *prices_out,
+                    fm_stats *stats, void *stream);
+/* Same with a HOST weight matrix (copy in is part of the call). */
+int fm_assign_solve_host(fm_assign *a, const int32_t *weights, int64_t alpha,
+                         int32_t flags, int64_t *objective_out, int32_t *match_out,
+                         int64_t *prices_out, fm_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLOWMATCH_B200_H */

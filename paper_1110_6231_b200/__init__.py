@@ -1,0 +1,53 @@
+"""flowmatch on B200: lock-free push-relabel grid max-flow / min-cut and cost-scaling
+dense assignment, as hand-written sm_100a CUDA behind a C ABI (libfm_b200.so).
+
+The public names mirror the reference package ``flowmatch`` for the hot path
+(``hybrid_solve``, ``solve_assignment``, ``SolveReport``, ``FlowNetwork``,
+``build_network``, ``AssignmentInstance``, ``InfeasibleInstanceError``, ...) so
+that callers switch by changing the import.  Grid graphs enter as
+:class:`GridNetwork` (structure-of-arrays capacities).
+"""
+
+from __future__ import annotations
+
+from . import generators
+from .assign import (
+    DEFAULT_ALPHA,
+    DEFAULT_ASSIGN_CYCLE,
+    AssignmentInstance,
+    AssignmentSolver,
+    InfeasibleInstanceError,
+    solve_assignment,
+)
+from .graph import (
+    FlowNetwork,
+    GridNetwork,
+    NetworkError,
+    SolveReport,
+    build_grid_network,
+    build_network,
+)
+from .maxflow import DEFAULT_CYCLE_BUDGET, GridSolver, hybrid_solve, min_cut
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AssignmentInstance",
+    "AssignmentSolver",
+    "DEFAULT_ALPHA",
+    "DEFAULT_ASSIGN_CYCLE",
+    "DEFAULT_CYCLE_BUDGET",
+    "FlowNetwork",
+    "GridNetwork",
+    "GridSolver",
+    "InfeasibleInstanceError",
+    "NetworkError",
+    "SolveReport",
+    "build_grid_network",
+    "build_network",
+    "generators",
+    "hybrid_solve",
+    "min_cut",
+    "solve_assignment",
+    "__version__",
+]

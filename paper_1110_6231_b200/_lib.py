@@ -1,0 +1,154 @@
+"""ctypes binding of libfm_b200.so (the C ABI declared in include/flowmatch_b200.h).
+
+The CUDA library is the only compute path: if it is missing or no CUDA device is
+visible, calls raise instead of falling back to anything on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfm_b200.so")
+
+FM_OK = 0
+FM_INFEASIBLE = 1
+FM_INVALID_ARG = 2
+FM_CUDA_ERROR = 3
+FM_NO_DEVICE = 4
+
+FM_GRID_CANCEL_VIOLATIONS = 0x1
+FM_GRID_NO_PRECANCEL = 0x2
+FM_GRID_NO_CUT = 0x4
+
+FM_ASSIGN_PRICE_UPDATE = 0x1
+FM_ASSIGN_ARC_FIX = 0x2
+FM_ASSIGN_VALIDATE = 0x4
+
+FM_ABSENT_WEIGHT = -(2**31)
+
+
+class FmStats(ctypes.Structure):
+    _fields_ = [
+        ("pushes", ctypes.c_int64),
+        ("relabels", ctypes.c_int64),
+        ("rounds", ctypes.c_int64),
+        ("launches", ctypes.c_int64),
+        ("pr_sweeps", ctypes.c_int64),
+        ("bfs_sweeps", ctypes.c_int64),
+        ("bfs_levels", ctypes.c_int64),
+        ("cut_sweeps", ctypes.c_int64),
+        ("refines", ctypes.c_int64),
+        ("bytes_push", ctypes.c_int64),
+        ("bytes_bfs", ctypes.c_int64),
+        ("pr_tiles", ctypes.c_int64),
+        ("ms_total", ctypes.c_double),
+        ("ms_push", ctypes.c_double),
+        ("ms_bfs", ctypes.c_double),
+        ("ms_cut", ctypes.c_double),
+        ("ms_h2d", ctypes.c_double),
+        ("ms_d2h", ctypes.c_double),
+        ("ms_pr_kern", ctypes.c_double),
+        ("ms_bfs_kern", ctypes.c_double),
+        ("pr_launches", ctypes.c_int64),
+        ("bfs_launches", ctypes.c_int64),
+        ("reserved", ctypes.c_int64 * 4),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
+        d["reserved"] = list(self.reserved)
+        return d
+
+
+# exported symbol -> (restype, argtypes); the tests check this list against the header
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+SIGNATURES = {
+    "fm_last_error": (ctypes.c_char_p, []),
+    "fm_device_count": (ctypes.c_int, []),
+    "fm_version": (ctypes.c_char_p, []),
+    "fm_grid_create": (ctypes.c_int, [_i32, _i32, _i32, ctypes.POINTER(_vp)]),
+    "fm_grid_destroy": (None, [_vp]),
+    "fm_grid_solve": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "fm_grid_solve_host": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32, _i32, _i32, _vp, _vp, _vp]),
+    "fm_grid_begin": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32]),
+    "fm_grid_round": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp]),
+    "fm_grid_export": (ctypes.c_int, [_vp] + [_vp] * 11),
+    "fm_grid_cut_host": (ctypes.c_int, [_vp, _vp, _vp]),
+    "fm_assign_create": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(_vp)]),
+    "fm_assign_destroy": (None, [_vp]),
+    "fm_assign_solve": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
+    "fm_assign_solve_host": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def build(force: bool = False) -> str:
+    """Compile libfm_b200.so in place with nvcc for sm_100a."""
+    cmd = ["make", "-s", "-C", _HERE]
+    if force:
+        subprocess.run(["make", "-s", "-C", _HERE, "clean"], check=True)
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def load():
+    """Load the library (never builds implicitly on a GPU box)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"CUDA extension {LIB_PATH} is missing; run __graft_entry__.build() "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    msg = load().fm_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str) -> None:
+    """Map C status codes onto the reference's exception types."""
+    if rc == FM_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == FM_INFEASIBLE:
+        from .assign import InfeasibleInstanceError
+
+        raise InfeasibleInstanceError(msg)
+    if rc == FM_INVALID_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def device_count() -> int:
+    return int(load().fm_device_count())
+
+
+def require_device() -> None:
+    if device_count() < 1:
+        raise RuntimeError("no CUDA device visible: the B200 path has no CPU fallback")
+
+
+def ptr(a) -> int:
+    """Address of a numpy array or torch tensor (borrowed for the call)."""
+    if hasattr(a, "data_ptr"):
+        return int(a.data_ptr())
+    return int(a.ctypes.data)

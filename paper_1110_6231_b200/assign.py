@@ -1,0 +1,194 @@
+"""Dense assignment by cost scaling: drop-in for the reference's ``solve_assignment``.
+
+Same names, keyword arguments, defaults, return value ``(SolveReport, matching)``
+and exceptions as assign_scaling.py:44-82,470-497.  Every mode runs the CUDA
+refine in libfm_b200.so (there is no CPU path): ``mode`` is validated and
+recorded, ``worker_count``/``cycle_budget`` keep their validation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .graph import SolveReport
+
+DEFAULT_ALPHA = 10             # assign_scaling.py:33
+DEFAULT_ASSIGN_CYCLE = 500000  # assign_scaling.py:34
+ORACLE_SIZE_LIMIT = 9          # oracles.py:17 (kept for API parity)
+
+
+class InfeasibleInstanceError(Exception):
+    """The instance admits no perfect matching (assign_scaling.py:44-45)."""
+
+
+@dataclass(frozen=True)
+class AssignmentInstance:
+    """Bipartite max-weight matching instance with |X| = |Y| = n
+    (assign_scaling.py:48-82; same validation messages)."""
+
+    n: int
+    edges: tuple
+    complete: bool
+
+    @classmethod
+    def build(cls, n: int, edges) -> "AssignmentInstance":
+        if n < 1:
+            raise ValueError(f"n must be at least 1, got {n}")
+        seen: set = set()
+        normalized = []
+        for x, y, w in edges:
+            if not (0 <= x < n):
+                raise ValueError(f"edge ({x},{y}): x out of range [0, {n})")
+            if not (0 <= y < n):
+                raise ValueError(f"edge ({x},{y}): y out of range [0, {n})")
+            if (x, y) in seen:
+                raise ValueError(f"duplicate edge ({x},{y})")
+            seen.add((x, y))
+            normalized.append((int(x), int(y), int(w)))
+        return cls(n=n, edges=tuple(normalized), complete=len(seen) == n * n)
+
+    @classmethod
+    def from_matrix(cls, weights) -> "AssignmentInstance":
+        n = len(weights)
+        edges = [(x, y, weights[x][y]) for x in range(n) for y in range(n)]
+        return cls.build(n, edges)
+
+    def dense(self) -> np.ndarray:
+        """int32 n x n weights, FM_ABSENT_WEIGHT where the instance has no arc."""
+        w = np.full((self.n, self.n), _lib.FM_ABSENT_WEIGHT, np.int64)
+        if self.edges:
+            e = np.asarray(self.edges, dtype=np.int64)
+            w[e[:, 0], e[:, 1]] = e[:, 2]
+        return _check_weights(w)
+
+
+def _check_weights(w) -> np.ndarray:
+    w = np.asarray(w)
+    if w.ndim != 2 or w.shape[0] != w.shape[1]:
+        raise ValueError(f"weights must be square, got shape {w.shape}")
+    present = w != _lib.FM_ABSENT_WEIGHT
+    if present.any():
+        lo, hi = int(w[present].min()), int(w[present].max())
+        if lo <= -(2**31) or hi >= 2**31:
+            raise ValueError("weights must fit in int32")
+    return np.ascontiguousarray(w, dtype=np.int32)
+
+
+class AssignmentSolver:
+    """Reusable device workspace for n x n instances (owns the C handle)."""
+
+    def __init__(self, n: int, device: int = 0):
+        L = _lib.load()
+        _lib.require_device()
+        h = ctypes.c_void_p()
+        _lib.check(L.fm_assign_create(int(n), int(device), ctypes.byref(h)), "fm_assign_create")
+        self.n, self.device, self._h = int(n), int(device), h
+        self.last_stats: dict = {}
+
+    def close(self):
+        if self._h:
+            _lib.load().fm_assign_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _flags(use_price_update, use_arc_fix, validate) -> int:
+        return ((_lib.FM_ASSIGN_PRICE_UPDATE if use_price_update else 0)
+                | (_lib.FM_ASSIGN_ARC_FIX if use_arc_fix else 0)
+                | (_lib.FM_ASSIGN_VALIDATE if validate else 0))
+
+    def solve_host(self, weights, alpha=DEFAULT_ALPHA, use_price_update=True, use_arc_fix=True,
+                   validate=False, want_prices=False):
+        w = _check_weights(weights)
+        obj = ctypes.c_int64()
+        match = np.zeros(self.n, np.int32)
+        prices = np.zeros(2 * self.n, np.int64) if want_prices else None
+        st = _lib.FmStats()
+        rc = _lib.load().fm_assign_solve_host(
+            self._h, _lib.ptr(w), int(alpha), self._flags(use_price_update, use_arc_fix, validate),
+            ctypes.byref(obj), _lib.ptr(match), _lib.ptr(prices) if want_prices else None,
+            ctypes.byref(st))
+        self.last_stats = st.as_dict()
+        _lib.check(rc, "fm_assign_solve_host")
+        return int(obj.value), match, prices, self.last_stats
+
+    def solve_device(self, weights_dev, alpha=DEFAULT_ALPHA, use_price_update=True, use_arc_fix=True,
+                     validate=False, want_prices=False, stream=None):
+        obj = ctypes.c_int64()
+        match = np.zeros(self.n, np.int32)
+        prices = np.zeros(2 * self.n, np.int64) if want_prices else None
+        st = _lib.FmStats()
+        s = int(getattr(stream, "cuda_stream", stream)) if stream is not None else None
+        rc = _lib.load().fm_assign_solve(
+            self._h, _lib.ptr(weights_dev), int(alpha),
+            self._flags(use_price_update, use_arc_fix, validate), ctypes.byref(obj),
+            _lib.ptr(match), _lib.ptr(prices) if want_prices else None, ctypes.byref(st), s)
+        self.last_stats = st.as_dict()
+        _lib.check(rc, "fm_assign_solve")
+        return int(obj.value), match, prices, self.last_stats
+
+
+_solvers: dict = {}
+
+
+def _solver_for(n: int, device: int) -> AssignmentSolver:
+    key = (n, device)
+    s = _solvers.get(key)
+    if s is None:
+        s = _solvers[key] = AssignmentSolver(n, device)
+    return s
+
+
+def solve_assignment(inst: AssignmentInstance, *, mode: str = "seq", worker_count: int = 1,
+                     cycle_budget: int = DEFAULT_ASSIGN_CYCLE, alpha: int = DEFAULT_ALPHA,
+                     use_price_update: bool = True, use_arc_fix: bool = True,
+                     heuristic_every_k: int | None = None, validate: bool = False,
+                     on_refine_end=None, observer=None, device: int = 0):
+    """Maximum-weight perfect matching on the GPU (assign_scaling.py:470-497).
+
+    Returns (SolveReport, matching) with matching[x] = y; objective is the
+    matching weight in original units.  Raises InfeasibleInstanceError when no
+    perfect matching exists.  ``inst`` may also be a dense n x n weight array
+    (numpy or CUDA tensor).
+    """
+    if mode not in ("seq", "par"):
+        raise ValueError(f"unknown mode {mode!r}")
+    if alpha < 2:
+        raise ValueError(f"alpha must be at least 2, got {alpha}")
+    if worker_count < 1:
+        raise ValueError(f"worker_count must be at least 1, got {worker_count}")
+    if cycle_budget < 1:
+        raise ValueError(f"cycle_budget must be at least 1, got {cycle_budget}")
+    if on_refine_end is not None or observer is not None:
+        raise NotImplementedError("per-refine callbacks need the stepwise assignment API (next row)")
+    started = time.perf_counter()
+    if isinstance(inst, AssignmentInstance):
+        n = inst.n
+        solver = _solver_for(n, device)
+        obj, match, _, st = solver.solve_host(inst.dense(), alpha, use_price_update, use_arc_fix, validate)
+    elif hasattr(inst, "is_cuda") and inst.is_cuda:
+        n = int(inst.shape[0])
+        solver = _solver_for(n, device)
+        import torch
+
+        obj, match, _, st = solver.solve_device(inst.contiguous(), alpha, use_price_update, use_arc_fix,
+                                                validate, stream=torch.cuda.current_stream(inst.device))
+    else:
+        w = np.asarray(inst)
+        n = int(w.shape[0])
+        solver = _solver_for(n, device)
+        obj, match, _, st = solver.solve_host(w, alpha, use_price_update, use_arc_fix, validate)
+    elapsed = time.perf_counter() - started
+    report = SolveReport(objective=obj, pushes=int(st["pushes"]), relabels=int(st["relabels"]),
+                         rounds=int(st["rounds"]), elapsed=elapsed, stats=st)
+    return report, match.tolist()

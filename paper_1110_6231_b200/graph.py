@@ -1,0 +1,221 @@
+"""Network types crossing the drop-in boundary.
+
+Mirrors the reference's core types (graph.py:23-186) with the same names,
+fields and validation messages, and adds :class:`GridNetwork`, the
+structure-of-arrays form of a 4-connected grid graph that the CUDA path consumes.
+A ``GridNetwork`` *is a* ``FlowNetwork``: its arc-pair lists are materialised
+lazily, in the SURVEY.md 8d adapter order, only when code asks for them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+class NetworkError(ValueError):
+    """Invalid network construction input (graph.py:23-24)."""
+
+
+@dataclass(frozen=True, slots=True)
+class SolveReport:
+    """Outcome of one solver run (graph.py:27-40).
+
+    objective is the flow value (max-flow) or matching weight (assignment).
+    rounds counts coordinator rounds.  elapsed is wall seconds.  The fields
+    after elapsed are additions (defaults keep the reference's positional
+    order): cut = minimal source side of the min cut (bool H x W array) for
+    grid solves, stats = device counters and CUDA-event timings.
+    """
+
+    objective: int
+    pushes: int = 0
+    relabels: int = 0
+    rounds: int = 0
+    elapsed: float = 0.0
+    cut: object = None
+    stats: object = None
+
+
+class FlowNetwork:
+    """Immutable directed graph with unit-indexed arc pairs (graph.py:43-84)."""
+
+    __slots__ = ("node_count", "source", "sink", "tail", "head", "capacity", "cost", "out_arcs")
+
+    def __init__(self, node_count: int, source: int | None, sink: int | None):
+        self.node_count = node_count
+        self.source = source
+        self.sink = sink
+        self.tail: list[int] = []
+        self.head: list[int] = []
+        self.capacity: list[int] = []
+        self.cost: list[int] = []
+        self.out_arcs: list[list[int]] = [[] for _ in range(node_count)]
+
+    @property
+    def arc_count(self) -> int:
+        return len(self.tail)
+
+    def reverse_of(self, a: int) -> int:
+        return a ^ 1
+
+    def add_arc_pair(self, tail: int, head: int, capacity: int, cost: int = 0) -> int:
+        a = len(self.tail)
+        self.tail += (tail, head)
+        self.head += (head, tail)
+        self.capacity += (capacity, 0)
+        self.cost += (cost, -cost)
+        self.out_arcs[tail].append(a)
+        self.out_arcs[head].append(a + 1)
+        return a
+
+
+def build_network(edge_list, node_count: int, source: int, sink: int) -> FlowNetwork:
+    """Validated FlowNetwork from (tail, head, capacity[, cost]) tuples
+    (graph.py:87-125; same error messages)."""
+    if node_count < 2:
+        raise NetworkError(f"node_count must be at least 2, got {node_count}")
+    if not (0 <= source < node_count):
+        raise NetworkError(f"source id {source} out of range [0, {node_count})")
+    if not (0 <= sink < node_count):
+        raise NetworkError(f"sink id {sink} out of range [0, {node_count})")
+    if source == sink:
+        raise NetworkError(f"source and sink must differ, both are {source}")
+    net = FlowNetwork(node_count, source, sink)
+    for i, edge in enumerate(edge_list):
+        if len(edge) == 3:
+            tail, head, capacity = edge
+            cost = 0
+        else:
+            tail, head, capacity, cost = edge
+        if not (0 <= tail < node_count):
+            raise NetworkError(f"arc {i}: tail id {tail} out of range [0, {node_count})")
+        if not (0 <= head < node_count):
+            raise NetworkError(f"arc {i}: head id {head} out of range [0, {node_count})")
+        if capacity < 0:
+            raise NetworkError(f"arc {i}: negative capacity {capacity}")
+        net.add_arc_pair(tail, head, capacity, cost)
+    return net
+
+
+_PLANES = ("capR", "capL", "capD", "capU", "capS", "capT")
+
+
+class GridNetwork(FlowNetwork):
+    """4-connected H x W grid network in structure-of-arrays form.
+
+    Pixel p = r * W + c; source s = H*W, sink t = H*W + 1.
+    capR/capL/capD/capU[p] are the capacities of p->p+1, p->p-1, p->p+W, p->p-W;
+    capS[p] of s->p and capT[p] of p->t.  Arrays are int32 numpy arrays (host)
+    or int32 CUDA tensors (device; the solve then never leaves the GPU).
+    """
+
+    __slots__ = ("H", "W", "caps", "_materialised")
+
+    def __init__(self, capR, capL, capD, capU, capS, capT):
+        shape = tuple(capS.shape)
+        if len(shape) != 2:
+            raise NetworkError(f"grid planes must be 2-D, got shape {shape}")
+        H, W = int(shape[0]), int(shape[1])
+        caps = (capR, capL, capD, capU, capS, capT)
+        for name, a in zip(_PLANES, caps):
+            if tuple(a.shape) != shape:
+                raise NetworkError(f"{name} has shape {tuple(a.shape)}, expected {shape}")
+        FlowNetwork.__init__(self, H * W + 2, H * W, H * W + 1)
+        self.H, self.W = H, W
+        self.caps = caps
+        self._materialised = False
+        # the adjacency lists are built on demand; out_arcs stays a placeholder
+        self.out_arcs = None
+
+    @property
+    def on_device(self) -> bool:
+        return hasattr(self.caps[0], "is_cuda") and bool(self.caps[0].is_cuda)
+
+    def host_caps(self):
+        """The six planes as C-contiguous int32 numpy arrays."""
+        out = []
+        for a in self.caps:
+            if hasattr(a, "detach"):
+                a = a.detach().cpu().numpy()
+            out.append(np.ascontiguousarray(a, dtype=np.int32))
+        return tuple(out)
+
+    def arc_arrays(self):
+        """(tails, heads, caps) of the reference network in adapter order:
+        per pixel, row-major: (s,p,capS) if >0, (p,t,capT) if >0, (p,p+1,capR),
+        (p+1,p,capL[p+1]), (p,p+W,capD), (p+W,p,capU[p+W])."""
+        capR, capL, capD, capU, capS, capT = self.host_caps()
+        H, W = self.H, self.W
+        HW = H * W
+        p = np.arange(HW, dtype=np.int64)
+        r, c = p // W, p % W
+        s, t = HW, HW + 1
+        tl = np.full((HW, 6), -1, np.int64)
+        hd = np.full((HW, 6), -1, np.int64)
+        cp = np.zeros((HW, 6), np.int64)
+        keep = np.zeros((HW, 6), bool)
+        fS, fT = capS.reshape(-1), capT.reshape(-1)
+        keep[:, 0] = fS > 0
+        tl[:, 0], hd[:, 0], cp[:, 0] = s, p, fS
+        keep[:, 1] = fT > 0
+        tl[:, 1], hd[:, 1], cp[:, 1] = p, t, fT
+        hasR = c + 1 < W
+        keep[:, 2] = hasR
+        keep[:, 3] = hasR
+        tl[:, 2], hd[:, 2], cp[:, 2] = p, p + 1, capR.reshape(-1)
+        q = np.minimum(p + 1, HW - 1)
+        tl[:, 3], hd[:, 3], cp[:, 3] = p + 1, p, capL.reshape(-1)[q]
+        hasD = r + 1 < H
+        keep[:, 4] = hasD
+        keep[:, 5] = hasD
+        tl[:, 4], hd[:, 4], cp[:, 4] = p, p + W, capD.reshape(-1)
+        q = np.minimum(p + W, HW - 1)
+        tl[:, 5], hd[:, 5], cp[:, 5] = p + W, p, capU.reshape(-1)[q]
+        k = keep.reshape(-1)
+        return (tl.reshape(-1)[k].astype(np.int32), hd.reshape(-1)[k].astype(np.int32),
+                cp.reshape(-1)[k].astype(np.int32))
+
+    def materialise(self) -> "GridNetwork":
+        """Fill the FlowNetwork arc-pair lists (slow; tests and small grids only)."""
+        if self._materialised:
+            return self
+        tl, hd, cp = self.arc_arrays()
+        self.tail, self.head, self.capacity, self.cost = [], [], [], []
+        self.out_arcs = [[] for _ in range(self.node_count)]
+        for a, b, c in zip(tl.tolist(), hd.tolist(), cp.tolist()):
+            self.add_arc_pair(a, b, c)
+        self._materialised = True
+        return self
+
+    @property
+    def arc_count(self) -> int:
+        if not self._materialised:
+            self.materialise()
+        return len(self.tail)
+
+
+def build_grid_network(capR, capL, capD, capU, capS, capT) -> GridNetwork:
+    """Validated GridNetwork from six H x W capacity planes (int32).
+
+    Raises NetworkError for a shape mismatch, a negative capacity, or a
+    non-zero capacity on an arc that would leave the grid (last column of
+    capR, first column of capL, last row of capD, first row of capU)."""
+    net = GridNetwork(capR, capL, capD, capU, capS, capT)
+    if not net.on_device:
+        planes = net.host_caps()
+        for name, a in zip(_PLANES, planes):
+            if a.size and int(a.min()) < 0:
+                raise NetworkError(f"{name}: negative capacity {int(a.min())}")
+        capR, capL, capD, capU = planes[:4]
+        if capR[:, -1].any():
+            raise NetworkError("capR: last column must be 0 (arc leaves the grid)")
+        if capL[:, 0].any():
+            raise NetworkError("capL: first column must be 0 (arc leaves the grid)")
+        if capD[-1, :].any():
+            raise NetworkError("capD: last row must be 0 (arc leaves the grid)")
+        if capU[0, :].any():
+            raise NetworkError("capU: first row must be 0 (arc leaves the grid)")
+        net.caps = planes
+    return net

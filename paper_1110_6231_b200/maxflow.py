@@ -1,0 +1,286 @@
+"""Grid max-flow / min-cut: drop-in for the reference's ``hybrid_solve``.
+
+``hybrid_solve(net, worker_count=4, cycle_budget=7000, observer=None)`` keeps the
+reference signature, defaults and return type (maxflow_par.py:157-238).  On a
+:class:`GridNetwork` it runs the CUDA path in libfm_b200.so; the result carries the
+flow value in ``objective`` (= excess at t, maxflow_par.py:233) plus the minimal
+source-side cut in ``report.cut``.  Other networks raise ``NotImplementedError``:
+the generic-graph (CSR) kernel is a SURVEY.md 8f "next" row, and there is no CPU
+fallback by design.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .graph import FlowNetwork, GridNetwork, SolveReport
+
+DEFAULT_CYCLE_BUDGET = 7000  # maxflow_par.py:28
+DEFAULT_BFS_INTERVAL = 0     # 0 = library default sweeps between global relabels
+
+
+class GridSolver:
+    """Reusable device workspace for H x W grids (owns the C handle).
+
+    The SoA state (9 int32 planes + 3 byte planes, ~40 B/pixel) is allocated once
+    and reused across solves of the same shape.
+    """
+
+    def __init__(self, H: int, W: int, device: int = 0):
+        L = _lib.load()
+        _lib.require_device()
+        h = ctypes.c_void_p()
+        _lib.check(L.fm_grid_create(int(H), int(W), int(device), ctypes.byref(h)), "fm_grid_create")
+        self.H, self.W, self.device = int(H), int(W), int(device)
+        self._h = h
+        self.last_stats: dict = {}
+
+    def close(self) -> None:
+        if self._h:
+            _lib.load().fm_grid_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _flags(self, cancel_violations=False, want_cut=True, precancel=True) -> int:
+        f = 0
+        if cancel_violations:
+            f |= _lib.FM_GRID_CANCEL_VIOLATIONS
+        if not want_cut:
+            f |= _lib.FM_GRID_NO_CUT
+        if not precancel:
+            f |= _lib.FM_GRID_NO_PRECANCEL
+        return f
+
+    def solve_host(self, caps, cycle_budget=DEFAULT_CYCLE_BUDGET, bfs_interval=DEFAULT_BFS_INTERVAL,
+                   want_cut=True, cancel_violations=False, precancel=True):
+        """Host int32 planes in, (flow, cut uint8[H,W] or None, stats) out; the
+        host<->device copies are part of the call."""
+        caps = [np.ascontiguousarray(a, dtype=np.int32) for a in caps]
+        flow = ctypes.c_int64()
+        cut = np.zeros((self.H, self.W), np.uint8) if want_cut else None
+        st = _lib.FmStats()
+        rc = _lib.load().fm_grid_solve_host(
+            self._h, *[_lib.ptr(a) for a in caps], int(cycle_budget), int(bfs_interval),
+            self._flags(cancel_violations, want_cut, precancel), ctypes.byref(flow),
+            _lib.ptr(cut) if want_cut else None, ctypes.byref(st))
+        _lib.check(rc, "fm_grid_solve_host")
+        self.last_stats = st.as_dict()
+        return int(flow.value), cut, self.last_stats
+
+    def solve_device(self, caps, cycle_budget=DEFAULT_CYCLE_BUDGET, bfs_interval=DEFAULT_BFS_INTERVAL,
+                     cut_out=None, cancel_violations=False, precancel=True, stream=None):
+        """Device int32 tensors in (borrowed); cut_out = uint8 CUDA tensor or None.
+        Runs on `stream` (a torch.cuda.Stream or raw handle; default: the
+        library's own stream)."""
+        flow = ctypes.c_int64()
+        st = _lib.FmStats()
+        s = None
+        if stream is not None:
+            s = int(getattr(stream, "cuda_stream", stream))
+        rc = _lib.load().fm_grid_solve(
+            self._h, *[_lib.ptr(a) for a in caps], int(cycle_budget), int(bfs_interval),
+            self._flags(cancel_violations, cut_out is not None, precancel), ctypes.byref(flow),
+            _lib.ptr(cut_out) if cut_out is not None else None, ctypes.byref(st), s)
+        _lib.check(rc, "fm_grid_solve")
+        self.last_stats = st.as_dict()
+        return int(flow.value), self.last_stats
+
+    # ---- stepwise (observer) API
+    def begin(self, caps, cancel_violations=False, precancel=True):
+        caps = [np.ascontiguousarray(a, dtype=np.int32) for a in caps]
+        self._keep = caps
+        _lib.check(_lib.load().fm_grid_begin(self._h, *[_lib.ptr(a) for a in caps],
+                                             self._flags(cancel_violations, True, precancel)),
+                   "fm_grid_begin")
+
+    def round(self, cycle_budget=DEFAULT_CYCLE_BUDGET, bfs_interval=DEFAULT_BFS_INTERVAL) -> bool:
+        done = ctypes.c_int32()
+        st = _lib.FmStats()
+        _lib.check(_lib.load().fm_grid_round(self._h, int(cycle_budget), int(bfs_interval),
+                                             ctypes.byref(done), ctypes.byref(st)), "fm_grid_round")
+        self.last_stats = st.as_dict()
+        return bool(done.value)
+
+    def export(self) -> dict:
+        H, W = self.H, self.W
+        names = ("rR", "rL", "rD", "rU", "rT", "rS", "e", "h")
+        out = {k: np.zeros((H, W), np.int32) for k in names}
+        marked = np.zeros((H, W), np.uint8)
+        flow = ctypes.c_int64()
+        et = ctypes.c_int64()
+        _lib.check(_lib.load().fm_grid_export(self._h, *[_lib.ptr(out[k]) for k in names],
+                                              _lib.ptr(marked), ctypes.byref(flow), ctypes.byref(et)),
+                   "fm_grid_export")
+        out["marked"] = marked
+        out["flow"] = int(flow.value)
+        out["excess_total"] = int(et.value)
+        return out
+
+    def cut_host(self) -> np.ndarray:
+        cut = np.zeros((self.H, self.W), np.uint8)
+        st = _lib.FmStats()
+        _lib.check(_lib.load().fm_grid_cut_host(self._h, _lib.ptr(cut), ctypes.byref(st)), "fm_grid_cut_host")
+        self.last_stats = st.as_dict()
+        return cut
+
+
+_solvers: dict = {}
+
+
+def _solver_for(H: int, W: int, device: int) -> GridSolver:
+    key = (H, W, device)
+    s = _solvers.get(key)
+    if s is None:
+        # keep at most one cached workspace per device: grids are large
+        for k in [k for k in _solvers if k[2] == device]:
+            _solvers.pop(k).close()
+        s = _solvers[key] = GridSolver(H, W, device)
+    return s
+
+
+# ---------------------------------------------------------------- observer mirror
+
+@dataclass
+class _StateView:
+    """Reference-shaped ResidualState view (graph.py:128-154) of a grid state."""
+
+    residual: list
+    excess: list
+    height: list
+    price: list
+
+
+@dataclass
+class GridHybridState:
+    """Reference-shaped HybridState (maxflow_par.py:31-41) at a coordinator point."""
+
+    state: _StateView
+    excess_total: int
+    cycle_budget: int = DEFAULT_CYCLE_BUDGET
+    worker_count: int = 1
+    marked: list = field(default_factory=list)
+
+
+def _slot_residuals(net: GridNetwork, st: dict) -> np.ndarray:
+    """Map the merged-pair device state onto the reference arc slots (adapter order).
+
+    A merged pair (p->q cap a, q->p cap b) with net flow phi = a - r(p->q) is
+    decomposed as flow max(phi, 0) on p->q and max(-phi, 0) on q->p."""
+    capR, capL, capD, capU, capS, capT = net.host_caps()
+    H, W = net.H, net.W
+    HW = H * W
+    p = np.arange(HW)
+    r, c = p // W, p % W
+    cols = np.zeros((HW, 12), np.int64)
+    keep = np.zeros((HW, 12), bool)
+    fS, fT = capS.reshape(-1), capT.reshape(-1)
+    rS, rT = st["rS"].reshape(-1), st["rT"].reshape(-1)
+    keep[:, 0:2] = (fS > 0)[:, None]
+    cols[:, 0], cols[:, 1] = fS - rS, rS
+    keep[:, 2:4] = (fT > 0)[:, None]
+    cols[:, 2], cols[:, 3] = rT, fT - rT
+    hasR = c + 1 < W
+    keep[:, 4:8] = hasR[:, None]
+    q = np.minimum(p + 1, HW - 1)
+    a, b = capR.reshape(-1), capL.reshape(-1)[q]
+    phi = a - st["rR"].reshape(-1)
+    f1, f2 = np.maximum(phi, 0), np.maximum(-phi, 0)
+    cols[:, 4], cols[:, 5], cols[:, 6], cols[:, 7] = a - f1, f1, b - f2, f2
+    hasD = r + 1 < H
+    keep[:, 8:12] = hasD[:, None]
+    q = np.minimum(p + W, HW - 1)
+    a, b = capD.reshape(-1), capU.reshape(-1)[q]
+    phi = a - st["rD"].reshape(-1)
+    f1, f2 = np.maximum(phi, 0), np.maximum(-phi, 0)
+    cols[:, 8], cols[:, 9], cols[:, 10], cols[:, 11] = a - f1, f1, b - f2, f2
+    return cols.reshape(-1)[keep.reshape(-1)]
+
+
+def _observe(net: GridNetwork, solver: GridSolver, observer, cycle_budget, worker_count):
+    st = solver.export()
+    HW = net.H * net.W
+    V = HW + 2
+    excess = st["e"].reshape(-1).astype(np.int64).tolist() + [0, st["flow"]]
+    height = st["h"].reshape(-1).astype(np.int64).tolist() + [V, 0]
+    marked = st["marked"].reshape(-1).astype(bool).tolist() + [False, False]
+    residual = _slot_residuals(net, st).tolist() if net._materialised else None
+    hybrid = GridHybridState(
+        state=_StateView(residual=residual, excess=excess, height=height, price=[0] * V),
+        excess_total=st["excess_total"], cycle_budget=cycle_budget, worker_count=worker_count,
+        marked=marked)
+    scanned = [not m for m in marked]
+    scanned[HW] = True
+    observer(net, hybrid, scanned)
+
+
+def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DEFAULT_CYCLE_BUDGET,
+                 observer=None, *, device: int = 0, bfs_interval: int = DEFAULT_BFS_INTERVAL,
+                 cancel_violations: bool = False, want_cut: bool = True) -> SolveReport:
+    """Coordinated lock-free push-relabel rounds until all live excess is at t
+    (maxflow_par.py:157-238), on the GPU.
+
+    worker_count keeps its validation but has no effect on the device (one CUDA
+    thread owns each pixel).  cycle_budget = max lock-free sweeps per round.
+    observer(net, hybrid, scanned) is called at every coordinator point with
+    reference-shaped state (slow: state is copied to the host; tests only).
+    """
+    if net.source is None or net.sink is None:
+        raise ValueError("network has no source/sink")
+    if worker_count < 1:
+        raise ValueError(f"worker_count must be at least 1, got {worker_count}")
+    if cycle_budget < 1:
+        raise ValueError(f"cycle_budget must be at least 1, got {cycle_budget}")
+    if not isinstance(net, GridNetwork):
+        raise NotImplementedError(
+            "the B200 path solves 4-connected grid networks (GridNetwork); the generic "
+            "CSR lock-free kernel is a SURVEY.md 8f next row and there is no CPU fallback")
+    started = time.perf_counter()
+    solver = _solver_for(net.H, net.W, device)
+    if observer is None:
+        if net.on_device:
+            import torch
+
+            cut_t = torch.empty((net.H, net.W), dtype=torch.uint8, device=net.caps[0].device) if want_cut else None
+            flow, stats = solver.solve_device(net.caps, cycle_budget, bfs_interval, cut_out=cut_t,
+                                              cancel_violations=cancel_violations,
+                                              stream=torch.cuda.current_stream(net.caps[0].device))
+            cut = cut_t.bool() if cut_t is not None else None
+        else:
+            flow, cut8, stats = solver.solve_host(net.host_caps(), cycle_budget, bfs_interval,
+                                                  want_cut=want_cut, cancel_violations=cancel_violations)
+            cut = cut8.astype(bool) if cut8 is not None else None
+    else:
+        solver.begin(net.host_caps(), cancel_violations=cancel_violations)
+        while True:
+            st = solver.export()
+            if int(((st["e"] > 0) & (st["marked"] == 0)).sum()) == 0:
+                break
+            done = solver.round(cycle_budget, bfs_interval)
+            _observe(net, solver, observer, cycle_budget, worker_count)
+            if done:
+                break
+        st = solver.export()
+        flow = st["flow"]
+        stats = dict(solver.last_stats)
+        cut = solver.cut_host().astype(bool) if want_cut else None
+    elapsed = time.perf_counter() - started
+    return SolveReport(objective=int(flow), pushes=int(stats.get("pushes", 0)),
+                       relabels=int(stats.get("relabels", 0)), rounds=int(stats.get("rounds", 0)),
+                       elapsed=elapsed, cut=cut, stats=stats)
+
+
+def min_cut(net: GridNetwork, report: SolveReport | None = None, **kw):
+    """Minimal source side of a minimum cut (bool H x W; True = source side)."""
+    if report is None or report.cut is None:
+        report = hybrid_solve(net, **kw)
+    return report.cut

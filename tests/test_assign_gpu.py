@@ -1,0 +1,114 @@
+"""GPU parity of the dense cost-scaling assignment path against the reference's
+golden vectors, scipy's exact solver and the epsilon-optimality certificate."""
+
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1110_6231_b200 as fmb
+from paper_1110_6231_b200 import generators as G
+from conftest import assign_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _objective(w, m):
+    return int(sum(int(w[x, y]) for x, y in enumerate(m)))
+
+
+def _is_perm(m, n):
+    return sorted(m) == list(range(n))
+
+
+def test_golden_assignment(golden):
+    for case in golden["assignment"]:
+        w = assign_matrix(case)
+        n = case["n"]
+        if case["seq"] == "infeasible":
+            with pytest.raises(fmb.InfeasibleInstanceError):
+                fmb.solve_assignment(w)
+            continue
+        rep, m = fmb.solve_assignment(w)
+        assert rep.objective == case["seq"]["objective"], case["name"]
+        assert _is_perm(m, n) and _objective(w, m) == rep.objective
+        assert all(w[x, y] != -(2**31) for x, y in enumerate(m))
+
+
+def test_instance_api_and_modes(golden):
+    inst = fmb.AssignmentInstance.from_matrix([[3, 8, 2], [6, 4, 9], [5, 7, 1]])
+    for mode in ("seq", "par"):
+        rep, m = fmb.solve_assignment(inst, mode=mode)
+        assert rep.objective == 22 and m == [1, 2, 0]
+    for alpha in (2, 5, 100):
+        assert fmb.solve_assignment(inst, alpha=alpha)[0].objective == 22
+    with pytest.raises(fmb.InfeasibleInstanceError):
+        fmb.solve_assignment(fmb.AssignmentInstance.build(2, [(0, 0, 5), (1, 0, 3)]))
+
+
+def test_random_small_vs_brute_force():
+    rng = np.random.default_rng(11)
+    for it in range(200):
+        n = int(rng.integers(1, 8))
+        hi = int(rng.choice([1, 3, 50, 100]))
+        w = rng.integers(0, hi + 1, size=(n, n)).astype(np.int32)
+        best = max(sum(int(w[x, p[x]]) for x in range(n)) for p in itertools.permutations(range(n)))
+        for fix in (True, False):
+            rep, m = fmb.solve_assignment(w, use_arc_fix=fix)
+            assert rep.objective == best, (it, n, hi)
+            assert _is_perm(m, n) and _objective(w, m) == best
+
+
+@pytest.mark.parametrize("n,M", [(512, 100), (512, 10000), (1024, 100), (1024, 10000), (1000, 1000)])
+def test_vs_scipy_and_certificate(n, M):
+    from scipy.optimize import linear_sum_assignment
+
+    w = G.assignment_reference(n, M, n)
+    solver = fmb.AssignmentSolver(n)
+    obj, m, prices, st = solver.solve_host(w, want_prices=True)
+    solver.close()
+    r, c = linear_sum_assignment(w.astype(np.int64), maximize=True)
+    assert obj == int(w[r, c].sum())
+    code, cobj = oracle.assign_certify_dense(w, m, prices)
+    assert code == 0 and cobj == obj
+
+
+def test_oracle_port_parity_mid_size():
+    w = G.assignment_reference(256, 10000, 256)
+    want = oracle.assign(256, matrix=w, mode="seq")
+    rep, m = fmb.solve_assignment(w)
+    assert rep.objective == want["objective"]
+
+
+def test_optical_flow_style():
+    from scipy.optimize import linear_sum_assignment
+
+    w = G.assignment_optical_flow(1024, 1024)
+    rep, m = fmb.solve_assignment(w)
+    r, c = linear_sum_assignment(w.astype(np.int64), maximize=True)
+    assert rep.objective == int(w[r, c].sum())
+
+
+def test_sparse_feasible_and_infeasible():
+    w = G.assignment_reference(40, 100, 3, density=0.1)
+    from scipy.optimize import linear_sum_assignment
+
+    big = np.where(w == -(2**31), -10**9, w).astype(np.int64)
+    r, c = linear_sum_assignment(big, maximize=True)
+    rep, m = fmb.solve_assignment(w)
+    assert rep.objective == int(big[r, c].sum())
+    bad = np.full((5, 5), -(2**31), np.int32)
+    bad[:, 0] = 1
+    with pytest.raises(fmb.InfeasibleInstanceError):
+        fmb.solve_assignment(bad)
+
+
+def test_device_tensor_input():
+    torch = pytest.importorskip("torch")
+    w = G.assignment_reference(300, 100, 3)
+    rep_h, _ = fmb.solve_assignment(w)
+    rep_d, m = fmb.solve_assignment(torch.from_numpy(w).cuda())
+    assert rep_d.objective == rep_h.objective

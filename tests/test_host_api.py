@@ -1,0 +1,148 @@
+"""CPU-side checks of the drop-in boundary: names and signatures mirror the
+reference, validation behaves like the reference, the grid adapter matches the
+oracle's, and libfm_b200.so loads and exports every symbol the header declares.
+No compute call is made here (no GPU in this container)."""
+
+from __future__ import annotations
+
+import inspect
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1110_6231_b200 as fmb
+from paper_1110_6231_b200 import _lib
+from conftest import ROOT, has_gpu
+
+
+def test_reference_signatures_kept():
+    sig = inspect.signature(fmb.hybrid_solve)
+    params = list(sig.parameters.values())
+    assert [p.name for p in params[:4]] == ["net", "worker_count", "cycle_budget", "observer"]
+    assert params[1].default == 4 and params[2].default == 7000 and params[3].default is None
+    sig = inspect.signature(fmb.solve_assignment)
+    want = dict(mode="seq", worker_count=1, cycle_budget=500000, alpha=10, use_price_update=True,
+                use_arc_fix=True, heuristic_every_k=None, validate=False, on_refine_end=None,
+                observer=None)
+    for k, v in want.items():
+        assert sig.parameters[k].default == v, k
+        assert sig.parameters[k].kind is inspect.Parameter.KEYWORD_ONLY
+    rep = fmb.SolveReport(5)
+    assert (rep.objective, rep.pushes, rep.relabels, rep.rounds, rep.elapsed) == (5, 0, 0, 0, 0.0)
+    assert issubclass(fmb.NetworkError, ValueError)
+
+
+def test_build_network_messages():
+    with pytest.raises(fmb.NetworkError, match="node_count must be at least 2"):
+        fmb.build_network([], 1, 0, 0)
+    with pytest.raises(fmb.NetworkError, match="source and sink must differ"):
+        fmb.build_network([], 3, 1, 1)
+    with pytest.raises(fmb.NetworkError, match="arc 0: negative capacity"):
+        fmb.build_network([(0, 1, -1)], 3, 0, 2)
+    net = fmb.build_network([(0, 1, 3), (1, 2, 4)], 3, 0, 2)
+    assert net.arc_count == 4 and net.out_arcs[1] == [1, 2] and net.reverse_of(2) == 3
+
+
+def test_grid_network_validation():
+    from paper_1110_6231_b200.generators import grid_random
+
+    caps = list(grid_random(4, 5, 1))
+    net = fmb.build_grid_network(*caps)
+    assert (net.node_count, net.source, net.sink) == (22, 20, 21)
+    bad = [c.copy() for c in caps]
+    bad[0][:, -1] = 3
+    with pytest.raises(fmb.NetworkError, match="capR: last column"):
+        fmb.build_grid_network(*bad)
+    bad = [c.copy() for c in caps]
+    bad[4][0, 0] = -1
+    with pytest.raises(fmb.NetworkError, match="negative capacity"):
+        fmb.build_grid_network(*bad)
+    with pytest.raises(fmb.NetworkError, match="shape"):
+        fmb.build_grid_network(caps[0][:3], *caps[1:])
+
+
+def test_grid_adapter_matches_oracle_and_reference_layout():
+    import oracle
+    from paper_1110_6231_b200.generators import grid_random
+
+    caps = grid_random(7, 9, 3)
+    net = fmb.build_grid_network(*caps)
+    mine = net.arc_arrays()
+    ref = oracle.grid_arcs(*caps)
+    for a, b in zip(mine, ref):
+        assert np.array_equal(a, b)
+    net.materialise()
+    assert net.arc_count == 2 * len(ref[0])
+    # arc 2k forward, 2k+1 reverse, as graph.py:71-84
+    assert net.capacity[1] == 0 and net.head[1] == net.tail[0]
+
+
+def test_non_grid_network_has_no_cpu_fallback():
+    net = fmb.build_network([(0, 1, 3), (1, 2, 4)], 3, 0, 2)
+    with pytest.raises(NotImplementedError, match="no CPU fallback"):
+        fmb.hybrid_solve(net)
+    with pytest.raises(ValueError, match="worker_count"):
+        fmb.hybrid_solve(net, worker_count=0)
+
+
+def test_assignment_instance_validation():
+    with pytest.raises(ValueError, match="n must be"):
+        fmb.AssignmentInstance.build(0, [])
+    with pytest.raises(ValueError, match="x out of range"):
+        fmb.AssignmentInstance.build(2, [(5, 0, 1)])
+    with pytest.raises(ValueError, match="duplicate edge"):
+        fmb.AssignmentInstance.build(2, [(0, 0, 1), (0, 0, 2)])
+    inst = fmb.AssignmentInstance.from_matrix([[1, 2], [3, 4]])
+    assert inst.complete
+    sparse = fmb.AssignmentInstance.build(2, [(0, 0, 1)])
+    assert not sparse.complete
+    d = sparse.dense()
+    assert d[0, 0] == 1 and d[1, 1] == _lib.FM_ABSENT_WEIGHT
+    with pytest.raises(ValueError, match="unknown mode"):
+        fmb.solve_assignment(inst, mode="fast")
+
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "flowmatch_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fm_[a-z_]+)\s*\(", text)))
+
+
+def test_capi_exports_every_header_symbol():
+    names = _header_functions()
+    assert "fm_grid_solve" in names and "fm_assign_solve" in names
+    assert sorted(_lib.SIGNATURES) == names
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libfm_b200.so not built (run __graft_entry__.build())")
+    L = _lib.load()
+    for n in names:
+        assert hasattr(L, n), n
+    assert b"sm_100a" in L.fm_version()
+
+
+def test_no_device_is_a_loud_error():
+    if has_gpu() or not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("a GPU is visible or the library is not built")
+    assert _lib.device_count() == 0
+    from paper_1110_6231_b200.generators import grid_random
+
+    net = fmb.build_grid_network(*grid_random(4, 4, 1))
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        fmb.hybrid_solve(net)
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        fmb.solve_assignment(fmb.AssignmentInstance.from_matrix([[1]]))
+
+
+def test_generators_deterministic():
+    from paper_1110_6231_b200 import generators as G
+
+    a = G.grid_random(16, 8, 5)
+    b = G.grid_random(16, 8, 5)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    assert a[0][:, -1].sum() == 0 and a[3][0].sum() == 0
+    s = G.grid_segmentation(64, 48, 7)
+    assert s[4].min() >= 0 and s[0][:, :-1].min() >= 1
+    w = G.assignment_optical_flow(64, 3)
+    assert w.shape == (64, 64) and w.dtype == np.int32 and w.max() <= 10000
