@@ -56,6 +56,8 @@ extern "C" {
 #define FM_GRID_CANCEL_VIOLATIONS 0x1 /* run the maxflow_par.py:132-154 pass each round */
 #define FM_GRID_NO_PRECANCEL 0x2      /* do not pre-route min(capS, capT) straight to t */
 #define FM_GRID_NO_CUT 0x4            /* skip the min-cut reach */
+#define FM_GRID_GLOBAL_SWEEP 0x8      /* A/B: one-thread-per-pixel global-memory sweeps (K1 v1)
+                                         instead of the tile-resident kernel (K1 v2) */
 
 /* assignment flags (match solve_assignment keyword arguments) */
 #define FM_ASSIGN_PRICE_UPDATE 0x1 /* use_price_update (assign_scaling.py:208-276) */

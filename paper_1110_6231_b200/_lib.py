@@ -23,6 +23,7 @@ FM_NO_DEVICE = 4
 FM_GRID_CANCEL_VIOLATIONS = 0x1
 FM_GRID_NO_PRECANCEL = 0x2
 FM_GRID_NO_CUT = 0x4
+FM_GRID_GLOBAL_SWEEP = 0x8
 
 FM_ASSIGN_PRICE_UPDATE = 0x1
 FM_ASSIGN_ARC_FIX = 0x2

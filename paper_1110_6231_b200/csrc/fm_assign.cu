@@ -36,6 +36,20 @@ namespace {
 constexpr int ATHREADS = 512;            // 16 warps per CTA
 constexpr int AWARPS = ATHREADS / 32;
 constexpr long long I64_MAX = 0x7fffffffffffffffLL;
+constexpr int LINF = 0x3fffffff;         // "unlabelled" in the price update
+
+// cnt[] slots
+constexpr int C_X0 = 0, C_Y0 = 2;        // X / Y list counts (double-buffered)
+constexpr int C_INFEASIBLE = 4;          // 1 no residual arc, 2 inconsistent, 3 budget
+constexpr int C_EXIT = 5;                // rounds kernel exit: 0 done, 1 price update due
+constexpr int C_ROUND = 6;               // next round index (persists across launches)
+constexpr int C_RELABELS = 7;            // relabels since the last price update
+constexpr int C_PU_CHG = 8;              // price update: changed flags [8], [9]
+constexpr int C_PU_LAST = 10;            // price update: max label over active nodes
+constexpr int C_COUNT = 12;
+// ops[] slots
+constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXED = 4,
+              O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7;
 
 struct AssignDev {
     const int32_t *w;      // n x n weights (row x), FM_ABSENT_WEIGHT = no arc
@@ -45,127 +59,206 @@ struct AssignDev {
     uint32_t *fixed;       // arc-fix bitmask, row-major n x nw words
     uint8_t *frozen;       // frozen[x]: x's matched arc is fixed (its flow never changes)
     int32_t *frozen_in;    // frozen_in[y]: number of frozen matches into y
+    int32_t *lx, *ly;      // price-update labels
     int32_t *xlist[2], *ylist[2];
-    int32_t *cnt;          // [0..1] X list counts, [2..3] Y list counts, [4] infeasible, [5] tail flag
-    unsigned long long *ops;  // [0] pushes [1] relabels [2] rounds [3] tail rounds [4] fixed pairs
+    int32_t *cnt;
+    unsigned long long *ops;
     int32_t n, nw;
     int64_t scale;         // n + 1
     int64_t eps;
+    int64_t max_bucket;    // scaled_cost_bound / eps + 2 (assign_scaling.py:232)
     int use_fix;
 };
 
-__device__ __forceinline__ bool is_fixed(const AssignDev &a, int x, int y) {
-    return a.use_fix && ((__ldcg(a.fixed + (size_t)x * a.nw + (y >> 5)) >> (y & 31)) & 1u);
+__device__ __forceinline__ long long floordiv(long long a, long long b) {
+    long long q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) q--;
+    return q;
 }
 
 // (value, index) min with the lower index winning ties (first arc in the
 // reference's out-arc order wins, assign_par.py:84-90)
+__device__ __forceinline__ void argmin_merge(long long &v, int &i, long long ov, int oi) {
+    if (ov < v || (ov == v && oi < i)) { v = ov; i = oi; }
+}
 __device__ __forceinline__ void warp_argmin(long long &v, int &i) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const long long ov = __shfl_xor_sync(0xffffffffu, v, o);
         const int oi = __shfl_xor_sync(0xffffffffu, i, o);
-        if (ov < v || (ov == v && oi < i)) { v = ov; i = oi; }
+        argmin_merge(v, i, ov, oi);
     }
 }
-
-// min over non-fixed present arcs of x of the part-reduced cost c(x,y) - p(y)
-// (assign_scaling.py:170-182, assign_par.py:82-90).  Whole warp; result in all lanes.
-__device__ void scan_row(const AssignDev &a, int x, long long &best, int &arg) {
-    const int32_t *row = a.w + (size_t)x * a.n;
-    const int lane = threadIdx.x & 31;
-    long long bv = I64_MAX;
-    int bi = INT32_MAX;
-    if ((a.n & 3) == 0) {
-        const int4 *row4 = reinterpret_cast<const int4 *>(row);
-        const int n4 = a.n >> 2;
-        for (int j = lane; j < n4; j += 32) {
-            const int4 w4 = __ldg(row4 + j);
-            const int wv[4] = {w4.x, w4.y, w4.z, w4.w};
+// CTA-wide argmin; result in every thread
+__device__ __forceinline__ void cta_argmin(long long &v, int &i) {
+    __shared__ long long s_v[AWARPS];
+    __shared__ int s_i[AWARPS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    warp_argmin(v, i);
+    __syncthreads();
+    if (lane == 0) { s_v[wid] = v; s_i[wid] = i; }
+    __syncthreads();
+    v = s_v[0]; i = s_i[0];
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int y = 4 * j + k;
-                if (wv[k] == FM_ABSENT_WEIGHT || is_fixed(a, x, y)) continue;
-                const long long v = -(long long)wv[k] * a.scale - __ldcg((const long long *)a.py + y);
-                if (v < bv) { bv = v; bi = y; }
+    for (int k = 1; k < AWARPS; k++) argmin_merge(v, i, s_v[k], s_i[k]);
+}
+
+// Partial scan of row x by thread t of a group of T threads: min over present,
+// non-fixed arcs of the part-reduced cost c(x,y) - p(y) (assign_scaling.py:170-182,
+// assign_par.py:82-90).  int4 weight loads and longlong2 price loads, four chunks
+// in flight per thread.
+__device__ __forceinline__ void row_partial(const AssignDev &a, int x, int t, int T,
+                                            long long &bv, int &bi) {
+    const int n = a.n;
+    const int32_t *row = a.w + (size_t)x * n;
+    const uint32_t *frow = a.fixed + (size_t)x * a.nw;
+    if ((n & 3) == 0) {
+        const int n4 = n >> 2;
+        const int4 *row4 = reinterpret_cast<const int4 *>(row);
+        const longlong2 *py2 = reinterpret_cast<const longlong2 *>(a.py);
+        for (int j0 = t; j0 < n4; j0 += 4 * T) {
+            int4 w[4];
+            longlong2 pa[4], pb[4];
+            uint32_t fw[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = j0 + u * T;
+                if (j < n4) {
+                    w[u] = __ldg(row4 + j);
+                    pa[u] = __ldcg(py2 + 2 * j);
+                    pb[u] = __ldcg(py2 + 2 * j + 1);
+                    fw[u] = a.use_fix ? (__ldg(frow + (j >> 3)) >> ((4 * j) & 31)) : 0u;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = j0 + u * T;
+                if (j >= n4) continue;
+                const int wv[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+                const long long pv[4] = {pa[u].x, pa[u].y, pb[u].x, pb[u].y};
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    if (wv[k] == FM_ABSENT_WEIGHT || ((fw[u] >> k) & 1u)) continue;
+                    const long long v = -(long long)wv[k] * a.scale - pv[k];
+                    if (v < bv) { bv = v; bi = 4 * j + k; }
+                }
             }
         }
     } else {
-        for (int y = lane; y < a.n; y += 32) {
+        for (int y = t; y < n; y += T) {
             const int wv = __ldg(row + y);
-            if (wv == FM_ABSENT_WEIGHT || is_fixed(a, x, y)) continue;
+            if (wv == FM_ABSENT_WEIGHT) continue;
+            if (a.use_fix && ((__ldg(frow + (y >> 5)) >> (y & 31)) & 1u)) continue;
             const long long v = -(long long)wv * a.scale - __ldcg((const long long *)a.py + y);
             if (v < bv) { bv = v; bi = y; }
         }
     }
-    warp_argmin(bv, bi);
-    best = bv;
-    arg = bi;
 }
 
-// X op: relabel if the cheapest arc is not admissible, then push one unit on it.
+// Partial scan for Y op: over x matched to y (non-frozen) of the reverse arc's
+// part-reduced cost +(n+1) w(x,y) - p(x).
+__device__ __forceinline__ void ycand_partial(const AssignDev &a, int y, int t, int T,
+                                              long long &bv, int &bi) {
+    const int n = a.n;
+    if ((n & 3) == 0) {
+        const int n4 = n >> 2;
+        const int4 *m4 = reinterpret_cast<const int4 *>(a.match);
+        for (int j0 = t; j0 < n4; j0 += 4 * T) {
+            int4 mm[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = j0 + u * T;
+                mm[u] = j < n4 ? __ldcg(m4 + j) : make_int4(-1, -1, -1, -1);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = j0 + u * T;
+                const int mv[4] = {mm[u].x, mm[u].y, mm[u].z, mm[u].w};
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    if (mv[k] != y) continue;
+                    const int x = 4 * j + k;
+                    if (__ldcg(a.frozen + x)) continue;
+                    const long long v = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale -
+                                        __ldcg((const long long *)a.px + x);
+                    if (v < bv) { bv = v; bi = x; }
+                }
+            }
+        }
+    } else {
+        for (int x = t; x < n; x += T) {
+            if (__ldcg(a.match + x) != y || __ldcg(a.frozen + x)) continue;
+            const long long v = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale -
+                                __ldcg((const long long *)a.px + x);
+            if (v < bv) { bv = v; bi = x; }
+        }
+    }
+}
+
+// X op by one group (warp when CTA_WIDE is false, else the whole CTA): relabel if
+// the cheapest arc is not admissible, then push the unit on it.
+template <bool CTA_WIDE>
 __device__ void x_op(const AssignDev &a, int x, int32_t *ylist_next, int32_t *ycnt_next,
                      unsigned long long &pushes, unsigned long long &relabels) {
-    long long best;
-    int y;
-    scan_row(a, x, best, y);
-    const int lane = threadIdx.x & 31;
-    if (lane == 0) {
+    long long best = I64_MAX;
+    int y = INT32_MAX;
+    const int t = CTA_WIDE ? threadIdx.x : (threadIdx.x & 31);
+    row_partial(a, x, t, CTA_WIDE ? ATHREADS : 32, best, y);
+    if (CTA_WIDE) cta_argmin(best, y); else warp_argmin(best, y);
+    if (t == 0) {
         if (y == INT32_MAX) {
-            atomicExch(a.cnt + 4, 1);  // active node with no residual arc: infeasible
+            atomicExch(a.cnt + C_INFEASIBLE, 1);  // active node with no residual arc
         } else {
             const long long px = a.px[x];
-            if (!(best < -px)) {       // not admissible: p(x) <- -(best + eps)
+            if (!(best < -px)) {                 // not admissible: p(x) <- -(best + eps)
                 a.px[x] = -(best + a.eps);
                 relabels++;
+                atomicAdd(a.cnt + C_RELABELS, 1);
             }
-            a.match[x] = y;            // unit push x -> y
+            a.match[x] = y;                      // unit push x -> y
             pushes++;
             const int old = atomicAdd(a.ey + y, 1);
             if (old == 0) ylist_next[atomicAdd(ycnt_next, 1)] = y;
         }
     }
-    __syncwarp();
+    if (CTA_WIDE) __syncthreads(); else __syncwarp();
 }
 
-// Y op: while y holds excess, push a unit back to its cheapest incoming X
-// (reverse arc cost +(n+1) w), relabelling y first when it is not admissible.
+// Y op: while y holds excess, push a unit back to its cheapest incoming X,
+// relabelling y first when that reverse arc is not admissible.
+template <bool CTA_WIDE>
 __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
                      unsigned long long &pushes, unsigned long long &relabels) {
-    const int lane = threadIdx.x & 31;
+    const int t = CTA_WIDE ? threadIdx.x : (threadIdx.x & 31);
     int ey = __ldcg(a.ey + y);
     long long py = __ldcg((const long long *)a.py + y);
     while (ey > 0) {
         long long bv = I64_MAX;
         int bi = INT32_MAX;
-        for (int x = lane; x < a.n; x += 32) {
-            if (__ldcg(a.match + x) != y || __ldcg(a.frozen + x)) continue;
-            const long long v = (long long)__ldg(a.w + (size_t)x * a.n + y) * a.scale -
-                                __ldcg((const long long *)a.px + x);
-            if (v < bv) { bv = v; bi = x; }
-        }
-        warp_argmin(bv, bi);
+        ycand_partial(a, y, t, CTA_WIDE ? ATHREADS : 32, bv, bi);
+        if (CTA_WIDE) cta_argmin(bv, bi); else warp_argmin(bv, bi);
         if (bi == INT32_MAX) {  // cannot happen for a consistent state
-            if (lane == 0) atomicExch(a.cnt + 4, 2);
+            if (t == 0) atomicExch(a.cnt + C_INFEASIBLE, 2);
             break;
         }
-        if (lane == 0) {
+        if (t == 0) {
             if (!(bv < -py)) {
                 py = -(bv + a.eps);
                 relabels++;
+                atomicAdd(a.cnt + C_RELABELS, 1);
             }
             a.match[bi] = -1;
             xlist_next[atomicAdd(xcnt_next, 1)] = bi;
             pushes++;
         }
         ey--;
-        __syncwarp();
+        if (CTA_WIDE) __syncthreads(); else __syncwarp();
     }
-    if (lane == 0) {
+    if (t == 0) {
         a.py[y] = py;
         a.ey[y] = ey;
     }
-    __syncwarp();
+    if (CTA_WIDE) __syncthreads(); else __syncwarp();
 }
 
 // begin_refine (assign_scaling.py:145-182) fused with the first X phase: drop
@@ -175,28 +268,28 @@ __global__ void __launch_bounds__(ATHREADS) begin_refine_kernel(AssignDev a) {
     const int warp = (blockIdx.x * ATHREADS + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * ATHREADS) >> 5;
     const int lane = threadIdx.x & 31;
-    unsigned long long pushes = 0, relabels = 0;
+    unsigned long long pushes = 0;
     for (int x = warp; x < a.n; x += nwarps) {
-        long long best;
-        int y;
-        scan_row(a, x, best, y);
+        long long best = I64_MAX;
+        int y = INT32_MAX;
+        row_partial(a, x, lane, 32, best, y);
+        warp_argmin(best, y);
         if (lane == 0) {
             if (y != INT32_MAX) a.px[x] = -(best + a.eps);
             if (!a.frozen[x]) {
                 if (y == INT32_MAX) {
                     a.match[x] = -1;
-                    atomicExch(a.cnt + 4, 1);
+                    atomicExch(a.cnt + C_INFEASIBLE, 1);
                 } else {
                     a.match[x] = y;
                     pushes++;
                     const int old = atomicAdd(a.ey + y, 1);
-                    if (old == 0) a.ylist[0][atomicAdd(a.cnt + 2, 1)] = y;
+                    if (old == 0) a.ylist[0][atomicAdd(a.cnt + C_Y0, 1)] = y;
                 }
             }
         }
     }
-    if (lane == 0 && pushes) atomicAdd(a.ops + 0, pushes);
-    (void)relabels;
+    if (lane == 0 && pushes) atomicAdd(a.ops + O_PUSH, pushes);
 }
 
 // excess of y after flow removal: supplies (-1) + frozen flows (assign_scaling.py:158-168)
@@ -208,52 +301,177 @@ __global__ void reset_excess_kernel(AssignDev a) {
 // The refine's push/relabel rounds (refine_par's coordinator loop, assign_par.py:162-236)
 // as one cooperative kernel.  Round r: Y phase over ylist[r&1] -> xlist[r&1];
 // grid barrier; X phase over xlist[r&1] -> ylist[(r+1)&1]; grid barrier.
+// Exits when no Y holds excess (refine done) or when a price update is due
+// (relabels since the last one >= pu_threshold); the round index persists in cnt.
+// Once the Y list is short the other CTAs leave and CTA 0 finishes alone with
+// CTA-wide ops and CTA barriers (the long single-digit tail).
 __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, int tail_threshold,
-                                                                 long long round_budget) {
+                                                                 long long round_budget,
+                                                                 int pu_threshold) {
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31;
     const int gwarp = (blockIdx.x * ATHREADS + threadIdx.x) >> 5;
     const int gwarps = (gridDim.x * ATHREADS) >> 5;
     const int cwarp = threadIdx.x >> 5;
-    unsigned long long pushes = 0, relabels = 0, rounds = 0, tail_rounds = 0;
+    unsigned long long pushes = 0, relabels = 0, rounds = 0, tail_rounds = 0, tail_ops = 0;
     bool tail = false;
-    for (int r = 0;; r++) {
+    int r = __ldcg(a.cnt + C_ROUND);
+    for (;; r++) {
         const int b = r & 1, nb = b ^ 1;
-        const int ny = __ldcg(a.cnt + 2 + b);
-        if (ny == 0 || __ldcg(a.cnt + 4)) break;
+        const int ny = __ldcg(a.cnt + C_Y0 + b);
+        if (ny == 0 || __ldcg(a.cnt + C_INFEASIBLE)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 0;
+            break;
+        }
+        if (pu_threshold > 0 && __ldcg(a.cnt + C_RELABELS) >= pu_threshold) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 1;
+            break;
+        }
         if (r >= round_budget) {  // prices diverge: no perfect matching (assign_par.py:221-226)
-            if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(a.cnt + 4, 3);
+            if (blockIdx.x == 0 && threadIdx.x == 0) { atomicExch(a.cnt + C_INFEASIBLE, 3); a.cnt[C_EXIT] = 0; }
             break;
         }
         if (!tail && ny <= tail_threshold) {
             tail = true;
-            if (blockIdx.x != 0) break;  // CTA 0 finishes the refine alone
+            if (blockIdx.x != 0) break;  // CTA 0 finishes alone
         }
         rounds++;
         if (tail) tail_rounds++;
-        const int wi = tail ? cwarp : gwarp;
-        const int wn = tail ? AWARPS : gwarps;
         // ---- Y phase
-        if ((tail || blockIdx.x == 0) && threadIdx.x == 0) {
-            a.cnt[nb] = 0;      // X list of round r+1 (last read in round r-1)
-            a.cnt[2 + nb] = 0;  // Y list of round r+1 (last read at round r-1)
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            a.cnt[C_X0 + nb] = 0;   // X list of round r+1 (last read in round r-1)
+            a.cnt[C_Y0 + nb] = 0;   // Y list of round r+1 (last read at round r-1)
         }
-        for (int i = wi; i < ny; i += wn)
-            y_op(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + b, pushes, relabels);
-        if (tail) { __threadfence_block(); __syncthreads(); } else grid.sync();
-        // ---- X phase
-        const int nx = __ldcg(a.cnt + b);
-        for (int i = wi; i < nx; i += wn)
-            x_op(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + 2 + nb, pushes, relabels);
-        if (tail) { __threadfence_block(); __syncthreads(); } else grid.sync();
+        if (tail) {
+            const unsigned long long p0 = pushes + relabels;
+            if (ny <= 2) {
+                for (int i = 0; i < ny; i++)
+                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+            } else {
+                for (int i = cwarp; i < ny; i += AWARPS)
+                    y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+            }
+            __threadfence_block();
+            __syncthreads();
+            const int nx = __ldcg(a.cnt + C_X0 + b);
+            if (nx <= 2) {
+                for (int i = 0; i < nx; i++)
+                    x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+            } else {
+                for (int i = cwarp; i < nx; i += AWARPS)
+                    x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+            }
+            __threadfence_block();
+            __syncthreads();
+            tail_ops += pushes + relabels - p0;
+        } else {
+            for (int i = gwarp; i < ny; i += gwarps)
+                y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+            grid.sync();
+            const int nx = __ldcg(a.cnt + C_X0 + b);
+            for (int i = gwarp; i < nx; i += gwarps)
+                x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+            grid.sync();
+        }
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_ROUND] = r;
     if (lane == 0) {
-        if (pushes) atomicAdd(a.ops + 0, pushes);
-        if (relabels) atomicAdd(a.ops + 1, relabels);
+        if (pushes) atomicAdd(a.ops + O_PUSH, pushes);
+        if (relabels) atomicAdd(a.ops + O_RELABEL, relabels);
     }
-    if (threadIdx.x == 0 && (blockIdx.x == 0)) {
-        atomicAdd(a.ops + 2, rounds);
-        atomicAdd(a.ops + 3, tail_rounds);
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        atomicAdd(a.ops + O_ROUNDS, rounds);
+        atomicAdd(a.ops + O_TAIL_ROUNDS, tail_rounds);
+        atomicAdd(a.ops + O_TAIL_OPS, tail_ops);
+    }
+    (void)cwarp;
+}
+
+// price_update_heuristic (assign_scaling.py:208-276) at a quiescent point of the
+// refine: label every node with its distance to the deficit set over residual
+// arcs, arc length floor(c_p / eps) + 1 (>= 0), in eps units; then lower each
+// price by eps * min(label, last + 1), last = the largest label of an active node.
+// The reference scans Dial buckets; here the same labels come from a Bellman-Ford
+// fixpoint over the dense matrix (X step: warp per row; Y step: one thread per
+// matched X, atomicMin into its Y), one grid barrier per half-step.
+__global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a) {
+    cg::grid_group grid = cg::this_grid();
+    const int n = a.n;
+    const int tid = blockIdx.x * ATHREADS + threadIdx.x, nthr = gridDim.x * ATHREADS;
+    const int lane = threadIdx.x & 31;
+    const int gwarp = tid >> 5, gwarps = nthr >> 5;
+    for (int v = tid; v < n; v += nthr) {
+        a.ly[v] = __ldcg(a.ey + v) < 0 ? 0 : LINF;
+        a.lx[v] = LINF;
+    }
+    if (tid == 0) { a.cnt[C_PU_CHG] = 0; a.cnt[C_PU_CHG + 1] = 0; a.cnt[C_PU_LAST] = 0; }
+    grid.sync();
+    int it = 0;
+    for (;; it++) {
+        int32_t *chg = a.cnt + C_PU_CHG + (it & 1);
+        bool changed = false;
+        // X step: l(x) = min over residual x->y of l(y) + floor(c_p(x,y)/eps) + 1
+        for (int x = gwarp; x < n; x += gwarps) {
+            const int32_t *row = a.w + (size_t)x * n;
+            const uint32_t *frow = a.fixed + (size_t)x * a.nw;
+            const int mx = __ldcg(a.match + x);
+            const long long px = __ldcg((const long long *)a.px + x);
+            int best = LINF;
+            for (int y = lane; y < n; y += 32) {
+                const int ly = __ldcg(a.ly + y);
+                if (ly >= LINF || y == mx) continue;
+                const int wv = __ldg(row + y);
+                if (wv == FM_ABSENT_WEIGHT) continue;
+                if (a.use_fix && ((__ldg(frow + (y >> 5)) >> (y & 31)) & 1u)) continue;
+                const long long rc = -(long long)wv * a.scale + px - __ldcg((const long long *)a.py + y);
+                long long len = floordiv(rc, a.eps) + 1;
+                if (len < 0) len = 0;
+                const long long cand = (long long)ly + len;
+                if (cand <= a.max_bucket && cand < best) best = (int)cand;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+            if (lane == 0 && best < __ldcg(a.lx + x)) { a.lx[x] = best; changed = true; }
+        }
+        grid.sync();
+        // Y step: l(y) = min over x matched to y (non-frozen) of l(x) + floor(c_p(y->x)/eps) + 1
+        for (int x = tid; x < n; x += nthr) {
+            const int y = __ldcg(a.match + x);
+            const int lxv = __ldcg(a.lx + x);
+            if (y < 0 || lxv >= LINF || __ldcg(a.frozen + x)) continue;
+            const long long rc = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale -
+                                 __ldcg((const long long *)a.px + x) + __ldcg((const long long *)a.py + y);
+            long long len = floordiv(rc, a.eps) + 1;
+            if (len < 0) len = 0;
+            const long long cand = (long long)lxv + len;
+            if (cand > a.max_bucket) continue;
+            const int old = atomicMin(a.ly + y, (int)cand);
+            if ((int)cand < old) changed = true;
+        }
+        if (tid == 0) a.cnt[C_PU_CHG + ((it + 1) & 1)] = 0;
+        if (__syncthreads_or(changed) && threadIdx.x == 0) atomicExch(chg, 1);
+        grid.sync();
+        if (__ldcg(chg) == 0) break;
+    }
+    // last = max label over active nodes (unmatched X, Y with positive excess)
+    int last = 0;
+    for (int v = tid; v < n; v += nthr) {
+        if (__ldcg(a.match + v) < 0 && !__ldcg(a.frozen + v)) last = max(last, min(__ldcg(a.lx + v), LINF));
+        if (__ldcg(a.ey + v) > 0) last = max(last, min(__ldcg(a.ly + v), LINF));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+    if (lane == 0 && last) atomicMax(a.cnt + C_PU_LAST, last);
+    grid.sync();
+    const long long K = min((long long)__ldcg(a.cnt + C_PU_LAST), (long long)a.max_bucket) + 1;
+    for (int v = tid; v < n; v += nthr) {
+        a.px[v] -= a.eps * min((long long)a.lx[v], K);
+        a.py[v] -= a.eps * min((long long)a.ly[v], K);
+    }
+    if (tid == 0) {
+        a.cnt[C_RELABELS] = 0;
+        atomicAdd(a.ops + O_PU, 1ull);
+        atomicAdd(a.ops + O_PU_ITERS, (unsigned long long)(it + 1));
     }
 }
 
@@ -290,7 +508,7 @@ __global__ void arc_fix_kernel(AssignDev a) {
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0 && cnt) atomicAdd(a.ops + 4, cnt);
+    if (lane == 0 && cnt) atomicAdd(a.ops + O_FIXED, cnt);
 }
 
 // max |w| over present arcs (scaled_cost_bound = (n+1) max|w|, assign_scaling.py:133)
@@ -374,34 +592,45 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
     const double budget_d = std::max(1e4, 40.0 * n * (double)n * std::max<double>(1.0, (double)A->h_acc[2]));
     const long long round_budget = budget_d > 4e18 ? (long long)4e18 : (long long)budget_d;
     long long eps = std::max(1LL, bound);
-    const int tail_threshold = AWARPS;
+    const int tail_threshold = 4;
+    const int pu_threshold = (flags & FM_ASSIGN_PRICE_UPDATE) ? std::max(64, n / 4) : 0;
     int rc = FM_OK;
     for (;;) {
         eps = std::max(1LL, (eps + alpha - 1) / alpha);   // -(-eps // alpha)
         d.eps = eps;
-        FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * 8, s));
+        d.max_bucket = bound / eps + 2;
+        FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * C_COUNT, s));
         reset_excess_kernel<<<(n + 255) / 256, 256, 0, s>>>(d);
         FM_CHECK_LAUNCH();
         begin_refine_kernel<<<std::max(1, std::min((n + AWARPS - 1) / AWARPS, A->sms * 4)), ATHREADS, 0, s>>>(d);
         FM_CHECK_LAUNCH();
-        void *args[] = {(void *)&d, (void *)&tail_threshold, (void *)&round_budget};
-        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
-                                                  dim3(ATHREADS), args, 0, s));
-        A->st.launches += 3;
+        A->st.launches += 2;
+        for (;;) {
+            void *args[] = {(void *)&d, (void *)&tail_threshold, (void *)&round_budget, (void *)&pu_threshold};
+            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
+                                                      dim3(ATHREADS), args, 0, s));
+            A->st.launches++;
+            FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, d.cnt, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, s));
+            FM_CHECK_CUDA(cudaStreamSynchronize(s));
+            if (A->h_cnt[C_INFEASIBLE] || A->h_cnt[C_EXIT] != 1) break;
+            void *pargs[] = {(void *)&d};
+            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->coop_blocks),
+                                                      dim3(ATHREADS), pargs, 0, s));
+            A->st.launches++;
+        }
         if (d.use_fix) {
             arc_fix_kernel<<<std::max(1, std::min((n + 7) / 8, A->sms * 8)), 256, 0, s>>>(d);
             FM_CHECK_LAUNCH();
             A->st.launches++;
         }
         A->st.refines++;
-        FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, d.cnt, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, s));
-        FM_CHECK_CUDA(cudaStreamSynchronize(s));
-        if (A->h_cnt[4]) {
+        if (A->h_cnt[C_INFEASIBLE]) {
+            const int why = A->h_cnt[C_INFEASIBLE];
             rc = FM_INFEASIBLE;
-            fm_set_error(A->h_cnt[4] == 1 ? "active node has no residual arc: instance admits no perfect matching"
-                         : A->h_cnt[4] == 3 ? "operation budget exceeded; prices diverge, instance admits no perfect matching"
-                                            : "inconsistent Y excess during refine");
-            if (A->h_cnt[4] == 2) { rc = FM_CUDA_ERROR; break; }
+            fm_set_error(why == 1 ? "active node has no residual arc: instance admits no perfect matching"
+                         : why == 3 ? "operation budget exceeded; prices diverge, instance admits no perfect matching"
+                                    : "inconsistent Y excess during refine");
+            if (why == 2) rc = FM_CUDA_ERROR;
             break;
         }
         if (eps == 1) break;
@@ -429,8 +658,11 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
     A->st.pushes = (int64_t)A->h_ops[0];
     A->st.relabels = (int64_t)A->h_ops[1];
     A->st.rounds = (int64_t)A->h_ops[2];
-    A->st.pr_sweeps = (int64_t)A->h_ops[3];  // rounds run by the single-CTA tail
-    A->st.reserved[0] = (int64_t)A->h_ops[4]; // pairs fixed
+    A->st.pr_sweeps = (int64_t)A->h_ops[O_TAIL_ROUNDS];  // rounds run by the single-CTA tail
+    A->st.reserved[0] = (int64_t)A->h_ops[O_FIXED];      // pairs fixed
+    A->st.reserved[1] = (int64_t)A->h_ops[O_PU];         // price updates
+    A->st.reserved[2] = (int64_t)A->h_ops[O_PU_ITERS];   // Bellman-Ford iterations in them
+    A->st.reserved[3] = (int64_t)A->h_ops[O_TAIL_OPS];   // ops done by the single-CTA tail
     // algorithmic bytes: every op scans one weight row (4n) + n prices (8n); the
     // begin phase and arc fixing read the whole matrix once each per refine
     A->st.bytes_push = (A->st.pushes + A->st.relabels) * 12LL * n +
@@ -465,12 +697,14 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMalloc((void **)&d.xlist[1], sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.ylist[0], sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.ylist[1], sizeof(int32_t) * n) == cudaSuccess &&
-              cudaMalloc((void **)&d.cnt, sizeof(int32_t) * 8) == cudaSuccess &&
+              cudaMalloc((void **)&d.cnt, sizeof(int32_t) * C_COUNT) == cudaSuccess &&
+              cudaMalloc((void **)&d.lx, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&d.ly, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * 8) == cudaSuccess &&
               cudaMalloc((void **)&A->acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
               cudaMallocHost((void **)&A->h_ops, sizeof(unsigned long long) * 8) == cudaSuccess &&
               cudaMallocHost((void **)&A->h_acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
-              cudaMallocHost((void **)&A->h_cnt, sizeof(int32_t) * 8) == cudaSuccess &&
+              cudaMallocHost((void **)&A->h_cnt, sizeof(int32_t) * C_COUNT) == cudaSuccess &&
               cudaStreamCreateWithFlags(&A->own_stream, cudaStreamNonBlocking) == cudaSuccess;
     if (!ok) {
         fm_set_error("fm_assign_create: allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -480,8 +714,10 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
     A->stream = A->own_stream;
     cudaDeviceGetAttribute(&A->sms, cudaDevAttrMultiProcessorCount, device);
     int per_sm = 0;
+    int per_sm2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_rounds_kernel, ATHREADS, 0);
-    A->coop_blocks = std::max(1, std::min(per_sm, 2) * A->sms);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, price_update_kernel, ATHREADS, 0);
+    A->coop_blocks = std::max(1, std::min(std::min(per_sm, per_sm2), 2) * A->sms);
     *out = A;
     return FM_OK;
 }
@@ -491,6 +727,7 @@ extern "C" void fm_assign_destroy(fm_assign *A) {
     cudaSetDevice(A->device);
     void *dev[] = {A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.frozen, A->d.frozen_in,
                    A->d.xlist[0], A->d.xlist[1], A->d.ylist[0], A->d.ylist[1], A->d.cnt, A->d.ops,
+                   A->d.lx, A->d.ly,
                    A->acc, A->in_w};
     for (void *p : dev) if (p) cudaFree(p);
     if (A->h_ops) cudaFreeHost(A->h_ops);

@@ -8,6 +8,7 @@
 // cut by a seeded residual reach.  See DESIGN.md.
 #include <algorithm>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "fm_common.cuh"
@@ -27,6 +28,13 @@ struct GridDev {
     int32_t *e, *h, *rR, *rL, *rD, *rU, *rT, *rS, *cS;
     int32_t *dist;
     uint8_t *mask, *marked, *cut;
+    // tile-resident kernel (K1 v2): flow pushed across a tile border is parked in
+    // an inbox of the receiving pixel (inflow_h: across a vertical tile border,
+    // inflow_v: across a horizontal one) until the receiving tile next loads
+    int32_t *inflow_h, *inflow_v;
+    int32_t *tile_active;   // tile had an active pixel when it was last written back
+    int32_t *tile_inflow;   // someone parked flow in this tile's inboxes
+    int32_t ntx, nty;       // tiles per row / column
     int32_t H, W;
     int32_t V;      // node count |V| = H*W + 2 (the source's height)
     int32_t INF;    // "unreached" distance sentinel (== V)
@@ -67,6 +75,8 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
         g.rU[p] = max(cu, 0);
         g.h[p] = 0;
         g.marked[p] = 0;
+        g.inflow_h[p] = 0;
+        g.inflow_v[p] = 0;
         sum += cs;
     }
     // grid-stride kernel with 1-D blocks of 256
@@ -160,6 +170,199 @@ __global__ void __launch_bounds__(256) pr_sweep_kernel(GridDev g, int32_t *activ
 }
 
 // ----------------------------------------------------------------------------
+// K1 (v2, default): tile-resident lock-free push-relabel.  One CTA stages a 32x32
+// tile (e, h, four direction residuals, sink residual) plus a 1-pixel halo of
+// neighbour heights in shared memory and runs up to k_local lock-free passes of
+// the maxflow_par.py:95-128 operation with shared-memory atomics.  No barrier
+// orders the passes (warps free-run, as the reference's workers do); a CTA-wide
+// vote every 4 passes ends the visit once no pixel of the tile is active.
+// A push across the tile border lowers the sender's own residual and parks the
+// amount in the receiver's inbox, so no other CTA ever writes a word this CTA
+// holds in shared memory; the receiver folds its inbox into e and the reverse
+// residual when it next loads (or the coordinator does, before a global relabel).
+// Halo heights are a snapshot: stale reads are tolerated by the lock-free
+// argument, exactly like a worker reading a neighbour's height.
+// ----------------------------------------------------------------------------
+constexpr int PT_W = 32, PT_H = 32, PT_TY = 16;          // 512 threads, 2 rows each
+constexpr int PT_ROWS = PT_H / PT_TY;
+
+__global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_local,
+                                                               int32_t *processed,
+                                                               unsigned long long *ops) {
+    __shared__ int32_t s_e[PT_H][PT_W];
+    __shared__ int32_t s_h[PT_H + 2][PT_W + 2];
+    __shared__ int32_t s_r[4][PT_H][PT_W];   // R, L, D, U
+    __shared__ int32_t s_t[PT_H][PT_W];
+    __shared__ int s_go;
+    const int tile = blockIdx.x;
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int r0 = tyi * PT_H, c0 = txi * PT_W;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    if (tx == 0 && ty == 0) {
+        int go = g.tile_active[tile];
+        if (atomicExch(g.tile_inflow + tile, 0)) go = 1;
+        s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    __threadfence();
+    const int V = g.V;
+    const int c = c0 + tx;
+    int32_t rs[PT_ROWS];
+#pragma unroll
+    for (int k = 0; k < PT_ROWS; k++) {
+        const int lr = ty + k * PT_TY;
+        const int r = r0 + lr;
+        if (r < g.H && c < g.W) {
+            const int64_t p = (int64_t)r * g.W + c;
+            int32_t e = g.e[p];
+            int32_t rr = g.rR[p], rl = g.rL[p], rd = g.rD[p], ru = g.rU[p];
+            if (tx == 0 && c > 0) { const int32_t d = atomicExch(g.inflow_h + p, 0); e += d; rl += d; }
+            if (tx == PT_W - 1 && c + 1 < g.W) { const int32_t d = atomicExch(g.inflow_h + p, 0); e += d; rr += d; }
+            if (lr == 0 && r > 0) { const int32_t d = atomicExch(g.inflow_v + p, 0); e += d; ru += d; }
+            if (lr == PT_H - 1 && r + 1 < g.H) { const int32_t d = atomicExch(g.inflow_v + p, 0); e += d; rd += d; }
+            s_e[lr][tx] = e;
+            s_h[lr + 1][tx + 1] = g.h[p];
+            s_r[0][lr][tx] = rr; s_r[1][lr][tx] = rl; s_r[2][lr][tx] = rd; s_r[3][lr][tx] = ru;
+            s_t[lr][tx] = g.rT[p];
+            rs[k] = g.rS[p];
+        } else {
+            s_e[lr][tx] = 0;
+            s_h[lr + 1][tx + 1] = V;
+            s_r[0][lr][tx] = s_r[1][lr][tx] = s_r[2][lr][tx] = s_r[3][lr][tx] = 0;
+            s_t[lr][tx] = 0;
+            rs[k] = 0;
+        }
+    }
+    // halo snapshot of neighbour heights
+    {
+        const int tid = ty * PT_W + tx;
+        if (tid < 4 * PT_W) {
+            const int side = tid / PT_W, i = tid % PT_W;
+            int r, cc, hr, hc;
+            if (side == 0) { r = r0 - 1; cc = c0 + i; hr = 0; hc = i + 1; }
+            else if (side == 1) { r = r0 + PT_H; cc = c0 + i; hr = PT_H + 1; hc = i + 1; }
+            else if (side == 2) { r = r0 + i; cc = c0 - 1; hr = i + 1; hc = 0; }
+            else { r = r0 + i; cc = c0 + PT_W; hr = i + 1; hc = PT_W + 1; }
+            s_h[hr][hc] = (r >= 0 && r < g.H && cc >= 0 && cc < g.W) ? g.h[(int64_t)r * g.W + cc] : V;
+        }
+    }
+    __syncthreads();
+
+    volatile int32_t *ve = &s_e[0][0];
+    volatile int32_t *vh = &s_h[0][0];
+    volatile int32_t *vt = &s_t[0][0];
+    constexpr int HS = PT_W + 2;  // s_h row stride
+    long long pushes = 0, relabels = 0;
+    for (int it = 0; it < k_local; it++) {
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < PT_ROWS; k++) {
+            const int lr = ty + k * PT_TY;
+            const int li = lr * PT_W + tx;
+            const int32_t e = ve[li];
+            if (e <= 0) continue;
+            const int hi = (lr + 1) * HS + tx + 1;
+            const int32_t hp = vh[hi];
+            if (hp >= V) continue;
+            any = true;
+            const int32_t rt = vt[li];
+            if (rt > 0 && hp > 0) {                       // sink at height 0
+                const int32_t d = min(e, rt);
+                vt[li] = rt - d;                          // owner-only word
+                atomicSub(&s_e[lr][tx], d);
+                pushes++;
+                continue;
+            }
+            const int r = r0 + lr;
+            int32_t best_h = INT32_MAX, best_r = 0;
+            int dir = -1;
+            if (rt > 0) { best_h = 0; dir = 4; }
+            const int32_t rr = *(volatile int32_t *)&s_r[0][lr][tx];
+            if (rr > 0 && c + 1 < g.W) { const int32_t hq = vh[hi + 1]; if (hq < best_h) { best_h = hq; best_r = rr; dir = 0; } }
+            const int32_t rl = *(volatile int32_t *)&s_r[1][lr][tx];
+            if (rl > 0 && c > 0) { const int32_t hq = vh[hi - 1]; if (hq < best_h) { best_h = hq; best_r = rl; dir = 1; } }
+            const int32_t rd = *(volatile int32_t *)&s_r[2][lr][tx];
+            if (rd > 0 && r + 1 < g.H) { const int32_t hq = vh[hi + HS]; if (hq < best_h) { best_h = hq; best_r = rd; dir = 2; } }
+            const int32_t ru = *(volatile int32_t *)&s_r[3][lr][tx];
+            if (ru > 0 && r > 0) { const int32_t hq = vh[hi - HS]; if (hq < best_h) { best_h = hq; best_r = ru; dir = 3; } }
+            if (rs[k] > 0 && V < best_h) { best_h = V; dir = 5; }
+            if (dir < 0) continue;
+            if (hp > best_h && dir < 4) {
+                const int32_t d = min(e, best_r);
+                atomicSub(&s_e[lr][tx], d);
+                atomicSub(&s_r[dir][lr][tx], d);
+                int qr = lr, qc = tx;
+                if (dir == 0) qc++; else if (dir == 1) qc--; else if (dir == 2) qr++; else qr--;
+                const int rev = dir ^ 1;                  // R<->L, D<->U
+                if (qr >= 0 && qr < PT_H && qc >= 0 && qc < PT_W) {
+                    atomicAdd(&s_r[rev][qr][qc], d);
+                    atomicAdd(&s_e[qr][qc], d);
+                } else {
+                    const int64_t q = (int64_t)(r0 + qr) * g.W + (c0 + qc);
+                    atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + q, d);
+                    __threadfence();
+                    const int nt = (dir == 0) ? tile + 1 : (dir == 1) ? tile - 1
+                                 : (dir == 2) ? tile + g.ntx : tile - g.ntx;
+                    g.tile_inflow[nt] = 1;
+                }
+                pushes++;
+            } else {
+                vh[hi] = best_h + 1;
+                relabels++;
+            }
+        }
+        if ((it & 3) == 3 && !__syncthreads_or(any)) break;
+    }
+    __syncthreads();
+    bool act = false;
+#pragma unroll
+    for (int k = 0; k < PT_ROWS; k++) {
+        const int lr = ty + k * PT_TY;
+        const int r = r0 + lr;
+        if (r < g.H && c < g.W) {
+            const int64_t p = (int64_t)r * g.W + c;
+            const int32_t e = s_e[lr][tx], h = s_h[lr + 1][tx + 1];
+            g.e[p] = e;
+            g.h[p] = h;
+            g.rR[p] = s_r[0][lr][tx]; g.rL[p] = s_r[1][lr][tx];
+            g.rD[p] = s_r[2][lr][tx]; g.rU[p] = s_r[3][lr][tx];
+            g.rT[p] = s_t[lr][tx];
+            act |= (e > 0 && h < V);
+        }
+    }
+    const int any_act = __syncthreads_or(act);
+    if (tx == 0 && ty == 0) {
+        g.tile_active[tile] = any_act;
+        atomicAdd(processed, 1);
+    }
+    block_add_i64<PT_W * PT_TY / 32>(pushes, ops + 0);
+    block_add_i64<PT_W * PT_TY / 32>(relabels, ops + 1);
+}
+
+// fold every parked inbox into e and the reverse residual (coordinator point)
+__global__ void integrate_inflow_kernel(GridDev g) {
+    const int tile = blockIdx.x;
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int r0 = tyi * PT_H, c0 = txi * PT_W;
+    const int i = threadIdx.x;  // 0..127: top, bottom, left, right
+    const int side = i / PT_W, j = i % PT_W;
+    int r, c;
+    if (side == 0) { r = r0; c = c0 + j; }
+    else if (side == 1) { r = r0 + PT_H - 1; c = c0 + j; }
+    else if (side == 2) { r = r0 + j; c = c0; }
+    else { r = r0 + j; c = c0 + PT_W - 1; }
+    if (r >= g.H || c >= g.W) return;
+    const int64_t p = (int64_t)r * g.W + c;
+    // a tile corner is visited by two threads (one per side): e needs an atomic
+    if (side == 0 && r > 0) { const int32_t d = g.inflow_v[p]; if (d) { g.inflow_v[p] = 0; atomicAdd(g.e + p, d); g.rU[p] += d; } }
+    if (side == 1 && r + 1 < g.H) { const int32_t d = g.inflow_v[p]; if (d) { g.inflow_v[p] = 0; atomicAdd(g.e + p, d); g.rD[p] += d; } }
+    if (side == 2 && c > 0) { const int32_t d = g.inflow_h[p]; if (d) { g.inflow_h[p] = 0; atomicAdd(g.e + p, d); g.rL[p] += d; } }
+    if (side == 3 && c + 1 < g.W) { const int32_t d = g.inflow_h[p]; if (d) { g.inflow_h[p] = 0; atomicAdd(g.e + p, d); g.rR[p] += d; } }
+    if (i == 0) g.tile_inflow[tile] = 0;
+}
+
+// ----------------------------------------------------------------------------
 // cancel_violations (maxflow_par.py:132-154), opt-in: saturate every residual arc
 // whose tail sits more than one level above its head.  Mates of cancelled arcs
 // have the lower endpoint as tail and never violate, so arcs are independent.
@@ -220,11 +423,35 @@ __global__ void bfs_init_kernel(GridDev g) {
     }
 }
 
-__global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int32_t *changed_flag) {
+// Frontier-driven: a tile is visited only when its own flag is set (all tiles on
+// the first sweep, afterwards only tiles whose halo changed in the previous sweep).
+// A visit runs to the tile's local fixpoint, writes back what changed and flags the
+// neighbour tiles across every border that changed.  Converged when a sweep
+// changes nothing.
+__device__ __forceinline__ void flag_changed_borders(const GridDev &g, int tile, int tyi, int txi,
+                                                     int bt, int bb, int bl, int br, int32_t *flag_nxt) {
+    if (bt && tyi > 0) flag_nxt[tile - g.ntx] = 1;
+    if (bb && tyi + 1 < g.nty) flag_nxt[tile + g.ntx] = 1;
+    if (bl && txi > 0) flag_nxt[tile - 1] = 1;
+    if (br && txi + 1 < g.ntx) flag_nxt[tile + 1] = 1;
+}
+
+__global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int32_t *flag_cur, int32_t *flag_nxt,
+                                                       int32_t *changed_count) {
     __shared__ int32_t sd[TILE_H + 2][TILE_W + 2];
-    const int c0 = blockIdx.x * TILE_W, r0 = blockIdx.y * TILE_H;
+    __shared__ int s_go, s_b[4];
+    const int tile = blockIdx.x;
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int c0 = txi * TILE_W, r0 = tyi * TILE_H;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * TILE_W + tx;
+    if (tid == 0) {
+        s_go = flag_cur[tile];
+        if (s_go) flag_cur[tile] = 0;
+        s_b[0] = s_b[1] = s_b[2] = s_b[3] = 0;
+    }
+    __syncthreads();
+    if (!s_go) return;
     for (int i = tid; i < (TILE_H + 2) * (TILE_W + 2); i += TILE_W * BLK_Y) {
         const int lr = i / (TILE_W + 2), lc = i % (TILE_W + 2);
         const int r = r0 + lr - 1, c = c0 + lc - 1;
@@ -263,11 +490,22 @@ __global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int32_t *chang
     if (any) {
 #pragma unroll
         for (int k = 0; k < ROWS_PER_THREAD; k++) {
-            const int r = r0 + ty + k * BLK_Y;
-            const int32_t v = sd[ty + k * BLK_Y + 1][tx + 1];
-            if (r < g.H && c < g.W && v != d0[k]) g.dist[(int64_t)r * g.W + c] = v;
+            const int lr = ty + k * BLK_Y;
+            const int r = r0 + lr;
+            const int32_t v = sd[lr + 1][tx + 1];
+            if (r < g.H && c < g.W && v != d0[k]) {
+                g.dist[(int64_t)r * g.W + c] = v;
+                if (lr == 0) s_b[0] = 1;
+                if (lr == TILE_H - 1) s_b[1] = 1;
+                if (tx == 0) s_b[2] = 1;
+                if (tx == TILE_W - 1) s_b[3] = 1;
+            }
         }
-        if (tid == 0) *changed_flag = 1;
+        __syncthreads();
+        if (tid == 0) {
+            flag_changed_borders(g, tile, tyi, txi, s_b[0], s_b[1], s_b[2], s_b[3], flag_nxt);
+            atomicAdd(changed_count, 1);
+        }
     }
 }
 
@@ -286,6 +524,10 @@ __global__ void bfs_finalize_kernel(GridDev g, unsigned long long *acc /* [0] ac
             g.h[p] = d;
             active += e > 0;
             lvl = max(lvl, d);
+            if (e > 0) {
+                const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
+                g.tile_active[(r / PT_H) * g.ntx + c / PT_W] = 1;
+            }
         } else {
             if (g.h[p] < g.V) g.h[p] = g.V;
             if (!g.marked[p]) { g.marked[p] = 1; mex += e; }
@@ -331,11 +573,22 @@ __global__ void cut_init_kernel(GridDev g) {
     }
 }
 
-__global__ void __launch_bounds__(256) cut_tile_kernel(GridDev g, int32_t *changed_flag) {
+__global__ void __launch_bounds__(256) cut_tile_kernel(GridDev g, int32_t *flag_cur, int32_t *flag_nxt,
+                                                       int32_t *changed_count) {
     __shared__ uint8_t ss[TILE_H + 2][TILE_W + 2];
-    const int c0 = blockIdx.x * TILE_W, r0 = blockIdx.y * TILE_H;
+    __shared__ int s_go, s_b[4];
+    const int tile = blockIdx.x;
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int c0 = txi * TILE_W, r0 = tyi * TILE_H;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * TILE_W + tx;
+    if (tid == 0) {
+        s_go = flag_cur[tile];
+        if (s_go) flag_cur[tile] = 0;
+        s_b[0] = s_b[1] = s_b[2] = s_b[3] = 0;
+    }
+    __syncthreads();
+    if (!s_go) return;
     for (int i = tid; i < (TILE_H + 2) * (TILE_W + 2); i += TILE_W * BLK_Y) {
         const int lr = i / (TILE_W + 2), lc = i % (TILE_W + 2);
         const int r = r0 + lr - 1, c = c0 + lc - 1;
@@ -371,10 +624,21 @@ __global__ void __launch_bounds__(256) cut_tile_kernel(GridDev g, int32_t *chang
     if (any) {
 #pragma unroll
         for (int k = 0; k < ROWS_PER_THREAD; k++) {
-            const int r = r0 + ty + k * BLK_Y;
-            if (grew[k] && r < g.H && c < g.W) g.cut[(int64_t)r * g.W + c] = 1;
+            const int lr = ty + k * BLK_Y;
+            const int r = r0 + lr;
+            if (grew[k] && r < g.H && c < g.W) {
+                g.cut[(int64_t)r * g.W + c] = 1;
+                if (lr == 0) s_b[0] = 1;
+                if (lr == TILE_H - 1) s_b[1] = 1;
+                if (tx == 0) s_b[2] = 1;
+                if (tx == TILE_W - 1) s_b[3] = 1;
+            }
         }
-        if (tid == 0) *changed_flag = 1;
+        __syncthreads();
+        if (tid == 0) {
+            flag_changed_borders(g, tile, tyi, txi, s_b[0], s_b[1], s_b[2], s_b[3], flag_nxt);
+            atomicAdd(changed_count, 1);
+        }
     }
 }
 
@@ -419,6 +683,10 @@ struct fm_grid {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {};
     int grid_blocks = 0;                 // 1-D grid-stride kernels
+    int ntiles = 0;                      // 32 x 32 tiles of the tile-resident kernel
+    int32_t *d_tflag = nullptr;          // 2 x ntiles frontier flags
+    int k_local = 0;                     // tuning overrides (env FM_K_LOCAL / FM_BFS_INTERVAL)
+    int bfs_interval_env = 0;
     // solve state
     int32_t flags_solve = 0;
     long long sum_capS = 0;
@@ -447,8 +715,41 @@ float elapsed(fm_grid *g) {
     return ms;
 }
 
-dim3 tile_grid(const fm_grid *g) {
-    return dim3((g->W + TILE_W - 1) / TILE_W, (g->H + TILE_H - 1) / TILE_H);
+
+// Repeated frontier sweeps of a tile fixpoint kernel until a sweep changes nothing.
+// Launch i consumes flag buffer i&1 and fills the other; the per-launch count of
+// changed tiles lands in flags[i] (batches of 4 launches per host check).
+template <typename K>
+int frontier_sweeps(fm_grid *g, K kernel, int64_t *sweeps, int64_t *launches, double *ms_kern) {
+    int32_t *fa = g->d_tflag, *fb = g->d_tflag + g->ntiles;
+    FM_CHECK_CUDA(cudaMemsetAsync(fa, 0x01, sizeof(int32_t) * g->ntiles, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(fb, 0, sizeof(int32_t) * g->ntiles, g->stream));
+    const int batch = 4;
+    int i = 0;
+    for (;;) {
+        FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
+        cudaEventRecord(g->ev[2], g->stream);
+        for (int j = 0; j < batch; j++, i++) {
+            int32_t *cur = (i & 1) ? fb : fa, *nxt = (i & 1) ? fa : fb;
+            kernel<<<g->ntiles, dim3(TILE_W, BLK_Y), 0, g->stream>>>(g->d, cur, nxt, g->flags + j);
+        }
+        FM_CHECK_LAUNCH();
+        cudaEventRecord(g->ev[3], g->stream);
+        g->st.launches += batch;
+        *launches += batch;
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int32_t) * batch,
+                                      cudaMemcpyDeviceToHost, g->stream));
+        FM_TRY(sync_stream(g));
+        *ms_kern += elapsed_between(g->ev[2], g->ev[3]);
+        int idle_at = -1;
+        for (int j = 0; j < batch; j++) {
+            if (!g->h_flags[j]) { idle_at = j; break; }
+            g->st.reserved[0] += g->h_flags[j];   // tile visits that changed something
+        }
+        *sweeps += idle_at < 0 ? batch : idle_at + 1;
+        if (idle_at >= 0) break;
+    }
+    return FM_OK;
 }
 
 // global relabel + gap + marking; leaves the active-pixel count in g->active
@@ -457,26 +758,9 @@ int global_relabel(fm_grid *g) {
     bfs_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
     FM_CHECK_LAUNCH();
     g->st.launches++;
-    const dim3 tg = tile_grid(g);
-    const int batch = 4;
-    for (;;) {
-        FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
-        cudaEventRecord(g->ev[2], g->stream);
-        for (int i = 0; i < batch; i++) {
-            bfs_tile_kernel<<<tg, dim3(TILE_W, BLK_Y), 0, g->stream>>>(g->d, g->flags + i);
-        }
-        FM_CHECK_LAUNCH();
-        cudaEventRecord(g->ev[3], g->stream);
-        g->st.launches += batch;
-        g->st.bfs_launches += batch;
-        g->st.bfs_sweeps += batch;
-        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int32_t) * batch,
-                                      cudaMemcpyDeviceToHost, g->stream));
-        FM_TRY(sync_stream(g));
-        g->st.ms_bfs_kern += elapsed_between(g->ev[2], g->ev[3]);
-        if (g->h_flags[batch - 1] == 0) break;
-    }
+    FM_TRY(frontier_sweeps(g, bfs_tile_kernel, &g->st.bfs_sweeps, &g->st.bfs_launches, &g->st.ms_bfs_kern));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d.tile_active, 0, sizeof(int32_t) * g->ntiles, g->stream));
     bfs_finalize_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 4);
     FM_CHECK_LAUNCH();
     g->st.launches++;
@@ -495,6 +779,7 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
                  const int32_t *capU, const int32_t *capS, const int32_t *capT, int32_t flags) {
     g->flags_solve = flags;
     memset(&g->st, 0, sizeof(g->st));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d.tile_inflow, 0, sizeof(int32_t) * g->ntiles, g->stream));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 16, g->stream));
     grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
@@ -514,14 +799,15 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     return global_relabel(g);
 }
 
-// one coordinator round: lock-free sweeps until an idle sweep or the budget,
+// one coordinator round: lock-free launches until an idle launch or the budget,
 // then cancel (opt-in), global relabel, gap, mark (maxflow_par.py:195-229)
-int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
+constexpr int K_LOCAL_DEFAULT = 64;     // lock-free passes per tile visit
+constexpr int BFS_INTERVAL_DEFAULT = 8;  // tile launches between global relabels
+
+int run_round_global(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int32_t *done_out) {
     const int32_t cap = std::max(1, std::min(cycle_budget, bfs_interval > 0 ? bfs_interval : 64));
     const dim3 grid((g->W + TILE_W - 1) / TILE_W, (g->H + BLK_Y - 1) / BLK_Y);
     int32_t done = 0;
-    cudaEventRecord(g->ev[0], g->stream);
-    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
     while (done < cap) {
         const int batch = std::min(8, cap - done);
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
@@ -541,6 +827,56 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
         done += idle_at < 0 ? batch : idle_at + 1;
         if (idle_at >= 0) break;
     }
+    g->st.pr_sweeps += done;
+    g->st.pr_tiles += (int64_t)done * g->ntiles;
+    *done_out = done;
+    return FM_OK;
+}
+
+int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
+    const int k_local = std::max(1, std::min(cycle_budget, g->k_local > 0 ? g->k_local : K_LOCAL_DEFAULT));
+    if (bfs_interval <= 0 && g->bfs_interval_env > 0) bfs_interval = g->bfs_interval_env;
+    const int32_t cap = std::max(1, std::min((cycle_budget + k_local - 1) / k_local,
+                                             bfs_interval > 0 ? bfs_interval : BFS_INTERVAL_DEFAULT));
+    int32_t done = 0;
+    while (done < cap) {
+        const int batch = std::min(4, cap - done);
+        FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
+        cudaEventRecord(g->ev[2], g->stream);
+        for (int i = 0; i < batch; i++)
+            pr_tile_kernel<<<g->ntiles, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->flags + i, g->acc + 10);
+        FM_CHECK_LAUNCH();
+        cudaEventRecord(g->ev[3], g->stream);
+        g->st.launches += batch;
+        g->st.pr_launches += batch;
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int32_t) * batch,
+                                      cudaMemcpyDeviceToHost, g->stream));
+        FM_TRY(sync_stream(g));
+        g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
+        int idle_at = -1;
+        for (int i = 0; i < batch; i++) {
+            if (!g->h_flags[i]) { idle_at = i; break; }
+            g->st.pr_tiles += g->h_flags[i];
+        }
+        done += idle_at < 0 ? batch : idle_at + 1;
+        if (idle_at >= 0) break;
+    }
+    integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    g->st.pr_sweeps += done;
+    return FM_OK;
+}
+
+int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
+    cudaEventRecord(g->ev[0], g->stream);
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
+    int32_t sweeps = 0;
+    if (g->flags_solve & FM_GRID_GLOBAL_SWEEP) {
+        FM_TRY(run_round_global(g, cycle_budget, bfs_interval, &sweeps));
+    } else {
+        FM_TRY(run_round_tiles(g, cycle_budget, bfs_interval));
+    }
     if (g->flags_solve & FM_GRID_CANCEL_VIOLATIONS) {
         cancel_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 12);
         FM_CHECK_LAUNCH();
@@ -553,10 +889,7 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     g->st.ms_push += elapsed(g);
     g->st.pushes += (int64_t)g->h_acc[10];
     g->st.relabels += (int64_t)g->h_acc[11];
-    g->st.pr_sweeps += done;
-    g->st.bytes_push += (int64_t)done * 32 * g->HW + 16 * (int64_t)g->h_acc[10];
     FM_TRY(global_relabel(g));
-    g->st.bytes_bfs += 0;
     g->st.rounds++;
     return FM_OK;
 }
@@ -566,20 +899,10 @@ int compute_cut(fm_grid *g, uint8_t *cut_out_dev) {
     cut_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
     FM_CHECK_LAUNCH();
     g->st.launches++;
-    const dim3 tg = tile_grid(g);
-    const int batch = 4;
-    for (;;) {
-        FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
-        for (int i = 0; i < batch; i++)
-            cut_tile_kernel<<<tg, dim3(TILE_W, BLK_Y), 0, g->stream>>>(g->d, g->flags + i);
-        FM_CHECK_LAUNCH();
-        g->st.launches += batch;
-        g->st.cut_sweeps += batch;
-        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int32_t) * batch,
-                                      cudaMemcpyDeviceToHost, g->stream));
-        FM_TRY(sync_stream(g));
-        if (g->h_flags[batch - 1] == 0) break;
-    }
+    double cut_kern = 0.0;
+    int64_t cut_launches = 0;
+    FM_TRY(frontier_sweeps(g, cut_tile_kernel, &g->st.cut_sweeps, &cut_launches, &cut_kern));
+    g->st.launches += 0;
     if (cut_out_dev && cut_out_dev != g->d.cut)
         FM_CHECK_CUDA(cudaMemcpyAsync(cut_out_dev, g->d.cut, (size_t)g->HW, cudaMemcpyDeviceToDevice, g->stream));
     cudaEventRecord(g->ev[1], g->stream);
@@ -645,9 +968,14 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     FM_CHECK_CUDA(cudaSetDevice(device));
     fm_grid *g = new fm_grid();
     g->H = H; g->W = W; g->device = device; g->HW = (int64_t)H * W;
+    g->d.ntx = (W + PT_W - 1) / PT_W;
+    g->d.nty = (H + PT_H - 1) / PT_H;
+    g->ntiles = g->d.ntx * g->d.nty;
+    if (const char *v = getenv("FM_K_LOCAL")) g->k_local = atoi(v);
+    if (const char *v = getenv("FM_BFS_INTERVAL")) g->bfs_interval_env = atoi(v);
     const size_t n4 = sizeof(int32_t) * (size_t)g->HW, n1 = (size_t)g->HW;
     int32_t **planes[] = {&g->d.e, &g->d.h, &g->d.rR, &g->d.rL, &g->d.rD, &g->d.rU,
-                          &g->d.rT, &g->d.rS, &g->d.cS, &g->d.dist};
+                          &g->d.rT, &g->d.rS, &g->d.cS, &g->d.dist, &g->d.inflow_h, &g->d.inflow_v};
     for (auto pp : planes) {
         if (cudaMalloc((void **)pp, n4) != cudaSuccess) {
             fm_set_error("cudaMalloc of %zu bytes failed", n4);
@@ -659,6 +987,9 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         cudaMalloc((void **)&g->d.marked, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->d.cut, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
+        cudaMalloc((void **)&g->d.tile_active, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->d.tile_inflow, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->d_tflag, sizeof(int32_t) * 2 * (size_t)g->ntiles) != cudaSuccess ||
         cudaMalloc((void **)&g->flags, sizeof(int32_t) * 64) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_flags, sizeof(int32_t) * 64) != cudaSuccess ||
@@ -683,7 +1014,8 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (!g) return;
     cudaSetDevice(g->device);
     int32_t *planes[] = {g->d.e, g->d.h, g->d.rR, g->d.rL, g->d.rD, g->d.rU,
-                         g->d.rT, g->d.rS, g->d.cS, g->d.dist, g->in_caps};
+                         g->d.rT, g->d.rS, g->d.cS, g->d.dist, g->d.inflow_h, g->d.inflow_v,
+                         g->d.tile_active, g->d.tile_inflow, g->d_tflag, g->in_caps};
     for (auto p : planes) if (p) cudaFree(p);
     if (g->d.mask) cudaFree(g->d.mask);
     if (g->d.marked) cudaFree(g->d.marked);

@@ -51,8 +51,8 @@ class GridSolver:
         except Exception:
             pass
 
-    def _flags(self, cancel_violations=False, want_cut=True, precancel=True) -> int:
-        f = 0
+    def _flags(self, cancel_violations=False, want_cut=True, precancel=True, global_sweep=False) -> int:
+        f = _lib.FM_GRID_GLOBAL_SWEEP if global_sweep else 0
         if cancel_violations:
             f |= _lib.FM_GRID_CANCEL_VIOLATIONS
         if not want_cut:
@@ -62,7 +62,7 @@ class GridSolver:
         return f
 
     def solve_host(self, caps, cycle_budget=DEFAULT_CYCLE_BUDGET, bfs_interval=DEFAULT_BFS_INTERVAL,
-                   want_cut=True, cancel_violations=False, precancel=True):
+                   want_cut=True, cancel_violations=False, precancel=True, global_sweep=False):
         """Host int32 planes in, (flow, cut uint8[H,W] or None, stats) out; the
         host<->device copies are part of the call."""
         caps = [np.ascontiguousarray(a, dtype=np.int32) for a in caps]
@@ -71,14 +71,15 @@ class GridSolver:
         st = _lib.FmStats()
         rc = _lib.load().fm_grid_solve_host(
             self._h, *[_lib.ptr(a) for a in caps], int(cycle_budget), int(bfs_interval),
-            self._flags(cancel_violations, want_cut, precancel), ctypes.byref(flow),
+            self._flags(cancel_violations, want_cut, precancel, global_sweep), ctypes.byref(flow),
             _lib.ptr(cut) if want_cut else None, ctypes.byref(st))
         _lib.check(rc, "fm_grid_solve_host")
         self.last_stats = st.as_dict()
         return int(flow.value), cut, self.last_stats
 
     def solve_device(self, caps, cycle_budget=DEFAULT_CYCLE_BUDGET, bfs_interval=DEFAULT_BFS_INTERVAL,
-                     cut_out=None, cancel_violations=False, precancel=True, stream=None):
+                     cut_out=None, cancel_violations=False, precancel=True, stream=None,
+                     global_sweep=False):
         """Device int32 tensors in (borrowed); cut_out = uint8 CUDA tensor or None.
         Runs on `stream` (a torch.cuda.Stream or raw handle; default: the
         library's own stream)."""
@@ -89,7 +90,7 @@ class GridSolver:
             s = int(getattr(stream, "cuda_stream", stream))
         rc = _lib.load().fm_grid_solve(
             self._h, *[_lib.ptr(a) for a in caps], int(cycle_budget), int(bfs_interval),
-            self._flags(cancel_violations, cut_out is not None, precancel), ctypes.byref(flow),
+            self._flags(cancel_violations, cut_out is not None, precancel, global_sweep), ctypes.byref(flow),
             _lib.ptr(cut_out) if cut_out is not None else None, ctypes.byref(st), s)
         _lib.check(rc, "fm_grid_solve")
         self.last_stats = st.as_dict()
