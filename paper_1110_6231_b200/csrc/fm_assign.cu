@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <string.h>
+#include <stdlib.h>
 
 #include "fm_common.cuh"
 
@@ -365,12 +366,24 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             __syncthreads();
             tail_ops += pushes + relabels - p0;
         } else {
-            for (int i = gwarp; i < ny; i += gwarps)
-                y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+            // a list no longer than the grid gets one CTA per node (one L2 round trip
+            // per row scan); longer lists get one warp per node
+            if (ny <= (int)gridDim.x) {
+                for (int i = blockIdx.x; i < ny; i += gridDim.x)
+                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+            } else {
+                for (int i = gwarp; i < ny; i += gwarps)
+                    y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+            }
             grid.sync();
             const int nx = __ldcg(a.cnt + C_X0 + b);
-            for (int i = gwarp; i < nx; i += gwarps)
-                x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+            if (nx <= (int)gridDim.x) {
+                for (int i = blockIdx.x; i < nx; i += gridDim.x)
+                    x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+            } else {
+                for (int i = gwarp; i < nx; i += gwarps)
+                    x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+            }
             grid.sync();
         }
     }
@@ -387,71 +400,101 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
     (void)cwarp;
 }
 
+// floor(rc / eps) for eps >= 1 via a double quotient corrected by one step
+// (|rc| < 2^52 here), avoiding a 64-bit integer division per arc
+__device__ __forceinline__ long long floordiv_eps(long long rc, long long eps, double inv_eps) {
+    if (eps == 1) return rc;
+    long long q = (long long)floor((double)rc * inv_eps);
+    const long long r = rc - q * eps;
+    if (r < 0) q--; else if (r >= eps) q++;
+    return q;
+}
+
 // price_update_heuristic (assign_scaling.py:208-276) at a quiescent point of the
 // refine: label every node with its distance to the deficit set over residual
 // arcs, arc length floor(c_p / eps) + 1 (>= 0), in eps units; then lower each
 // price by eps * min(label, last + 1), last = the largest label of an active node.
-// The reference scans Dial buckets; here the same labels come from a Bellman-Ford
-// fixpoint over the dense matrix (X step: warp per row; Y step: one thread per
-// matched X, atomicMin into its Y), one grid barrier per half-step.
-__global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a) {
+// The reference scans Dial buckets; here the same labels come from a frontier
+// Bellman-Ford: X step = one CTA per Y whose label dropped, relaxing every arc x->y
+// along row y of the transposed weights (coalesced) with atomicMin on l(x); Y step
+// = one thread per X whose label dropped, relaxing its matched reverse arc.
+struct PuDev {
+    const int32_t *wt;      // transposed weights: wt[y*n + x] = w(x, y)
+    int32_t *fy[2], *fx[2]; // frontiers
+    int32_t *in_fx, *in_fy; // frontier membership flags
+    int32_t *cnt;           // [0..1] |fy|, [2..3] |fx|
+};
+
+__global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuDev f) {
     cg::grid_group grid = cg::this_grid();
     const int n = a.n;
     const int tid = blockIdx.x * ATHREADS + threadIdx.x, nthr = gridDim.x * ATHREADS;
     const int lane = threadIdx.x & 31;
-    const int gwarp = tid >> 5, gwarps = nthr >> 5;
+    const double inv_eps = 1.0 / (double)a.eps;
+    if (tid == 0) a.cnt[C_PU_LAST] = 0;  // read by every thread after the last barrier
     for (int v = tid; v < n; v += nthr) {
-        a.ly[v] = __ldcg(a.ey + v) < 0 ? 0 : LINF;
         a.lx[v] = LINF;
+        f.in_fx[v] = 0;
+        if (__ldcg(a.ey + v) < 0) {
+            a.ly[v] = 0;
+            f.in_fy[v] = 1;
+            f.fy[0][atomicAdd(f.cnt + 0, 1)] = v;
+        } else {
+            a.ly[v] = LINF;
+            f.in_fy[v] = 0;
+        }
     }
-    if (tid == 0) { a.cnt[C_PU_CHG] = 0; a.cnt[C_PU_CHG + 1] = 0; a.cnt[C_PU_LAST] = 0; }
     grid.sync();
     int it = 0;
     for (;; it++) {
-        int32_t *chg = a.cnt + C_PU_CHG + (it & 1);
-        bool changed = false;
-        // X step: l(x) = min over residual x->y of l(y) + floor(c_p(x,y)/eps) + 1
-        for (int x = gwarp; x < n; x += gwarps) {
-            const int32_t *row = a.w + (size_t)x * n;
-            const uint32_t *frow = a.fixed + (size_t)x * a.nw;
-            const int mx = __ldcg(a.match + x);
-            const long long px = __ldcg((const long long *)a.px + x);
-            int best = LINF;
-            for (int y = lane; y < n; y += 32) {
-                const int ly = __ldcg(a.ly + y);
-                if (ly >= LINF || y == mx) continue;
-                const int wv = __ldg(row + y);
+        const int b = it & 1, nb = b ^ 1;
+        const int ny = __ldcg(f.cnt + b);
+        if (ny == 0) break;
+        if (tid == 0) { f.cnt[nb] = 0; f.cnt[2 + nb] = 0; }
+        // X step: for y in the frontier, l(x) <- min(l(x), l(y) + len(x -> y))
+        for (int i = blockIdx.x; i < ny; i += gridDim.x) {
+            const int y = __ldcg(f.fy[b] + i);
+            if (threadIdx.x == 0) f.in_fy[y] = 0;
+            const int lyv = __ldcg(a.ly + y);
+            const long long pyv = __ldcg((const long long *)a.py + y);
+            const int32_t *col = f.wt + (size_t)y * n;
+            for (int x = threadIdx.x; x < n; x += ATHREADS) {
+                const int wv = __ldg(col + x);
                 if (wv == FM_ABSENT_WEIGHT) continue;
-                if (a.use_fix && ((__ldg(frow + (y >> 5)) >> (y & 31)) & 1u)) continue;
-                const long long rc = -(long long)wv * a.scale + px - __ldcg((const long long *)a.py + y);
-                long long len = floordiv(rc, a.eps) + 1;
+                const int lxv = __ldcg(a.lx + x);
+                if (lyv >= lxv) continue;                              // cannot improve (len >= 0)
+                if (__ldcg(a.match + x) == y) continue;               // flow arc: not residual forward
+                if (a.use_fix && ((__ldg(a.fixed + (size_t)x * a.nw + (y >> 5)) >> (y & 31)) & 1u)) continue;
+                const long long rc = -(long long)wv * a.scale + __ldcg((const long long *)a.px + x) - pyv;
+                long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
                 if (len < 0) len = 0;
-                const long long cand = (long long)ly + len;
-                if (cand <= a.max_bucket && cand < best) best = (int)cand;
+                const long long cand = (long long)lyv + len;
+                if (cand > a.max_bucket || cand >= lxv) continue;
+                const int old = atomicMin(a.lx + x, (int)cand);
+                if ((int)cand < old && atomicExch(f.in_fx + x, 1) == 0)
+                    f.fx[b][atomicAdd(f.cnt + 2 + b, 1)] = x;
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-            if (lane == 0 && best < __ldcg(a.lx + x)) { a.lx[x] = best; changed = true; }
         }
         grid.sync();
-        // Y step: l(y) = min over x matched to y (non-frozen) of l(x) + floor(c_p(y->x)/eps) + 1
-        for (int x = tid; x < n; x += nthr) {
+        // Y step: for x in the frontier with a (non-frozen) unit on x -> y,
+        // l(y) <- min(l(y), l(x) + len(y -> x))
+        const int nx = __ldcg(f.cnt + 2 + b);
+        for (int i = tid; i < nx; i += nthr) {
+            const int x = __ldcg(f.fx[b] + i);
+            f.in_fx[x] = 0;
             const int y = __ldcg(a.match + x);
-            const int lxv = __ldcg(a.lx + x);
-            if (y < 0 || lxv >= LINF || __ldcg(a.frozen + x)) continue;
+            if (y < 0 || __ldcg(a.frozen + x)) continue;
             const long long rc = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale -
                                  __ldcg((const long long *)a.px + x) + __ldcg((const long long *)a.py + y);
-            long long len = floordiv(rc, a.eps) + 1;
+            long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
             if (len < 0) len = 0;
-            const long long cand = (long long)lxv + len;
+            const long long cand = (long long)__ldcg(a.lx + x) + len;
             if (cand > a.max_bucket) continue;
             const int old = atomicMin(a.ly + y, (int)cand);
-            if ((int)cand < old) changed = true;
+            if ((int)cand < old && atomicExch(f.in_fy + y, 1) == 0)
+                f.fy[nb][atomicAdd(f.cnt + nb, 1)] = y;
         }
-        if (tid == 0) a.cnt[C_PU_CHG + ((it + 1) & 1)] = 0;
-        if (__syncthreads_or(changed) && threadIdx.x == 0) atomicExch(chg, 1);
         grid.sync();
-        if (__ldcg(chg) == 0) break;
     }
     // last = max label over active nodes (unmatched X, Y with positive excess)
     int last = 0;
@@ -470,8 +513,24 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a) {
     }
     if (tid == 0) {
         a.cnt[C_RELABELS] = 0;
+        f.cnt[0] = f.cnt[1] = f.cnt[2] = f.cnt[3] = 0;
         atomicAdd(a.ops + O_PU, 1ull);
         atomicAdd(a.ops + O_PU_ITERS, (unsigned long long)(it + 1));
+    }
+}
+
+// wt = w^T (32 x 32 shared-memory tiles)
+__global__ void transpose_kernel(const int32_t *w, int32_t *wt, int n) {
+    __shared__ int32_t t[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int r = by + j, c = bx + threadIdx.x;
+        if (r < n && c < n) t[j][threadIdx.x] = w[(size_t)r * n + c];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int r = bx + j, c = by + threadIdx.x;
+        if (r < n && c < n) wt[(size_t)r * n + c] = t[threadIdx.x][j];
     }
 }
 
@@ -556,7 +615,11 @@ struct fm_assign {
     int32_t *h_cnt = nullptr;
     unsigned long long *h_acc = nullptr;
     cudaStream_t own_stream = nullptr, stream = nullptr;
-    int coop_blocks = 0, sms = 0;
+    int coop_blocks = 0, pu_blocks = 0, sms = 0;
+    PuDev pu{};
+    int32_t *wt = nullptr;
+    cudaEvent_t ev[2] = {};
+    bool pu_pending = false;
     fm_stats st{};
 };
 
@@ -583,6 +646,13 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
     FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * 8, s));
     FM_CHECK_CUDA(cudaMemsetAsync(A->acc, 0, sizeof(unsigned long long) * 4, s));
     weight_bound_kernel<<<A->sms * 4, 256, 0, s>>>(w, (int64_t)n * n, A->acc);
+    if (flags & FM_ASSIGN_PRICE_UPDATE) {
+        A->pu.wt = A->wt;
+        transpose_kernel<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, s>>>(w, A->wt, n);
+        FM_CHECK_LAUNCH();
+        FM_CHECK_CUDA(cudaMemsetAsync(A->pu.cnt, 0, sizeof(int32_t) * 4, s));
+        A->st.launches++;
+    }
     FM_CHECK_LAUNCH();
     A->st.launches++;
     FM_CHECK_CUDA(cudaMemcpyAsync(A->h_acc, A->acc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
@@ -592,13 +662,16 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
     const double budget_d = std::max(1e4, 40.0 * n * (double)n * std::max<double>(1.0, (double)A->h_acc[2]));
     const long long round_budget = budget_d > 4e18 ? (long long)4e18 : (long long)budget_d;
     long long eps = std::max(1LL, bound);
-    const int tail_threshold = 4;
-    const int pu_threshold = (flags & FM_ASSIGN_PRICE_UPDATE) ? std::max(64, n / 4) : 0;
+    const int tail_threshold = 1;
+    int pu_threshold = (flags & FM_ASSIGN_PRICE_UPDATE) ? std::max(64, n / 16) : 0;
+    if (const char *v = getenv("FM_PU_THRESHOLD")) if (pu_threshold) pu_threshold = atoi(v);
+    int tail_threshold_env = tail_threshold;
+    if (const char *v = getenv("FM_TAIL_THRESHOLD")) tail_threshold_env = atoi(v);
     int rc = FM_OK;
     for (;;) {
         eps = std::max(1LL, (eps + alpha - 1) / alpha);   // -(-eps // alpha)
         d.eps = eps;
-        d.max_bucket = bound / eps + 2;
+        d.max_bucket = std::min<long long>(bound / eps + 2, LINF - 1);
         FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * C_COUNT, s));
         reset_excess_kernel<<<(n + 255) / 256, 256, 0, s>>>(d);
         FM_CHECK_LAUNCH();
@@ -606,17 +679,26 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
         FM_CHECK_LAUNCH();
         A->st.launches += 2;
         for (;;) {
-            void *args[] = {(void *)&d, (void *)&tail_threshold, (void *)&round_budget, (void *)&pu_threshold};
+            void *args[] = {(void *)&d, (void *)&tail_threshold_env, (void *)&round_budget, (void *)&pu_threshold};
             FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
                                                       dim3(ATHREADS), args, 0, s));
             A->st.launches++;
             FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, d.cnt, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, s));
             FM_CHECK_CUDA(cudaStreamSynchronize(s));
+            if (A->pu_pending) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, A->ev[0], A->ev[1]);
+                A->st.ms_bfs += ms;   // price-update kernels
+                A->pu_pending = false;
+            }
             if (A->h_cnt[C_INFEASIBLE] || A->h_cnt[C_EXIT] != 1) break;
-            void *pargs[] = {(void *)&d};
-            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->coop_blocks),
+            void *pargs[] = {(void *)&d, (void *)&A->pu};
+            cudaEventRecord(A->ev[0], s);
+            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->pu_blocks),
                                                       dim3(ATHREADS), pargs, 0, s));
+            cudaEventRecord(A->ev[1], s);
             A->st.launches++;
+            A->pu_pending = true;
         }
         if (d.use_fix) {
             arc_fix_kernel<<<std::max(1, std::min((n + 7) / 8, A->sms * 8)), 256, 0, s>>>(d);
@@ -654,7 +736,7 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
     A->st.ms_total = ms;
-    A->st.ms_push = ms;
+    A->st.ms_push = ms - A->st.ms_bfs;  // everything but the price updates
     A->st.pushes = (int64_t)A->h_ops[0];
     A->st.relabels = (int64_t)A->h_ops[1];
     A->st.rounds = (int64_t)A->h_ops[2];
@@ -699,6 +781,14 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMalloc((void **)&d.ylist[1], sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.cnt, sizeof(int32_t) * C_COUNT) == cudaSuccess &&
               cudaMalloc((void **)&d.lx, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&A->wt, sizeof(int32_t) * (size_t)n * n) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.fy[0], sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.fy[1], sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.fx[0], sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.fx[1], sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.in_fx, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.in_fy, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.cnt, sizeof(int32_t) * 4) == cudaSuccess &&
               cudaMalloc((void **)&d.ly, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * 8) == cudaSuccess &&
               cudaMalloc((void **)&A->acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
@@ -712,12 +802,15 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
         return FM_CUDA_ERROR;
     }
     A->stream = A->own_stream;
+    cudaEventCreate(&A->ev[0]);
+    cudaEventCreate(&A->ev[1]);
     cudaDeviceGetAttribute(&A->sms, cudaDevAttrMultiProcessorCount, device);
     int per_sm = 0;
     int per_sm2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_rounds_kernel, ATHREADS, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, price_update_kernel, ATHREADS, 0);
-    A->coop_blocks = std::max(1, std::min(std::min(per_sm, per_sm2), 2) * A->sms);
+    A->coop_blocks = std::max(1, std::min(per_sm, 2) * A->sms);
+    A->pu_blocks = std::max(1, std::min(per_sm2, 2) * A->sms);
     *out = A;
     return FM_OK;
 }
@@ -727,13 +820,15 @@ extern "C" void fm_assign_destroy(fm_assign *A) {
     cudaSetDevice(A->device);
     void *dev[] = {A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.frozen, A->d.frozen_in,
                    A->d.xlist[0], A->d.xlist[1], A->d.ylist[0], A->d.ylist[1], A->d.cnt, A->d.ops,
-                   A->d.lx, A->d.ly,
+                   A->d.lx, A->d.ly, A->wt, A->pu.fy[0], A->pu.fy[1], A->pu.fx[0], A->pu.fx[1],
+                   A->pu.in_fx, A->pu.in_fy, A->pu.cnt,
                    A->acc, A->in_w};
     for (void *p : dev) if (p) cudaFree(p);
     if (A->h_ops) cudaFreeHost(A->h_ops);
     if (A->h_acc) cudaFreeHost(A->h_acc);
     if (A->h_cnt) cudaFreeHost(A->h_cnt);
     if (A->own_stream) cudaStreamDestroy(A->own_stream);
+    for (auto e : A->ev) if (e) cudaEventDestroy(e);
     delete A;
 }
 

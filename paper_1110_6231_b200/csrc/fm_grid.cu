@@ -686,6 +686,7 @@ struct fm_grid {
     int ntiles = 0;                      // 32 x 32 tiles of the tile-resident kernel
     int32_t *d_tflag = nullptr;          // 2 x ntiles frontier flags
     int k_local = 0;                     // tuning overrides (env FM_K_LOCAL / FM_BFS_INTERVAL)
+    int trace = 0;                       // env FM_TRACE=1: one stderr line per round
     int bfs_interval_env = 0;
     // solve state
     int32_t flags_solve = 0;
@@ -869,6 +870,8 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
 }
 
 int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
+    const fm_stats before = g->st;
+    const long long active_before = g->active;
     cudaEventRecord(g->ev[0], g->stream);
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
     int32_t sweeps = 0;
@@ -891,6 +894,13 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     g->st.relabels += (int64_t)g->h_acc[11];
     FM_TRY(global_relabel(g));
     g->st.rounds++;
+    if (g->trace)
+        fprintf(stderr, "[fm_grid] round %lld active %lld -> %lld | launches %lld tiles %lld pushes %lld relabels %lld "
+                "push %.3f ms | bfs sweeps %lld %.3f ms levels %lld\n", (long long)g->st.rounds, active_before, g->active,
+                (long long)(g->st.pr_sweeps - before.pr_sweeps), (long long)(g->st.pr_tiles - before.pr_tiles),
+                (long long)(g->st.pushes - before.pushes), (long long)(g->st.relabels - before.relabels),
+                g->st.ms_push - before.ms_push, (long long)(g->st.bfs_sweeps - before.bfs_sweeps),
+                g->st.ms_bfs - before.ms_bfs, (long long)g->st.bfs_levels);
     return FM_OK;
 }
 
@@ -973,6 +983,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->ntiles = g->d.ntx * g->d.nty;
     if (const char *v = getenv("FM_K_LOCAL")) g->k_local = atoi(v);
     if (const char *v = getenv("FM_BFS_INTERVAL")) g->bfs_interval_env = atoi(v);
+    if (const char *v = getenv("FM_TRACE")) g->trace = atoi(v);
     const size_t n4 = sizeof(int32_t) * (size_t)g->HW, n1 = (size_t)g->HW;
     int32_t **planes[] = {&g->d.e, &g->d.h, &g->d.rR, &g->d.rL, &g->d.rD, &g->d.rU,
                           &g->d.rT, &g->d.rS, &g->d.cS, &g->d.dist, &g->d.inflow_h, &g->d.inflow_v};
