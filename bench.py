@@ -221,20 +221,24 @@ def main():
     K = args.steps
     pr_ms, bfs_ms = agg.get("ms_pr_kern", 0.0), agg.get("ms_bfs_kern", 0.0)
     if pr_ms >= bfs_ms:
+        # pr_tile_kernel: every visited 32x32 tile loads e, h, rR, rL, rD, rU, rT, rS
+        # (32 B/px) + a 128-px halo of heights, and stores 7 planes (28 B/px)
         launches = max(1, agg.get("pr_launches", 1))
-        bytes_per_launch = (32 * HW * agg.get("pr_sweeps", 0) + 16 * agg.get("pushes", 0)) / launches
+        bytes_per_launch = agg.get("pr_tiles", 0) * (1024 * (32 + 28) + 128 * 4) / launches
         dur = pr_ms / launches
-        kname = "pr_sweep_kernel"
+        kname = "pr_tile_kernel"
     else:
+        # bfs_tile_kernel: dist (4 B) + mask (1 B) per pixel of a visited tile + halo,
+        # changed distances written back (<= 4 B/px)
         launches = max(1, agg.get("bfs_launches", 1))
-        bytes_per_launch = 9 * HW
+        bytes_per_launch = 9 * HW * agg.get("bfs_sweeps", 0) / max(1, agg.get("bfs_launches", 1))
         dur = bfs_ms / launches
         kname = "bfs_tile_kernel"
     achieved = bytes_per_launch / (dur / 1000.0) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "kernel": kname,
                 "peak_source": peak_src, "bytes_per_launch": int(bytes_per_launch),
-                "launch_ms": round(dur, 5), "kernel_share_of_step": round((pr_ms if kname == 'pr_sweep_kernel' else bfs_ms) / max(1e-9, ms_total), 3)}
+                "launch_ms": round(dur, 5), "kernel_share_of_step": round((pr_ms if kname == 'pr_tile_kernel' else bfs_ms) / max(1e-9, ms_total), 3)}
 
     # end to end through the public API with pinned host buffers
     e2e = None
@@ -294,7 +298,7 @@ def main():
         if not args.no_cpu_baseline and ws == 1:
             cpu = cpu_baseline_grid(os.cpu_count() or 1)
         per = {k: round(v / K, 3) if isinstance(v, float) else v // K for k, v in agg.items()
-               if k in ("pushes", "relabels", "rounds", "launches", "pr_sweeps", "bfs_sweeps", "bfs_levels",
+               if k in ("pushes", "relabels", "rounds", "launches", "pr_sweeps", "pr_tiles", "bfs_sweeps", "bfs_levels",
                         "cut_sweeps", "ms_total", "ms_push", "ms_bfs", "ms_cut", "ms_pr_kern", "ms_bfs_kern")}
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,

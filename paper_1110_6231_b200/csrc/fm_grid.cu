@@ -7,6 +7,7 @@
 // (maxflow_seq.py:119-160, maxflow_par.py:220-226), and the minimal source-side
 // cut by a seeded residual reach.  See DESIGN.md.
 #include <algorithm>
+#include <climits>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -24,6 +25,30 @@ constexpr int NWARPS = TILE_W * BLK_Y / 32;
 // residual mask bits
 constexpr uint8_t M_R = 1, M_L = 2, M_D = 4, M_U = 8, M_T = 16;
 
+// Work list of tiles for persistent CTAs, double-buffered by launch parity p:
+// launch p drains list[p] (clearing each tile's flag as it is taken) and fills
+// list[p^1] (the flag dedups).  cnt = {count0, work1, count1, work0} so the two
+// words a launch of parity p needs zeroed (count[p^1], work[p]) are adjacent.
+struct TileQueue {
+    int32_t *list[2];
+    int32_t *flag[2];
+    int32_t *cnt;
+};
+
+__device__ __forceinline__ void tq_push(const TileQueue &q, int parity, int tile) {
+    if (atomicExch(q.flag[parity] + tile, 1) == 0) q.list[parity][atomicAdd(q.cnt + 2 * parity, 1)] = tile;
+}
+
+// next tile of launch parity p for this CTA (thread 0 calls; -1 when drained)
+__device__ __forceinline__ int tq_take(const TileQueue &q, int parity, int all_tiles, int ntiles) {
+    const int i = atomicAdd(q.cnt + (parity ? 1 : 3), 1);
+    if (all_tiles) return i < ntiles ? i : -1;
+    if (i >= __ldcg(q.cnt + 2 * parity)) return -1;
+    const int t = __ldcg(q.list[parity] + i);
+    q.flag[parity][t] = 0;
+    return t;
+}
+
 struct GridDev {
     int32_t *e, *h, *rR, *rL, *rD, *rU, *rT, *rS, *cS;
     int32_t *dist;
@@ -32,9 +57,9 @@ struct GridDev {
     // an inbox of the receiving pixel (inflow_h: across a vertical tile border,
     // inflow_v: across a horizontal one) until the receiving tile next loads
     int32_t *inflow_h, *inflow_v;
-    int32_t *tile_active;   // tile had an active pixel when it was last written back
-    int32_t *tile_inflow;   // someone parked flow in this tile's inboxes
     int32_t ntx, nty;       // tiles per row / column
+    TileQueue pq;           // push-relabel work list
+    TileQueue bq;           // BFS / cut frontier work list
     int32_t H, W;
     int32_t V;      // node count |V| = H*W + 2 (the source's height)
     int32_t INF;    // "unreached" distance sentinel (== V)
@@ -186,25 +211,24 @@ __global__ void __launch_bounds__(256) pr_sweep_kernel(GridDev g, int32_t *activ
 constexpr int PT_W = 32, PT_H = 32, PT_TY = 16;          // 512 threads, 2 rows each
 constexpr int PT_ROWS = PT_H / PT_TY;
 
-__global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_local,
+__global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_local, int parity,
                                                                int32_t *processed,
                                                                unsigned long long *ops) {
     __shared__ int32_t s_e[PT_H][PT_W];
     __shared__ int32_t s_h[PT_H + 2][PT_W + 2];
     __shared__ int32_t s_r[4][PT_H][PT_W];   // R, L, D, U
     __shared__ int32_t s_t[PT_H][PT_W];
-    __shared__ int s_go;
-    const int tile = blockIdx.x;
+    __shared__ int s_tile;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    long long pushes = 0, relabels = 0;
+    for (;;) {
+    __syncthreads();
+    if (tx == 0 && ty == 0) s_tile = tq_take(g.pq, parity, 0, 0);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile < 0) break;
     const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
     const int r0 = tyi * PT_H, c0 = txi * PT_W;
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    if (tx == 0 && ty == 0) {
-        int go = g.tile_active[tile];
-        if (atomicExch(g.tile_inflow + tile, 0)) go = 1;
-        s_go = go;
-    }
-    __syncthreads();
-    if (!s_go) return;
     __threadfence();
     const int V = g.V;
     const int c = c0 + tx;
@@ -253,7 +277,6 @@ __global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_
     volatile int32_t *vh = &s_h[0][0];
     volatile int32_t *vt = &s_t[0][0];
     constexpr int HS = PT_W + 2;  // s_h row stride
-    long long pushes = 0, relabels = 0;
     for (int it = 0; it < k_local; it++) {
         bool any = false;
 #pragma unroll
@@ -304,7 +327,7 @@ __global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_
                     __threadfence();
                     const int nt = (dir == 0) ? tile + 1 : (dir == 1) ? tile - 1
                                  : (dir == 2) ? tile + g.ntx : tile - g.ntx;
-                    g.tile_inflow[nt] = 1;
+                    tq_push(g.pq, parity ^ 1, nt);
                 }
                 pushes++;
             } else {
@@ -333,9 +356,10 @@ __global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_
     }
     const int any_act = __syncthreads_or(act);
     if (tx == 0 && ty == 0) {
-        g.tile_active[tile] = any_act;
+        if (any_act) tq_push(g.pq, parity ^ 1, tile);
         atomicAdd(processed, 1);
     }
+    }  // tile loop
     block_add_i64<PT_W * PT_TY / 32>(pushes, ops + 0);
     block_add_i64<PT_W * PT_TY / 32>(relabels, ops + 1);
 }
@@ -359,7 +383,6 @@ __global__ void integrate_inflow_kernel(GridDev g) {
     if (side == 1 && r + 1 < g.H) { const int32_t d = g.inflow_v[p]; if (d) { g.inflow_v[p] = 0; atomicAdd(g.e + p, d); g.rD[p] += d; } }
     if (side == 2 && c > 0) { const int32_t d = g.inflow_h[p]; if (d) { g.inflow_h[p] = 0; atomicAdd(g.e + p, d); g.rL[p] += d; } }
     if (side == 3 && c + 1 < g.W) { const int32_t d = g.inflow_h[p]; if (d) { g.inflow_h[p] = 0; atomicAdd(g.e + p, d); g.rR[p] += d; } }
-    if (i == 0) g.tile_inflow[tile] = 0;
 }
 
 // ----------------------------------------------------------------------------
@@ -429,29 +452,30 @@ __global__ void bfs_init_kernel(GridDev g) {
 // neighbour tiles across every border that changed.  Converged when a sweep
 // changes nothing.
 __device__ __forceinline__ void flag_changed_borders(const GridDev &g, int tile, int tyi, int txi,
-                                                     int bt, int bb, int bl, int br, int32_t *flag_nxt) {
-    if (bt && tyi > 0) flag_nxt[tile - g.ntx] = 1;
-    if (bb && tyi + 1 < g.nty) flag_nxt[tile + g.ntx] = 1;
-    if (bl && txi > 0) flag_nxt[tile - 1] = 1;
-    if (br && txi + 1 < g.ntx) flag_nxt[tile + 1] = 1;
+                                                     int bt, int bb, int bl, int br, int parity) {
+    if (bt && tyi > 0) tq_push(g.bq, parity, tile - g.ntx);
+    if (bb && tyi + 1 < g.nty) tq_push(g.bq, parity, tile + g.ntx);
+    if (bl && txi > 0) tq_push(g.bq, parity, tile - 1);
+    if (br && txi + 1 < g.ntx) tq_push(g.bq, parity, tile + 1);
 }
 
-__global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int32_t *flag_cur, int32_t *flag_nxt,
+__global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int parity, int all_tiles,
                                                        int32_t *changed_count) {
     __shared__ int32_t sd[TILE_H + 2][TILE_W + 2];
-    __shared__ int s_go, s_b[4];
-    const int tile = blockIdx.x;
-    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
-    const int c0 = txi * TILE_W, r0 = tyi * TILE_H;
+    __shared__ int s_tile, s_b[4];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * TILE_W + tx;
+    for (;;) {
+    __syncthreads();
     if (tid == 0) {
-        s_go = flag_cur[tile];
-        if (s_go) flag_cur[tile] = 0;
+        s_tile = tq_take(g.bq, parity, all_tiles, g.ntx * g.nty);
         s_b[0] = s_b[1] = s_b[2] = s_b[3] = 0;
     }
     __syncthreads();
-    if (!s_go) return;
+    const int tile = s_tile;
+    if (tile < 0) break;
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int c0 = txi * TILE_W, r0 = tyi * TILE_H;
     for (int i = tid; i < (TILE_H + 2) * (TILE_W + 2); i += TILE_W * BLK_Y) {
         const int lr = i / (TILE_W + 2), lc = i % (TILE_W + 2);
         const int r = r0 + lr - 1, c = c0 + lc - 1;
@@ -503,10 +527,11 @@ __global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int32_t *flag_
         }
         __syncthreads();
         if (tid == 0) {
-            flag_changed_borders(g, tile, tyi, txi, s_b[0], s_b[1], s_b[2], s_b[3], flag_nxt);
+            flag_changed_borders(g, tile, tyi, txi, s_b[0], s_b[1], s_b[2], s_b[3], parity ^ 1);
             atomicAdd(changed_count, 1);
         }
     }
+    }  // tile loop
 }
 
 // gap_relabel (maxflow_seq.py:149-160) + marking (maxflow_par.py:223-226):
@@ -526,7 +551,8 @@ __global__ void bfs_finalize_kernel(GridDev g, unsigned long long *acc /* [0] ac
             lvl = max(lvl, d);
             if (e > 0) {
                 const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
-                g.tile_active[(r / PT_H) * g.ntx + c / PT_W] = 1;
+                const int t = (r / PT_H) * g.ntx + c / PT_W;
+                if (!__ldcg(g.pq.flag[0] + t)) tq_push(g.pq, 0, t);
             }
         } else {
             if (g.h[p] < g.V) g.h[p] = g.V;
@@ -573,22 +599,23 @@ __global__ void cut_init_kernel(GridDev g) {
     }
 }
 
-__global__ void __launch_bounds__(256) cut_tile_kernel(GridDev g, int32_t *flag_cur, int32_t *flag_nxt,
+__global__ void __launch_bounds__(256) cut_tile_kernel(GridDev g, int parity, int all_tiles,
                                                        int32_t *changed_count) {
     __shared__ uint8_t ss[TILE_H + 2][TILE_W + 2];
-    __shared__ int s_go, s_b[4];
-    const int tile = blockIdx.x;
-    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
-    const int c0 = txi * TILE_W, r0 = tyi * TILE_H;
+    __shared__ int s_tile, s_b[4];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * TILE_W + tx;
+    for (;;) {
+    __syncthreads();
     if (tid == 0) {
-        s_go = flag_cur[tile];
-        if (s_go) flag_cur[tile] = 0;
+        s_tile = tq_take(g.bq, parity, all_tiles, g.ntx * g.nty);
         s_b[0] = s_b[1] = s_b[2] = s_b[3] = 0;
     }
     __syncthreads();
-    if (!s_go) return;
+    const int tile = s_tile;
+    if (tile < 0) break;
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int c0 = txi * TILE_W, r0 = tyi * TILE_H;
     for (int i = tid; i < (TILE_H + 2) * (TILE_W + 2); i += TILE_W * BLK_Y) {
         const int lr = i / (TILE_W + 2), lc = i % (TILE_W + 2);
         const int r = r0 + lr - 1, c = c0 + lc - 1;
@@ -636,10 +663,11 @@ __global__ void __launch_bounds__(256) cut_tile_kernel(GridDev g, int32_t *flag_
         }
         __syncthreads();
         if (tid == 0) {
-            flag_changed_borders(g, tile, tyi, txi, s_b[0], s_b[1], s_b[2], s_b[3], flag_nxt);
+            flag_changed_borders(g, tile, tyi, txi, s_b[0], s_b[1], s_b[2], s_b[3], parity ^ 1);
             atomicAdd(changed_count, 1);
         }
     }
+    }  // tile loop
 }
 
 // sum of e over all pixels (flow = sum capS - sum e: node conservation)
@@ -684,7 +712,9 @@ struct fm_grid {
     cudaEvent_t ev[4] = {};
     int grid_blocks = 0;                 // 1-D grid-stride kernels
     int ntiles = 0;                      // 32 x 32 tiles of the tile-resident kernel
-    int32_t *d_tflag = nullptr;          // 2 x ntiles frontier flags
+    int32_t *d_queues = nullptr;         // push + BFS tile work lists
+    int sms = 148;
+    int relabel_div = 0;                 // env FM_RELABEL_DIV
     int k_local = 0;                     // tuning overrides (env FM_K_LOCAL / FM_BFS_INTERVAL)
     int trace = 0;                       // env FM_TRACE=1: one stderr line per round
     int bfs_interval_env = 0;
@@ -717,22 +747,35 @@ float elapsed(fm_grid *g) {
 }
 
 
+int tq_reset(fm_grid *g, const TileQueue &q) {
+    FM_CHECK_CUDA(cudaMemsetAsync(q.flag[0], 0, sizeof(int32_t) * 2 * (size_t)g->ntiles, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(q.cnt, 0, sizeof(int32_t) * 4, g->stream));
+    return FM_OK;
+}
+
+// zero count[p^1] and work[p] before a launch of parity p
+int tq_arm(fm_grid *g, const TileQueue &q, int p) {
+    FM_CHECK_CUDA(cudaMemsetAsync(q.cnt + (p ? 0 : 2), 0, sizeof(int32_t) * 2, g->stream));
+    return FM_OK;
+}
+
 // Repeated frontier sweeps of a tile fixpoint kernel until a sweep changes nothing.
-// Launch i consumes flag buffer i&1 and fills the other; the per-launch count of
-// changed tiles lands in flags[i] (batches of 4 launches per host check).
+// Sweep 0 visits every tile; sweep i drains bq.list[i&1] and fills the other list
+// with the neighbours of tiles whose border changed.  Persistent CTAs take tiles
+// from the list, so a sweep over a small frontier costs a few microseconds.  The
+// per-sweep count of changed tiles lands in flags[j] (batches of 4 per host check).
 template <typename K>
 int frontier_sweeps(fm_grid *g, K kernel, int64_t *sweeps, int64_t *launches, double *ms_kern) {
-    int32_t *fa = g->d_tflag, *fb = g->d_tflag + g->ntiles;
-    FM_CHECK_CUDA(cudaMemsetAsync(fa, 0x01, sizeof(int32_t) * g->ntiles, g->stream));
-    FM_CHECK_CUDA(cudaMemsetAsync(fb, 0, sizeof(int32_t) * g->ntiles, g->stream));
+    FM_TRY(tq_reset(g, g->d.bq));
     const int batch = 4;
+    const int blocks = std::min(g->ntiles, g->sms * 8);
     int i = 0;
     for (;;) {
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
         cudaEventRecord(g->ev[2], g->stream);
         for (int j = 0; j < batch; j++, i++) {
-            int32_t *cur = (i & 1) ? fb : fa, *nxt = (i & 1) ? fa : fb;
-            kernel<<<g->ntiles, dim3(TILE_W, BLK_Y), 0, g->stream>>>(g->d, cur, nxt, g->flags + j);
+            FM_TRY(tq_arm(g, g->d.bq, i & 1));
+            kernel<<<blocks, dim3(TILE_W, BLK_Y), 0, g->stream>>>(g->d, i & 1, i == 0 ? 1 : 0, g->flags + j);
         }
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[3], g->stream);
@@ -753,7 +796,8 @@ int frontier_sweeps(fm_grid *g, K kernel, int64_t *sweeps, int64_t *launches, do
     return FM_OK;
 }
 
-// global relabel + gap + marking; leaves the active-pixel count in g->active
+// global relabel + gap + marking; leaves the active-pixel count in g->active and
+// the tiles holding active pixels in the push work list (parity 0)
 int global_relabel(fm_grid *g) {
     cudaEventRecord(g->ev[0], g->stream);
     bfs_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
@@ -761,7 +805,7 @@ int global_relabel(fm_grid *g) {
     g->st.launches++;
     FM_TRY(frontier_sweeps(g, bfs_tile_kernel, &g->st.bfs_sweeps, &g->st.bfs_launches, &g->st.ms_bfs_kern));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
-    FM_CHECK_CUDA(cudaMemsetAsync(g->d.tile_active, 0, sizeof(int32_t) * g->ntiles, g->stream));
+    FM_TRY(tq_reset(g, g->d.pq));
     bfs_finalize_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 4);
     FM_CHECK_LAUNCH();
     g->st.launches++;
@@ -780,7 +824,6 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
                  const int32_t *capU, const int32_t *capS, const int32_t *capT, int32_t flags) {
     g->flags_solve = flags;
     memset(&g->st, 0, sizeof(g->st));
-    FM_CHECK_CUDA(cudaMemsetAsync(g->d.tile_inflow, 0, sizeof(int32_t) * g->ntiles, g->stream));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 16, g->stream));
     grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
@@ -800,10 +843,15 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     return global_relabel(g);
 }
 
-// one coordinator round: lock-free launches until an idle launch or the budget,
-// then cancel (opt-in), global relabel, gap, mark (maxflow_par.py:195-229)
-constexpr int K_LOCAL_DEFAULT = 64;     // lock-free passes per tile visit
-constexpr int BFS_INTERVAL_DEFAULT = 8;  // tile launches between global relabels
+// One coordinator round: lock-free launches over the work list of tiles until an
+// idle launch, until relabels since the last global relabel reach the relabel
+// budget (the O(V)-work trigger of the reference's sequential solver,
+// maxflow_seq.py:197-205 -- heuristic_period relabels between global relabels),
+// or until the launch cap; then cancel (opt-in), global relabel, gap, mark
+// (maxflow_par.py:195-229).
+constexpr int K_LOCAL_DEFAULT = 32;      // lock-free passes per tile visit
+constexpr int MAX_LAUNCHES_DEFAULT = 16; // launch cap per round
+constexpr int RELABEL_DIV_DEFAULT = 16;  // relabel budget = H*W / div
 
 int run_round_global(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int32_t *done_out) {
     const int32_t cap = std::max(1, std::min(cycle_budget, bfs_interval > 0 ? bfs_interval : 64));
@@ -838,19 +886,27 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     const int k_local = std::max(1, std::min(cycle_budget, g->k_local > 0 ? g->k_local : K_LOCAL_DEFAULT));
     if (bfs_interval <= 0 && g->bfs_interval_env > 0) bfs_interval = g->bfs_interval_env;
     const int32_t cap = std::max(1, std::min((cycle_budget + k_local - 1) / k_local,
-                                             bfs_interval > 0 ? bfs_interval : BFS_INTERVAL_DEFAULT));
+                                             bfs_interval > 0 ? bfs_interval : MAX_LAUNCHES_DEFAULT));
+    const long long relabel_budget =
+        std::max<long long>(1024, g->HW / (g->relabel_div > 0 ? g->relabel_div : RELABEL_DIV_DEFAULT));
+    const int blocks = std::min(g->ntiles, g->sms * 3);
     int32_t done = 0;
     while (done < cap) {
         const int batch = std::min(4, cap - done);
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
         cudaEventRecord(g->ev[2], g->stream);
-        for (int i = 0; i < batch; i++)
-            pr_tile_kernel<<<g->ntiles, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->flags + i, g->acc + 10);
+        for (int i = 0; i < batch; i++) {
+            const int p = (done + i) & 1;
+            FM_TRY(tq_arm(g, g->d.pq, p));
+            pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, p, g->flags + i, g->acc + 10);
+        }
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[3], g->stream);
         g->st.launches += batch;
         g->st.pr_launches += batch;
         FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int32_t) * batch,
+                                      cudaMemcpyDeviceToHost, g->stream));
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 10, g->acc + 10, sizeof(unsigned long long) * 2,
                                       cudaMemcpyDeviceToHost, g->stream));
         FM_TRY(sync_stream(g));
         g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
@@ -861,6 +917,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
         }
         done += idle_at < 0 ? batch : idle_at + 1;
         if (idle_at >= 0) break;
+        if ((long long)g->h_acc[11] >= relabel_budget) break;
     }
     integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
     FM_CHECK_LAUNCH();
@@ -984,6 +1041,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_K_LOCAL")) g->k_local = atoi(v);
     if (const char *v = getenv("FM_BFS_INTERVAL")) g->bfs_interval_env = atoi(v);
     if (const char *v = getenv("FM_TRACE")) g->trace = atoi(v);
+    if (const char *v = getenv("FM_RELABEL_DIV")) g->relabel_div = atoi(v);
     const size_t n4 = sizeof(int32_t) * (size_t)g->HW, n1 = (size_t)g->HW;
     int32_t **planes[] = {&g->d.e, &g->d.h, &g->d.rR, &g->d.rL, &g->d.rD, &g->d.rU,
                           &g->d.rT, &g->d.rS, &g->d.cS, &g->d.dist, &g->d.inflow_h, &g->d.inflow_v};
@@ -998,9 +1056,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         cudaMalloc((void **)&g->d.marked, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->d.cut, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
-        cudaMalloc((void **)&g->d.tile_active, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
-        cudaMalloc((void **)&g->d.tile_inflow, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
-        cudaMalloc((void **)&g->d_tflag, sizeof(int32_t) * 2 * (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->d_queues, sizeof(int32_t) * (8 * (size_t)g->ntiles + 8)) != cudaSuccess ||
         cudaMalloc((void **)&g->flags, sizeof(int32_t) * 64) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_flags, sizeof(int32_t) * 64) != cudaSuccess ||
@@ -1010,12 +1066,25 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         return FM_CUDA_ERROR;
     }
     for (auto &e : g->ev) cudaEventCreate(&e);
+    {
+        TileQueue *qs[2] = {&g->d.pq, &g->d.bq};
+        int32_t *base = g->d_queues;
+        for (int k = 0; k < 2; k++) {
+            // [list0 | list1 | flag0 | flag1] per queue, then 4 counters per queue
+            qs[k]->list[0] = base + (size_t)(4 * k + 0) * g->ntiles;
+            qs[k]->list[1] = base + (size_t)(4 * k + 1) * g->ntiles;
+            qs[k]->flag[0] = base + (size_t)(4 * k + 2) * g->ntiles;
+            qs[k]->flag[1] = base + (size_t)(4 * k + 3) * g->ntiles;
+            qs[k]->cnt = base + (size_t)8 * g->ntiles + 4 * k;
+        }
+    }
     g->stream = g->own_stream;
     g->d.H = H; g->d.W = W;
     g->d.V = (int32_t)(g->HW + 2);
     g->d.INF = g->d.V;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    g->sms = sms;
     g->grid_blocks = (int)std::min<int64_t>((g->HW + 255) / 256, (int64_t)sms * 8);
     *out = g;
     return FM_OK;
@@ -1026,7 +1095,7 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     cudaSetDevice(g->device);
     int32_t *planes[] = {g->d.e, g->d.h, g->d.rR, g->d.rL, g->d.rD, g->d.rU,
                          g->d.rT, g->d.rS, g->d.cS, g->d.dist, g->d.inflow_h, g->d.inflow_v,
-                         g->d.tile_active, g->d.tile_inflow, g->d_tflag, g->in_caps};
+                         g->d_queues, g->in_caps};
     for (auto p : planes) if (p) cudaFree(p);
     if (g->d.mask) cudaFree(g->d.mask);
     if (g->d.marked) cudaFree(g->d.marked);
