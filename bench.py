@@ -8,8 +8,10 @@ resident in HBM.  value = Medges/s = E_grid / solve seconds, E_grid =
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N > 1) every rank solves its own 4096^2 instance (seed 4096 +
-rank): independent replicas, weak scaling; time = max over ranks.
+Under torchrun (N > 1) the ranks solve ONE grid of N * 4096^2 pixels (N=2: 8192 x
+4096, N=4: 8192^2, N=8: 16384 x 8192) split in row bands, one band per GPU, boundary
+rows exchanged with NCCL send/recv (paper_1110_6231_b200/bands.py): weak scaling,
+time = max over ranks.
 ``--impl reference`` times the reference algorithm's CPU port (oracle/, C
 restatement of hybrid_solve with real threads) on a bounded sample.
 """
@@ -18,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -143,6 +146,105 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def grid_shape_for(ws: int, S: int):
+    """Weak scaling: N ranks solve one grid of N * S^2 pixels split in row bands
+    (N=1: S x S, N=2: 2S x S, N=4: 2S x 2S, N=8: 4S x 2S)."""
+    wf = 2 ** (int(math.log2(ws)) // 2) if ws > 1 else 1
+    W = S * wf
+    return ws * S * S // W, W
+
+
+def run_banded(args, ws, rank, local):
+    """N > 1: one band per rank of a (N * S^2)-pixel grid, boundary rows over NCCL."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1110_6231_b200 import bands as B
+    from paper_1110_6231_b200 import generators as G
+
+    S = args.size
+    H, W = grid_shape_for(ws, S)
+    spans = B.band_rows(H, ws)
+    r0, r1 = spans[rank]
+    gt, gb = rank > 0, rank + 1 < ws
+    rows = G.grid_random_rows(H, W, S, r0 - gt, r1 + gb)
+    caps_band = B.band_caps_from_rows(rows, gt, gb)
+    band = B.Band(caps_band, gt, gb, H * W + 2, local)
+    stream = torch.cuda.current_stream()
+    flows = set()
+    for _ in range(args.warmup):
+        f, _, _ = B.solve_distributed(None, gt, gb, H * W, rank, ws, local, band=band)
+        flows.add(f)
+    clocks = Clocks(local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    agg = {}
+    for _ in range(args.steps):
+        f, _, st = B.solve_distributed(None, gt, gb, H * W, rank, ws, local, band=band)
+        flows.add(f)
+        for k, v in st.items():
+            agg[k] = agg.get(k, 0) + v
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    assert len(flows) == 1, f"flow changed across steps: {flows}"
+    flow = flows.pop()
+    value = e_grid(H, W) / (ms_step / 1000.0) / 1e6
+    bst = band.stats()
+    # e2e: host planes -> this rank's band -> solve -> cut back to the host
+    e2e = None
+    if not args.no_e2e:
+        pinned = [torch.from_numpy(c).pin_memory() for c in caps_band]
+        times = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            band.load_caps(pinned)
+            torch.cuda.synchronize()
+            f, _, _ = B.solve_distributed(None, gt, gb, H * W, rank, ws, local, band=band)
+            band.cut_host()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            assert f == flow
+        tt = torch.tensor([statistics.mean(times)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(e_grid(H, W) / float(tt.item()) / 1e6, 3), "unit": UNIT,
+               "h2d_bytes_per_step": 6 * 4 * H * W, "d2h_bytes_per_step": H * W + 8 * ws,
+               "ms_per_step": round(1000 * float(tt.item()), 3),
+               "api": "paper_1110_6231_b200.bands.solve_distributed (one band per rank)"}
+    HWb = (r1 - r0) * W
+    peak, peak_src = measured_peak_hbm()
+    launches = max(1, bst.get("pr_launches", 1))
+    bpl = bst.get("pr_tiles", 0) * (1024 * 60 + 512) / launches
+    dur = max(1e-9, bst.get("ms_pr_kern", 0.0)) / launches
+    roofline = {"bound": "hbm", "achieved": round(bpl / (dur / 1000.0) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(bpl / (dur / 1000.0) / 1e9 / peak, 4), "traffic": None, "kernel": "pr_tile_kernel",
+                "peak_source": peak_src, "scope": "rank 0 band, cumulative over warmup + timed solves"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                "config": {"workload": f"grid max-flow + min-cut {H}x{W} 4-connected in {ws} row bands "
+                                       f"(blocked generator G_b seed {S}; {S}^2 pixels per GPU)",
+                           "E_grid": e_grid(H, W), "flow": flow, "parallelism": f"row bands x{ws} (NCCL send/recv)",
+                           "band_rows": r1 - r0, "band_pixels": HWb,
+                           "l2": "inputs larger than L2", "cycle_budget": 7000},
+                "roofline": roofline, "cpu_baseline": None, "e2e": e2e,
+                "gpu_launches": int(bst.get("launches", 0)), "clocks": clk,
+                "coordinator": {k: (round(v / args.steps, 3) if isinstance(v, float) else v // args.steps)
+                                for k, v in agg.items()}}
+        print(json.dumps(line), flush=True)
+    band.close()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -156,6 +258,8 @@ def main():
     ap.add_argument("--no-assign", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test the banded path with several ranks sharing fewer GPUs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -165,11 +269,17 @@ def main():
     import torch
 
     ws, rank, local = dist_env()
+    if args.dist_backend == "gloo":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+        return run_banded(args, ws, rank, local)
     import paper_1110_6231_b200 as fmb
     from paper_1110_6231_b200 import generators as G
 

@@ -140,6 +140,36 @@ int fm_grid_export(fm_grid *g, int32_t *rR, int32_t *rL, int32_t *rD, int32_t *r
 /* Minimal source-side cut of the current state into a HOST buffer. */
 int fm_grid_cut_host(fm_grid *g, uint8_t *cut_out, fm_stats *stats);
 
+/* Copy the current cut plane without recomputing it (dst host or device). */
+int fm_grid_cut_plane(fm_grid *g, uint8_t *dst, int32_t dst_on_host);
+/* Counters of the last / current solve. */
+int fm_grid_stats(fm_grid *g, fm_stats *stats);
+
+/* ------------------------------------------------------------ row bands
+ * Multi-GPU grid path: the handle holds one horizontal band of a
+ * larger grid plus a ghost row (frozen copy of the neighbour band's boundary row)
+ * on each side that has a neighbour.  Orchestrated by paper_1110_6231_b200.bands;
+ * every step syncs its stream before returning.  cap* and row buffers: DEVICE. */
+#define FM_ROW_FLOW 0  /* out: flow parked in the ghost row (zeroed) | in: flow into our boundary row */
+#define FM_ROW_H 1     /* out: boundary-row heights               | in: ghost heights */
+#define FM_ROW_RES 2   /* out: boundary residual toward the ghost  | in: ghost residual toward us */
+#define FM_ROW_DIST 3  /* out: boundary BFS distance               | in: ghost distance (re-queues tiles) */
+#define FM_ROW_CUT 4   /* out: boundary cut bit                    | in: ghost cut bit (re-queues tiles) */
+/* global_nodes = H*W + 2 of the WHOLE grid: heights, the source height |V| and the
+ * BFS sentinel must agree across bands. */
+int fm_grid_band_config(fm_grid *g, int32_t ghost_top, int32_t ghost_bottom, int64_t global_nodes);
+int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t *capL,
+                      const int32_t *capD, const int32_t *capU, const int32_t *capS,
+                      const int32_t *capT, int32_t flags, int64_t *sum_caps_out);
+int fm_grid_band_bfs(fm_grid *g, int32_t phase, int64_t *changed);
+int fm_grid_band_finalize(fm_grid *g, int64_t *out /* active, marked excess, deepest level */);
+int fm_grid_band_push(fm_grid *g, int32_t max_launches, int32_t cycle_budget,
+                      int64_t *out /* pushes, relabels, launches, idle */);
+int fm_grid_band_cut(fm_grid *g, int32_t phase, int64_t *changed);
+int fm_grid_band_rows(fm_grid *g, int32_t direction /* 0 out, 1 in */, int32_t side /* 0 top, 1 bottom */,
+                      int32_t kind, int32_t *buf, int64_t *changed);
+int fm_grid_band_flow(fm_grid *g, int64_t *out);
+
 /* ------------------------------------------------------------- assignment */
 typedef struct fm_assign fm_assign;
 

@@ -81,6 +81,16 @@ SIGNATURES = {
     "fm_grid_round": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp]),
     "fm_grid_export": (ctypes.c_int, [_vp] + [_vp] * 11),
     "fm_grid_cut_host": (ctypes.c_int, [_vp, _vp, _vp]),
+    "fm_grid_cut_plane": (ctypes.c_int, [_vp, _vp, _i32]),
+    "fm_grid_stats": (ctypes.c_int, [_vp, _vp]),
+    "fm_grid_band_config": (ctypes.c_int, [_vp, _i32, _i32, _i64]),
+    "fm_grid_band_init": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32, _vp]),
+    "fm_grid_band_bfs": (ctypes.c_int, [_vp, _i32, _vp]),
+    "fm_grid_band_finalize": (ctypes.c_int, [_vp, _vp]),
+    "fm_grid_band_push": (ctypes.c_int, [_vp, _i32, _i32, _vp]),
+    "fm_grid_band_cut": (ctypes.c_int, [_vp, _i32, _vp]),
+    "fm_grid_band_rows": (ctypes.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
+    "fm_grid_band_flow": (ctypes.c_int, [_vp, _vp]),
     "fm_assign_create": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(_vp)]),
     "fm_assign_destroy": (None, [_vp]),
     "fm_assign_solve": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),

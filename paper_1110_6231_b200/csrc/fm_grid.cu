@@ -49,6 +49,9 @@ __device__ __forceinline__ int tq_take(const TileQueue &q, int parity, int all_t
     return t;
 }
 
+struct GridDev;
+__device__ __forceinline__ bool is_ghost_row(const GridDev &g, int r);
+
 struct GridDev {
     int32_t *e, *h, *rR, *rL, *rD, *rU, *rT, *rS, *cS;
     int32_t *dist;
@@ -60,10 +63,19 @@ struct GridDev {
     int32_t ntx, nty;       // tiles per row / column
     TileQueue pq;           // push-relabel work list
     TileQueue bq;           // BFS / cut frontier work list
+    // row-band mode (multi-GPU): row 0 / row H-1 is a ghost copy of the neighbour
+    // band's boundary row.  Ghost pixels never act; flow pushed into them is
+    // shipped to the owner band; their h / dist / cut / residual toward us are
+    // imported from the owner.
+    int32_t ghost_top, ghost_bot;
     int32_t H, W;
     int32_t V;      // node count |V| = H*W + 2 (the source's height)
     int32_t INF;    // "unreached" distance sentinel (== V)
 };
+
+__device__ __forceinline__ bool is_ghost_row(const GridDev &g, int r) {
+    return (g.ghost_top && r == 0) || (g.ghost_bot && r == g.H - 1);
+}
 
 // ----------------------------------------------------------------------------
 // init: hybrid_init + init_preflow (maxflow_par.py:44-62, maxflow_seq.py:47-64).
@@ -233,10 +245,12 @@ __global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_
     const int V = g.V;
     const int c = c0 + tx;
     int32_t rs[PT_ROWS];
+    bool ghost[PT_ROWS];
 #pragma unroll
     for (int k = 0; k < PT_ROWS; k++) {
         const int lr = ty + k * PT_TY;
         const int r = r0 + lr;
+        ghost[k] = is_ghost_row(g, r);
         if (r < g.H && c < g.W) {
             const int64_t p = (int64_t)r * g.W + c;
             int32_t e = g.e[p];
@@ -283,6 +297,7 @@ __global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_
         for (int k = 0; k < PT_ROWS; k++) {
             const int lr = ty + k * PT_TY;
             const int li = lr * PT_W + tx;
+            if (ghost[k]) continue;                      // owned by the neighbour band
             const int32_t e = ve[li];
             if (e <= 0) continue;
             const int hi = (lr + 1) * HS + tx + 1;
@@ -351,7 +366,7 @@ __global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_
             g.rR[p] = s_r[0][lr][tx]; g.rL[p] = s_r[1][lr][tx];
             g.rD[p] = s_r[2][lr][tx]; g.rU[p] = s_r[3][lr][tx];
             g.rT[p] = s_t[lr][tx];
-            act |= (e > 0 && h < V);
+            act |= (e > 0 && h < V && !ghost[k]);
         }
     }
     const int any_act = __syncthreads_or(act);
@@ -396,6 +411,7 @@ __global__ void cancel_kernel(GridDev g, unsigned long long *count) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
+        if (is_ghost_row(g, r)) continue;
         const int32_t hp = g.h[p];
         int32_t moved = 0;
         const int32_t rt = g.rT[p];
@@ -441,6 +457,7 @@ __global__ void bfs_init_kernel(GridDev g) {
         if (r + 1 < g.H && g.rD[p] > 0) m |= M_D;
         if (r > 0 && g.rU[p] > 0) m |= M_U;
         if (g.rT[p] > 0) m |= M_T;
+        if (is_ghost_row(g, r)) m = 0;    // distance imported from the owner band
         g.mask[p] = m;
         g.dist[p] = (m & M_T) ? 1 : g.INF;
     }
@@ -543,6 +560,7 @@ __global__ void bfs_finalize_kernel(GridDev g, unsigned long long *acc /* [0] ac
     int32_t lvl = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
          p += (int64_t)gridDim.x * blockDim.x) {
+        if ((g.ghost_top && p < g.W) || (g.ghost_bot && p >= HW - g.W)) continue;
         const int32_t d = g.dist[p];
         const int32_t e = g.e[p];
         if (d < g.INF) {
@@ -594,8 +612,9 @@ __global__ void cut_init_kernel(GridDev g) {
         if (c > 0 && g.rR[p - 1] > 0) m |= M_L;
         if (r + 1 < g.H && g.rU[p + g.W] > 0) m |= M_D;
         if (r > 0 && g.rD[p - g.W] > 0) m |= M_U;
-        g.mask[p] = m;
-        g.cut[p] = (g.e[p] > 0 || g.cS[p] - g.rS[p] > 0) ? 1 : 0;
+        const bool gh = is_ghost_row(g, r);
+        g.mask[p] = gh ? 0 : m;           // ghost membership is imported from the owner band
+        g.cut[p] = (!gh && (g.e[p] > 0 || g.cS[p] - g.rS[p] > 0)) ? 1 : 0;
     }
 }
 
@@ -676,7 +695,7 @@ __global__ void sum_e_kernel(GridDev g, unsigned long long *acc) {
     long long s = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
          p += (int64_t)gridDim.x * blockDim.x)
-        s += g.e[p];
+        if (!((g.ghost_top && p < g.W) || (g.ghost_bot && p >= HW - g.W))) s += g.e[p];
     __shared__ long long red[8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -687,6 +706,67 @@ __global__ void sum_e_kernel(GridDev g, unsigned long long *acc) {
         long long t = 0;
         for (int i = 0; i < (int)(blockDim.x >> 5); i++) t += red[i];
         if (t) atomicAdd(acc, (unsigned long long)t);
+    }
+}
+
+
+// ----------------------------------------------------------------------------
+// row-band exchange (multi-GPU): one thread per column.  side 0 = top, 1 = bottom.
+// kind 0 ROW_FLOW: out = flow parked in the ghost row (then zeroed) | in = flow
+//        arriving in our boundary row: e += v and the residual toward the ghost += v
+// kind 1 ROW_H:    out = boundary-row heights | in = ghost heights
+// kind 2 ROW_RES:  out = boundary-row residual toward the ghost | in = ghost residual toward us
+// kind 3 ROW_DIST: out = boundary-row BFS distance | in = ghost distance (tiles re-queued if changed)
+// kind 4 ROW_CUT:  out = boundary-row cut bit | in = ghost cut bit (tiles re-queued if changed)
+// ----------------------------------------------------------------------------
+__global__ void band_rows_out_kernel(GridDev g, int side, int kind, int32_t *dst) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= g.W) return;
+    const int64_t gr = side == 0 ? 0 : g.H - 1;        // ghost row
+    const int64_t br = side == 0 ? 1 : g.H - 2;        // our boundary row
+    const int64_t pg = gr * g.W + c, pb = br * g.W + c;
+    int32_t v = 0;
+    if (kind == 0) { v = g.e[pg]; g.e[pg] = 0; }
+    else if (kind == 1) v = g.h[pb];
+    else if (kind == 2) v = side == 0 ? g.rU[pb] : g.rD[pb];
+    else if (kind == 3) v = g.dist[pb];
+    else v = g.cut[pb];
+    dst[c] = v;
+}
+
+__global__ void band_rows_in_kernel(GridDev g, int side, int kind, const int32_t *src, int pq_parity,
+                                    int bq_parity, int32_t *changed) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= g.W) return;
+    const int64_t gr = side == 0 ? 0 : g.H - 1;
+    const int64_t br = side == 0 ? 1 : g.H - 2;
+    const int64_t pg = gr * g.W + c, pb = br * g.W + c;
+    const int t = ((int)br / PT_H) * g.ntx + c / PT_W;   // tile of our boundary pixel
+    const int32_t v = src[c];
+    if (kind == 0) {
+        if (v) {
+            g.e[pb] += v;
+            if (side == 0) g.rU[pb] += v; else g.rD[pb] += v;
+            tq_push(g.pq, pq_parity, t);
+            atomicAdd(changed, 1);
+        }
+    } else if (kind == 1) {
+        g.h[pg] = v;
+    } else if (kind == 2) {
+        if (side == 0) g.rD[pg] = v; else g.rU[pg] = v;
+    } else if (kind == 3) {
+        if (g.dist[pg] != v) {
+            g.dist[pg] = v;
+            tq_push(g.bq, bq_parity, t);
+            atomicAdd(changed, 1);
+        }
+    } else {
+        const uint8_t b = v ? 1 : 0;
+        if (g.cut[pg] != b) {
+            g.cut[pg] = b;
+            tq_push(g.bq, bq_parity, t);
+            atomicAdd(changed, 1);
+        }
     }
 }
 
@@ -715,6 +795,9 @@ struct fm_grid {
     int32_t *d_queues = nullptr;         // push + BFS tile work lists
     int sms = 148;
     int relabel_div = 0;                 // env FM_RELABEL_DIV
+    int pq_parity = 0;                   // parity of the next push launch
+    int bq_parity = 0;                   // parity of the next BFS / cut sweep
+    int32_t *d_band = nullptr;           // band exchange: changed counter
     int k_local = 0;                     // tuning overrides (env FM_K_LOCAL / FM_BFS_INTERVAL)
     int trace = 0;                       // env FM_TRACE=1: one stderr line per round
     int bfs_interval_env = 0;
@@ -765,17 +848,24 @@ int tq_arm(fm_grid *g, const TileQueue &q, int p) {
 // from the list, so a sweep over a small frontier costs a few microseconds.  The
 // per-sweep count of changed tiles lands in flags[j] (batches of 4 per host check).
 template <typename K>
-int frontier_sweeps(fm_grid *g, K kernel, int64_t *sweeps, int64_t *launches, double *ms_kern) {
-    FM_TRY(tq_reset(g, g->d.bq));
+int frontier_sweeps(fm_grid *g, K kernel, bool first_all, int64_t *sweeps, int64_t *launches,
+                    double *ms_kern) {
+    if (first_all) {
+        FM_TRY(tq_reset(g, g->d.bq));
+        g->bq_parity = 0;
+    }
     const int batch = 4;
     const int blocks = std::min(g->ntiles, g->sms * 8);
-    int i = 0;
+    bool first = first_all;
     for (;;) {
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
         cudaEventRecord(g->ev[2], g->stream);
-        for (int j = 0; j < batch; j++, i++) {
-            FM_TRY(tq_arm(g, g->d.bq, i & 1));
-            kernel<<<blocks, dim3(TILE_W, BLK_Y), 0, g->stream>>>(g->d, i & 1, i == 0 ? 1 : 0, g->flags + j);
+        for (int j = 0; j < batch; j++) {
+            const int p = g->bq_parity;
+            FM_TRY(tq_arm(g, g->d.bq, p));
+            kernel<<<blocks, dim3(TILE_W, BLK_Y), 0, g->stream>>>(g->d, p, first ? 1 : 0, g->flags + j);
+            first = false;
+            g->bq_parity ^= 1;
         }
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[3], g->stream);
@@ -803,9 +893,10 @@ int global_relabel(fm_grid *g) {
     bfs_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
     FM_CHECK_LAUNCH();
     g->st.launches++;
-    FM_TRY(frontier_sweeps(g, bfs_tile_kernel, &g->st.bfs_sweeps, &g->st.bfs_launches, &g->st.ms_bfs_kern));
+    FM_TRY(frontier_sweeps(g, bfs_tile_kernel, true, &g->st.bfs_sweeps, &g->st.bfs_launches, &g->st.ms_bfs_kern));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
     FM_TRY(tq_reset(g, g->d.pq));
+    g->pq_parity = 0;
     bfs_finalize_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 4);
     FM_CHECK_LAUNCH();
     g->st.launches++;
@@ -882,7 +973,7 @@ int run_round_global(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int
     return FM_OK;
 }
 
-int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
+int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int32_t *idle_out = nullptr) {
     const int k_local = std::max(1, std::min(cycle_budget, g->k_local > 0 ? g->k_local : K_LOCAL_DEFAULT));
     if (bfs_interval <= 0 && g->bfs_interval_env > 0) bfs_interval = g->bfs_interval_env;
     const int32_t cap = std::max(1, std::min((cycle_budget + k_local - 1) / k_local,
@@ -896,9 +987,10 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
         cudaEventRecord(g->ev[2], g->stream);
         for (int i = 0; i < batch; i++) {
-            const int p = (done + i) & 1;
+            const int p = g->pq_parity;
             FM_TRY(tq_arm(g, g->d.pq, p));
             pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, p, g->flags + i, g->acc + 10);
+            g->pq_parity ^= 1;
         }
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[3], g->stream);
@@ -916,7 +1008,10 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
             g->st.pr_tiles += g->h_flags[i];
         }
         done += idle_at < 0 ? batch : idle_at + 1;
-        if (idle_at >= 0) break;
+        if (idle_at >= 0) {
+            if (idle_out) *idle_out = 1;
+            break;
+        }
         if ((long long)g->h_acc[11] >= relabel_budget) break;
     }
     integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
@@ -968,7 +1063,7 @@ int compute_cut(fm_grid *g, uint8_t *cut_out_dev) {
     g->st.launches++;
     double cut_kern = 0.0;
     int64_t cut_launches = 0;
-    FM_TRY(frontier_sweeps(g, cut_tile_kernel, &g->st.cut_sweeps, &cut_launches, &cut_kern));
+    FM_TRY(frontier_sweeps(g, cut_tile_kernel, true, &g->st.cut_sweeps, &cut_launches, &cut_kern));
     g->st.launches += 0;
     if (cut_out_dev && cut_out_dev != g->d.cut)
         FM_CHECK_CUDA(cudaMemcpyAsync(cut_out_dev, g->d.cut, (size_t)g->HW, cudaMemcpyDeviceToDevice, g->stream));
@@ -1100,6 +1195,7 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->d.mask) cudaFree(g->d.mask);
     if (g->d.marked) cudaFree(g->d.marked);
     if (g->d.cut) cudaFree(g->d.cut);
+    if (g->d_band) cudaFree(g->d_band);
     if (g->acc) cudaFree(g->acc);
     if (g->flags) cudaFree(g->flags);
     if (g->h_acc) cudaFreeHost(g->h_acc);
@@ -1236,5 +1332,185 @@ extern "C" int fm_grid_cut_host(fm_grid *g, uint8_t *cut_out, fm_stats *stats) {
     FM_CHECK_CUDA(cudaMemcpyAsync(cut_out, g->d.cut, (size_t)g->HW, cudaMemcpyDeviceToHost, g->stream));
     FM_TRY(sync_stream(g));
     if (stats) *stats = g->st;
+    return FM_OK;
+}
+
+// ============================================================================
+// row-band steps (multi-GPU grid path; orchestrated by paper_1110_6231_b200.bands)
+// ============================================================================
+extern "C" int fm_grid_band_config(fm_grid *g, int32_t ghost_top, int32_t ghost_bottom,
+                                   int64_t global_nodes) {
+    if (!g || g->H < 1 + (ghost_top ? 1 : 0) + (ghost_bottom ? 1 : 0) || global_nodes < g->HW + 2 ||
+        global_nodes > (int64_t)INT32_MAX / 2 - 4) {
+        fm_set_error("fm_grid_band_config: band too short for its ghost rows, or bad global node count");
+        return FM_INVALID_ARG;
+    }
+    g->d.ghost_top = ghost_top ? 1 : 0;
+    g->d.ghost_bot = ghost_bottom ? 1 : 0;
+    // heights, the source height and the BFS sentinel must agree across bands
+    g->d.V = (int32_t)global_nodes;
+    g->d.INF = g->d.V;
+    if (!g->d_band) FM_CHECK_CUDA(cudaMalloc((void **)&g->d_band, sizeof(int32_t) * 4));
+    return FM_OK;
+}
+
+extern "C" int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t *capL,
+                                 const int32_t *capD, const int32_t *capU, const int32_t *capS,
+                                 const int32_t *capT, int32_t flags, int64_t *sum_caps_out) {
+    if (!g) { fm_set_error("fm_grid_band_init: null handle"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    g->flags_solve = flags;
+    memset(&g->st, 0, sizeof(g->st));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 16, g->stream));
+    grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
+        g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 2,
+                                  cudaMemcpyDeviceToHost, g->stream));
+    FM_TRY(sync_stream(g));
+    if (g->h_acc[1] != 0) { fm_set_error("negative capacity in grid input"); return FM_INVALID_ARG; }
+    g->sum_capS = (long long)g->h_acc[0];
+    g->excess_total = g->sum_capS;
+    FM_TRY(tq_reset(g, g->d.pq));
+    FM_TRY(tq_reset(g, g->d.bq));
+    g->pq_parity = g->bq_parity = 0;
+    if (sum_caps_out) *sum_caps_out = g->sum_capS;
+    return FM_OK;
+}
+
+// phase 0: residual masks + sweeps from every tile; phase 1: sweeps from the tiles
+// queued by imported ghost distances.  *changed = tile visits that changed something.
+extern "C" int fm_grid_band_bfs(fm_grid *g, int32_t phase, int64_t *changed) {
+    if (!g) { fm_set_error("fm_grid_band_bfs: null handle"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    const int64_t before = g->st.reserved[0];
+    if (phase == 0) {
+        bfs_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
+        FM_CHECK_LAUNCH();
+        g->st.launches++;
+    }
+    FM_TRY(frontier_sweeps(g, bfs_tile_kernel, phase == 0, &g->st.bfs_sweeps, &g->st.bfs_launches,
+                           &g->st.ms_bfs_kern));
+    if (changed) *changed = g->st.reserved[0] - before;
+    return FM_OK;
+}
+
+// gap + marking + active tiles; out = {active pixels, newly marked excess, deepest level}
+extern "C" int fm_grid_band_finalize(fm_grid *g, int64_t *out) {
+    if (!g) { fm_set_error("fm_grid_band_finalize: null handle"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
+    FM_TRY(tq_reset(g, g->d.pq));
+    g->pq_parity = 0;
+    bfs_finalize_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 4);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 4, g->acc + 4, sizeof(unsigned long long) * 3,
+                                  cudaMemcpyDeviceToHost, g->stream));
+    FM_TRY(sync_stream(g));
+    g->active = (long long)g->h_acc[4];
+    g->excess_total -= (long long)g->h_acc[5];
+    g->st.bfs_levels = std::max<int64_t>(g->st.bfs_levels, (int64_t)g->h_acc[6]);
+    if (out) { out[0] = g->active; out[1] = (int64_t)g->h_acc[5]; out[2] = (int64_t)g->h_acc[6]; }
+    return FM_OK;
+}
+
+// up to max_launches tile launches (stops on an idle launch or the relabel budget),
+// then folds every inbox; out = {pushes, relabels, launches, idle}
+extern "C" int fm_grid_band_push(fm_grid *g, int32_t max_launches, int32_t cycle_budget, int64_t *out) {
+    if (!g || max_launches < 1 || cycle_budget < 1) { fm_set_error("fm_grid_band_push: invalid argument"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    const fm_stats before = g->st;
+    cudaEventRecord(g->ev[0], g->stream);
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
+    int32_t idle = 0;
+    FM_TRY(run_round_tiles(g, cycle_budget, max_launches, &idle));
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 10, g->acc + 10, sizeof(unsigned long long) * 2,
+                                  cudaMemcpyDeviceToHost, g->stream));
+    cudaEventRecord(g->ev[1], g->stream);
+    FM_TRY(sync_stream(g));
+    g->st.ms_push += elapsed(g);
+    g->st.pushes += (int64_t)g->h_acc[10];
+    g->st.relabels += (int64_t)g->h_acc[11];
+    if (out) {
+        out[0] = (int64_t)g->h_acc[10];
+        out[1] = (int64_t)g->h_acc[11];
+        out[2] = g->st.pr_sweeps - before.pr_sweeps;
+        out[3] = idle;
+    }
+    return FM_OK;
+}
+
+// phase 0: seeds + sweeps from every tile; phase 1: sweeps from imported ghost changes
+extern "C" int fm_grid_band_cut(fm_grid *g, int32_t phase, int64_t *changed) {
+    if (!g) { fm_set_error("fm_grid_band_cut: null handle"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    const int64_t before = g->st.reserved[0];
+    if (phase == 0) {
+        cut_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
+        FM_CHECK_LAUNCH();
+        g->st.launches++;
+    }
+    double kern = 0.0;
+    int64_t launches = 0;
+    FM_TRY(frontier_sweeps(g, cut_tile_kernel, phase == 0, &g->st.cut_sweeps, &launches, &kern));
+    if (changed) *changed = g->st.reserved[0] - before;
+    return FM_OK;
+}
+
+// direction 0: export row `kind` of `side` into buf (DEVICE int32[W]);
+// direction 1: import buf into the ghost / boundary row.  *changed = imported cells that
+// changed something (flow received, distance or cut bit updated).
+extern "C" int fm_grid_band_rows(fm_grid *g, int32_t direction, int32_t side, int32_t kind,
+                                 int32_t *buf, int64_t *changed) {
+    if (!g || !buf || side < 0 || side > 1 || kind < 0 || kind > 4 ||
+        (side == 0 && !g->d.ghost_top) || (side == 1 && !g->d.ghost_bot)) {
+        fm_set_error("fm_grid_band_rows: invalid argument (no ghost row on that side?)");
+        return FM_INVALID_ARG;
+    }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    const int blocks = (g->W + 255) / 256;
+    if (direction == 0) {
+        band_rows_out_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, kind, buf);
+        FM_CHECK_LAUNCH();
+        FM_TRY(sync_stream(g));
+        if (changed) *changed = 0;
+    } else {
+        FM_CHECK_CUDA(cudaMemsetAsync(g->d_band, 0, sizeof(int32_t), g->stream));
+        band_rows_in_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, kind, buf, g->pq_parity,
+                                                          g->bq_parity, g->d_band);
+        FM_CHECK_LAUNCH();
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->d_band, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+        FM_TRY(sync_stream(g));
+        if (changed) *changed = g->h_flags[0];
+    }
+    g->st.launches++;
+    return FM_OK;
+}
+
+// sum over our own (non-ghost) pixels of capS - e: the band's share of the flow
+extern "C" int fm_grid_band_flow(fm_grid *g, int64_t *out) {
+    if (!g || !out) { fm_set_error("fm_grid_band_flow: invalid argument"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    long long f = 0;
+    FM_TRY(current_flow(g, &f));
+    *out = f;
+    return FM_OK;
+}
+
+extern "C" int fm_grid_stats(fm_grid *g, fm_stats *stats) {
+    if (!g || !stats) { fm_set_error("fm_grid_stats: invalid argument"); return FM_INVALID_ARG; }
+    *stats = g->st;
+    return FM_OK;
+}
+
+// copy the current cut plane (no recompute) to dst (host when dst_on_host, else device)
+extern "C" int fm_grid_cut_plane(fm_grid *g, uint8_t *dst, int32_t dst_on_host) {
+    if (!g || !dst) { fm_set_error("fm_grid_cut_plane: invalid argument"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    FM_CHECK_CUDA(cudaMemcpyAsync(dst, g->d.cut, (size_t)g->HW,
+                                  dst_on_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, g->stream));
+    FM_TRY(sync_stream(g));
     return FM_OK;
 }

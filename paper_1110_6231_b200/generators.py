@@ -165,3 +165,40 @@ def assignment_optical_flow(n: int = 4096, seed: int = 4096) -> np.ndarray:
         dp = np.abs(pred[a:b, None, :] - py[None, :, :]).sum(-1)
         w[a:b] = np.maximum(0, 10000 - dd - np.rint(20.0 * dp).astype(np.int64)).astype(np.int32)
     return w
+
+
+BLOCK_ROWS = 512
+
+
+def grid_random_rows(H: int, W: int, seed: int, r0: int, r1: int):
+    """Rows [r0, r1) of the *blocked* generator G_b used for multi-GPU grids: rows
+    come in blocks of 512, block b drawn like generator G from PCG64([seed, b]) (same
+    ranges and plane order), so every rank builds its band without the whole grid.
+    Returns the six planes restricted to those rows (arcs leaving the grid zeroed)."""
+    if not (0 <= r0 < r1 <= H):
+        raise ValueError("bad row range")
+    planes = [[] for _ in range(6)]
+    for b in range(r0 // BLOCK_ROWS, (r1 - 1) // BLOCK_ROWS + 1):
+        lo, hi = b * BLOCK_ROWS, min(H, (b + 1) * BLOCK_ROWS)
+        g = np.random.Generator(np.random.PCG64([seed, b]))
+        n = hi - lo
+        blk = [g.integers(0, 101, size=(n, W), dtype=np.int32),
+               g.integers(0, 101, size=(n, W), dtype=np.int32)]
+        blk += [g.integers(1, 101, size=(n, W), dtype=np.int32) for _ in range(4)]
+        a, z = max(lo, r0), min(hi, r1)
+        # order of the returned planes: R, L, D, U, S, T (drawn as S, T, R, L, D, U)
+        for k, src in enumerate((2, 3, 4, 5, 0, 1)):
+            planes[k].append(blk[src][a - lo:z - lo])
+    capR, capL, capD, capU, capS, capT = [np.ascontiguousarray(np.concatenate(p)) for p in planes]
+    capR[:, -1] = 0
+    capL[:, 0] = 0
+    if r1 == H:
+        capD[-1, :] = 0
+    if r0 == 0:
+        capU[0, :] = 0
+    return capR, capL, capD, capU, capS, capT
+
+
+def grid_random_blocked(H: int, W: int, seed: int):
+    """The whole grid of the blocked generator (tests / single-GPU reference)."""
+    return grid_random_rows(H, W, seed, 0, H)
