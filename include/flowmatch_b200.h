@@ -155,6 +155,7 @@ int fm_grid_stats(fm_grid *g, fm_stats *stats);
 #define FM_ROW_RES 2   /* out: boundary residual toward the ghost  | in: ghost residual toward us */
 #define FM_ROW_DIST 3  /* out: boundary BFS distance               | in: ghost distance (re-queues tiles) */
 #define FM_ROW_CUT 4   /* out: boundary cut bit                    | in: ghost cut bit (re-queues tiles) */
+#define FM_ROW_PUSH_STATE 5 /* FLOW | H | RES as three consecutive rows (buffer of 3 W) */
 /* global_nodes = H*W + 2 of the WHOLE grid: heights, the source height |V| and the
  * BFS sentinel must agree across bands. */
 int fm_grid_band_config(fm_grid *g, int32_t ghost_top, int32_t ghost_bottom, int64_t global_nodes);

@@ -33,7 +33,7 @@ import numpy as np
 from . import _lib
 from .graph import SolveReport
 
-ROW_FLOW, ROW_H, ROW_RES, ROW_DIST, ROW_CUT = 0, 1, 2, 3, 4
+ROW_FLOW, ROW_H, ROW_RES, ROW_DIST, ROW_CUT, ROW_PUSH_STATE = 0, 1, 2, 3, 4, 5
 TOP, BOTTOM = 0, 1
 TILE = 32
 
@@ -107,8 +107,9 @@ class Band:
         self.device = device
         dev = torch.device("cuda", device)
         self.caps = [torch.from_numpy(np.ascontiguousarray(c)).to(dev) for c in caps_band]
-        self.buf = {s: torch.empty(self.W, dtype=torch.int32, device=dev) for s in (TOP, BOTTOM)}
-        self.rbuf = {s: torch.empty(self.W, dtype=torch.int32, device=dev) for s in (TOP, BOTTOM)}
+        # row buffers sized for the widest message (ROW_PUSH_STATE: 3 rows)
+        self.buf = {s: torch.empty(3 * self.W, dtype=torch.int32, device=dev) for s in (TOP, BOTTOM)}
+        self.rbuf = {s: torch.empty(3 * self.W, dtype=torch.int32, device=dev) for s in (TOP, BOTTOM)}
 
     def sides(self):
         return ([TOP] if self.ghost_top else []) + ([BOTTOM] if self.ghost_bot else [])
@@ -159,7 +160,7 @@ class Band:
         return int(out.value)
 
     def rows_out(self, side: int, kind: int):
-        b = self.buf[side]
+        b = self.buf[side][: (3 if kind == ROW_PUSH_STATE else 1) * self.W]
         _lib.check(_lib.load().fm_grid_band_rows(self._h, 0, int(side), int(kind), _lib.ptr(b), None),
                    "fm_grid_band_rows")
         return b
@@ -253,7 +254,7 @@ class DistTransport:
         for side in b.sides():
             peer = self.rank - 1 if side == TOP else self.rank + 1
             out = b.rows_out(side, kind)
-            rb = b.rbuf[side]
+            rb = b.rbuf[side][: out.numel()]
             if getattr(self, "host_staging", False):
                 out, rb = out.cpu(), torch.empty(rb.shape, dtype=rb.dtype)
             recv[side] = rb
@@ -268,9 +269,10 @@ class DistTransport:
         for side in b.sides():
             src = recv[side]
             if src.device.type == "cpu" and b.rbuf[side].device.type == "cuda":
-                b.rbuf[side].copy_(src)
+                dst = b.rbuf[side][: src.numel()]
+                dst.copy_(src)
                 torch.cuda.current_stream().synchronize()
-                src = b.rbuf[side]
+                src = dst
             changed += b.rows_in(side, kind, src)
         return changed
 
@@ -338,24 +340,24 @@ class BandedSolve:
         active = self.global_relabel()
         budget = max(1024, (self.total_pixels or 1) // self.relabel_div)
         while active > 0:
-            launches = relabels = 0
+            batches = relabels = 0
             while True:
+                # every decision below uses all-reduced values or the batch count, so
+                # all ranks take the same branch (their collectives stay matched)
                 idle_all = True
                 for b in bands:
-                    p, r, l, idle = b.push(self.lpe, self.cycle_budget)
+                    p, r, _, idle = b.push(self.lpe, self.cycle_budget)
                     self.stats["pushes"] += p
                     self.stats["relabels"] += r
                     relabels += r
-                    launches = max(launches, l)
                     idle_all &= idle
-                moved = self.tr.exchange(ROW_FLOW)
-                self.tr.exchange(ROW_H)
-                self.tr.exchange(ROW_RES)
+                batches += 1
+                moved = self.tr.exchange(ROW_PUSH_STATE)
                 self.stats["exchanges"] += 1
                 tot = self.tr.sum([moved, 0 if idle_all else 1, relabels])
                 if tot[0] == 0 and tot[1] == 0:
                     break
-                if tot[2] >= budget or launches >= self.max_launches:
+                if tot[2] >= budget or batches * self.lpe >= self.max_launches:
                     break
             active = self.global_relabel()
             self.stats["rounds"] += 1

@@ -1464,28 +1464,32 @@ extern "C" int fm_grid_band_cut(fm_grid *g, int32_t phase, int64_t *changed) {
 // changed something (flow received, distance or cut bit updated).
 extern "C" int fm_grid_band_rows(fm_grid *g, int32_t direction, int32_t side, int32_t kind,
                                  int32_t *buf, int64_t *changed) {
-    if (!g || !buf || side < 0 || side > 1 || kind < 0 || kind > 4 ||
+    if (!g || !buf || side < 0 || side > 1 || kind < 0 || kind > 5 ||
         (side == 0 && !g->d.ghost_top) || (side == 1 && !g->d.ghost_bot)) {
         fm_set_error("fm_grid_band_rows: invalid argument (no ghost row on that side?)");
         return FM_INVALID_ARG;
     }
     FM_CHECK_CUDA(cudaSetDevice(g->device));
     const int blocks = (g->W + 255) / 256;
+    // kind 5 (FM_ROW_PUSH_STATE) = flow | heights | residuals, three rows in one buffer
+    const int k0 = kind == 5 ? 0 : kind, k1 = kind == 5 ? 2 : kind;
     if (direction == 0) {
-        band_rows_out_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, kind, buf);
+        for (int k = k0; k <= k1; k++)
+            band_rows_out_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, k, buf + (size_t)(k - k0) * g->W);
         FM_CHECK_LAUNCH();
         FM_TRY(sync_stream(g));
         if (changed) *changed = 0;
     } else {
         FM_CHECK_CUDA(cudaMemsetAsync(g->d_band, 0, sizeof(int32_t), g->stream));
-        band_rows_in_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, kind, buf, g->pq_parity,
-                                                          g->bq_parity, g->d_band);
+        for (int k = k0; k <= k1; k++)
+            band_rows_in_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, k, buf + (size_t)(k - k0) * g->W,
+                                                              g->pq_parity, g->bq_parity, g->d_band);
         FM_CHECK_LAUNCH();
         FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->d_band, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
         FM_TRY(sync_stream(g));
         if (changed) *changed = g->h_flags[0];
     }
-    g->st.launches++;
+    g->st.launches += k1 - k0 + 1;
     return FM_OK;
 }
 
