@@ -116,12 +116,13 @@ def load():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("FM_LIB_PATH", LIB_PATH)  # A/B builds of the same ABI
+        if not os.path.exists(path):
             raise RuntimeError(
-                f"CUDA extension {LIB_PATH} is missing; run __graft_entry__.build() "
+                f"CUDA extension {path} is missing; run __graft_entry__.build() "
                 "(there is no CPU fallback)"
             )
-        lib = ctypes.CDLL(LIB_PATH)
+        lib = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -68,14 +68,15 @@ class AssignmentInstance:
 
 
 def _check_weights(w) -> np.ndarray:
+    """Square int32 matrix (INT32_MIN = absent arc).  An int32 input is taken as is;
+    wider integer inputs are range-checked before the narrowing copy."""
     w = np.asarray(w)
     if w.ndim != 2 or w.shape[0] != w.shape[1]:
         raise ValueError(f"weights must be square, got shape {w.shape}")
-    present = w != _lib.FM_ABSENT_WEIGHT
-    if present.any():
-        lo, hi = int(w[present].min()), int(w[present].max())
-        if lo <= -(2**31) or hi >= 2**31:
-            raise ValueError("weights must fit in int32")
+    if w.dtype == np.int32:
+        return np.ascontiguousarray(w)
+    if w.size and (int(w.min()) < -(2**31) or int(w.max()) >= 2**31):
+        raise ValueError("weights must fit in int32")
     return np.ascontiguousarray(w, dtype=np.int32)
 
 

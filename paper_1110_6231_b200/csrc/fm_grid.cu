@@ -223,7 +223,10 @@ __global__ void __launch_bounds__(256) pr_sweep_kernel(GridDev g, int32_t *activ
 constexpr int PT_W = 32, PT_H = 32, PT_TY = 16;          // 512 threads, 2 rows each
 constexpr int PT_ROWS = PT_H / PT_TY;
 
-__global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_local, int parity,
+#ifndef FM_PT_MINBLOCKS
+#define FM_PT_MINBLOCKS 4  // 32 registers: 4 CTAs (2048 threads) per SM
+#endif
+__global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(GridDev g, int k_local, int steps, int parity,
                                                                int32_t *processed,
                                                                unsigned long long *ops) {
     __shared__ int32_t s_e[PT_H][PT_W];
@@ -298,35 +301,46 @@ __global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_
             const int lr = ty + k * PT_TY;
             const int li = lr * PT_W + tx;
             if (ghost[k]) continue;                      // owned by the neighbour band
-            const int32_t e = ve[li];
-            if (e <= 0) continue;
             const int hi = (lr + 1) * HS + tx + 1;
-            const int32_t hp = vh[hi];
-            if (hp >= V) continue;
-            any = true;
-            const int32_t rt = vt[li];
-            if (rt > 0 && hp > 0) {                       // sink at height 0
-                const int32_t d = min(e, rt);
-                vt[li] = rt - d;                          // owner-only word
-                atomicSub(&s_e[lr][tx], d);
-                pushes++;
-                continue;
-            }
             const int r = r0 + lr;
-            int32_t best_h = INT32_MAX, best_r = 0;
-            int dir = -1;
-            if (rt > 0) { best_h = 0; dir = 4; }
-            const int32_t rr = *(volatile int32_t *)&s_r[0][lr][tx];
-            if (rr > 0 && c + 1 < g.W) { const int32_t hq = vh[hi + 1]; if (hq < best_h) { best_h = hq; best_r = rr; dir = 0; } }
-            const int32_t rl = *(volatile int32_t *)&s_r[1][lr][tx];
-            if (rl > 0 && c > 0) { const int32_t hq = vh[hi - 1]; if (hq < best_h) { best_h = hq; best_r = rl; dir = 1; } }
-            const int32_t rd = *(volatile int32_t *)&s_r[2][lr][tx];
-            if (rd > 0 && r + 1 < g.H) { const int32_t hq = vh[hi + HS]; if (hq < best_h) { best_h = hq; best_r = rd; dir = 2; } }
-            const int32_t ru = *(volatile int32_t *)&s_r[3][lr][tx];
-            if (ru > 0 && r > 0) { const int32_t hq = vh[hi - HS]; if (hq < best_h) { best_h = hq; best_r = ru; dir = 3; } }
-            if (rs[k] > 0 && V < best_h) { best_h = V; dir = 5; }
-            if (dir < 0) continue;
-            if (hp > best_h && dir < 4) {
+            // up to `steps` operations on this pixel per pass: a relabel is always
+            // followed by the push it enables (the pixel now sits one above its
+            // lowest residual neighbour), and the pixel keeps discharging while it
+            // holds excess -- a sequence of maxflow_par.py:98-125 operations by the
+            // pixel's owner, each one lock-free
+            for (int st = 0; st < steps; st++) {
+                const int32_t e = ve[li];
+                if (e <= 0) break;
+                int32_t hp = vh[hi];
+                if (hp >= V) break;
+                any = true;
+                const int32_t rt = vt[li];
+                if (rt > 0) {                             // sink at height 0
+                    if (hp == 0) { vh[hi] = 1; relabels++; }
+                    const int32_t d = min(e, rt);
+                    vt[li] = rt - d;                      // owner-only word
+                    atomicSub(&s_e[lr][tx], d);
+                    pushes++;
+                    continue;
+                }
+                int32_t best_h = INT32_MAX, best_r = 0;
+                int dir = -1;
+                const int32_t rr = *(volatile int32_t *)&s_r[0][lr][tx];
+                if (rr > 0 && c + 1 < g.W) { const int32_t hq = vh[hi + 1]; if (hq < best_h) { best_h = hq; best_r = rr; dir = 0; } }
+                const int32_t rl = *(volatile int32_t *)&s_r[1][lr][tx];
+                if (rl > 0 && c > 0) { const int32_t hq = vh[hi - 1]; if (hq < best_h) { best_h = hq; best_r = rl; dir = 1; } }
+                const int32_t rd = *(volatile int32_t *)&s_r[2][lr][tx];
+                if (rd > 0 && r + 1 < g.H) { const int32_t hq = vh[hi + HS]; if (hq < best_h) { best_h = hq; best_r = rd; dir = 2; } }
+                const int32_t ru = *(volatile int32_t *)&s_r[3][lr][tx];
+                if (ru > 0 && r > 0) { const int32_t hq = vh[hi - HS]; if (hq < best_h) { best_h = hq; best_r = ru; dir = 3; } }
+                if (rs[k] > 0 && V < best_h) { best_h = V; dir = 5; }
+                if (dir < 0) break;                       // nothing residual: written off later
+                if (hp <= best_h) {                       // relabel (owner-only)
+                    hp = best_h + 1;
+                    vh[hi] = hp;
+                    relabels++;
+                    if (dir == 5) break;                  // climbed above the source: inactive
+                }
                 const int32_t d = min(e, best_r);
                 atomicSub(&s_e[lr][tx], d);
                 atomicSub(&s_r[dir][lr][tx], d);
@@ -345,9 +359,6 @@ __global__ void __launch_bounds__(PT_W * PT_TY) pr_tile_kernel(GridDev g, int k_
                     tq_push(g.pq, parity ^ 1, nt);
                 }
                 pushes++;
-            } else {
-                vh[hi] = best_h + 1;
-                relabels++;
             }
         }
         if ((it & 3) == 3 && !__syncthreads_or(any)) break;
@@ -796,6 +807,8 @@ struct fm_grid {
     int sms = 148;
     int relabel_div = 0;                 // env FM_RELABEL_DIV
     int pq_parity = 0;                   // parity of the next push launch
+    int pt_per_sm = 3;                   // resident pr_tile CTAs per SM (occupancy query)
+    int op_steps = 1;                    // operations per pixel per pass (env FM_OP_STEPS)
     int bq_parity = 0;                   // parity of the next BFS / cut sweep
     int32_t *d_band = nullptr;           // band exchange: changed counter
     int k_local = 0;                     // tuning overrides (env FM_K_LOCAL / FM_BFS_INTERVAL)
@@ -980,7 +993,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
                                              bfs_interval > 0 ? bfs_interval : MAX_LAUNCHES_DEFAULT));
     const long long relabel_budget =
         std::max<long long>(1024, g->HW / (g->relabel_div > 0 ? g->relabel_div : RELABEL_DIV_DEFAULT));
-    const int blocks = std::min(g->ntiles, g->sms * 3);
+    const int blocks = std::min(g->ntiles, g->sms * g->pt_per_sm);
     int32_t done = 0;
     while (done < cap) {
         const int batch = std::min(4, cap - done);
@@ -989,7 +1002,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
         for (int i = 0; i < batch; i++) {
             const int p = g->pq_parity;
             FM_TRY(tq_arm(g, g->d.pq, p));
-            pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, p, g->flags + i, g->acc + 10);
+            pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, p, g->flags + i, g->acc + 10);
             g->pq_parity ^= 1;
         }
         FM_CHECK_LAUNCH();
@@ -1137,6 +1150,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_BFS_INTERVAL")) g->bfs_interval_env = atoi(v);
     if (const char *v = getenv("FM_TRACE")) g->trace = atoi(v);
     if (const char *v = getenv("FM_RELABEL_DIV")) g->relabel_div = atoi(v);
+    if (const char *v = getenv("FM_OP_STEPS")) g->op_steps = std::max(1, atoi(v));
     const size_t n4 = sizeof(int32_t) * (size_t)g->HW, n1 = (size_t)g->HW;
     int32_t **planes[] = {&g->d.e, &g->d.h, &g->d.rR, &g->d.rL, &g->d.rD, &g->d.rU,
                           &g->d.rT, &g->d.rS, &g->d.cS, &g->d.dist, &g->d.inflow_h, &g->d.inflow_v};
@@ -1180,6 +1194,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     g->sms = sms;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pt_per_sm, pr_tile_kernel, PT_W * PT_TY, 0);
+    g->pt_per_sm = std::max(1, g->pt_per_sm);
     g->grid_blocks = (int)std::min<int64_t>((g->HW + 255) / 256, (int64_t)sms * 8);
     *out = g;
     return FM_OK;
