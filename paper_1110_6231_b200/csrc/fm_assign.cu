@@ -34,7 +34,10 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int ATHREADS = 512;            // 16 warps per CTA
+#ifndef FM_ATHREADS
+#define FM_ATHREADS 512
+#endif
+constexpr int ATHREADS = FM_ATHREADS;    // threads per CTA of the refine kernels
 constexpr int AWARPS = ATHREADS / 32;
 constexpr long long I64_MAX = 0x7fffffffffffffffLL;
 constexpr int LINF = 0x3fffffff;         // "unlabelled" in the price update
@@ -50,7 +53,13 @@ constexpr int C_PU_LAST = 10;            // price update: max label over active 
 constexpr int C_COUNT = 12;
 // ops[] slots
 constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXED = 4,
-              O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7;
+              O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7, O_TAIL_NS = 8, O_MULTI_NS = 9;
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct AssignDev {
     const int32_t *w;      // n x n weights (row x), FM_ABSENT_WEIGHT = no arc
@@ -204,13 +213,13 @@ __device__ void x_op(const AssignDev &a, int x, int32_t *ylist_next, int32_t *yc
     long long best = I64_MAX;
     int y = INT32_MAX;
     const int t = CTA_WIDE ? threadIdx.x : (threadIdx.x & 31);
+    const long long px = t == 0 ? __ldcg((const long long *)a.px + x) : 0;  // overlaps the scan
     row_partial(a, x, t, CTA_WIDE ? ATHREADS : 32, best, y);
     if (CTA_WIDE) cta_argmin(best, y); else warp_argmin(best, y);
     if (t == 0) {
         if (y == INT32_MAX) {
             atomicExch(a.cnt + C_INFEASIBLE, 1);  // active node with no residual arc
         } else {
-            const long long px = a.px[x];
             if (!(best < -px)) {                 // not admissible: p(x) <- -(best + eps)
                 a.px[x] = -(best + a.eps);
                 relabels++;
@@ -226,34 +235,108 @@ __device__ void x_op(const AssignDev &a, int x, int32_t *ylist_next, int32_t *yc
 }
 
 // Y op: while y holds excess, push a unit back to its cheapest incoming X,
-// relabelling y first when that reverse arc is not admissible.
+// relabelling y first when that reverse arc is not admissible.  One scan of
+// match[] gathers the incoming X (with their reverse part-reduced costs) into
+// shared memory; y's own relabels do not change their order, so the excess
+// units go back to the gathered candidates in increasing cost order without
+// rescanning.  More than YCAP incoming units falls back to one scan per unit.
+constexpr int YCAP = 64;
+
 template <bool CTA_WIDE>
 __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
                      unsigned long long &pushes, unsigned long long &relabels) {
+    __shared__ long long s_cv[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
+    __shared__ int s_cx[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
+    __shared__ int s_cn[CTA_WIDE ? 1 : AWARPS];
+    constexpr int CAP = CTA_WIDE ? 4 * YCAP : YCAP;
     const int t = CTA_WIDE ? threadIdx.x : (threadIdx.x & 31);
+    const int T = CTA_WIDE ? ATHREADS : 32;
+    const int slot = CTA_WIDE ? 0 : (threadIdx.x >> 5);
+    long long *cv = s_cv[slot];
+    int *cx = s_cx[slot];
     int ey = __ldcg(a.ey + y);
     long long py = __ldcg((const long long *)a.py + y);
-    while (ey > 0) {
-        long long bv = I64_MAX;
-        int bi = INT32_MAX;
-        ycand_partial(a, y, t, CTA_WIDE ? ATHREADS : 32, bv, bi);
-        if (CTA_WIDE) cta_argmin(bv, bi); else warp_argmin(bv, bi);
-        if (bi == INT32_MAX) {  // cannot happen for a consistent state
-            if (t == 0) atomicExch(a.cnt + C_INFEASIBLE, 2);
-            break;
-        }
-        if (t == 0) {
-            if (!(bv < -py)) {
-                py = -(bv + a.eps);
-                relabels++;
-                atomicAdd(a.cnt + C_RELABELS, 1);
+    if (ey <= 0) return;
+    // ---- gather
+    if (t == 0) s_cn[slot] = 0;
+    if (CTA_WIDE) __syncthreads(); else __syncwarp();
+    const int n = a.n;
+    const auto take = [&](int x) {
+        if (__ldcg(a.frozen + x)) return;
+        const long long v = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale - __ldcg((const long long *)a.px + x);
+        const int k = atomicAdd(&s_cn[slot], 1);
+        if (k < CAP) { cx[k] = x; cv[k] = v; }
+    };
+    if ((n & 3) == 0) {
+        const int n4 = n >> 2;
+        const int4 *m4 = reinterpret_cast<const int4 *>(a.match);
+        for (int j0 = t; j0 < n4; j0 += 4 * T) {
+            int4 mm[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = j0 + u * T;
+                mm[u] = j < n4 ? __ldcg(m4 + j) : make_int4(-1, -1, -1, -1);
             }
-            a.match[bi] = -1;
-            xlist_next[atomicAdd(xcnt_next, 1)] = bi;
-            pushes++;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int j = j0 + u * T;
+                if (mm[u].x == y) take(4 * j + 0);
+                if (mm[u].y == y) take(4 * j + 1);
+                if (mm[u].z == y) take(4 * j + 2);
+                if (mm[u].w == y) take(4 * j + 3);
+            }
         }
-        ey--;
-        if (CTA_WIDE) __syncthreads(); else __syncwarp();
+    } else {
+        for (int x = t; x < n; x += T)
+            if (__ldcg(a.match + x) == y) take(x);
+    }
+    if (CTA_WIDE) __syncthreads(); else __syncwarp();
+    const int cnt = s_cn[slot];
+    if (cnt > CAP) {
+        // ---- overflow: one scan per unit (the original scheme)
+        while (ey > 0) {
+            long long bv = I64_MAX;
+            int bi = INT32_MAX;
+            ycand_partial(a, y, t, T, bv, bi);
+            if (CTA_WIDE) cta_argmin(bv, bi); else warp_argmin(bv, bi);
+            if (bi == INT32_MAX) {
+                if (t == 0) atomicExch(a.cnt + C_INFEASIBLE, 2);
+                break;
+            }
+            if (t == 0) {
+                if (!(bv < -py)) { py = -(bv + a.eps); relabels++; atomicAdd(a.cnt + C_RELABELS, 1); }
+                a.match[bi] = -1;
+                xlist_next[atomicAdd(xcnt_next, 1)] = bi;
+                pushes++;
+            }
+            ey--;
+            if (CTA_WIDE) __syncthreads(); else __syncwarp();
+        }
+    } else {
+        // ---- push back to the cheapest gathered candidates, one per excess unit
+        while (ey > 0) {
+            long long bv = I64_MAX;
+            int bi = INT32_MAX, bk = -1;
+            for (int k = t; k < cnt; k += T)
+                if (cv[k] < bv || (cv[k] == bv && cx[k] < bi)) { bv = cv[k]; bi = cx[k]; bk = k; }
+            // argmin over (v, x); carry the buffer slot along with the index
+            long long v2 = bv;
+            int i2 = bi;
+            if (CTA_WIDE) cta_argmin(v2, i2); else warp_argmin(v2, i2);
+            if (i2 == INT32_MAX) {
+                if (t == 0) atomicExch(a.cnt + C_INFEASIBLE, 2);
+                break;
+            }
+            if (bi == i2 && bk >= 0) cv[bk] = I64_MAX;   // the owner lane retires the slot
+            if (t == 0) {
+                if (!(v2 < -py)) { py = -(v2 + a.eps); relabels++; atomicAdd(a.cnt + C_RELABELS, 1); }
+                a.match[i2] = -1;
+                xlist_next[atomicAdd(xcnt_next, 1)] = i2;
+                pushes++;
+            }
+            ey--;
+            if (CTA_WIDE) __syncthreads(); else __syncwarp();
+        }
     }
     if (t == 0) {
         a.py[y] = py;
@@ -315,9 +398,15 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
     const int gwarps = (gridDim.x * ATHREADS) >> 5;
     const int cwarp = threadIdx.x >> 5;
     unsigned long long pushes = 0, relabels = 0, rounds = 0, tail_rounds = 0, tail_ops = 0;
+    unsigned long long tail_ns = 0, multi_ns = 0, t_round = globaltimer();
     bool tail = false;
     int r = __ldcg(a.cnt + C_ROUND);
     for (;; r++) {
+        {
+            const unsigned long long now = globaltimer();
+            if (tail) tail_ns += now - t_round; else multi_ns += now - t_round;
+            t_round = now;
+        }
         const int b = r & 1, nb = b ^ 1;
         const int ny = __ldcg(a.cnt + C_Y0 + b);
         if (ny == 0 || __ldcg(a.cnt + C_INFEASIBLE)) {
@@ -396,6 +485,8 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
         atomicAdd(a.ops + O_ROUNDS, rounds);
         atomicAdd(a.ops + O_TAIL_ROUNDS, tail_rounds);
         atomicAdd(a.ops + O_TAIL_OPS, tail_ops);
+        atomicAdd(a.ops + O_TAIL_NS, tail_ns);
+        atomicAdd(a.ops + O_MULTI_NS, multi_ns);
     }
     (void)cwarp;
 }
@@ -643,7 +734,7 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
     FM_CHECK_CUDA(cudaMemsetAsync(d.frozen, 0, n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.frozen_in, 0, sizeof(int32_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.fixed, 0, sizeof(uint32_t) * (size_t)n * d.nw, s));
-    FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * 8, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * 16, s));
     FM_CHECK_CUDA(cudaMemsetAsync(A->acc, 0, sizeof(unsigned long long) * 4, s));
     weight_bound_kernel<<<A->sms * 4, 256, 0, s>>>(w, (int64_t)n * n, A->acc);
     if (flags & FM_ASSIGN_PRICE_UPDATE) {
@@ -723,7 +814,7 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
         A->st.launches++;
     }
     cudaEventRecord(t1, s);
-    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_ops, d.ops, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToHost, s));
+    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_ops, d.ops, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost, s));
     FM_CHECK_CUDA(cudaMemcpyAsync(A->h_acc, A->acc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     if (match_out) FM_CHECK_CUDA(cudaMemcpyAsync(match_out, d.match, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
     if (prices_out) {
@@ -745,6 +836,8 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
     A->st.reserved[1] = (int64_t)A->h_ops[O_PU];         // price updates
     A->st.reserved[2] = (int64_t)A->h_ops[O_PU_ITERS];   // Bellman-Ford iterations in them
     A->st.reserved[3] = (int64_t)A->h_ops[O_TAIL_OPS];   // ops done by the single-CTA tail
+    A->st.ms_cut = 1e-6 * (double)A->h_ops[O_TAIL_NS];   // time in single-CTA tail rounds
+    A->st.ms_d2h = 1e-6 * (double)A->h_ops[O_MULTI_NS];  // time in grid-wide rounds
     // algorithmic bytes: every op scans one weight row (4n) + n prices (8n); the
     // begin phase and arc fixing read the whole matrix once each per refine
     A->st.bytes_push = (A->st.pushes + A->st.relabels) * 12LL * n +
@@ -790,9 +883,9 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMalloc((void **)&A->pu.in_fy, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&A->pu.cnt, sizeof(int32_t) * 4) == cudaSuccess &&
               cudaMalloc((void **)&d.ly, sizeof(int32_t) * n) == cudaSuccess &&
-              cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * 8) == cudaSuccess &&
+              cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * 16) == cudaSuccess &&
               cudaMalloc((void **)&A->acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
-              cudaMallocHost((void **)&A->h_ops, sizeof(unsigned long long) * 8) == cudaSuccess &&
+              cudaMallocHost((void **)&A->h_ops, sizeof(unsigned long long) * 16) == cudaSuccess &&
               cudaMallocHost((void **)&A->h_acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
               cudaMallocHost((void **)&A->h_cnt, sizeof(int32_t) * C_COUNT) == cudaSuccess &&
               cudaStreamCreateWithFlags(&A->own_stream, cudaStreamNonBlocking) == cudaSuccess;
