@@ -171,6 +171,17 @@ int fm_grid_band_rows(fm_grid *g, int32_t direction /* 0 out, 1 in */, int32_t s
                       int32_t kind, int32_t *buf, int64_t *changed);
 int fm_grid_band_flow(fm_grid *g, int64_t *out);
 
+/* ---------------------------------------------------------- generic (CSR)
+ * hybrid_solve on an arbitrary FlowNetwork (maxflow_par.py:157-238): the arc-pair
+ * forward star of graph.py:43-84 as CSR (HOST arrays, copied in): ostart[n+1],
+ * oarc[m2] = out-arc slot ids per node in input order, head[m2], cap[m2] (reverse
+ * slots 0).  Outputs (HOST, any may be NULL): flow, cut[n] (1 = source side of the
+ * minimal min cut), final residuals res[m2] and excesses ex[n]. */
+int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const int64_t *ostart,
+                 const int32_t *oarc, const int32_t *head, const int32_t *cap,
+                 int32_t cycle_budget, int32_t flags, int64_t *flow_out, uint8_t *cut_out,
+                 int32_t *res_out, int64_t *ex_out, fm_stats *stats);
+
 /* ------------------------------------------------------------- assignment */
 typedef struct fm_assign fm_assign;
 

@@ -242,9 +242,9 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
     if cycle_budget < 1:
         raise ValueError(f"cycle_budget must be at least 1, got {cycle_budget}")
     if not isinstance(net, GridNetwork):
-        raise NotImplementedError(
-            "the B200 path solves 4-connected grid networks (GridNetwork); the generic "
-            "CSR lock-free kernel is a SURVEY.md 8f next row and there is no CPU fallback")
+        if observer is not None:
+            raise NotImplementedError("observer hooks are supported on GridNetwork solves")
+        return csr_solve(net, cycle_budget)
     started = time.perf_counter()
     solver = _solver_for(net.H, net.W, device)
     if observer is None:
@@ -278,6 +278,47 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
     return SolveReport(objective=int(flow), pushes=int(stats.get("pushes", 0)),
                        relabels=int(stats.get("relabels", 0)), rounds=int(stats.get("rounds", 0)),
                        elapsed=elapsed, cut=cut, stats=stats)
+
+
+def csr_arrays(net: FlowNetwork):
+    """(ostart, oarc, head, cap) of a FlowNetwork's arc-pair forward star
+    (graph.py:43-84): out-arc lists keep input order."""
+    n = net.node_count
+    head = np.ascontiguousarray(net.head, dtype=np.int32)
+    cap = np.ascontiguousarray(net.capacity, dtype=np.int32)
+    lens = np.fromiter((len(l) for l in net.out_arcs), dtype=np.int64, count=n)
+    ostart = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=ostart[1:])
+    oarc = np.fromiter((a for l in net.out_arcs for a in l), dtype=np.int32, count=int(ostart[-1]))
+    return ostart, oarc, head, cap
+
+
+def csr_solve(net: FlowNetwork, cycle_budget: int = DEFAULT_CYCLE_BUDGET, want_state: bool = False):
+    """Generic-graph lock-free push-relabel on the GPU (fm_csr.cu).  Returns a
+    SolveReport whose cut is a bool[node_count] (True = source side)."""
+    L = _lib.load()
+    _lib.require_device()
+    if net.source is None or net.sink is None:
+        raise ValueError("network has no source/sink")
+    started = time.perf_counter()
+    ostart, oarc, head, cap = csr_arrays(net)
+    n, m2 = net.node_count, len(head)
+    flow = ctypes.c_int64()
+    cut = np.zeros(n, np.uint8)
+    res = np.zeros(max(1, m2), np.int32) if want_state else None
+    ex = np.zeros(n, np.int64) if want_state else None
+    st = _lib.FmStats()
+    p = lambda a: _lib.ptr(a) if a is not None and a.size else None
+    rc = L.fm_csr_solve(n, int(net.source), int(net.sink), m2, _lib.ptr(ostart), p(oarc), p(head), p(cap),
+                        int(cycle_budget), 0, ctypes.byref(flow), _lib.ptr(cut), p(res), p(ex),
+                        ctypes.byref(st))
+    _lib.check(rc, "fm_csr_solve")
+    stats = st.as_dict()
+    if want_state:
+        stats["residual"], stats["excess"] = res[:m2], ex
+    return SolveReport(objective=int(flow.value), pushes=int(st.pushes), relabels=int(st.relabels),
+                       rounds=int(st.rounds), elapsed=time.perf_counter() - started, cut=cut.astype(bool),
+                       stats=stats)
 
 
 def min_cut(net: GridNetwork, report: SolveReport | None = None, **kw):

@@ -79,12 +79,18 @@ def test_grid_adapter_matches_oracle_and_reference_layout():
     assert net.capacity[1] == 0 and net.head[1] == net.tail[0]
 
 
-def test_non_grid_network_has_no_cpu_fallback():
+def test_non_grid_network_needs_the_device():
     net = fmb.build_network([(0, 1, 3), (1, 2, 4)], 3, 0, 2)
-    with pytest.raises(NotImplementedError, match="no CPU fallback"):
-        fmb.hybrid_solve(net)
     with pytest.raises(ValueError, match="worker_count"):
         fmb.hybrid_solve(net, worker_count=0)
+    from paper_1110_6231_b200.maxflow import csr_arrays
+
+    ostart, oarc, head, cap = csr_arrays(net)
+    assert ostart.tolist() == [0, 1, 3, 4] and oarc.tolist() == [0, 1, 2, 3]
+    assert head.tolist() == [1, 0, 2, 1] and cap.tolist() == [3, 0, 4, 0]
+    if not has_gpu() and os.path.exists(_lib.LIB_PATH):
+        with pytest.raises(RuntimeError, match="no CUDA device"):
+            fmb.hybrid_solve(net)
 
 
 def test_assignment_instance_validation():
