@@ -200,6 +200,16 @@ int fm_assign_solve_host(fm_assign *a, const int32_t *weights, int64_t alpha,
                          int32_t flags, int64_t *objective_out, int32_t *match_out,
                          int64_t *prices_out, fm_stats *stats);
 
+/* Stepwise solve, one refine at a time (solve_assignment's on_refine_end hook,
+ * assign_scaling.py:419-420,451-452).  begin copies HOST weights; refine runs one
+ * epsilon phase and reports the new epsilon and whether it was the last (eps == 1);
+ * state copies prices (2n), match (n) and the arc-fix bitmask (n * ceil(n/32)
+ * words, bit y of row x) to HOST buffers (any may be NULL). */
+int fm_assign_begin(fm_assign *a, const int32_t *weights, int64_t alpha, int32_t flags);
+int fm_assign_refine(fm_assign *a, int64_t *eps_out, int32_t *done_out);
+int fm_assign_state(fm_assign *a, int64_t *prices, int32_t *match, uint32_t *fixed,
+                    int64_t *objective_out, fm_stats *stats);
+
 #ifdef __cplusplus
 }
 #endif

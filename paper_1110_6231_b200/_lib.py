@@ -96,6 +96,9 @@ SIGNATURES = {
     "fm_assign_destroy": (None, [_vp]),
     "fm_assign_solve": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "fm_assign_solve_host": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),
+    "fm_assign_begin": (ctypes.c_int, [_vp, _vp, _i64, _i32]),
+    "fm_assign_refine": (ctypes.c_int, [_vp, _vp, _vp]),
+    "fm_assign_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

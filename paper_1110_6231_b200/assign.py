@@ -139,6 +139,104 @@ class AssignmentSolver:
         return int(obj.value), match, prices, self.last_stats
 
 
+    # ---- stepwise API (on_refine_end)
+    def begin(self, weights, alpha=DEFAULT_ALPHA, use_price_update=True, use_arc_fix=True, validate=False):
+        w = _check_weights(weights)
+        self._keep = w
+        _lib.check(_lib.load().fm_assign_begin(self._h, _lib.ptr(w), int(alpha),
+                                               self._flags(use_price_update, use_arc_fix, validate)),
+                   "fm_assign_begin")
+
+    def refine(self):
+        eps = ctypes.c_int64()
+        done = ctypes.c_int32()
+        _lib.check(_lib.load().fm_assign_refine(self._h, ctypes.byref(eps), ctypes.byref(done)), "fm_assign_refine")
+        return int(eps.value), bool(done.value)
+
+    def state(self):
+        n = self.n
+        prices = np.zeros(2 * n, np.int64)
+        match = np.zeros(n, np.int32)
+        fixed = np.zeros(n * ((n + 31) // 32), np.uint32)
+        obj = ctypes.c_int64()
+        st = _lib.FmStats()
+        _lib.check(_lib.load().fm_assign_state(self._h, _lib.ptr(prices), _lib.ptr(match), _lib.ptr(fixed),
+                                               ctypes.byref(obj), ctypes.byref(st)), "fm_assign_state")
+        self.last_stats = st.as_dict()
+        return prices, match, fixed.reshape(n, -1), int(obj.value)
+
+
+class _ResidualView:
+    """ResidualState-shaped view (graph.py:128-154) of the device state."""
+
+    def __init__(self, residual, excess, price):
+        self.residual = residual
+        self.excess = excess
+        self.height = [0] * len(excess)
+        self.price = price
+
+
+class ScalingView:
+    """ScalingState-shaped view (assign_scaling.py:102-117) handed to on_refine_end:
+    net is the reference's min-cost network (reduce_to_mincost, arcs in instance edge
+    order), state.residual / state.price / fixed describe the device state at the end
+    of the refine (all excesses are zero there)."""
+
+    def __init__(self, n, xs, ys, ws, instance, alpha, bound):
+        from .graph import FlowNetwork
+
+        self.n = n
+        self.instance = instance
+        self.alpha = alpha
+        self.scaled_cost_bound = bound
+        self.supplies = [1] * n + [-1] * n
+        net = FlowNetwork(2 * n, None, None)
+        for x, y, w in zip(xs.tolist(), ys.tolist(), ws.tolist()):
+            net.add_arc_pair(x, n + y, 1, -(w * (n + 1)))
+        self.net = net
+        self._xs, self._ys = xs, ys
+        self.epsilon = 1
+        self.state = None
+        self.fixed = []
+
+    def update(self, eps, prices, match, fixed_bits):
+        matched = match[self._xs] == self._ys
+        res = np.empty(2 * len(self._xs), np.int64)
+        res[0::2] = np.where(matched, 0, 1)
+        res[1::2] = 1 - res[0::2]
+        fx = ((fixed_bits[self._xs, self._ys >> 5] >> (self._ys & 31).astype(np.uint32)) & 1).astype(bool)
+        fixed = np.repeat(fx, 2)
+        self.epsilon = eps
+        self.state = _ResidualView(res.tolist(), [0] * (2 * self.n), prices.tolist())
+        self.fixed = fixed.tolist()
+
+
+def _solve_stepwise(inst, w, alpha, use_price_update, use_arc_fix, validate, on_refine_end, device):
+    n = w.shape[0]
+    solver = _solver_for(n, device)
+    started = time.perf_counter()
+    if isinstance(inst, AssignmentInstance) and inst.edges:
+        e = np.asarray(inst.edges, dtype=np.int64)
+        xs, ys, ws = e[:, 0], e[:, 1], e[:, 2]
+    else:
+        xs, ys = np.nonzero(w != _lib.FM_ABSENT_WEIGHT)
+        ws = w[xs, ys].astype(np.int64)
+    bound = int(np.abs(ws).max()) * (n + 1) if len(ws) else 0
+    view = ScalingView(n, xs, ys, ws, inst if isinstance(inst, AssignmentInstance) else None, alpha, bound)
+    solver.begin(w, alpha, use_price_update, use_arc_fix, validate)
+    while True:
+        eps, done = solver.refine()
+        prices, match, fixed, obj = solver.state()
+        view.update(eps, prices, match, fixed)
+        on_refine_end(view)
+        if done:
+            break
+    st = solver.last_stats
+    report = SolveReport(objective=obj, pushes=int(st["pushes"]), relabels=int(st["relabels"]),
+                         rounds=int(st["rounds"]), elapsed=time.perf_counter() - started, stats=st)
+    return report, match.tolist()
+
+
 _solvers: dict = {}
 
 
@@ -170,8 +268,14 @@ def solve_assignment(inst: AssignmentInstance, *, mode: str = "seq", worker_coun
         raise ValueError(f"worker_count must be at least 1, got {worker_count}")
     if cycle_budget < 1:
         raise ValueError(f"cycle_budget must be at least 1, got {cycle_budget}")
-    if on_refine_end is not None or observer is not None:
-        raise NotImplementedError("per-refine callbacks need the stepwise assignment API (next row)")
+    if observer is not None:
+        raise NotImplementedError("observer (per coordinator round) is not exposed by the device refine; "
+                                  "use on_refine_end")
+    if on_refine_end is not None:
+        w = inst.dense() if isinstance(inst, AssignmentInstance) else (
+            inst.detach().cpu().numpy() if hasattr(inst, "detach") else np.asarray(inst))
+        return _solve_stepwise(inst, _check_weights(w), alpha, use_price_update, use_arc_fix, validate,
+                               on_refine_end, device)
     started = time.perf_counter()
     if isinstance(inst, AssignmentInstance):
         n = inst.n

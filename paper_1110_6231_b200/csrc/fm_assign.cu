@@ -709,34 +709,39 @@ struct fm_assign {
     int coop_blocks = 0, pu_blocks = 0, sms = 0;
     PuDev pu{};
     int32_t *wt = nullptr;
-    cudaEvent_t ev[2] = {};
+    cudaEvent_t ev[4] = {};
     bool pu_pending = false;
+    // solve state (also drives the stepwise API)
+    long long alpha = 10, bound = 0, eps = 1, round_budget = 0;
+    int pu_threshold = 0, tail_threshold = 1;
+    int32_t flags = 0;
     fm_stats st{};
 };
 
 namespace {
 
-int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags,
-                        int64_t *objective_out, int32_t *match_out, int64_t *prices_out) {
+// make_scaling_state (assign_scaling.py:127-142): prices 0, eps0 = max(1, bound)
+int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     const int n = A->n;
     AssignDev &d = A->d;
     d.w = w;
     d.use_fix = (flags & FM_ASSIGN_ARC_FIX) ? 1 : 0;
+    A->alpha = alpha;
+    A->flags = flags;
     memset(&A->st, 0, sizeof(A->st));
     cudaStream_t s = A->stream;
-    cudaEvent_t t0, t1;
-    FM_CHECK_CUDA(cudaEventCreate(&t0));
-    FM_CHECK_CUDA(cudaEventCreate(&t1));
-    cudaEventRecord(t0, s);
-    // make_scaling_state (assign_scaling.py:127-142): prices 0, eps0 = max(1, bound)
+    cudaEventRecord(A->ev[2], s);
     FM_CHECK_CUDA(cudaMemsetAsync(d.px, 0, sizeof(int64_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.py, 0, sizeof(int64_t) * n, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(d.match, 0xff, sizeof(int32_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.frozen, 0, n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.frozen_in, 0, sizeof(int32_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.fixed, 0, sizeof(uint32_t) * (size_t)n * d.nw, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * 16, s));
     FM_CHECK_CUDA(cudaMemsetAsync(A->acc, 0, sizeof(unsigned long long) * 4, s));
     weight_bound_kernel<<<A->sms * 4, 256, 0, s>>>(w, (int64_t)n * n, A->acc);
+    FM_CHECK_LAUNCH();
+    A->st.launches++;
     if (flags & FM_ASSIGN_PRICE_UPDATE) {
         A->pu.wt = A->wt;
         transpose_kernel<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, s>>>(w, A->wt, n);
@@ -744,76 +749,86 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
         FM_CHECK_CUDA(cudaMemsetAsync(A->pu.cnt, 0, sizeof(int32_t) * 4, s));
         A->st.launches++;
     }
-    FM_CHECK_LAUNCH();
-    A->st.launches++;
     FM_CHECK_CUDA(cudaMemcpyAsync(A->h_acc, A->acc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     FM_CHECK_CUDA(cudaStreamSynchronize(s));
-    const long long bound = (long long)A->h_acc[0] * (long long)(n + 1);
+    A->bound = (long long)A->h_acc[0] * (long long)(n + 1);
     // _ops_budget (assign_scaling.py:374-377) = max(1e4, 40 n^2 m); every round does >= 1 op
     const double budget_d = std::max(1e4, 40.0 * n * (double)n * std::max<double>(1.0, (double)A->h_acc[2]));
-    const long long round_budget = budget_d > 4e18 ? (long long)4e18 : (long long)budget_d;
-    long long eps = std::max(1LL, bound);
-    const int tail_threshold = 1;
-    int pu_threshold = (flags & FM_ASSIGN_PRICE_UPDATE) ? std::max(64, n / 16) : 0;
-    if (const char *v = getenv("FM_PU_THRESHOLD")) if (pu_threshold) pu_threshold = atoi(v);
-    int tail_threshold_env = tail_threshold;
-    if (const char *v = getenv("FM_TAIL_THRESHOLD")) tail_threshold_env = atoi(v);
-    int rc = FM_OK;
+    A->round_budget = budget_d > 4e18 ? (long long)4e18 : (long long)budget_d;
+    A->eps = std::max(1LL, A->bound);
+    A->pu_threshold = (flags & FM_ASSIGN_PRICE_UPDATE) ? std::max(64, n / 16) : 0;
+    if (const char *v = getenv("FM_PU_THRESHOLD")) if (A->pu_threshold) A->pu_threshold = atoi(v);
+    A->tail_threshold = 1;
+    if (const char *v = getenv("FM_TAIL_THRESHOLD")) A->tail_threshold = atoi(v);
+    return FM_OK;
+}
+
+// one refine (assign_scaling.py:145-182 + assign_par.py:115-237): eps <- max(1, ceil(eps/alpha)),
+// begin_refine fused with the first X phase, lock-free rounds with price updates, arc fixing
+int assign_one_refine(fm_assign *A) {
+    const int n = A->n;
+    AssignDev &d = A->d;
+    cudaStream_t s = A->stream;
+    long long eps = std::max(1LL, (A->eps + A->alpha - 1) / A->alpha);   // -(-eps // alpha)
+    A->eps = eps;
+    d.eps = eps;
+    d.max_bucket = std::min<long long>(A->bound / eps + 2, LINF - 1);
+    FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * C_COUNT, s));
+    reset_excess_kernel<<<(n + 255) / 256, 256, 0, s>>>(d);
+    FM_CHECK_LAUNCH();
+    begin_refine_kernel<<<std::max(1, std::min((n + AWARPS - 1) / AWARPS, A->sms * 4)), ATHREADS, 0, s>>>(d);
+    FM_CHECK_LAUNCH();
+    A->st.launches += 2;
     for (;;) {
-        eps = std::max(1LL, (eps + alpha - 1) / alpha);   // -(-eps // alpha)
-        d.eps = eps;
-        d.max_bucket = std::min<long long>(bound / eps + 2, LINF - 1);
-        FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * C_COUNT, s));
-        reset_excess_kernel<<<(n + 255) / 256, 256, 0, s>>>(d);
-        FM_CHECK_LAUNCH();
-        begin_refine_kernel<<<std::max(1, std::min((n + AWARPS - 1) / AWARPS, A->sms * 4)), ATHREADS, 0, s>>>(d);
-        FM_CHECK_LAUNCH();
-        A->st.launches += 2;
-        for (;;) {
-            void *args[] = {(void *)&d, (void *)&tail_threshold_env, (void *)&round_budget, (void *)&pu_threshold};
-            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
-                                                      dim3(ATHREADS), args, 0, s));
-            A->st.launches++;
-            FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, d.cnt, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, s));
-            FM_CHECK_CUDA(cudaStreamSynchronize(s));
-            if (A->pu_pending) {
-                float ms = 0.f;
-                cudaEventElapsedTime(&ms, A->ev[0], A->ev[1]);
-                A->st.ms_bfs += ms;   // price-update kernels
-                A->pu_pending = false;
-            }
-            if (A->h_cnt[C_INFEASIBLE] || A->h_cnt[C_EXIT] != 1) break;
-            void *pargs[] = {(void *)&d, (void *)&A->pu};
-            cudaEventRecord(A->ev[0], s);
-            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->pu_blocks),
-                                                      dim3(ATHREADS), pargs, 0, s));
-            cudaEventRecord(A->ev[1], s);
-            A->st.launches++;
-            A->pu_pending = true;
+        void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold};
+        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
+                                                  dim3(ATHREADS), args, 0, s));
+        A->st.launches++;
+        FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, d.cnt, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, s));
+        FM_CHECK_CUDA(cudaStreamSynchronize(s));
+        if (A->pu_pending) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, A->ev[0], A->ev[1]);
+            A->st.ms_bfs += ms;   // price-update kernels
+            A->pu_pending = false;
         }
-        if (d.use_fix) {
-            arc_fix_kernel<<<std::max(1, std::min((n + 7) / 8, A->sms * 8)), 256, 0, s>>>(d);
-            FM_CHECK_LAUNCH();
-            A->st.launches++;
-        }
-        A->st.refines++;
-        if (A->h_cnt[C_INFEASIBLE]) {
-            const int why = A->h_cnt[C_INFEASIBLE];
-            rc = FM_INFEASIBLE;
-            fm_set_error(why == 1 ? "active node has no residual arc: instance admits no perfect matching"
-                         : why == 3 ? "operation budget exceeded; prices diverge, instance admits no perfect matching"
-                                    : "inconsistent Y excess during refine");
-            if (why == 2) rc = FM_CUDA_ERROR;
-            break;
-        }
-        if (eps == 1) break;
+        if (A->h_cnt[C_INFEASIBLE] || A->h_cnt[C_EXIT] != 1) break;
+        void *pargs[] = {(void *)&d, (void *)&A->pu};
+        cudaEventRecord(A->ev[0], s);
+        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->pu_blocks),
+                                                  dim3(ATHREADS), pargs, 0, s));
+        cudaEventRecord(A->ev[1], s);
+        A->st.launches++;
+        A->pu_pending = true;
     }
-    if (rc == FM_OK) {
-        objective_kernel<<<std::max(1, std::min((n + 255) / 256, A->sms * 2)), 256, 0, s>>>(w, d.match, n, A->acc + 1);
+    if (d.use_fix) {
+        arc_fix_kernel<<<std::max(1, std::min((n + 7) / 8, A->sms * 8)), 256, 0, s>>>(d);
         FM_CHECK_LAUNCH();
         A->st.launches++;
     }
-    cudaEventRecord(t1, s);
+    A->st.refines++;
+    if (A->h_cnt[C_INFEASIBLE]) {
+        const int why = A->h_cnt[C_INFEASIBLE];
+        fm_set_error(why == 1 ? "active node has no residual arc: instance admits no perfect matching"
+                     : why == 3 ? "operation budget exceeded; prices diverge, instance admits no perfect matching"
+                                : "inconsistent Y excess during refine");
+        return why == 2 ? FM_CUDA_ERROR : FM_INFEASIBLE;
+    }
+    return FM_OK;
+}
+
+// objective, counters and host copies (assign_scaling.py:456-466)
+int assign_finish(fm_assign *A, int rc, int64_t *objective_out, int32_t *match_out, int64_t *prices_out) {
+    const int n = A->n;
+    AssignDev &d = A->d;
+    cudaStream_t s = A->stream;
+    if (rc == FM_OK) {
+        FM_CHECK_CUDA(cudaMemsetAsync(A->acc + 1, 0, sizeof(unsigned long long), s));
+        objective_kernel<<<std::max(1, std::min((n + 255) / 256, A->sms * 2)), 256, 0, s>>>(d.w, d.match, n, A->acc + 1);
+        FM_CHECK_LAUNCH();
+        A->st.launches++;
+    }
+    cudaEventRecord(A->ev[3], s);
     FM_CHECK_CUDA(cudaMemcpyAsync(A->h_ops, d.ops, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost, s));
     FM_CHECK_CUDA(cudaMemcpyAsync(A->h_acc, A->acc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     if (match_out) FM_CHECK_CUDA(cudaMemcpyAsync(match_out, d.match, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
@@ -823,14 +838,12 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
     }
     FM_CHECK_CUDA(cudaStreamSynchronize(s));
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, t0, t1);
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
+    cudaEventElapsedTime(&ms, A->ev[2], A->ev[3]);
     A->st.ms_total = ms;
     A->st.ms_push = ms - A->st.ms_bfs;  // everything but the price updates
-    A->st.pushes = (int64_t)A->h_ops[0];
-    A->st.relabels = (int64_t)A->h_ops[1];
-    A->st.rounds = (int64_t)A->h_ops[2];
+    A->st.pushes = (int64_t)A->h_ops[O_PUSH];
+    A->st.relabels = (int64_t)A->h_ops[O_RELABEL];
+    A->st.rounds = (int64_t)A->h_ops[O_ROUNDS];
     A->st.pr_sweeps = (int64_t)A->h_ops[O_TAIL_ROUNDS];  // rounds run by the single-CTA tail
     A->st.reserved[0] = (int64_t)A->h_ops[O_FIXED];      // pairs fixed
     A->st.reserved[1] = (int64_t)A->h_ops[O_PU];         // price updates
@@ -844,6 +857,17 @@ int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t f
                        A->st.refines * (int64_t)n * n * 4 * (d.use_fix ? 2 : 1);
     if (rc == FM_OK && objective_out) *objective_out = (int64_t)A->h_acc[1];
     return rc;
+}
+
+int assign_solve_device(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags,
+                        int64_t *objective_out, int32_t *match_out, int64_t *prices_out) {
+    FM_TRY(assign_setup(A, w, alpha, flags));
+    int rc = FM_OK;
+    for (;;) {
+        rc = assign_one_refine(A);
+        if (rc != FM_OK || A->eps == 1) break;
+    }
+    return assign_finish(A, rc, objective_out, match_out, prices_out);
 }
 
 }  // namespace
@@ -895,8 +919,7 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
         return FM_CUDA_ERROR;
     }
     A->stream = A->own_stream;
-    cudaEventCreate(&A->ev[0]);
-    cudaEventCreate(&A->ev[1]);
+    for (auto &e : A->ev) cudaEventCreate(&e);
     cudaDeviceGetAttribute(&A->sms, cudaDevAttrMultiProcessorCount, device);
     int per_sm = 0;
     int per_sm2 = 0;
@@ -965,4 +988,40 @@ extern "C" int fm_assign_solve_host(fm_assign *A, const int32_t *weights, int64_
     A->st.ms_h2d = h2d;
     if (stats) *stats = A->st;
     return rc;
+}
+
+// ---- stepwise API (on_refine_end support): begin, one refine at a time, state export
+extern "C" int fm_assign_begin(fm_assign *A, const int32_t *weights, int64_t alpha, int32_t flags) {
+    if (!A || !weights || alpha < 2) {
+        fm_set_error("fm_assign_begin: invalid argument (alpha must be >= 2)");
+        return FM_INVALID_ARG;
+    }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    A->stream = A->own_stream;
+    const size_t bytes = sizeof(int32_t) * (size_t)A->n * A->n;
+    if (!A->in_w) FM_CHECK_CUDA(cudaMalloc((void **)&A->in_w, bytes));
+    FM_CHECK_CUDA(cudaMemcpyAsync(A->in_w, weights, bytes, cudaMemcpyHostToDevice, A->stream));
+    return assign_setup(A, A->in_w, alpha, flags);
+}
+
+extern "C" int fm_assign_refine(fm_assign *A, int64_t *eps_out, int32_t *done_out) {
+    if (!A) { fm_set_error("fm_assign_refine: null handle"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    const int rc = assign_one_refine(A);
+    if (eps_out) *eps_out = A->eps;
+    if (done_out) *done_out = A->eps == 1;
+    return rc;
+}
+
+// prices (2n: X then Y), match (n), fixed bitmask (n * ceil(n/32) words, row-major)
+extern "C" int fm_assign_state(fm_assign *A, int64_t *prices, int32_t *match, uint32_t *fixed,
+                               int64_t *objective_out, fm_stats *stats) {
+    if (!A) { fm_set_error("fm_assign_state: null handle"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    cudaStream_t s = A->stream;
+    if (fixed) FM_CHECK_CUDA(cudaMemcpyAsync(fixed, A->d.fixed, sizeof(uint32_t) * (size_t)A->n * A->nw,
+                                             cudaMemcpyDeviceToHost, s));
+    FM_TRY(assign_finish(A, FM_OK, objective_out, match, prices));
+    if (stats) *stats = A->st;
+    return FM_OK;
 }

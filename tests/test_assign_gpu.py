@@ -112,3 +112,45 @@ def test_device_tensor_input():
     rep_h, _ = fmb.solve_assignment(w)
     rep_d, m = fmb.solve_assignment(torch.from_numpy(w).cuda())
     assert rep_d.objective == rep_h.objective
+
+
+def _eps_optimal(view):
+    """graph.py:167-186 is_epsilon_optimal on the reference-shaped view."""
+    net, st = view.net, view.state
+    for a in range(net.arc_count):
+        if st.residual[a] <= 0 or view.fixed[a]:
+            continue
+        rc = net.cost[a] + st.price[net.tail[a]] - st.price[net.head[a]]
+        if rc < -view.epsilon:
+            return False
+    return True
+
+
+def test_epsilon_optimal_after_every_refine():
+    """test_assign_seq.py:210-229 on the GPU refine: the state handed to
+    on_refine_end is epsilon-optimal, the last refine runs at epsilon 1."""
+    import random
+
+    rng = random.Random(13)
+    for _ in range(12):
+        n = rng.randint(1, 9)
+        matrix = [[rng.randint(0, 100) for _ in range(n)] for _ in range(n)]
+        seen = []
+
+        def check(view):
+            seen.append(view.epsilon)
+            assert _eps_optimal(view)
+
+        rep, m = fmb.solve_assignment(fmb.AssignmentInstance.from_matrix(matrix), on_refine_end=check)
+        best = max(sum(matrix[x][p[x]] for x in range(n)) for p in itertools.permutations(range(n)))
+        assert seen and seen[-1] == 1 and rep.objective == best
+
+
+def test_on_refine_end_larger_and_heuristics_off():
+    w = G.assignment_reference(64, 10000, 64)
+    for pu, af in ((True, True), (False, False)):
+        eps = []
+        rep, m = fmb.solve_assignment(w, use_price_update=pu, use_arc_fix=af,
+                                      on_refine_end=lambda v: (eps.append(v.epsilon), _eps_optimal(v) or pytest.fail("not eps-optimal")))
+        want = oracle.assign(64, matrix=w)["objective"]
+        assert rep.objective == want and eps[-1] == 1 and eps == sorted(eps, reverse=True)
