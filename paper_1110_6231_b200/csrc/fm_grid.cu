@@ -226,7 +226,7 @@ constexpr int PT_ROWS = PT_H / PT_TY;
 #ifndef FM_PT_MINBLOCKS
 #define FM_PT_MINBLOCKS 4  // 32 registers: 4 CTAs (2048 threads) per SM
 #endif
-__global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(GridDev g, int k_local, int steps, int fused, int parity,
+__global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(GridDev g, int k_local, int steps, int fused, int vote_mask, int parity,
                                                                int32_t *processed,
                                                                unsigned long long *ops) {
     __shared__ int32_t s_e[PT_H][PT_W];
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(
                 pushes++;
             }
         }
-        if ((it & 3) == 3 && !__syncthreads_or(any)) break;
+        if ((it & vote_mask) == vote_mask && !__syncthreads_or(any)) break;
     }
     __syncthreads();
     bool act = false;
@@ -812,6 +812,7 @@ struct fm_grid {
     int pt_per_sm = 3;                   // resident pr_tile CTAs per SM (occupancy query)
     int op_steps = 1;                    // operations per pixel per pass (env FM_OP_STEPS)
     int op_fused = 0;                    // relabel then push in one operation (env FM_OP_FUSED)
+    int vote_mask = 7;                   // CTA activity vote every vote_mask+1 passes (env FM_VOTE)
     int bq_parity = 0;                   // parity of the next BFS / cut sweep
     int32_t *d_band = nullptr;           // band exchange: changed counter
     int k_local = 0;                     // tuning overrides (env FM_K_LOCAL / FM_BFS_INTERVAL)
@@ -1005,7 +1006,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
         for (int i = 0; i < batch; i++) {
             const int p = g->pq_parity;
             FM_TRY(tq_arm(g, g->d.pq, p));
-            pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10);
+            pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, g->vote_mask, p, g->flags + i, g->acc + 10);
             g->pq_parity ^= 1;
         }
         FM_CHECK_LAUNCH();
@@ -1155,6 +1156,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_RELABEL_DIV")) g->relabel_div = atoi(v);
     if (const char *v = getenv("FM_OP_STEPS")) g->op_steps = std::max(1, atoi(v));
     if (const char *v = getenv("FM_OP_FUSED")) g->op_fused = atoi(v);
+    if (const char *v = getenv("FM_VOTE")) g->vote_mask = std::max(1, atoi(v)) - 1;
     const size_t n4 = sizeof(int32_t) * (size_t)g->HW, n1 = (size_t)g->HW;
     int32_t **planes[] = {&g->d.e, &g->d.h, &g->d.rR, &g->d.rL, &g->d.rD, &g->d.rU,
                           &g->d.rT, &g->d.rS, &g->d.cS, &g->d.dist, &g->d.inflow_h, &g->d.inflow_v};
