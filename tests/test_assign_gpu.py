@@ -154,3 +154,29 @@ def test_on_refine_end_larger_and_heuristics_off():
                                       on_refine_end=lambda v: (eps.append(v.epsilon), _eps_optimal(v) or pytest.fail("not eps-optimal")))
         want = oracle.assign(64, matrix=w)["objective"]
         assert rep.objective == want and eps[-1] == 1 and eps == sorted(eps, reverse=True)
+
+
+@pytest.mark.parametrize("n,M", [(999, 100), (1023, 10000), (2048, 10000)])
+def test_scalar_path_and_n2048_vs_scipy(n, M):
+    """n not a multiple of 4 takes the scalar row-scan path; n = 2048 a mid size."""
+    from scipy.optimize import linear_sum_assignment
+
+    w = G.assignment_reference(n, M, n)
+    solver = fmb.AssignmentSolver(n)
+    obj, m, prices, _ = solver.solve_host(w, want_prices=True)
+    solver.close()
+    r, c = linear_sum_assignment(w.astype(np.int64), maximize=True)
+    assert obj == int(w[r, c].sum())
+    assert oracle.assign_certify_dense(w, m, prices)[0] == 0
+
+
+def test_sparse_mid_size_vs_scipy():
+    from scipy.optimize import linear_sum_assignment
+
+    w = G.assignment_reference(300, 1000, 7, density=0.05)
+    w64 = w.astype(np.int64)
+    big = np.where(w64 == -(2**31), -10**12, w64)
+    r, c = linear_sum_assignment(big, maximize=True)
+    rep, m = fmb.solve_assignment(w)
+    assert rep.objective == int(big[r, c].sum())
+    assert all(w[x, y] != -(2**31) for x, y in enumerate(m))

@@ -81,3 +81,30 @@ def test_multiprocess_bands_gloo_on_one_gpu():
         assert flow == want["value"]
         cut[r0:r1] = c.astype(bool)
     assert (cut == want["cut"]).all()
+
+
+@pytest.mark.parametrize("nb", [3, 8])
+def test_bands_segmentation_and_many_bands(nb):
+    caps = G.grid_segmentation(512, 384, 11)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    flow, cut, _ = B.solve_virtual_bands(caps, nb)
+    assert flow == want["value"] and (cut == want["cut"]).all()
+
+
+def test_bands_blocked_generator_rows():
+    # the multi-GPU bench builds each band from its own rows of the blocked generator
+    H, W = 600, 200
+    full = G.grid_random_blocked(H, W, 3)
+    want = oracle.grid_maxflow(*full, solver="seq")
+    spans = B.band_rows(H, 3)
+    bands = []
+    for k, (r0, r1) in enumerate(spans):
+        gt, gb = k > 0, k + 1 < len(spans)
+        rows = G.grid_random_rows(H, W, 3, r0 - gt, r1 + gb)
+        bc = B.band_caps_from_rows(rows, gt, gb)
+        assert all(np.array_equal(a, b) for a, b in zip(bc, B.band_caps(full, r0, r1, gt, gb)))
+        bands.append(B.Band(bc, gt, gb, H * W + 2))
+    co = B.BandedSolve(B.LocalTransport(bands), total_pixels=H * W)
+    assert co.run() == want["value"]
+    for b in bands:
+        b.close()

@@ -134,3 +134,29 @@ def test_certificate_at_config_sizes(shape, kind):
     solver.close()
     assert code == 0, code
     assert fl == cc == flow
+
+
+def test_segmentation_1024_vs_oracle():
+    caps = G.grid_segmentation(1024, 1024, 2048)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    rep = _solve(caps)
+    assert rep.objective == want["value"]
+    assert (rep.cut == want["cut"]).all()
+
+
+def test_certificate_at_4096():
+    caps = G.grid_random(4096, 4096, 4096)
+    solver = fmb.GridSolver(4096, 4096)
+    flow, cut, st = solver.solve_host(caps)
+    state = solver.export()
+    code, fl, cc, ns = oracle.grid_certify(caps, state, cut)
+    solver.close()
+    assert code == 0 and fl == cc == flow
+
+
+@pytest.mark.parametrize("H,W", [(1, 1), (1, 5), (7, 1), (33, 65)])
+def test_degenerate_shapes(H, W):
+    caps = G.grid_random(H, W, H * 100 + W)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    rep = _solve(caps)
+    assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
