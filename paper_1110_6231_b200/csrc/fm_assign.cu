@@ -53,7 +53,8 @@ constexpr int C_PU_LAST = 10;            // price update: max label over active 
 constexpr int C_COUNT = 12;
 // ops[] slots
 constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXED = 4,
-              O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7, O_TAIL_NS = 8, O_MULTI_NS = 9;
+              O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7, O_TAIL_NS = 8, O_MULTI_NS = 9,
+              O_PH_Y = 10, O_PH_SYNC1 = 11, O_PH_X = 12, O_PH_SYNC2 = 13;  // multi-round phase ns (CTA 0)
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -70,6 +71,7 @@ struct AssignDev {
     uint8_t *frozen;       // frozen[x]: x's matched arc is fixed (its flow never changes)
     int32_t *frozen_in;    // frozen_in[y]: number of frozen matches into y
     int32_t *lx, *ly;      // price-update labels
+    int32_t *ybcnt, *ybuf; // per-Y buckets of incoming X (YCAP slots each) for long Y lists
     int32_t *xlist[2], *ylist[2];
     int32_t *cnt;
     unsigned long long *ops;
@@ -77,14 +79,10 @@ struct AssignDev {
     int64_t scale;         // n + 1
     int64_t eps;
     int64_t max_bucket;    // scaled_cost_bound / eps + 2 (assign_scaling.py:232)
+    int32_t pu_cap0;       // first label cap of the price update (0 = 8)
     int use_fix;
 };
 
-__device__ __forceinline__ long long floordiv(long long a, long long b) {
-    long long q = a / b;
-    if ((a % b != 0) && ((a < 0) != (b < 0))) q--;
-    return q;
-}
 
 // (value, index) min with the lower index winning ties (first arc in the
 // reference's out-arc order wins, assign_par.py:84-90)
@@ -240,7 +238,8 @@ __device__ void x_op(const AssignDev &a, int x, int32_t *ylist_next, int32_t *yc
 // shared memory; y's own relabels do not change their order, so the excess
 // units go back to the gathered candidates in increasing cost order without
 // rescanning.  More than YCAP incoming units falls back to one scan per unit.
-constexpr int YCAP = 64;
+constexpr int YCAP = 64;                // candidates gathered per Y op in shared memory
+constexpr int YBUCKET = 256;            // per-Y bucket slots for long Y lists (= YB_CAP)
 
 template <bool CTA_WIDE>
 __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
@@ -319,7 +318,6 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
             int bi = INT32_MAX, bk = -1;
             for (int k = t; k < cnt; k += T)
                 if (cv[k] < bv || (cv[k] == bv && cx[k] < bi)) { bv = cv[k]; bi = cx[k]; bk = k; }
-            // argmin over (v, x); carry the buffer slot along with the index
             long long v2 = bv;
             int i2 = bi;
             if (CTA_WIDE) cta_argmin(v2, i2); else warp_argmin(v2, i2);
@@ -343,6 +341,97 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
         a.ey[y] = ey;
     }
     if (CTA_WIDE) __syncthreads(); else __syncwarp();
+}
+
+// Batch push-back of a Y holding ey excess units over its cnt incoming candidates
+// (v, x), v = reverse part-reduced cost: the units go back to the ey cheapest
+// candidates in increasing (v, x) order -- exactly the sequence of one-unit Y ops,
+// since y's own relabels never reorder the candidates.  Each lane ranks its
+// candidates against all others, the ranked costs are laid out in shared memory,
+// lane 0 replays the relabel sequence (p(y) <- -(v + eps) whenever the next arc is
+// not admissible) and the whole batch is appended with one list reservation.
+constexpr int YB_PER_LANE = 8;               // up to 256 candidates per warp
+constexpr int YB_CAP = 32 * YB_PER_LANE;
+
+__device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, int cnt,
+                             const long long (&v)[YB_PER_LANE], const int (&xs)[YB_PER_LANE],
+                             long long *s_sorted, int32_t *xlist_next, int32_t *xcnt_next,
+                             unsigned long long &pushes, unsigned long long &relabels) {
+    const int lane = threadIdx.x & 31;
+    int rank[YB_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < YB_PER_LANE; k++) rank[k] = 0;
+    for (int src = 0; src < 32; src++) {
+#pragma unroll
+        for (int j = 0; j < YB_PER_LANE; j++) {
+            const long long ov = __shfl_sync(0xffffffffu, v[j], src);
+            const int ox = __shfl_sync(0xffffffffu, xs[j], src);
+            if (ox == INT32_MAX) continue;
+#pragma unroll
+            for (int k = 0; k < YB_PER_LANE; k++)
+                if (ov < v[k] || (ov == v[k] && ox < xs[k])) rank[k]++;
+        }
+    }
+    int base = 0;
+    if (lane == 0) base = atomicAdd(xcnt_next, ey);
+    base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+    for (int k = 0; k < YB_PER_LANE; k++) {
+        if (xs[k] != INT32_MAX && rank[k] < ey) {
+            s_sorted[rank[k]] = v[k];
+            a.match[xs[k]] = -1;
+            xlist_next[base + rank[k]] = xs[k];
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        unsigned long long rl = 0;
+        for (int k = 0; k < ey; k++) {
+            const long long vk = s_sorted[k];
+            if (!(vk < -py)) { py = -(vk + a.eps); rl++; }
+        }
+        relabels += rl;
+        pushes += ey;
+        if (rl) atomicAdd(a.cnt + C_RELABELS, (int)rl);
+        a.py[y] = py;
+        a.ey[y] = 0;
+    }
+    __syncwarp();
+    (void)cnt;
+}
+
+// Y op over a pre-bucketed candidate list (long Y lists): the incoming X of y were
+// collected once per phase into ybuf[y*YCAP ..]; one warp per y.
+__device__ void y_op_bucketed(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
+                              unsigned long long &pushes, unsigned long long &relabels,
+                              long long *s_sorted) {
+    const int lane = threadIdx.x & 31;
+    const int cnt = __ldcg(a.ybcnt + y);
+    const int ey = __ldcg(a.ey + y);
+    if (cnt > YBUCKET || ey >= cnt) {       // bucket overflow (or inconsistent): scan match[] instead
+        y_op<false>(a, y, xlist_next, xcnt_next, pushes, relabels);
+        if (lane == 0) a.ybcnt[y] = 0;
+        __syncwarp();
+        return;
+    }
+    const long long py = __ldcg((const long long *)a.py + y);
+    const int n = a.n;
+    long long v[YB_PER_LANE];
+    int xs[YB_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < YB_PER_LANE; k++) {
+        const int i = lane + 32 * k;
+        v[k] = I64_MAX;
+        xs[k] = INT32_MAX;
+        if (i < cnt) {
+            const int x = __ldcg(a.ybuf + (size_t)y * YBUCKET + i);
+            xs[k] = x;
+            v[k] = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale - __ldcg((const long long *)a.px + x);
+        }
+    }
+    if (ey > 0) y_batch_warp(a, y, ey, py, cnt, v, xs, s_sorted, xlist_next, xcnt_next, pushes, relabels);
+    if (lane == 0) a.ybcnt[y] = 0;
+    __syncwarp();
 }
 
 // begin_refine (assign_scaling.py:145-182) fused with the first X phase: drop
@@ -399,6 +488,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
     const int cwarp = threadIdx.x >> 5;
     unsigned long long pushes = 0, relabels = 0, rounds = 0, tail_rounds = 0, tail_ops = 0;
     unsigned long long tail_ns = 0, multi_ns = 0, t_round = globaltimer();
+    __shared__ long long s_sorted[AWARPS][YB_CAP];
     bool tail = false;
     int r = __ldcg(a.cnt + C_ROUND);
     for (;; r++) {
@@ -457,14 +547,28 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
         } else {
             // a list no longer than the grid gets one CTA per node (one L2 round trip
             // per row scan); longer lists get one warp per node
+            const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
+            unsigned long long t0 = timer ? globaltimer() : 0, t1 = 0;
             if (ny <= (int)gridDim.x) {
                 for (int i = blockIdx.x; i < ny; i += gridDim.x)
                     y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
             } else {
+                // long list: bucket every incoming X by its Y in one pass over match[]
+                const int gtid = blockIdx.x * ATHREADS + threadIdx.x, gthr = gridDim.x * ATHREADS;
+                for (int x = gtid; x < a.n; x += gthr) {
+                    const int y = __ldcg(a.match + x);
+                    if (y < 0 || __ldcg(a.frozen + x) || __ldcg(a.ey + y) <= 0) continue;
+                    const int k = atomicAdd(a.ybcnt + y, 1);
+                    if (k < YBUCKET) a.ybuf[(size_t)y * YBUCKET + k] = x;
+                }
+                grid.sync();
                 for (int i = gwarp; i < ny; i += gwarps)
-                    y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+                    y_op_bucketed(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels,
+                                  s_sorted[threadIdx.x >> 5]);
             }
+            if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_Y, t1 - t0); t0 = t1; }
             grid.sync();
+            if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC1, t1 - t0); t0 = t1; }
             const int nx = __ldcg(a.cnt + C_X0 + b);
             if (nx <= (int)gridDim.x) {
                 for (int i = blockIdx.x; i < nx; i += gridDim.x)
@@ -473,7 +577,9 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
                 for (int i = gwarp; i < nx; i += gwarps)
                     x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
             }
+            if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_X, t1 - t0); t0 = t1; }
             grid.sync();
+            if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC2, t1 - t0); }
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_ROUND] = r;
@@ -522,81 +628,111 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     const int tid = blockIdx.x * ATHREADS + threadIdx.x, nthr = gridDim.x * ATHREADS;
     const int lane = threadIdx.x & 31;
     const double inv_eps = 1.0 / (double)a.eps;
-    if (tid == 0) a.cnt[C_PU_LAST] = 0;  // read by every thread after the last barrier
+    // Labels are only needed up to last + 1 (last = the largest label of an active
+    // node): explore with a label cap, and widen it (x8) only if some active node is
+    // still unlabelled.  Under a cap every node whose true label is <= cap gets its
+    // exact label (labels never decrease along a shortest path), which is all the
+    // final min(label, last + 1) needs.
+    long long cap = min((long long)a.max_bucket, (long long)(a.pu_cap0 > 0 ? a.pu_cap0 : 8));
+    int it_total = 0;
+    __shared__ int s_ly;
+    __shared__ long long s_py;
+    for (;;) {
+    if (tid == 0) { a.cnt[C_PU_LAST] = 0; a.cnt[C_PU_CHG] = 0; }
     for (int v = tid; v < n; v += nthr) {
         a.lx[v] = LINF;
-        f.in_fx[v] = 0;
         if (__ldcg(a.ey + v) < 0) {
             a.ly[v] = 0;
             f.in_fy[v] = 1;
-            f.fy[0][atomicAdd(f.cnt + 0, 1)] = v;
+            f.fy[0][atomicAdd(f.cnt + 0, 1)] = v;   // iteration 0's frontier (counter 0 of 3)
         } else {
             a.ly[v] = LINF;
             f.in_fy[v] = 0;
         }
     }
     grid.sync();
+    // One barrier per iteration: the Y step is folded into the X step -- whenever
+    // l(x) drops, x's matched reverse arc is relaxed into its Y right away (chaotic
+    // relaxation reaches the same fixpoint).  Frontier counters are triple-buffered so
+    // the counter of iteration it+2 can be zeroed during iteration it.
     int it = 0;
     for (;; it++) {
         const int b = it & 1, nb = b ^ 1;
-        const int ny = __ldcg(f.cnt + b);
+        const int ny = __ldcg(f.cnt + it % 3);
         if (ny == 0) break;
-        if (tid == 0) { f.cnt[nb] = 0; f.cnt[2 + nb] = 0; }
-        // X step: for y in the frontier, l(x) <- min(l(x), l(y) + len(x -> y))
+        if (tid == 0) f.cnt[(it + 2) % 3] = 0;
         for (int i = blockIdx.x; i < ny; i += gridDim.x) {
             const int y = __ldcg(f.fy[b] + i);
-            if (threadIdx.x == 0) f.in_fy[y] = 0;
-            const int lyv = __ldcg(a.ly + y);
-            const long long pyv = __ldcg((const long long *)a.py + y);
+            if (threadIdx.x == 0) {
+                f.in_fy[y] = 0;          // clear before reading l(y): a later drop re-queues y
+                __threadfence();
+                s_ly = __ldcg(a.ly + y);
+                s_py = __ldcg((const long long *)a.py + y);
+            }
+            __syncthreads();
+            const int lyv = s_ly;
+            const long long pyv = s_py;
             const int32_t *col = f.wt + (size_t)y * n;
             for (int x = threadIdx.x; x < n; x += ATHREADS) {
                 const int wv = __ldg(col + x);
                 if (wv == FM_ABSENT_WEIGHT) continue;
                 const int lxv = __ldcg(a.lx + x);
                 if (lyv >= lxv) continue;                              // cannot improve (len >= 0)
-                if (__ldcg(a.match + x) == y) continue;               // flow arc: not residual forward
+                const int mx = __ldcg(a.match + x);
+                if (mx == y) continue;                                 // flow arc: not residual forward
                 if (a.use_fix && ((__ldg(a.fixed + (size_t)x * a.nw + (y >> 5)) >> (y & 31)) & 1u)) continue;
-                const long long rc = -(long long)wv * a.scale + __ldcg((const long long *)a.px + x) - pyv;
+                const long long px = __ldcg((const long long *)a.px + x);
+                const long long rc = -(long long)wv * a.scale + px - pyv;
                 long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
                 if (len < 0) len = 0;
                 const long long cand = (long long)lyv + len;
-                if (cand > a.max_bucket || cand >= lxv) continue;
+                if (cand > cap || cand >= lxv) continue;
                 const int old = atomicMin(a.lx + x, (int)cand);
-                if ((int)cand < old && atomicExch(f.in_fx + x, 1) == 0)
-                    f.fx[b][atomicAdd(f.cnt + 2 + b, 1)] = x;
+                if ((int)cand >= old || mx < 0 || __ldcg(a.frozen + x)) continue;
+                // l(x) dropped: relax x's unit arc y2 -> x (reverse of the matched arc)
+                const long long rc2 = (long long)__ldg(a.w + (size_t)x * n + mx) * a.scale - px +
+                                      __ldcg((const long long *)a.py + mx);
+                long long len2 = floordiv_eps(rc2, a.eps, inv_eps) + 1;
+                if (len2 < 0) len2 = 0;
+                const long long cand2 = cand + len2;
+                if (cand2 > cap) continue;
+                const int old2 = atomicMin(a.ly + mx, (int)cand2);
+                if ((int)cand2 < old2) {
+                    __threadfence();
+                    if (atomicExch(f.in_fy + mx, 1) == 0) f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;
+                }
             }
-        }
-        grid.sync();
-        // Y step: for x in the frontier with a (non-frozen) unit on x -> y,
-        // l(y) <- min(l(y), l(x) + len(y -> x))
-        const int nx = __ldcg(f.cnt + 2 + b);
-        for (int i = tid; i < nx; i += nthr) {
-            const int x = __ldcg(f.fx[b] + i);
-            f.in_fx[x] = 0;
-            const int y = __ldcg(a.match + x);
-            if (y < 0 || __ldcg(a.frozen + x)) continue;
-            const long long rc = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale -
-                                 __ldcg((const long long *)a.px + x) + __ldcg((const long long *)a.py + y);
-            long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
-            if (len < 0) len = 0;
-            const long long cand = (long long)__ldcg(a.lx + x) + len;
-            if (cand > a.max_bucket) continue;
-            const int old = atomicMin(a.ly + y, (int)cand);
-            if ((int)cand < old && atomicExch(f.in_fy + y, 1) == 0)
-                f.fy[nb][atomicAdd(f.cnt + nb, 1)] = y;
+            __syncthreads();
         }
         grid.sync();
     }
-    // last = max label over active nodes (unmatched X, Y with positive excess)
-    int last = 0;
+    it_total += it + 1;
+    // last = max label over active nodes (unmatched X, Y with positive excess);
+    // an active node left unlabelled under the cap asks for a wider cap
+    int last = 0, missing = 0;
     for (int v = tid; v < n; v += nthr) {
-        if (__ldcg(a.match + v) < 0 && !__ldcg(a.frozen + v)) last = max(last, min(__ldcg(a.lx + v), LINF));
-        if (__ldcg(a.ey + v) > 0) last = max(last, min(__ldcg(a.ly + v), LINF));
+        if (__ldcg(a.match + v) < 0 && !__ldcg(a.frozen + v)) {
+            const int l = __ldcg(a.lx + v);
+            if (l >= LINF) missing = 1; else last = max(last, l);
+        }
+        if (__ldcg(a.ey + v) > 0) {
+            const int l = __ldcg(a.ly + v);
+            if (l >= LINF) missing = 1; else last = max(last, l);
+        }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+    for (int o = 16; o > 0; o >>= 1) {
+        last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+        missing |= __shfl_xor_sync(0xffffffffu, missing, o);
+    }
     if (lane == 0 && last) atomicMax(a.cnt + C_PU_LAST, last);
+    if (lane == 0 && missing) atomicOr(a.cnt + C_PU_CHG, 1);
     grid.sync();
+    if (!__ldcg(a.cnt + C_PU_CHG) || cap >= a.max_bucket) break;
+    cap = min(cap * 8, (long long)a.max_bucket);
+    if (tid == 0) { f.cnt[0] = f.cnt[1] = f.cnt[2] = 0; }
+    grid.sync();
+    }  // cap loop
     const long long K = min((long long)__ldcg(a.cnt + C_PU_LAST), (long long)a.max_bucket) + 1;
     for (int v = tid; v < n; v += nthr) {
         a.px[v] -= a.eps * min((long long)a.lx[v], K);
@@ -606,7 +742,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
         a.cnt[C_RELABELS] = 0;
         f.cnt[0] = f.cnt[1] = f.cnt[2] = f.cnt[3] = 0;
         atomicAdd(a.ops + O_PU, 1ull);
-        atomicAdd(a.ops + O_PU_ITERS, (unsigned long long)(it + 1));
+        atomicAdd(a.ops + O_PU_ITERS, (unsigned long long)it_total);
     }
 }
 
@@ -736,6 +872,7 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     FM_CHECK_CUDA(cudaMemsetAsync(d.match, 0xff, sizeof(int32_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.frozen, 0, n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.frozen_in, 0, sizeof(int32_t) * n, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(d.ybcnt, 0, sizeof(int32_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.fixed, 0, sizeof(uint32_t) * (size_t)n * d.nw, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * 16, s));
     FM_CHECK_CUDA(cudaMemsetAsync(A->acc, 0, sizeof(unsigned long long) * 4, s));
@@ -760,6 +897,8 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     if (const char *v = getenv("FM_PU_THRESHOLD")) if (A->pu_threshold) A->pu_threshold = atoi(v);
     A->tail_threshold = 1;
     if (const char *v = getenv("FM_TAIL_THRESHOLD")) A->tail_threshold = atoi(v);
+    d.pu_cap0 = 256;
+    if (const char *v = getenv("FM_PU_CAP")) d.pu_cap0 = atoi(v);
     return FM_OK;
 }
 
@@ -851,6 +990,9 @@ int assign_finish(fm_assign *A, int rc, int64_t *objective_out, int32_t *match_o
     A->st.reserved[3] = (int64_t)A->h_ops[O_TAIL_OPS];   // ops done by the single-CTA tail
     A->st.ms_cut = 1e-6 * (double)A->h_ops[O_TAIL_NS];   // time in single-CTA tail rounds
     A->st.ms_d2h = 1e-6 * (double)A->h_ops[O_MULTI_NS];  // time in grid-wide rounds
+    A->st.ms_pr_kern = 1e-6 * (double)A->h_ops[O_PH_Y];  // CTA 0's Y phases in grid-wide rounds
+    A->st.ms_bfs_kern = 1e-6 * (double)A->h_ops[O_PH_X]; // CTA 0's X phases in grid-wide rounds
+    A->st.bytes_bfs = (int64_t)(A->h_ops[O_PH_SYNC1] + A->h_ops[O_PH_SYNC2]);  // ns in grid barriers
     // algorithmic bytes: every op scans one weight row (4n) + n prices (8n); the
     // begin phase and arc fixing read the whole matrix once each per refine
     A->st.bytes_push = (A->st.pushes + A->st.relabels) * 12LL * n +
@@ -898,6 +1040,8 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMalloc((void **)&d.ylist[1], sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.cnt, sizeof(int32_t) * C_COUNT) == cudaSuccess &&
               cudaMalloc((void **)&d.lx, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&d.ybcnt, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&d.ybuf, sizeof(int32_t) * (size_t)n * YBUCKET) == cudaSuccess &&
               cudaMalloc((void **)&A->wt, sizeof(int32_t) * (size_t)n * n) == cudaSuccess &&
               cudaMalloc((void **)&A->pu.fy[0], sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&A->pu.fy[1], sizeof(int32_t) * n) == cudaSuccess &&
@@ -936,7 +1080,7 @@ extern "C" void fm_assign_destroy(fm_assign *A) {
     cudaSetDevice(A->device);
     void *dev[] = {A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.frozen, A->d.frozen_in,
                    A->d.xlist[0], A->d.xlist[1], A->d.ylist[0], A->d.ylist[1], A->d.cnt, A->d.ops,
-                   A->d.lx, A->d.ly, A->wt, A->pu.fy[0], A->pu.fy[1], A->pu.fx[0], A->pu.fx[1],
+                   A->d.lx, A->d.ly, A->d.ybcnt, A->d.ybuf, A->wt, A->pu.fy[0], A->pu.fy[1], A->pu.fx[0], A->pu.fx[1],
                    A->pu.in_fx, A->pu.in_fy, A->pu.cnt,
                    A->acc, A->in_w};
     for (void *p : dev) if (p) cudaFree(p);
