@@ -68,6 +68,11 @@ struct GridDev {
     // shipped to the owner band; their h / dist / cut / residual toward us are
     // imported from the owner.
     int32_t ghost_top, ghost_bot;
+    // local relabel (tail rounds): tiles touched by pushes since the last relabel, and
+    // the region R (touched tiles dilated by a margin) a local relabel recomputes;
+    // region == nullptr means "global"
+    uint8_t *touched;
+    const uint8_t *region;
     int32_t H, W;
     int32_t V;      // node count |V| = H*W + 2 (the source's height)
     int32_t INF;    // "unreached" distance sentinel (== V)
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(
                     const int nt = (dir == 0) ? tile + 1 : (dir == 1) ? tile - 1
                                  : (dir == 2) ? tile + g.ntx : tile - g.ntx;
                     tq_push(g.pq, parity ^ 1, nt);
+                    g.touched[nt] = 1;
                 }
                 pushes++;
             }
@@ -385,6 +391,7 @@ __global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(
     const int any_act = __syncthreads_or(act);
     if (tx == 0 && ty == 0) {
         if (any_act) tq_push(g.pq, parity ^ 1, tile);
+        g.touched[tile] = 1;
         atomicAdd(processed, 1);
     }
     }  // tile loop
@@ -483,10 +490,11 @@ __global__ void bfs_init_kernel(GridDev g) {
 // changes nothing.
 __device__ __forceinline__ void flag_changed_borders(const GridDev &g, int tile, int tyi, int txi,
                                                      int bt, int bb, int bl, int br, int parity) {
-    if (bt && tyi > 0) tq_push(g.bq, parity, tile - g.ntx);
-    if (bb && tyi + 1 < g.nty) tq_push(g.bq, parity, tile + g.ntx);
-    if (bl && txi > 0) tq_push(g.bq, parity, tile - 1);
-    if (br && txi + 1 < g.ntx) tq_push(g.bq, parity, tile + 1);
+    const auto in = [&](int t) { return !g.region || g.region[t]; };  // local relabel stays in R
+    if (bt && tyi > 0 && in(tile - g.ntx)) tq_push(g.bq, parity, tile - g.ntx);
+    if (bb && tyi + 1 < g.nty && in(tile + g.ntx)) tq_push(g.bq, parity, tile + g.ntx);
+    if (bl && txi > 0 && in(tile - 1)) tq_push(g.bq, parity, tile - 1);
+    if (br && txi + 1 < g.ntx && in(tile + 1)) tq_push(g.bq, parity, tile + 1);
 }
 
 __global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int parity, int all_tiles,
@@ -562,6 +570,93 @@ __global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int parity, in
         }
     }
     }  // tile loop
+}
+
+// ----------------------------------------------------------------------------
+// Local relabel (tail rounds).  R = tiles touched since the last relabel, dilated by
+// `margin` tiles.  Outside R nothing moved, so dist[] there still holds the labels of
+// the last relabel (= h for reached pixels, INF for written-off ones); distances only
+// grow, so those are valid lower bounds, and relaxing R against them as frozen values
+// gives every pixel of R a valid label (exact when its shortest path stays in R or
+// crosses pixels whose distance did not change).  A pixel of R left at INF has no
+// residual path to t at all -- every path leaving R meets a pixel already unreachable --
+// so the gap relabel and the write-off stay exact.
+// ----------------------------------------------------------------------------
+__global__ void region_build_kernel(GridDev g, uint8_t *region, int margin, int32_t *count) {
+    const int nt = g.ntx * g.nty;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+        const int ty = t / g.ntx, tx = t - ty * g.ntx;
+        bool in = false;
+        for (int dy = -margin; dy <= margin && !in; dy++) {
+            const int yy = ty + dy;
+            if (yy < 0 || yy >= g.nty) continue;
+            for (int dx = -margin; dx <= margin; dx++) {
+                const int xx = tx + dx;
+                if (xx >= 0 && xx < g.ntx && g.touched[yy * g.ntx + xx]) { in = true; break; }
+            }
+        }
+        region[t] = in ? 1 : 0;
+        if (in) {
+            g.bq.flag[0][t] = 1;
+            g.bq.list[0][atomicAdd(g.bq.cnt + 0, 1)] = t;
+            atomicAdd(count, 1);
+        }
+    }
+}
+
+// residual masks and seeds for the pixels of R only (one CTA per listed tile)
+__global__ void bfs_init_local_kernel(GridDev g) {
+    const int n = __ldcg(g.bq.cnt + 0);
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const int tile = g.bq.list[0][i];
+        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+        for (int k = threadIdx.x; k < TILE_W * TILE_H; k += blockDim.x) {
+            const int r = tyi * TILE_H + k / TILE_W, c = txi * TILE_W + k % TILE_W;
+            if (r >= g.H || c >= g.W) continue;
+            const int64_t p = (int64_t)r * g.W + c;
+            uint8_t m = 0;
+            if (c + 1 < g.W && g.rR[p] > 0) m |= M_R;
+            if (c > 0 && g.rL[p] > 0) m |= M_L;
+            if (r + 1 < g.H && g.rD[p] > 0) m |= M_D;
+            if (r > 0 && g.rU[p] > 0) m |= M_U;
+            if (g.rT[p] > 0) m |= M_T;
+            if (is_ghost_row(g, r)) m = 0;
+            g.mask[p] = m;
+            g.dist[p] = (m & M_T) ? 1 : g.INF;
+        }
+    }
+}
+
+// gap + marking + active tiles over R only (active pixels only ever live in R)
+__global__ void bfs_finalize_local_kernel(GridDev g, const int32_t *list, int n,
+                                          unsigned long long *acc) {
+    long long active = 0, mex = 0;
+    int32_t lvl = 0;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const int tile = list[i];
+        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+        bool act_tile = false;
+        for (int k = threadIdx.x; k < TILE_W * TILE_H; k += blockDim.x) {
+            const int r = tyi * TILE_H + k / TILE_W, c = txi * TILE_W + k % TILE_W;
+            if (r >= g.H || c >= g.W || is_ghost_row(g, r)) continue;
+            const int64_t p = (int64_t)r * g.W + c;
+            const int32_t d = g.dist[p];
+            const int32_t e = g.e[p];
+            if (d < g.INF) {
+                g.h[p] = d;
+                active += e > 0;
+                act_tile |= e > 0;
+                lvl = max(lvl, d);
+            } else {
+                if (g.h[p] < g.V) g.h[p] = g.V;
+                if (!g.marked[p]) { g.marked[p] = 1; mex += e; }
+            }
+        }
+        if (__syncthreads_or(act_tile) && threadIdx.x == 0) tq_push(g.pq, 0, tile);
+    }
+    if (active) atomicAdd(&acc[0], (unsigned long long)active);
+    if (mex) atomicAdd(&acc[1], (unsigned long long)mex);
+    if (lvl) atomicMax(&acc[2], (unsigned long long)lvl);
 }
 
 // gap_relabel (maxflow_seq.py:149-160) + marking (maxflow_par.py:223-226):
@@ -815,6 +910,13 @@ struct fm_grid {
     int vote_mask = 7;                   // CTA activity vote every vote_mask+1 passes (env FM_VOTE)
     int bq_parity = 0;                   // parity of the next BFS / cut sweep
     int32_t *d_band = nullptr;           // band exchange: changed counter
+    uint8_t *d_touched = nullptr;        // per tile: pushed into since the last relabel
+    uint8_t *d_region = nullptr;         // per tile: in the local relabel's region
+    int32_t *d_rlist = nullptr;          // region tile list (+ count at the end)
+    int local_div = 64;                  // local relabel once active <= H*W/local_div (0: never)
+    int local_max = 12;                  // consecutive local relabels before a global one
+    int local_margin = 2;                // region dilation in tiles
+    int local_streak = 0;
     int k_local = 0;                     // tuning overrides (env FM_K_LOCAL / FM_BFS_INTERVAL)
     int trace = 0;                       // env FM_TRACE=1: one stderr line per round
     int bfs_interval_env = 0;
@@ -925,13 +1027,60 @@ int global_relabel(fm_grid *g) {
     g->active = (long long)g->h_acc[4];
     g->excess_total -= (long long)g->h_acc[5];
     g->st.bfs_levels = std::max<int64_t>(g->st.bfs_levels, (int64_t)g->h_acc[6]);
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
     return FM_OK;
+}
+
+// Local relabel over the region of tiles touched since the last relabel (see
+// region_build_kernel).  Falls back to the global relabel when the region is large.
+int local_relabel(fm_grid *g) {
+    cudaEventRecord(g->ev[0], g->stream);
+    FM_TRY(tq_reset(g, g->d.bq));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d_rlist + g->ntiles, 0, sizeof(int32_t), g->stream));
+    region_build_kernel<<<(g->ntiles + 255) / 256, 256, 0, g->stream>>>(g->d, g->d_region, g->local_margin,
+                                                                         g->d_rlist + g->ntiles);
+    FM_CHECK_LAUNCH();
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->d_rlist, g->d.bq.list[0], sizeof(int32_t) * g->ntiles,
+                                  cudaMemcpyDeviceToDevice, g->stream));
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->d_rlist + g->ntiles, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+    FM_TRY(sync_stream(g));
+    const int nr = g->h_flags[0];
+    g->st.launches++;
+    if (nr > g->ntiles / 4) return global_relabel(g);
+    g->d.region = g->d_region;
+    bfs_init_local_kernel<<<std::max(1, std::min(nr, g->sms * 8)), 256, 0, g->stream>>>(g->d);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    g->bq_parity = 0;
+    int rc = frontier_sweeps(g, bfs_tile_kernel, false, &g->st.bfs_sweeps, &g->st.bfs_launches, &g->st.ms_bfs_kern);
+    if (rc == FM_OK) {
+        FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
+        FM_TRY(tq_reset(g, g->d.pq));
+        g->pq_parity = 0;
+        bfs_finalize_local_kernel<<<std::max(1, std::min(nr, g->sms * 8)), 256, 0, g->stream>>>(
+            g->d, g->d_rlist, nr, g->acc + 4);
+        FM_CHECK_LAUNCH();
+        g->st.launches++;
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 4, g->acc + 4, sizeof(unsigned long long) * 3,
+                                      cudaMemcpyDeviceToHost, g->stream));
+        cudaEventRecord(g->ev[1], g->stream);
+        FM_TRY(sync_stream(g));
+        g->st.ms_bfs += elapsed(g);
+        g->active = (long long)g->h_acc[4];
+        g->excess_total -= (long long)g->h_acc[5];
+        g->st.reserved[1]++;  // local relabels
+    }
+    g->d.region = nullptr;
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
+    return rc;
 }
 
 int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int32_t *capD,
                  const int32_t *capU, const int32_t *capS, const int32_t *capT, int32_t flags) {
     g->flags_solve = flags;
+    g->local_streak = 0;
     memset(&g->st, 0, sizeof(g->st));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 16, g->stream));
     grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
@@ -1061,7 +1210,16 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     g->st.ms_push += elapsed(g);
     g->st.pushes += (int64_t)g->h_acc[10];
     g->st.relabels += (int64_t)g->h_acc[11];
-    FM_TRY(global_relabel(g));
+    const bool go_local = g->local_div > 0 && !(g->flags_solve & FM_GRID_GLOBAL_SWEEP) &&
+                          !(g->flags_solve & FM_GRID_CANCEL_VIOLATIONS) &&
+                          g->active <= g->HW / g->local_div && g->local_streak < g->local_max;
+    if (go_local) {
+        g->local_streak++;
+        FM_TRY(local_relabel(g));
+    } else {
+        g->local_streak = 0;
+        FM_TRY(global_relabel(g));
+    }
     g->st.rounds++;
     if (g->trace)
         fprintf(stderr, "[fm_grid] round %lld active %lld -> %lld | launches %lld tiles %lld pushes %lld relabels %lld "
@@ -1157,6 +1315,9 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_OP_STEPS")) g->op_steps = std::max(1, atoi(v));
     if (const char *v = getenv("FM_OP_FUSED")) g->op_fused = atoi(v);
     if (const char *v = getenv("FM_VOTE")) g->vote_mask = std::max(1, atoi(v)) - 1;
+    if (const char *v = getenv("FM_LOCAL_DIV")) g->local_div = atoi(v);
+    if (const char *v = getenv("FM_LOCAL_MAX")) g->local_max = atoi(v);
+    if (const char *v = getenv("FM_LOCAL_MARGIN")) g->local_margin = atoi(v);
     const size_t n4 = sizeof(int32_t) * (size_t)g->HW, n1 = (size_t)g->HW;
     int32_t **planes[] = {&g->d.e, &g->d.h, &g->d.rR, &g->d.rL, &g->d.rD, &g->d.rU,
                           &g->d.rT, &g->d.rS, &g->d.cS, &g->d.dist, &g->d.inflow_h, &g->d.inflow_v};
@@ -1172,6 +1333,9 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         cudaMalloc((void **)&g->d.cut, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
         cudaMalloc((void **)&g->d_queues, sizeof(int32_t) * (8 * (size_t)g->ntiles + 8)) != cudaSuccess ||
+        cudaMalloc((void **)&g->d_touched, (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->d_region, (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->d_rlist, sizeof(int32_t) * ((size_t)g->ntiles + 1)) != cudaSuccess ||
         cudaMalloc((void **)&g->flags, sizeof(int32_t) * 64) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_flags, sizeof(int32_t) * 64) != cudaSuccess ||
@@ -1194,6 +1358,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         }
     }
     g->stream = g->own_stream;
+    g->d.touched = g->d_touched;
+    g->d.region = nullptr;
     g->d.H = H; g->d.W = W;
     g->d.V = (int32_t)(g->HW + 2);
     g->d.INF = g->d.V;
@@ -1218,6 +1384,9 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->d.marked) cudaFree(g->d.marked);
     if (g->d.cut) cudaFree(g->d.cut);
     if (g->d_band) cudaFree(g->d_band);
+    if (g->d_touched) cudaFree(g->d_touched);
+    if (g->d_region) cudaFree(g->d_region);
+    if (g->d_rlist) cudaFree(g->d_rlist);
     if (g->acc) cudaFree(g->acc);
     if (g->flags) cudaFree(g->flags);
     if (g->h_acc) cudaFreeHost(g->h_acc);
@@ -1394,6 +1563,7 @@ extern "C" int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t 
     if (g->h_acc[1] != 0) { fm_set_error("negative capacity in grid input"); return FM_INVALID_ARG; }
     g->sum_capS = (long long)g->h_acc[0];
     g->excess_total = g->sum_capS;
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
     FM_TRY(tq_reset(g, g->d.pq));
     FM_TRY(tq_reset(g, g->d.bq));
     g->pq_parity = g->bq_parity = 0;
