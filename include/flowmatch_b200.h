@@ -200,6 +200,17 @@ int fm_assign_solve_host(fm_assign *a, const int32_t *weights, int64_t alpha,
                          int32_t flags, int64_t *objective_out, int32_t *match_out,
                          int64_t *prices_out, fm_stats *stats);
 
+/* ------------------------------------------------------------------ DIMACS
+ * Ingest of the reference's file formats (dimacs.py:123-248) with the same
+ * validation and line-numbered messages (fm_last_error).  Call once with null
+ * arrays to get the counts, then with arrays of at least that many entries.
+ * max: out_nst = {node_count, source, sink} (0-based), arcs in file order.
+ * asn: *out_n = nodes per side, edges (x, y, w) with sides mapped to 0..n-1. */
+int fm_dimacs_parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
+                        int32_t *tails, int32_t *heads, int32_t *caps, int64_t cap_arcs);
+int fm_dimacs_parse_asn(const char *text, int64_t len, int32_t *out_n, int64_t *out_m,
+                        int32_t *xs, int32_t *ys, int64_t *ws, int64_t cap_edges);
+
 /* Stepwise solve, one refine at a time (solve_assignment's on_refine_end hook,
  * assign_scaling.py:419-420,451-452).  begin copies HOST weights; refine runs one
  * epsilon phase and reports the new epsilon and whether it was the last (eps == 1);

@@ -19,6 +19,18 @@ from .assign import (
     InfeasibleInstanceError,
     solve_assignment,
 )
+from .cli import cli_main
+from .dimacs import (
+    InstanceFile,
+    ParseError,
+    detect_kind,
+    generate,
+    load_max,
+    parse_dimacs_asn,
+    parse_dimacs_max,
+    serialize_instance,
+    serialize_network,
+)
 from .graph import (
     FlowNetwork,
     GridNetwork,
@@ -41,10 +53,20 @@ __all__ = [
     "GridNetwork",
     "GridSolver",
     "InfeasibleInstanceError",
+    "InstanceFile",
+    "ParseError",
     "NetworkError",
     "SolveReport",
     "build_grid_network",
     "build_network",
+    "cli_main",
+    "detect_kind",
+    "generate",
+    "load_max",
+    "parse_dimacs_asn",
+    "parse_dimacs_max",
+    "serialize_instance",
+    "serialize_network",
     "generators",
     "hybrid_solve",
     "min_cut",

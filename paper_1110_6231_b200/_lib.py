@@ -91,6 +91,8 @@ SIGNATURES = {
     "fm_grid_band_cut": (ctypes.c_int, [_vp, _i32, _vp]),
     "fm_grid_band_rows": (ctypes.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
     "fm_grid_band_flow": (ctypes.c_int, [_vp, _vp]),
+    "fm_dimacs_parse_max": (ctypes.c_int, [ctypes.c_char_p, _i64, _vp, _vp, _vp, _vp, _vp, _i64]),
+    "fm_dimacs_parse_asn": (ctypes.c_int, [ctypes.c_char_p, _i64, _vp, _vp, _vp, _vp, _vp, _i64]),
     "fm_csr_solve": (ctypes.c_int, [_i32, _i32, _i32, _i64] + [_vp] * 4 + [_i32, _i32] + [_vp] * 5),
     "fm_assign_create": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(_vp)]),
     "fm_assign_destroy": (None, [_vp]),
