@@ -55,6 +55,7 @@ __device__ __forceinline__ bool is_ghost_row(const GridDev &g, int r);
 struct GridDev {
     int32_t *e, *h, *rR, *rL, *rD, *rU, *rT, *rS, *cS;
     int32_t *dist;
+    uint32_t *rbits;        // K2 bit planes: per tile, 5 x 32 words (R, L, D, U, T arcs; lane = row)
     uint8_t *mask, *marked, *cut;
     // tile-resident kernel (K1 v2): flow pushed across a tile border is parked in
     // an inbox of the receiving pixel (inflow_h: across a vertical tile border,
@@ -399,6 +400,284 @@ __global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(
     block_add_i64<PT_W * PT_TY / 32>(relabels, ops + 1);
 }
 
+// ----------------------------------------------------------------------------
+// K1 (v3, default): the same tile-resident lock-free operation, driven by per-pass
+// lists of active pixels instead of a scan of all 1024 pixels per pass.
+//
+// A v2 pass costs every warp a scan of its rows while only a few percent of the
+// pixels are active (ncu: ~1 thread per warp executes the operation body, 30% of
+// stall samples sit in the activity vote).  Here the pixels a pass operates on are
+// listed in shared memory and dealt out to consecutive threads, so warps run
+// operations with most lanes busy.  While a pass lists more than 32 pixels the
+// whole CTA works on it (one barrier per pass); once a list fits one warp, warp 0
+// carries on alone with warp-synchronous passes and the other warps sleep at the
+// final barrier, so sparse passes pay neither a CTA barrier nor idle warps' issue.
+//
+// List maintenance (each pixel appears at most once per list):
+//  * after its operation(s) the owner re-lists its pixel iff its excess is still
+//    positive (the value its own atomicSub returned) and it sits below the source;
+//  * a push re-lists the receiver iff the receiver's atomicAdd saw e <= 0, i.e. this
+//    push made it active.  An owner whose own atomicSub left e <= 0 stops working
+//    on the pixel, so "owner saw e > 0 last" and "a sender saw e <= 0" exclude each
+//    other in the atomic order on e(p): exactly one of them lists p.
+// Pixels left out (no residual arc, above the source) are rescanned when the tile
+// is next loaded.  Lists are double-buffered; three counters rotate so that the
+// counter the next pass fills is zeroed one barrier before it is used.
+// Flow pushed across the tile border goes to the receiver's inbox (fire-and-forget
+// RED); the neighbour tile is queued for the next launch once, at the end of the
+// visit (the launch boundary orders the inbox writes before its next load).
+// ----------------------------------------------------------------------------
+constexpr int PL_TY = 8, PL_NT = PT_W * PL_TY, PL_ROWS = PT_H / PL_TY;
+#ifndef FM_PL_MINBLOCKS
+#define FM_PL_MINBLOCKS 6
+#endif
+
+__device__ __forceinline__ void pl_append_warp(bool want, int idx, int *cnt, uint16_t *list) {
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(cnt, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (want) list[base + __popc(m & ((1u << lane) - 1))] = (uint16_t)idx;
+}
+
+struct PlTile {
+    int32_t *e, *h, *t;        // shared planes (h with a 1-pixel halo, row stride PT_W + 2)
+    int32_t (*r)[PT_H * PT_W];
+    const uint8_t *f;
+    int *nbr;                  // bit d: flow was parked in the inbox of neighbour tile d
+    int r0, c0;
+};
+
+// One listed pixel: up to `steps` operations of maxflow_par.py:98-125 by its owner.
+// Returns whether the owner re-lists it; *recv = the in-tile receiver its last push
+// activated (-1 if none); receivers of earlier pushes are listed directly.
+__device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int li, int steps, int fused,
+                                        int *cnt_next, uint16_t *lout, int *recv,
+                                        long long &pushes, long long &relabels) {
+    constexpr int HS = PT_W + 2;
+    volatile int32_t *ve = T.e;
+    volatile int32_t *vh = T.h;
+    volatile int32_t *vt = T.t;
+    const int V = g.V;
+    const int lr = li >> 5, lc = li & 31;
+    const int hi = (lr + 1) * HS + lc + 1;
+    const int r = T.r0 + lr, c = T.c0 + lc;
+    const uint8_t f = T.f[li];
+    if (f & 2) return false;                               // ghost row: owned by the neighbour band
+    int32_t e = ve[li];
+    int32_t hp = vh[hi];
+    for (int st = 0; st < steps; st++) {
+        if (e <= 0 || hp >= V) return false;
+        const int32_t rt = vt[li];
+        if (rt > 0) {                                      // sink at height 0
+            if (hp == 0) { hp = 1; vh[hi] = 1; relabels++; }
+            const int32_t d = min(e, rt);
+            vt[li] = rt - d;
+            e = atomicSub(&T.e[li], d) - d;
+            pushes++;
+            continue;
+        }
+        const int32_t rr = *(volatile int32_t *)&T.r[0][li];
+        const int32_t rl = *(volatile int32_t *)&T.r[1][li];
+        const int32_t rd = *(volatile int32_t *)&T.r[2][li];
+        const int32_t ru = *(volatile int32_t *)&T.r[3][li];
+        const int32_t hR = vh[hi + 1], hL = vh[hi - 1], hD = vh[hi + HS], hU = vh[hi - HS];
+        int32_t best_h = INT32_MAX, best_r = 0;
+        int dir = -1;
+        if (rr > 0 && c + 1 < g.W && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
+        if (rl > 0 && c > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
+        if (rd > 0 && r + 1 < g.H && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
+        if (ru > 0 && r > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
+        if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
+        if (dir < 0) return false;                         // nothing residual: rescanned on next load
+        if (hp <= best_h) {                                // relabel (owner-only)
+            hp = best_h + 1;
+            vh[hi] = hp;
+            relabels++;
+            if (dir == 5) return false;                    // above the source: inactive
+            if (!fused) break;
+        }
+        const int32_t d = min(e, best_r);
+        atomicSub(&T.r[dir][li], d);
+        int qr = lr, qc = lc;
+        if (dir == 0) qc++; else if (dir == 1) qc--; else if (dir == 2) qr++; else qr--;
+        if (qr >= 0 && qr < PT_H && qc >= 0 && qc < PT_W) {
+            const int qi = qr * PT_W + qc;
+            atomicAdd(&T.r[dir ^ 1][qi], d);
+            const int32_t old = atomicAdd(&T.e[qi], d);
+            if (old <= 0 && old + d > 0) {
+                if (*recv >= 0) lout[atomicAdd(cnt_next, 1)] = (uint16_t)*recv;
+                *recv = qi;
+            }
+        } else {
+            const int64_t q = (int64_t)(T.r0 + qr) * g.W + (T.c0 + qc);
+            atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + q, d);
+            atomicOr(T.nbr, 1 << dir);
+        }
+        e = atomicSub(&T.e[li], d) - d;                    // last: the owner's view of e(p)
+        pushes++;
+    }
+    return e > 0 && hp < V;
+}
+
+__global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev g, int k_local, int steps, int fused,
+                                                                       int parity, int32_t *processed,
+                                                                       unsigned long long *ops) {
+    __shared__ int32_t s_e[PT_H * PT_W];
+    __shared__ int32_t s_h[(PT_H + 2) * (PT_W + 2)];
+    __shared__ int32_t s_r[4][PT_H * PT_W];   // R, L, D, U
+    __shared__ int32_t s_t[PT_H * PT_W];
+    __shared__ uint8_t s_f[PT_H * PT_W];      // bit 0: residual arc to s, bit 1: ghost row
+    __shared__ uint16_t s_list[2][PT_H * PT_W];
+    __shared__ int s_cnt[3];
+    __shared__ int s_nbr;
+    __shared__ int s_tile;
+    constexpr int HS = PT_W + 2;
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * PT_W + tx;
+    const int V = g.V;
+    long long pushes = 0, relabels = 0, passes = 0, items = 0;
+    for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+        s_tile = tq_take(g.pq, parity, 0, 0);
+        s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
+        s_nbr = 0;
+    }
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile < 0) break;
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const PlTile T{s_e, s_h, s_t, s_r, s_f, &s_nbr, tyi * PT_H, txi * PT_W};
+    const int r0 = T.r0, c0 = T.c0;
+#pragma unroll
+    for (int k = 0; k < PL_ROWS; k++) {
+        const int lr = ty + k * PL_TY;
+        const int r = r0 + lr, c = c0 + tx;
+        const int li = lr * PT_W + tx;
+        if (r < g.H && c < g.W) {
+            const int64_t p = (int64_t)r * g.W + c;
+            int32_t e = g.e[p];
+            int32_t rr = g.rR[p], rl = g.rL[p], rd = g.rD[p], ru = g.rU[p];
+            if (tx == 0 && c > 0) { const int32_t d = atomicExch(g.inflow_h + p, 0); e += d; rl += d; }
+            if (tx == PT_W - 1 && c + 1 < g.W) { const int32_t d = atomicExch(g.inflow_h + p, 0); e += d; rr += d; }
+            if (lr == 0 && r > 0) { const int32_t d = atomicExch(g.inflow_v + p, 0); e += d; ru += d; }
+            if (lr == PT_H - 1 && r + 1 < g.H) { const int32_t d = atomicExch(g.inflow_v + p, 0); e += d; rd += d; }
+            s_e[li] = e;
+            s_h[(lr + 1) * HS + tx + 1] = g.h[p];
+            s_r[0][li] = rr; s_r[1][li] = rl; s_r[2][li] = rd; s_r[3][li] = ru;
+            s_t[li] = g.rT[p];
+            s_f[li] = (g.rS[p] > 0 ? 1 : 0) | (is_ghost_row(g, r) ? 2 : 0);
+        } else {
+            s_e[li] = 0;
+            s_h[(lr + 1) * HS + tx + 1] = V;
+            s_r[0][li] = s_r[1][li] = s_r[2][li] = s_r[3][li] = 0;
+            s_t[li] = 0;
+            s_f[li] = 2;
+        }
+    }
+    if (tid < 4 * PT_W) {   // halo snapshot of neighbour heights
+        const int side = tid / PT_W, i = tid % PT_W;
+        int r, cc, hr, hc;
+        if (side == 0) { r = r0 - 1; cc = c0 + i; hr = 0; hc = i + 1; }
+        else if (side == 1) { r = r0 + PT_H; cc = c0 + i; hr = PT_H + 1; hc = i + 1; }
+        else if (side == 2) { r = r0 + i; cc = c0 - 1; hr = i + 1; hc = 0; }
+        else { r = r0 + i; cc = c0 + PT_W; hr = i + 1; hc = PT_W + 1; }
+        s_h[hr * HS + hc] = (r >= 0 && r < g.H && cc >= 0 && cc < g.W) ? g.h[(int64_t)r * g.W + cc] : V;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PL_ROWS; k++) {
+        const int lr = ty + k * PL_TY;
+        const int li = lr * PT_W + tx;
+        pl_append_warp(s_e[li] > 0 && s_h[(lr + 1) * HS + tx + 1] < V && !(s_f[li] & 2), li, &s_cnt[0], s_list[0]);
+    }
+    // dense passes: the whole CTA, one barrier per pass
+    int it = 0;
+    bool solo = false;
+    for (; it < k_local; it++) {
+        __syncthreads();
+        const int n = s_cnt[it % 3];
+        if (n == 0) break;
+        if (n <= 32) { solo = true; break; }
+        passes++;
+        items += n;
+        int *cnt_next = &s_cnt[(it + 1) % 3];
+        if (tid == 0) s_cnt[(it + 2) % 3] = 0;
+        const uint16_t *lin = s_list[it & 1];
+        uint16_t *lout = s_list[(it + 1) & 1];
+        for (int base = 0; base < n; base += PL_NT) {
+            if (base + (tid & ~31) >= n) break;        // warp-uniform
+            const int i = base + tid;
+            int recv = -1;
+            const bool keep = i < n && pl_item(g, T, lin[i], steps, fused, cnt_next, lout, &recv, pushes, relabels);
+            pl_append_warp(keep, i < n ? lin[i] : 0, cnt_next, lout);
+            pl_append_warp(recv >= 0, recv, cnt_next, lout);
+        }
+    }
+    // sparse passes: warp 0 alone, warp-synchronous
+    if (solo && tid < 32) {
+        for (; it < k_local; it++) {
+            __syncwarp();
+            const int n = s_cnt[it % 3];
+            if (n == 0) break;
+            passes++;
+            items += n;
+            int *cnt_next = &s_cnt[(it + 1) % 3];
+            if (tid == 0) s_cnt[(it + 2) % 3] = 0;
+            const uint16_t *lin = s_list[it & 1];
+            uint16_t *lout = s_list[(it + 1) & 1];
+            __syncwarp();
+            for (int base = 0; base < n; base += 32) {
+                const int i = base + tid;
+                int recv = -1;
+                const int li = i < n ? lin[i] : 0;
+                const bool keep = i < n && pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, pushes, relabels);
+                pl_append_warp(keep, li, cnt_next, lout);
+                pl_append_warp(recv >= 0, recv, cnt_next, lout);
+            }
+        }
+    }
+    __syncthreads();
+    bool act = false;
+#pragma unroll
+    for (int k = 0; k < PL_ROWS; k++) {
+        const int lr = ty + k * PL_TY;
+        const int r = r0 + lr, c = c0 + tx;
+        const int li = lr * PT_W + tx;
+        if (r < g.H && c < g.W) {
+            const int64_t p = (int64_t)r * g.W + c;
+            const int32_t e = s_e[li], h = s_h[(lr + 1) * HS + tx + 1];
+            g.e[p] = e;
+            g.h[p] = h;
+            g.rR[p] = s_r[0][li]; g.rL[p] = s_r[1][li];
+            g.rD[p] = s_r[2][li]; g.rU[p] = s_r[3][li];
+            g.rT[p] = s_t[li];
+            act |= (e > 0 && h < V && !(s_f[li] & 2));
+        }
+    }
+    const int any_act = __syncthreads_or(act);
+    if (tid == 0) {
+        if (any_act) tq_push(g.pq, parity ^ 1, tile);
+        g.touched[tile] = 1;
+        const int nb = s_nbr;
+        if (nb & 1) { tq_push(g.pq, parity ^ 1, tile + 1); g.touched[tile + 1] = 1; }
+        if (nb & 2) { tq_push(g.pq, parity ^ 1, tile - 1); g.touched[tile - 1] = 1; }
+        if (nb & 4) { tq_push(g.pq, parity ^ 1, tile + g.ntx); g.touched[tile + g.ntx] = 1; }
+        if (nb & 8) { tq_push(g.pq, parity ^ 1, tile - g.ntx); g.touched[tile - g.ntx] = 1; }
+        atomicAdd(processed, 1);
+    }
+    }  // tile loop
+    block_add_i64<PL_NT / 32>(pushes, ops + 0);
+    block_add_i64<PL_NT / 32>(relabels, ops + 1);
+    if (tid == 0) {   // diagnostics: passes run and list items dealt (ops[3], ops[4]) -- thread 0 saw them all
+        if (passes) atomicAdd(ops + 3, (unsigned long long)passes);
+        if (items) atomicAdd(ops + 4, (unsigned long long)items);
+    }
+}
+
 // fold every parked inbox into e and the reverse residual (coordinator point)
 __global__ void integrate_inflow_kernel(GridDev g) {
     const int tile = blockIdx.x;
@@ -570,6 +849,358 @@ __global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int parity, in
         }
     }
     }  // tile loop
+}
+
+// ----------------------------------------------------------------------------
+// K2 (bit-parallel, default): the same tile fixpoint, one warp per 32x32 tile with
+// the tile's residual arcs as bit planes (lane = tile row, bit = column).
+//
+// bfs_init_bits_kernel builds, per tile row, five words with warp ballots:
+// R/L/D/U (pixel has a residual arc toward that neighbour) and T (arc to the sink).
+// bfs_bits_kernel then runs a level-synchronous multi-source BFS inside the tile:
+// level 1 = T pixels, every halo pixel (and imported ghost-row pixel) of distance v
+// is a source entering at level v, and one level expands the whole tile with a few
+// shifts, shuffles and ANDs:
+//     N = ((F >> 1) & R) | ((F << 1) & L) | (F_below & D) | (F_above & U),  N &= ~seen
+// Empty level ranges jump straight to the next halo distance.  A visit recomputes
+// the tile from its current halo; distances only fall as halos fall, and the
+// write-back keeps min(old, new), so stale halo reads can never raise a label.
+// The v1 per-pixel Jacobi kernel (bfs_tile_kernel) stays behind FM_BFS_BITS=0.
+// ----------------------------------------------------------------------------
+constexpr int BB_WARPS = 4;   // tiles in flight per CTA (one per warp)
+
+__device__ __forceinline__ void bits_row(const GridDev &g, int tile, int lr, int lane) {
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int r = tyi * PT_H + lr, c = txi * PT_W + lane;
+    const bool in = r < g.H && c < g.W && !is_ghost_row(g, r);
+    const int64_t p = (int64_t)r * g.W + c;
+    const bool aR = in && c + 1 < g.W && g.rR[p] > 0;
+    const bool aL = in && c > 0 && g.rL[p] > 0;
+    const bool aD = in && r + 1 < g.H && g.rD[p] > 0;
+    const bool aU = in && r > 0 && g.rU[p] > 0;
+    const bool aT = in && g.rT[p] > 0;
+    const uint32_t w[5] = {__ballot_sync(0xffffffffu, aR), __ballot_sync(0xffffffffu, aL),
+                           __ballot_sync(0xffffffffu, aD), __ballot_sync(0xffffffffu, aU),
+                           __ballot_sync(0xffffffffu, aT)};
+    uint32_t *B = g.rbits + (size_t)tile * 160 + lr;
+    if (lane < 5) B[lane * 32] = w[lane];
+    if (r < g.H && c < g.W) g.dist[p] = aT ? 1 : g.INF;
+}
+
+// listed == 0: every tile; listed == 1: the tiles of bq.list[0] (local relabel region)
+__global__ void bfs_init_bits_kernel(GridDev g, int listed) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nrows = listed ? (int64_t)__ldcg(g.bq.cnt + 0) * PT_H : (int64_t)g.ntx * g.nty * PT_H;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int k = (int)(w / PT_H), lr = (int)(w % PT_H);
+        bits_row(g, listed ? g.bq.list[0][k] : k, lr, lane);
+    }
+}
+
+__device__ __forceinline__ int warp_min_i32(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__global__ void __launch_bounds__(32 * BB_WARPS) bfs_bits_kernel(GridDev g, int parity, int all_tiles,
+                                                               int32_t *changed_count) {
+    __shared__ int32_t s_d[BB_WARPS][PT_H * (PT_W + 1)];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t *sd = s_d[wid];
+    const int INF = g.INF;
+    for (;;) {
+        int tile = 0;
+        if (lane == 0) tile = tq_take(g.bq, parity, all_tiles, g.ntx * g.nty);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile < 0) break;
+        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+        const int r0 = tyi * PT_H, c0 = txi * PT_W;
+        const uint32_t *B = g.rbits + (size_t)tile * 160;
+        const uint32_t mR = B[lane], mL = B[32 + lane], mD = B[64 + lane], mU = B[96 + lane], mT = B[128 + lane];
+        // halo distances: lane = column for the rows above / below, lane = row for the columns left / right
+        const int cl = c0 + lane, rl = r0 + lane;
+        const int ht = (r0 > 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 - 1) * g.W + cl) : INF;
+        const int hb = (r0 + PT_H < g.H && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + PT_H) * g.W + cl) : INF;
+        const int hl = (c0 > 0 && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 - 1) : INF;
+        const int hr = (c0 + PT_W < g.W && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + PT_W) : INF;
+        // ghost rows (row bands) hold imported distances: sources, never recomputed
+        const int g0 = (g.ghost_top && r0 == 0) ? 0 : -1;
+        const int g1 = (g.ghost_bot && g.H - 1 >= r0 && g.H - 1 < r0 + PT_H) ? g.H - 1 - r0 : -1;
+        const int gv0 = (g0 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g0) * g.W + cl) : INF;
+        const int gv1 = (g1 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g1) * g.W + cl) : INF;
+        uint32_t F = mT, seen = mT;
+        for (uint32_t x = mT; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = 1;
+        int L = 1;
+        for (;;) {
+            if (g0 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv0 == L); if (lane == g0) F |= s; }
+            if (g1 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv1 == L); if (lane == g1) F |= s; }
+            const uint32_t tb = __ballot_sync(0xffffffffu, ht == L);
+            const uint32_t bb = __ballot_sync(0xffffffffu, hb == L);
+            uint32_t up = __shfl_up_sync(0xffffffffu, F, 1);
+            uint32_t dn = __shfl_down_sync(0xffffffffu, F, 1);
+            if (lane == 0) up = tb;
+            if (lane == 31) dn = bb;
+            uint32_t N = ((F >> 1) & mR) | ((F << 1) & mL) | (dn & mD) | (up & mU);
+            if (hr == L) N |= mR & 0x80000000u;
+            if (hl == L) N |= mL & 1u;
+            N &= ~seen;
+            seen |= N;
+            L++;
+            for (uint32_t x = N; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = L;
+            F = N;
+            if (!__any_sync(0xffffffffu, F != 0)) {
+                int m = INF;
+                if (ht >= L) m = min(m, ht);
+                if (hb >= L) m = min(m, hb);
+                if (hl >= L) m = min(m, hl);
+                if (hr >= L) m = min(m, hr);
+                if (gv0 >= L) m = min(m, gv0);
+                if (gv1 >= L) m = min(m, gv1);
+                m = warp_min_i32(m);
+                if (m >= INF) break;
+                L = m;
+            }
+        }
+        __syncwarp();
+        // write back min(old, new); note which borders changed
+        bool bt = false, bbot = false, bl = false, br = false;
+        for (int i = 0; i < PT_H; i++) {
+            const int r = r0 + i;
+            if (r >= g.H) break;
+            const uint32_t sr = __shfl_sync(0xffffffffu, seen, i);
+            if (i == g0 || i == g1 || cl >= g.W || !((sr >> lane) & 1)) continue;
+            const int64_t p = (int64_t)r * g.W + cl;
+            const int nv = sd[i * (PT_W + 1) + lane];
+            if (nv < ld_cg(g.dist + p)) {
+                g.dist[p] = nv;
+                bt |= i == 0;
+                bbot |= i == PT_H - 1;
+                bl |= lane == 0;
+                br |= lane == PT_W - 1;
+            }
+        }
+        const int b0 = __any_sync(0xffffffffu, bt), b1 = __any_sync(0xffffffffu, bbot);
+        const int b2 = __any_sync(0xffffffffu, bl), b3 = __any_sync(0xffffffffu, br);
+        if (lane == 0 && (b0 | b1 | b2 | b3)) {
+            flag_changed_borders(g, tile, tyi, txi, b0, b1, b2, b3, parity ^ 1);
+            atomicAdd(changed_count, 1);
+        }
+        __syncwarp();
+    }
+}
+
+// ----------------------------------------------------------------------------
+// K2 as ONE persistent launch (default): the tile fixpoint driven by a device work
+// queue instead of host-synchronised sweeps.  A tile whose border distances fell
+// queues its neighbours (flag-deduplicated); warps take tiles until the queue is
+// empty and no tile is in flight (asynchronous chaotic relaxation: every value is a
+// path length and only falls, so the fixpoint reached is the BFS distance whatever
+// the order).  The queue is a ring of slots: a warp reserves slot `head++` and
+// waits for it to be filled (tail++ by a producer) or for `pending` (queued + in
+// flight tiles) to reach 0, which ends the launch.  Every CTA is resident (grid =
+// occupancy), so a waiting warp never blocks the producer it waits for.
+// ----------------------------------------------------------------------------
+struct RingQ {
+    int32_t *slot;          // cap entries, -1 = empty
+    int32_t *flag;          // per tile: queued
+    unsigned int *ctr;      // [0] head, [32] tail, [64] pending, [96] tile visits that changed a border (one line each)
+    int32_t cap;
+};
+
+// initial content: tiles list0[0..*count0) (count0 != nullptr) or every tile
+__global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, const int32_t *count0) {
+    const int n0 = count0 ? __ldcg(count0) : ntiles;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < q.cap; i += gridDim.x * blockDim.x) {
+        if (i < n0) {
+            const int t = count0 ? list0[i] : i;
+            q.slot[i] = t;
+            q.flag[t] = 1;
+        } else {
+            q.slot[i] = -1;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) { q.ctr[0] = 0; q.ctr[32] = n0; q.ctr[64] = n0; q.ctr[96] = 0; }
+}
+
+// Tile states: 0 idle, 1 queued, 2 in flight, 3 in flight + stale again.  A tile is
+// never processed by two warps at once (so a visit owns its pixels' distances); a
+// push that finds it in flight marks it 3 and the owner runs it again.
+__device__ __forceinline__ void ringq_push(const RingQ &q, int t) {
+    for (;;) {
+        const int o = atomicCAS(q.flag + t, 0, 1);
+        if (o == 0) {
+            atomicAdd(q.ctr + 64, 1u);
+            const unsigned s = atomicAdd(q.ctr + 32, 1u);
+            __threadfence();   // the distances that made t stale are visible before t is
+            *(volatile int32_t *)(q.slot + (s % (unsigned)q.cap)) = t;
+            return;
+        }
+        if (o != 2 || atomicCAS(q.flag + t, 2, 3) == 2) return;   // queued / already marked
+    }
+}
+
+__global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, RingQ q) {
+    __shared__ int32_t s_d[BB_WARPS][PT_H * (PT_W + 1)];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t *sd = s_d[wid];
+    const int INF = g.INF;
+    for (;;) {
+        int tile = -1;
+        if (lane == 0) {
+            const unsigned s = atomicAdd(q.ctr + 0, 1u) % (unsigned)q.cap;
+            volatile int32_t *vs = q.slot + s;
+            for (unsigned ns = 32;; ns = min(ns * 2, 1024u)) {
+                tile = *vs;
+                if (tile >= 0) { *vs = -1; break; }
+                if (*(volatile unsigned *)(q.ctr + 64) == 0) break;
+                __nanosleep(ns);
+            }
+            if (tile >= 0) { atomicExch(q.flag + tile, 2); __threadfence(); }
+        }
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile < 0) break;
+        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+        const int r0 = tyi * PT_H, c0 = txi * PT_W;
+        const int cl = c0 + lane, rl = r0 + lane;
+        const int g0 = (g.ghost_top && r0 == 0) ? 0 : -1;
+        const int g1 = (g.ghost_bot && g.H - 1 >= r0 && g.H - 1 < r0 + PT_H) ? g.H - 1 - r0 : -1;
+        const uint32_t *B = g.rbits + (size_t)tile * 160;
+        const uint32_t mR = B[lane], mL = B[32 + lane], mD = B[64 + lane], mU = B[96 + lane], mT = B[128 + lane];
+        bool again = true;
+        while (again) {
+        // the tile's current distances (lane = column), read once per visit
+#pragma unroll 8
+        for (int i = 0; i < PT_H; i++) {
+            const int r = r0 + i;
+            sd[i * (PT_W + 1) + lane] = (r < g.H && cl < g.W) ? ld_cg(g.dist + (int64_t)r * g.W + cl) : INF;
+        }
+        const int ht = (r0 > 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 - 1) * g.W + cl) : INF;
+        const int hb = (r0 + PT_H < g.H && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + PT_H) * g.W + cl) : INF;
+        const int hl = (c0 > 0 && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 - 1) : INF;
+        const int hr = (c0 + PT_W < g.W && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + PT_W) : INF;
+        __syncwarp();
+        const int gv0 = g0 >= 0 ? sd[g0 * (PT_W + 1) + lane] : INF;
+        const int gv1 = g1 >= 0 ? sd[g1 * (PT_W + 1) + lane] : INF;
+        // level-synchronous BFS; a pixel reached at level L keeps min(old, L)
+        uint32_t F = mT, seen = mT, chg = 0;
+        for (uint32_t x = mT; x; x &= x - 1) {
+            const int k = lane * (PT_W + 1) + __ffs(x) - 1;
+            if (sd[k] > 1) { sd[k] = 1; chg |= x & (~x + 1); }
+        }
+        int L = 1;
+        for (;;) {
+            if (g0 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv0 == L); if (lane == g0) F |= s; }
+            if (g1 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv1 == L); if (lane == g1) F |= s; }
+            const uint32_t tb = __ballot_sync(0xffffffffu, ht == L);
+            const uint32_t bb = __ballot_sync(0xffffffffu, hb == L);
+            uint32_t up = __shfl_up_sync(0xffffffffu, F, 1);
+            uint32_t dn = __shfl_down_sync(0xffffffffu, F, 1);
+            if (lane == 0) up = tb;
+            if (lane == 31) dn = bb;
+            uint32_t N = ((F >> 1) & mR) | ((F << 1) & mL) | (dn & mD) | (up & mU);
+            if (hr == L) N |= mR & 0x80000000u;
+            if (hl == L) N |= mL & 1u;
+            N &= ~seen;
+            seen |= N;
+            L++;
+            for (uint32_t x = N; x; x &= x - 1) {
+                const int k = lane * (PT_W + 1) + __ffs(x) - 1;
+                if (sd[k] > L) { sd[k] = L; chg |= x & (~x + 1); }
+            }
+            F = N;
+            if (!__any_sync(0xffffffffu, F != 0)) {
+                int m = INF;
+                if (ht >= L) m = min(m, ht);
+                if (hb >= L) m = min(m, hb);
+                if (hl >= L) m = min(m, hl);
+                if (hr >= L) m = min(m, hr);
+                if (gv0 >= L) m = min(m, gv0);
+                if (gv1 >= L) m = min(m, gv1);
+                m = warp_min_i32(m);
+                if (m >= INF) break;
+                L = m;
+            }
+        }
+        __syncwarp();
+        // write back the pixels that fell (this warp owns the tile while in flight)
+        const uint32_t any_chg = __ballot_sync(0xffffffffu, chg != 0);
+        for (uint32_t rows = any_chg; rows; rows &= rows - 1) {
+            const int i = __ffs(rows) - 1;
+            const uint32_t cr = __shfl_sync(0xffffffffu, chg, i);
+            if ((cr >> lane) & 1) g.dist[(int64_t)(r0 + i) * g.W + cl] = sd[i * (PT_W + 1) + lane];
+        }
+        const int b0 = any_chg & 1, b1 = (any_chg >> 31) & 1;
+        const int b2 = __any_sync(0xffffffffu, chg & 1u), b3 = __any_sync(0xffffffffu, chg >> 31);
+        int st = 0;
+        if (lane == 0) {
+            if (any_chg) atomicAdd(q.ctr + 96, 1u);
+            if (b0 | b1 | b2 | b3) {
+                __threadfence();
+                const auto in = [&](int t) { return !g.region || g.region[t]; };
+                if (b0 && tyi > 0 && in(tile - g.ntx)) ringq_push(q, tile - g.ntx);
+                if (b1 && tyi + 1 < g.nty && in(tile + g.ntx)) ringq_push(q, tile + g.ntx);
+                if (b2 && txi > 0 && in(tile - 1)) ringq_push(q, tile - 1);
+                if (b3 && txi + 1 < g.ntx && in(tile + 1)) ringq_push(q, tile + 1);
+            }
+            st = atomicCAS(q.flag + tile, 2, 0);
+            if (st == 3) { atomicExch(q.flag + tile, 2); __threadfence(); }
+            else atomicSub(q.ctr + 64, 1u);   // after the pushes: pending never reads 0 early
+        }
+        again = __shfl_sync(0xffffffffu, st, 0) == 3;
+        __syncwarp();
+        }  // while again
+    }
+}
+
+// gap_relabel + marking (as bfs_finalize_kernel), one CTA per tile so each tile with
+// an active pixel is queued once
+__global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsigned long long *acc) {
+    long long active = 0, mex = 0;
+    int32_t lvl = 0;
+    const int nt = g.ntx * g.nty;
+    for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+        bool act = false;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int lr = (threadIdx.x >> 5) + 8 * k;
+            const int r = tyi * PT_H + lr, c = txi * PT_W + (threadIdx.x & 31);
+            if (r >= g.H || c >= g.W || is_ghost_row(g, r)) continue;
+            const int64_t p = (int64_t)r * g.W + c;
+            const int32_t d = g.dist[p];
+            const int32_t e = g.e[p];
+            if (d < g.INF) {
+                g.h[p] = d;
+                active += e > 0;
+                act |= e > 0;
+                lvl = max(lvl, d);
+            } else {
+                if (g.h[p] < g.V) g.h[p] = g.V;
+                if (!g.marked[p]) { g.marked[p] = 1; mex += e; }
+            }
+        }
+        if (__syncthreads_or(act) && threadIdx.x == 0) tq_push(g.pq, 0, tile);
+    }
+    __shared__ long long red[2][8];
+    __shared__ int32_t redl[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        active += __shfl_xor_sync(0xffffffffu, active, o);
+        mex += __shfl_xor_sync(0xffffffffu, mex, o);
+        lvl = max(lvl, __shfl_xor_sync(0xffffffffu, lvl, o));
+    }
+    if (lane == 0) { red[0][wid] = active; red[1][wid] = mex; redl[wid] = lvl; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long a = 0, m = 0; int32_t l = 0;
+        for (int i = 0; i < 8; i++) { a += red[0][i]; m += red[1][i]; l = max(l, redl[i]); }
+        if (a) atomicAdd(&acc[0], (unsigned long long)a);
+        if (m) atomicAdd(&acc[1], (unsigned long long)m);
+        if (l) atomicMax(&acc[2], (unsigned long long)l);
+    }
 }
 
 // ----------------------------------------------------------------------------
@@ -908,6 +1539,16 @@ struct fm_grid {
     int op_steps = 1;                    // operations per pixel per pass (env FM_OP_STEPS)
     int op_fused = 0;                    // relabel then push in one operation (env FM_OP_FUSED)
     int vote_mask = 7;                   // CTA activity vote every vote_mask+1 passes (env FM_VOTE)
+    int bfs_bits = 2;                    // 2: persistent bit-parallel BFS (bfs_ring_kernel), 1: bit-parallel
+                                         // sweeps (bfs_bits_kernel), 0: v1 Jacobi sweeps (env FM_BFS_BITS)
+    int bb_per_sm = 8;                   // resident bfs_bits CTAs per SM (occupancy query)
+    int br_per_sm = 8;                   // resident bfs_ring CTAs per SM (occupancy query, <= br_cap)
+    int br_cap = 6;                      // env FM_BR_CAP
+    RingQ rq{};                          // device work queue of the persistent BFS
+    bool ring_stats_pending = false;
+    int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (env FM_PR_KERNEL)
+    int pl_per_sm = 6;                   // resident pr_list CTAs per SM (occupancy query)
+    int k_local_list = 0;                // passes per visit of the list kernel (env FM_K_LOCAL_LIST)
     int bq_parity = 0;                   // parity of the next BFS / cut sweep
     int32_t *d_band = nullptr;           // band exchange: changed counter
     uint8_t *d_touched = nullptr;        // per tile: pushed into since the last relabel
@@ -968,13 +1609,13 @@ int tq_arm(fm_grid *g, const TileQueue &q, int p) {
 // per-sweep count of changed tiles lands in flags[j] (batches of 4 per host check).
 template <typename K>
 int frontier_sweeps(fm_grid *g, K kernel, bool first_all, int64_t *sweeps, int64_t *launches,
-                    double *ms_kern) {
+                    double *ms_kern, dim3 block = dim3(TILE_W, BLK_Y), int nblocks = 0) {
     if (first_all) {
         FM_TRY(tq_reset(g, g->d.bq));
         g->bq_parity = 0;
     }
     const int batch = 4;
-    const int blocks = std::min(g->ntiles, g->sms * 8);
+    const int blocks = nblocks > 0 ? nblocks : std::min(g->ntiles, g->sms * 8);
     bool first = first_all;
     for (;;) {
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
@@ -982,7 +1623,7 @@ int frontier_sweeps(fm_grid *g, K kernel, bool first_all, int64_t *sweeps, int64
         for (int j = 0; j < batch; j++) {
             const int p = g->bq_parity;
             FM_TRY(tq_arm(g, g->d.bq, p));
-            kernel<<<blocks, dim3(TILE_W, BLK_Y), 0, g->stream>>>(g->d, p, first ? 1 : 0, g->flags + j);
+            kernel<<<blocks, block, 0, g->stream>>>(g->d, p, first ? 1 : 0, g->flags + j);
             first = false;
             g->bq_parity ^= 1;
         }
@@ -1005,24 +1646,86 @@ int frontier_sweeps(fm_grid *g, K kernel, bool first_all, int64_t *sweeps, int64
     return FM_OK;
 }
 
+// residual arcs for the BFS (all tiles, or the listed local-relabel region)
+int bfs_init(fm_grid *g, bool listed, int nlisted = 0) {
+    if (g->bfs_bits) {
+        const int rows = (listed ? nlisted : g->ntiles) * PT_H;
+        const int blocks = std::max(1, std::min((rows + 7) / 8, g->sms * 16));
+        bfs_init_bits_kernel<<<blocks, 256, 0, g->stream>>>(g->d, listed ? 1 : 0);
+    } else if (listed) {
+        bfs_init_local_kernel<<<std::max(1, std::min(nlisted, g->sms * 8)), 256, 0, g->stream>>>(g->d);
+    } else {
+        bfs_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
+    }
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    return FM_OK;
+}
+
+// BFS fixpoint over the tiles (all of them, or the ones queued in bq[bq_parity]).
+// bfs_bits == 2 (default): one persistent launch over the device ring queue; the
+// visit count lands in h_flags[8] and the kernel time between ev[2] / ev[3], both
+// collected by bfs_collect() after the caller's next stream sync.
+int bfs_sweeps(fm_grid *g, bool first_all) {
+    if (g->bfs_bits == 2) {
+        const int32_t *list0 = first_all ? nullptr : g->d.bq.list[g->bq_parity];
+        const int32_t *cnt0 = first_all ? nullptr : g->d.bq.cnt + 2 * g->bq_parity;
+        ringq_init_kernel<<<std::min((g->rq.cap + 255) / 256, g->sms * 8), 256, 0, g->stream>>>(g->rq, g->ntiles, list0, cnt0);
+        FM_CHECK_LAUNCH();
+        cudaEventRecord(g->ev[2], g->stream);
+        bfs_ring_kernel<<<g->sms * g->br_per_sm, 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+        FM_CHECK_LAUNCH();
+        cudaEventRecord(g->ev[3], g->stream);
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 8, g->rq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+        FM_TRY(tq_reset(g, g->d.bq));
+        g->bq_parity = 0;
+        g->st.launches += 2;
+        g->st.bfs_sweeps += 1;
+        g->st.bfs_launches += 1;
+        g->ring_stats_pending = true;
+        return FM_OK;
+    }
+    if (g->bfs_bits)
+        return frontier_sweeps(g, bfs_bits_kernel, first_all, &g->st.bfs_sweeps, &g->st.bfs_launches,
+                               &g->st.ms_bfs_kern, dim3(32 * BB_WARPS),
+                               std::min((g->ntiles + BB_WARPS - 1) / BB_WARPS, g->sms * g->bb_per_sm));
+    return frontier_sweeps(g, bfs_tile_kernel, first_all, &g->st.bfs_sweeps, &g->st.bfs_launches,
+                           &g->st.ms_bfs_kern);
+}
+
+// after a stream sync: fold the ring BFS's kernel time and visit count into the stats
+void bfs_collect(fm_grid *g) {
+    if (!g->ring_stats_pending) return;
+    g->ring_stats_pending = false;
+    g->st.ms_bfs_kern += elapsed_between(g->ev[2], g->ev[3]);
+    g->st.reserved[0] += g->h_flags[8];
+}
+
+int bfs_finalize(fm_grid *g) {
+    if (g->bfs_bits)
+        bfs_finalize_tiles_kernel<<<std::min(g->ntiles, g->sms * 8), 256, 0, g->stream>>>(g->d, g->acc + 4);
+    else
+        bfs_finalize_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 4);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    return FM_OK;
+}
+
 // global relabel + gap + marking; leaves the active-pixel count in g->active and
 // the tiles holding active pixels in the push work list (parity 0)
 int global_relabel(fm_grid *g) {
     cudaEventRecord(g->ev[0], g->stream);
-    bfs_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
-    FM_CHECK_LAUNCH();
-    g->st.launches++;
-    FM_TRY(frontier_sweeps(g, bfs_tile_kernel, true, &g->st.bfs_sweeps, &g->st.bfs_launches, &g->st.ms_bfs_kern));
+    FM_TRY(bfs_init(g, false));
+    FM_TRY(bfs_sweeps(g, true));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
     FM_TRY(tq_reset(g, g->d.pq));
     g->pq_parity = 0;
-    bfs_finalize_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 4);
-    FM_CHECK_LAUNCH();
-    g->st.launches++;
+    FM_TRY(bfs_finalize(g));
     FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 4, g->acc + 4, sizeof(unsigned long long) * 3,
                                   cudaMemcpyDeviceToHost, g->stream));
     cudaEventRecord(g->ev[1], g->stream);
     FM_TRY(sync_stream(g));
+    bfs_collect(g);
     g->st.ms_bfs += elapsed(g);
     g->active = (long long)g->h_acc[4];
     g->excess_total -= (long long)g->h_acc[5];
@@ -1048,11 +1751,9 @@ int local_relabel(fm_grid *g) {
     g->st.launches++;
     if (nr > g->ntiles / 4) return global_relabel(g);
     g->d.region = g->d_region;
-    bfs_init_local_kernel<<<std::max(1, std::min(nr, g->sms * 8)), 256, 0, g->stream>>>(g->d);
-    FM_CHECK_LAUNCH();
-    g->st.launches++;
+    FM_TRY(bfs_init(g, true, nr));
     g->bq_parity = 0;
-    int rc = frontier_sweeps(g, bfs_tile_kernel, false, &g->st.bfs_sweeps, &g->st.bfs_launches, &g->st.ms_bfs_kern);
+    int rc = bfs_sweeps(g, false);
     if (rc == FM_OK) {
         FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
         FM_TRY(tq_reset(g, g->d.pq));
@@ -1065,6 +1766,7 @@ int local_relabel(fm_grid *g) {
                                       cudaMemcpyDeviceToHost, g->stream));
         cudaEventRecord(g->ev[1], g->stream);
         FM_TRY(sync_stream(g));
+        bfs_collect(g);
         g->st.ms_bfs += elapsed(g);
         g->active = (long long)g->h_acc[4];
         g->excess_total -= (long long)g->h_acc[5];
@@ -1106,7 +1808,8 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
 // maxflow_seq.py:197-205 -- heuristic_period relabels between global relabels),
 // or until the launch cap; then cancel (opt-in), global relabel, gap, mark
 // (maxflow_par.py:195-229).
-constexpr int K_LOCAL_DEFAULT = 32;      // lock-free passes per tile visit
+constexpr int K_LOCAL_DEFAULT = 32;      // lock-free passes per tile visit (v2)
+constexpr int K_LOCAL_LIST_DEFAULT = 16; // passes per tile visit (v3: a pass over an empty list ends it)
 constexpr int MAX_LAUNCHES_DEFAULT = 16; // launch cap per round
 constexpr int RELABEL_DIV_DEFAULT = 16;  // relabel budget = H*W / div
 
@@ -1140,13 +1843,15 @@ int run_round_global(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int
 }
 
 int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int32_t *idle_out = nullptr) {
-    const int k_local = std::max(1, std::min(cycle_budget, g->k_local > 0 ? g->k_local : K_LOCAL_DEFAULT));
+    const int k_default = g->pr_kernel == 1 ? (g->k_local_list > 0 ? g->k_local_list : K_LOCAL_LIST_DEFAULT)
+                                            : (g->k_local > 0 ? g->k_local : K_LOCAL_DEFAULT);
+    const int k_local = std::max(1, std::min(cycle_budget, k_default));
     if (bfs_interval <= 0 && g->bfs_interval_env > 0) bfs_interval = g->bfs_interval_env;
     const int32_t cap = std::max(1, std::min((cycle_budget + k_local - 1) / k_local,
                                              bfs_interval > 0 ? bfs_interval : MAX_LAUNCHES_DEFAULT));
     const long long relabel_budget =
         std::max<long long>(1024, g->HW / (g->relabel_div > 0 ? g->relabel_div : RELABEL_DIV_DEFAULT));
-    const int blocks = std::min(g->ntiles, g->sms * g->pt_per_sm);
+    const int blocks = std::min(g->ntiles, g->sms * (g->pr_kernel == 1 ? g->pl_per_sm : g->pt_per_sm));
     int32_t done = 0;
     while (done < cap) {
         const int batch = std::min(4, cap - done);
@@ -1155,7 +1860,10 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
         for (int i = 0; i < batch; i++) {
             const int p = g->pq_parity;
             FM_TRY(tq_arm(g, g->d.pq, p));
-            pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, g->vote_mask, p, g->flags + i, g->acc + 10);
+            if (g->pr_kernel == 1)
+                pr_list_kernel<<<blocks, dim3(PT_W, PL_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10);
+            else
+                pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, g->vote_mask, p, g->flags + i, g->acc + 10);
             g->pq_parity ^= 1;
         }
         FM_CHECK_LAUNCH();
@@ -1203,13 +1911,15 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
         FM_CHECK_LAUNCH();
         g->st.launches++;
     }
-    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 10, g->acc + 10, sizeof(unsigned long long) * 2,
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 10, g->acc + 10, sizeof(unsigned long long) * 5,
                                   cudaMemcpyDeviceToHost, g->stream));
     cudaEventRecord(g->ev[1], g->stream);
     FM_TRY(sync_stream(g));
     g->st.ms_push += elapsed(g);
     g->st.pushes += (int64_t)g->h_acc[10];
     g->st.relabels += (int64_t)g->h_acc[11];
+    g->st.reserved[2] = (int64_t)g->h_acc[13];   // list-kernel passes (cumulative per solve)
+    g->st.reserved[3] = (int64_t)g->h_acc[14];   // list-kernel items
     const bool go_local = g->local_div > 0 && !(g->flags_solve & FM_GRID_GLOBAL_SWEEP) &&
                           !(g->flags_solve & FM_GRID_CANCEL_VIOLATIONS) &&
                           g->active <= g->HW / g->local_div && g->local_streak < g->local_max;
@@ -1315,6 +2025,10 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_OP_STEPS")) g->op_steps = std::max(1, atoi(v));
     if (const char *v = getenv("FM_OP_FUSED")) g->op_fused = atoi(v);
     if (const char *v = getenv("FM_VOTE")) g->vote_mask = std::max(1, atoi(v)) - 1;
+    if (const char *v = getenv("FM_PR_KERNEL")) g->pr_kernel = atoi(v);
+    if (const char *v = getenv("FM_BFS_BITS")) g->bfs_bits = atoi(v);
+    if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
+    if (const char *v = getenv("FM_K_LOCAL_LIST")) g->k_local_list = atoi(v);
     if (const char *v = getenv("FM_LOCAL_DIV")) g->local_div = atoi(v);
     if (const char *v = getenv("FM_LOCAL_MAX")) g->local_max = atoi(v);
     if (const char *v = getenv("FM_LOCAL_MARGIN")) g->local_margin = atoi(v);
@@ -1329,6 +2043,9 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         }
     }
     if (cudaMalloc((void **)&g->d.mask, n1) != cudaSuccess ||
+        cudaMalloc((void **)&g->d.rbits, sizeof(uint32_t) * 160 * (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->rq.flag, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->rq.ctr, sizeof(unsigned int) * 128) != cudaSuccess ||
         cudaMalloc((void **)&g->d.marked, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->d.cut, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
@@ -1368,6 +2085,20 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->sms = sms;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pt_per_sm, pr_tile_kernel, PT_W * PT_TY, 0);
     g->pt_per_sm = std::max(1, g->pt_per_sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pl_per_sm, pr_list_kernel, PT_W * PL_TY, 0);
+    g->pl_per_sm = std::max(1, g->pl_per_sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->bb_per_sm, bfs_bits_kernel, 32 * BB_WARPS, 0);
+    g->bb_per_sm = std::max(1, g->bb_per_sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->br_per_sm, bfs_ring_kernel, 32 * BB_WARPS, 0);
+    g->br_per_sm = std::max(1, std::min(g->br_per_sm, g->br_cap));
+    // ring capacity: every tile once + one reserved slot per resident warp
+    g->rq.cap = g->ntiles + g->sms * g->br_per_sm * BB_WARPS + 64;
+    if (cudaMalloc((void **)&g->rq.slot, sizeof(int32_t) * (size_t)g->rq.cap) != cudaSuccess ||
+        cudaMemset(g->rq.flag, 0, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess) {
+        fm_set_error("fm_grid_create: allocation failed");
+        fm_grid_destroy(g);
+        return FM_CUDA_ERROR;
+    }
     g->grid_blocks = (int)std::min<int64_t>((g->HW + 255) / 256, (int64_t)sms * 8);
     *out = g;
     return FM_OK;
@@ -1381,6 +2112,10 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
                          g->d_queues, g->in_caps};
     for (auto p : planes) if (p) cudaFree(p);
     if (g->d.mask) cudaFree(g->d.mask);
+    if (g->d.rbits) cudaFree(g->d.rbits);
+    if (g->rq.slot) cudaFree(g->rq.slot);
+    if (g->rq.flag) cudaFree(g->rq.flag);
+    if (g->rq.ctr) cudaFree(g->rq.ctr);
     if (g->d.marked) cudaFree(g->d.marked);
     if (g->d.cut) cudaFree(g->d.cut);
     if (g->d_band) cudaFree(g->d_band);
@@ -1577,13 +2312,12 @@ extern "C" int fm_grid_band_bfs(fm_grid *g, int32_t phase, int64_t *changed) {
     if (!g) { fm_set_error("fm_grid_band_bfs: null handle"); return FM_INVALID_ARG; }
     FM_CHECK_CUDA(cudaSetDevice(g->device));
     const int64_t before = g->st.reserved[0];
-    if (phase == 0) {
-        bfs_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
-        FM_CHECK_LAUNCH();
-        g->st.launches++;
+    if (phase == 0) FM_TRY(bfs_init(g, false));
+    FM_TRY(bfs_sweeps(g, phase == 0));
+    if (g->ring_stats_pending) {
+        FM_TRY(sync_stream(g));
+        bfs_collect(g);
     }
-    FM_TRY(frontier_sweeps(g, bfs_tile_kernel, phase == 0, &g->st.bfs_sweeps, &g->st.bfs_launches,
-                           &g->st.ms_bfs_kern));
     if (changed) *changed = g->st.reserved[0] - before;
     return FM_OK;
 }
@@ -1595,9 +2329,7 @@ extern "C" int fm_grid_band_finalize(fm_grid *g, int64_t *out) {
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
     FM_TRY(tq_reset(g, g->d.pq));
     g->pq_parity = 0;
-    bfs_finalize_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 4);
-    FM_CHECK_LAUNCH();
-    g->st.launches++;
+    FM_TRY(bfs_finalize(g));
     FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 4, g->acc + 4, sizeof(unsigned long long) * 3,
                                   cudaMemcpyDeviceToHost, g->stream));
     FM_TRY(sync_stream(g));
