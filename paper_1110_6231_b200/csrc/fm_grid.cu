@@ -7,6 +7,8 @@
 // (maxflow_seq.py:119-160, maxflow_par.py:220-226), and the minimal source-side
 // cut by a seeded residual reach.  See DESIGN.md.
 #include <algorithm>
+#include <thread>
+#include <vector>
 #include <climits>
 #include <stdio.h>
 #include <stdlib.h>
@@ -1007,6 +1009,8 @@ struct RingQ {
     int32_t *flag;          // per tile: queued
     unsigned int *ctr;      // [0] head, [32] tail, [64] pending, [96] tile visits that changed a border (one line each)
     int32_t cap;
+    int32_t rerun;          // a tile found stale again while in flight: 1 rerun at once, 0 requeue
+    int32_t ns0, ns1;       // idle-poll backoff (ns)
 };
 
 // initial content: tiles list0[0..*count0) (count0 != nullptr) or every tile
@@ -1051,7 +1055,7 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
         if (lane == 0) {
             const unsigned s = atomicAdd(q.ctr + 0, 1u) % (unsigned)q.cap;
             volatile int32_t *vs = q.slot + s;
-            for (unsigned ns = 32;; ns = min(ns * 2, 1024u)) {
+            for (unsigned ns = q.ns0;; ns = min(ns * 2, (unsigned)q.ns1)) {
                 tile = *vs;
                 if (tile >= 0) { *vs = -1; break; }
                 if (*(volatile unsigned *)(q.ctr + 64) == 0) break;
@@ -1145,8 +1149,18 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
                 if (b3 && txi + 1 < g.ntx && in(tile + 1)) ringq_push(q, tile + 1);
             }
             st = atomicCAS(q.flag + tile, 2, 0);
-            if (st == 3) { atomicExch(q.flag + tile, 2); __threadfence(); }
-            else atomicSub(q.ctr + 64, 1u);   // after the pushes: pending never reads 0 early
+            if (st == 3) {
+                if (q.rerun) { atomicExch(q.flag + tile, 2); __threadfence(); }
+                else {   // back of the queue (its neighbours get time to settle); still pending
+                    atomicExch(q.flag + tile, 1);
+                    const unsigned s2 = atomicAdd(q.ctr + 32, 1u);
+                    __threadfence();
+                    *(volatile int32_t *)(q.slot + (s2 % (unsigned)q.cap)) = tile;
+                    st = 0;
+                }
+            } else {
+                atomicSub(q.ctr + 64, 1u);   // after the pushes: pending never reads 0 early
+            }
         }
         again = __shfl_sync(0xffffffffu, st, 0) == 3;
         __syncwarp();
@@ -1526,6 +1540,7 @@ struct fm_grid {
     // host-input staging for *_host / begin
     int32_t *in_caps = nullptr;          // 6 * HW
     uint8_t *d_cut_tmp = nullptr;
+    uint8_t *h_cut_stage = nullptr;      // pinned bounce buffer for the cut (host-output calls)
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {};
@@ -1570,6 +1585,21 @@ struct fm_grid {
 };
 
 namespace {
+
+// host copy into freshly allocated (not yet faulted-in) memory: first-touch page
+// faults dominate, and they proceed in parallel across threads
+void parallel_memcpy(void *dst, const void *src, size_t n) {
+    const size_t chunk = (size_t)2 << 20;
+    const int nt = (int)std::min<size_t>(8, (n + chunk - 1) / chunk);
+    if (nt <= 1) { memcpy(dst, src, n); return; }
+    std::vector<std::thread> th;
+    const size_t per = (n + nt - 1) / nt;
+    for (int i = 0; i < nt; i++) {
+        const size_t a = (size_t)i * per, b = std::min(n, a + per);
+        if (a < b) th.emplace_back([=] { memcpy((char *)dst + a, (const char *)src + a, b - a); });
+    }
+    for (auto &t : th) t.join();
+}
 
 int sync_stream(fm_grid *g) {
     FM_CHECK_CUDA(cudaStreamSynchronize(g->stream));
@@ -2028,6 +2058,10 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_PR_KERNEL")) g->pr_kernel = atoi(v);
     if (const char *v = getenv("FM_BFS_BITS")) g->bfs_bits = atoi(v);
     if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
+    g->rq.rerun = 0; g->rq.ns0 = 128; g->rq.ns1 = 2048;
+    if (const char *v = getenv("FM_BR_RERUN")) g->rq.rerun = atoi(v);
+    if (const char *v = getenv("FM_BR_NS0")) g->rq.ns0 = atoi(v);
+    if (const char *v = getenv("FM_BR_NS1")) g->rq.ns1 = atoi(v);
     if (const char *v = getenv("FM_K_LOCAL_LIST")) g->k_local_list = atoi(v);
     if (const char *v = getenv("FM_LOCAL_DIV")) g->local_div = atoi(v);
     if (const char *v = getenv("FM_LOCAL_MAX")) g->local_max = atoi(v);
@@ -2126,6 +2160,7 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->flags) cudaFree(g->flags);
     if (g->h_acc) cudaFreeHost(g->h_acc);
     if (g->h_flags) cudaFreeHost(g->h_flags);
+    if (g->h_cut_stage) cudaFreeHost(g->h_cut_stage);
     for (auto e : g->ev) if (e) cudaEventDestroy(e);
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
     delete g;
@@ -2188,11 +2223,16 @@ extern "C" int fm_grid_solve_host(fm_grid *g, const int32_t *capR, const int32_t
                           cycle_budget, bfs_interval, flags, flow_out, nullptr);
     float d2h = 0.f;
     if (rc == FM_OK && cut_out && !(flags & FM_GRID_NO_CUT)) {
+        // D2H through a pinned bounce buffer (pageable D2H runs at a few GB/s), then one
+        // host memcpy into the caller's array
         cudaEventRecord(a, g->stream);
-        if (cudaMemcpyAsync(cut_out, g->d.cut, HW, cudaMemcpyDeviceToHost, g->stream) != cudaSuccess)
+        if (!g->h_cut_stage && cudaMallocHost((void **)&g->h_cut_stage, HW) != cudaSuccess) g->h_cut_stage = nullptr;
+        uint8_t *dst = g->h_cut_stage ? g->h_cut_stage : cut_out;
+        if (cudaMemcpyAsync(dst, g->d.cut, HW, cudaMemcpyDeviceToHost, g->stream) != cudaSuccess)
             rc = FM_CUDA_ERROR;
         cudaEventRecord(b, g->stream);
         cudaEventSynchronize(b);
+        if (rc == FM_OK && dst != cut_out) parallel_memcpy(cut_out, dst, HW);
         cudaEventElapsedTime(&d2h, a, b);
     }
     cudaEventDestroy(a);

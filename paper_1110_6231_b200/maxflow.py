@@ -63,11 +63,12 @@ class GridSolver:
 
     def solve_host(self, caps, cycle_budget=DEFAULT_CYCLE_BUDGET, bfs_interval=DEFAULT_BFS_INTERVAL,
                    want_cut=True, cancel_violations=False, precancel=True, global_sweep=False):
-        """Host int32 planes in, (flow, cut uint8[H,W] or None, stats) out; the
+        """Host int32 planes in, (flow, cut bool[H,W] or None, stats) out; the
         host<->device copies are part of the call."""
         caps = [np.ascontiguousarray(a, dtype=np.int32) for a in caps]
         flow = ctypes.c_int64()
-        cut = np.zeros((self.H, self.W), np.uint8) if want_cut else None
+        # bool and uint8 share the 0/1 byte layout: the cut lands in its final array
+        cut = np.empty((self.H, self.W), np.bool_) if want_cut else None
         st = _lib.FmStats()
         rc = _lib.load().fm_grid_solve_host(
             self._h, *[_lib.ptr(a) for a in caps], int(cycle_budget), int(bfs_interval),
@@ -257,9 +258,8 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
                                               stream=torch.cuda.current_stream(net.caps[0].device))
             cut = cut_t.bool() if cut_t is not None else None
         else:
-            flow, cut8, stats = solver.solve_host(net.host_caps(), cycle_budget, bfs_interval,
-                                                  want_cut=want_cut, cancel_violations=cancel_violations)
-            cut = cut8.astype(bool) if cut8 is not None else None
+            flow, cut, stats = solver.solve_host(net.host_caps(), cycle_budget, bfs_interval,
+                                                 want_cut=want_cut, cancel_violations=cancel_violations)
     else:
         solver.begin(net.host_caps(), cancel_violations=cancel_violations)
         while True:
