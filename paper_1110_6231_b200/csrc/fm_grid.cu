@@ -1442,6 +1442,96 @@ __global__ void __launch_bounds__(256) cut_tile_kernel(GridDev g, int parity, in
     }  // tile loop
 }
 
+// ----------------------------------------------------------------------------
+// K3 bit-parallel (default): the cut closure with the tile's incoming residual arcs
+// as bit planes (lane = tile row, bit = column), one warp per tile:
+//     S |= ((S >> 1) & inR) | ((S << 1) & inL) | (S_below & inD) | (S_above & inU)
+// (+ the halo's cut bits) until no word changes.  The cut bytes stay the exchanged /
+// returned representation; a visit ORs in the pixels it adds.  cut_tile_kernel
+// stays behind FM_BFS_BITS=0.
+// ----------------------------------------------------------------------------
+__global__ void cut_init_bits_kernel(GridDev g) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nrows = (int64_t)g.ntx * g.nty * PT_H;
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int tile = (int)(w / PT_H), lr = (int)(w % PT_H);
+        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+        const int r = tyi * PT_H + lr, c = txi * PT_W + lane;
+        const bool in = r < g.H && c < g.W && !is_ghost_row(g, r);
+        const int64_t p = (int64_t)r * g.W + c;
+        const bool aR = in && c + 1 < g.W && g.rL[p + 1] > 0;     // residual arc (p+1) -> p
+        const bool aL = in && c > 0 && g.rR[p - 1] > 0;
+        const bool aD = in && r + 1 < g.H && g.rU[p + g.W] > 0;
+        const bool aU = in && r > 0 && g.rD[p - g.W] > 0;
+        const bool seed = in && (g.e[p] > 0 || g.cS[p] - g.rS[p] > 0);
+        const uint32_t wd[5] = {__ballot_sync(0xffffffffu, aR), __ballot_sync(0xffffffffu, aL),
+                                __ballot_sync(0xffffffffu, aD), __ballot_sync(0xffffffffu, aU),
+                                __ballot_sync(0xffffffffu, seed)};
+        uint32_t *B = g.rbits + (size_t)tile * 160 + lr;
+        if (lane < 5) B[lane * 32] = wd[lane];
+        if (r < g.H && c < g.W) g.cut[p] = seed ? 1 : 0;
+    }
+}
+
+__global__ void __launch_bounds__(32 * BB_WARPS) cut_bits_kernel(GridDev g, int parity, int all_tiles,
+                                                               int32_t *changed_count) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int tile = 0;
+        if (lane == 0) tile = tq_take(g.bq, parity, all_tiles, g.ntx * g.nty);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile < 0) break;
+        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+        const int r0 = tyi * PT_H, c0 = txi * PT_W;
+        const int cl = c0 + lane, rl = r0 + lane;
+        const uint32_t *B = g.rbits + (size_t)tile * 160;
+        const uint32_t iR = B[lane], iL = B[32 + lane], iD = B[64 + lane], iU = B[96 + lane];
+        // current cut words of the tile (row i built by a ballot over its 32 columns)
+        uint32_t S = 0;
+#pragma unroll 8
+        for (int i = 0; i < PT_H; i++) {
+            const int r = r0 + i;
+            const bool b = r < g.H && cl < g.W && __ldcg(g.cut + (int64_t)r * g.W + cl);
+            const uint32_t wv = __ballot_sync(0xffffffffu, b);
+            if (lane == i) S = wv;
+        }
+        const uint32_t S0 = S;
+        const uint32_t top = __ballot_sync(0xffffffffu, r0 > 0 && cl < g.W && __ldcg(g.cut + (int64_t)(r0 - 1) * g.W + cl));
+        const uint32_t bot = __ballot_sync(0xffffffffu, r0 + PT_H < g.H && cl < g.W &&
+                                                        __ldcg(g.cut + (int64_t)(r0 + PT_H) * g.W + cl));
+        const bool hl = c0 > 0 && rl < g.H && __ldcg(g.cut + (int64_t)rl * g.W + c0 - 1);
+        const bool hr = c0 + PT_W < g.W && rl < g.H && __ldcg(g.cut + (int64_t)rl * g.W + c0 + PT_W);
+        if (hr) S |= iR & 0x80000000u;
+        if (hl) S |= iL & 1u;
+        if (lane == 0) S |= top & iU;
+        if (lane == 31) S |= bot & iD;
+        for (;;) {
+            const uint32_t up = __shfl_up_sync(0xffffffffu, S, 1), dn = __shfl_down_sync(0xffffffffu, S, 1);
+            uint32_t N = S | ((S >> 1) & iR) | ((S << 1) & iL);
+            if (lane > 0) N |= up & iU;
+            if (lane < 31) N |= dn & iD;
+            const bool ch = N != S;
+            S = N;
+            if (!__any_sync(0xffffffffu, ch)) break;
+        }
+        const uint32_t add = S & ~S0;
+        const uint32_t rows = __ballot_sync(0xffffffffu, add != 0);
+        for (uint32_t x = rows; x; x &= x - 1) {
+            const int i = __ffs(x) - 1;
+            const uint32_t a = __shfl_sync(0xffffffffu, add, i);
+            if ((a >> lane) & 1) g.cut[(int64_t)(r0 + i) * g.W + cl] = 1;
+        }
+        const int b0 = rows & 1, b1 = (rows >> 31) & 1;
+        const int b2 = __any_sync(0xffffffffu, add & 1u), b3 = __any_sync(0xffffffffu, add >> 31);
+        if (lane == 0 && (b0 | b1 | b2 | b3)) {
+            flag_changed_borders(g, tile, tyi, txi, b0, b1, b2, b3, parity ^ 1);
+            atomicAdd(changed_count, 1);
+        }
+        __syncwarp();
+    }
+}
+
 // sum of e over all pixels (flow = sum capS - sum e: node conservation)
 __global__ void sum_e_kernel(GridDev g, unsigned long long *acc) {
     const int64_t HW = (int64_t)g.H * g.W;
@@ -1971,15 +2061,33 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     return FM_OK;
 }
 
-int compute_cut(fm_grid *g, uint8_t *cut_out_dev) {
-    cudaEventRecord(g->ev[0], g->stream);
-    cut_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
+// seeded residual reach: seeds + residual masks, then tile fixpoint sweeps
+int cut_init(fm_grid *g) {
+    if (g->bfs_bits) {
+        const int rows = g->ntiles * PT_H;
+        cut_init_bits_kernel<<<std::max(1, std::min((rows + 7) / 8, g->sms * 16)), 256, 0, g->stream>>>(g->d);
+    } else {
+        cut_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
+    }
     FM_CHECK_LAUNCH();
     g->st.launches++;
+    return FM_OK;
+}
+
+int cut_sweeps(fm_grid *g, bool first_all) {
     double cut_kern = 0.0;
     int64_t cut_launches = 0;
-    FM_TRY(frontier_sweeps(g, cut_tile_kernel, true, &g->st.cut_sweeps, &cut_launches, &cut_kern));
-    g->st.launches += 0;
+    if (g->bfs_bits)
+        return frontier_sweeps(g, cut_bits_kernel, first_all, &g->st.cut_sweeps, &cut_launches, &cut_kern,
+                               dim3(32 * BB_WARPS),
+                               std::min((g->ntiles + BB_WARPS - 1) / BB_WARPS, g->sms * g->bb_per_sm));
+    return frontier_sweeps(g, cut_tile_kernel, first_all, &g->st.cut_sweeps, &cut_launches, &cut_kern);
+}
+
+int compute_cut(fm_grid *g, uint8_t *cut_out_dev) {
+    cudaEventRecord(g->ev[0], g->stream);
+    FM_TRY(cut_init(g));
+    FM_TRY(cut_sweeps(g, true));
     if (cut_out_dev && cut_out_dev != g->d.cut)
         FM_CHECK_CUDA(cudaMemcpyAsync(cut_out_dev, g->d.cut, (size_t)g->HW, cudaMemcpyDeviceToDevice, g->stream));
     cudaEventRecord(g->ev[1], g->stream);
@@ -2411,14 +2519,8 @@ extern "C" int fm_grid_band_cut(fm_grid *g, int32_t phase, int64_t *changed) {
     if (!g) { fm_set_error("fm_grid_band_cut: null handle"); return FM_INVALID_ARG; }
     FM_CHECK_CUDA(cudaSetDevice(g->device));
     const int64_t before = g->st.reserved[0];
-    if (phase == 0) {
-        cut_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
-        FM_CHECK_LAUNCH();
-        g->st.launches++;
-    }
-    double kern = 0.0;
-    int64_t launches = 0;
-    FM_TRY(frontier_sweeps(g, cut_tile_kernel, phase == 0, &g->st.cut_sweeps, &launches, &kern));
+    if (phase == 0) FM_TRY(cut_init(g));
+    FM_TRY(cut_sweeps(g, phase == 0));
     if (changed) *changed = g->st.reserved[0] - before;
     return FM_OK;
 }
