@@ -525,34 +525,35 @@ __device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int l
     return e > 0 && hp < V;
 }
 
-__global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev g, int k_local, int steps, int fused,
-                                                                       int parity, int32_t *processed,
-                                                                       unsigned long long *ops) {
-    __shared__ int32_t s_e[PT_H * PT_W];
-    __shared__ int32_t s_h[(PT_H + 2) * (PT_W + 2)];
-    __shared__ int32_t s_r[4][PT_H * PT_W];   // R, L, D, U
-    __shared__ int32_t s_t[PT_H * PT_W];
-    __shared__ uint8_t s_f[PT_H * PT_W];      // bit 0: residual arc to s, bit 1: ghost row
-    __shared__ uint16_t s_list[2][PT_H * PT_W];
-    __shared__ int s_cnt[3];
-    __shared__ int s_nbr;
-    __shared__ int s_tile;
+struct PlSmem {
+    int32_t e[PT_H * PT_W];
+    int32_t h[(PT_H + 2) * (PT_W + 2)];
+    int32_t r[4][PT_H * PT_W];   // R, L, D, U
+    int32_t t[PT_H * PT_W];
+    uint8_t f[PT_H * PT_W];      // bit 0: residual arc to s, bit 1: ghost row
+    uint16_t list[2][PT_H * PT_W];
+    int cnt[3];
+    int nbr;
+    int tile;
+    int flag;
+    long long red[PL_NT / 32];
+};
+
+struct PlCounters {
+    long long pushes = 0, relabels = 0, passes = 0, items = 0;
+};
+
+// One visit of `tile`: load (folding the inboxes), list-driven passes, write back.
+// Returns (CTA-uniform) whether the tile still holds an active pixel; S.nbr = the
+// neighbour tiles whose inboxes received flow.  Starts and ends with a barrier.
+__device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, int k_local, int steps,
+                                         int fused, PlCounters &C) {
     constexpr int HS = PT_W + 2;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * PT_W + tx;
     const int V = g.V;
-    long long pushes = 0, relabels = 0, passes = 0, items = 0;
-    for (;;) {
-    __syncthreads();
-    if (tid == 0) {
-        s_tile = tq_take(g.pq, parity, 0, 0);
-        s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
-        s_nbr = 0;
-    }
-    __syncthreads();
-    const int tile = s_tile;
-    if (tile < 0) break;
+    if (tid == 0) { S.cnt[0] = S.cnt[1] = S.cnt[2] = 0; S.nbr = 0; }
     const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
-    const PlTile T{s_e, s_h, s_t, s_r, s_f, &s_nbr, tyi * PT_H, txi * PT_W};
+    const PlTile T{S.e, S.h, S.t, S.r, S.f, &S.nbr, tyi * PT_H, txi * PT_W};
     const int r0 = T.r0, c0 = T.c0;
 #pragma unroll
     for (int k = 0; k < PL_ROWS; k++) {
@@ -567,17 +568,17 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev
             if (tx == PT_W - 1 && c + 1 < g.W) { const int32_t d = atomicExch(g.inflow_h + p, 0); e += d; rr += d; }
             if (lr == 0 && r > 0) { const int32_t d = atomicExch(g.inflow_v + p, 0); e += d; ru += d; }
             if (lr == PT_H - 1 && r + 1 < g.H) { const int32_t d = atomicExch(g.inflow_v + p, 0); e += d; rd += d; }
-            s_e[li] = e;
-            s_h[(lr + 1) * HS + tx + 1] = g.h[p];
-            s_r[0][li] = rr; s_r[1][li] = rl; s_r[2][li] = rd; s_r[3][li] = ru;
-            s_t[li] = g.rT[p];
-            s_f[li] = (g.rS[p] > 0 ? 1 : 0) | (is_ghost_row(g, r) ? 2 : 0);
+            S.e[li] = e;
+            S.h[(lr + 1) * HS + tx + 1] = g.h[p];
+            S.r[0][li] = rr; S.r[1][li] = rl; S.r[2][li] = rd; S.r[3][li] = ru;
+            S.t[li] = g.rT[p];
+            S.f[li] = (g.rS[p] > 0 ? 1 : 0) | (is_ghost_row(g, r) ? 2 : 0);
         } else {
-            s_e[li] = 0;
-            s_h[(lr + 1) * HS + tx + 1] = V;
-            s_r[0][li] = s_r[1][li] = s_r[2][li] = s_r[3][li] = 0;
-            s_t[li] = 0;
-            s_f[li] = 2;
+            S.e[li] = 0;
+            S.h[(lr + 1) * HS + tx + 1] = V;
+            S.r[0][li] = S.r[1][li] = S.r[2][li] = S.r[3][li] = 0;
+            S.t[li] = 0;
+            S.f[li] = 2;
         }
     }
     if (tid < 4 * PT_W) {   // halo snapshot of neighbour heights
@@ -587,34 +588,34 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev
         else if (side == 1) { r = r0 + PT_H; cc = c0 + i; hr = PT_H + 1; hc = i + 1; }
         else if (side == 2) { r = r0 + i; cc = c0 - 1; hr = i + 1; hc = 0; }
         else { r = r0 + i; cc = c0 + PT_W; hr = i + 1; hc = PT_W + 1; }
-        s_h[hr * HS + hc] = (r >= 0 && r < g.H && cc >= 0 && cc < g.W) ? g.h[(int64_t)r * g.W + cc] : V;
+        S.h[hr * HS + hc] = (r >= 0 && r < g.H && cc >= 0 && cc < g.W) ? g.h[(int64_t)r * g.W + cc] : V;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < PL_ROWS; k++) {
         const int lr = ty + k * PL_TY;
         const int li = lr * PT_W + tx;
-        pl_append_warp(s_e[li] > 0 && s_h[(lr + 1) * HS + tx + 1] < V && !(s_f[li] & 2), li, &s_cnt[0], s_list[0]);
+        pl_append_warp(S.e[li] > 0 && S.h[(lr + 1) * HS + tx + 1] < V && !(S.f[li] & 2), li, &S.cnt[0], S.list[0]);
     }
     // dense passes: the whole CTA, one barrier per pass
     int it = 0;
     bool solo = false;
     for (; it < k_local; it++) {
         __syncthreads();
-        const int n = s_cnt[it % 3];
+        const int n = S.cnt[it % 3];
         if (n == 0) break;
         if (n <= 32) { solo = true; break; }
-        passes++;
-        items += n;
-        int *cnt_next = &s_cnt[(it + 1) % 3];
-        if (tid == 0) s_cnt[(it + 2) % 3] = 0;
-        const uint16_t *lin = s_list[it & 1];
-        uint16_t *lout = s_list[(it + 1) & 1];
+        C.passes++;
+        C.items += n;
+        int *cnt_next = &S.cnt[(it + 1) % 3];
+        if (tid == 0) S.cnt[(it + 2) % 3] = 0;
+        const uint16_t *lin = S.list[it & 1];
+        uint16_t *lout = S.list[(it + 1) & 1];
         for (int base = 0; base < n; base += PL_NT) {
             if (base + (tid & ~31) >= n) break;        // warp-uniform
             const int i = base + tid;
             int recv = -1;
-            const bool keep = i < n && pl_item(g, T, lin[i], steps, fused, cnt_next, lout, &recv, pushes, relabels);
+            const bool keep = i < n && pl_item(g, T, lin[i], steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels);
             pl_append_warp(keep, i < n ? lin[i] : 0, cnt_next, lout);
             pl_append_warp(recv >= 0, recv, cnt_next, lout);
         }
@@ -623,20 +624,20 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev
     if (solo && tid < 32) {
         for (; it < k_local; it++) {
             __syncwarp();
-            const int n = s_cnt[it % 3];
+            const int n = S.cnt[it % 3];
             if (n == 0) break;
-            passes++;
-            items += n;
-            int *cnt_next = &s_cnt[(it + 1) % 3];
-            if (tid == 0) s_cnt[(it + 2) % 3] = 0;
-            const uint16_t *lin = s_list[it & 1];
-            uint16_t *lout = s_list[(it + 1) & 1];
+            C.passes++;
+            C.items += n;
+            int *cnt_next = &S.cnt[(it + 1) % 3];
+            if (tid == 0) S.cnt[(it + 2) % 3] = 0;
+            const uint16_t *lin = S.list[it & 1];
+            uint16_t *lout = S.list[(it + 1) & 1];
             __syncwarp();
             for (int base = 0; base < n; base += 32) {
                 const int i = base + tid;
                 int recv = -1;
                 const int li = i < n ? lin[i] : 0;
-                const bool keep = i < n && pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, pushes, relabels);
+                const bool keep = i < n && pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels);
                 pl_append_warp(keep, li, cnt_next, lout);
                 pl_append_warp(recv >= 0, recv, cnt_next, lout);
             }
@@ -651,32 +652,47 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev
         const int li = lr * PT_W + tx;
         if (r < g.H && c < g.W) {
             const int64_t p = (int64_t)r * g.W + c;
-            const int32_t e = s_e[li], h = s_h[(lr + 1) * HS + tx + 1];
+            const int32_t e = S.e[li], h = S.h[(lr + 1) * HS + tx + 1];
             g.e[p] = e;
             g.h[p] = h;
-            g.rR[p] = s_r[0][li]; g.rL[p] = s_r[1][li];
-            g.rD[p] = s_r[2][li]; g.rU[p] = s_r[3][li];
-            g.rT[p] = s_t[li];
-            act |= (e > 0 && h < V && !(s_f[li] & 2));
+            g.rR[p] = S.r[0][li]; g.rL[p] = S.r[1][li];
+            g.rD[p] = S.r[2][li]; g.rU[p] = S.r[3][li];
+            g.rT[p] = S.t[li];
+            act |= (e > 0 && h < V && !(S.f[li] & 2));
         }
     }
-    const int any_act = __syncthreads_or(act);
-    if (tid == 0) {
-        if (any_act) tq_push(g.pq, parity ^ 1, tile);
-        g.touched[tile] = 1;
-        const int nb = s_nbr;
-        if (nb & 1) { tq_push(g.pq, parity ^ 1, tile + 1); g.touched[tile + 1] = 1; }
-        if (nb & 2) { tq_push(g.pq, parity ^ 1, tile - 1); g.touched[tile - 1] = 1; }
-        if (nb & 4) { tq_push(g.pq, parity ^ 1, tile + g.ntx); g.touched[tile + g.ntx] = 1; }
-        if (nb & 8) { tq_push(g.pq, parity ^ 1, tile - g.ntx); g.touched[tile - g.ntx] = 1; }
-        atomicAdd(processed, 1);
+    return __syncthreads_or(act) != 0;
+}
+
+__global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev g, int k_local, int steps, int fused,
+                                                                       int parity, int32_t *processed,
+                                                                       unsigned long long *ops) {
+    __shared__ PlSmem S;
+    const int tid = threadIdx.y * PT_W + threadIdx.x;
+    PlCounters C;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) S.tile = tq_take(g.pq, parity, 0, 0);
+        __syncthreads();
+        const int tile = S.tile;
+        if (tile < 0) break;
+        const bool any_act = pl_visit(g, S, tile, k_local, steps, fused, C);
+        if (tid == 0) {
+            if (any_act) tq_push(g.pq, parity ^ 1, tile);
+            g.touched[tile] = 1;
+            const int nb = S.nbr;
+            if (nb & 1) { tq_push(g.pq, parity ^ 1, tile + 1); g.touched[tile + 1] = 1; }
+            if (nb & 2) { tq_push(g.pq, parity ^ 1, tile - 1); g.touched[tile - 1] = 1; }
+            if (nb & 4) { tq_push(g.pq, parity ^ 1, tile + g.ntx); g.touched[tile + g.ntx] = 1; }
+            if (nb & 8) { tq_push(g.pq, parity ^ 1, tile - g.ntx); g.touched[tile - g.ntx] = 1; }
+            atomicAdd(processed, 1);
+        }
     }
-    }  // tile loop
-    block_add_i64<PL_NT / 32>(pushes, ops + 0);
-    block_add_i64<PL_NT / 32>(relabels, ops + 1);
+    block_add_i64<PL_NT / 32>(C.pushes, ops + 0);
+    block_add_i64<PL_NT / 32>(C.relabels, ops + 1);
     if (tid == 0) {   // diagnostics: passes run and list items dealt (ops[3], ops[4]) -- thread 0 saw them all
-        if (passes) atomicAdd(ops + 3, (unsigned long long)passes);
-        if (items) atomicAdd(ops + 4, (unsigned long long)items);
+        if (C.passes) atomicAdd(ops + 3, (unsigned long long)C.passes);
+        if (C.items) atomicAdd(ops + 4, (unsigned long long)C.items);
     }
 }
 
@@ -1025,7 +1041,10 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
             q.slot[i] = -1;
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) { q.ctr[0] = 0; q.ctr[32] = n0; q.ctr[64] = n0; q.ctr[96] = 0; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        q.ctr[0] = 0; q.ctr[32] = n0; q.ctr[64] = n0; q.ctr[96] = 0;
+        q.ctr[128] = 0; q.ctr[160] = 0; q.ctr[161] = 0; q.ctr[224] = n0;
+    }
 }
 
 // Tile states: 0 idle, 1 queued, 2 in flight, 3 in flight + stale again.  A tile is
@@ -1165,6 +1184,97 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
         again = __shfl_sync(0xffffffffu, st, 0) == 3;
         __syncwarp();
         }  // while again
+    }
+}
+
+// ----------------------------------------------------------------------------
+// K1 as ONE persistent launch per round (default): pl_visit over a device ring
+// queue of tiles instead of a sequence of launches over double-buffered lists.
+// A tile is queued when it holds active pixels after a visit or when flow is
+// parked in its inbox; CTAs take tiles until the queue drains (round over: every
+// pixel is inactive or written off) or the round's relabel budget / visit cap is
+// reached (stop flag).  Flow crosses any number of tiles within the launch, so the
+// tail rounds no longer pay one launch + host sync per tile hop.
+// States as in the BFS ring (0 idle, 1 queued, 2 in flight, 3 in flight + more
+// inflow); only the owner moves a tile out of 2/3, so a tile is never in the queue
+// twice and never visited by two CTAs at once (its smem copy is the only writer).
+// ctr: [0] head [32] tail [64] pending [96] visits [128] stop [160] relabels (u64)
+//      [224] initial tiles.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ void ring_enqueue(const RingQ &q, int t) {
+    const unsigned s = atomicAdd(q.ctr + 32, 1u);
+    __threadfence();
+    *(volatile int32_t *)(q.slot + (s % (unsigned)q.cap)) = t;
+}
+
+__global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_ring_kernel(GridDev g, RingQ q, int k_local, int steps,
+                                                                       int fused, long long relabel_budget,
+                                                                       int visit_mult, unsigned long long *ops) {
+    __shared__ PlSmem S;
+    const int tid = threadIdx.y * PT_W + threadIdx.x;
+    volatile unsigned *stop = q.ctr + 128;
+    unsigned long long *rel_total = (unsigned long long *)(q.ctr + 160);
+    PlCounters C;
+    const unsigned visit_cap = (unsigned)max(64, visit_mult * (int)__ldcg(q.ctr + 224));
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            int tile = -1;
+            if (!*stop) {
+                const unsigned s = atomicAdd(q.ctr + 0, 1u) % (unsigned)q.cap;
+                volatile int32_t *vs = q.slot + s;
+                for (unsigned ns = q.ns0;; ns = min(ns * 2, (unsigned)q.ns1)) {
+                    tile = *vs;
+                    if (tile >= 0) { *vs = -1; break; }
+                    if (*(volatile unsigned *)(q.ctr + 64) == 0 || *stop) break;
+                    __nanosleep(ns);
+                }
+                if (tile >= 0) { atomicExch(q.flag + tile, 2); __threadfence(); }
+            }
+            S.tile = tile;
+        }
+        __syncthreads();
+        const int tile = S.tile;
+        if (tile < 0) break;
+        const long long rel0 = C.relabels;
+        const bool act = pl_visit(g, S, tile, k_local, steps, fused, C);
+        // this visit's relabels, CTA-wide (for the round's relabel budget)
+        long long dr = C.relabels - rel0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dr += __shfl_xor_sync(0xffffffffu, dr, o);
+        if ((tid & 31) == 0) S.red[tid >> 5] = dr;
+        __syncthreads();
+        if (tid == 0) {
+            long long vr = 0;
+            for (int w = 0; w < PL_NT / 32; w++) vr += S.red[w];
+            g.touched[tile] = 1;
+            const int nb = S.nbr;
+            const int nts[4] = {tile + 1, tile - 1, tile + g.ntx, tile - g.ntx};
+            for (int d = 0; d < 4; d++) {
+                if (!((nb >> d) & 1)) continue;
+                const int t = nts[d];
+                g.touched[t] = 1;
+                for (;;) {   // queue t, or mark it for a requeue by its owner
+                    const int o = atomicCAS(q.flag + t, 0, 1);
+                    if (o == 0) { atomicAdd(q.ctr + 64, 1u); ring_enqueue(q, t); break; }
+                    if (o != 2 || atomicCAS(q.flag + t, 2, 3) == 2) break;
+                }
+            }
+            const unsigned long long rt = atomicAdd(rel_total, (unsigned long long)vr) + (unsigned long long)vr;
+            const unsigned nv = atomicAdd(q.ctr + 96, 1u) + 1;
+            if (rt >= (unsigned long long)relabel_budget || nv >= visit_cap) *stop = 1;
+            // leave flight: back to the queue if still active or fed while in flight
+            int o = atomicCAS(q.flag + tile, 2, act ? 1 : 0);
+            if (o == 3) { atomicExch(q.flag + tile, 1); o = 2; ring_enqueue(q, tile); }
+            else if (act) ring_enqueue(q, tile);
+            else atomicSub(q.ctr + 64, 1u);
+        }
+    }
+    block_add_i64<PL_NT / 32>(C.pushes, ops + 0);
+    block_add_i64<PL_NT / 32>(C.relabels, ops + 1);
+    if (tid == 0) {
+        if (C.passes) atomicAdd(ops + 3, (unsigned long long)C.passes);
+        if (C.items) atomicAdd(ops + 4, (unsigned long long)C.items);
     }
 }
 
@@ -1650,7 +1760,11 @@ struct fm_grid {
     int br_per_sm = 8;                   // resident bfs_ring CTAs per SM (occupancy query, <= br_cap)
     int br_cap = 6;                      // env FM_BR_CAP
     RingQ rq{};                          // device work queue of the persistent BFS
+    RingQ prq{};                         // device work queue of the persistent push round
+    int pr_ring = 0;                     // 1: one persistent pr_ring_kernel launch per round (env FM_PR_RING; experimental, slower)
+    int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (env FM_VISIT_MULT)
     bool ring_stats_pending = false;
+    bool pr_stats_pending = false;
     int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (env FM_PR_KERNEL)
     int pl_per_sm = 6;                   // resident pr_list CTAs per SM (occupancy query)
     int k_local_list = 0;                // passes per visit of the list kernel (env FM_K_LOCAL_LIST)
@@ -2015,6 +2129,33 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
     return FM_OK;
 }
 
+// One coordinator round as a single persistent launch over the device tile queue
+// (pr_ring_kernel), seeded with the tiles the last relabel found active.  Kernel
+// time and visit count are collected after the caller's stream sync.
+int run_round_ring(fm_grid *g, int32_t cycle_budget) {
+    const int k_default = g->k_local_list > 0 ? g->k_local_list : K_LOCAL_LIST_DEFAULT;
+    const int k_local = std::max(1, std::min(cycle_budget, k_default));
+    const long long relabel_budget =
+        std::max<long long>(1024, g->HW / (g->relabel_div > 0 ? g->relabel_div : RELABEL_DIV_DEFAULT));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->prq.flag, 0, sizeof(int32_t) * (size_t)g->ntiles, g->stream));
+    ringq_init_kernel<<<std::min((g->prq.cap + 255) / 256, g->sms * 8), 256, 0, g->stream>>>(
+        g->prq, g->ntiles, g->d.pq.list[0], g->d.pq.cnt + 0);
+    FM_CHECK_LAUNCH();
+    cudaEventRecord(g->ev[2], g->stream);
+    pr_ring_kernel<<<g->sms * g->pl_per_sm, dim3(PT_W, PL_TY), 0, g->stream>>>(
+        g->d, g->prq, k_local, g->op_steps, g->op_fused, relabel_budget, g->visit_mult, g->acc + 10);
+    FM_CHECK_LAUNCH();
+    cudaEventRecord(g->ev[3], g->stream);
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 9, g->prq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+    integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
+    FM_CHECK_LAUNCH();
+    g->st.launches += 3;
+    g->st.pr_launches += 1;
+    g->st.pr_sweeps += 1;
+    g->pr_stats_pending = true;
+    return FM_OK;
+}
+
 int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     const fm_stats before = g->st;
     const long long active_before = g->active;
@@ -2023,6 +2164,8 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     int32_t sweeps = 0;
     if (g->flags_solve & FM_GRID_GLOBAL_SWEEP) {
         FM_TRY(run_round_global(g, cycle_budget, bfs_interval, &sweeps));
+    } else if (g->pr_ring && g->pr_kernel == 1 && bfs_interval <= 0 && g->bfs_interval_env <= 0) {
+        FM_TRY(run_round_ring(g, cycle_budget));
     } else {
         FM_TRY(run_round_tiles(g, cycle_budget, bfs_interval));
     }
@@ -2035,6 +2178,11 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
                                   cudaMemcpyDeviceToHost, g->stream));
     cudaEventRecord(g->ev[1], g->stream);
     FM_TRY(sync_stream(g));
+    if (g->pr_stats_pending) {
+        g->pr_stats_pending = false;
+        g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
+        g->st.pr_tiles += g->h_flags[9];
+    }
     g->st.ms_push += elapsed(g);
     g->st.pushes += (int64_t)g->h_acc[10];
     g->st.relabels += (int64_t)g->h_acc[11];
@@ -2166,6 +2314,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_PR_KERNEL")) g->pr_kernel = atoi(v);
     if (const char *v = getenv("FM_BFS_BITS")) g->bfs_bits = atoi(v);
     if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
+    if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
+    if (const char *v = getenv("FM_VISIT_MULT")) g->visit_mult = std::max(1, atoi(v));
     g->rq.rerun = 0; g->rq.ns0 = 128; g->rq.ns1 = 2048;
     if (const char *v = getenv("FM_BR_RERUN")) g->rq.rerun = atoi(v);
     if (const char *v = getenv("FM_BR_NS0")) g->rq.ns0 = atoi(v);
@@ -2187,7 +2337,9 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (cudaMalloc((void **)&g->d.mask, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->d.rbits, sizeof(uint32_t) * 160 * (size_t)g->ntiles) != cudaSuccess ||
         cudaMalloc((void **)&g->rq.flag, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
-        cudaMalloc((void **)&g->rq.ctr, sizeof(unsigned int) * 128) != cudaSuccess ||
+        cudaMalloc((void **)&g->rq.ctr, sizeof(unsigned int) * 256) != cudaSuccess ||
+        cudaMalloc((void **)&g->prq.flag, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->prq.ctr, sizeof(unsigned int) * 256) != cudaSuccess ||
         cudaMalloc((void **)&g->d.marked, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->d.cut, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
@@ -2235,7 +2387,10 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->br_per_sm = std::max(1, std::min(g->br_per_sm, g->br_cap));
     // ring capacity: every tile once + one reserved slot per resident warp
     g->rq.cap = g->ntiles + g->sms * g->br_per_sm * BB_WARPS + 64;
+    g->prq.cap = g->ntiles + g->sms * g->pl_per_sm + 64;
+    g->prq.rerun = 0; g->prq.ns0 = g->rq.ns0; g->prq.ns1 = g->rq.ns1;
     if (cudaMalloc((void **)&g->rq.slot, sizeof(int32_t) * (size_t)g->rq.cap) != cudaSuccess ||
+        cudaMalloc((void **)&g->prq.slot, sizeof(int32_t) * (size_t)g->prq.cap) != cudaSuccess ||
         cudaMemset(g->rq.flag, 0, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess) {
         fm_set_error("fm_grid_create: allocation failed");
         fm_grid_destroy(g);
@@ -2258,6 +2413,9 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->rq.slot) cudaFree(g->rq.slot);
     if (g->rq.flag) cudaFree(g->rq.flag);
     if (g->rq.ctr) cudaFree(g->rq.ctr);
+    if (g->prq.slot) cudaFree(g->prq.slot);
+    if (g->prq.flag) cudaFree(g->prq.flag);
+    if (g->prq.ctr) cudaFree(g->prq.ctr);
     if (g->d.marked) cudaFree(g->d.marked);
     if (g->d.cut) cudaFree(g->d.cut);
     if (g->d_band) cudaFree(g->d_band);
