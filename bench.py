@@ -93,6 +93,16 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/ncu_traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)[kernel]
+        return round(d["dram_bytes_per_launch"]), d.get("source")
+    except Exception:
+        return None, None
+
+
 def cpu_baseline_grid(threads: int):
     """Reference hybrid_solve restated in C (oracle/), all host threads, bounded sample."""
     import oracle
@@ -311,6 +321,7 @@ def main():
         for k, v in st.items():
             if isinstance(v, (int, float)):
                 agg[k] = agg.get(k, 0) + v
+        agg["bfs_tile_visits"] = agg.get("bfs_tile_visits", 0) + int(st["reserved"][0])
     ev1.record(stream)
     torch.cuda.synchronize()
     if ws > 1:
@@ -331,22 +342,24 @@ def main():
     K = args.steps
     pr_ms, bfs_ms = agg.get("ms_pr_kern", 0.0), agg.get("ms_bfs_kern", 0.0)
     if pr_ms >= bfs_ms:
-        # pr_tile_kernel: every visited 32x32 tile loads e, h, rR, rL, rD, rU, rT, rS
-        # (32 B/px) + a 128-px halo of heights, and stores 7 planes (28 B/px)
+        # pr_list_kernel (K1 v3): every visited 32x32 tile loads e, h, rR, rL, rD, rU,
+        # rT, rS (32 B/px) + a 128-px halo of heights, and stores 7 planes (28 B/px)
         launches = max(1, agg.get("pr_launches", 1))
         bytes_per_launch = agg.get("pr_tiles", 0) * (1024 * (32 + 28) + 128 * 4) / launches
         dur = pr_ms / launches
-        kname = "pr_tile_kernel"
+        kname = "pr_list_kernel"
     else:
-        # bfs_tile_kernel: dist (4 B) + mask (1 B) per pixel of a visited tile + halo,
-        # changed distances written back (<= 4 B/px)
+        # bfs_ring_kernel: per tile visit 640 B of arc bits + 4 KB of distances read,
+        # <= 4 KB written; visits per launch from the solve stats
         launches = max(1, agg.get("bfs_launches", 1))
-        bytes_per_launch = 9 * HW * agg.get("bfs_sweeps", 0) / max(1, agg.get("bfs_launches", 1))
+        bytes_per_launch = (640 + 8192) * agg.get("bfs_tile_visits", 0) / launches
         dur = bfs_ms / launches
-        kname = "bfs_tile_kernel"
+        kname = "bfs_ring_kernel"
     achieved = bytes_per_launch / (dur / 1000.0) / 1e9
+    traffic, traffic_src = ncu_traffic(kname)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None, "kernel": kname,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": kname,
                 "peak_source": peak_src, "bytes_per_launch": int(bytes_per_launch),
                 "launch_ms": round(dur, 5), "kernel_share_of_step": round((pr_ms if kname == 'pr_tile_kernel' else bfs_ms) / max(1e-9, ms_total), 3)}
 

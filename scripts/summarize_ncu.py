@@ -2,6 +2,7 @@
 
     python scripts/summarize_ncu.py launches gpurun_out/launches.csv > profiles/X_launches.md
     python scripts/summarize_ncu.py full gpurun_out/prof.ncu-rep > profiles/X_full.md
+    python scripts/summarize_ncu.py traffic gpurun_out/traffic.csv > profiles/ncu_traffic.json
 """
 import collections
 import csv
@@ -60,5 +61,34 @@ def full(path):
         print()
 
 
+def traffic(path):
+    """Per-kernel mean DRAM bytes and duration per launch from an ncu --metrics
+    dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv log (JSON)."""
+    import json
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ki, ii, mi, vi, ui = (h.index("Kernel Name"), h.index("ID"), h.index("Metric Name"),
+                          h.index("Metric Value"), h.index("Metric Unit"))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "nsecond": 1e-3,
+             "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+    per = collections.defaultdict(lambda: collections.defaultdict(float))
+    names = {}
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        names[r[ii]] = r[ki].split("(")[0].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        per[r[ii]][r[mi]] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for lid, m in per.items():
+        a = agg[names[lid]]
+        a[0] += 1
+        a[1] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+        a[2] += m.get("gpu__time_duration.sum", 0.0)
+    out = {k: {"launches": v[0], "dram_bytes_per_launch": v[1] / v[0], "duration_us_per_launch": v[2] / v[0],
+               "source": path} for k, v in agg.items()}
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](sys.argv[2])

@@ -18,7 +18,7 @@ for cfg in cfgs:
     os.environ["FM_K_LOCAL"], os.environ["FM_BFS_INTERVAL"] = kl, bi
     solver = fmb.GridSolver(S, S)
     gs = kl == "global"
-    for i in range(3):
+    for i in range(int(os.environ.get("REPS", "3"))):
         f, st = solver.solve_device(dev, cut_out=cut, global_sweep=gs)
     print(kind, S, cfg, "flow", f, {k: (round(st[k], 2) if isinstance(st[k], float) else st[k]) for k in keys},
           "bfs_tile_visits_changed", st["reserved"][0], "list_passes", st["reserved"][2], "list_items", st["reserved"][3], flush=True)
