@@ -1762,6 +1762,7 @@ struct fm_grid {
     RingQ rq{};                          // device work queue of the persistent BFS
     RingQ prq{};                         // device work queue of the persistent push round
     int pr_ring = 0;                     // 1: one persistent pr_ring_kernel launch per round (env FM_PR_RING; experimental, slower)
+    int pr_batch = 4;                    // push launches between host checks of the round triggers (env FM_PR_BATCH)
     int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (env FM_VISIT_MULT)
     bool ring_stats_pending = false;
     bool pr_stats_pending = false;
@@ -2088,7 +2089,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
     const int blocks = std::min(g->ntiles, g->sms * (g->pr_kernel == 1 ? g->pl_per_sm : g->pt_per_sm));
     int32_t done = 0;
     while (done < cap) {
-        const int batch = std::min(4, cap - done);
+        const int batch = std::min(g->pr_batch, cap - done);
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
         cudaEventRecord(g->ev[2], g->stream);
         for (int i = 0; i < batch; i++) {
@@ -2315,6 +2316,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_BFS_BITS")) g->bfs_bits = atoi(v);
     if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
     if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
+    if (const char *v = getenv("FM_PR_BATCH")) g->pr_batch = std::max(1, std::min(16, atoi(v)));
     if (const char *v = getenv("FM_VISIT_MULT")) g->visit_mult = std::max(1, atoi(v));
     g->rq.rerun = 0; g->rq.ns0 = 128; g->rq.ns1 = 2048;
     if (const char *v = getenv("FM_BR_RERUN")) g->rq.rerun = atoi(v);
