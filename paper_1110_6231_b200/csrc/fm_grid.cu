@@ -430,6 +430,22 @@ __global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(
 // visit (the launch boundary orders the inbox writes before its next load).
 // ----------------------------------------------------------------------------
 constexpr int PL_TY = 8, PL_NT = PT_W * PL_TY, PL_ROWS = PT_H / PL_TY;
+// heights with a 1-pixel halo, rows padded to 40 words so each interior row starts
+// 16-byte aligned (column c at PL_HC + c; halo columns at PL_HC - 1 and PL_HC + 32)
+constexpr int PL_HS = 40, PL_HC = 4;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+// 4-byte copy; zero-fills the destination when !pred
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool pred) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
 #ifndef FM_PL_MINBLOCKS
 #define FM_PL_MINBLOCKS 6
 #endif
@@ -459,13 +475,13 @@ struct PlTile {
 __device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int li, int steps, int fused,
                                         int *cnt_next, uint16_t *lout, int *recv,
                                         long long &pushes, long long &relabels) {
-    constexpr int HS = PT_W + 2;
+    constexpr int HS = PL_HS;
     volatile int32_t *ve = T.e;
     volatile int32_t *vh = T.h;
     volatile int32_t *vt = T.t;
     const int V = g.V;
     const int lr = li >> 5, lc = li & 31;
-    const int hi = (lr + 1) * HS + lc + 1;
+    const int hi = (lr + 1) * HS + lc + PL_HC;
     const int r = T.r0 + lr, c = T.c0 + lc;
     const uint8_t f = T.f[li];
     if (f & 2) return false;                               // ghost row: owned by the neighbour band
@@ -527,7 +543,7 @@ __device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int l
 
 struct PlSmem {
     int32_t e[PT_H * PT_W];
-    int32_t h[(PT_H + 2) * (PT_W + 2)];
+    int32_t h[(PT_H + 2) * PL_HS];
     int32_t r[4][PT_H * PT_W];   // R, L, D, U
     int32_t t[PT_H * PT_W];
     uint8_t f[PT_H * PT_W];      // bit 0: residual arc to s, bit 1: ghost row
@@ -541,6 +557,9 @@ struct PlSmem {
 
 struct PlCounters {
     long long pushes = 0, relabels = 0, passes = 0, items = 0;
+#ifdef FM_PL_TIMING
+    long long t_load = 0, t_pass = 0, t_store = 0, visits = 0, solo = 0;
+#endif
 };
 
 // One visit of `tile`: load (folding the inboxes), list-driven passes, write back.
@@ -548,55 +567,97 @@ struct PlCounters {
 // neighbour tiles whose inboxes received flow.  Starts and ends with a barrier.
 __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, int k_local, int steps,
                                          int fused, PlCounters &C) {
-    constexpr int HS = PT_W + 2;
+    constexpr int HS = PL_HS;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * PT_W + tx;
     const int V = g.V;
     if (tid == 0) { S.cnt[0] = S.cnt[1] = S.cnt[2] = 0; S.nbr = 0; }
+#ifdef FM_PL_TIMING
+    long long t0 = clock64(), t1 = 0, t2 = 0;
+#endif
     const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
     const PlTile T{S.e, S.h, S.t, S.r, S.f, &S.nbr, tyi * PT_H, txi * PT_W};
     const int r0 = T.r0, c0 = T.c0;
+    int32_t *stage = (int32_t *)&S.list[0][0];   // rS staging (the lists are built afterwards)
+    // load: asynchronous global -> shared copies, thread = (row, 4-column chunk)
+    {
+        const int lrow = tid >> 3, ch = tid & 7;
+        const int r = r0 + lrow, cb = c0 + 4 * ch;
+        const int li = lrow * PT_W + 4 * ch, hi = (lrow + 1) * HS + PL_HC + 4 * ch;
+        if (r < g.H && cb + 4 <= g.W && (g.W & 3) == 0) {
+            const int64_t p = (int64_t)r * g.W + cb;
+            cp_async16(&S.e[li], g.e + p);
+            cp_async16(&S.r[0][li], g.rR + p);
+            cp_async16(&S.r[1][li], g.rL + p);
+            cp_async16(&S.r[2][li], g.rD + p);
+            cp_async16(&S.r[3][li], g.rU + p);
+            cp_async16(&S.t[li], g.rT + p);
+            cp_async16(&S.h[hi], g.h + p);
+            cp_async16(&stage[li], g.rS + p);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const bool in = r < g.H && cb + j < g.W;
+                const int64_t p = in ? (int64_t)r * g.W + cb + j : 0;
+                cp_async4(&S.e[li + j], g.e + p, in);
+                cp_async4(&S.r[0][li + j], g.rR + p, in);
+                cp_async4(&S.r[1][li + j], g.rL + p, in);
+                cp_async4(&S.r[2][li + j], g.rD + p, in);
+                cp_async4(&S.r[3][li + j], g.rU + p, in);
+                cp_async4(&S.t[li + j], g.rT + p, in);
+                cp_async4(&S.h[hi + j], g.h + p, in);
+                cp_async4(&stage[li + j], g.rS + p, in);
+            }
+        }
+    }
+    // halo heights (a snapshot: stale reads are the lock-free argument's business) and
+    // the inboxes of the border pixels, both issued while the copies are in flight
+    int32_t inbox = 0;
+    int ib_li = -1, ib_dir = 0;
+    if (tid < 4 * PT_W) {
+        const int side = tid / PT_W, i = tid % PT_W;
+        int r, cc, hidx;
+        if (side == 0) { r = r0 - 1; cc = c0 + i; hidx = PL_HC + i; }
+        else if (side == 1) { r = r0 + PT_H; cc = c0 + i; hidx = (PT_H + 1) * HS + PL_HC + i; }
+        else if (side == 2) { r = r0 + i; cc = c0 - 1; hidx = (i + 1) * HS + PL_HC - 1; }
+        else { r = r0 + i; cc = c0 + PT_W; hidx = (i + 1) * HS + PL_HC + PT_W; }
+        const bool hin = r >= 0 && r < g.H && cc >= 0 && cc < g.W;
+        cp_async4(&S.h[hidx], g.h + (hin ? (int64_t)r * g.W + cc : 0), hin);
+        // border pixel of this side and its inbox (flow parked by the neighbour tile)
+        const int lr = side == 0 ? 0 : side == 1 ? PT_H - 1 : i;
+        const int lc = side == 2 ? 0 : side == 3 ? PT_W - 1 : i;
+        const int pr = r0 + lr, pc = c0 + lc;
+        const bool has = pr < g.H && pc < g.W &&
+                         (side == 0 ? pr > 0 : side == 1 ? pr + 1 < g.H : side == 2 ? pc > 0 : pc + 1 < g.W);
+        if (has) {
+            const int64_t p = (int64_t)pr * g.W + pc;
+            inbox = atomicExch((side < 2 ? g.inflow_v : g.inflow_h) + p, 0);
+            ib_li = lr * PT_W + lc;
+            ib_dir = side == 0 ? 3 : side == 1 ? 2 : side == 2 ? 1 : 0;   // residual toward the sender
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (inbox) {
+        atomicAdd(&S.e[ib_li], inbox);          // a corner pixel has two inboxes
+        S.r[ib_dir][ib_li] += inbox;
+    }
 #pragma unroll
     for (int k = 0; k < PL_ROWS; k++) {
         const int lr = ty + k * PL_TY;
         const int r = r0 + lr, c = c0 + tx;
         const int li = lr * PT_W + tx;
-        if (r < g.H && c < g.W) {
-            const int64_t p = (int64_t)r * g.W + c;
-            int32_t e = g.e[p];
-            int32_t rr = g.rR[p], rl = g.rL[p], rd = g.rD[p], ru = g.rU[p];
-            if (tx == 0 && c > 0) { const int32_t d = atomicExch(g.inflow_h + p, 0); e += d; rl += d; }
-            if (tx == PT_W - 1 && c + 1 < g.W) { const int32_t d = atomicExch(g.inflow_h + p, 0); e += d; rr += d; }
-            if (lr == 0 && r > 0) { const int32_t d = atomicExch(g.inflow_v + p, 0); e += d; ru += d; }
-            if (lr == PT_H - 1 && r + 1 < g.H) { const int32_t d = atomicExch(g.inflow_v + p, 0); e += d; rd += d; }
-            S.e[li] = e;
-            S.h[(lr + 1) * HS + tx + 1] = g.h[p];
-            S.r[0][li] = rr; S.r[1][li] = rl; S.r[2][li] = rd; S.r[3][li] = ru;
-            S.t[li] = g.rT[p];
-            S.f[li] = (g.rS[p] > 0 ? 1 : 0) | (is_ghost_row(g, r) ? 2 : 0);
-        } else {
-            S.e[li] = 0;
-            S.h[(lr + 1) * HS + tx + 1] = V;
-            S.r[0][li] = S.r[1][li] = S.r[2][li] = S.r[3][li] = 0;
-            S.t[li] = 0;
-            S.f[li] = 2;
-        }
-    }
-    if (tid < 4 * PT_W) {   // halo snapshot of neighbour heights
-        const int side = tid / PT_W, i = tid % PT_W;
-        int r, cc, hr, hc;
-        if (side == 0) { r = r0 - 1; cc = c0 + i; hr = 0; hc = i + 1; }
-        else if (side == 1) { r = r0 + PT_H; cc = c0 + i; hr = PT_H + 1; hc = i + 1; }
-        else if (side == 2) { r = r0 + i; cc = c0 - 1; hr = i + 1; hc = 0; }
-        else { r = r0 + i; cc = c0 + PT_W; hr = i + 1; hc = PT_W + 1; }
-        S.h[hr * HS + hc] = (r >= 0 && r < g.H && cc >= 0 && cc < g.W) ? g.h[(int64_t)r * g.W + cc] : V;
+        S.f[li] = (r < g.H && c < g.W) ? ((stage[li] > 0 ? 1 : 0) | (is_ghost_row(g, r) ? 2 : 0)) : 2;
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < PL_ROWS; k++) {
         const int lr = ty + k * PL_TY;
         const int li = lr * PT_W + tx;
-        pl_append_warp(S.e[li] > 0 && S.h[(lr + 1) * HS + tx + 1] < V && !(S.f[li] & 2), li, &S.cnt[0], S.list[0]);
+        pl_append_warp(S.e[li] > 0 && S.h[(lr + 1) * HS + PL_HC + tx] < V && !(S.f[li] & 2), li, &S.cnt[0], S.list[0]);
     }
+#ifdef FM_PL_TIMING
+    t1 = clock64();
+#endif
     // dense passes: the whole CTA, one barrier per pass
     int it = 0;
     bool solo = false;
@@ -621,6 +682,9 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
         }
     }
     // sparse passes: warp 0 alone, warp-synchronous
+#ifdef FM_PL_TIMING
+    if (solo && tid == 0) C.solo++;
+#endif
     if (solo && tid < 32) {
         for (; it < k_local; it++) {
             __syncwarp();
@@ -644,6 +708,9 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
         }
     }
     __syncthreads();
+#ifdef FM_PL_TIMING
+    t2 = clock64();
+#endif
     bool act = false;
 #pragma unroll
     for (int k = 0; k < PL_ROWS; k++) {
@@ -652,7 +719,7 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
         const int li = lr * PT_W + tx;
         if (r < g.H && c < g.W) {
             const int64_t p = (int64_t)r * g.W + c;
-            const int32_t e = S.e[li], h = S.h[(lr + 1) * HS + tx + 1];
+            const int32_t e = S.e[li], h = S.h[(lr + 1) * HS + PL_HC + tx];
             g.e[p] = e;
             g.h[p] = h;
             g.rR[p] = S.r[0][li]; g.rL[p] = S.r[1][li];
@@ -661,7 +728,11 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
             act |= (e > 0 && h < V && !(S.f[li] & 2));
         }
     }
-    return __syncthreads_or(act) != 0;
+    const bool any = __syncthreads_or(act) != 0;
+#ifdef FM_PL_TIMING
+    if (tid == 0) { C.t_load += t1 - t0; C.t_pass += t2 - t1; C.t_store += clock64() - t2; C.visits++; }
+#endif
+    return any;
 }
 
 __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev g, int k_local, int steps, int fused,
@@ -693,6 +764,11 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev
     if (tid == 0) {   // diagnostics: passes run and list items dealt (ops[3], ops[4]) -- thread 0 saw them all
         if (C.passes) atomicAdd(ops + 3, (unsigned long long)C.passes);
         if (C.items) atomicAdd(ops + 4, (unsigned long long)C.items);
+#ifdef FM_PL_TIMING
+        atomicAdd(ops + 6, (unsigned long long)C.t_load); atomicAdd(ops + 7, (unsigned long long)C.t_pass);
+        atomicAdd(ops + 8, (unsigned long long)C.t_store); atomicAdd(ops + 9, (unsigned long long)C.visits);
+        atomicAdd(ops + 10, (unsigned long long)C.solo);
+#endif
     }
 }
 
@@ -2018,7 +2094,7 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     g->local_streak = 0;
     memset(&g->st, 0, sizeof(g->st));
     FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
-    FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 16, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 32, g->stream));
     grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
     FM_CHECK_LAUNCH();
@@ -2280,6 +2356,13 @@ int solve_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);
     g->st.ms_total = ms;
+    if (g->trace >= 2) {   // FM_PL_TIMING builds: per-visit cycle split of the push kernel
+        unsigned long long h[5] = {};
+        cudaMemcpy(h, g->acc + 16, sizeof(h), cudaMemcpyDeviceToHost);
+        const double v = h[3] ? (double)h[3] : 1.0;
+        fprintf(stderr, "[fm_grid] visits %llu (solo %llu) cycles/visit: load %.0f passes %.0f store %.0f\n",
+                h[3], h[4], h[0] / v, h[1] / v, h[2] / v);
+    }
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
     if (rc == FM_OK && flow_out) *flow_out = flow;
@@ -2344,13 +2427,13 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         cudaMalloc((void **)&g->prq.ctr, sizeof(unsigned int) * 256) != cudaSuccess ||
         cudaMalloc((void **)&g->d.marked, n1) != cudaSuccess ||
         cudaMalloc((void **)&g->d.cut, n1) != cudaSuccess ||
-        cudaMalloc((void **)&g->acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
+        cudaMalloc((void **)&g->acc, sizeof(unsigned long long) * 32) != cudaSuccess ||
         cudaMalloc((void **)&g->d_queues, sizeof(int32_t) * (8 * (size_t)g->ntiles + 8)) != cudaSuccess ||
         cudaMalloc((void **)&g->d_touched, (size_t)g->ntiles) != cudaSuccess ||
         cudaMalloc((void **)&g->d_region, (size_t)g->ntiles) != cudaSuccess ||
         cudaMalloc((void **)&g->d_rlist, sizeof(int32_t) * ((size_t)g->ntiles + 1)) != cudaSuccess ||
         cudaMalloc((void **)&g->flags, sizeof(int32_t) * 64) != cudaSuccess ||
-        cudaMallocHost((void **)&g->h_acc, sizeof(unsigned long long) * 16) != cudaSuccess ||
+        cudaMallocHost((void **)&g->h_acc, sizeof(unsigned long long) * 32) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_flags, sizeof(int32_t) * 64) != cudaSuccess ||
         cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
         fm_set_error("fm_grid_create: allocation failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -2595,7 +2678,7 @@ extern "C" int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t 
     FM_CHECK_CUDA(cudaSetDevice(g->device));
     g->flags_solve = flags;
     memset(&g->st, 0, sizeof(g->st));
-    FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 16, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 32, g->stream));
     grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
     FM_CHECK_LAUNCH();
