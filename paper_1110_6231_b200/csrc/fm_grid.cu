@@ -469,6 +469,80 @@ struct PlTile {
     int r0, c0;
 };
 
+// The default operation (steps == 1, not fused: one maxflow_par.py:98-125 operation
+// per listed pixel per pass) with every shared-memory read issued up front and the
+// two pushes' atomics in flight together: the pass is a latency chain, so fewer
+// dependent round trips is what makes it faster.  Same results as pl_item.
+__device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li, int *recv,
+                                       long long &pushes, long long &relabels) {
+    constexpr int HS = PL_HS;
+    volatile int32_t *ve = T.e;
+    volatile int32_t *vh = T.h;
+    volatile int32_t *vt = T.t;
+    const int V = g.V;
+    const int lr = li >> 5, lc = li & 31;
+    const int hi = (lr + 1) * HS + lc + PL_HC;
+    const int r = T.r0 + lr, c = T.c0 + lc;
+    const uint8_t f = T.f[li];
+    const int32_t e = ve[li], hp = vh[hi], rt = vt[li];
+    const int32_t rr = *(volatile int32_t *)&T.r[0][li];
+    const int32_t rl = *(volatile int32_t *)&T.r[1][li];
+    const int32_t rd = *(volatile int32_t *)&T.r[2][li];
+    const int32_t ru = *(volatile int32_t *)&T.r[3][li];
+    const int32_t hR = vh[hi + 1], hL = vh[hi - 1], hD = vh[hi + HS], hU = vh[hi - HS];
+    if ((f & 2) || e <= 0 || hp >= V) return false;
+    if (rt > 0) {                                          // sink at height 0
+        if (hp == 0) { vh[hi] = 1; relabels++; }
+        const int32_t d = min(e, rt);
+        vt[li] = rt - d;
+        pushes++;
+        return atomicSub(&T.e[li], d) - d > 0;
+    }
+    int32_t best_h = INT32_MAX, best_r = 0;
+    int dir = -1;
+    if (rr > 0 && c + 1 < g.W && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
+    if (rl > 0 && c > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
+    if (rd > 0 && r + 1 < g.H && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
+    if (ru > 0 && r > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
+    if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
+    if (dir < 0) return false;                             // nothing residual: rescanned on next load
+    if (hp <= best_h) {                                    // relabel (owner-only); the push waits
+        vh[hi] = best_h + 1;
+        relabels++;
+        return dir != 5;                                   // above the source: inactive
+    }
+    const int32_t d = min(e, best_r);
+    int qr = lr, qc = lc;
+    if (dir == 0) qc++; else if (dir == 1) qc--; else if (dir == 2) qr++; else qr--;
+    atomicSub(&T.r[dir][li], d);
+    int32_t old = 1;
+    if (qr >= 0 && qr < PT_H && qc >= 0 && qc < PT_W) {
+        const int qi = qr * PT_W + qc;
+        atomicAdd(&T.r[dir ^ 1][qi], d);
+        old = atomicAdd(&T.e[qi], d);
+        if (old <= 0 && old + d > 0) *recv = qi;
+    } else {
+        const int64_t q = (int64_t)(T.r0 + qr) * g.W + (T.c0 + qc);
+        atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + q, d);
+        atomicOr(T.nbr, 1 << dir);
+    }
+    pushes++;
+    return atomicSub(&T.e[li], d) - d > 0;                 // the owner's view of e(p); hp < V here
+}
+
+// two candidates per lane (the pixel itself, the receiver it activated), one list reservation
+__device__ __forceinline__ void pl_append2_warp(bool wa, int ia, bool wb, int ib, int *cnt, uint16_t *list) {
+    const unsigned ma = __ballot_sync(0xffffffffu, wa), mb = __ballot_sync(0xffffffffu, wb);
+    if (!(ma | mb)) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(cnt, __popc(ma) + __popc(mb));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (wa) list[base + __popc(ma & lt)] = (uint16_t)ia;
+    if (wb) list[base + __popc(ma) + __popc(mb & lt)] = (uint16_t)ib;
+}
+
 // One listed pixel: up to `steps` operations of maxflow_par.py:98-125 by its owner.
 // Returns whether the owner re-lists it; *recv = the in-tile receiver its last push
 // activated (-1 if none); receivers of earlier pushes are listed directly.
@@ -558,7 +632,7 @@ struct PlSmem {
 struct PlCounters {
     long long pushes = 0, relabels = 0, passes = 0, items = 0;
 #ifdef FM_PL_TIMING
-    long long t_load = 0, t_pass = 0, t_store = 0, visits = 0, solo = 0;
+    long long t_load = 0, t_pass = 0, t_store = 0, visits = 0, solo = 0, t_solo = 0, dense_passes = 0, solo_passes = 0;
 #endif
 };
 
@@ -659,6 +733,7 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
     t1 = clock64();
 #endif
     // dense passes: the whole CTA, one barrier per pass
+    const bool simple = steps == 1 && !fused;
     int it = 0;
     bool solo = false;
     for (; it < k_local; it++) {
@@ -676,14 +751,17 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
             if (base + (tid & ~31) >= n) break;        // warp-uniform
             const int i = base + tid;
             int recv = -1;
-            const bool keep = i < n && pl_item(g, T, lin[i], steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels);
-            pl_append_warp(keep, i < n ? lin[i] : 0, cnt_next, lout);
-            pl_append_warp(recv >= 0, recv, cnt_next, lout);
+            const int li = i < n ? lin[i] : 0;
+            const bool keep = i < n && (simple ? pl_op1(g, T, li, &recv, C.pushes, C.relabels)
+                                               : pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels));
+            pl_append2_warp(keep, li, recv >= 0, recv, cnt_next, lout);
         }
     }
     // sparse passes: warp 0 alone, warp-synchronous
 #ifdef FM_PL_TIMING
     if (solo && tid == 0) C.solo++;
+    const long long ts0 = clock64();
+    const int it_dense = it;
 #endif
     if (solo && tid < 32) {
         for (; it < k_local; it++) {
@@ -701,12 +779,15 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
                 const int i = base + tid;
                 int recv = -1;
                 const int li = i < n ? lin[i] : 0;
-                const bool keep = i < n && pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels);
-                pl_append_warp(keep, li, cnt_next, lout);
-                pl_append_warp(recv >= 0, recv, cnt_next, lout);
+                const bool keep = i < n && (simple ? pl_op1(g, T, li, &recv, C.pushes, C.relabels)
+                                                   : pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels));
+                pl_append2_warp(keep, li, recv >= 0, recv, cnt_next, lout);
             }
         }
     }
+#ifdef FM_PL_TIMING
+    if (tid == 0) { C.t_solo += clock64() - ts0; C.dense_passes += it_dense; C.solo_passes += it - it_dense; }
+#endif
     __syncthreads();
 #ifdef FM_PL_TIMING
     t2 = clock64();
@@ -768,6 +849,8 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev
         atomicAdd(ops + 6, (unsigned long long)C.t_load); atomicAdd(ops + 7, (unsigned long long)C.t_pass);
         atomicAdd(ops + 8, (unsigned long long)C.t_store); atomicAdd(ops + 9, (unsigned long long)C.visits);
         atomicAdd(ops + 10, (unsigned long long)C.solo);
+        atomicAdd(ops + 11, (unsigned long long)C.t_solo); atomicAdd(ops + 12, (unsigned long long)C.dense_passes);
+        atomicAdd(ops + 13, (unsigned long long)C.solo_passes);
 #endif
     }
 }
@@ -2357,11 +2440,12 @@ int solve_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     cudaEventElapsedTime(&ms, t0, t1);
     g->st.ms_total = ms;
     if (g->trace >= 2) {   // FM_PL_TIMING builds: per-visit cycle split of the push kernel
-        unsigned long long h[5] = {};
+        unsigned long long h[8] = {};
         cudaMemcpy(h, g->acc + 16, sizeof(h), cudaMemcpyDeviceToHost);
         const double v = h[3] ? (double)h[3] : 1.0;
-        fprintf(stderr, "[fm_grid] visits %llu (solo %llu) cycles/visit: load %.0f passes %.0f store %.0f\n",
-                h[3], h[4], h[0] / v, h[1] / v, h[2] / v);
+        fprintf(stderr, "[fm_grid] visits %llu (solo %llu) cycles/visit: load %.0f passes %.0f (solo part %.0f) store %.0f"
+                " | passes/visit dense %.2f solo %.2f\n",
+                h[3], h[4], h[0] / v, h[1] / v, h[5] / v, h[2] / v, h[6] / v, h[7] / v);
     }
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
