@@ -763,7 +763,31 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
     const long long ts0 = clock64();
     const int it_dense = it;
 #endif
-    if (solo && tid < 32) {
+    if (solo && tid < 32 && simple) {
+        // one warp is the only reader and writer of the lists now: the next list's
+        // length is the warp's own running count (no shared counter round trip)
+        int n = S.cnt[it % 3];
+        const unsigned lt = (1u << tid) - 1;
+        for (; it < k_local && n > 0; it++) {
+            C.passes++;
+            C.items += n;
+            const uint16_t *lin = S.list[it & 1];
+            uint16_t *lout = S.list[(it + 1) & 1];
+            int nn = 0;
+            for (int base = 0; base < n; base += 32) {
+                const int i = base + tid;
+                int recv = -1;
+                const int li = i < n ? lin[i] : 0;
+                const bool keep = i < n && pl_op1(g, T, li, &recv, C.pushes, C.relabels);
+                const unsigned ma = __ballot_sync(0xffffffffu, keep), mb = __ballot_sync(0xffffffffu, recv >= 0);
+                if (keep) lout[nn + __popc(ma & lt)] = (uint16_t)li;
+                if (recv >= 0) lout[nn + __popc(ma) + __popc(mb & lt)] = (uint16_t)recv;
+                nn += __popc(ma) + __popc(mb);
+            }
+            __syncwarp();
+            n = nn;
+        }
+    } else if (solo && tid < 32) {
         for (; it < k_local; it++) {
             __syncwarp();
             const int n = S.cnt[it % 3];
