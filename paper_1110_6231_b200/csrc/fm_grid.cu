@@ -79,6 +79,7 @@ struct GridDev {
     int32_t H, W;
     int32_t V;      // node count |V| = H*W + 2 (the source's height)
     int32_t INF;    // "unreached" distance sentinel (== V)
+    int32_t solo_max;   // push kernel: a pass listing <= solo_max pixels runs on warp 0 alone
 };
 
 __device__ __forceinline__ bool is_ghost_row(const GridDev &g, int r) {
@@ -740,7 +741,7 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
         __syncthreads();
         const int n = S.cnt[it % 3];
         if (n == 0) break;
-        if (n <= 32) { solo = true; break; }
+        if (n <= g.solo_max) { solo = true; break; }
         C.passes++;
         C.items += n;
         int *cnt_next = &S.cnt[(it + 1) % 3];
@@ -2507,6 +2508,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_BFS_BITS")) g->bfs_bits = atoi(v);
     if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
     if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
+    g->d.solo_max = 32;
+    if (const char *v = getenv("FM_SOLO_MAX")) g->d.solo_max = atoi(v);
     if (const char *v = getenv("FM_PR_BATCH")) g->pr_batch = std::max(1, std::min(16, atoi(v)));
     if (const char *v = getenv("FM_VISIT_MULT")) g->visit_mult = std::max(1, atoi(v));
     g->rq.rerun = 0; g->rq.ns0 = 128; g->rq.ns1 = 2048;
