@@ -54,7 +54,8 @@ constexpr int C_COUNT = 12;
 // ops[] slots
 constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXED = 4,
               O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7, O_TAIL_NS = 8, O_MULTI_NS = 9,
-              O_PH_Y = 10, O_PH_SYNC1 = 11, O_PH_X = 12, O_PH_SYNC2 = 13;  // multi-round phase ns (CTA 0)
+              O_PH_Y = 10, O_PH_SYNC1 = 11, O_PH_X = 12, O_PH_SYNC2 = 13,  // multi-round phase ns (CTA 0)
+              O_PU_YS = 14, O_PU_ITNS = 15, O_PU_YNS = 3;  // price update: frontier Y visits, ns in BF iterations (CTA 0)
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -68,6 +69,7 @@ struct AssignDev {
     int32_t *match;        // match[x] = y carrying x's unit, -1 if x holds its excess
     int32_t *ey;           // excess of y
     uint32_t *fixed;       // arc-fix bitmask, row-major n x nw words
+    uint32_t *fixed_t;     // its transpose (row y, bit x): the price update scans columns
     uint8_t *frozen;       // frozen[x]: x's matched arc is fixed (its flow never changes)
     int32_t *frozen_in;    // frozen_in[y]: number of frozen matches into y
     int32_t *lx, *ly;      // price-update labels
@@ -471,6 +473,22 @@ __global__ void reset_excess_kernel(AssignDev a) {
         a.ey[y] = -1 + a.frozen_in[y];
 }
 
+// Control words read right after a grid barrier: one thread per CTA loads them and
+// the CTA shares them (thousands of warps loading one L2 line at the same moment
+// serialise on its slice; ncu put half of the price update's stall samples there).
+__device__ __forceinline__ void cta_bcast3(const int32_t *p0, const int32_t *p1, const int32_t *p2,
+                                           int &v0, int &v1, int &v2) {
+    __shared__ int s_b[3];
+    __syncthreads();   // the previous broadcast has been read by every thread
+    if (threadIdx.x == 0) {
+        s_b[0] = __ldcg(p0);
+        s_b[1] = p1 ? __ldcg(p1) : 0;
+        s_b[2] = p2 ? __ldcg(p2) : 0;
+    }
+    __syncthreads();
+    v0 = s_b[0]; v1 = s_b[1]; v2 = s_b[2];
+}
+
 // The refine's push/relabel rounds (refine_par's coordinator loop, assign_par.py:162-236)
 // as one cooperative kernel.  Round r: Y phase over ylist[r&1] -> xlist[r&1];
 // grid barrier; X phase over xlist[r&1] -> ylist[(r+1)&1]; grid barrier.
@@ -498,12 +516,13 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             t_round = now;
         }
         const int b = r & 1, nb = b ^ 1;
-        const int ny = __ldcg(a.cnt + C_Y0 + b);
-        if (ny == 0 || __ldcg(a.cnt + C_INFEASIBLE)) {
+        int ny, infeasible, relabels_since;
+        cta_bcast3(a.cnt + C_Y0 + b, a.cnt + C_INFEASIBLE, a.cnt + C_RELABELS, ny, infeasible, relabels_since);
+        if (ny == 0 || infeasible) {
             if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 0;
             break;
         }
-        if (pu_threshold > 0 && __ldcg(a.cnt + C_RELABELS) >= pu_threshold) {
+        if (pu_threshold > 0 && relabels_since >= pu_threshold) {
             if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 1;
             break;
         }
@@ -569,7 +588,8 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_Y, t1 - t0); t0 = t1; }
             grid.sync();
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC1, t1 - t0); t0 = t1; }
-            const int nx = __ldcg(a.cnt + C_X0 + b);
+            int nx, u1, u2;
+            cta_bcast3(a.cnt + C_X0 + b, nullptr, nullptr, nx, u1, u2);
             if (nx <= (int)gridDim.x) {
                 for (int i = blockIdx.x; i < nx; i += gridDim.x)
                     x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
@@ -635,7 +655,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     // final min(label, last + 1) needs.
     long long cap = min((long long)a.max_bucket, (long long)(a.pu_cap0 > 0 ? a.pu_cap0 : 8));
     int it_total = 0;
-    __shared__ int s_ly;
+    __shared__ int s_ly, s_y;
     __shared__ long long s_py;
     for (;;) {
     if (tid == 0) { a.cnt[C_PU_LAST] = 0; a.cnt[C_PU_CHG] = 0; }
@@ -656,31 +676,106 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     // relaxation reaches the same fixpoint).  Frontier counters are triple-buffered so
     // the counter of iteration it+2 can be zeroed during iteration it.
     int it = 0;
+    const unsigned long long t_it0 = globaltimer();
     for (;; it++) {
         const int b = it & 1, nb = b ^ 1;
-        const int ny = __ldcg(f.cnt + it % 3);
+        int ny, u1, u2;
+        cta_bcast3(f.cnt + it % 3, nullptr, nullptr, ny, u1, u2);
         if (ny == 0) break;
+        if (tid == 0) atomicAdd(a.ops + O_PU_YS, (unsigned long long)ny);
         if (tid == 0) f.cnt[(it + 2) % 3] = 0;
+        const unsigned long long t_y0 = globaltimer();
+        // thread 0 fetches each frontier Y's header (clear its queued flag, then read
+        // l(y), p(y)) one Y ahead, so the next header's round trips overlap this scan
+        int nxt_y = -1, nxt_l = 0;
+        long long nxt_p = 0;
+        if (threadIdx.x == 0 && blockIdx.x < ny) {
+            nxt_y = __ldcg(f.fy[b] + blockIdx.x);
+            f.in_fy[nxt_y] = 0;          // clear before reading l(y): a later drop re-queues y
+            __threadfence();
+            nxt_l = __ldcg(a.ly + nxt_y);
+            nxt_p = __ldcg((const long long *)a.py + nxt_y);
+        }
         for (int i = blockIdx.x; i < ny; i += gridDim.x) {
-            const int y = __ldcg(f.fy[b] + i);
             if (threadIdx.x == 0) {
-                f.in_fy[y] = 0;          // clear before reading l(y): a later drop re-queues y
-                __threadfence();
-                s_ly = __ldcg(a.ly + y);
-                s_py = __ldcg((const long long *)a.py + y);
+                s_y = nxt_y; s_ly = nxt_l; s_py = nxt_p;
+                if (i + (int)gridDim.x < ny) {
+                    nxt_y = __ldcg(f.fy[b] + i + gridDim.x);
+                    f.in_fy[nxt_y] = 0;
+                    __threadfence();
+                    nxt_l = __ldcg(a.ly + nxt_y);
+                    nxt_p = __ldcg((const long long *)a.py + nxt_y);
+                }
             }
             __syncthreads();
+            const int y = s_y;
             const int lyv = s_ly;
             const long long pyv = s_py;
             const int32_t *col = f.wt + (size_t)y * n;
-            for (int x = threadIdx.x; x < n; x += ATHREADS) {
+            // vector path: 8 consecutive x per thread, every operand loaded up front
+            // (int4 weights / labels / matches, longlong2 prices) so a thread's scan is
+            // one L2 round trip instead of a chain of dependent ones
+            const int nv8 = (n & 7) ? 0 : n;
+            for (int x0 = threadIdx.x * 8; x0 < nv8; x0 += ATHREADS * 8) {
+                const int4 w0 = __ldg((const int4 *)(col + x0)), w1 = __ldg((const int4 *)(col + x0 + 4));
+                const int4 l0 = __ldcg((const int4 *)(a.lx + x0)), l1 = __ldcg((const int4 *)(a.lx + x0 + 4));
+                const int4 m0 = __ldcg((const int4 *)(a.match + x0)), m1 = __ldcg((const int4 *)(a.match + x0 + 4));
+                longlong2 pv[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) pv[k] = __ldcg((const longlong2 *)(a.px + x0) + k);
+                uint32_t fb = 0;
+                if (a.use_fix) fb = (__ldg(a.fixed_t + (size_t)y * a.nw + (x0 >> 5)) >> (x0 & 31)) & 0xffu;
+                const int wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+                const int lxv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+                const int mxv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+                const long long pxv[8] = {pv[0].x, pv[0].y, pv[1].x, pv[1].y, pv[2].x, pv[2].y, pv[3].x, pv[3].y};
+                // stage 1: candidate labels; stage 2: all atomicMin on l(x) in flight
+                // together; stage 3: the matched reverse arcs of the x that dropped
+                int cand[8], old[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    cand[k] = LINF;
+                    if (wv[k] == FM_ABSENT_WEIGHT || lyv >= lxv[k] || mxv[k] == y || ((fb >> k) & 1u)) continue;
+                    const long long rc = -(long long)wv[k] * a.scale + pxv[k] - pyv;
+                    long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
+                    if (len < 0) len = 0;
+                    const long long c1 = (long long)lyv + len;
+                    if (c1 <= cap && c1 < lxv[k]) cand[k] = (int)c1;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; k++) old[k] = cand[k] < LINF ? atomicMin(a.lx + x0 + k, cand[k]) : LINF;
+                int w2[8];
+                long long py2[8];
+                uint8_t fz[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const bool go = cand[k] < old[k] && mxv[k] >= 0;
+                    w2[k] = go ? __ldg(a.w + (size_t)(x0 + k) * n + mxv[k]) : 0;
+                    py2[k] = go ? __ldcg((const long long *)a.py + mxv[k]) : 0;
+                    fz[k] = go ? __ldcg(a.frozen + x0 + k) : 1;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    if (!(cand[k] < old[k]) || mxv[k] < 0 || fz[k]) continue;
+                    const long long rc2 = (long long)w2[k] * a.scale - pxv[k] + py2[k];
+                    long long len2 = floordiv_eps(rc2, a.eps, inv_eps) + 1;
+                    if (len2 < 0) len2 = 0;
+                    const long long cand2 = cand[k] + len2;
+                    if (cand2 > cap) continue;
+                    const int mx = mxv[k];
+                    const int old2 = atomicMin(a.ly + mx, (int)cand2);
+                    if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0)
+                        f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;   // read after the grid barrier
+                }
+            }
+            for (int x = nv8 + threadIdx.x; x < n; x += ATHREADS) {
                 const int wv = __ldg(col + x);
                 if (wv == FM_ABSENT_WEIGHT) continue;
                 const int lxv = __ldcg(a.lx + x);
                 if (lyv >= lxv) continue;                              // cannot improve (len >= 0)
                 const int mx = __ldcg(a.match + x);
                 if (mx == y) continue;                                 // flow arc: not residual forward
-                if (a.use_fix && ((__ldg(a.fixed + (size_t)x * a.nw + (y >> 5)) >> (y & 31)) & 1u)) continue;
+                if (a.use_fix && ((__ldg(a.fixed_t + (size_t)y * a.nw + (x >> 5)) >> (x & 31)) & 1u)) continue;
                 const long long px = __ldcg((const long long *)a.px + x);
                 const long long rc = -(long long)wv * a.scale + px - pyv;
                 long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
@@ -697,16 +792,16 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
                 const long long cand2 = cand + len2;
                 if (cand2 > cap) continue;
                 const int old2 = atomicMin(a.ly + mx, (int)cand2);
-                if ((int)cand2 < old2) {
-                    __threadfence();
-                    if (atomicExch(f.in_fy + mx, 1) == 0) f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;
-                }
+                if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0)
+                    f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;
             }
             __syncthreads();
         }
+        if (tid == 0) atomicAdd(a.ops + O_PU_YNS, globaltimer() - t_y0);
         grid.sync();
     }
     it_total += it + 1;
+    if (tid == 0) atomicAdd(a.ops + O_PU_ITNS, globaltimer() - t_it0);
     // last = max label over active nodes (unmatched X, Y with positive excess);
     // an active node left unlabelled under the cap asks for a wider cap
     int last = 0, missing = 0;
@@ -728,7 +823,9 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     if (lane == 0 && last) atomicMax(a.cnt + C_PU_LAST, last);
     if (lane == 0 && missing) atomicOr(a.cnt + C_PU_CHG, 1);
     grid.sync();
-    if (!__ldcg(a.cnt + C_PU_CHG) || cap >= a.max_bucket) break;
+    int chg, u1, u2;
+    cta_bcast3(a.cnt + C_PU_CHG, nullptr, nullptr, chg, u1, u2);
+    if (!chg || cap >= a.max_bucket) break;
     cap = min(cap * 8, (long long)a.max_bucket);
     if (tid == 0) { f.cnt[0] = f.cnt[1] = f.cnt[2] = 0; }
     grid.sync();
@@ -795,6 +892,26 @@ __global__ void arc_fix_kernel(AssignDev a) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0 && cnt) atomicAdd(a.ops + O_FIXED, cnt);
+}
+
+// fixed_t = transpose of the fixed bitmask: one warp per 32 x 32 bit block, lane i
+// holds row x = 32 bx + i and 32 ballots deal out the transposed rows
+__global__ void bit_transpose_kernel(const uint32_t *in, uint32_t *out, int n, int nw) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int blk = warp; blk < nw * nw; blk += nwarps) {
+        const int bx = blk / nw, by = blk - bx * nw;
+        const int x = bx * 32 + lane;
+        const uint32_t v = x < n ? in[(size_t)x * nw + by] : 0u;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (v >> j) & 1u);
+            if (lane == j) mine = b;
+        }
+        const int y = by * 32 + lane;
+        if (y < n) out[(size_t)y * nw + bx] = mine;
+    }
 }
 
 // max |w| over present arcs (scaled_cost_bound = (n+1) max|w|, assign_scaling.py:133)
@@ -874,6 +991,7 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     FM_CHECK_CUDA(cudaMemsetAsync(d.frozen_in, 0, sizeof(int32_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.ybcnt, 0, sizeof(int32_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.fixed, 0, sizeof(uint32_t) * (size_t)n * d.nw, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(d.fixed_t, 0, sizeof(uint32_t) * (size_t)n * d.nw, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * 16, s));
     FM_CHECK_CUDA(cudaMemsetAsync(A->acc, 0, sizeof(unsigned long long) * 4, s));
     weight_bound_kernel<<<A->sms * 4, 256, 0, s>>>(w, (int64_t)n * n, A->acc);
@@ -944,6 +1062,10 @@ int assign_one_refine(fm_assign *A) {
         arc_fix_kernel<<<std::max(1, std::min((n + 7) / 8, A->sms * 8)), 256, 0, s>>>(d);
         FM_CHECK_LAUNCH();
         A->st.launches++;
+        bit_transpose_kernel<<<std::max(1, std::min((d.nw * d.nw + 7) / 8, A->sms * 8)), 256, 0, s>>>(
+            d.fixed, d.fixed_t, n, d.nw);
+        FM_CHECK_LAUNCH();
+        A->st.launches++;
     }
     A->st.refines++;
     if (A->h_cnt[C_INFEASIBLE]) {
@@ -987,6 +1109,8 @@ int assign_finish(fm_assign *A, int rc, int64_t *objective_out, int32_t *match_o
     A->st.reserved[0] = (int64_t)A->h_ops[O_FIXED];      // pairs fixed
     A->st.reserved[1] = (int64_t)A->h_ops[O_PU];         // price updates
     A->st.reserved[2] = (int64_t)A->h_ops[O_PU_ITERS];   // Bellman-Ford iterations in them
+    A->st.cut_sweeps = (int64_t)A->h_ops[O_PU_YS];       // price update: frontier Y visits
+    A->st.pr_tiles = (int64_t)A->h_ops[O_PU_ITNS];       // price update: ns inside Bellman-Ford iterations (CTA 0)
     A->st.reserved[3] = (int64_t)A->h_ops[O_TAIL_OPS];   // ops done by the single-CTA tail
     A->st.ms_cut = 1e-6 * (double)A->h_ops[O_TAIL_NS];   // time in single-CTA tail rounds
     A->st.ms_d2h = 1e-6 * (double)A->h_ops[O_MULTI_NS];  // time in grid-wide rounds
@@ -1032,6 +1156,7 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMalloc((void **)&d.match, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.ey, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.fixed, sizeof(uint32_t) * (size_t)n * A->nw) == cudaSuccess &&
+              cudaMalloc((void **)&d.fixed_t, sizeof(uint32_t) * (size_t)n * A->nw) == cudaSuccess &&
               cudaMalloc((void **)&d.frozen, n) == cudaSuccess &&
               cudaMalloc((void **)&d.frozen_in, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.xlist[0], sizeof(int32_t) * n) == cudaSuccess &&
@@ -1078,7 +1203,7 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
 extern "C" void fm_assign_destroy(fm_assign *A) {
     if (!A) return;
     cudaSetDevice(A->device);
-    void *dev[] = {A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.frozen, A->d.frozen_in,
+    void *dev[] = {A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.fixed_t, A->d.frozen, A->d.frozen_in,
                    A->d.xlist[0], A->d.xlist[1], A->d.ylist[0], A->d.ylist[1], A->d.cnt, A->d.ops,
                    A->d.lx, A->d.ly, A->d.ybcnt, A->d.ybuf, A->wt, A->pu.fy[0], A->pu.fy[1], A->pu.fx[0], A->pu.fx[1],
                    A->pu.in_fx, A->pu.in_fy, A->pu.cnt,
