@@ -1071,7 +1071,7 @@ __global__ void __launch_bounds__(256) bfs_tile_kernel(GridDev g, int parity, in
 // ----------------------------------------------------------------------------
 constexpr int BB_WARPS = 4;   // tiles in flight per CTA (one per warp)
 
-__device__ __forceinline__ void bits_row(const GridDev &g, int tile, int lr, int lane) {
+__device__ __forceinline__ uint32_t bits_row(const GridDev &g, int tile, int lr, int lane) {
     const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
     const int r = tyi * PT_H + lr, c = txi * PT_W + lane;
     const bool in = r < g.H && c < g.W && !is_ghost_row(g, r);
@@ -1087,16 +1087,21 @@ __device__ __forceinline__ void bits_row(const GridDev &g, int tile, int lr, int
     uint32_t *B = g.rbits + (size_t)tile * 160 + lr;
     if (lane < 5) B[lane * 32] = w[lane];
     if (r < g.H && c < g.W) g.dist[p] = aT ? 1 : g.INF;
+    return w[4];
 }
 
-// listed == 0: every tile; listed == 1: the tiles of bq.list[0] (local relabel region)
-__global__ void bfs_init_bits_kernel(GridDev g, int listed) {
+// listed == 0: every tile; listed == 1: the tiles of bq.list[0] (local relabel region).
+// seed (with listed == 0): queue the tiles holding a sink arc in bq[0] -- the only
+// tiles whose first BFS visit can find anything; the rest are queued by neighbours.
+__global__ void bfs_init_bits_kernel(GridDev g, int listed, int seed) {
     const int lane = threadIdx.x & 31;
     const int64_t nrows = listed ? (int64_t)__ldcg(g.bq.cnt + 0) * PT_H : (int64_t)g.ntx * g.nty * PT_H;
     for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int k = (int)(w / PT_H), lr = (int)(w % PT_H);
-        bits_row(g, listed ? g.bq.list[0][k] : k, lr, lane);
+        const int tile = listed ? g.bq.list[0][k] : k;
+        const uint32_t t_bits = bits_row(g, tile, lr, lane);
+        if (seed && t_bits && lane == 0) tq_push(g.bq, 0, tile);
     }
 }
 
@@ -1227,7 +1232,8 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         q.ctr[0] = 0; q.ctr[32] = n0; q.ctr[64] = n0; q.ctr[96] = 0;
-        q.ctr[128] = 0; q.ctr[160] = 0; q.ctr[161] = 0; q.ctr[224] = n0;
+        q.ctr[128] = 0; q.ctr[160] = 0; q.ctr[161] = 0; q.ctr[192] = 0; q.ctr[224] = n0;
+        q.ctr[240] = q.ctr[241] = q.ctr[244] = q.ctr[245] = 0;
     }
 }
 
@@ -1276,26 +1282,30 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
         const uint32_t *B = g.rbits + (size_t)tile * 160;
         const uint32_t mR = B[lane], mL = B[32 + lane], mD = B[64 + lane], mU = B[96 + lane], mT = B[128 + lane];
         bool again = true;
+#ifdef FM_BFS_TIMING
+        const long long tv0 = clock64();
+        int lv = 0;
+#endif
         while (again) {
-        // the tile's current distances (lane = column), read once per visit
-#pragma unroll 8
-        for (int i = 0; i < PT_H; i++) {
-            const int r = r0 + i;
-            sd[i * (PT_W + 1) + lane] = (r < g.H && cl < g.W) ? ld_cg(g.dist + (int64_t)r * g.W + cl) : INF;
-        }
+        // Halo distances, the tile's own border distances (for change detection) and
+        // imported ghost rows.  The interior is recomputed from scratch: a visit's
+        // halos are never larger than the previous visit's (distances only fall and
+        // the owner is exclusive), so every pixel it reaches gets a value <= the old one
+        // and can be written without reading it first.
         const int ht = (r0 > 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 - 1) * g.W + cl) : INF;
         const int hb = (r0 + PT_H < g.H && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + PT_H) * g.W + cl) : INF;
         const int hl = (c0 > 0 && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 - 1) : INF;
         const int hr = (c0 + PT_W < g.W && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + PT_W) : INF;
-        __syncwarp();
-        const int gv0 = g0 >= 0 ? sd[g0 * (PT_W + 1) + lane] : INF;
-        const int gv1 = g1 >= 0 ? sd[g1 * (PT_W + 1) + lane] : INF;
-        // level-synchronous BFS; a pixel reached at level L keeps min(old, L)
-        uint32_t F = mT, seen = mT, chg = 0;
-        for (uint32_t x = mT; x; x &= x - 1) {
-            const int k = lane * (PT_W + 1) + __ffs(x) - 1;
-            if (sd[k] > 1) { sd[k] = 1; chg |= x & (~x + 1); }
-        }
+        const int last_r = min(PT_H, g.H - r0) - 1, last_c = min(PT_W, g.W - c0) - 1;
+        const int ot = cl < g.W ? ld_cg(g.dist + (int64_t)r0 * g.W + cl) : INF;                 // own top row
+        const int ob = cl < g.W ? ld_cg(g.dist + (int64_t)(r0 + last_r) * g.W + cl) : INF;      // own bottom row
+        const int ol = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0) : INF;                  // own left column
+        const int orr = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + last_c) : INF;        // own right column
+        const int gv0 = (g0 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g0) * g.W + cl) : INF;
+        const int gv1 = (g1 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g1) * g.W + cl) : INF;
+        // level-synchronous BFS; sd[row][col] = level at which the pixel was reached
+        uint32_t F = mT, seen = mT;
+        for (uint32_t x = mT; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = 1;
         int L = 1;
         for (;;) {
             if (g0 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv0 == L); if (lane == g0) F |= s; }
@@ -1312,10 +1322,10 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
             N &= ~seen;
             seen |= N;
             L++;
-            for (uint32_t x = N; x; x &= x - 1) {
-                const int k = lane * (PT_W + 1) + __ffs(x) - 1;
-                if (sd[k] > L) { sd[k] = L; chg |= x & (~x + 1); }
-            }
+#ifdef FM_BFS_TIMING
+            lv++;
+#endif
+            for (uint32_t x = N; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = L;
             F = N;
             if (!__any_sync(0xffffffffu, F != 0)) {
                 int m = INF;
@@ -1331,18 +1341,31 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
             }
         }
         __syncwarp();
-        // write back the pixels that fell (this warp owns the tile while in flight)
-        const uint32_t any_chg = __ballot_sync(0xffffffffu, chg != 0);
-        for (uint32_t rows = any_chg; rows; rows &= rows - 1) {
+        // write back every reached pixel (lane = column); borders compared with the old values
+        const uint32_t any_seen = __ballot_sync(0xffffffffu, seen != 0);
+        bool ct = false, cb = false;
+        for (uint32_t rows = any_seen; rows; rows &= rows - 1) {
             const int i = __ffs(rows) - 1;
-            const uint32_t cr = __shfl_sync(0xffffffffu, chg, i);
-            if ((cr >> lane) & 1) g.dist[(int64_t)(r0 + i) * g.W + cl] = sd[i * (PT_W + 1) + lane];
+            const uint32_t sr = __shfl_sync(0xffffffffu, seen, i);
+            if (((sr >> lane) & 1) && cl < g.W && i != g0 && i != g1) {
+                const int v = sd[i * (PT_W + 1) + lane];
+                g.dist[(int64_t)(r0 + i) * g.W + cl] = v;
+                ct |= i == 0 && v < ot;
+                cb |= i == last_r && v < ob;
+            }
         }
-        const int b0 = any_chg & 1, b1 = (any_chg >> 31) & 1;
-        const int b2 = __any_sync(0xffffffffu, chg & 1u), b3 = __any_sync(0xffffffffu, chg >> 31);
+        // own left / right columns: lane = row
+        const bool sl = (seen & 1u) && lane <= last_r && lane != g0 && lane != g1;
+        const bool sr_ = ((seen >> last_c) & 1u) && lane <= last_r && lane != g0 && lane != g1;
+        const bool cl_ = sl && sd[lane * (PT_W + 1)] < ol;
+        const bool cr_ = sr_ && sd[lane * (PT_W + 1) + last_c] < orr;
+        const uint32_t any_chg = __ballot_sync(0xffffffffu, ct || cb || cl_ || cr_);
+        const int b0 = __any_sync(0xffffffffu, ct), b1 = __any_sync(0xffffffffu, cb);
+        const int b2 = __any_sync(0xffffffffu, cl_), b3 = __any_sync(0xffffffffu, cr_);
         int st = 0;
         if (lane == 0) {
             if (any_chg) atomicAdd(q.ctr + 96, 1u);
+            atomicAdd(q.ctr + 192, 1u);   // every visit (diagnostics)
             if (b0 | b1 | b2 | b3) {
                 __threadfence();
                 const auto in = [&](int t) { return !g.region || g.region[t]; };
@@ -1368,6 +1391,12 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
         again = __shfl_sync(0xffffffffu, st, 0) == 3;
         __syncwarp();
         }  // while again
+#ifdef FM_BFS_TIMING
+        if (lane == 0) {
+            atomicAdd((unsigned long long *)(q.ctr + 240), (unsigned long long)(clock64() - tv0));
+            atomicAdd((unsigned long long *)(q.ctr + 244), (unsigned long long)lv);
+        }
+#endif
     }
 }
 
@@ -2070,7 +2099,9 @@ int bfs_init(fm_grid *g, bool listed, int nlisted = 0) {
     if (g->bfs_bits) {
         const int rows = (listed ? nlisted : g->ntiles) * PT_H;
         const int blocks = std::max(1, std::min((rows + 7) / 8, g->sms * 16));
-        bfs_init_bits_kernel<<<blocks, 256, 0, g->stream>>>(g->d, listed ? 1 : 0);
+        const int seed = !listed && g->bfs_bits == 2;
+        if (seed) FM_TRY(tq_reset(g, g->d.bq));
+        bfs_init_bits_kernel<<<blocks, 256, 0, g->stream>>>(g->d, listed ? 1 : 0, seed);
     } else if (listed) {
         bfs_init_local_kernel<<<std::max(1, std::min(nlisted, g->sms * 8)), 256, 0, g->stream>>>(g->d);
     } else {
@@ -2087,8 +2118,9 @@ int bfs_init(fm_grid *g, bool listed, int nlisted = 0) {
 // collected by bfs_collect() after the caller's next stream sync.
 int bfs_sweeps(fm_grid *g, bool first_all) {
     if (g->bfs_bits == 2) {
-        const int32_t *list0 = first_all ? nullptr : g->d.bq.list[g->bq_parity];
-        const int32_t *cnt0 = first_all ? nullptr : g->d.bq.cnt + 2 * g->bq_parity;
+        // first_all: the tiles bfs_init queued (those with a sink arc) -- see bfs_init_bits_kernel
+        const int32_t *list0 = first_all ? g->d.bq.list[0] : g->d.bq.list[g->bq_parity];
+        const int32_t *cnt0 = first_all ? g->d.bq.cnt + 0 : g->d.bq.cnt + 2 * g->bq_parity;
         ringq_init_kernel<<<std::min((g->rq.cap + 255) / 256, g->sms * 8), 256, 0, g->stream>>>(g->rq, g->ntiles, list0, cnt0);
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[2], g->stream);
@@ -2096,6 +2128,8 @@ int bfs_sweeps(fm_grid *g, bool first_all) {
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[3], g->stream);
         FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 8, g->rq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 10, g->rq.ctr + 192, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 11, g->rq.ctr + 224, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
         FM_TRY(tq_reset(g, g->d.bq));
         g->bq_parity = 0;
         g->st.launches += 2;
@@ -2118,6 +2152,16 @@ void bfs_collect(fm_grid *g) {
     g->ring_stats_pending = false;
     g->st.ms_bfs_kern += elapsed_between(g->ev[2], g->ev[3]);
     g->st.reserved[0] += g->h_flags[8];
+    const float kms = elapsed_between(g->ev[2], g->ev[3]);
+    if (g->trace) {
+        unsigned long long tv[3] = {};
+        cudaMemcpy(tv, g->rq.ctr + 240, sizeof(tv), cudaMemcpyDeviceToHost);   // FM_BFS_TIMING builds
+        const double warps = (double)g->sms * g->br_per_sm * BB_WARPS;
+        fprintf(stderr, "[fm_grid]   bfs ring: %d seeded tiles, %d visits (%d changed), %.3f ms | busy %.2f, "
+                "cycles/visit %.0f, levels/visit %.1f\n", g->h_flags[11], g->h_flags[10], g->h_flags[8], kms,
+                tv[0] / (kms * 1.965e6 * warps), tv[0] / (double)std::max(1, g->h_flags[10]),
+                tv[2] / (double)std::max(1, g->h_flags[10]));
+    }
 }
 
 int bfs_finalize(fm_grid *g) {
