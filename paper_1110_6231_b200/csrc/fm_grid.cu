@@ -1971,7 +1971,7 @@ struct fm_grid {
                                          // sweeps (bfs_bits_kernel), 0: v1 Jacobi sweeps (env FM_BFS_BITS)
     int bb_per_sm = 8;                   // resident bfs_bits CTAs per SM (occupancy query)
     int br_per_sm = 8;                   // resident bfs_ring CTAs per SM (occupancy query, <= br_cap)
-    int br_cap = 6;                      // env FM_BR_CAP
+    int br_cap = 8;                      // env FM_BR_CAP
     RingQ rq{};                          // device work queue of the persistent BFS
     RingQ prq{};                         // device work queue of the persistent push round
     int pr_ring = 0;                     // 1: one persistent pr_ring_kernel launch per round (env FM_PR_RING; experimental, slower)
