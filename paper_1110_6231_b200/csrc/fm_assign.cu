@@ -55,7 +55,7 @@ constexpr int C_COUNT = 12;
 constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXED = 4,
               O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7, O_TAIL_NS = 8, O_MULTI_NS = 9,
               O_PH_Y = 10, O_PH_SYNC1 = 11, O_PH_X = 12, O_PH_SYNC2 = 13,  // multi-round phase ns (CTA 0)
-              O_PU_YS = 14, O_PU_ITNS = 15, O_PU_YNS = 3;  // price update: frontier Y visits, ns in BF iterations (CTA 0)
+              O_PU_YS = 14, O_PU_ITNS = 15;  // price update: frontier Y visits, ns in BF iterations (CTA 0)
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -684,7 +684,6 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
         if (ny == 0) break;
         if (tid == 0) atomicAdd(a.ops + O_PU_YS, (unsigned long long)ny);
         if (tid == 0) f.cnt[(it + 2) % 3] = 0;
-        const unsigned long long t_y0 = globaltimer();
         // thread 0 fetches each frontier Y's header (clear its queued flag, then read
         // l(y), p(y)) one Y ahead, so the next header's round trips overlap this scan
         int nxt_y = -1, nxt_l = 0;
@@ -797,7 +796,6 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
             }
             __syncthreads();
         }
-        if (tid == 0) atomicAdd(a.ops + O_PU_YNS, globaltimer() - t_y0);
         grid.sync();
     }
     it_total += it + 1;
