@@ -1233,7 +1233,7 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         q.ctr[0] = 0; q.ctr[32] = n0; q.ctr[64] = n0; q.ctr[96] = 0;
         q.ctr[128] = 0; q.ctr[160] = 0; q.ctr[161] = 0; q.ctr[192] = 0; q.ctr[224] = n0;
-        q.ctr[240] = q.ctr[241] = q.ctr[244] = q.ctr[245] = 0;
+        q.ctr[240] = q.ctr[241] = q.ctr[244] = q.ctr[245] = q.ctr[246] = q.ctr[247] = 0;
     }
 }
 
@@ -1307,6 +1307,9 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
         uint32_t F = mT, seen = mT;
         for (uint32_t x = mT; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = 1;
         int L = 1;
+#ifdef FM_BFS_TIMING
+        const long long tl0 = clock64();
+#endif
         for (;;) {
             if (g0 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv0 == L); if (lane == g0) F |= s; }
             if (g1 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv1 == L); if (lane == g1) F |= s; }
@@ -1341,6 +1344,9 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
             }
         }
         __syncwarp();
+#ifdef FM_BFS_TIMING
+        if (lane == 0) atomicAdd((unsigned long long *)(q.ctr + 246), (unsigned long long)(clock64() - tl0));
+#endif
         // write back every reached pixel (lane = column); borders compared with the old values
         const uint32_t any_seen = __ballot_sync(0xffffffffu, seen != 0);
         bool ct = false, cb = false;
@@ -1363,17 +1369,25 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
         const int b0 = __any_sync(0xffffffffu, ct), b1 = __any_sync(0xffffffffu, cb);
         const int b2 = __any_sync(0xffffffffu, cl_), b3 = __any_sync(0xffffffffu, cr_);
         int st = 0;
+        // lanes 0-3 queue the up / down / left / right neighbour in parallel (each queue
+        // push is a chain of atomics; the fence publishes the warp's distance writes)
+        if (lane < 4) {
+            int nt = -1;
+            if (lane == 0 && b0 && tyi > 0) nt = tile - g.ntx;
+            if (lane == 1 && b1 && tyi + 1 < g.nty) nt = tile + g.ntx;
+            if (lane == 2 && b2 && txi > 0) nt = tile - 1;
+            if (lane == 3 && b3 && txi + 1 < g.ntx) nt = tile + 1;
+            if (nt >= 0 && (!g.region || g.region[nt])) {
+                __threadfence();
+                ringq_push(q, nt);
+            }
+        }
+        __syncwarp();   // the pushes (pending++) precede lane 0's pending-- below
         if (lane == 0) {
             if (any_chg) atomicAdd(q.ctr + 96, 1u);
+#ifdef FM_BFS_TIMING
             atomicAdd(q.ctr + 192, 1u);   // every visit (diagnostics)
-            if (b0 | b1 | b2 | b3) {
-                __threadfence();
-                const auto in = [&](int t) { return !g.region || g.region[t]; };
-                if (b0 && tyi > 0 && in(tile - g.ntx)) ringq_push(q, tile - g.ntx);
-                if (b1 && tyi + 1 < g.nty && in(tile + g.ntx)) ringq_push(q, tile + g.ntx);
-                if (b2 && txi > 0 && in(tile - 1)) ringq_push(q, tile - 1);
-                if (b3 && txi + 1 < g.ntx && in(tile + 1)) ringq_push(q, tile + 1);
-            }
+#endif
             st = atomicCAS(q.flag + tile, 2, 0);
             if (st == 3) {
                 if (q.rerun) { atomicExch(q.flag + tile, 2); __threadfence(); }
@@ -2154,13 +2168,13 @@ void bfs_collect(fm_grid *g) {
     g->st.reserved[0] += g->h_flags[8];
     const float kms = elapsed_between(g->ev[2], g->ev[3]);
     if (g->trace) {
-        unsigned long long tv[3] = {};
+        unsigned long long tv[4] = {};
         cudaMemcpy(tv, g->rq.ctr + 240, sizeof(tv), cudaMemcpyDeviceToHost);   // FM_BFS_TIMING builds
         const double warps = (double)g->sms * g->br_per_sm * BB_WARPS;
         fprintf(stderr, "[fm_grid]   bfs ring: %d seeded tiles, %d visits (%d changed), %.3f ms | busy %.2f, "
-                "cycles/visit %.0f, levels/visit %.1f\n", g->h_flags[11], g->h_flags[10], g->h_flags[8], kms,
+                "cycles/visit %.0f (level loop %.0f), levels/visit %.1f\n", g->h_flags[11], g->h_flags[10], g->h_flags[8], kms,
                 tv[0] / (kms * 1.965e6 * warps), tv[0] / (double)std::max(1, g->h_flags[10]),
-                tv[2] / (double)std::max(1, g->h_flags[10]));
+                tv[3] / (double)std::max(1, g->h_flags[10]), tv[2] / (double)std::max(1, g->h_flags[10]));
     }
 }
 
