@@ -1989,6 +1989,8 @@ struct fm_grid {
     RingQ rq{};                          // device work queue of the persistent BFS
     RingQ prq{};                         // device work queue of the persistent push round
     int pr_ring = 0;                     // 1: one persistent pr_ring_kernel launch per round (env FM_PR_RING; experimental, slower)
+    int k_tail = 0;                      // passes per visit in tail rounds (0: k_local) (env FM_K_TAIL)
+    int tail_div = 1024;                 // tail round: active pixels <= H*W / tail_div (env FM_TAIL_DIV)
     int pr_batch = 4;                    // push launches between host checks of the round triggers (env FM_PR_BATCH)
     int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (env FM_VISIT_MULT)
     bool ring_stats_pending = false;
@@ -2322,7 +2324,9 @@ int run_round_global(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int
 int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int32_t *idle_out = nullptr) {
     const int k_default = g->pr_kernel == 1 ? (g->k_local_list > 0 ? g->k_local_list : K_LOCAL_LIST_DEFAULT)
                                             : (g->k_local > 0 ? g->k_local : K_LOCAL_DEFAULT);
-    const int k_local = std::max(1, std::min(cycle_budget, k_default));
+    // tail rounds (few active pixels, far from the sink): more passes per visit
+    const bool tail = g->k_tail > 0 && g->active <= g->HW / std::max(1, g->tail_div);
+    const int k_local = std::max(1, std::min(cycle_budget, tail ? g->k_tail : k_default));
     if (bfs_interval <= 0 && g->bfs_interval_env > 0) bfs_interval = g->bfs_interval_env;
     const int32_t cap = std::max(1, std::min((cycle_budget + k_local - 1) / k_local,
                                              bfs_interval > 0 ? bfs_interval : MAX_LAUNCHES_DEFAULT));
@@ -2568,6 +2572,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
     g->d.solo_max = 32;
     if (const char *v = getenv("FM_SOLO_MAX")) g->d.solo_max = atoi(v);
+    if (const char *v = getenv("FM_K_TAIL")) g->k_tail = atoi(v);
+    if (const char *v = getenv("FM_TAIL_DIV")) g->tail_div = atoi(v);
     if (const char *v = getenv("FM_PR_BATCH")) g->pr_batch = std::max(1, std::min(16, atoi(v)));
     if (const char *v = getenv("FM_VISIT_MULT")) g->visit_mult = std::max(1, atoi(v));
     g->rq.rerun = 0; g->rq.ns0 = 128; g->rq.ns1 = 2048;
@@ -2635,6 +2641,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->pt_per_sm = std::max(1, g->pt_per_sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pl_per_sm, pr_list_kernel, PT_W * PL_TY, 0);
     g->pl_per_sm = std::max(1, g->pl_per_sm);
+    if (const char *v = getenv("FM_PL_PER_SM")) g->pl_per_sm = std::max(1, std::min(g->pl_per_sm, atoi(v)));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->bb_per_sm, bfs_bits_kernel, 32 * BB_WARPS, 0);
     g->bb_per_sm = std::max(1, g->bb_per_sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->br_per_sm, bfs_ring_kernel, 32 * BB_WARPS, 0);
