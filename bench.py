@@ -268,6 +268,7 @@ def main():
     ap.add_argument("--no-assign", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-big", action="store_true", help="skip the 8192^2 single-GPU solve")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test the banded path with several ranks sharing fewer GPUs")
     args = ap.parse_args()
@@ -403,6 +404,26 @@ def main():
                "solve_ms": round(ms2, 3), "medges_per_s": round(e_grid(2048, 2048) / (ms2 / 1000) / 1e6, 1),
                "rounds": st2["rounds"], "pushes": st2["pushes"], "relabels": st2["relabels"]}
 
+    # config 3's grid (8192^2, generator G seed 8192) on this single GPU: the N=1 point
+    # of the row-band scaling series
+    big = None
+    if rank == 0 and not args.no_assign and not args.no_big:
+        B8 = 8192
+        cb = [torch.from_numpy(np.ascontiguousarray(c)).cuda() for c in G.grid_random(B8, B8, B8)]
+        cut3 = torch.empty((B8, B8), dtype=torch.uint8, device="cuda")
+        sv = fmb.GridSolver(B8, B8, device=local)
+        sv.solve_device(cb, cut_out=cut3, stream=stream)
+        tms = []
+        for _ in range(2):
+            f3, st3 = sv.solve_device(cb, cut_out=cut3, stream=stream)
+            tms.append(st3["ms_total"])
+        sv.close()
+        del cb, cut3
+        ms3 = statistics.mean(tms)
+        big = {"workload": "generator G 8192x8192 seed 8192 on 1 GPU (config 3, N=1)", "flow": f3,
+               "solve_ms": round(ms3, 3), "medges_per_s": round(e_grid(B8, B8) / (ms3 / 1000) / 1e6, 1),
+               "rounds": st3["rounds"], "pushes": st3["pushes"], "relabels": st3["relabels"]}
+
     # assignment n = 4096 (single GPU; replicas only)
     assign = None
     if not args.no_assign and rank == 0:
@@ -463,7 +484,7 @@ def main():
                            "cycle_budget": 7000, "bfs_interval": args.bfs_interval},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(agg.get("launches", 0)), "clocks": clk,
-                "per_solve": per, "segmentation_2048": seg, "assignment_n4096": assign}
+                "per_solve": per, "segmentation_2048": seg, "grid_8192_1gpu": big, "assignment_n4096": assign}
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()

@@ -160,3 +160,14 @@ def test_degenerate_shapes(H, W):
     want = oracle.grid_maxflow(*caps, solver="seq")
     rep = _solve(caps)
     assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
+
+
+def test_certificate_at_8192():
+    """Config 3's grid on one GPU: certified maximum flow and minimal cut."""
+    caps = G.grid_random(8192, 8192, 8192)
+    solver = fmb.GridSolver(8192, 8192)
+    flow, cut, st = solver.solve_host(caps)
+    state = solver.export()
+    code, fl, cc, ns = oracle.grid_certify(caps, state, cut)
+    solver.close()
+    assert code == 0 and fl == cc == flow
