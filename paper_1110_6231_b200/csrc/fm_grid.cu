@@ -1514,12 +1514,42 @@ __global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsi
     for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
         const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
         bool act = false;
+        const int r = tyi * PT_H + (threadIdx.x >> 3), c = txi * PT_W + 4 * (threadIdx.x & 7);
+        if ((g.W & 3) == 0 && (tyi + 1) * PT_H <= g.H && (txi + 1) * PT_W <= g.W) {
+            // interior tile, W % 4 == 0: 4 consecutive pixels per thread, 16-byte accesses
+            const int64_t p = (int64_t)r * g.W + c;
+            if (!is_ghost_row(g, r)) {
+                const int4 d4 = *(const int4 *)(g.dist + p), e4 = *(const int4 *)(g.e + p);
+                int4 h4 = *(const int4 *)(g.h + p);
+                uchar4 m4 = *(const uchar4 *)(g.marked + p);
+                const int dv[4] = {d4.x, d4.y, d4.z, d4.w}, ev[4] = {e4.x, e4.y, e4.z, e4.w};
+                int hv[4] = {h4.x, h4.y, h4.z, h4.w};
+                unsigned char mv[4] = {m4.x, m4.y, m4.z, m4.w};
+                bool mchg = false;
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    if (dv[j] < g.INF) {
+                        hv[j] = dv[j];
+                        active += ev[j] > 0;
+                        act |= ev[j] > 0;
+                        lvl = max(lvl, dv[j]);
+                    } else {
+                        if (hv[j] < g.V) hv[j] = g.V;
+                        if (!mv[j]) { mv[j] = 1; mex += ev[j]; mchg = true; }
+                    }
+                }
+                *(int4 *)(g.h + p) = make_int4(hv[0], hv[1], hv[2], hv[3]);
+                if (mchg) *(uchar4 *)(g.marked + p) = make_uchar4(mv[0], mv[1], mv[2], mv[3]);
+            }
+            if (__syncthreads_or(act) && threadIdx.x == 0) tq_push(g.pq, 0, tile);
+            continue;
+        }
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const int lr = (threadIdx.x >> 5) + 8 * k;
-            const int r = tyi * PT_H + lr, c = txi * PT_W + (threadIdx.x & 31);
-            if (r >= g.H || c >= g.W || is_ghost_row(g, r)) continue;
-            const int64_t p = (int64_t)r * g.W + c;
+            const int rr = tyi * PT_H + lr, cc = txi * PT_W + (threadIdx.x & 31);
+            if (rr >= g.H || cc >= g.W || is_ghost_row(g, rr)) continue;
+            const int64_t p = (int64_t)rr * g.W + cc;
             const int32_t d = g.dist[p];
             const int32_t e = g.e[p];
             if (d < g.INF) {
