@@ -1101,7 +1101,7 @@ __global__ void bfs_init_bits_kernel(GridDev g, int listed, int seed) {
         const int k = (int)(w / PT_H), lr = (int)(w % PT_H);
         const int tile = listed ? g.bq.list[0][k] : k;
         const uint32_t t_bits = bits_row(g, tile, lr, lane);
-        if (seed && t_bits && lane == 0) tq_push(g.bq, 0, tile);
+        if (seed && t_bits && lane == 0 && !__ldcg(g.bq.flag[0] + tile)) tq_push(g.bq, 0, tile);
     }
 }
 
@@ -1507,11 +1507,14 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_ring_kernel(GridDev
 
 // gap_relabel + marking (as bfs_finalize_kernel), one CTA per tile so each tile with
 // an active pixel is queued once
-__global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsigned long long *acc) {
+// list == nullptr: every tile; else the n tiles of `list` (local relabel region)
+__global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsigned long long *acc,
+                                                                 const int32_t *list, int n) {
     long long active = 0, mex = 0;
     int32_t lvl = 0;
-    const int nt = g.ntx * g.nty;
-    for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+    const int nt = list ? n : g.ntx * g.nty;
+    for (int it = blockIdx.x; it < nt; it += gridDim.x) {
+        const int tile = list ? list[it] : it;
         const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
         bool act = false;
         const int r = tyi * PT_H + (threadIdx.x >> 3), c = txi * PT_W + 4 * (threadIdx.x & 7);
@@ -2212,7 +2215,7 @@ void bfs_collect(fm_grid *g) {
 
 int bfs_finalize(fm_grid *g) {
     if (g->bfs_bits)
-        bfs_finalize_tiles_kernel<<<std::min(g->ntiles, g->sms * 8), 256, 0, g->stream>>>(g->d, g->acc + 4);
+        bfs_finalize_tiles_kernel<<<std::min(g->ntiles, g->sms * 8), 256, 0, g->stream>>>(g->d, g->acc + 4, nullptr, 0);
     else
         bfs_finalize_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 4);
     FM_CHECK_LAUNCH();
@@ -2267,8 +2270,12 @@ int local_relabel(fm_grid *g) {
         FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
         FM_TRY(tq_reset(g, g->d.pq));
         g->pq_parity = 0;
-        bfs_finalize_local_kernel<<<std::max(1, std::min(nr, g->sms * 8)), 256, 0, g->stream>>>(
-            g->d, g->d_rlist, nr, g->acc + 4);
+        if (g->bfs_bits)
+            bfs_finalize_tiles_kernel<<<std::max(1, std::min(nr, g->sms * 8)), 256, 0, g->stream>>>(
+                g->d, g->acc + 4, g->d_rlist, nr);
+        else
+            bfs_finalize_local_kernel<<<std::max(1, std::min(nr, g->sms * 8)), 256, 0, g->stream>>>(
+                g->d, g->d_rlist, nr, g->acc + 4);
         FM_CHECK_LAUNCH();
         g->st.launches++;
         FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 4, g->acc + 4, sizeof(unsigned long long) * 3,
