@@ -144,6 +144,52 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
 }
 
 // ----------------------------------------------------------------------------
+// Two-hop pre-routing (after init, before the first global relabel): a pixel holding
+// excess sends it straight on through a neighbour that still has sink capacity
+// (s -> p -> q -> t augmentations).  After pre-cancellation a pixel either holds
+// excess or sink capacity, never both, so the only contended word is rT(q), taken
+// with a compare-and-swap; residual pairs are updated atomically.  The result is a
+// valid preflow, so flow value and minimal cut are unchanged; it only removes work
+// the first push rounds would otherwise do pixel by pixel.
+// ----------------------------------------------------------------------------
+__global__ void two_hop_kernel(GridDev g) {
+    const int64_t HW = (int64_t)g.H * g.W;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t e = g.e[p];
+        if (e <= 0) continue;
+        const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
+        if (is_ghost_row(g, r)) continue;
+        int32_t *fwd[4] = {g.rR, g.rL, g.rD, g.rU};
+        int32_t *rev[4] = {g.rL, g.rR, g.rU, g.rD};
+        const bool ok[4] = {c + 1 < g.W, c > 0, r + 1 < g.H, r > 0};
+        const int64_t qs[4] = {p + 1, p - 1, p + g.W, p - g.W};
+#pragma unroll
+        for (int d = 0; d < 4; d++) {
+            if (e <= 0 || !ok[d]) continue;
+            const int64_t q = qs[d];
+            if (is_ghost_row(g, (int32_t)(q / g.W))) continue;
+            const int32_t rp = *(volatile int32_t *)(fwd[d] + p);
+            int32_t want = min(e, rp);
+            if (want <= 0) continue;
+            int32_t t = *(volatile int32_t *)(g.rT + q), take = 0;
+            while (t > 0) {
+                take = min(want, t);
+                const int32_t old = atomicCAS(g.rT + q, t, t - take);
+                if (old == t) break;
+                t = old;
+                take = 0;
+            }
+            if (take <= 0) continue;
+            e -= take;
+            atomicSub(fwd[d] + p, take);
+            atomicAdd(rev[d] + q, take);
+        }
+        g.e[p] = e;
+    }
+}
+
+// ----------------------------------------------------------------------------
 // K1 (v1): one lock-free sweep, one thread per pixel (maxflow_par.py:95-128).
 // Skip if e <= 0 or h >= |V|; find the lowest residual neighbour among
 // {t (height 0), right, left, down, up, s (height |V|)}; push min(e, r) with four
@@ -2022,6 +2068,7 @@ struct fm_grid {
     RingQ rq{};                          // device work queue of the persistent BFS
     RingQ prq{};                         // device work queue of the persistent push round
     int pr_ring = 0;                     // 1: one persistent pr_ring_kernel launch per round (env FM_PR_RING; experimental, slower)
+    int two_hop = 1;                     // two-hop pre-routing after init (env FM_TWO_HOP)
     int k_tail = 0;                      // passes per visit in tail rounds (0: k_local) (env FM_K_TAIL)
     int tail_div = 1024;                 // tail round: active pixels <= H*W / tail_div (env FM_TAIL_DIV)
     int pr_batch = 4;                    // push launches between host checks of the round triggers (env FM_PR_BATCH)
@@ -2315,6 +2362,11 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     // HybridState.excess_total = sum of excess after init_preflow = sum capS
     // (maxflow_par.py:56); pre-cancelled units are already at t.
     g->excess_total = g->sum_capS;
+    if (g->two_hop && !(flags & FM_GRID_NO_PRECANCEL)) {
+        two_hop_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
+        FM_CHECK_LAUNCH();
+        g->st.launches++;
+    }
     return global_relabel(g);
 }
 
@@ -2610,6 +2662,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->d.solo_max = 32;
     if (const char *v = getenv("FM_SOLO_MAX")) g->d.solo_max = atoi(v);
     if (const char *v = getenv("FM_K_TAIL")) g->k_tail = atoi(v);
+    if (const char *v = getenv("FM_TWO_HOP")) g->two_hop = atoi(v);
     if (const char *v = getenv("FM_TAIL_DIV")) g->tail_div = atoi(v);
     if (const char *v = getenv("FM_PR_BATCH")) g->pr_batch = std::max(1, std::min(16, atoi(v)));
     if (const char *v = getenv("FM_VISIT_MULT")) g->visit_mult = std::max(1, atoi(v));
