@@ -154,39 +154,43 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
 // ----------------------------------------------------------------------------
 __global__ void two_hop_kernel(GridDev g) {
     const int64_t HW = (int64_t)g.H * g.W;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        int32_t e = g.e[p];
-        if (e <= 0) continue;
-        const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
-        if (is_ghost_row(g, r)) continue;
-        int32_t *fwd[4] = {g.rR, g.rL, g.rD, g.rU};
-        int32_t *rev[4] = {g.rL, g.rR, g.rU, g.rD};
-        const bool ok[4] = {c + 1 < g.W, c > 0, r + 1 < g.H, r > 0};
-        const int64_t qs[4] = {p + 1, p - 1, p + g.W, p - g.W};
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one thread per pixel
+    if (p >= HW) return;
+    int32_t e = g.e[p];
+    if (e <= 0) return;
+    const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
+    if (is_ghost_row(g, r)) return;
+    int32_t *fwd[4] = {g.rR, g.rL, g.rD, g.rU};
+    int32_t *rev[4] = {g.rL, g.rR, g.rU, g.rD};
+    const bool ok[4] = {c + 1 < g.W && !is_ghost_row(g, r), c > 0 && !is_ghost_row(g, r),
+                        r + 1 < g.H && !is_ghost_row(g, r + 1), r > 0 && !is_ghost_row(g, r - 1)};
+    const int64_t qs[4] = {p + 1, p - 1, p + g.W, p - g.W};
+    // every operand first (one round trip), then a compare-and-swap only where a
+    // neighbour has sink capacity left
+    int32_t rp[4], t[4];
 #pragma unroll
-        for (int d = 0; d < 4; d++) {
-            if (e <= 0 || !ok[d]) continue;
-            const int64_t q = qs[d];
-            if (is_ghost_row(g, (int32_t)(q / g.W))) continue;
-            const int32_t rp = *(volatile int32_t *)(fwd[d] + p);
-            int32_t want = min(e, rp);
-            if (want <= 0) continue;
-            int32_t t = *(volatile int32_t *)(g.rT + q), take = 0;
-            while (t > 0) {
-                take = min(want, t);
-                const int32_t old = atomicCAS(g.rT + q, t, t - take);
-                if (old == t) break;
-                t = old;
-                take = 0;
-            }
-            if (take <= 0) continue;
-            e -= take;
-            atomicSub(fwd[d] + p, take);
-            atomicAdd(rev[d] + q, take);
-        }
-        g.e[p] = e;
+    for (int d = 0; d < 4; d++) {
+        rp[d] = ok[d] ? *(volatile int32_t *)(fwd[d] + p) : 0;
+        t[d] = ok[d] ? *(volatile int32_t *)(g.rT + qs[d]) : 0;
     }
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        const int32_t want = min(e, rp[d]);
+        if (want <= 0 || t[d] <= 0) continue;
+        int32_t tv = t[d], take = 0;
+        while (tv > 0) {
+            take = min(want, tv);
+            const int32_t old = atomicCAS(g.rT + qs[d], tv, tv - take);
+            if (old == tv) break;
+            tv = old;
+            take = 0;
+        }
+        if (take <= 0) continue;
+        e -= take;
+        atomicSub(fwd[d] + p, take);
+        atomicAdd(rev[d] + qs[d], take);
+    }
+    g.e[p] = e;
 }
 
 // ----------------------------------------------------------------------------
@@ -2363,7 +2367,7 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     // (maxflow_par.py:56); pre-cancelled units are already at t.
     g->excess_total = g->sum_capS;
     if (g->two_hop && !(flags & FM_GRID_NO_PRECANCEL)) {
-        two_hop_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d);
+        two_hop_kernel<<<(unsigned)((g->HW + 255) / 256), 256, 0, g->stream>>>(g->d);
         FM_CHECK_LAUNCH();
         g->st.launches++;
     }
