@@ -80,6 +80,7 @@ struct GridDev {
     int32_t V;      // node count |V| = H*W + 2 (the source's height)
     int32_t INF;    // "unreached" distance sentinel (== V)
     int32_t solo_max;   // push kernel: a pass listing <= solo_max pixels runs on warp 0 alone
+    int32_t k_solo;     // push kernel: at most this many solo passes per visit (0: up to k_local)
 };
 
 __device__ __forceinline__ bool is_ghost_row(const GridDev &g, int r) {
@@ -819,7 +820,8 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
         // length is the warp's own running count (no shared counter round trip)
         int n = S.cnt[it % 3];
         const unsigned lt = (1u << tid) - 1;
-        for (; it < k_local && n > 0; it++) {
+        const int it_end = g.k_solo > 0 ? min(k_local, it + g.k_solo) : k_local;
+        for (; it < it_end && n > 0; it++) {
             C.passes++;
             C.items += n;
             const uint16_t *lin = S.list[it & 1];
@@ -2664,6 +2666,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
     if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
     g->d.solo_max = 32;
+    g->d.k_solo = 0;
+    if (const char *v = getenv("FM_K_SOLO")) g->d.k_solo = atoi(v);
     if (const char *v = getenv("FM_SOLO_MAX")) g->d.solo_max = atoi(v);
     if (const char *v = getenv("FM_K_TAIL")) g->k_tail = atoi(v);
     if (const char *v = getenv("FM_TWO_HOP")) g->two_hop = atoi(v);
