@@ -2383,7 +2383,7 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
 // or until the launch cap; then cancel (opt-in), global relabel, gap, mark
 // (maxflow_par.py:195-229).
 constexpr int K_LOCAL_DEFAULT = 32;      // lock-free passes per tile visit (v2)
-constexpr int K_LOCAL_LIST_DEFAULT = 16; // passes per tile visit (v3: a pass over an empty list ends it)
+constexpr int K_LOCAL_LIST_DEFAULT = 20; // passes per tile visit (v3: a pass over an empty list ends it)
 constexpr int MAX_LAUNCHES_DEFAULT = 16; // launch cap per round
 constexpr int RELABEL_DIV_DEFAULT = 16;  // relabel budget = H*W / div
 
