@@ -117,6 +117,11 @@ __device__ __forceinline__ void cta_argmin(long long &v, int &i) {
 // non-fixed arcs of the part-reduced cost c(x,y) - p(y) (assign_scaling.py:170-182,
 // assign_par.py:82-90).  int4 weight loads and longlong2 price loads, four chunks
 // in flight per thread.
+#ifndef FM_RP_CHUNKS
+#define FM_RP_CHUNKS 2
+#endif
+constexpr int RP_CHUNKS = FM_RP_CHUNKS;
+
 __device__ __forceinline__ void row_partial(const AssignDev &a, int x, int t, int T,
                                             long long &bv, int &bi) {
     const int n = a.n;
@@ -126,12 +131,14 @@ __device__ __forceinline__ void row_partial(const AssignDev &a, int x, int t, in
         const int n4 = n >> 2;
         const int4 *row4 = reinterpret_cast<const int4 *>(row);
         const longlong2 *py2 = reinterpret_cast<const longlong2 *>(a.py);
-        for (int j0 = t; j0 < n4; j0 += 4 * T) {
-            int4 w[4];
-            longlong2 pa[4], pb[4];
-            uint32_t fw[4];
+        // RP_CHUNKS int4 chunks in flight per thread (2: the cooperative kernel's
+        // 128-register cap spilled the 4-chunk version to local memory)
+        for (int j0 = t; j0 < n4; j0 += RP_CHUNKS * T) {
+            int4 w[RP_CHUNKS];
+            longlong2 pa[RP_CHUNKS], pb[RP_CHUNKS];
+            uint32_t fw[RP_CHUNKS];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < RP_CHUNKS; u++) {
                 const int j = j0 + u * T;
                 if (j < n4) {
                     w[u] = __ldg(row4 + j);
@@ -141,7 +148,7 @@ __device__ __forceinline__ void row_partial(const AssignDev &a, int x, int t, in
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < RP_CHUNKS; u++) {
                 const int j = j0 + u * T;
                 if (j >= n4) continue;
                 const int wv[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
