@@ -194,6 +194,59 @@ __global__ void two_hop_kernel(GridDev g) {
     g.e[p] = e;
 }
 
+// Three-hop pre-routing (after the two-hop pass): s -> p -> q -> q2 -> t through a
+// neighbour q and one of q's neighbours q2 with spare sink capacity.  r(q -> q2) is
+// reserved first and rT(q2) second (each by compare-and-swap, the unused part of the
+// reservation handed back), so concurrent paths through q never overdraw it.
+__device__ __forceinline__ int32_t cas_take(int32_t *w, int32_t want) {
+    int32_t v = *(volatile int32_t *)w;
+    while (v > 0) {
+        const int32_t take = min(want, v);
+        const int32_t old = atomicCAS(w, v, v - take);
+        if (old == v) return take;
+        v = old;
+    }
+    return 0;
+}
+
+__global__ void three_hop_kernel(GridDev g) {
+    const int64_t HW = (int64_t)g.H * g.W;
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= HW) return;
+    int32_t e = g.e[p];
+    if (e <= 0) return;
+    const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
+    if (is_ghost_row(g, r)) return;
+    int32_t *fwd[4] = {g.rR, g.rL, g.rD, g.rU};
+    int32_t *rev[4] = {g.rL, g.rR, g.rU, g.rD};
+    const int dr[4] = {0, 0, 1, -1}, dc[4] = {1, -1, 0, 0};
+    for (int d1 = 0; d1 < 4 && e > 0; d1++) {
+        const int32_t qr = r + dr[d1], qc = c + dc[d1];
+        if (qr < 0 || qr >= g.H || qc < 0 || qc >= g.W || is_ghost_row(g, qr)) continue;
+        const int64_t q = (int64_t)qr * g.W + qc;
+        for (int d2 = 0; d2 < 4 && e > 0; d2++) {
+            if (d2 == (d1 ^ 1)) continue;                         // back to p
+            const int32_t r2 = qr + dr[d2], c2 = qc + dc[d2];
+            if (r2 < 0 || r2 >= g.H || c2 < 0 || c2 >= g.W || is_ghost_row(g, r2)) continue;
+            const int64_t q2 = (int64_t)r2 * g.W + c2;
+            const int32_t rpq = *(volatile int32_t *)(fwd[d1] + p);
+            const int32_t want = min(e, rpq);
+            if (want <= 0) break;                                 // p -> q saturated
+            if (*(volatile int32_t *)(g.rT + q2) <= 0 || *(volatile int32_t *)(fwd[d2] + q) <= 0) continue;
+            const int32_t a = cas_take(fwd[d2] + q, want);        // reserve q -> q2
+            if (a <= 0) continue;
+            const int32_t b = cas_take(g.rT + q2, a);             // then q2 -> t
+            if (b < a) atomicAdd(fwd[d2] + q, a - b);             // hand back the unused part
+            if (b <= 0) continue;
+            e -= b;
+            atomicSub(fwd[d1] + p, b);
+            atomicAdd(rev[d1] + q, b);
+            atomicAdd(rev[d2] + q2, b);
+        }
+    }
+    g.e[p] = e;
+}
+
 // ----------------------------------------------------------------------------
 // K1 (v1): one lock-free sweep, one thread per pixel (maxflow_par.py:95-128).
 // Skip if e <= 0 or h >= |V|; find the lowest residual neighbour among
@@ -2346,6 +2399,8 @@ int local_relabel(fm_grid *g) {
     return rc;
 }
 
+int current_flow(fm_grid *g, long long *flow);
+
 int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int32_t *capD,
                  const int32_t *capU, const int32_t *capS, const int32_t *capT, int32_t flags) {
     g->flags_solve = flags;
@@ -2368,10 +2423,25 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     // HybridState.excess_total = sum of excess after init_preflow = sum capS
     // (maxflow_par.py:56); pre-cancelled units are already at t.
     g->excess_total = g->sum_capS;
+    if (g->trace) {
+        long long f = 0;
+        FM_TRY(current_flow(g, &f));
+        fprintf(stderr, "[fm_grid] after pre-cancellation: %lld of %lld source units at the sink\n", f, g->sum_capS);
+    }
     if (g->two_hop && !(flags & FM_GRID_NO_PRECANCEL)) {
         two_hop_kernel<<<(unsigned)((g->HW + 255) / 256), 256, 0, g->stream>>>(g->d);
         FM_CHECK_LAUNCH();
         g->st.launches++;
+        if (g->two_hop >= 2) {
+            three_hop_kernel<<<(unsigned)((g->HW + 255) / 256), 256, 0, g->stream>>>(g->d);
+            FM_CHECK_LAUNCH();
+            g->st.launches++;
+        }
+        if (g->trace) {
+            long long f = 0;
+            FM_TRY(current_flow(g, &f));
+            fprintf(stderr, "[fm_grid] after two-hop pre-routing: %lld of %lld source units at the sink\n", f, g->sum_capS);
+        }
     }
     return global_relabel(g);
 }

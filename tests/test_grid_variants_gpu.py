@@ -34,6 +34,7 @@ VARIANTS = {
     "no_local_relabel": {"FM_LOCAL_DIV": "0"},
     "br_rerun": {"FM_BR_RERUN": "1", "FM_BR_CAP": "2"},
     "no_two_hop": {"FM_TWO_HOP": "0"},
+    "three_hop": {"FM_TWO_HOP": "2"},
 }
 
 CASES = [("G", 96, 160, 11), ("G", 257, 130, 12), ("S", 200, 256, 2048), ("G", 31, 33, 13)]
