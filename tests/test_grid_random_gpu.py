@@ -1,0 +1,64 @@
+"""Randomised grid parity beyond the fixed cases: random shapes (odd, non-multiple-of-32,
+tall/wide strips), capacity ranges from {0,1} to wide int32 values, sparse sink /
+source arcs.  Small instances are compared bit-exactly with the pinned CPU oracle
+(flow value and minimal cut); larger ones are certified (valid preflow, cut = seeded
+residual reach, cut capacity == flow)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1110_6231_b200 as fmb
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_caps(rng, H, W, hi, p_src, p_snk):
+    caps = [rng.integers(0, hi + 1, size=(H, W)).astype(np.int32) for _ in range(4)]
+    capS = (rng.integers(0, hi + 1, size=(H, W)) * (rng.random((H, W)) < p_src)).astype(np.int32)
+    capT = (rng.integers(0, hi + 1, size=(H, W)) * (rng.random((H, W)) < p_snk)).astype(np.int32)
+    caps[0][:, -1] = 0
+    caps[1][:, 0] = 0
+    caps[2][-1, :] = 0
+    caps[3][0, :] = 0
+    return caps + [capS, capT]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_shapes_vs_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    H, W = int(rng.integers(1, 200)), int(rng.integers(1, 200))
+    hi = int(rng.choice([1, 7, 100, 100000]))
+    caps = _random_caps(rng, H, W, hi, float(rng.uniform(0.05, 1.0)), float(rng.uniform(0.05, 1.0)))
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
+    assert rep.objective == want["value"], (seed, H, W, hi)
+    assert (rep.cut == want["cut"]).all(), (seed, H, W, hi)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_medium_certified(seed):
+    rng = np.random.default_rng(2000 + seed)
+    H, W = int(rng.integers(300, 1100)), int(rng.integers(300, 1100))
+    hi = int(rng.choice([3, 100, 1000000]))
+    caps = _random_caps(rng, H, W, hi, float(rng.uniform(0.1, 1.0)), float(rng.uniform(0.1, 1.0)))
+    solver = fmb.GridSolver(H, W)
+    try:
+        flow, cut, _ = solver.solve_host(caps)
+        state = solver.export()
+    finally:
+        solver.close()
+    code, fl, cc, _ = oracle.grid_certify(caps, state, cut)
+    assert code == 0, (seed, H, W, hi, code)
+    assert fl == cc == flow
+
+
+@pytest.mark.parametrize("shape", [(1, 4097), (4097, 1), (2, 3000), (3000, 3), (33, 1025)])
+def test_strips_vs_oracle(shape):
+    rng = np.random.default_rng(shape[0] * 7919 + shape[1])
+    caps = _random_caps(rng, shape[0], shape[1], 50, 0.5, 0.5)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
+    assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
