@@ -642,6 +642,11 @@ __device__ __forceinline__ long long floordiv_eps(long long rc, long long eps, d
 // Bellman-Ford: X step = one CTA per Y whose label dropped, relaxing every arc x->y
 // along row y of the transposed weights (coalesced) with atomicMin on l(x); Y step
 // = one thread per X whose label dropped, relaxing its matched reverse arc.
+constexpr int PU_GROUPS = 4;   // price update: up to this many frontier Y per CTA in flight
+__device__ __forceinline__ void group_sync(int grp, int nthreads) {   // named barrier of one thread group
+    asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(nthreads) : "memory");
+}
+
 struct PuDev {
     const int32_t *wt;      // transposed weights: wt[y*n + x] = w(x, y)
     int32_t *fy[2], *fx[2]; // frontiers
@@ -662,8 +667,8 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     // final min(label, last + 1) needs.
     long long cap = min((long long)a.max_bucket, (long long)(a.pu_cap0 > 0 ? a.pu_cap0 : 8));
     int it_total = 0;
-    __shared__ int s_ly, s_y;
-    __shared__ long long s_py;
+    __shared__ int s_ly[PU_GROUPS], s_y[PU_GROUPS];
+    __shared__ long long s_py[PU_GROUPS];
     for (;;) {
     if (tid == 0) { a.cnt[C_PU_LAST] = 0; a.cnt[C_PU_CHG] = 0; }
     for (int v = tid; v < n; v += nthr) {
@@ -691,38 +696,46 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
         if (ny == 0) break;
         if (tid == 0) atomicAdd(a.ops + O_PU_YS, (unsigned long long)ny);
         if (tid == 0) f.cnt[(it + 2) % 3] = 0;
-        // thread 0 fetches each frontier Y's header (clear its queued flag, then read
-        // l(y), p(y)) one Y ahead, so the next header's round trips overlap this scan
+        // Each CTA works on PU_GROUPS frontier Y at once (one group of GT threads per Y,
+        // group barriers): a column scan is a latency chain, so several in flight per
+        // SM beat one CTA-wide scan after another.  The group leader fetches each Y's
+        // header (clear its queued flag, then read l(y), p(y)) one Y ahead, so the next
+        // header's round trips overlap this scan.
+        // groups only pay when the frontier outnumbers the CTAs (a group's scan is
+        // PU_GROUPS times longer than a CTA-wide one)
+        const int ng = ny > (int)gridDim.x ? PU_GROUPS : 1, PU_GT = ATHREADS / ng;
+        const int grp = threadIdx.x / PU_GT, gt = threadIdx.x - grp * PU_GT;
+        const int istep = gridDim.x * ng;
         int nxt_y = -1, nxt_l = 0;
         long long nxt_p = 0;
-        if (threadIdx.x == 0 && blockIdx.x < ny) {
-            nxt_y = __ldcg(f.fy[b] + blockIdx.x);
+        if (gt == 0 && blockIdx.x * ng + grp < ny) {
+            nxt_y = __ldcg(f.fy[b] + blockIdx.x * ng + grp);
             f.in_fy[nxt_y] = 0;          // clear before reading l(y): a later drop re-queues y
             __threadfence();
             nxt_l = __ldcg(a.ly + nxt_y);
             nxt_p = __ldcg((const long long *)a.py + nxt_y);
         }
-        for (int i = blockIdx.x; i < ny; i += gridDim.x) {
-            if (threadIdx.x == 0) {
-                s_y = nxt_y; s_ly = nxt_l; s_py = nxt_p;
-                if (i + (int)gridDim.x < ny) {
-                    nxt_y = __ldcg(f.fy[b] + i + gridDim.x);
+        for (int i = blockIdx.x * ng + grp; i < ny; i += istep) {
+            if (gt == 0) {
+                s_y[grp] = nxt_y; s_ly[grp] = nxt_l; s_py[grp] = nxt_p;
+                if (i + istep < ny) {
+                    nxt_y = __ldcg(f.fy[b] + i + istep);
                     f.in_fy[nxt_y] = 0;
                     __threadfence();
                     nxt_l = __ldcg(a.ly + nxt_y);
                     nxt_p = __ldcg((const long long *)a.py + nxt_y);
                 }
             }
-            __syncthreads();
-            const int y = s_y;
-            const int lyv = s_ly;
-            const long long pyv = s_py;
+            group_sync(grp, PU_GT);
+            const int y = s_y[grp];
+            const int lyv = s_ly[grp];
+            const long long pyv = s_py[grp];
             const int32_t *col = f.wt + (size_t)y * n;
             // vector path: 8 consecutive x per thread, every operand loaded up front
             // (int4 weights / labels / matches, longlong2 prices) so a thread's scan is
             // one L2 round trip instead of a chain of dependent ones
             const int nv8 = (n & 7) ? 0 : n;
-            for (int x0 = threadIdx.x * 8; x0 < nv8; x0 += ATHREADS * 8) {
+            for (int x0 = gt * 8; x0 < nv8; x0 += PU_GT * 8) {
                 const int4 w0 = __ldg((const int4 *)(col + x0)), w1 = __ldg((const int4 *)(col + x0 + 4));
                 const int4 l0 = __ldcg((const int4 *)(a.lx + x0)), l1 = __ldcg((const int4 *)(a.lx + x0 + 4));
                 const int4 m0 = __ldcg((const int4 *)(a.match + x0)), m1 = __ldcg((const int4 *)(a.match + x0 + 4));
@@ -774,7 +787,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
                         f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;   // read after the grid barrier
                 }
             }
-            for (int x = nv8 + threadIdx.x; x < n; x += ATHREADS) {
+            for (int x = nv8 + gt; x < n; x += PU_GT) {
                 const int wv = __ldg(col + x);
                 if (wv == FM_ABSENT_WEIGHT) continue;
                 const int lxv = __ldcg(a.lx + x);
@@ -801,7 +814,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
                 if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0)
                     f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;
             }
-            __syncthreads();
+            group_sync(grp, PU_GT);
         }
         grid.sync();
     }
