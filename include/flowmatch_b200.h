@@ -159,6 +159,11 @@ int fm_grid_stats(fm_grid *g, fm_stats *stats);
 /* global_nodes = H*W + 2 of the WHOLE grid: heights, the source height |V| and the
  * BFS sentinel must agree across bands. */
 int fm_grid_band_config(fm_grid *g, int32_t ghost_top, int32_t ghost_bottom, int64_t global_nodes);
+/* Run the band's steps on `stream` (a cudaStream_t, e.g. the caller's NCCL-ordered torch
+ * stream; NULL = the library's own stream).  With a caller stream, the row export
+ * (fm_grid_band_rows direction 0) is only enqueued: anything the caller orders after it on
+ * that stream (an NCCL send) sees the exported row without a host synchronisation. */
+int fm_grid_band_stream(fm_grid *g, void *stream);
 int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t *capL,
                       const int32_t *capD, const int32_t *capU, const int32_t *capS,
                       const int32_t *capT, int32_t flags, int64_t *sum_caps_out);

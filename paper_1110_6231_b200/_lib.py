@@ -84,6 +84,7 @@ SIGNATURES = {
     "fm_grid_cut_plane": (ctypes.c_int, [_vp, _vp, _i32]),
     "fm_grid_stats": (ctypes.c_int, [_vp, _vp]),
     "fm_grid_band_config": (ctypes.c_int, [_vp, _i32, _i32, _i64]),
+    "fm_grid_band_stream": (ctypes.c_int, [_vp, _vp]),
     "fm_grid_band_init": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32, _vp]),
     "fm_grid_band_bfs": (ctypes.c_int, [_vp, _i32, _vp]),
     "fm_grid_band_finalize": (ctypes.c_int, [_vp, _vp]),

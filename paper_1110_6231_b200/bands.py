@@ -106,6 +106,10 @@ class Band:
                    "fm_grid_band_config")
         self.device = device
         dev = torch.device("cuda", device)
+        # band steps on torch's current stream: row exports are then ordered before the
+        # NCCL sends that read them without a host synchronisation
+        _lib.check(L.fm_grid_band_stream(h, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)),
+                   "fm_grid_band_stream")
         self.caps = [torch.from_numpy(np.ascontiguousarray(c)).to(dev) for c in caps_band]
         # row buffers sized for the widest message (ROW_PUSH_STATE: 3 rows)
         self.buf = {s: torch.empty(3 * self.W, dtype=torch.int32, device=dev) for s in (TOP, BOTTOM)}
@@ -262,8 +266,8 @@ class DistTransport:
             ops.append(dist.P2POp(dist.irecv, rb, peer))
         if ops:
             for r in dist.batch_isend_irecv(ops):
-                r.wait()
-        if torch.cuda.is_available():
+                r.wait()   # NCCL: the current stream (the bands' stream) waits for the transfers
+        if getattr(self, "host_staging", False) and torch.cuda.is_available():
             torch.cuda.current_stream().synchronize()
         changed = 0
         for side in b.sides():

@@ -2134,6 +2134,7 @@ struct fm_grid {
     int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (env FM_VISIT_MULT)
     bool ring_stats_pending = false;
     bool pr_stats_pending = false;
+    bool band_user_stream = false;       // band steps run on a caller stream (fm_grid_band_stream)
     int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (env FM_PR_KERNEL)
     int pl_per_sm = 6;                   // resident pr_list CTAs per SM (occupancy query)
     int k_local_list = 0;                // passes per visit of the list kernel (env FM_K_LOCAL_LIST)
@@ -2999,6 +3000,14 @@ extern "C" int fm_grid_cut_host(fm_grid *g, uint8_t *cut_out, fm_stats *stats) {
 // ============================================================================
 // row-band steps (multi-GPU grid path; orchestrated by paper_1110_6231_b200.bands)
 // ============================================================================
+extern "C" int fm_grid_band_stream(fm_grid *g, void *stream) {
+    if (!g) { fm_set_error("fm_grid_band_stream: null handle"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    set_stream(g, stream);
+    g->band_user_stream = stream != nullptr;
+    return FM_OK;
+}
+
 extern "C" int fm_grid_band_config(fm_grid *g, int32_t ghost_top, int32_t ghost_bottom,
                                    int64_t global_nodes) {
     if (!g || g->H < 1 + (ghost_top ? 1 : 0) + (ghost_bottom ? 1 : 0) || global_nodes < g->HW + 2 ||
@@ -3130,7 +3139,7 @@ extern "C" int fm_grid_band_rows(fm_grid *g, int32_t direction, int32_t side, in
         for (int k = k0; k <= k1; k++)
             band_rows_out_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, k, buf + (size_t)(k - k0) * g->W);
         FM_CHECK_LAUNCH();
-        FM_TRY(sync_stream(g));
+        if (!g->band_user_stream) FM_TRY(sync_stream(g));   // else ordered on the caller's stream
         if (changed) *changed = 0;
     } else {
         FM_CHECK_CUDA(cudaMemsetAsync(g->d_band, 0, sizeof(int32_t), g->stream));
