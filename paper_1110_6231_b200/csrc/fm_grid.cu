@@ -619,20 +619,22 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
     const int32_t d = min(e, best_r);
     int qr = lr, qc = lc;
     if (dir == 0) qc++; else if (dir == 1) qc--; else if (dir == 2) qr++; else qr--;
+    // both returning atomics in flight before either result is used (passes are
+    // barrier-separated, so the order of the owner's and the receiver's updates is free)
+    const int32_t oldp = atomicSub(&T.e[li], d);           // the owner's view of e(p)
     atomicSub(&T.r[dir][li], d);
-    int32_t old = 1;
+    pushes++;
     if (qr >= 0 && qr < PT_H && qc >= 0 && qc < PT_W) {
         const int qi = qr * PT_W + qc;
         atomicAdd(&T.r[dir ^ 1][qi], d);
-        old = atomicAdd(&T.e[qi], d);
+        const int32_t old = atomicAdd(&T.e[qi], d);
         if (old <= 0 && old + d > 0) *recv = qi;
     } else {
         const int64_t q = (int64_t)(T.r0 + qr) * g.W + (T.c0 + qc);
         atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + q, d);
         atomicOr(T.nbr, 1 << dir);
     }
-    pushes++;
-    return atomicSub(&T.e[li], d) - d > 0;                 // the owner's view of e(p); hp < V here
+    return oldp - d > 0;                                   // hp < V here
 }
 
 // two candidates per lane (the pixel itself, the receiver it activated), one list reservation
