@@ -1198,17 +1198,17 @@ __device__ __forceinline__ uint32_t bits_row(const GridDev &g, int tile, int lr,
 }
 
 // listed == 0: every tile; listed == 1: the tiles of bq.list[0] (local relabel region).
-// seed (with listed == 0): queue the tiles holding a sink arc in bq[0] -- the only
-// tiles whose first BFS visit can find anything; the rest are queued by neighbours.
-__global__ void bfs_init_bits_kernel(GridDev g, int listed, int seed) {
+// (Seeding the ring with only the tiles that hold a sink arc is NOT enough: a tile
+// without one next to a sink pixel on its neighbour's border is never notified -- that
+// border value is 1 from the start and never "changes" -- so every tile is queued.)
+__global__ void bfs_init_bits_kernel(GridDev g, int listed) {
     const int lane = threadIdx.x & 31;
     const int64_t nrows = listed ? (int64_t)__ldcg(g.bq.cnt + 0) * PT_H : (int64_t)g.ntx * g.nty * PT_H;
     for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int k = (int)(w / PT_H), lr = (int)(w % PT_H);
         const int tile = listed ? g.bq.list[0][k] : k;
-        const uint32_t t_bits = bits_row(g, tile, lr, lane);
-        if (seed && t_bits && lane == 0 && !__ldcg(g.bq.flag[0] + tile)) tq_push(g.bq, 0, tile);
+        bits_row(g, tile, lr, lane);
     }
 }
 
@@ -2257,9 +2257,7 @@ int bfs_init(fm_grid *g, bool listed, int nlisted = 0) {
     if (g->bfs_bits) {
         const int rows = (listed ? nlisted : g->ntiles) * PT_H;
         const int blocks = std::max(1, std::min((rows + 7) / 8, g->sms * 16));
-        const int seed = !listed && g->bfs_bits == 2;
-        if (seed) FM_TRY(tq_reset(g, g->d.bq));
-        bfs_init_bits_kernel<<<blocks, 256, 0, g->stream>>>(g->d, listed ? 1 : 0, seed);
+        bfs_init_bits_kernel<<<blocks, 256, 0, g->stream>>>(g->d, listed ? 1 : 0);
     } else if (listed) {
         bfs_init_local_kernel<<<std::max(1, std::min(nlisted, g->sms * 8)), 256, 0, g->stream>>>(g->d);
     } else {
@@ -2276,9 +2274,9 @@ int bfs_init(fm_grid *g, bool listed, int nlisted = 0) {
 // collected by bfs_collect() after the caller's next stream sync.
 int bfs_sweeps(fm_grid *g, bool first_all) {
     if (g->bfs_bits == 2) {
-        // first_all: the tiles bfs_init queued (those with a sink arc) -- see bfs_init_bits_kernel
-        const int32_t *list0 = first_all ? g->d.bq.list[0] : g->d.bq.list[g->bq_parity];
-        const int32_t *cnt0 = first_all ? g->d.bq.cnt + 0 : g->d.bq.cnt + 2 * g->bq_parity;
+        // first_all: every tile (see bfs_init_bits_kernel); else the tiles queued in bq
+        const int32_t *list0 = first_all ? nullptr : g->d.bq.list[g->bq_parity];
+        const int32_t *cnt0 = first_all ? nullptr : g->d.bq.cnt + 2 * g->bq_parity;
         ringq_init_kernel<<<std::min((g->rq.cap + 255) / 256, g->sms * 8), 256, 0, g->stream>>>(g->rq, g->ntiles, list0, cnt0);
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[2], g->stream);

@@ -62,3 +62,44 @@ def test_strips_vs_oracle(shape):
     want = oracle.grid_maxflow(*caps, solver="seq")
     rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
     assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
+
+
+def _stress_case(seed, k):
+    """Case k of scripts/stress_grid.py's generator (same draw order)."""
+    rng = np.random.default_rng(seed)
+    for _ in range(k + 1):
+        H, W = int(rng.integers(1, 400)), int(rng.integers(1, 400))
+        hi = int(rng.choice([1, 2, 5, 30, 100, 5000]))
+        caps = [rng.integers(0, hi + 1, size=(H, W)).astype(np.int32) for _ in range(4)]
+        ps, pt = rng.uniform(0.02, 1.0, 2)
+        capS = (rng.integers(0, hi + 1, size=(H, W)) * (rng.random((H, W)) < ps)).astype(np.int32)
+        capT = (rng.integers(0, hi + 1, size=(H, W)) * (rng.random((H, W)) < pt)).astype(np.int32)
+        caps[0][:, -1] = 0
+        caps[1][:, 0] = 0
+        caps[2][-1, :] = 0
+        caps[3][0, :] = 0
+        caps = caps + [capS, capT]
+    return caps
+
+
+def test_regression_sparse_sink_borders():
+    """scripts/stress_grid.py seed 7 case 270 (392 x 353, unit capacities, sparse sink
+    arcs): a BFS that queued only the tiles holding a sink arc never revisited a tile
+    whose only link to the sink is a sink pixel on its neighbour's border (that value is
+    1 from the start, so no change is ever signalled) -- flow 31076 instead of 31077."""
+    caps = _stress_case(7, 270)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    assert want["value"] == 31077
+    for _ in range(3):
+        rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
+        assert rep.objective == 31077 and (rep.cut == want["cut"]).all()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_sparse_sink_grids(seed):
+    rng = np.random.default_rng(3000 + seed)
+    H, W = int(rng.integers(200, 420)), int(rng.integers(200, 420))
+    caps = _random_caps(rng, H, W, int(rng.choice([1, 3])), 0.5, float(rng.choice([0.005, 0.02, 0.05])))
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
+    assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
