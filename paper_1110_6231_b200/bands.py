@@ -365,7 +365,12 @@ class BandedSolve:
                     break
             active = self.global_relabel()
             self.stats["rounds"] += 1
-        # minimal source-side cut: seeded reach, then boundary exchange to a fixpoint
+        # minimal source-side cut: seeded reach, then boundary exchange to a fixpoint.
+        # The ghost rows' residuals toward us must be current first: the RES rows of the
+        # last push exchange were exported before that exchange's flow was folded in, so a
+        # ghost arc opened by it would be missing from the reach (stress-found: cut short of
+        # the minimal one next to band borders, flow correct)
+        self.tr.exchange(ROW_RES)
         for b in bands:
             b.cut(0)
         while True:

@@ -108,3 +108,41 @@ def test_bands_blocked_generator_rows():
     assert co.run() == want["value"]
     for b in bands:
         b.close()
+
+
+def _stress_band_case(seed, k):
+    """Case k of scripts/stress_bands.py's generator (same draw order)."""
+    rng = np.random.default_rng(seed)
+    for _ in range(k + 1):
+        nb = int(rng.integers(2, 5))
+        H, W = int(rng.integers(66 * nb, 300)), int(rng.integers(1, 300))
+        hi = int(rng.choice([1, 3, 30, 100]))
+        caps = [rng.integers(0, hi + 1, size=(H, W)).astype(np.int32) for _ in range(4)]
+        ps, pt = rng.uniform(0.02, 1.0, 2)
+        capS = (rng.integers(0, hi + 1, size=(H, W)) * (rng.random((H, W)) < ps)).astype(np.int32)
+        capT = (rng.integers(0, hi + 1, size=(H, W)) * (rng.random((H, W)) < pt)).astype(np.int32)
+        caps[0][:, -1] = 0
+        caps[1][:, 0] = 0
+        caps[2][-1, :] = 0
+        caps[3][0, :] = 0
+        caps = caps + [capS, capT]
+    return caps, nb
+
+
+@pytest.mark.parametrize("k", [132, 149])
+def test_regression_band_cut_ghost_residuals(k):
+    """scripts/stress_bands.py seed 5: the cut came out short of the minimal one next to
+    band borders (flow correct) because the ghost rows' residuals toward the band were
+    those exported before the last push exchange folded its flow in."""
+    caps, nb = _stress_band_case(5, k)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    flow, cut, _ = B.solve_virtual_bands(caps, nb)
+    assert flow == want["value"] and (cut == want["cut"]).all()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_band_cases(seed):
+    caps, nb = _stress_band_case(100 + seed, 0)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    flow, cut, _ = B.solve_virtual_bands(caps, nb)
+    assert flow == want["value"] and (cut == want["cut"]).all()
