@@ -98,9 +98,9 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
                                  const int32_t *__restrict__ capU,
                                  const int32_t *__restrict__ capS,
                                  const int32_t *__restrict__ capT, int precancel,
-                                 unsigned long long *acc /* [0]=sum capS [1]=invalid */) {
+                                 unsigned long long *acc /* [0]=sum capS [1]=negative [2]=too large */) {
     const int64_t HW = (int64_t)g.H * g.W;
-    long long sum = 0, bad = 0;
+    long long sum = 0, bad = 0, big = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
@@ -110,6 +110,13 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
         int32_t cd = r + 1 < g.H ? capD[p] : 0;
         int32_t cu = r > 0 ? capU[p] : 0;
         bad += (cs < 0) | (ct < 0) | (cr < 0) | (cl < 0) | (cd < 0) | (cu < 0);
+        // int32 device state: the excess of p is at most capS + the capacities into p, and
+        // a merged pair's residual at most the pair's two capacities (the reference's
+        // Python ints have no such limit, so larger inputs are refused, not wrapped)
+        const long long inR = c > 0 ? max(capR[p - 1], 0) : 0, inL = c + 1 < g.W ? max(capL[p + 1], 0) : 0;
+        const long long inD = r > 0 ? max(capD[p - g.W], 0) : 0, inU = r + 1 < g.H ? max(capU[p + g.W], 0) : 0;
+        big += ((long long)max(cs, 0) + inR + inL + inD + inU > (long long)INT32_MAX) |
+               ((long long)max(cr, 0) + inL > (long long)INT32_MAX) | ((long long)max(cd, 0) + inU > (long long)INT32_MAX);
         cs = max(cs, 0); ct = max(ct, 0);
         const int32_t m = precancel ? min(cs, ct) : 0;
         g.e[p] = cs - m;
@@ -127,20 +134,22 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
         sum += cs;
     }
     // grid-stride kernel with 1-D blocks of 256
-    __shared__ long long red[2][8];
+    __shared__ long long red[3][8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sum += __shfl_xor_sync(0xffffffffu, sum, o);
         bad += __shfl_xor_sync(0xffffffffu, bad, o);
+        big += __shfl_xor_sync(0xffffffffu, big, o);
     }
-    if (lane == 0) { red[0][wid] = sum; red[1][wid] = bad; }
+    if (lane == 0) { red[0][wid] = sum; red[1][wid] = bad; red[2][wid] = big; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        long long s = 0, b = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); i++) { s += red[0][i]; b += red[1][i]; }
+        long long s = 0, b = 0, x = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) { s += red[0][i]; b += red[1][i]; x += red[2][i]; }
         if (s) atomicAdd(&acc[0], (unsigned long long)s);
         if (b) atomicAdd(&acc[1], (unsigned long long)b);
+        if (x) atomicAdd(&acc[2], (unsigned long long)x);
     }
 }
 
@@ -2413,11 +2422,16 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
     FM_CHECK_LAUNCH();
     g->st.launches++;
-    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 2,
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 3,
                                   cudaMemcpyDeviceToHost, g->stream));
     FM_TRY(sync_stream(g));
     if (g->h_acc[1] != 0) {
         fm_set_error("negative capacity in grid input (%llu entries)", g->h_acc[1]);
+        return FM_INVALID_ARG;
+    }
+    if (g->h_acc[2] != 0) {
+        fm_set_error("grid capacities too large for the int32 device state: %llu pixels where capS plus the "
+                     "capacities into the pixel, or a neighbour pair's two capacities, exceed 2^31-1", g->h_acc[2]);
         return FM_INVALID_ARG;
     }
     g->sum_capS = (long long)g->h_acc[0];
@@ -3036,10 +3050,11 @@ extern "C" int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t 
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
     FM_CHECK_LAUNCH();
     g->st.launches++;
-    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 2,
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 3,
                                   cudaMemcpyDeviceToHost, g->stream));
     FM_TRY(sync_stream(g));
     if (g->h_acc[1] != 0) { fm_set_error("negative capacity in grid input"); return FM_INVALID_ARG; }
+    if (g->h_acc[2] != 0) { fm_set_error("grid capacities too large for the int32 device state"); return FM_INVALID_ARG; }
     g->sum_capS = (long long)g->h_acc[0];
     g->excess_total = g->sum_capS;
     FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));

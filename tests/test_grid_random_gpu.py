@@ -103,3 +103,27 @@ def test_sparse_sink_grids(seed):
     want = oracle.grid_maxflow(*caps, solver="seq")
     rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
     assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
+
+
+def test_int32_capacity_limits():
+    """The device state is int32: capacities whose sums could overflow it (excess of a
+    pixel = capS + the capacities into it; a merged pair's residual = its two
+    capacities) are refused with ValueError instead of being wrapped silently; below the
+    limit the answer is exact."""
+    rng = np.random.default_rng(5)
+    H, W = 60, 70
+
+    def caps_upto(hi):
+        caps = [rng.integers(0, hi, size=(H, W), dtype=np.int64).astype(np.int32) for _ in range(6)]
+        caps[0][:, -1] = 0
+        caps[1][:, 0] = 0
+        caps[2][-1, :] = 0
+        caps[3][0, :] = 0
+        return caps
+
+    ok = caps_upto(2**28)
+    want = oracle.grid_maxflow(*ok, solver="seq")
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*ok))
+    assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
+    with pytest.raises(ValueError):
+        fmb.hybrid_solve(fmb.build_grid_network(*caps_upto(2**31 - 1)))
