@@ -957,11 +957,28 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
     return any;
 }
 
+// ----------------------------------------------------------------------------
+// One push round as a CUDA graph: a while-conditional node whose body is a single
+// pr_list_kernel launch.  The launch's last CTA to finish evaluates the round's
+// triggers -- idle launch, launch cap, relabel budget at batch boundaries (the host
+// loop's checks, in the same order) -- arms the tile queue for the next launch and
+// sets the loop condition, so a round runs without a host round trip per batch.
+// ----------------------------------------------------------------------------
+struct PrCtl {
+    int32_t parity, done, cap, batch, stop, processed, finished, pad;
+    long long budget;
+    unsigned long long tiles;
+};
+
 __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev g, int k_local, int steps, int fused,
-                                                                       int parity, int32_t *processed,
-                                                                       unsigned long long *ops) {
+                                                                       int parity_arg, int32_t *processed,
+                                                                       unsigned long long *ops,
+                                                                       PrCtl *ctl, cudaGraphConditionalHandle loop) {
     __shared__ PlSmem S;
     const int tid = threadIdx.y * PT_W + threadIdx.x;
+    // graph launches read the launch parity from the round's control block (processed
+    // then points into it); host launches pass it as an argument
+    const int parity = ctl ? __ldcg(&ctl->parity) : parity_arg;
     PlCounters C;
     for (;;) {
         __syncthreads();
@@ -993,6 +1010,27 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev
         atomicAdd(ops + 11, (unsigned long long)C.t_solo); atomicAdd(ops + 12, (unsigned long long)C.dense_passes);
         atomicAdd(ops + 13, (unsigned long long)C.solo_passes);
 #endif
+    }
+    if (ctl && tid == 0) {
+        __threadfence();
+        if (atomicAdd(&ctl->finished, 1) == (int)gridDim.x - 1) {   // last CTA: round control
+            __threadfence();
+            const int nproc = __ldcg(&ctl->processed);
+            const int done = ctl->done + 1;
+            const bool stop = nproc == 0 || done >= ctl->cap ||
+                              (done % ctl->batch == 0 && (long long)__ldcg(ops + 1) >= ctl->budget);
+            const int pn = parity ^ 1;
+            g.pq.cnt[pn ? 0 : 2] = 0;              // tq_arm for the next launch
+            g.pq.cnt[(pn ? 0 : 2) + 1] = 0;
+            ctl->done = done;
+            ctl->tiles += nproc;
+            ctl->parity = pn;
+            ctl->stop = stop;
+            if (!stop) ctl->processed = 0;         // kept when stopping: 0 marks an idle launch
+            ctl->finished = 0;
+            __threadfence();
+            cudaGraphSetConditional(loop, stop ? 0u : 1u);
+        }
     }
 }
 
@@ -2145,6 +2183,12 @@ struct fm_grid {
     int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (env FM_VISIT_MULT)
     bool ring_stats_pending = false;
     bool pr_stats_pending = false;
+    int pr_graph = 0;                    // 1: the push round's launch loop runs as a device while-graph (env FM_PR_GRAPH; measured neutral)
+    cudaGraph_t prg = nullptr;           // that graph, its instance and the launch parameters it was built for
+    cudaGraphExec_t prg_exec = nullptr;
+    GridDev prg_d{};
+    int prg_key[4] = {0, 0, 0, 0};
+    bool prg_pending = false;            // round control block read back, consumed after the caller's sync
     bool band_user_stream = false;       // band steps run on a caller stream (fm_grid_band_stream)
     int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (env FM_PR_KERNEL)
     int pl_per_sm = 6;                   // resident pr_list CTAs per SM (occupancy query)
@@ -2501,6 +2545,64 @@ int run_round_global(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int
     return FM_OK;
 }
 
+// The round control block lives in flags[32..41]; its host mirror in h_flags[32..41].
+PrCtl *pr_ctl_dev(fm_grid *g) { return reinterpret_cast<PrCtl *>(g->flags + 32); }
+PrCtl *pr_ctl_host(fm_grid *g) { return reinterpret_cast<PrCtl *>(g->h_flags + 32); }
+
+// (Re)build the push-round while-graph for these launch parameters (body: one
+// pr_list_kernel node whose last CTA sets the loop condition).  Rebuilt only when a
+// parameter baked into the node changes.
+int pr_graph_build(fm_grid *g, int k_local, int blocks) {
+    const int key[4] = {k_local, blocks, g->op_steps, g->op_fused};
+    if (g->prg_exec && !memcmp(key, g->prg_key, sizeof(key)) && !memcmp(&g->d, &g->prg_d, sizeof(GridDev)))
+        return FM_OK;
+    if (g->prg_exec) { cudaGraphExecDestroy(g->prg_exec); g->prg_exec = nullptr; }
+    if (g->prg) { cudaGraphDestroy(g->prg); g->prg = nullptr; }
+    FM_CHECK_CUDA(cudaGraphCreate(&g->prg, 0));
+    cudaGraphConditionalHandle handle;
+    FM_CHECK_CUDA(cudaGraphConditionalHandleCreate(&handle, g->prg, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t loop;
+    FM_CHECK_CUDA(cudaGraphAddNode(&loop, g->prg, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+
+    PrCtl *ctl = pr_ctl_dev(g);
+    GridDev d = g->d;
+    int steps = g->op_steps, fused = g->op_fused, parity0 = 0;
+    int32_t *processed = &ctl->processed;
+    unsigned long long *ops = g->acc + 10;
+    void *pr_args[] = {&d, &k_local, &steps, &fused, &parity0, &processed, &ops, &ctl, &handle};
+    cudaKernelNodeParams kp{};
+    kp.func = (void *)pr_list_kernel;
+    kp.gridDim = dim3(blocks);
+    kp.blockDim = dim3(PT_W, PL_TY);
+    kp.kernelParams = pr_args;
+    cudaGraphNode_t n;
+    FM_CHECK_CUDA(cudaGraphAddKernelNode(&n, body, nullptr, 0, &kp));
+    FM_CHECK_CUDA(cudaGraphInstantiate(&g->prg_exec, g->prg, 0));
+    memcpy(g->prg_key, key, sizeof(key));
+    g->prg_d = g->d;
+    return FM_OK;
+}
+
+// Fold the control block of the last graph round into the stats (after a stream sync).
+void pr_graph_consume(fm_grid *g, int32_t *idle_out) {
+    if (!g->prg_pending) return;
+    g->prg_pending = false;
+    const PrCtl *c = pr_ctl_host(g);
+    g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
+    g->st.launches += c->done;
+    g->st.pr_launches += c->done;
+    g->st.pr_sweeps += c->done;
+    g->st.pr_tiles += (int64_t)c->tiles;
+    g->pq_parity = c->parity;
+    if (idle_out) *idle_out = c->processed == 0 ? 1 : 0;
+}
+
 int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int32_t *idle_out = nullptr) {
     const int k_default = g->pr_kernel == 1 ? (g->k_local_list > 0 ? g->k_local_list : K_LOCAL_LIST_DEFAULT)
                                             : (g->k_local > 0 ? g->k_local : K_LOCAL_DEFAULT);
@@ -2513,6 +2615,26 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
     const long long relabel_budget =
         std::max<long long>(1024, g->HW / (g->relabel_div > 0 ? g->relabel_div : RELABEL_DIV_DEFAULT));
     const int blocks = std::min(g->ntiles, g->sms * (g->pr_kernel == 1 ? g->pl_per_sm : g->pt_per_sm));
+    if (g->pr_graph && g->pr_kernel == 1) {
+        FM_TRY(pr_graph_build(g, k_local, blocks));
+        PrCtl *h = pr_ctl_host(g);
+        *h = PrCtl{};
+        h->parity = g->pq_parity;
+        h->cap = cap;
+        h->batch = std::max(1, g->pr_batch);
+        h->budget = relabel_budget;
+        FM_CHECK_CUDA(cudaMemcpyAsync(pr_ctl_dev(g), h, sizeof(PrCtl), cudaMemcpyHostToDevice, g->stream));
+        FM_TRY(tq_arm(g, g->d.pq, g->pq_parity));
+        cudaEventRecord(g->ev[2], g->stream);
+        FM_CHECK_CUDA(cudaGraphLaunch(g->prg_exec, g->stream));
+        cudaEventRecord(g->ev[3], g->stream);
+        FM_CHECK_CUDA(cudaMemcpyAsync(h, pr_ctl_dev(g), sizeof(PrCtl), cudaMemcpyDeviceToHost, g->stream));
+        g->prg_pending = true;
+        integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
+        FM_CHECK_LAUNCH();
+        g->st.launches++;
+        return FM_OK;
+    }
     int32_t done = 0;
     while (done < cap) {
         const int batch = std::min(g->pr_batch, cap - done);
@@ -2522,7 +2644,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
             const int p = g->pq_parity;
             FM_TRY(tq_arm(g, g->d.pq, p));
             if (g->pr_kernel == 1)
-                pr_list_kernel<<<blocks, dim3(PT_W, PL_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10);
+                pr_list_kernel<<<blocks, dim3(PT_W, PL_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10, nullptr, 0);
             else
                 pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, g->vote_mask, p, g->flags + i, g->acc + 10);
             g->pq_parity ^= 1;
@@ -2605,6 +2727,7 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
                                   cudaMemcpyDeviceToHost, g->stream));
     cudaEventRecord(g->ev[1], g->stream);
     FM_TRY(sync_stream(g));
+    pr_graph_consume(g, nullptr);
     if (g->pr_stats_pending) {
         g->pr_stats_pending = false;
         g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
@@ -2750,6 +2873,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_BFS_BITS")) g->bfs_bits = atoi(v);
     if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
     if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
+    if (const char *v = getenv("FM_PR_GRAPH")) g->pr_graph = atoi(v);
     g->d.solo_max = 32;
     g->d.k_solo = 0;
     if (const char *v = getenv("FM_K_SOLO")) g->d.k_solo = atoi(v);
@@ -2871,6 +2995,8 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->h_acc) cudaFreeHost(g->h_acc);
     if (g->h_flags) cudaFreeHost(g->h_flags);
     if (g->h_cut_stage) cudaFreeHost(g->h_cut_stage);
+    if (g->prg_exec) cudaGraphExecDestroy(g->prg_exec);
+    if (g->prg) cudaGraphDestroy(g->prg);
     for (auto e : g->ev) if (e) cudaEventDestroy(e);
     if (g->own_stream) cudaStreamDestroy(g->own_stream);
     delete g;
@@ -3113,6 +3239,7 @@ extern "C" int fm_grid_band_push(fm_grid *g, int32_t max_launches, int32_t cycle
                                   cudaMemcpyDeviceToHost, g->stream));
     cudaEventRecord(g->ev[1], g->stream);
     FM_TRY(sync_stream(g));
+    pr_graph_consume(g, &idle);
     g->st.ms_push += elapsed(g);
     g->st.pushes += (int64_t)g->h_acc[10];
     g->st.relabels += (int64_t)g->h_acc[11];

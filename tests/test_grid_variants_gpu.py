@@ -35,6 +35,8 @@ VARIANTS = {
     "br_rerun": {"FM_BR_RERUN": "1", "FM_BR_CAP": "2"},
     "no_two_hop": {"FM_TWO_HOP": "0"},
     "three_hop": {"FM_TWO_HOP": "2"},
+    "pr_graph": {"FM_PR_GRAPH": "1"},
+    "pr_graph_b1": {"FM_PR_GRAPH": "1", "FM_PR_BATCH": "1"},
 }
 
 CASES = [("G", 96, 160, 11), ("G", 257, 130, 12), ("S", 200, 256, 2048), ("G", 31, 33, 13)]
