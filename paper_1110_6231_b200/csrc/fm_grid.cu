@@ -98,9 +98,9 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
                                  const int32_t *__restrict__ capU,
                                  const int32_t *__restrict__ capS,
                                  const int32_t *__restrict__ capT, int precancel,
-                                 unsigned long long *acc /* [0]=sum capS [1]=negative [2]=too large */) {
+                                 unsigned long long *acc /* [0]=sum capS [1]=negative [2]=too large [3]=pair > 65535 */) {
     const int64_t HW = (int64_t)g.H * g.W;
-    long long sum = 0, bad = 0, big = 0;
+    long long sum = 0, bad = 0, big = 0, wide = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
@@ -117,6 +117,8 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
         const long long inD = r > 0 ? max(capD[p - g.W], 0) : 0, inU = r + 1 < g.H ? max(capU[p + g.W], 0) : 0;
         big += ((long long)max(cs, 0) + inR + inL + inD + inU > (long long)INT32_MAX) |
                ((long long)max(cr, 0) + inL > (long long)INT32_MAX) | ((long long)max(cd, 0) + inU > (long long)INT32_MAX);
+        // pairs too wide for the packed 16-bit residual fields of the push kernel
+        wide += ((long long)max(cr, 0) + inL > 65535) | ((long long)max(cd, 0) + inU > 65535);
         cs = max(cs, 0); ct = max(ct, 0);
         const int32_t m = precancel ? min(cs, ct) : 0;
         g.e[p] = cs - m;
@@ -134,22 +136,24 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
         sum += cs;
     }
     // grid-stride kernel with 1-D blocks of 256
-    __shared__ long long red[3][8];
+    __shared__ long long red[4][8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         sum += __shfl_xor_sync(0xffffffffu, sum, o);
         bad += __shfl_xor_sync(0xffffffffu, bad, o);
         big += __shfl_xor_sync(0xffffffffu, big, o);
+        wide += __shfl_xor_sync(0xffffffffu, wide, o);
     }
-    if (lane == 0) { red[0][wid] = sum; red[1][wid] = bad; red[2][wid] = big; }
+    if (lane == 0) { red[0][wid] = sum; red[1][wid] = bad; red[2][wid] = big; red[3][wid] = wide; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        long long s = 0, b = 0, x = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); i++) { s += red[0][i]; b += red[1][i]; x += red[2][i]; }
+        long long s = 0, b = 0, x = 0, w = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) { s += red[0][i]; b += red[1][i]; x += red[2][i]; w += red[3][i]; }
         if (s) atomicAdd(&acc[0], (unsigned long long)s);
         if (b) atomicAdd(&acc[1], (unsigned long long)b);
         if (x) atomicAdd(&acc[2], (unsigned long long)x);
+        if (w) atomicAdd(&acc[3], (unsigned long long)w);
     }
 }
 
@@ -575,9 +579,14 @@ __device__ __forceinline__ void pl_append_warp(bool want, int idx, int *cnt, uin
     if (want) list[base + __popc(m & ((1u << lane) - 1))] = (uint16_t)idx;
 }
 
+__device__ __forceinline__ uint2 pk_pack(int32_t r, int32_t l, int32_t d, int32_t u) {
+    return make_uint2((uint32_t)r | ((uint32_t)l << 16), (uint32_t)d | ((uint32_t)u << 16));
+}
+
 struct PlTile {
     int32_t *e, *h, *t;        // shared planes (h with a 1-pixel halo, row stride PT_W + 2)
     int32_t (*r)[PT_H * PT_W];
+    uint2 *r2;                 // packed-residual kernel: {R | L << 16, D | U << 16} per pixel
     const uint8_t *f;
     int *nbr;                  // bit d: flow was parked in the inbox of neighbour tile d
     int r0, c0;
@@ -588,7 +597,7 @@ struct PlTile {
 // two pushes' atomics in flight together: the pass is a latency chain, so fewer
 // dependent round trips is what makes it faster.  Same results as pl_item.
 __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li, int *recv,
-                                       long long &pushes, long long &relabels) {
+                                       unsigned &pushes, unsigned &relabels) {
     constexpr int HS = PL_HS;
     volatile int32_t *ve = T.e;
     volatile int32_t *vh = T.h;
@@ -646,6 +655,69 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
     return oldp - d > 0;                                   // hp < V here
 }
 
+// pl_op1 over packed residuals: the four residuals of a pixel are 16-bit fields of two
+// 32-bit shared words, {R | L << 16, D | U << 16} (used when every neighbour pair's two
+// capacities sum to <= 65535: a field then never leaves [0, 65535], so a shifted 32-bit
+// atomic add is exact; a pair's two residuals share a word index), so the operation
+// reads them with one 64-bit load and shared memory per tile shrinks by 8 KB.
+__device__ __forceinline__ bool pk_op1(const GridDev &g, const PlTile &T, int li, int *recv,
+                                       unsigned &pushes, unsigned &relabels) {
+    constexpr int HS = PL_HS;
+    volatile int32_t *ve = T.e;
+    volatile int32_t *vh = T.h;
+    volatile int32_t *vt = T.t;
+    const int V = g.V;
+    const int lr = li >> 5, lc = li & 31;
+    const int hi = (lr + 1) * HS + lc + PL_HC;
+    const int r = T.r0 + lr, c = T.c0 + lc;
+    const uint8_t f = T.f[li];
+    const int32_t e = ve[li], hp = vh[hi], rt = vt[li];
+    const unsigned long long w64 = *(volatile unsigned long long *)&T.r2[li];
+    const uint2 w = make_uint2((uint32_t)w64, (uint32_t)(w64 >> 32));
+    const int32_t hR = vh[hi + 1], hL = vh[hi - 1], hD = vh[hi + HS], hU = vh[hi - HS];
+    if ((f & 2) || e <= 0 || hp >= V) return false;
+    if (rt > 0) {                                          // sink at height 0
+        if (hp == 0) { vh[hi] = 1; relabels++; }
+        const int32_t d = min(e, rt);
+        vt[li] = rt - d;
+        pushes++;
+        return atomicSub(&T.e[li], d) - d > 0;
+    }
+    const int32_t rr = (int32_t)(w.x & 0xffff), rl = (int32_t)(w.x >> 16);
+    const int32_t rd = (int32_t)(w.y & 0xffff), ru = (int32_t)(w.y >> 16);
+    int32_t best_h = INT32_MAX, best_r = 0;
+    int dir = -1;
+    if (rr > 0 && c + 1 < g.W && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
+    if (rl > 0 && c > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
+    if (rd > 0 && r + 1 < g.H && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
+    if (ru > 0 && r > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
+    if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
+    if (dir < 0) return false;
+    if (hp <= best_h) {
+        vh[hi] = best_h + 1;
+        relabels++;
+        return dir != 5;
+    }
+    const int32_t d = min(e, best_r);
+    int qr = lr, qc = lc;
+    if (dir == 0) qc++; else if (dir == 1) qc--; else if (dir == 2) qr++; else qr--;
+    const int32_t oldp = atomicSub(&T.e[li], d);
+    uint32_t *rw = reinterpret_cast<uint32_t *>(T.r2);
+    atomicAdd(&rw[2 * li + (dir >> 1)], 0u - ((uint32_t)d << (16 * (dir & 1))));
+    pushes++;
+    if (qr >= 0 && qr < PT_H && qc >= 0 && qc < PT_W) {
+        const int qi = qr * PT_W + qc;
+        atomicAdd(&rw[2 * qi + (dir >> 1)], (uint32_t)d << (16 * ((dir & 1) ^ 1)));
+        const int32_t old = atomicAdd(&T.e[qi], d);
+        if (old <= 0 && old + d > 0) *recv = qi;
+    } else {
+        const int64_t q = (int64_t)(T.r0 + qr) * g.W + (T.c0 + qc);
+        atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + q, d);
+        atomicOr(T.nbr, 1 << dir);
+    }
+    return oldp - d > 0;
+}
+
 // two candidates per lane (the pixel itself, the receiver it activated), one list reservation
 __device__ __forceinline__ void pl_append2_warp(bool wa, int ia, bool wb, int ib, int *cnt, uint16_t *list) {
     const unsigned ma = __ballot_sync(0xffffffffu, wa), mb = __ballot_sync(0xffffffffu, wb);
@@ -664,7 +736,7 @@ __device__ __forceinline__ void pl_append2_warp(bool wa, int ia, bool wb, int ib
 // activated (-1 if none); receivers of earlier pushes are listed directly.
 __device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int li, int steps, int fused,
                                         int *cnt_next, uint16_t *lout, int *recv,
-                                        long long &pushes, long long &relabels) {
+                                        unsigned &pushes, unsigned &relabels) {
     constexpr int HS = PL_HS;
     volatile int32_t *ve = T.e;
     volatile int32_t *vh = T.h;
@@ -731,10 +803,13 @@ __device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int l
     return e > 0 && hp < V;
 }
 
-struct PlSmem {
+template <bool PK> struct PlRes { int32_t r[4][PT_H * PT_W]; };              // R, L, D, U
+template <> struct PlRes<true> { uint2 r2[PT_H * PT_W]; };                  // packed 16-bit fields
+
+template <bool PK> struct PlSmemT {
     int32_t e[PT_H * PT_W];
     int32_t h[(PT_H + 2) * PL_HS];
-    int32_t r[4][PT_H * PT_W];   // R, L, D, U
+    PlRes<PK> res;
     int32_t t[PT_H * PT_W];
     uint8_t f[PT_H * PT_W];      // bit 0: residual arc to s, bit 1: ghost row
     uint16_t list[2][PT_H * PT_W];
@@ -744,9 +819,10 @@ struct PlSmem {
     int flag;
     long long red[PL_NT / 32];
 };
+using PlSmem = PlSmemT<false>;
 
 struct PlCounters {
-    long long pushes = 0, relabels = 0, passes = 0, items = 0;
+    unsigned pushes = 0, relabels = 0, passes = 0, items = 0;   // per thread per launch: 32 bits suffice
 #ifdef FM_PL_TIMING
     long long t_load = 0, t_pass = 0, t_store = 0, visits = 0, solo = 0, t_solo = 0, dense_passes = 0, solo_passes = 0;
 #endif
@@ -755,7 +831,8 @@ struct PlCounters {
 // One visit of `tile`: load (folding the inboxes), list-driven passes, write back.
 // Returns (CTA-uniform) whether the tile still holds an active pixel; S.nbr = the
 // neighbour tiles whose inboxes received flow.  Starts and ends with a barrier.
-__device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, int k_local, int steps,
+template <bool PK>
+__device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int tile, int k_local, int steps,
                                          int fused, PlCounters &C) {
     constexpr int HS = PL_HS;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * PT_W + tx;
@@ -765,7 +842,9 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
     long long t0 = clock64(), t1 = 0, t2 = 0;
 #endif
     const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
-    const PlTile T{S.e, S.h, S.t, S.r, S.f, &S.nbr, tyi * PT_H, txi * PT_W};
+    PlTile T;
+    if constexpr (PK) T = PlTile{S.e, S.h, S.t, nullptr, S.res.r2, S.f, &S.nbr, tyi * PT_H, txi * PT_W};
+    else T = PlTile{S.e, S.h, S.t, S.res.r, nullptr, S.f, &S.nbr, tyi * PT_H, txi * PT_W};
     const int r0 = T.r0, c0 = T.c0;
     int32_t *stage = (int32_t *)&S.list[0][0];   // rS staging (the lists are built afterwards)
     // load: asynchronous global -> shared copies, thread = (row, 4-column chunk)
@@ -776,10 +855,19 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
         if (r < g.H && cb + 4 <= g.W && (g.W & 3) == 0) {
             const int64_t p = (int64_t)r * g.W + cb;
             cp_async16(&S.e[li], g.e + p);
-            cp_async16(&S.r[0][li], g.rR + p);
-            cp_async16(&S.r[1][li], g.rL + p);
-            cp_async16(&S.r[2][li], g.rD + p);
-            cp_async16(&S.r[3][li], g.rU + p);
+            if constexpr (PK) {
+                const int4 a = __ldcg((const int4 *)(g.rR + p)), b = __ldcg((const int4 *)(g.rL + p));
+                const int4 d = __ldcg((const int4 *)(g.rD + p)), u = __ldcg((const int4 *)(g.rU + p));
+                S.res.r2[li + 0] = pk_pack(a.x, b.x, d.x, u.x);
+                S.res.r2[li + 1] = pk_pack(a.y, b.y, d.y, u.y);
+                S.res.r2[li + 2] = pk_pack(a.z, b.z, d.z, u.z);
+                S.res.r2[li + 3] = pk_pack(a.w, b.w, d.w, u.w);
+            } else {
+                cp_async16(&S.res.r[0][li], g.rR + p);
+                cp_async16(&S.res.r[1][li], g.rL + p);
+                cp_async16(&S.res.r[2][li], g.rD + p);
+                cp_async16(&S.res.r[3][li], g.rU + p);
+            }
             cp_async16(&S.t[li], g.rT + p);
             cp_async16(&S.h[hi], g.h + p);
             cp_async16(&stage[li], g.rS + p);
@@ -789,10 +877,14 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
                 const bool in = r < g.H && cb + j < g.W;
                 const int64_t p = in ? (int64_t)r * g.W + cb + j : 0;
                 cp_async4(&S.e[li + j], g.e + p, in);
-                cp_async4(&S.r[0][li + j], g.rR + p, in);
-                cp_async4(&S.r[1][li + j], g.rL + p, in);
-                cp_async4(&S.r[2][li + j], g.rD + p, in);
-                cp_async4(&S.r[3][li + j], g.rU + p, in);
+                if constexpr (PK) {
+                    S.res.r2[li + j] = in ? pk_pack(__ldcg(g.rR + p), __ldcg(g.rL + p), __ldcg(g.rD + p), __ldcg(g.rU + p)) : make_uint2(0u, 0u);
+                } else {
+                    cp_async4(&S.res.r[0][li + j], g.rR + p, in);
+                    cp_async4(&S.res.r[1][li + j], g.rL + p, in);
+                    cp_async4(&S.res.r[2][li + j], g.rD + p, in);
+                    cp_async4(&S.res.r[3][li + j], g.rU + p, in);
+                }
                 cp_async4(&S.t[li + j], g.rT + p, in);
                 cp_async4(&S.h[hi + j], g.h + p, in);
                 cp_async4(&stage[li + j], g.rS + p, in);
@@ -829,7 +921,8 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
     __syncthreads();
     if (inbox) {
         atomicAdd(&S.e[ib_li], inbox);          // a corner pixel has two inboxes
-        S.r[ib_dir][ib_li] += inbox;
+        if constexpr (PK) atomicAdd(reinterpret_cast<uint32_t *>(S.res.r2) + 2 * ib_li + (ib_dir >> 1), (uint32_t)inbox << (16 * (ib_dir & 1)));
+        else S.res.r[ib_dir][ib_li] += inbox;
     }
 #pragma unroll
     for (int k = 0; k < PL_ROWS; k++) {
@@ -868,8 +961,10 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
             const int i = base + tid;
             int recv = -1;
             const int li = i < n ? lin[i] : 0;
-            const bool keep = i < n && (simple ? pl_op1(g, T, li, &recv, C.pushes, C.relabels)
-                                               : pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels));
+            bool keep;
+            if constexpr (PK) keep = i < n && pk_op1(g, T, li, &recv, C.pushes, C.relabels);   // simple only
+            else keep = i < n && (simple ? pl_op1(g, T, li, &recv, C.pushes, C.relabels)
+                                         : pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels));
             pl_append2_warp(keep, li, recv >= 0, recv, cnt_next, lout);
         }
     }
@@ -895,7 +990,9 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
                 const int i = base + tid;
                 int recv = -1;
                 const int li = i < n ? lin[i] : 0;
-                const bool keep = i < n && pl_op1(g, T, li, &recv, C.pushes, C.relabels);
+                bool keep;
+                if constexpr (PK) keep = i < n && pk_op1(g, T, li, &recv, C.pushes, C.relabels);
+                else keep = i < n && pl_op1(g, T, li, &recv, C.pushes, C.relabels);
                 const unsigned ma = __ballot_sync(0xffffffffu, keep), mb = __ballot_sync(0xffffffffu, recv >= 0);
                 if (keep) lout[nn + __popc(ma & lt)] = (uint16_t)li;
                 if (recv >= 0) lout[nn + __popc(ma) + __popc(mb & lt)] = (uint16_t)recv;
@@ -904,7 +1001,7 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
             __syncwarp();
             n = nn;
         }
-    } else if (solo && tid < 32) {
+    } else if (!PK && solo && tid < 32) {
         for (; it < k_local; it++) {
             __syncwarp();
             const int n = S.cnt[it % 3];
@@ -920,8 +1017,10 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
                 const int i = base + tid;
                 int recv = -1;
                 const int li = i < n ? lin[i] : 0;
-                const bool keep = i < n && (simple ? pl_op1(g, T, li, &recv, C.pushes, C.relabels)
-                                                   : pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels));
+                bool keep = false;
+                if constexpr (!PK)
+                    keep = i < n && (simple ? pl_op1(g, T, li, &recv, C.pushes, C.relabels)
+                                            : pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels));
                 pl_append2_warp(keep, li, recv >= 0, recv, cnt_next, lout);
             }
         }
@@ -944,8 +1043,14 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmem &S, int tile, 
             const int32_t e = S.e[li], h = S.h[(lr + 1) * HS + PL_HC + tx];
             g.e[p] = e;
             g.h[p] = h;
-            g.rR[p] = S.r[0][li]; g.rL[p] = S.r[1][li];
-            g.rD[p] = S.r[2][li]; g.rU[p] = S.r[3][li];
+            if constexpr (PK) {
+                const uint2 w = S.res.r2[li];
+                g.rR[p] = (int32_t)(w.x & 0xffff); g.rL[p] = (int32_t)(w.x >> 16);
+                g.rD[p] = (int32_t)(w.y & 0xffff); g.rU[p] = (int32_t)(w.y >> 16);
+            } else {
+                g.rR[p] = S.res.r[0][li]; g.rL[p] = S.res.r[1][li];
+                g.rD[p] = S.res.r[2][li]; g.rU[p] = S.res.r[3][li];
+            }
             g.rT[p] = S.t[li];
             act |= (e > 0 && h < V && !(S.f[li] & 2));
         }
@@ -970,11 +1075,15 @@ struct PrCtl {
     unsigned long long tiles;
 };
 
-__global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_list_kernel(GridDev g, int k_local, int steps, int fused,
+#ifndef FM_PK_MINBLOCKS
+#define FM_PK_MINBLOCKS 8
+#endif
+template <bool PK>
+__global__ void __launch_bounds__(PL_NT, PK ? FM_PK_MINBLOCKS : FM_PL_MINBLOCKS) pr_list_kernel(GridDev g, int k_local, int steps, int fused,
                                                                        int parity_arg, int32_t *processed,
                                                                        unsigned long long *ops,
                                                                        PrCtl *ctl, cudaGraphConditionalHandle loop) {
-    __shared__ PlSmem S;
+    __shared__ PlSmemT<PK> S;
     const int tid = threadIdx.y * PT_W + threadIdx.x;
     // graph launches read the launch parity from the round's control block (processed
     // then points into it); host launches pass it as an argument
@@ -2187,11 +2296,14 @@ struct fm_grid {
     cudaGraph_t prg = nullptr;           // that graph, its instance and the launch parameters it was built for
     cudaGraphExec_t prg_exec = nullptr;
     GridDev prg_d{};
-    int prg_key[4] = {0, 0, 0, 0};
+    int prg_key[5] = {0, 0, 0, 0, 0};
     bool prg_pending = false;            // round control block read back, consumed after the caller's sync
     bool band_user_stream = false;       // band steps run on a caller stream (fm_grid_band_stream)
     int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (env FM_PR_KERNEL)
     int pl_per_sm = 6;                   // resident pr_list CTAs per SM (occupancy query)
+    int pk_per_sm = 8;                   // same, packed-residual instance (occupancy query)
+    int pk = 1;                          // packed 16-bit residuals in the push kernel when the input allows (env FM_PACKED)
+    bool pk_ok = false;                  // this solve's input allows them (every pair sum <= 65535)
     int k_local_list = 0;                // passes per visit of the list kernel (env FM_K_LOCAL_LIST)
     int bq_parity = 0;                   // parity of the next BFS / cut sweep
     int32_t *d_band = nullptr;           // band exchange: changed counter
@@ -2466,9 +2578,10 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
     FM_CHECK_LAUNCH();
     g->st.launches++;
-    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 3,
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 4,
                                   cudaMemcpyDeviceToHost, g->stream));
     FM_TRY(sync_stream(g));
+    g->pk_ok = g->h_acc[3] == 0;
     if (g->h_acc[1] != 0) {
         fm_set_error("negative capacity in grid input (%llu entries)", g->h_acc[1]);
         return FM_INVALID_ARG;
@@ -2552,8 +2665,8 @@ PrCtl *pr_ctl_host(fm_grid *g) { return reinterpret_cast<PrCtl *>(g->h_flags + 3
 // (Re)build the push-round while-graph for these launch parameters (body: one
 // pr_list_kernel node whose last CTA sets the loop condition).  Rebuilt only when a
 // parameter baked into the node changes.
-int pr_graph_build(fm_grid *g, int k_local, int blocks) {
-    const int key[4] = {k_local, blocks, g->op_steps, g->op_fused};
+int pr_graph_build(fm_grid *g, int k_local, int blocks, bool pk) {
+    const int key[5] = {k_local, blocks, g->op_steps, g->op_fused, pk ? 1 : 0};
     if (g->prg_exec && !memcmp(key, g->prg_key, sizeof(key)) && !memcmp(&g->d, &g->prg_d, sizeof(GridDev)))
         return FM_OK;
     if (g->prg_exec) { cudaGraphExecDestroy(g->prg_exec); g->prg_exec = nullptr; }
@@ -2577,7 +2690,7 @@ int pr_graph_build(fm_grid *g, int k_local, int blocks) {
     unsigned long long *ops = g->acc + 10;
     void *pr_args[] = {&d, &k_local, &steps, &fused, &parity0, &processed, &ops, &ctl, &handle};
     cudaKernelNodeParams kp{};
-    kp.func = (void *)pr_list_kernel;
+    kp.func = pk ? (void *)pr_list_kernel<true> : (void *)pr_list_kernel<false>;
     kp.gridDim = dim3(blocks);
     kp.blockDim = dim3(PT_W, PL_TY);
     kp.kernelParams = pr_args;
@@ -2614,9 +2727,10 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
                                              bfs_interval > 0 ? bfs_interval : MAX_LAUNCHES_DEFAULT));
     const long long relabel_budget =
         std::max<long long>(1024, g->HW / (g->relabel_div > 0 ? g->relabel_div : RELABEL_DIV_DEFAULT));
-    const int blocks = std::min(g->ntiles, g->sms * (g->pr_kernel == 1 ? g->pl_per_sm : g->pt_per_sm));
+    const bool pk = g->pk && g->pk_ok && g->op_steps == 1 && !g->op_fused;
+    const int blocks = std::min(g->ntiles, g->sms * (g->pr_kernel == 1 ? (pk ? g->pk_per_sm : g->pl_per_sm) : g->pt_per_sm));
     if (g->pr_graph && g->pr_kernel == 1) {
-        FM_TRY(pr_graph_build(g, k_local, blocks));
+        FM_TRY(pr_graph_build(g, k_local, blocks, pk));
         PrCtl *h = pr_ctl_host(g);
         *h = PrCtl{};
         h->parity = g->pq_parity;
@@ -2644,7 +2758,8 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
             const int p = g->pq_parity;
             FM_TRY(tq_arm(g, g->d.pq, p));
             if (g->pr_kernel == 1)
-                pr_list_kernel<<<blocks, dim3(PT_W, PL_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10, nullptr, 0);
+                (pk ? pr_list_kernel<true> : pr_list_kernel<false>)<<<blocks, dim3(PT_W, PL_TY), 0, g->stream>>>(
+                    g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10, nullptr, 0);
             else
                 pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, g->vote_mask, p, g->flags + i, g->acc + 10);
             g->pq_parity ^= 1;
@@ -2874,6 +2989,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
     if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
     if (const char *v = getenv("FM_PR_GRAPH")) g->pr_graph = atoi(v);
+    if (const char *v = getenv("FM_PACKED")) g->pk = atoi(v);
     g->d.solo_max = 32;
     g->d.k_solo = 0;
     if (const char *v = getenv("FM_K_SOLO")) g->d.k_solo = atoi(v);
@@ -2946,7 +3062,9 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->sms = sms;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pt_per_sm, pr_tile_kernel, PT_W * PT_TY, 0);
     g->pt_per_sm = std::max(1, g->pt_per_sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pl_per_sm, pr_list_kernel, PT_W * PL_TY, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pl_per_sm, pr_list_kernel<false>, PT_W * PL_TY, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pk_per_sm, pr_list_kernel<true>, PT_W * PL_TY, 0);
+    if (const char *v = getenv("FM_PK_OCC")) g->pk_per_sm = std::max(1, std::min(g->pk_per_sm, atoi(v)));
     g->pl_per_sm = std::max(1, g->pl_per_sm);
     if (const char *v = getenv("FM_PL_PER_SM")) g->pl_per_sm = std::max(1, std::min(g->pl_per_sm, atoi(v)));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->bb_per_sm, bfs_bits_kernel, 32 * BB_WARPS, 0);
@@ -3176,9 +3294,10 @@ extern "C" int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t 
         g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
     FM_CHECK_LAUNCH();
     g->st.launches++;
-    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 3,
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 4,
                                   cudaMemcpyDeviceToHost, g->stream));
     FM_TRY(sync_stream(g));
+    g->pk_ok = g->h_acc[3] == 0;
     if (g->h_acc[1] != 0) { fm_set_error("negative capacity in grid input"); return FM_INVALID_ARG; }
     if (g->h_acc[2] != 0) { fm_set_error("grid capacities too large for the int32 device state"); return FM_INVALID_ARG; }
     g->sum_capS = (long long)g->h_acc[0];

@@ -4,12 +4,21 @@
     python scripts/summarize_ncu.py full gpurun_out/prof.ncu-rep > profiles/X_full.md
     python scripts/summarize_ncu.py traffic gpurun_out/traffic.csv > profiles/ncu_traffic.json
 """
+import re
 import collections
 import csv
 import io
 import subprocess
 import sys
 
+
+
+def kname(raw):
+    """Kernel name without namespace, return type, template arguments or parameters."""
+    n = raw.replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+    n = n.split("(")[0]
+    n = re.sub(r"<[^<>]*>", "", n)
+    return n.replace("void ", "").strip()
 
 def launches(path):
     rows = list(csv.reader(open(path)))
@@ -21,7 +30,7 @@ def launches(path):
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
-        name = r[ki].split("(")[0].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        name = kname(r[ki])
         agg[name][0] += 1
         agg[name][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     tot = sum(v[1] for v in agg.values())
@@ -77,7 +86,7 @@ def traffic(path):
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
-        names[r[ii]] = r[ki].split("(")[0].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        names[r[ii]] = kname(r[ki])
         per[r[ii]][r[mi]] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for lid, m in per.items():

@@ -127,3 +127,21 @@ def test_int32_capacity_limits():
     assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
     with pytest.raises(ValueError):
         fmb.hybrid_solve(fmb.build_grid_network(*caps_upto(2**31 - 1)))
+
+
+@pytest.mark.parametrize("hi", [32767, 32768, 65535])
+def test_packed_residual_boundary(hi):
+    """The push kernel packs a pixel's four residuals into 16-bit fields when every
+    neighbour pair's two capacities sum to <= 65535 and keeps int32 residuals
+    otherwise: capacities at and just past that limit (with pairs saturated at the
+    maximum) stay bit-exact on both sides of the switch."""
+    rng = np.random.default_rng(hi)
+    H, W = 150, 170
+    caps = _random_caps(rng, H, W, hi, 0.6, 0.6)
+    caps[0][::3, :-1] = hi      # pairs at the maximum sum
+    caps[1][::3, 1:] = hi
+    caps[2][:-1, ::5] = hi
+    caps[3][1:, ::5] = hi
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
+    assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()

@@ -36,6 +36,7 @@ VARIANTS = {
     "no_two_hop": {"FM_TWO_HOP": "0"},
     "three_hop": {"FM_TWO_HOP": "2"},
     "pr_graph": {"FM_PR_GRAPH": "1"},
+    "unpacked": {"FM_PACKED": "0"},
     "pr_graph_b1": {"FM_PR_GRAPH": "1", "FM_PR_BATCH": "1"},
 }
 
