@@ -83,6 +83,7 @@ struct AssignDev {
     int64_t max_bucket;    // scaled_cost_bound / eps + 2 (assign_scaling.py:232)
     int32_t pu_cap0;       // first label cap of the price update (0 = 8)
     int use_fix;
+    int ybatch_min;         // gathered Y op: rank-batch the push-back from this many units (env FM_YBATCH_MIN)
 };
 
 
@@ -252,7 +253,7 @@ constexpr int YBUCKET = 256;            // per-Y bucket slots for long Y lists (
 
 template <bool CTA_WIDE>
 __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
-                     unsigned long long &pushes, unsigned long long &relabels) {
+                     unsigned long long &pushes, unsigned long long &relabels, long long *sbuf) {
     __shared__ long long s_cv[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
     __shared__ int s_cx[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
     __shared__ int s_cn[CTA_WIDE ? 1 : AWARPS];
@@ -320,6 +321,43 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
             ey--;
             if (CTA_WIDE) __syncthreads(); else __syncwarp();
         }
+    } else if (ey >= a.ybatch_min && ey < cnt) {
+        // ---- batch: the ey cheapest candidates in (v, x) order are exactly the units
+        // the one-unit loop below would push back (y's relabels never reorder them).
+        // Rank every candidate against the others, lay the chosen costs out in rank
+        // order (sbuf: >= CAP entries of the caller's shared scratch), append the
+        // batch with one list reservation and replay the relabel sequence.
+        __shared__ int s_base[CTA_WIDE ? 1 : AWARPS];
+        if (t == 0) s_base[slot] = atomicAdd(xcnt_next, ey);
+        if (CTA_WIDE) __syncthreads(); else __syncwarp();
+        const int base = s_base[slot];
+        for (int k = t; k < cnt; k += T) {
+            const long long vk = cv[k];
+            const int xk = cx[k];
+            int rank = 0;
+#pragma unroll 8
+            for (int j = 0; j < cnt; j++) {
+                const long long vj = cv[j];
+                rank += (vj < vk || (vj == vk && cx[j] < xk)) ? 1 : 0;
+            }
+            if (rank < ey) {
+                sbuf[rank] = vk;
+                a.match[xk] = -1;
+                xlist_next[base + rank] = xk;
+            }
+        }
+        if (CTA_WIDE) __syncthreads(); else __syncwarp();
+        if (t == 0) {
+            unsigned long long rl = 0;
+            for (int k = 0; k < ey; k++) {
+                const long long vk = sbuf[k];
+                if (!(vk < -py)) { py = -(vk + a.eps); rl++; }
+            }
+            relabels += rl;
+            pushes += ey;
+            if (rl) atomicAdd(a.cnt + C_RELABELS, (int)rl);
+        }
+        ey = 0;
     } else {
         // ---- push back to the cheapest gathered candidates, one per excess unit
         while (ey > 0) {
@@ -418,7 +456,7 @@ __device__ void y_op_bucketed(const AssignDev &a, int y, int32_t *xlist_next, in
     const int cnt = __ldcg(a.ybcnt + y);
     const int ey = __ldcg(a.ey + y);
     if (cnt > YBUCKET || ey >= cnt) {       // bucket overflow (or inconsistent): scan match[] instead
-        y_op<false>(a, y, xlist_next, xcnt_next, pushes, relabels);
+        y_op<false>(a, y, xlist_next, xcnt_next, pushes, relabels, s_sorted);
         if (lane == 0) a.ybcnt[y] = 0;
         __syncwarp();
         return;
@@ -552,10 +590,10 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             const unsigned long long p0 = pushes + relabels;
             if (ny <= 2) {
                 for (int i = 0; i < ny; i++)
-                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0]);
             } else {
                 for (int i = cwarp; i < ny; i += AWARPS)
-                    y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+                    y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[cwarp]);
             }
             __threadfence_block();
             __syncthreads();
@@ -577,7 +615,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             unsigned long long t0 = timer ? globaltimer() : 0, t1 = 0;
             if (ny <= (int)gridDim.x) {
                 for (int i = blockIdx.x; i < ny; i += gridDim.x)
-                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels);
+                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0]);
             } else {
                 // long list: bucket every incoming X by its Y in one pass over match[]
                 const int gtid = blockIdx.x * ATHREADS + threadIdx.x, gthr = gridDim.x * ATHREADS;
@@ -997,6 +1035,8 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     AssignDev &d = A->d;
     d.w = w;
     d.use_fix = (flags & FM_ASSIGN_ARC_FIX) ? 1 : 0;
+    d.ybatch_min = 2;
+    if (const char *v = getenv("FM_YBATCH_MIN")) d.ybatch_min = std::max(1, atoi(v));
     A->alpha = alpha;
     A->flags = flags;
     memset(&A->st, 0, sizeof(A->st));

@@ -180,3 +180,24 @@ def test_sparse_mid_size_vs_scipy():
     rep, m = fmb.solve_assignment(w)
     assert rep.objective == int(big[r, c].sum())
     assert all(w[x, y] != -(2**31) for x, y in enumerate(m))
+
+
+@pytest.mark.parametrize("ybatch_min", ["1", "1000000"])
+def test_y_batch_threshold_variants(ybatch_min, monkeypatch):
+    """The gathered Y op pushes its excess back either unit by unit (an argmin per
+    unit) or, from FM_YBATCH_MIN units on, as one rank-ordered batch; both orders are
+    the same sequence of reference operations, so objective and matching agree with
+    scipy's exact solver either way (knob read at solver creation)."""
+    from scipy.optimize import linear_sum_assignment
+    monkeypatch.setenv("FM_YBATCH_MIN", ybatch_min)
+    rng = np.random.default_rng(int(ybatch_min) % 97)
+    for n, M in ((300, 10000), (700, 100), (1024, 10)):
+        w = rng.integers(0, M + 1, size=(n, n)).astype(np.int32)
+        r, c = linear_sum_assignment(w.astype(np.int64), maximize=True)
+        solver = fmb.AssignmentSolver(n)
+        try:
+            obj, m, _, _ = solver.solve_host(w)
+        finally:
+            solver.close()
+        m = list(m)
+        assert obj == int(w[r, c].sum()) and _is_perm(m, n) and _objective(w, m) == obj
