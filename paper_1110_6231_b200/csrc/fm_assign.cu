@@ -681,6 +681,7 @@ __device__ __forceinline__ long long floordiv_eps(long long rc, long long eps, d
 // along row y of the transposed weights (coalesced) with atomicMin on l(x); Y step
 // = one thread per X whose label dropped, relaxing its matched reverse arc.
 constexpr int PU_GROUPS = 4;   // price update: up to this many frontier Y per CTA in flight
+constexpr int PU_RING_EXTRA = 16384;   // ring slots beyond n (>= the price update's groups + 64)
 __device__ __forceinline__ void group_sync(int grp, int nthreads) {   // named barrier of one thread group
     asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(nthreads) : "memory");
 }
@@ -690,7 +691,103 @@ struct PuDev {
     int32_t *fy[2], *fx[2]; // frontiers
     int32_t *in_fx, *in_fy; // frontier membership flags
     int32_t *cnt;           // [0..1] |fy|, [2..3] |fx|
+    // queue-driven variant (ring_on, env FM_PU_RING): frontier Y in a ring of ring_cap
+    // slots (-1 = empty); rctr[0] head, [32] tail, [64] pending (queued + in flight)
+    int32_t *ring;
+    unsigned int *rctr;
+    int ring_cap, ring_on;
 };
+
+// One frontier Y of the price update, scanned by a group of GT threads (thread gt):
+// relax every arc x->y into l(x) and, where l(x) dropped, x's matched reverse arc into
+// its Y; push(y2) queues a Y whose label dropped (its queued flag already set).
+template <typename Push>
+__device__ __forceinline__ void pu_scan_y(const AssignDev &a, const PuDev &f, int y, int lyv, long long pyv,
+                                          long long cap, double inv_eps, int gt, int PU_GT, Push push) {
+    const int n = a.n;
+    const int32_t *col = f.wt + (size_t)y * n;
+    // vector path: 8 consecutive x per thread, every operand loaded up front
+    // (int4 weights / labels / matches, longlong2 prices) so a thread's scan is
+    // one L2 round trip instead of a chain of dependent ones
+    const int nv8 = (n & 7) ? 0 : n;
+    for (int x0 = gt * 8; x0 < nv8; x0 += PU_GT * 8) {
+        const int4 w0 = __ldg((const int4 *)(col + x0)), w1 = __ldg((const int4 *)(col + x0 + 4));
+        const int4 l0 = __ldcg((const int4 *)(a.lx + x0)), l1 = __ldcg((const int4 *)(a.lx + x0 + 4));
+        const int4 m0 = __ldcg((const int4 *)(a.match + x0)), m1 = __ldcg((const int4 *)(a.match + x0 + 4));
+        longlong2 pv[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) pv[k] = __ldcg((const longlong2 *)(a.px + x0) + k);
+        uint32_t fb = 0;
+        if (a.use_fix) fb = (__ldg(a.fixed_t + (size_t)y * a.nw + (x0 >> 5)) >> (x0 & 31)) & 0xffu;
+        const int wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+        const int lxv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+        const int mxv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        const long long pxv[8] = {pv[0].x, pv[0].y, pv[1].x, pv[1].y, pv[2].x, pv[2].y, pv[3].x, pv[3].y};
+        // stage 1: candidate labels; stage 2: all atomicMin on l(x) in flight
+        // together; stage 3: the matched reverse arcs of the x that dropped
+        int cand[8], old[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            cand[k] = LINF;
+            if (wv[k] == FM_ABSENT_WEIGHT || lyv >= lxv[k] || mxv[k] == y || ((fb >> k) & 1u)) continue;
+            const long long rc = -(long long)wv[k] * a.scale + pxv[k] - pyv;
+            long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
+            if (len < 0) len = 0;
+            const long long c1 = (long long)lyv + len;
+            if (c1 <= cap && c1 < lxv[k]) cand[k] = (int)c1;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) old[k] = cand[k] < LINF ? atomicMin(a.lx + x0 + k, cand[k]) : LINF;
+        int w2[8];
+        long long py2[8];
+        uint8_t fz[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const bool go = cand[k] < old[k] && mxv[k] >= 0;
+            w2[k] = go ? __ldg(a.w + (size_t)(x0 + k) * n + mxv[k]) : 0;
+            py2[k] = go ? __ldcg((const long long *)a.py + mxv[k]) : 0;
+            fz[k] = go ? __ldcg(a.frozen + x0 + k) : 1;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (!(cand[k] < old[k]) || mxv[k] < 0 || fz[k]) continue;
+            const long long rc2 = (long long)w2[k] * a.scale - pxv[k] + py2[k];
+            long long len2 = floordiv_eps(rc2, a.eps, inv_eps) + 1;
+            if (len2 < 0) len2 = 0;
+            const long long cand2 = cand[k] + len2;
+            if (cand2 > cap) continue;
+            const int mx = mxv[k];
+            const int old2 = atomicMin(a.ly + mx, (int)cand2);
+            if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0) push(mx);
+        }
+    }
+    for (int x = nv8 + gt; x < n; x += PU_GT) {
+        const int wv = __ldg(col + x);
+        if (wv == FM_ABSENT_WEIGHT) continue;
+        const int lxv = __ldcg(a.lx + x);
+        if (lyv >= lxv) continue;                              // cannot improve (len >= 0)
+        const int mx = __ldcg(a.match + x);
+        if (mx == y) continue;                                 // flow arc: not residual forward
+        if (a.use_fix && ((__ldg(a.fixed_t + (size_t)y * a.nw + (x >> 5)) >> (x & 31)) & 1u)) continue;
+        const long long px = __ldcg((const long long *)a.px + x);
+        const long long rc = -(long long)wv * a.scale + px - pyv;
+        long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
+        if (len < 0) len = 0;
+        const long long cand = (long long)lyv + len;
+        if (cand > cap || cand >= lxv) continue;
+        const int old = atomicMin(a.lx + x, (int)cand);
+        if ((int)cand >= old || mx < 0 || __ldcg(a.frozen + x)) continue;
+        // l(x) dropped: relax x's unit arc y2 -> x (reverse of the matched arc)
+        const long long rc2 = (long long)__ldg(a.w + (size_t)x * n + mx) * a.scale - px +
+                              __ldcg((const long long *)a.py + mx);
+        long long len2 = floordiv_eps(rc2, a.eps, inv_eps) + 1;
+        if (len2 < 0) len2 = 0;
+        const long long cand2 = cand + len2;
+        if (cand2 > cap) continue;
+        const int old2 = atomicMin(a.ly + mx, (int)cand2);
+        if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0) push(mx);
+    }
+}
 
 __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuDev f) {
     cg::grid_group grid = cg::this_grid();
@@ -714,7 +811,12 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
         if (__ldcg(a.ey + v) < 0) {
             a.ly[v] = 0;
             f.in_fy[v] = 1;
-            f.fy[0][atomicAdd(f.cnt + 0, 1)] = v;   // iteration 0's frontier (counter 0 of 3)
+            if (f.ring_on) {
+                atomicAdd(f.rctr + 64, 1u);
+                f.ring[atomicAdd(f.rctr + 32, 1u)] = v;   // slots are empty, tail starts at 0
+            } else {
+                f.fy[0][atomicAdd(f.cnt + 0, 1)] = v;   // iteration 0's frontier (counter 0 of 3)
+            }
         } else {
             a.ly[v] = LINF;
             f.in_fy[v] = 0;
@@ -727,6 +829,53 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     // the counter of iteration it+2 can be zeroed during iteration it.
     int it = 0;
     const unsigned long long t_it0 = globaltimer();
+    if (f.ring_on) {
+        // Queue-driven relaxation, no grid barrier per wave: groups take frontier Y from
+        // the ring until it is empty and nothing is in flight (chaotic relaxation: every
+        // label is a path length and only falls, so the fixpoint is the same).  The ring
+        // holds more slots than queued entries (<= n, one per Y) plus waiting groups, an
+        // entry is taken with an exchange (one taker) and a slot refilled only when empty
+        // (CAS), so no entry is lost, duplicated or overwritten.
+        const int PU_GT = ATHREADS / PU_GROUPS;
+        const int grp = threadIdx.x / PU_GT, gt = threadIdx.x - grp * PU_GT;
+        unsigned long long ys = 0;
+        for (;;) {
+            if (gt == 0) {
+                int y = -1;
+                const unsigned sl = atomicAdd(f.rctr + 0, 1u) % (unsigned)f.ring_cap;
+                for (unsigned ns = 32;; ns = min(ns * 2, 1024u)) {
+                    if (*(volatile int32_t *)(f.ring + sl) >= 0) {
+                        const int v = atomicExch(f.ring + sl, -1);   // exactly one taker per entry
+                        if (v >= 0) { y = v; break; }
+                    }
+                    if (*(volatile unsigned *)(f.rctr + 64) == 0) break;
+                    __nanosleep(ns);
+                }
+                s_y[grp] = y;
+                if (y >= 0) {
+                    f.in_fy[y] = 0;          // clear before reading l(y): a later drop re-queues y
+                    __threadfence();
+                    s_ly[grp] = __ldcg(a.ly + y);
+                    s_py[grp] = __ldcg((const long long *)a.py + y);
+                    ys++;
+                }
+            }
+            group_sync(grp, PU_GT);
+            const int y = s_y[grp];
+            if (y < 0) break;
+            pu_scan_y(a, f, y, s_ly[grp], s_py[grp], cap, inv_eps, gt, PU_GT, [&](int mx) {
+                atomicAdd(f.rctr + 64, 1u);
+                const unsigned t = atomicAdd(f.rctr + 32, 1u);
+                __threadfence();             // labels (and pending) visible before the entry
+                int32_t *slot = f.ring + t % (unsigned)f.ring_cap;
+                while (atomicCAS(slot, -1, mx) != -1) __nanosleep(64);
+            });
+            group_sync(grp, PU_GT);
+            if (gt == 0) { __threadfence(); atomicSub(f.rctr + 64, 1u); }
+        }
+        if (gt == 0 && ys) atomicAdd(a.ops + O_PU_YS, ys);
+        grid.sync();
+    } else
     for (;; it++) {
         const int b = it & 1, nb = b ^ 1;
         int ny, u1, u2;
@@ -768,90 +917,9 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
             const int y = s_y[grp];
             const int lyv = s_ly[grp];
             const long long pyv = s_py[grp];
-            const int32_t *col = f.wt + (size_t)y * n;
-            // vector path: 8 consecutive x per thread, every operand loaded up front
-            // (int4 weights / labels / matches, longlong2 prices) so a thread's scan is
-            // one L2 round trip instead of a chain of dependent ones
-            const int nv8 = (n & 7) ? 0 : n;
-            for (int x0 = gt * 8; x0 < nv8; x0 += PU_GT * 8) {
-                const int4 w0 = __ldg((const int4 *)(col + x0)), w1 = __ldg((const int4 *)(col + x0 + 4));
-                const int4 l0 = __ldcg((const int4 *)(a.lx + x0)), l1 = __ldcg((const int4 *)(a.lx + x0 + 4));
-                const int4 m0 = __ldcg((const int4 *)(a.match + x0)), m1 = __ldcg((const int4 *)(a.match + x0 + 4));
-                longlong2 pv[4];
-#pragma unroll
-                for (int k = 0; k < 4; k++) pv[k] = __ldcg((const longlong2 *)(a.px + x0) + k);
-                uint32_t fb = 0;
-                if (a.use_fix) fb = (__ldg(a.fixed_t + (size_t)y * a.nw + (x0 >> 5)) >> (x0 & 31)) & 0xffu;
-                const int wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-                const int lxv[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
-                const int mxv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
-                const long long pxv[8] = {pv[0].x, pv[0].y, pv[1].x, pv[1].y, pv[2].x, pv[2].y, pv[3].x, pv[3].y};
-                // stage 1: candidate labels; stage 2: all atomicMin on l(x) in flight
-                // together; stage 3: the matched reverse arcs of the x that dropped
-                int cand[8], old[8];
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    cand[k] = LINF;
-                    if (wv[k] == FM_ABSENT_WEIGHT || lyv >= lxv[k] || mxv[k] == y || ((fb >> k) & 1u)) continue;
-                    const long long rc = -(long long)wv[k] * a.scale + pxv[k] - pyv;
-                    long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
-                    if (len < 0) len = 0;
-                    const long long c1 = (long long)lyv + len;
-                    if (c1 <= cap && c1 < lxv[k]) cand[k] = (int)c1;
-                }
-#pragma unroll
-                for (int k = 0; k < 8; k++) old[k] = cand[k] < LINF ? atomicMin(a.lx + x0 + k, cand[k]) : LINF;
-                int w2[8];
-                long long py2[8];
-                uint8_t fz[8];
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    const bool go = cand[k] < old[k] && mxv[k] >= 0;
-                    w2[k] = go ? __ldg(a.w + (size_t)(x0 + k) * n + mxv[k]) : 0;
-                    py2[k] = go ? __ldcg((const long long *)a.py + mxv[k]) : 0;
-                    fz[k] = go ? __ldcg(a.frozen + x0 + k) : 1;
-                }
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    if (!(cand[k] < old[k]) || mxv[k] < 0 || fz[k]) continue;
-                    const long long rc2 = (long long)w2[k] * a.scale - pxv[k] + py2[k];
-                    long long len2 = floordiv_eps(rc2, a.eps, inv_eps) + 1;
-                    if (len2 < 0) len2 = 0;
-                    const long long cand2 = cand[k] + len2;
-                    if (cand2 > cap) continue;
-                    const int mx = mxv[k];
-                    const int old2 = atomicMin(a.ly + mx, (int)cand2);
-                    if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0)
-                        f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;   // read after the grid barrier
-                }
-            }
-            for (int x = nv8 + gt; x < n; x += PU_GT) {
-                const int wv = __ldg(col + x);
-                if (wv == FM_ABSENT_WEIGHT) continue;
-                const int lxv = __ldcg(a.lx + x);
-                if (lyv >= lxv) continue;                              // cannot improve (len >= 0)
-                const int mx = __ldcg(a.match + x);
-                if (mx == y) continue;                                 // flow arc: not residual forward
-                if (a.use_fix && ((__ldg(a.fixed_t + (size_t)y * a.nw + (x >> 5)) >> (x & 31)) & 1u)) continue;
-                const long long px = __ldcg((const long long *)a.px + x);
-                const long long rc = -(long long)wv * a.scale + px - pyv;
-                long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
-                if (len < 0) len = 0;
-                const long long cand = (long long)lyv + len;
-                if (cand > cap || cand >= lxv) continue;
-                const int old = atomicMin(a.lx + x, (int)cand);
-                if ((int)cand >= old || mx < 0 || __ldcg(a.frozen + x)) continue;
-                // l(x) dropped: relax x's unit arc y2 -> x (reverse of the matched arc)
-                const long long rc2 = (long long)__ldg(a.w + (size_t)x * n + mx) * a.scale - px +
-                                      __ldcg((const long long *)a.py + mx);
-                long long len2 = floordiv_eps(rc2, a.eps, inv_eps) + 1;
-                if (len2 < 0) len2 = 0;
-                const long long cand2 = cand + len2;
-                if (cand2 > cap) continue;
-                const int old2 = atomicMin(a.ly + mx, (int)cand2);
-                if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0)
-                    f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;
-            }
+            pu_scan_y(a, f, y, lyv, pyv, cap, inv_eps, gt, PU_GT, [&](int mx) {
+                f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;   // read after the grid barrier
+            });
             group_sync(grp, PU_GT);
         }
         grid.sync();
@@ -883,7 +951,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     cta_bcast3(a.cnt + C_PU_CHG, nullptr, nullptr, chg, u1, u2);
     if (!chg || cap >= a.max_bucket) break;
     cap = min(cap * 8, (long long)a.max_bucket);
-    if (tid == 0) { f.cnt[0] = f.cnt[1] = f.cnt[2] = 0; }
+    if (tid == 0) { f.cnt[0] = f.cnt[1] = f.cnt[2] = 0; f.rctr[0] = f.rctr[32] = f.rctr[64] = 0; }
     grid.sync();
     }  // cap loop
     const long long K = min((long long)__ldcg(a.cnt + C_PU_LAST), (long long)a.max_bucket) + 1;
@@ -894,6 +962,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     if (tid == 0) {
         a.cnt[C_RELABELS] = 0;
         f.cnt[0] = f.cnt[1] = f.cnt[2] = f.cnt[3] = 0;
+        f.rctr[0] = f.rctr[32] = f.rctr[64] = 0;
         atomicAdd(a.ops + O_PU, 1ull);
         atomicAdd(a.ops + O_PU_ITERS, (unsigned long long)it_total);
     }
@@ -1060,6 +1129,14 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
         transpose_kernel<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, s>>>(w, A->wt, n);
         FM_CHECK_LAUNCH();
         FM_CHECK_CUDA(cudaMemsetAsync(A->pu.cnt, 0, sizeof(int32_t) * 4, s));
+        // > queued entries (<= n) + groups waiting on a slot (pu_blocks * PU_GROUPS)
+        A->pu.ring_cap = n + std::min(PU_RING_EXTRA, A->pu_blocks * PU_GROUPS + 64);
+        A->pu.ring_on = 1;
+        if (const char *v = getenv("FM_PU_RING")) A->pu.ring_on = atoi(v) ? 1 : 0;
+        if (A->pu.ring_on) {
+            FM_CHECK_CUDA(cudaMemsetAsync(A->pu.ring, 0xff, sizeof(int32_t) * ((size_t)n + PU_RING_EXTRA), s));
+            FM_CHECK_CUDA(cudaMemsetAsync(A->pu.rctr, 0, sizeof(unsigned int) * 96, s));
+        }
         A->st.launches++;
     }
     FM_CHECK_CUDA(cudaMemcpyAsync(A->h_acc, A->acc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
@@ -1233,6 +1310,10 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMalloc((void **)&A->pu.in_fx, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&A->pu.in_fy, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&A->pu.cnt, sizeof(int32_t) * 4) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.ring, sizeof(int32_t) * ((size_t)n + PU_RING_EXTRA)) == cudaSuccess &&
+              cudaMalloc((void **)&A->pu.rctr, sizeof(unsigned int) * 96) == cudaSuccess &&
+              cudaMemset(A->pu.ring, 0xff, sizeof(int32_t) * ((size_t)n + PU_RING_EXTRA)) == cudaSuccess &&
+              cudaMemset(A->pu.rctr, 0, sizeof(unsigned int) * 96) == cudaSuccess &&
               cudaMalloc((void **)&d.ly, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * 16) == cudaSuccess &&
               cudaMalloc((void **)&A->acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
@@ -1264,7 +1345,7 @@ extern "C" void fm_assign_destroy(fm_assign *A) {
     void *dev[] = {A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.fixed_t, A->d.frozen, A->d.frozen_in,
                    A->d.xlist[0], A->d.xlist[1], A->d.ylist[0], A->d.ylist[1], A->d.cnt, A->d.ops,
                    A->d.lx, A->d.ly, A->d.ybcnt, A->d.ybuf, A->wt, A->pu.fy[0], A->pu.fy[1], A->pu.fx[0], A->pu.fx[1],
-                   A->pu.in_fx, A->pu.in_fy, A->pu.cnt,
+                   A->pu.in_fx, A->pu.in_fy, A->pu.cnt, A->pu.ring, A->pu.rctr,
                    A->acc, A->in_w};
     for (void *p : dev) if (p) cudaFree(p);
     if (A->h_ops) cudaFreeHost(A->h_ops);

@@ -26,7 +26,10 @@ for case in range(n_cases):
     r, c = linear_sum_assignment(cost, maximize=True)
     want = int(w[r, c].astype(np.int64).sum())
     for rep_i in range(2):
+        tc = time.time()
         rep, m = fmb.solve_assignment(w)
+        if time.time() - tc > 2.0:
+            print(f"SLOW case {case} rep {rep_i}: n {n} hi {hi} sparse {sparse} {time.time() - tc:.1f} s", flush=True)
         got = int(sum(int(w[x, y]) for x, y in enumerate(m)))
         if rep.objective != want or got != want or sorted(m) != list(range(n)):
             bad += 1

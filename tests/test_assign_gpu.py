@@ -201,3 +201,34 @@ def test_y_batch_threshold_variants(ybatch_min, monkeypatch):
             solver.close()
         m = list(m)
         assert obj == int(w[r, c].sum()) and _is_perm(m, n) and _objective(w, m) == obj
+
+
+@pytest.mark.parametrize("ring", ["0", "1"])
+def test_price_update_barrier_and_queue_variants(ring, monkeypatch):
+    """The price update's label relaxation runs either as barrier-separated waves or
+    queue-driven without barriers (FM_PU_RING, read per solve); both reach the same
+    labels (a fixpoint of min-updates over path lengths), so the optimum and the
+    epsilon-optimality certificate hold either way, including sparse instances."""
+    from scipy.optimize import linear_sum_assignment
+    monkeypatch.setenv("FM_PU_RING", ring)
+    for n, M in ((1, 5), (7, 3), (64, 10000), (333, 100), (1024, 10000)):
+        w = G.assignment_reference(n, M, n + 7)
+        solver = fmb.AssignmentSolver(n)
+        try:
+            obj, m, prices, _ = solver.solve_host(w, want_prices=True)
+        finally:
+            solver.close()
+        r, c = linear_sum_assignment(w.astype(np.int64), maximize=True)
+        assert obj == int(w[r, c].sum())
+        code, cobj = oracle.assign_certify_dense(w, m, prices)
+        assert code == 0 and cobj == obj
+    rng = np.random.default_rng(int(ring) + 5)
+    n = 400
+    w = rng.integers(0, 1000, size=(n, n)).astype(np.int32)
+    keep = rng.random((n, n)) < 0.1
+    keep[np.arange(n), rng.permutation(n)] = True
+    w = np.where(keep, w, -(2**31)).astype(np.int32)
+    cost = np.where(w == -(2**31), -1e15, w.astype(np.float64))
+    r, c = linear_sum_assignment(cost, maximize=True)
+    rep, m = fmb.solve_assignment(w)
+    assert rep.objective == int(w[r, c].astype(np.int64).sum()) and sorted(m) == list(range(n))
