@@ -99,11 +99,11 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
                                  const int32_t *__restrict__ capS,
                                  const int32_t *__restrict__ capT, int precancel,
                                  unsigned long long *acc /* [0]=sum capS [1]=negative [2]=too large [3]=pair > 65535 */) {
-    const int64_t HW = (int64_t)g.H * g.W;
     long long sum = 0, bad = 0, big = 0, wide = 0;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
+    // rows over blocks, columns over threads: coalesced, and no 64-bit division per pixel
+    for (int32_t r = blockIdx.x; r < g.H; r += gridDim.x)
+    for (int32_t c = threadIdx.x; c < g.W; c += blockDim.x) {
+        const int64_t p = (int64_t)r * g.W + c;
         int32_t cs = capS[p], ct = capT[p];
         int32_t cr = c + 1 < g.W ? capR[p] : 0;
         int32_t cl = c > 0 ? capL[p] : 0;
@@ -166,13 +166,19 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
 // valid preflow, so flow value and minimal cut are unchanged; it only removes work
 // the first push rounds would otherwise do pixel by pixel.
 // ----------------------------------------------------------------------------
+__device__ __forceinline__ void two_hop_pixel(const GridDev &g, int32_t r, int32_t c);
+
+// one thread per pixel: x = column, rows over blockIdx.y (grid-stride past 65535 rows)
 __global__ void two_hop_kernel(GridDev g) {
-    const int64_t HW = (int64_t)g.H * g.W;
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // one thread per pixel
-    if (p >= HW) return;
+    const int32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= g.W) return;
+    for (int32_t r = blockIdx.y; r < g.H; r += gridDim.y) two_hop_pixel(g, r, c);
+}
+
+__device__ __forceinline__ void two_hop_pixel(const GridDev &g, int32_t r, int32_t c) {
+    const int64_t p = (int64_t)r * g.W + c;
     int32_t e = g.e[p];
     if (e <= 0) return;
-    const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
     if (is_ghost_row(g, r)) return;
     int32_t *fwd[4] = {g.rR, g.rL, g.rD, g.rU};
     int32_t *rev[4] = {g.rL, g.rR, g.rU, g.rD};
@@ -2601,7 +2607,7 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
         fprintf(stderr, "[fm_grid] after pre-cancellation: %lld of %lld source units at the sink\n", f, g->sum_capS);
     }
     if (g->two_hop && !(flags & FM_GRID_NO_PRECANCEL)) {
-        two_hop_kernel<<<(unsigned)((g->HW + 255) / 256), 256, 0, g->stream>>>(g->d);
+        two_hop_kernel<<<dim3((unsigned)((g->W + 255) / 256), (unsigned)std::min(g->H, 65535)), 256, 0, g->stream>>>(g->d);
         FM_CHECK_LAUNCH();
         g->st.launches++;
         if (g->two_hop >= 2) {
