@@ -1579,6 +1579,10 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
 #ifdef FM_BFS_TIMING
         const long long tl0 = clock64();
 #endif
+        // the level stores of step L are issued after step L+1's shuffles, so they run
+        // while the shuffles are in flight (P / PL: pixels reached last step, their level)
+        uint32_t P = 0;
+        int PL = 0;
         for (;;) {
             if (g0 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv0 == L); if (lane == g0) F |= s; }
             if (g1 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv1 == L); if (lane == g1) F |= s; }
@@ -1586,6 +1590,7 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
             const uint32_t bb = __ballot_sync(0xffffffffu, hb == L);
             uint32_t up = __shfl_up_sync(0xffffffffu, F, 1);
             uint32_t dn = __shfl_down_sync(0xffffffffu, F, 1);
+            for (uint32_t x = P; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = PL;
             if (lane == 0) up = tb;
             if (lane == 31) dn = bb;
             uint32_t N = ((F >> 1) & mR) | ((F << 1) & mL) | (dn & mD) | (up & mU);
@@ -1597,7 +1602,8 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
 #ifdef FM_BFS_TIMING
             lv++;
 #endif
-            for (uint32_t x = N; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = L;
+            P = N;
+            PL = L;
             F = N;
             if (!__any_sync(0xffffffffu, F != 0)) {
                 int m = INF;
