@@ -209,6 +209,7 @@ extern "C" int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const i
     FM_CSR_TRY(cudaMalloc((void **)&acc, sizeof(unsigned long long) * 8));
     FM_CSR_TRY(cudaMalloc((void **)&flags_d, sizeof(int32_t) * 4));
     cudaEventRecord(t0, stream);
+    FM_CSR_TRY(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 8, stream));   // op counters
     FM_CSR_TRY(cudaMemcpyAsync(d_ostart, ostart, sizeof(int64_t) * ((size_t)n + 1), cudaMemcpyHostToDevice, stream));
     if (m2 > 0) {
         FM_CSR_TRY(cudaMemcpyAsync(d_oarc, oarc, sizeof(int32_t) * m2, cudaMemcpyHostToDevice, stream));

@@ -1,0 +1,16 @@
+"""Small grid / segmentation / assignment / generic solves for compute-sanitizer runs
+(memcheck, initcheck, synccheck) on the GPU box: scripts/sanitize_smoke.py under
+`compute-sanitizer --tool <tool> python scripts/sanitize_smoke.py`."""
+import os, sys; sys.path.insert(0, os.getcwd())
+import numpy as np, paper_1110_6231_b200 as fmb
+from paper_1110_6231_b200 import generators as G
+for (H, W) in ((200, 256), (33, 70), (1, 97)):
+    caps = G.grid_random(H, W, 7)
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*caps)); print("grid", H, W, rep.objective)
+for (H, W) in ((100, 128),):
+    caps = G.grid_segmentation(H, W, 3)
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*caps)); print("seg", rep.objective)
+w = G.assignment_reference(96, 100, 5); rep, m = fmb.solve_assignment(w); print("assign", rep.objective)
+net = fmb.build_network([(0, 1, 3), (0, 2, 2), (1, 3, 2), (2, 3, 3), (1, 2, 1)], 4, 0, 3); print("csr", fmb.hybrid_solve(net).objective)
+from paper_1110_6231_b200 import bands as B
+flow, cut, st = B.solve_virtual_bands(G.grid_random(100, 70, 9), 3); print("bands", flow)
