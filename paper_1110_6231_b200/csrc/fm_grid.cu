@@ -1484,6 +1484,8 @@ struct RingQ {
     unsigned int *ctr;      // [0] head, [32] tail, [64] pending, [96] tile visits that changed a border (one line each)
     int32_t cap;
     int32_t rerun;          // a tile found stale again while in flight: 1 rerun at once, 0 requeue
+    int32_t *vis;           // per tile: visits in this launch (incremental re-visits, BFS ring)
+    int32_t incr;           // 1: a re-visit only propagates halo improvements (env FM_BFS_INCR)
     int32_t ns0, ns1;       // idle-poll backoff (ns)
 };
 
@@ -1491,6 +1493,7 @@ struct RingQ {
 __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, const int32_t *count0) {
     const int n0 = count0 ? __ldcg(count0) : ntiles;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < q.cap; i += gridDim.x * blockDim.x) {
+        if (q.vis && i < ntiles) q.vis[i] = 0;
         if (i < n0) {
             const int t = count0 ? list0[i] : i;
             q.slot[i] = t;
@@ -1572,8 +1575,60 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
         const int orr = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + last_c) : INF;        // own right column
         const int gv0 = (g0 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g0) * g.W + cl) : INF;
         const int gv1 = (g1 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g1) * g.W + cl) : INF;
+        uint32_t seen = 0;
+        const bool incr = q.incr && g0 < 0 && g1 < 0 && __ldcg(q.vis + tile) > 0;
+        if (incr) {
+        // Re-visit: the previous visit left a fixpoint for the halos it saw, and halos
+        // only fall, so only pixels that a now-shorter halo path improves change.  Load
+        // the current distances, seed the border pixels whose halo now gives a shorter
+        // path, and run the level loop from there keeping only improved pixels.
+        for (int i = 0; i < PT_H; i++)
+            sd[i * (PT_W + 1) + lane] = (r0 + i < g.H && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + i) * g.W + cl) : INF;
+        __syncwarp();
+        const uint32_t mU0 = __shfl_sync(0xffffffffu, mU, 0), mD31 = __shfl_sync(0xffffffffu, mD, PT_H - 1);
+        // smallest halo value >= lo whose path improves a border pixel (INF: none)
+        const auto next_seed = [&](int lo) -> int {
+            int m = INF;
+            if (ht >= lo && ht < INF && ((mU0 >> lane) & 1u) && ht + 1 < sd[lane]) m = min(m, ht);
+            if (hb >= lo && hb < INF && ((mD31 >> lane) & 1u) && hb + 1 < sd[(PT_H - 1) * (PT_W + 1) + lane]) m = min(m, hb);
+            if (hl >= lo && hl < INF && (mL & 1u) && hl + 1 < sd[lane * (PT_W + 1)]) m = min(m, hl);
+            if (hr >= lo && hr < INF && (mR & 0x80000000u) && hr + 1 < sd[lane * (PT_W + 1) + PT_W - 1]) m = min(m, hr);
+            return warp_min_i32(m);
+        };
+        int L = next_seed(0);
+        uint32_t F = 0;
+        while (L < INF) {
+            const uint32_t tb = __ballot_sync(0xffffffffu, ht == L);
+            const uint32_t bb = __ballot_sync(0xffffffffu, hb == L);
+            uint32_t up = __shfl_up_sync(0xffffffffu, F, 1);
+            uint32_t dn = __shfl_down_sync(0xffffffffu, F, 1);
+            if (lane == 0) up = tb;
+            if (lane == 31) dn = bb;
+            uint32_t N = ((F >> 1) & mR) | ((F << 1) & mL) | (dn & mD) | (up & mU);
+            if (hr == L) N |= mR & 0x80000000u;
+            if (hl == L) N |= mL & 1u;
+            uint32_t K = 0;   // the pixels level L+1 improves (own row: no cross-lane hazard)
+            for (uint32_t x = N; x; x &= x - 1) {
+                const int b = __ffs(x) - 1;
+                int32_t *d = &sd[lane * (PT_W + 1) + b];
+                if (L + 1 < *d) { *d = L + 1; K |= 1u << b; }
+            }
+            seen |= K;
+            F = K;
+            L++;
+#ifdef FM_BFS_TIMING
+            lv++;
+#endif
+            if (!__any_sync(0xffffffffu, F != 0)) {
+                __syncwarp();
+                L = next_seed(L);
+            }
+        }
+        __syncwarp();
+        } else {
         // level-synchronous BFS; sd[row][col] = level at which the pixel was reached
-        uint32_t F = mT, seen = mT;
+        uint32_t F = mT;
+        seen = mT;
         for (uint32_t x = mT; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = 1;
         int L = 1;
 #ifdef FM_BFS_TIMING
@@ -1622,6 +1677,7 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
 #ifdef FM_BFS_TIMING
         if (lane == 0) atomicAdd((unsigned long long *)(q.ctr + 246), (unsigned long long)(clock64() - tl0));
 #endif
+        }   // from-scratch visit
         // write back every reached pixel (lane = column); borders compared with the old values
         const uint32_t any_seen = __ballot_sync(0xffffffffu, seen != 0);
         bool ct = false, cb = false;
@@ -1659,6 +1715,7 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
         }
         __syncwarp();   // the pushes (pending++) precede lane 0's pending-- below
         if (lane == 0) {
+            if (q.vis) q.vis[tile] += 1;
             if (any_chg) atomicAdd(q.ctr + 96, 1u);
 #ifdef FM_BFS_TIMING
             atomicAdd(q.ctr + 192, 1u);   // every visit (diagnostics)
@@ -3002,6 +3059,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
     if (const char *v = getenv("FM_PR_GRAPH")) g->pr_graph = atoi(v);
     if (const char *v = getenv("FM_PACKED")) g->pk = atoi(v);
+    g->rq.incr = 1;
+    if (const char *v = getenv("FM_BFS_INCR")) g->rq.incr = atoi(v) ? 1 : 0;
     g->d.solo_max = 32;
     g->d.k_solo = 0;
     if (const char *v = getenv("FM_K_SOLO")) g->d.k_solo = atoi(v);
@@ -3089,7 +3148,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->prq.rerun = 0; g->prq.ns0 = g->rq.ns0; g->prq.ns1 = g->rq.ns1;
     if (cudaMalloc((void **)&g->rq.slot, sizeof(int32_t) * (size_t)g->rq.cap) != cudaSuccess ||
         cudaMalloc((void **)&g->prq.slot, sizeof(int32_t) * (size_t)g->prq.cap) != cudaSuccess ||
-        cudaMemset(g->rq.flag, 0, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess) {
+        cudaMemset(g->rq.flag, 0, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
+        cudaMalloc((void **)&g->rq.vis, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess) {
         fm_set_error("fm_grid_create: allocation failed");
         fm_grid_destroy(g);
         return FM_CUDA_ERROR;
@@ -3110,6 +3170,7 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->d.rbits) cudaFree(g->d.rbits);
     if (g->rq.slot) cudaFree(g->rq.slot);
     if (g->rq.flag) cudaFree(g->rq.flag);
+    if (g->rq.vis) cudaFree(g->rq.vis);
     if (g->rq.ctr) cudaFree(g->rq.ctr);
     if (g->prq.slot) cudaFree(g->prq.slot);
     if (g->prq.flag) cudaFree(g->prq.flag);

@@ -37,6 +37,9 @@ VARIANTS = {
     "three_hop": {"FM_TWO_HOP": "2"},
     "pr_graph": {"FM_PR_GRAPH": "1"},
     "unpacked": {"FM_PACKED": "0"},
+    "bfs_from_scratch": {"FM_BFS_INCR": "0"},
+    "bfs_incremental_rerun": {"FM_BFS_INCR": "1", "FM_BR_RERUN": "1"},
+    "bfs_incremental_no_local": {"FM_BFS_INCR": "1", "FM_LOCAL_DIV": "0"},
     "pr_graph_b1": {"FM_PR_GRAPH": "1", "FM_PR_BATCH": "1"},
 }
 
