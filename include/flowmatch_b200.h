@@ -34,8 +34,9 @@
  * t = H*W + 1) with antiparallel pairs merged; value and minimal cut are equal.
  *
  * Status codes (Python mirror maps 1 -> InfeasibleInstanceError, 2 -> ValueError,
- * 3/4 -> RuntimeError, as the reference raises at assign_scaling.py:44-45,
- * maxflow_par.py:168-173, maxflow_par.py:213-214).
+ * 3/4 -> RuntimeError, 5 -> AssertionError, as the reference raises at
+ * assign_scaling.py:44-45, maxflow_par.py:168-173, maxflow_par.py:213-214,
+ * assign_par.py:101-106,200-214).
  */
 #ifndef FLOWMATCH_B200_H
 #define FLOWMATCH_B200_H
@@ -51,6 +52,7 @@ extern "C" {
 #define FM_INVALID_ARG 2
 #define FM_CUDA_ERROR 3
 #define FM_NO_DEVICE 4
+#define FM_VALIDATION 5   /* validate=True invariant violated (the reference raises AssertionError) */
 
 /* grid solve flags */
 #define FM_GRID_CANCEL_VIOLATIONS 0x1 /* run the maxflow_par.py:132-154 pass each round */
@@ -103,6 +105,10 @@ typedef struct fm_grid fm_grid;
 
 int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **out);
 void fm_grid_destroy(fm_grid *g);
+/* Kernel-variant and tuning options (DESIGN.md section 4 switch table, lower-case
+ * names, e.g. "pr_kernel", "bfs_bits", "packed").  The library reads no environment
+ * variables; options apply from the next solve.  Unknown name -> FM_INVALID_ARG. */
+int fm_grid_set_option(fm_grid *g, const char *name, int64_t value);
 
 /* Whole solve on device.  cap* are DEVICE pointers (borrowed for the call).
  * cycle_budget = max lock-free sweeps per coordinator round (reference
@@ -192,6 +198,10 @@ typedef struct fm_assign fm_assign;
 
 int fm_assign_create(int32_t n, int32_t device, fm_assign **out);
 void fm_assign_destroy(fm_assign *a);
+/* Options: "heuristic_every_k" (a price update every k refine rounds,
+ * assign_par.py:228-234; 0 = off), and tuning switches "ybatch_min", "pu_ring",
+ * "pu_threshold", "tail_threshold", "pu_cap". */
+int fm_assign_set_option(fm_assign *a, const char *name, int64_t value);
 
 /* Dense max-weight perfect matching.  weights: DEVICE int32[n*n] row-major,
  * weights[x*n+y] = w(x, y) or FM_ABSENT_WEIGHT.  alpha >= 2 (DEFAULT_ALPHA 10,
@@ -225,6 +235,44 @@ int fm_assign_begin(fm_assign *a, const int32_t *weights, int64_t alpha, int32_t
 int fm_assign_refine(fm_assign *a, int64_t *eps_out, int32_t *done_out);
 int fm_assign_state(fm_assign *a, int64_t *prices, int32_t *match, uint32_t *fixed,
                     int64_t *objective_out, fm_stats *stats);
+
+/* Stateful refine on a caller's ScalingState (assign_scaling.py:102-142), one
+ * coordinator step per call, so refine_par (assign_par.py:115-237) and min_cost_loop
+ * (assign_scaling.py:400-467) keep their observer / on_refine_end hooks and their
+ * in-place state semantics.  All buffers HOST.
+ *   load: weights n*n (NULL = keep the loaded matrix), epsilon, scale (arc cost
+ *         c(x,y) = -scale * w(x,y); <= 0 means n + 1, the reduce_to_mincost scale),
+ *         bound (scaled_cost_bound, < 0 = max |c|), prices 2n (X then Y),
+ *         match n (match[x] = y carrying x's unit or -1), fixed n*ceil(n/32) words
+ *         (bit y of row x = pair (x, y) fixed).  Y excesses follow from match.
+ *   begin_refine: assign_scaling.py:145-182 (epsilon shrink, unfrozen flow dropped,
+ *         X prices reset), no push.
+ *   round: one coordinator round: every active X gets an op, then up to cycle_budget
+ *         Y/X phase pairs; out = {pushes, relabels, phase pairs, active nodes left}.
+ *   price_update: assign_scaling.py:208-276 (no-op without active nodes).
+ *   arc_fix: assign_scaling.py:185-205; *fixed_pairs = pairs newly fixed.
+ *   export: current prices / match / fixed / Y excess / epsilon (any NULL). */
+int fm_assign_load(fm_assign *a, const int32_t *weights, int64_t alpha, int32_t flags, int64_t epsilon,
+                   int64_t scale, int64_t bound, const int64_t *prices, const int32_t *match,
+                   const uint32_t *fixed);
+int fm_assign_begin_refine(fm_assign *a, int64_t *eps_out);
+int fm_assign_round(fm_assign *a, int32_t cycle_budget, int64_t *out);
+int fm_assign_price_update(fm_assign *a);
+int fm_assign_arc_fix(fm_assign *a, int64_t *fixed_pairs);
+int fm_assign_export(fm_assign *a, int64_t *prices, int32_t *match, uint32_t *fixed, int32_t *y_excess,
+                     int64_t *eps_out);
+
+/* Exact optimality certificate of a matching, independent of the solver (CLI
+ * verify; replaces the reference's brute-force oracle check, cli.py:157-188, for any
+ * n): *certified = 1 when match (HOST, n) is a perfect matching over present pairs
+ * whose residual graph has no negative cycle (Bellman-Ford from a virtual source,
+ * <= 2n + 2 passes; prices HOST 2n potentials at cost scale `scale` speed it up, or
+ * NULL), 0 when a negative cycle proves it suboptimal, -1 when it is not a perfect
+ * matching.  weights HOST, or DEVICE when weights_on_device.  Overwrites the handle's
+ * solve state. */
+int fm_assign_certify(fm_assign *a, const int32_t *weights, int32_t weights_on_device, const int32_t *match,
+                      const int64_t *prices, int64_t scale, int32_t *certified, int64_t *objective_out,
+                      int32_t *passes_out);
 
 #ifdef __cplusplus
 }

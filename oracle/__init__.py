@@ -73,7 +73,7 @@ def lib():
                              _c.c_int64, _c.c_int64, _c.c_int32, _c.c_int64, _i64p,
                              _i32p, _c.c_void_p]
     L.fmo_assign.restype = _c.c_int
-    L.fmo_assign_certify_dense.argtypes = [_c.c_int32, _i32p, _i32p, _i64p, _i64p]
+    L.fmo_assign_certify_dense.argtypes = [_c.c_int32, _i32p, _i32p, _c.c_void_p, _i64p]
     L.fmo_assign_certify_dense.restype = _c.c_int
     _lib = L
     return L
@@ -233,11 +233,14 @@ def assign(n, edges=None, matrix=None, mode="seq", alpha=10, cycle_budget=500000
                 rounds=int(out[3]), matching=match.tolist(), prices=price)
 
 
-def assign_certify_dense(w, matching, prices):
-    """0 = matching is a permutation and 1-optimal under the (n+1)-scaled costs."""
+def assign_certify_dense(w, matching, prices=None):
+    """EXACT certificate: 0 = perfect matching with no negative residual cycle (proven
+    maximum weight), 1 = not a perfect matching of present pairs, 2 = a negative cycle
+    (suboptimal).  prices (2n, scale n + 1) only speed up the Bellman-Ford passes."""
     w = np.ascontiguousarray(w, dtype=np.int32)
     n = w.shape[0]
-    out = np.zeros(1, np.int64)
+    out = np.zeros(2, np.int64)
+    p = None if prices is None else np.ascontiguousarray(prices, dtype=np.int64)
     code = lib().fmo_assign_certify_dense(n, w, np.ascontiguousarray(matching, dtype=np.int32),
-                                          np.ascontiguousarray(prices, dtype=np.int64), out)
+                                          p.ctypes.data if p is not None else None, out)
     return int(code), int(out[0])

@@ -17,6 +17,17 @@ from .assign import (
     AssignmentInstance,
     AssignmentSolver,
     InfeasibleInstanceError,
+    OpCounters,
+    ScalingState,
+    arc_fix,
+    begin_refine,
+    extract_matching,
+    make_scaling_state,
+    min_cost_loop,
+    price_update_heuristic,
+    reduce_to_mincost,
+    refine_par,
+    refine_seq,
     solve_assignment,
 )
 from .cli import cli_main
@@ -35,15 +46,34 @@ from .graph import (
     FlowNetwork,
     GridNetwork,
     NetworkError,
+    ResidualState,
     SolveReport,
     build_grid_network,
     build_network,
+    is_epsilon_optimal,
+    part_reduced_cost,
+    reduced_cost,
 )
 from .maxflow import DEFAULT_CYCLE_BUDGET, GridSolver, hybrid_solve, min_cut
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "OpCounters",
+    "ResidualState",
+    "ScalingState",
+    "arc_fix",
+    "begin_refine",
+    "extract_matching",
+    "is_epsilon_optimal",
+    "make_scaling_state",
+    "min_cost_loop",
+    "part_reduced_cost",
+    "price_update_heuristic",
+    "reduce_to_mincost",
+    "reduced_cost",
+    "refine_par",
+    "refine_seq",
     "AssignmentInstance",
     "AssignmentSolver",
     "DEFAULT_ALPHA",

@@ -6,10 +6,12 @@ visible, calls raise instead of falling back to anything on the CPU.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import subprocess
 import threading
+from collections import OrderedDict
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfm_b200.so")
@@ -19,6 +21,7 @@ FM_INFEASIBLE = 1
 FM_INVALID_ARG = 2
 FM_CUDA_ERROR = 3
 FM_NO_DEVICE = 4
+FM_VALIDATION = 5
 
 FM_GRID_CANCEL_VIOLATIONS = 0x1
 FM_GRID_NO_PRECANCEL = 0x2
@@ -102,6 +105,15 @@ SIGNATURES = {
     "fm_assign_begin": (ctypes.c_int, [_vp, _vp, _i64, _i32]),
     "fm_assign_refine": (ctypes.c_int, [_vp, _vp, _vp]),
     "fm_assign_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "fm_grid_set_option": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64]),
+    "fm_assign_set_option": (ctypes.c_int, [_vp, ctypes.c_char_p, _i64]),
+    "fm_assign_load": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "fm_assign_begin_refine": (ctypes.c_int, [_vp, _vp]),
+    "fm_assign_round": (ctypes.c_int, [_vp, _i32, _vp]),
+    "fm_assign_price_update": (ctypes.c_int, [_vp]),
+    "fm_assign_arc_fix": (ctypes.c_int, [_vp, _vp]),
+    "fm_assign_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "fm_assign_certify": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _i64, _vp, _vp, _vp]),
 }
 
 _lib = None
@@ -154,6 +166,8 @@ def check(rc: int, what: str) -> None:
         raise InfeasibleInstanceError(msg)
     if rc == FM_INVALID_ARG:
         raise ValueError(msg)
+    if rc == FM_VALIDATION:
+        raise AssertionError(msg)
     raise RuntimeError(msg)
 
 
@@ -171,3 +185,47 @@ def ptr(a) -> int:
     if hasattr(a, "data_ptr"):
         return int(a.data_ptr())
     return int(a.ctypes.data)
+
+
+class SolverCache:
+    """Device workspaces reused across calls, keyed by (shape..., device).
+
+    Each workspace carries a lock held for the whole solve: ctypes releases the
+    GIL during the foreign call, so two threads must never drive one handle at
+    once; a caller that finds it held gets a private workspace instead.  At most `per_device` workspaces stay cached per device; an evicted
+    workspace is only dropped from the cache, never closed here -- a thread still
+    solving on it holds a reference, and the handle is freed (its __del__) when
+    the last reference goes.
+    """
+
+    def __init__(self, per_device: int = 1):
+        self.per_device = per_device
+        self._d: OrderedDict = OrderedDict()
+        self._lock = threading.Lock()
+
+    @contextlib.contextmanager
+    def use(self, key, device: int, factory):
+        with self._lock:
+            ent = self._d.get(key)
+            if ent is None:
+                same = [k for k, v in self._d.items() if v[2] == device]
+                for k in same[: max(0, len(same) - self.per_device + 1)]:
+                    self._d.pop(k)
+                ent = self._d[key] = (factory(), threading.Lock(), device)
+            else:
+                self._d.move_to_end(key)
+            solver, lk, _ = ent
+        if not lk.acquire(blocking=False):
+            # busy (another thread, or a hook of this thread's own solve that calls back
+            # in): a private workspace keeps the two solves apart, like the reference's
+            # fresh state per call
+            yield factory()
+            return
+        try:
+            yield solver
+        finally:
+            lk.release()
+
+    def clear(self) -> None:
+        with self._lock:
+            self._d.clear()

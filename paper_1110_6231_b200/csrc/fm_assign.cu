@@ -25,6 +25,8 @@
 // grid-wide barriers; the long single-digit tail drops to one CTA with CTA barriers.
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <climits>
+#include <vector>
 #include <string.h>
 #include <stdlib.h>
 
@@ -44,8 +46,8 @@ constexpr int LINF = 0x3fffffff;         // "unlabelled" in the price update
 
 // cnt[] slots
 constexpr int C_X0 = 0, C_Y0 = 2;        // X / Y list counts (double-buffered)
-constexpr int C_INFEASIBLE = 4;          // 1 no residual arc, 2 inconsistent, 3 budget
-constexpr int C_EXIT = 5;                // rounds kernel exit: 0 done, 1 price update due
+constexpr int C_INFEASIBLE = 4;          // 1 no residual arc, 2 inconsistent, 3 budget, 4/5/6 validation
+constexpr int C_EXIT = 5;                // rounds kernel exit: 0 done, 1 price update due, 2 round cap
 constexpr int C_ROUND = 6;               // next round index (persists across launches)
 constexpr int C_RELABELS = 7;            // relabels since the last price update
 constexpr int C_PU_CHG = 8;              // price update: changed flags [8], [9]
@@ -56,6 +58,11 @@ constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXE
               O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7, O_TAIL_NS = 8, O_MULTI_NS = 9,
               O_PH_Y = 10, O_PH_SYNC1 = 11, O_PH_X = 12, O_PH_SYNC2 = 13,  // multi-round phase ns (CTA 0)
               O_PU_YS = 14, O_PU_ITNS = 15;  // price update: frontier Y visits, ns in BF iterations (CTA 0)
+
+// validate=True failures (assign_par.py:101-106,200-214; assign_scaling.py:274-275,333-336)
+constexpr int V_RELABEL = 4;             // a relabel failed to lower a price
+constexpr int V_OWNER = 5;               // a price word written by two ops in one phase
+constexpr int V_RAISE = 6;               // the price update would raise a price
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -84,7 +91,19 @@ struct AssignDev {
     int32_t pu_cap0;       // first label cap of the price update (0 = 8)
     int use_fix;
     int ybatch_min;         // gathered Y op: rank-batch the push-back from this many units (env FM_YBATCH_MIN)
+    int validate;          // validate=True: device-side invariant checks (codes V_*)
+    int32_t *pw;           // validate: last phase tag that wrote each price word (X then Y)
+    int32_t vbase;         // validate: tag base of this launch (phase tag = vbase + 2 r + 1|2)
 };
+
+// validate=True: a price write must lower the price and be the only write of its word
+// in this phase (owner-only writes, assign_par.py:101-106,200-214)
+__device__ __forceinline__ void check_price_write(const AssignDev &a, int node, long long oldp, long long newp,
+                                                  int tag) {
+    if (!a.validate) return;
+    if (newp >= oldp) atomicExch(a.cnt + C_INFEASIBLE, V_RELABEL);
+    if (tag && atomicExch(a.pw + node, tag) == tag) atomicExch(a.cnt + C_INFEASIBLE, V_OWNER);
+}
 
 
 // (value, index) min with the lower index winning ties (first arc in the
@@ -217,7 +236,7 @@ __device__ __forceinline__ void ycand_partial(const AssignDev &a, int y, int t, 
 // the cheapest arc is not admissible, then push the unit on it.
 template <bool CTA_WIDE>
 __device__ void x_op(const AssignDev &a, int x, int32_t *ylist_next, int32_t *ycnt_next,
-                     unsigned long long &pushes, unsigned long long &relabels) {
+                     unsigned long long &pushes, unsigned long long &relabels, int tag = 0) {
     long long best = I64_MAX;
     int y = INT32_MAX;
     const int t = CTA_WIDE ? threadIdx.x : (threadIdx.x & 31);
@@ -229,6 +248,7 @@ __device__ void x_op(const AssignDev &a, int x, int32_t *ylist_next, int32_t *yc
             atomicExch(a.cnt + C_INFEASIBLE, 1);  // active node with no residual arc
         } else {
             if (!(best < -px)) {                 // not admissible: p(x) <- -(best + eps)
+                check_price_write(a, x, px, -(best + a.eps), tag);
                 a.px[x] = -(best + a.eps);
                 relabels++;
                 atomicAdd(a.cnt + C_RELABELS, 1);
@@ -253,7 +273,7 @@ constexpr int YBUCKET = 256;            // per-Y bucket slots for long Y lists (
 
 template <bool CTA_WIDE>
 __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
-                     unsigned long long &pushes, unsigned long long &relabels, long long *sbuf) {
+                     unsigned long long &pushes, unsigned long long &relabels, long long *sbuf, int tag = 0) {
     __shared__ long long s_cv[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
     __shared__ int s_cx[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
     __shared__ int s_cn[CTA_WIDE ? 1 : AWARPS];
@@ -265,6 +285,7 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
     int *cx = s_cx[slot];
     int ey = __ldcg(a.ey + y);
     long long py = __ldcg((const long long *)a.py + y);
+    const long long py0 = py;
     if (ey <= 0) return;
     // ---- gather
     if (t == 0) s_cn[slot] = 0;
@@ -313,7 +334,10 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
                 break;
             }
             if (t == 0) {
-                if (!(bv < -py)) { py = -(bv + a.eps); relabels++; atomicAdd(a.cnt + C_RELABELS, 1); }
+                if (!(bv < -py)) {
+                    if (a.validate && -(bv + a.eps) >= py) atomicExch(a.cnt + C_INFEASIBLE, V_RELABEL);
+                    py = -(bv + a.eps); relabels++; atomicAdd(a.cnt + C_RELABELS, 1);
+                }
                 a.match[bi] = -1;
                 xlist_next[atomicAdd(xcnt_next, 1)] = bi;
                 pushes++;
@@ -351,7 +375,10 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
             unsigned long long rl = 0;
             for (int k = 0; k < ey; k++) {
                 const long long vk = sbuf[k];
-                if (!(vk < -py)) { py = -(vk + a.eps); rl++; }
+                if (!(vk < -py)) {
+                    if (a.validate && -(vk + a.eps) >= py) atomicExch(a.cnt + C_INFEASIBLE, V_RELABEL);
+                    py = -(vk + a.eps); rl++;
+                }
             }
             relabels += rl;
             pushes += ey;
@@ -374,7 +401,10 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
             }
             if (bi == i2 && bk >= 0) cv[bk] = I64_MAX;   // the owner lane retires the slot
             if (t == 0) {
-                if (!(v2 < -py)) { py = -(v2 + a.eps); relabels++; atomicAdd(a.cnt + C_RELABELS, 1); }
+                if (!(v2 < -py)) {
+                    if (a.validate && -(v2 + a.eps) >= py) atomicExch(a.cnt + C_INFEASIBLE, V_RELABEL);
+                    py = -(v2 + a.eps); relabels++; atomicAdd(a.cnt + C_RELABELS, 1);
+                }
                 a.match[i2] = -1;
                 xlist_next[atomicAdd(xcnt_next, 1)] = i2;
                 pushes++;
@@ -384,6 +414,8 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
         }
     }
     if (t == 0) {
+        if (py != py0 && a.validate && tag && atomicExch(a.pw + a.n + y, tag) == tag)
+            atomicExch(a.cnt + C_INFEASIBLE, V_OWNER);
         a.py[y] = py;
         a.ey[y] = ey;
     }
@@ -403,7 +435,7 @@ constexpr int YB_CAP = 32 * YB_PER_LANE;
 __device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, int cnt,
                              const long long (&v)[YB_PER_LANE], const int (&xs)[YB_PER_LANE],
                              long long *s_sorted, int32_t *xlist_next, int32_t *xcnt_next,
-                             unsigned long long &pushes, unsigned long long &relabels) {
+                             unsigned long long &pushes, unsigned long long &relabels, int tag) {
     const int lane = threadIdx.x & 31;
     int rank[YB_PER_LANE];
 #pragma unroll
@@ -440,6 +472,8 @@ __device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, in
         relabels += rl;
         pushes += ey;
         if (rl) atomicAdd(a.cnt + C_RELABELS, (int)rl);
+        if (rl && a.validate && tag && atomicExch(a.pw + a.n + y, tag) == tag)
+            atomicExch(a.cnt + C_INFEASIBLE, V_OWNER);
         a.py[y] = py;
         a.ey[y] = 0;
     }
@@ -451,12 +485,12 @@ __device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, in
 // collected once per phase into ybuf[y*YCAP ..]; one warp per y.
 __device__ void y_op_bucketed(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
                               unsigned long long &pushes, unsigned long long &relabels,
-                              long long *s_sorted) {
+                              long long *s_sorted, int tag) {
     const int lane = threadIdx.x & 31;
     const int cnt = __ldcg(a.ybcnt + y);
     const int ey = __ldcg(a.ey + y);
     if (cnt > YBUCKET || ey >= cnt) {       // bucket overflow (or inconsistent): scan match[] instead
-        y_op<false>(a, y, xlist_next, xcnt_next, pushes, relabels, s_sorted);
+        y_op<false>(a, y, xlist_next, xcnt_next, pushes, relabels, s_sorted, tag);
         if (lane == 0) a.ybcnt[y] = 0;
         __syncwarp();
         return;
@@ -476,7 +510,7 @@ __device__ void y_op_bucketed(const AssignDev &a, int y, int32_t *xlist_next, in
             v[k] = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale - __ldcg((const long long *)a.px + x);
         }
     }
-    if (ey > 0) y_batch_warp(a, y, ey, py, cnt, v, xs, s_sorted, xlist_next, xcnt_next, pushes, relabels);
+    if (ey > 0) y_batch_warp(a, y, ey, py, cnt, v, xs, s_sorted, xlist_next, xcnt_next, pushes, relabels, tag);
     if (lane == 0) a.ybcnt[y] = 0;
     __syncwarp();
 }
@@ -484,7 +518,9 @@ __device__ void y_op_bucketed(const AssignDev &a, int y, int32_t *xlist_next, in
 // begin_refine (assign_scaling.py:145-182) fused with the first X phase: drop
 // unfrozen flow, set p(x) = -(min part-reduced cost + eps) and push x's unit on
 // that arc (admissible at reduced cost -eps by construction).
-__global__ void __launch_bounds__(ATHREADS) begin_refine_kernel(AssignDev a) {
+// push = 0: the preamble alone (the stepwise begin_refine); unfrozen X are left
+// unmatched and active for the first round.
+__global__ void __launch_bounds__(ATHREADS) begin_refine_kernel(AssignDev a, int push) {
     const int warp = (blockIdx.x * ATHREADS + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * ATHREADS) >> 5;
     const int lane = threadIdx.x & 31;
@@ -496,7 +532,9 @@ __global__ void __launch_bounds__(ATHREADS) begin_refine_kernel(AssignDev a) {
         warp_argmin(best, y);
         if (lane == 0) {
             if (y != INT32_MAX) a.px[x] = -(best + a.eps);
-            if (!a.frozen[x]) {
+            if (!a.frozen[x] && !push) {
+                a.match[x] = -1;
+            } else if (!a.frozen[x]) {
                 if (y == INT32_MAX) {
                     a.match[x] = -1;
                     atomicExch(a.cnt + C_INFEASIBLE, 1);
@@ -543,7 +581,8 @@ __device__ __forceinline__ void cta_bcast3(const int32_t *p0, const int32_t *p1,
 // CTA-wide ops and CTA barriers (the long single-digit tail).
 __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, int tail_threshold,
                                                                  long long round_budget,
-                                                                 int pu_threshold) {
+                                                                 int pu_threshold, int max_rounds,
+                                                                 int pu_every_k) {
     cg::grid_group grid = cg::this_grid();
     const int lane = threadIdx.x & 31;
     const int gwarp = (blockIdx.x * ATHREADS + threadIdx.x) >> 5;
@@ -571,6 +610,16 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 1;
             break;
         }
+        // heuristic_every_k (assign_par.py:228-234): a price update every k rounds
+        if (pu_every_k > 0 && rounds > 0 && r % pu_every_k == 0) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 1;
+            break;
+        }
+        // coordinator round cap (cycle_budget rounds per coordinator round)
+        if (max_rounds > 0 && (long long)rounds >= max_rounds) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 2;
+            break;
+        }
         if (r >= round_budget) {  // prices diverge: no perfect matching (assign_par.py:221-226)
             if (blockIdx.x == 0 && threadIdx.x == 0) { atomicExch(a.cnt + C_INFEASIBLE, 3); a.cnt[C_EXIT] = 0; }
             break;
@@ -581,6 +630,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
         }
         rounds++;
         if (tail) tail_rounds++;
+        const int tag_y = a.vbase + 2 * r + 1, tag_x = tag_y + 1;   // validate: phase tags
         // ---- Y phase
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.cnt[C_X0 + nb] = 0;   // X list of round r+1 (last read in round r-1)
@@ -590,20 +640,20 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             const unsigned long long p0 = pushes + relabels;
             if (ny <= 2) {
                 for (int i = 0; i < ny; i++)
-                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0]);
+                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0], tag_y);
             } else {
                 for (int i = cwarp; i < ny; i += AWARPS)
-                    y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[cwarp]);
+                    y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[cwarp], tag_y);
             }
             __threadfence_block();
             __syncthreads();
             const int nx = __ldcg(a.cnt + C_X0 + b);
             if (nx <= 2) {
                 for (int i = 0; i < nx; i++)
-                    x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+                    x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
             } else {
                 for (int i = cwarp; i < nx; i += AWARPS)
-                    x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+                    x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
             }
             __threadfence_block();
             __syncthreads();
@@ -615,7 +665,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             unsigned long long t0 = timer ? globaltimer() : 0, t1 = 0;
             if (ny <= (int)gridDim.x) {
                 for (int i = blockIdx.x; i < ny; i += gridDim.x)
-                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0]);
+                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0], tag_y);
             } else {
                 // long list: bucket every incoming X by its Y in one pass over match[]
                 const int gtid = blockIdx.x * ATHREADS + threadIdx.x, gthr = gridDim.x * ATHREADS;
@@ -628,7 +678,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
                 grid.sync();
                 for (int i = gwarp; i < ny; i += gwarps)
                     y_op_bucketed(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels,
-                                  s_sorted[threadIdx.x >> 5]);
+                                  s_sorted[threadIdx.x >> 5], tag_y);
             }
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_Y, t1 - t0); t0 = t1; }
             grid.sync();
@@ -637,10 +687,10 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             cta_bcast3(a.cnt + C_X0 + b, nullptr, nullptr, nx, u1, u2);
             if (nx <= (int)gridDim.x) {
                 for (int i = blockIdx.x; i < nx; i += gridDim.x)
-                    x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+                    x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
             } else {
                 for (int i = gwarp; i < nx; i += gwarps)
-                    x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels);
+                    x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
             }
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_X, t1 - t0); t0 = t1; }
             grid.sync();
@@ -956,8 +1006,10 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     }  // cap loop
     const long long K = min((long long)__ldcg(a.cnt + C_PU_LAST), (long long)a.max_bucket) + 1;
     for (int v = tid; v < n; v += nthr) {
-        a.px[v] -= a.eps * min((long long)a.lx[v], K);
-        a.py[v] -= a.eps * min((long long)a.ly[v], K);
+        const long long dx = min((long long)a.lx[v], K), dy = min((long long)a.ly[v], K);
+        if (a.validate && (dx < 0 || dy < 0)) atomicExch(a.cnt + C_INFEASIBLE, V_RAISE);
+        a.px[v] -= a.eps * dx;
+        a.py[v] -= a.eps * dy;
     }
     if (tid == 0) {
         a.cnt[C_RELABELS] = 0;
@@ -1061,6 +1113,102 @@ __global__ void weight_bound_kernel(const int32_t *w, int64_t nn, unsigned long 
     }
 }
 
+// Loaded state (a reference ScalingState copied in): frozen[x] = x's matched arc is
+// fixed, frozen_in[y] = frozen matches into y, ey[y] = (#matched into y) - 1.
+__global__ void load_state_kernel(AssignDev a) {
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.n; x += gridDim.x * blockDim.x) {
+        const int y = a.match[x];
+        const bool fz = y >= 0 && ((a.fixed[(size_t)x * a.nw + (y >> 5)] >> (y & 31)) & 1u);
+        a.frozen[x] = fz ? 1 : 0;
+        if (y >= 0) {
+            atomicAdd(a.ey + y, 1);
+            if (fz) atomicAdd(a.frozen_in + y, 1);
+        }
+    }
+}
+
+// Coordinator round start (stepwise refine): list every active X (unmatched) in
+// xlist[0] and every Y holding excess in ylist[0]; the round counter restarts at 0.
+__global__ void active_lists_kernel(AssignDev a) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < a.n; v += gridDim.x * blockDim.x) {
+        if (a.match[v] < 0) a.xlist[0][atomicAdd(a.cnt + C_X0, 1)] = v;
+        if (a.ey[v] > 0) a.ylist[0][atomicAdd(a.cnt + C_Y0, 1)] = v;
+    }
+}
+
+// X phase over xlist[0] (the active X of a loaded / freshly begun refine): relabel
+// if needed, then push the unit, appending Y that become active to ylist[0].
+__global__ void __launch_bounds__(ATHREADS) x_phase_kernel(AssignDev a, int tag) {
+    const int warp = (blockIdx.x * ATHREADS + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * ATHREADS) >> 5;
+    const int nx = __ldcg(a.cnt + C_X0);
+    unsigned long long pushes = 0, relabels = 0;
+    for (int i = warp; i < nx; i += nwarps)
+        x_op<false>(a, __ldcg(a.xlist[0] + i), a.ylist[0], a.cnt + C_Y0, pushes, relabels, tag);
+    if ((threadIdx.x & 31) == 0) {
+        if (pushes) atomicAdd(a.ops + O_PUSH, pushes);
+        if (relabels) atomicAdd(a.ops + O_RELABEL, relabels);
+    }
+}
+
+// ---- exact optimality certificate (no negative residual cycle)
+// A perfect matching M is a maximum-weight matching iff the residual graph of M
+// (forward arcs x->y for every present, unmatched pair; reverse arcs y->x for the
+// matched pairs) has no negative cycle under the arc costs -w (scaled by any s > 0).
+// Shortest distances from a virtual source joined to every node by 0-cost arcs then
+// exist, and Bellman-Ford reaches them within 2n passes; a pass that still changes
+// a distance after 2n passes proves a negative cycle.  Reduced costs under the
+// solver's final prices make the distances start near their fixpoint (every arc is
+// >= -eps at the end of the last refine), so a few passes usually settle it.  Every
+// present arc counts, fixed or not: the certificate is independent of the solver.
+__global__ void certify_init_kernel(const int32_t *w, const int32_t *match, int n, long long *dx, long long *dy,
+                                    int32_t *bad /* not a perfect matching of present pairs */, int32_t *ycount) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        dx[v] = 0; dy[v] = 0;
+        const int y = match[v];
+        if (y < 0 || y >= n || w[(size_t)v * n + y] == FM_ABSENT_WEIGHT) atomicExch(bad, 1);
+        else if (atomicAdd(ycount + y, 1) != 0) atomicExch(bad, 1);
+    }
+}
+
+// forward pass: d(y) <- min(d(y), d(x) + c_p(x, y)) over present unmatched pairs; one
+// warp per row, coalesced row reads, an atomicMin only where a distance drops
+__global__ void certify_forward_kernel(const int32_t *w, const int32_t *match, const long long *px,
+                                       const long long *py, long long scale, int n, const long long *dx,
+                                       long long *dy, int32_t *changed) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    int chg = 0;
+    for (int x = warp; x < n; x += nwarps) {
+        const long long base = __ldcg(dx + x) + (px ? __ldg(px + x) : 0);
+        const int mx = __ldg(match + x);
+        const int32_t *row = w + (size_t)x * n;
+        for (int y = lane; y < n; y += 32) {
+            const int wv = __ldg(row + y);
+            if (wv == FM_ABSENT_WEIGHT || y == mx) continue;
+            const long long cand = base - (long long)wv * scale - (py ? __ldg(py + y) : 0);
+            if (cand < __ldcg(dy + y)) {
+                const long long old = atomicMin((long long *)dy + y, cand);
+                chg |= cand < old;
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, chg) && lane == 0) atomicExch(changed, 1);
+}
+
+// reverse pass: d(x) <- min(d(x), d(M(x)) + c_p(M(x) -> x)), c_p of the reverse arc
+// = -c_p(x, M(x))
+__global__ void certify_reverse_kernel(const int32_t *w, const int32_t *match, const long long *px,
+                                       const long long *py, long long scale, int n, long long *dx,
+                                       const long long *dy, int32_t *changed) {
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        const int y = match[x];
+        const long long rc = -(long long)w[(size_t)x * n + y] * scale + (px ? px[x] : 0) - (py ? py[y] : 0);
+        const long long cand = dy[y] - rc;
+        if (cand < dx[x]) { dx[x] = cand; atomicExch(changed, 1); }
+    }
+}
+
 __global__ void objective_kernel(const int32_t *w, const int32_t *match, int n,
                                  unsigned long long *out) {
     long long s = 0;
@@ -1091,7 +1239,9 @@ struct fm_assign {
     bool pu_pending = false;
     // solve state (also drives the stepwise API)
     long long alpha = 10, bound = 0, eps = 1, round_budget = 0;
-    int pu_threshold = 0, tail_threshold = 1;
+    int pu_threshold = 0, tail_threshold = 1, pu_every_k = 0;
+    // options (fm_assign_set_option; round-1 environment knobs)
+    int opt_ybatch_min = 2, opt_pu_ring = 1, opt_pu_threshold = -1, opt_tail_threshold = 1, opt_pu_cap = 256;
     int32_t flags = 0;
     fm_stats st{};
 };
@@ -1103,9 +1253,11 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     const int n = A->n;
     AssignDev &d = A->d;
     d.w = w;
+    d.scale = (int64_t)n + 1;
     d.use_fix = (flags & FM_ASSIGN_ARC_FIX) ? 1 : 0;
-    d.ybatch_min = 2;
-    if (const char *v = getenv("FM_YBATCH_MIN")) d.ybatch_min = std::max(1, atoi(v));
+    d.validate = (flags & FM_ASSIGN_VALIDATE) ? 1 : 0;
+    d.vbase = 0;
+    d.ybatch_min = std::max(1, A->opt_ybatch_min);
     A->alpha = alpha;
     A->flags = flags;
     memset(&A->st, 0, sizeof(A->st));
@@ -1121,6 +1273,7 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     FM_CHECK_CUDA(cudaMemsetAsync(d.fixed_t, 0, sizeof(uint32_t) * (size_t)n * d.nw, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * 16, s));
     FM_CHECK_CUDA(cudaMemsetAsync(A->acc, 0, sizeof(unsigned long long) * 4, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(d.pw, 0, sizeof(int32_t) * 2 * (size_t)n, s));
     weight_bound_kernel<<<A->sms * 4, 256, 0, s>>>(w, (int64_t)n * n, A->acc);
     FM_CHECK_LAUNCH();
     A->st.launches++;
@@ -1131,8 +1284,7 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
         FM_CHECK_CUDA(cudaMemsetAsync(A->pu.cnt, 0, sizeof(int32_t) * 4, s));
         // > queued entries (<= n) + groups waiting on a slot (pu_blocks * PU_GROUPS)
         A->pu.ring_cap = n + std::min(PU_RING_EXTRA, A->pu_blocks * PU_GROUPS + 64);
-        A->pu.ring_on = 1;
-        if (const char *v = getenv("FM_PU_RING")) A->pu.ring_on = atoi(v) ? 1 : 0;
+        A->pu.ring_on = A->opt_pu_ring ? 1 : 0;
         if (A->pu.ring_on) {
             FM_CHECK_CUDA(cudaMemsetAsync(A->pu.ring, 0xff, sizeof(int32_t) * ((size_t)n + PU_RING_EXTRA), s));
             FM_CHECK_CUDA(cudaMemsetAsync(A->pu.rctr, 0, sizeof(unsigned int) * 96, s));
@@ -1146,13 +1298,25 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     const double budget_d = std::max(1e4, 40.0 * n * (double)n * std::max<double>(1.0, (double)A->h_acc[2]));
     A->round_budget = budget_d > 4e18 ? (long long)4e18 : (long long)budget_d;
     A->eps = std::max(1LL, A->bound);
-    A->pu_threshold = (flags & FM_ASSIGN_PRICE_UPDATE) ? std::max(64, n / 16) : 0;
-    if (const char *v = getenv("FM_PU_THRESHOLD")) if (A->pu_threshold) A->pu_threshold = atoi(v);
-    A->tail_threshold = 1;
-    if (const char *v = getenv("FM_TAIL_THRESHOLD")) A->tail_threshold = atoi(v);
-    d.pu_cap0 = 256;
-    if (const char *v = getenv("FM_PU_CAP")) d.pu_cap0 = atoi(v);
+    A->pu_threshold = (flags & FM_ASSIGN_PRICE_UPDATE)
+                          ? (A->opt_pu_threshold >= 0 ? A->opt_pu_threshold : std::max(64, n / 16)) : 0;
+    A->tail_threshold = A->opt_tail_threshold;
+    d.pu_cap0 = A->opt_pu_cap;
     return FM_OK;
+}
+
+// C_INFEASIBLE word -> status code and message
+int assign_status(int why) {
+    switch (why) {
+    case 0: return FM_OK;
+    case 1: fm_set_error("active node has no residual arc: instance admits no perfect matching"); return FM_INFEASIBLE;
+    case 3: fm_set_error("operation budget exceeded; prices diverge, instance admits no perfect matching");
+            return FM_INFEASIBLE;
+    case V_RELABEL: fm_set_error("validate: relabel failed to lower a price"); return FM_VALIDATION;
+    case V_OWNER: fm_set_error("validate: price word written by two ops in one phase"); return FM_VALIDATION;
+    case V_RAISE: fm_set_error("validate: price update would raise a price"); return FM_VALIDATION;
+    default: fm_set_error("inconsistent Y excess during refine"); return FM_CUDA_ERROR;
+    }
 }
 
 // one refine (assign_scaling.py:145-182 + assign_par.py:115-237): eps <- max(1, ceil(eps/alpha)),
@@ -1168,11 +1332,15 @@ int assign_one_refine(fm_assign *A) {
     FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * C_COUNT, s));
     reset_excess_kernel<<<(n + 255) / 256, 256, 0, s>>>(d);
     FM_CHECK_LAUNCH();
-    begin_refine_kernel<<<std::max(1, std::min((n + AWARPS - 1) / AWARPS, A->sms * 4)), ATHREADS, 0, s>>>(d);
+    begin_refine_kernel<<<std::max(1, std::min((n + AWARPS - 1) / AWARPS, A->sms * 4)), ATHREADS, 0, s>>>(d, 1);
     FM_CHECK_LAUNCH();
     A->st.launches += 2;
     for (;;) {
-        void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold};
+        int no_cap = 0;
+        int every_k = (A->flags & FM_ASSIGN_PRICE_UPDATE) ? A->pu_every_k : 0;
+        d.vbase += 1 << 21;   // fresh validate phase tags per launch
+        void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold,
+                        (void *)&no_cap, (void *)&every_k};
         FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
                                                   dim3(ATHREADS), args, 0, s));
         A->st.launches++;
@@ -1203,14 +1371,7 @@ int assign_one_refine(fm_assign *A) {
         A->st.launches++;
     }
     A->st.refines++;
-    if (A->h_cnt[C_INFEASIBLE]) {
-        const int why = A->h_cnt[C_INFEASIBLE];
-        fm_set_error(why == 1 ? "active node has no residual arc: instance admits no perfect matching"
-                     : why == 3 ? "operation budget exceeded; prices diverge, instance admits no perfect matching"
-                                : "inconsistent Y excess during refine");
-        return why == 2 ? FM_CUDA_ERROR : FM_INFEASIBLE;
-    }
-    return FM_OK;
+    return assign_status(A->h_cnt[C_INFEASIBLE]);
 }
 
 // objective, counters and host copies (assign_scaling.py:456-466)
@@ -1315,6 +1476,7 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMemset(A->pu.ring, 0xff, sizeof(int32_t) * ((size_t)n + PU_RING_EXTRA)) == cudaSuccess &&
               cudaMemset(A->pu.rctr, 0, sizeof(unsigned int) * 96) == cudaSuccess &&
               cudaMalloc((void **)&d.ly, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&d.pw, sizeof(int32_t) * 2 * (size_t)n) == cudaSuccess &&
               cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * 16) == cudaSuccess &&
               cudaMalloc((void **)&A->acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
               cudaMallocHost((void **)&A->h_ops, sizeof(unsigned long long) * 16) == cudaSuccess &&
@@ -1344,7 +1506,7 @@ extern "C" void fm_assign_destroy(fm_assign *A) {
     cudaSetDevice(A->device);
     void *dev[] = {A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.fixed_t, A->d.frozen, A->d.frozen_in,
                    A->d.xlist[0], A->d.xlist[1], A->d.ylist[0], A->d.ylist[1], A->d.cnt, A->d.ops,
-                   A->d.lx, A->d.ly, A->d.ybcnt, A->d.ybuf, A->wt, A->pu.fy[0], A->pu.fy[1], A->pu.fx[0], A->pu.fx[1],
+                   A->d.lx, A->d.ly, A->d.pw, A->d.ybcnt, A->d.ybuf, A->wt, A->pu.fy[0], A->pu.fy[1], A->pu.fx[0], A->pu.fx[1],
                    A->pu.in_fx, A->pu.in_fy, A->pu.cnt, A->pu.ring, A->pu.rctr,
                    A->acc, A->in_w};
     for (void *p : dev) if (p) cudaFree(p);
@@ -1432,4 +1594,303 @@ extern "C" int fm_assign_state(fm_assign *A, int64_t *prices, int32_t *match, ui
     FM_TRY(assign_finish(A, FM_OK, objective_out, match, prices));
     if (stats) *stats = A->st;
     return FM_OK;
+}
+
+// ---- stateful API: a reference ScalingState (assign_scaling.py:102-142) loaded onto the
+// device, then begin_refine / refine_par rounds / price update / arc fixing as separate
+// coordinator steps (refine_par, assign_par.py:115-237; min_cost_loop, :400-467).
+namespace {
+
+int assign_sync_cnt(fm_assign *A) {
+    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, A->d.cnt, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, A->stream));
+    FM_CHECK_CUDA(cudaStreamSynchronize(A->stream));
+    return FM_OK;
+}
+
+int assign_ops(fm_assign *A, unsigned long long *out16) {
+    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_ops, A->d.ops, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost,
+                                  A->stream));
+    FM_CHECK_CUDA(cudaStreamSynchronize(A->stream));
+    memcpy(out16, A->h_ops, sizeof(unsigned long long) * 16);
+    return FM_OK;
+}
+
+}  // namespace
+
+extern "C" int fm_assign_load(fm_assign *A, const int32_t *weights, int64_t alpha, int32_t flags, int64_t eps,
+                              int64_t scale, int64_t bound, const int64_t *prices, const int32_t *match,
+                              const uint32_t *fixed) {
+    if (!A || alpha < 2 || eps < 1 || !prices || !match || !fixed) {
+        fm_set_error("fm_assign_load: invalid argument");
+        return FM_INVALID_ARG;
+    }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    A->stream = A->own_stream;
+    const int n = A->n;
+    for (int x = 0; x < n; x++)
+        if (match[x] < -1 || match[x] >= n) {
+            fm_set_error("fm_assign_load: match[%d] = %d out of range", x, match[x]);
+            return FM_INVALID_ARG;
+        }
+    const size_t bytes = sizeof(int32_t) * (size_t)n * n;
+    if (!A->in_w) {
+        if (!weights) { fm_set_error("fm_assign_load: no weight matrix loaded yet"); return FM_INVALID_ARG; }
+        FM_CHECK_CUDA(cudaMalloc((void **)&A->in_w, bytes));
+    }
+    cudaStream_t s = A->stream;
+    if (weights) FM_CHECK_CUDA(cudaMemcpyAsync(A->in_w, weights, bytes, cudaMemcpyHostToDevice, s));
+    FM_TRY(assign_setup(A, A->in_w, alpha, flags));
+    AssignDev &d = A->d;
+    // arc cost c(x, y) = -scale * w(x, y): scale n + 1 for reduce_to_mincost networks,
+    // 1 for a caller-built network whose costs are not multiples of n + 1
+    if (scale > 0) {
+        A->bound = A->bound / ((long long)n + 1) * scale;
+        d.scale = scale;
+    }
+    if (bound >= 0) A->bound = bound;   // the state's scaled_cost_bound
+    FM_CHECK_CUDA(cudaMemcpyAsync(d.px, prices, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    FM_CHECK_CUDA(cudaMemcpyAsync(d.py, prices + n, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    FM_CHECK_CUDA(cudaMemcpyAsync(d.match, match, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    FM_CHECK_CUDA(cudaMemcpyAsync(d.fixed, fixed, sizeof(uint32_t) * (size_t)n * d.nw, cudaMemcpyHostToDevice, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(d.ey, 0xff, sizeof(int32_t) * n, s));   // supplies: -1 per Y
+    load_state_kernel<<<std::max(1, std::min((n + 255) / 256, A->sms * 2)), 256, 0, s>>>(d);
+    FM_CHECK_LAUNCH();
+    bit_transpose_kernel<<<std::max(1, std::min((d.nw * d.nw + 7) / 8, A->sms * 8)), 256, 0, s>>>(
+        d.fixed, d.fixed_t, n, d.nw);
+    FM_CHECK_LAUNCH();
+    A->st.launches += 2;
+    A->eps = eps;
+    d.eps = eps;
+    d.max_bucket = std::min<long long>(A->bound / eps + 2, LINF - 1);
+    FM_CHECK_CUDA(cudaStreamSynchronize(s));
+    return FM_OK;
+}
+
+extern "C" int fm_assign_begin_refine(fm_assign *A, int64_t *eps_out) {
+    if (!A || !A->in_w) { fm_set_error("fm_assign_begin_refine: no state loaded"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    const int n = A->n;
+    AssignDev &d = A->d;
+    cudaStream_t s = A->stream;
+    A->eps = std::max(1LL, (A->eps + A->alpha - 1) / A->alpha);   // -(-eps // alpha)
+    d.eps = A->eps;
+    d.max_bucket = std::min<long long>(A->bound / A->eps + 2, LINF - 1);
+    FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * C_COUNT, s));
+    reset_excess_kernel<<<(n + 255) / 256, 256, 0, s>>>(d);
+    FM_CHECK_LAUNCH();
+    begin_refine_kernel<<<std::max(1, std::min((n + AWARPS - 1) / AWARPS, A->sms * 4)), ATHREADS, 0, s>>>(d, 0);
+    FM_CHECK_LAUNCH();
+    A->st.launches += 2;
+    FM_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (eps_out) *eps_out = A->eps;
+    return FM_OK;
+}
+
+// One coordinator round of refine_par: every active X gets an op, then up to
+// cycle_budget Y/X phase pairs (with price updates when the relabel budget asks; the
+// every-k schedule is the caller's, at coordinator points).
+// out = {pushes, relabels, rounds, active nodes left}.
+extern "C" int fm_assign_round(fm_assign *A, int32_t cycle_budget, int64_t *out) {
+    if (!A || !A->in_w || cycle_budget < 1 || !out) {
+        fm_set_error("fm_assign_round: invalid argument or no state loaded");
+        return FM_INVALID_ARG;
+    }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    const int n = A->n;
+    AssignDev &d = A->d;
+    cudaStream_t s = A->stream;
+    unsigned long long o0[16], o1[16];
+    FM_TRY(assign_ops(A, o0));
+    FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * C_COUNT, s));
+    active_lists_kernel<<<std::max(1, std::min((n + 255) / 256, A->sms * 2)), 256, 0, s>>>(d);
+    FM_CHECK_LAUNCH();
+    d.vbase += 1 << 21;
+    x_phase_kernel<<<std::max(1, std::min((n + AWARPS - 1) / AWARPS, A->sms * 4)), ATHREADS, 0, s>>>(d, d.vbase);
+    FM_CHECK_LAUNCH();
+    FM_CHECK_CUDA(cudaMemsetAsync(d.cnt + C_X0, 0, sizeof(int32_t), s));
+    A->st.launches += 2;
+    FM_TRY(assign_sync_cnt(A));
+    int rc = assign_status(A->h_cnt[C_INFEASIBLE]);
+    while (rc == FM_OK) {
+        const int done = A->h_cnt[C_ROUND];
+        int cap = cycle_budget - done;
+        if (cap <= 0) break;
+        d.vbase += 1 << 21;
+        int every_k = 0;
+        void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold,
+                        (void *)&cap, (void *)&every_k};
+        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
+                                                  dim3(ATHREADS), args, 0, s));
+        A->st.launches++;
+        FM_TRY(assign_sync_cnt(A));
+        rc = assign_status(A->h_cnt[C_INFEASIBLE]);
+        if (rc != FM_OK || A->h_cnt[C_EXIT] != 1) break;
+        void *pargs[] = {(void *)&d, (void *)&A->pu};
+        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->pu_blocks),
+                                                  dim3(ATHREADS), pargs, 0, s));
+        A->st.launches++;
+        FM_TRY(assign_sync_cnt(A));
+        rc = assign_status(A->h_cnt[C_INFEASIBLE]);
+    }
+    FM_TRY(assign_ops(A, o1));
+    const int r = A->h_cnt[C_ROUND];
+    out[0] = (int64_t)(o1[O_PUSH] - o0[O_PUSH]);
+    out[1] = (int64_t)(o1[O_RELABEL] - o0[O_RELABEL]);
+    out[2] = r;
+    out[3] = A->h_cnt[C_Y0 + (r & 1)];
+    return rc;
+}
+
+// price_update_heuristic (assign_scaling.py:208-276) at a coordinator point; a no-op
+// without active nodes (then there are no deficit nodes either: excesses sum to 0)
+extern "C" int fm_assign_price_update(fm_assign *A) {
+    if (!A || !A->in_w) { fm_set_error("fm_assign_price_update: no state loaded"); return FM_INVALID_ARG; }
+    if (!(A->flags & FM_ASSIGN_PRICE_UPDATE)) {
+        fm_set_error("fm_assign_price_update: state loaded without FM_ASSIGN_PRICE_UPDATE");
+        return FM_INVALID_ARG;
+    }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    const int n = A->n;
+    AssignDev &d = A->d;
+    cudaStream_t s = A->stream;
+    FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * C_COUNT, s));
+    active_lists_kernel<<<std::max(1, std::min((n + 255) / 256, A->sms * 2)), 256, 0, s>>>(d);
+    FM_CHECK_LAUNCH();
+    A->st.launches++;
+    FM_TRY(assign_sync_cnt(A));
+    if (A->h_cnt[C_X0] + A->h_cnt[C_Y0] == 0) return FM_OK;
+    void *pargs[] = {(void *)&d, (void *)&A->pu};
+    FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->pu_blocks), dim3(ATHREADS),
+                                              pargs, 0, s));
+    A->st.launches++;
+    FM_TRY(assign_sync_cnt(A));
+    return assign_status(A->h_cnt[C_INFEASIBLE]);
+}
+
+extern "C" int fm_assign_arc_fix(fm_assign *A, int64_t *fixed_pairs) {
+    if (!A || !A->in_w) { fm_set_error("fm_assign_arc_fix: no state loaded"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    const int n = A->n;
+    AssignDev &d = A->d;
+    cudaStream_t s = A->stream;
+    unsigned long long o0[16], o1[16];
+    FM_TRY(assign_ops(A, o0));
+    const int use_fix = d.use_fix;
+    d.use_fix = 1;
+    arc_fix_kernel<<<std::max(1, std::min((n + 7) / 8, A->sms * 8)), 256, 0, s>>>(d);
+    FM_CHECK_LAUNCH();
+    d.use_fix = use_fix;
+    bit_transpose_kernel<<<std::max(1, std::min((d.nw * d.nw + 7) / 8, A->sms * 8)), 256, 0, s>>>(
+        d.fixed, d.fixed_t, n, d.nw);
+    FM_CHECK_LAUNCH();
+    A->st.launches += 2;
+    FM_TRY(assign_ops(A, o1));
+    if (fixed_pairs) *fixed_pairs = (int64_t)(o1[O_FIXED] - o0[O_FIXED]);
+    return FM_OK;
+}
+
+// current state to HOST buffers (any may be NULL): prices 2n (X then Y), match n,
+// fixed n * ceil(n/32) words, Y excess n, epsilon
+extern "C" int fm_assign_export(fm_assign *A, int64_t *prices, int32_t *match, uint32_t *fixed, int32_t *ey,
+                                int64_t *eps_out) {
+    if (!A || !A->in_w) { fm_set_error("fm_assign_export: no state loaded"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    const int n = A->n;
+    AssignDev &d = A->d;
+    cudaStream_t s = A->stream;
+    if (prices) {
+        FM_CHECK_CUDA(cudaMemcpyAsync(prices, d.px, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+        FM_CHECK_CUDA(cudaMemcpyAsync(prices + n, d.py, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, s));
+    }
+    if (match) FM_CHECK_CUDA(cudaMemcpyAsync(match, d.match, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    if (fixed) FM_CHECK_CUDA(cudaMemcpyAsync(fixed, d.fixed, sizeof(uint32_t) * (size_t)n * d.nw,
+                                             cudaMemcpyDeviceToHost, s));
+    if (ey) FM_CHECK_CUDA(cudaMemcpyAsync(ey, d.ey, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    FM_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (eps_out) *eps_out = A->eps;
+    return FM_OK;
+}
+
+// Options (replace the round-1 environment knobs); take effect at the next solve /
+// load.  heuristic_every_k: a price update every k refine rounds (assign_par.py:228-234).
+extern "C" int fm_assign_set_option(fm_assign *A, const char *name, int64_t value) {
+    if (!A || !name) { fm_set_error("fm_assign_set_option: invalid argument"); return FM_INVALID_ARG; }
+    const int v = (int)std::max<int64_t>(INT32_MIN, std::min<int64_t>(INT32_MAX, value));
+    if (!strcmp(name, "heuristic_every_k")) A->pu_every_k = std::max(0, v);
+    else if (!strcmp(name, "ybatch_min")) A->opt_ybatch_min = std::max(1, v);
+    else if (!strcmp(name, "pu_ring")) A->opt_pu_ring = v;
+    else if (!strcmp(name, "pu_threshold")) A->opt_pu_threshold = v;
+    else if (!strcmp(name, "tail_threshold")) A->opt_tail_threshold = v;
+    else if (!strcmp(name, "pu_cap")) A->opt_pu_cap = v;
+    else { fm_set_error("fm_assign_set_option: unknown option '%s'", name); return FM_INVALID_ARG; }
+    return FM_OK;
+}
+
+// Exact optimality certificate of a matching (CLI verify, tests): *certified = 1 when
+// `match` is a perfect matching over present pairs with no negative residual cycle
+// (proven maximum weight), 0 when a negative cycle exists, -1 when it is not a
+// perfect matching.  weights HOST (copied in) or DEVICE (weights_on_device = 1);
+// match HOST; prices HOST 2n (X then Y, any scale-s potentials, or NULL).
+extern "C" int fm_assign_certify(fm_assign *A, const int32_t *weights, int32_t weights_on_device,
+                                 const int32_t *match, const int64_t *prices, int64_t scale,
+                                 int32_t *certified, int64_t *objective_out, int32_t *passes_out) {
+    if (!A || !weights || !match || !certified) { fm_set_error("fm_assign_certify: invalid argument"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(A->device));
+    const int n = A->n;
+    cudaStream_t s = A->own_stream;
+    const size_t bytes = sizeof(int32_t) * (size_t)n * n;
+    const int32_t *w = weights;
+    if (!weights_on_device) {
+        if (!A->in_w) FM_CHECK_CUDA(cudaMalloc((void **)&A->in_w, bytes));
+        FM_CHECK_CUDA(cudaMemcpyAsync(A->in_w, weights, bytes, cudaMemcpyHostToDevice, s));
+        w = A->in_w;
+    }
+    if (scale <= 0) scale = (int64_t)n + 1;
+    // scratch: the price-update label arrays and frontier buffers are free between solves
+    AssignDev &d = A->d;
+    long long *dx = (long long *)d.px, *dy = (long long *)d.py;   // overwritten: state of the last solve is gone
+    long long *ppx = nullptr, *ppy = nullptr;
+    int32_t *m = d.match, *ycount = d.ey, *flags = d.cnt;
+    long long *pbuf = nullptr;
+    if (prices) {
+        FM_CHECK_CUDA(cudaMalloc((void **)&pbuf, sizeof(long long) * 2 * (size_t)n));
+        FM_CHECK_CUDA(cudaMemcpyAsync(pbuf, prices, sizeof(long long) * 2 * (size_t)n, cudaMemcpyHostToDevice, s));
+        ppx = pbuf; ppy = pbuf + n;
+    }
+    FM_CHECK_CUDA(cudaMemcpyAsync(m, match, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(ycount, 0, sizeof(int32_t) * n, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * C_COUNT, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(A->acc, 0, sizeof(unsigned long long) * 4, s));
+    const int gb = std::max(1, std::min((n + 255) / 256, A->sms * 2));
+    certify_init_kernel<<<gb, 256, 0, s>>>(w, m, n, dx, dy, flags + 0, ycount);
+    FM_CHECK_LAUNCH();
+    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, flags, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, s));
+    FM_CHECK_CUDA(cudaStreamSynchronize(s));
+    int rc = FM_OK;
+    *certified = -1;
+    int passes = 0;
+    if (!A->h_cnt[0]) {
+        // every matched pair must be present
+        objective_kernel<<<gb, 256, 0, s>>>(w, m, n, A->acc + 1);
+        FM_CHECK_LAUNCH();
+        const int fb = std::max(1, std::min((n + 7) / 8, A->sms * 8));
+        bool converged = false;
+        for (passes = 1; passes <= 2 * n + 2; passes++) {
+            FM_CHECK_CUDA(cudaMemsetAsync(flags + 1, 0, sizeof(int32_t), s));
+            certify_forward_kernel<<<fb, 256, 0, s>>>(w, m, ppx, ppy, scale, n, dx, dy, flags + 1);
+            FM_CHECK_LAUNCH();
+            certify_reverse_kernel<<<gb, 256, 0, s>>>(w, m, ppx, ppy, scale, n, dx, dy, flags + 1);
+            FM_CHECK_LAUNCH();
+            FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, flags, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, s));
+            FM_CHECK_CUDA(cudaStreamSynchronize(s));
+            if (!A->h_cnt[1]) { converged = true; break; }
+        }
+        *certified = converged ? 1 : 0;
+        FM_CHECK_CUDA(cudaMemcpyAsync(A->h_acc, A->acc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
+        FM_CHECK_CUDA(cudaStreamSynchronize(s));
+        if (objective_out) *objective_out = (int64_t)A->h_acc[1];
+    }
+    if (pbuf) cudaFree(pbuf);
+    if (passes_out) *passes_out = passes;
+    return rc;
 }

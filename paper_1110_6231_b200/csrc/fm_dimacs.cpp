@@ -8,6 +8,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -45,7 +47,9 @@ bool to_int(const Tok &t, long long *v) {
     long long x = 0;
     for (; i < t.n; i++) {
         if (t.p[i] < '0' || t.p[i] > '9') return false;
-        x = x * 10 + (t.p[i] - '0');
+        const int d = t.p[i] - '0';
+        if (x > (INT64_MAX - d) / 10) return false;   // does not fit in int64
+        x = x * 10 + d;
     }
     *v = neg ? -x : x;
     return true;
@@ -86,8 +90,9 @@ int problem_line(Tok *t, int k, long long lineno, const char *expected, bool see
 
 // out_nst = {node_count, source, sink}; *out_m = arcs.  tails/heads/caps may be null
 // (count only) or hold at least *out_m (from a previous call) entries.
-extern "C" int fm_dimacs_parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
-                                   int32_t *tails, int32_t *heads, int32_t *caps, int64_t cap_arcs) {
+namespace {
+int parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
+              int32_t *tails, int32_t *heads, int32_t *caps, int64_t cap_arcs) {
     if (!text || len < 0 || !out_nst || !out_m) PERR("fm_dimacs_parse_max: invalid argument");
     long long n = -1, declared = 0, source = -1, sink = -1, m = 0;
     const char *p = text, *end = text + len;
@@ -147,14 +152,28 @@ extern "C" int fm_dimacs_parse_max(const char *text, int64_t len, int32_t *out_n
                                     (long long)cap_arcs, m);
     return FM_OK;
 }
+}  // namespace
+
+extern "C" int fm_dimacs_parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
+                                   int32_t *tails, int32_t *heads, int32_t *caps, int64_t cap_arcs) {
+    try {
+        return parse_max(text, len, out_nst, out_m, tails, heads, caps, cap_arcs);
+    } catch (const std::bad_alloc &) {
+        PERR("fm_dimacs_parse_max: out of memory");
+    } catch (...) {
+        PERR("fm_dimacs_parse_max: internal error");
+    }
+}
 
 // Assignment: out_nm = {n (per side)}; *out_m = edges; xs/ys/ws in file order with
 // X / Y ids mapped to 0..n-1 in sorted order (dimacs.py:187-248).
-extern "C" int fm_dimacs_parse_asn(const char *text, int64_t len, int32_t *out_n, int64_t *out_m,
-                                   int32_t *xs, int32_t *ys, int64_t *ws, int64_t cap_edges) {
+namespace {
+
+int parse_asn(const char *text, int64_t len, int32_t *out_n, int64_t *out_m,
+              int32_t *xs, int32_t *ys, int64_t *ws, int64_t cap_edges) {
     if (!text || len < 0 || !out_n || !out_m) PERR("fm_dimacs_parse_asn: invalid argument");
     long long n = -1, declared = 0;
-    std::vector<uint8_t> is_x;
+    std::vector<long long> xmarks;   // designated X ids (no O(n) allocation from the header)
     struct E { long long u, v, w, line; };
     std::vector<E> raw;
     const char *p = text, *end = text + len;
@@ -170,7 +189,6 @@ extern "C" int fm_dimacs_parse_asn(const char *text, int64_t len, int32_t *out_n
         const std::string tag = t[0].str();
         if (tag == "p") {
             if (problem_line(t, k, lineno, "asn", n >= 0, &n, &declared)) return FM_INVALID_ARG;
-            is_x.assign((size_t)n, 0);
             continue;
         }
         if (n < 0) PERR("line %lld: '%s' line before problem line", lineno, tag.c_str());
@@ -178,7 +196,7 @@ extern "C" int fm_dimacs_parse_asn(const char *text, int64_t len, int32_t *out_n
             if (k != 2) PERR("line %lld: malformed node designator", lineno);
             long long node;
             if (node_tok(t[1], lineno, n, &node)) return FM_INVALID_ARG;
-            is_x[(size_t)node] = 1;
+            xmarks.push_back(node);
         } else if (tag == "a") {
             if (k != 4) PERR("line %lld: malformed edge line", lineno);
             long long u, v, w;
@@ -190,37 +208,65 @@ extern "C" int fm_dimacs_parse_asn(const char *text, int64_t len, int32_t *out_n
         }
     }
     if (n < 0) PERR("missing problem line");
-    std::vector<long long> xi((size_t)n, -1), yi((size_t)n, -1);
-    long long nx = 0, ny = 0;
-    for (long long v = 0; v < n; v++) {
-        if (is_x[(size_t)v]) xi[(size_t)v] = nx++; else yi[(size_t)v] = ny++;
-    }
+    std::sort(xmarks.begin(), xmarks.end());
+    xmarks.erase(std::unique(xmarks.begin(), xmarks.end()), xmarks.end());
+    const long long nx = (long long)xmarks.size(), ny = n - nx;
     if (nx != ny)
         PERR("X side has %lld nodes, Y side has %lld: sides must be the same size", nx, ny);
     if ((long long)raw.size() != declared)
         PERR("edge count mismatch: problem line declares %lld, file has %lld", declared, (long long)raw.size());
     if (nx < 1) PERR("n must be at least 1, got 0");
+    if (nx > INT32_MAX) PERR("n = %lld exceeds int32", nx);
     *out_n = (int32_t)nx;
     *out_m = (int64_t)raw.size();
     if (!xs) return FM_OK;
     if (cap_edges < (int64_t)raw.size()) PERR("fm_dimacs_parse_asn: arrays too small");
-    std::vector<uint8_t> seen;
-    const bool dedup = nx <= 46340;   // n*n bitmap fits comfortably
-    if (dedup) seen.assign((size_t)(nx * nx), 0);
+    // X ids map to their rank among the designated ids, Y ids to their rank among the
+    // rest (dimacs.py:231-247); every same-side edge is reported before duplicates
+    // (the reference maps all edges, then AssignmentInstance.build checks them)
+    const auto xrank = [&](long long v) -> long long {
+        const auto it = std::lower_bound(xmarks.begin(), xmarks.end(), v);
+        return (it != xmarks.end() && *it == v) ? (long long)(it - xmarks.begin()) : -1;
+    };
+    const auto yrank = [&](long long v) -> long long {
+        return v - (long long)(std::lower_bound(xmarks.begin(), xmarks.end(), v) - xmarks.begin());
+    };
+    std::vector<unsigned long long> key(raw.size());
     for (size_t i = 0; i < raw.size(); i++) {
         const E &e = raw[i];
         long long x, y;
-        if (xi[(size_t)e.u] >= 0 && yi[(size_t)e.v] >= 0) { x = xi[(size_t)e.u]; y = yi[(size_t)e.v]; }
-        else if (yi[(size_t)e.u] >= 0 && xi[(size_t)e.v] >= 0) { x = xi[(size_t)e.v]; y = yi[(size_t)e.u]; }
+        const long long xu = xrank(e.u), xv = xrank(e.v);
+        if (xu >= 0 && xv < 0) { x = xu; y = yrank(e.v); }
+        else if (xu < 0 && xv >= 0) { x = xv; y = yrank(e.u); }
         else PERR("line %lld: edge endpoints on the same side", e.line);
-        if (dedup) {
-            uint8_t &s = seen[(size_t)(x * nx + y)];
-            if (s) PERR("duplicate edge (%lld,%lld)", x, y);
-            s = 1;
-        }
         xs[i] = (int32_t)x;
         ys[i] = (int32_t)y;
         ws[i] = e.w;
+        key[i] = ((unsigned long long)x << 32) | (unsigned long long)y;
     }
+    // duplicates: the first repeated (x, y) in file order (AssignmentInstance.build)
+    std::vector<uint32_t> order(raw.size());
+    for (size_t i = 0; i < order.size(); i++) order[i] = (uint32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key[a] < key[b]; });
+    size_t first_dup = raw.size();
+    for (size_t j = 1; j < order.size(); j++)
+        if (key[order[j]] == key[order[j - 1]] && (j < 2 || key[order[j - 2]] != key[order[j]]))
+            first_dup = std::min(first_dup, (size_t)order[j]);
+    if (first_dup < raw.size()) PERR("duplicate edge (%d,%d)", xs[first_dup], ys[first_dup]);
     return FM_OK;
+}
+
+}  // namespace
+
+// Assignment: *out_n = nodes per side; *out_m = edges; xs/ys/ws in file order with
+// X / Y ids mapped to 0..n-1 in sorted order (dimacs.py:187-248).
+extern "C" int fm_dimacs_parse_asn(const char *text, int64_t len, int32_t *out_n, int64_t *out_m,
+                                   int32_t *xs, int32_t *ys, int64_t *ws, int64_t cap_edges) {
+    try {
+        return parse_asn(text, len, out_n, out_m, xs, ys, ws, cap_edges);
+    } catch (const std::bad_alloc &) {
+        PERR("fm_dimacs_parse_asn: out of memory");
+    } catch (...) {
+        PERR("fm_dimacs_parse_asn: internal error");
+    }
 }

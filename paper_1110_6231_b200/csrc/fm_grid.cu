@@ -7,6 +7,7 @@
 // (maxflow_seq.py:119-160, maxflow_par.py:220-226), and the minimal source-side
 // cut by a seeded residual reach.  See DESIGN.md.
 #include <algorithm>
+#include <string>
 #include <thread>
 #include <vector>
 #include <climits>
@@ -1485,7 +1486,7 @@ struct RingQ {
     int32_t cap;
     int32_t rerun;          // a tile found stale again while in flight: 1 rerun at once, 0 requeue
     int32_t *vis;           // per tile: visits in this launch (incremental re-visits, BFS ring)
-    int32_t incr;           // 1: a re-visit only propagates halo improvements (env FM_BFS_INCR)
+    int32_t incr;           // 1: a re-visit only propagates halo improvements (option BFS_INCR)
     int32_t ns0, ns1;       // idle-poll backoff (ns)
 };
 
@@ -1720,6 +1721,10 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
 #ifdef FM_BFS_TIMING
             atomicAdd(q.ctr + 192, 1u);   // every visit (diagnostics)
 #endif
+            // release: the warp's distance stores (ordered before lane 0 by the
+            // __syncwarp above) are visible device-wide before the tile can be taken
+            // again -- an incremental re-visit on another SM reads the interior
+            __threadfence();
             st = atomicCAS(q.flag + tile, 2, 0);
             if (st == 3) {
                 if (q.rerun) { atomicExch(q.flag + tile, 2); __threadfence(); }
@@ -2340,40 +2345,40 @@ struct fm_grid {
     int ntiles = 0;                      // 32 x 32 tiles of the tile-resident kernel
     int32_t *d_queues = nullptr;         // push + BFS tile work lists
     int sms = 148;
-    int relabel_div = 0;                 // env FM_RELABEL_DIV
+    int relabel_div = 0;                 // option RELABEL_DIV
     int pq_parity = 0;                   // parity of the next push launch
     int pt_per_sm = 3;                   // resident pr_tile CTAs per SM (occupancy query)
-    int op_steps = 1;                    // operations per pixel per pass (env FM_OP_STEPS)
-    int op_fused = 0;                    // relabel then push in one operation (env FM_OP_FUSED)
-    int vote_mask = 7;                   // CTA activity vote every vote_mask+1 passes (env FM_VOTE)
+    int op_steps = 1;                    // operations per pixel per pass (option OP_STEPS)
+    int op_fused = 0;                    // relabel then push in one operation (option OP_FUSED)
+    int vote_mask = 7;                   // CTA activity vote every vote_mask+1 passes (option VOTE)
     int bfs_bits = 2;                    // 2: persistent bit-parallel BFS (bfs_ring_kernel), 1: bit-parallel
-                                         // sweeps (bfs_bits_kernel), 0: v1 Jacobi sweeps (env FM_BFS_BITS)
+                                         // sweeps (bfs_bits_kernel), 0: v1 Jacobi sweeps (option BFS_BITS)
     int bb_per_sm = 8;                   // resident bfs_bits CTAs per SM (occupancy query)
     int br_per_sm = 8;                   // resident bfs_ring CTAs per SM (occupancy query, <= br_cap)
-    int br_cap = 8;                      // env FM_BR_CAP
+    int br_cap = 8;                      // option BR_CAP
     RingQ rq{};                          // device work queue of the persistent BFS
     RingQ prq{};                         // device work queue of the persistent push round
-    int pr_ring = 0;                     // 1: one persistent pr_ring_kernel launch per round (env FM_PR_RING; experimental, slower)
-    int two_hop = 1;                     // two-hop pre-routing after init (env FM_TWO_HOP)
-    int k_tail = 0;                      // passes per visit in tail rounds (0: k_local) (env FM_K_TAIL)
-    int tail_div = 1024;                 // tail round: active pixels <= H*W / tail_div (env FM_TAIL_DIV)
-    int pr_batch = 4;                    // push launches between host checks of the round triggers (env FM_PR_BATCH)
-    int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (env FM_VISIT_MULT)
+    int pr_ring = 0;                     // 1: one persistent pr_ring_kernel launch per round (option PR_RING; experimental, slower)
+    int two_hop = 1;                     // two-hop pre-routing after init (option TWO_HOP)
+    int k_tail = 0;                      // passes per visit in tail rounds (0: k_local) (option K_TAIL)
+    int tail_div = 1024;                 // tail round: active pixels <= H*W / tail_div (option TAIL_DIV)
+    int pr_batch = 4;                    // push launches between host checks of the round triggers (option PR_BATCH)
+    int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (option VISIT_MULT)
     bool ring_stats_pending = false;
     bool pr_stats_pending = false;
-    int pr_graph = 0;                    // 1: the push round's launch loop runs as a device while-graph (env FM_PR_GRAPH; measured neutral)
+    int pr_graph = 0;                    // 1: the push round's launch loop runs as a device while-graph (option PR_GRAPH; measured neutral)
     cudaGraph_t prg = nullptr;           // that graph, its instance and the launch parameters it was built for
     cudaGraphExec_t prg_exec = nullptr;
     GridDev prg_d{};
     int prg_key[5] = {0, 0, 0, 0, 0};
     bool prg_pending = false;            // round control block read back, consumed after the caller's sync
     bool band_user_stream = false;       // band steps run on a caller stream (fm_grid_band_stream)
-    int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (env FM_PR_KERNEL)
+    int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (option PR_KERNEL)
     int pl_per_sm = 6;                   // resident pr_list CTAs per SM (occupancy query)
     int pk_per_sm = 8;                   // same, packed-residual instance (occupancy query)
-    int pk = 1;                          // packed 16-bit residuals in the push kernel when the input allows (env FM_PACKED)
+    int pk = 1;                          // packed 16-bit residuals in the push kernel when the input allows (option PACKED)
     bool pk_ok = false;                  // this solve's input allows them (every pair sum <= 65535)
-    int k_local_list = 0;                // passes per visit of the list kernel (env FM_K_LOCAL_LIST)
+    int k_local_list = 0;                // passes per visit of the list kernel (option K_LOCAL_LIST)
     int bq_parity = 0;                   // parity of the next BFS / cut sweep
     int32_t *d_band = nullptr;           // band exchange: changed counter
     uint8_t *d_touched = nullptr;        // per tile: pushed into since the last relabel
@@ -2383,8 +2388,9 @@ struct fm_grid {
     int local_max = 12;                  // consecutive local relabels before a global one
     int local_margin = 2;                // region dilation in tiles
     int local_streak = 0;
-    int k_local = 0;                     // tuning overrides (env FM_K_LOCAL / FM_BFS_INTERVAL)
-    int trace = 0;                       // env FM_TRACE=1: one stderr line per round
+    int pl_occ = 6, pk_occ = 8, br_occ = 8;  // occupancy maxima (options may only lower the CTAs per SM)
+    int k_local = 0;                     // tuning overrides (options k_local / bfs_interval)
+    int trace = 0;                       // option TRACE=1: one stderr line per round
     int bfs_interval_env = 0;
     // solve state
     int32_t flags_solve = 0;
@@ -3046,38 +3052,10 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->d.ntx = (W + PT_W - 1) / PT_W;
     g->d.nty = (H + PT_H - 1) / PT_H;
     g->ntiles = g->d.ntx * g->d.nty;
-    if (const char *v = getenv("FM_K_LOCAL")) g->k_local = atoi(v);
-    if (const char *v = getenv("FM_BFS_INTERVAL")) g->bfs_interval_env = atoi(v);
-    if (const char *v = getenv("FM_TRACE")) g->trace = atoi(v);
-    if (const char *v = getenv("FM_RELABEL_DIV")) g->relabel_div = atoi(v);
-    if (const char *v = getenv("FM_OP_STEPS")) g->op_steps = std::max(1, atoi(v));
-    if (const char *v = getenv("FM_OP_FUSED")) g->op_fused = atoi(v);
-    if (const char *v = getenv("FM_VOTE")) g->vote_mask = std::max(1, atoi(v)) - 1;
-    if (const char *v = getenv("FM_PR_KERNEL")) g->pr_kernel = atoi(v);
-    if (const char *v = getenv("FM_BFS_BITS")) g->bfs_bits = atoi(v);
-    if (const char *v = getenv("FM_BR_CAP")) g->br_cap = std::max(1, atoi(v));
-    if (const char *v = getenv("FM_PR_RING")) g->pr_ring = atoi(v);
-    if (const char *v = getenv("FM_PR_GRAPH")) g->pr_graph = atoi(v);
-    if (const char *v = getenv("FM_PACKED")) g->pk = atoi(v);
     g->rq.incr = 1;
-    if (const char *v = getenv("FM_BFS_INCR")) g->rq.incr = atoi(v) ? 1 : 0;
     g->d.solo_max = 32;
     g->d.k_solo = 0;
-    if (const char *v = getenv("FM_K_SOLO")) g->d.k_solo = atoi(v);
-    if (const char *v = getenv("FM_SOLO_MAX")) g->d.solo_max = atoi(v);
-    if (const char *v = getenv("FM_K_TAIL")) g->k_tail = atoi(v);
-    if (const char *v = getenv("FM_TWO_HOP")) g->two_hop = atoi(v);
-    if (const char *v = getenv("FM_TAIL_DIV")) g->tail_div = atoi(v);
-    if (const char *v = getenv("FM_PR_BATCH")) g->pr_batch = std::max(1, std::min(16, atoi(v)));
-    if (const char *v = getenv("FM_VISIT_MULT")) g->visit_mult = std::max(1, atoi(v));
     g->rq.rerun = 0; g->rq.ns0 = 128; g->rq.ns1 = 2048;
-    if (const char *v = getenv("FM_BR_RERUN")) g->rq.rerun = atoi(v);
-    if (const char *v = getenv("FM_BR_NS0")) g->rq.ns0 = atoi(v);
-    if (const char *v = getenv("FM_BR_NS1")) g->rq.ns1 = atoi(v);
-    if (const char *v = getenv("FM_K_LOCAL_LIST")) g->k_local_list = atoi(v);
-    if (const char *v = getenv("FM_LOCAL_DIV")) g->local_div = atoi(v);
-    if (const char *v = getenv("FM_LOCAL_MAX")) g->local_max = atoi(v);
-    if (const char *v = getenv("FM_LOCAL_MARGIN")) g->local_margin = atoi(v);
     const size_t n4 = sizeof(int32_t) * (size_t)g->HW, n1 = (size_t)g->HW;
     int32_t **planes[] = {&g->d.e, &g->d.h, &g->d.rR, &g->d.rL, &g->d.rD, &g->d.rU,
                           &g->d.rT, &g->d.rS, &g->d.cS, &g->d.dist, &g->d.inflow_h, &g->d.inflow_v};
@@ -3135,13 +3113,13 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->pt_per_sm = std::max(1, g->pt_per_sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pl_per_sm, pr_list_kernel<false>, PT_W * PL_TY, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->pk_per_sm, pr_list_kernel<true>, PT_W * PL_TY, 0);
-    if (const char *v = getenv("FM_PK_OCC")) g->pk_per_sm = std::max(1, std::min(g->pk_per_sm, atoi(v)));
+    g->pk_per_sm = std::max(1, g->pk_per_sm);
     g->pl_per_sm = std::max(1, g->pl_per_sm);
-    if (const char *v = getenv("FM_PL_PER_SM")) g->pl_per_sm = std::max(1, std::min(g->pl_per_sm, atoi(v)));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->bb_per_sm, bfs_bits_kernel, 32 * BB_WARPS, 0);
     g->bb_per_sm = std::max(1, g->bb_per_sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->br_per_sm, bfs_ring_kernel, 32 * BB_WARPS, 0);
     g->br_per_sm = std::max(1, std::min(g->br_per_sm, g->br_cap));
+    g->pl_occ = g->pl_per_sm; g->pk_occ = g->pk_per_sm; g->br_occ = g->br_per_sm;
     // ring capacity: every tile once + one reserved slot per resident warp
     g->rq.cap = g->ntiles + g->sms * g->br_per_sm * BB_WARPS + 64;
     g->prq.cap = g->ntiles + g->sms * g->pl_per_sm + 64;
@@ -3269,6 +3247,9 @@ extern "C" int fm_grid_solve_host(fm_grid *g, const int32_t *capR, const int32_t
         cudaEventRecord(a, g->stream);
         if (!g->h_cut_stage && cudaMallocHost((void **)&g->h_cut_stage, HW) != cudaSuccess) g->h_cut_stage = nullptr;
         uint8_t *dst = g->h_cut_stage ? g->h_cut_stage : cut_out;
+        // no bounce buffer: the D2H writes the caller's array directly, so the
+        // prefault thread (writing zeros into it) must be done first
+        if (dst == cut_out && prefault.joinable()) prefault.join();
         // chunked: the host copy of chunk k overlaps the D2H of chunk k+1
         constexpr int NCH = 4;
         cudaEvent_t ce[NCH];
@@ -3555,5 +3536,47 @@ extern "C" int fm_grid_cut_plane(fm_grid *g, uint8_t *dst, int32_t dst_on_host) 
     FM_CHECK_CUDA(cudaMemcpyAsync(dst, g->d.cut, (size_t)g->HW,
                                   dst_on_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, g->stream));
     FM_TRY(sync_stream(g));
+    return FM_OK;
+}
+
+// A/B and tuning options (replace the round-1 environment knobs; a library never
+// reads the caller's environment).  Take effect at the next solve.  Names are the
+// DESIGN.md section 4 switch names in lower case.
+extern "C" int fm_grid_set_option(fm_grid *g, const char *name, int64_t value) {
+    if (!g || !name) { fm_set_error("fm_grid_set_option: invalid argument"); return FM_INVALID_ARG; }
+    const int v = (int)std::max<int64_t>(INT32_MIN, std::min<int64_t>(INT32_MAX, value));
+    const std::string k(name);
+    if (k == "k_local") g->k_local = v;
+    else if (k == "bfs_interval") g->bfs_interval_env = v;
+    else if (k == "trace") g->trace = v;
+    else if (k == "relabel_div") g->relabel_div = v;
+    else if (k == "op_steps") g->op_steps = std::max(1, v);
+    else if (k == "op_fused") g->op_fused = v;
+    else if (k == "vote") g->vote_mask = std::max(1, v) - 1;
+    else if (k == "pr_kernel") g->pr_kernel = v;
+    else if (k == "bfs_bits") g->bfs_bits = v;
+    else if (k == "br_cap") { g->br_cap = std::max(1, v); g->br_per_sm = std::max(1, std::min(g->br_occ, g->br_cap));
+                              g->rq.cap = g->ntiles + g->sms * g->br_per_sm * BB_WARPS + 64; }
+    else if (k == "pr_ring") g->pr_ring = v;
+    else if (k == "pr_graph") g->pr_graph = v;
+    else if (k == "packed") g->pk = v;
+    else if (k == "bfs_incr") g->rq.incr = v ? 1 : 0;
+    else if (k == "k_solo") g->d.k_solo = v;
+    else if (k == "solo_max") g->d.solo_max = v;
+    else if (k == "k_tail") g->k_tail = v;
+    else if (k == "two_hop") g->two_hop = v;
+    else if (k == "tail_div") g->tail_div = v;
+    else if (k == "pr_batch") g->pr_batch = std::max(1, std::min(16, v));
+    else if (k == "visit_mult") g->visit_mult = std::max(1, v);
+    else if (k == "br_rerun") g->rq.rerun = v;
+    else if (k == "br_ns0") g->rq.ns0 = v;
+    else if (k == "br_ns1") g->rq.ns1 = v;
+    else if (k == "k_local_list") g->k_local_list = v;
+    else if (k == "local_div") g->local_div = v;
+    else if (k == "local_max") g->local_max = v;
+    else if (k == "local_margin") g->local_margin = v;
+    else if (k == "pk_occ") g->pk_per_sm = std::max(1, std::min(g->pk_occ, v));
+    else if (k == "pl_per_sm") g->pl_per_sm = std::max(1, std::min(g->pl_occ, v));
+    else { fm_set_error("fm_grid_set_option: unknown option '%s'", name); return FM_INVALID_ARG; }
     return FM_OK;
 }

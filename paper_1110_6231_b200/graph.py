@@ -71,6 +71,60 @@ class FlowNetwork:
         return a
 
 
+@dataclass(slots=True)
+class ResidualState:
+    """Mutable solver state (graph.py:128-154): residual[a] per arc, excess[x]
+    (negative = deficit), height (max-flow), price (assignment)."""
+
+    residual: list
+    excess: list
+    height: list
+    price: list
+
+    @classmethod
+    def fresh(cls, net: "FlowNetwork") -> "ResidualState":
+        n = net.node_count
+        return cls(residual=list(net.capacity), excess=[0] * n, height=[0] * n, price=[0] * n)
+
+    def flow_on(self, net: "FlowNetwork", a: int) -> int:
+        return net.capacity[a] - self.residual[a]
+
+
+def reduced_cost(net: "FlowNetwork", state: ResidualState, a: int) -> int:
+    """cost(a) + price(tail) - price(head) (graph.py:157-159)."""
+    return net.cost[a] + state.price[net.tail[a]] - state.price[net.head[a]]
+
+
+def part_reduced_cost(net: "FlowNetwork", state: ResidualState, a: int) -> int:
+    """cost(a) - price(head) (graph.py:162-164)."""
+    return net.cost[a] - state.price[net.head[a]]
+
+
+def is_epsilon_optimal(net: "FlowNetwork", state: ResidualState, epsilon: int, fixed=None) -> bool:
+    """True iff every residual, non-fixed arc has reduced cost >= -epsilon
+    (graph.py:167-186), evaluated over all arcs at once with numpy (object dtype
+    when the values leave int64)."""
+    m = len(net.tail)
+    if m == 0:
+        return True
+    try:
+        cost = np.asarray(net.cost, dtype=np.int64)
+        price = np.asarray(state.price, dtype=np.int64)
+        big = int(np.abs(cost).max()) + 2 * int(np.abs(price).max()) >= 2**62
+    except OverflowError:
+        big = True
+    if big:
+        cost = np.asarray(net.cost, dtype=object)
+        price = np.asarray(state.price, dtype=object)
+    tail = np.asarray(net.tail, dtype=np.int64)
+    head = np.asarray(net.head, dtype=np.int64)
+    live = np.asarray(state.residual, dtype=np.int64) > 0
+    if fixed is not None:
+        live &= ~np.asarray(fixed, dtype=bool)
+    rc = cost[live] + price[tail[live]] - price[head[live]]
+    return bool((rc >= -epsilon).all()) if len(rc) else True
+
+
 def build_network(edge_list, node_count: int, source: int, sink: int) -> FlowNetwork:
     """Validated FlowNetwork from (tail, head, capacity[, cost]) tuples
     (graph.py:87-125; same error messages)."""
@@ -196,26 +250,61 @@ class GridNetwork(FlowNetwork):
         return len(self.tail)
 
 
+def _device_planes(planes):
+    """Six CUDA planes as contiguous int32 tensors on one device.  Wider integer
+    inputs are range-checked before the narrowing copy; anything else raises."""
+    import torch
+
+    dev = planes[0].device
+    out = []
+    for name, a in zip(_PLANES, planes):
+        if not hasattr(a, "is_cuda") or not a.is_cuda:
+            raise NetworkError(f"{name}: mixed host and device planes")
+        if a.device != dev:
+            raise NetworkError(f"{name} is on {a.device}, expected {dev}")
+        if a.dtype != torch.int32:
+            if a.dtype.is_floating_point or a.dtype.is_complex or a.dtype == torch.bool:
+                raise NetworkError(f"{name}: capacities must be integers, got {a.dtype}")
+            if a.numel() and int(a.max()) >= 2**31:
+                raise NetworkError(f"{name}: capacity {int(a.max())} does not fit in int32")
+            a = a.to(torch.int32)
+        out.append(a.contiguous())
+    return out
+
+
 def build_grid_network(capR, capL, capD, capU, capS, capT) -> GridNetwork:
-    """Validated GridNetwork from six H x W capacity planes (int32).
+    """Validated GridNetwork from six H x W capacity planes (int32 numpy arrays or
+    CUDA tensors; other integer dtypes are range-checked and narrowed).
 
     Raises NetworkError for a shape mismatch, a negative capacity, or a
     non-zero capacity on an arc that would leave the grid (last column of
-    capR, first column of capL, last row of capD, first row of capU)."""
+    capR, first column of capL, last row of capD, first row of capU).  Device
+    planes get the same checks (a few reductions on their device)."""
     net = GridNetwork(capR, capL, capD, capU, capS, capT)
-    if not net.on_device:
+    if net.on_device:
+        import torch
+
+        planes = _device_planes(net.caps)
+        mins = torch.stack([a.min() for a in planes]).cpu().tolist() if planes[0].numel() else [0] * 6
+        for name, m in zip(_PLANES, mins):
+            if m < 0:
+                raise NetworkError(f"{name}: negative capacity {m}")
+        capR, capL, capD, capU = planes[:4]
+        edge = torch.stack([capR[:, -1].any(), capL[:, 0].any(), capD[-1, :].any(), capU[0, :].any()]).cpu().tolist()
+    else:
         planes = net.host_caps()
         for name, a in zip(_PLANES, planes):
             if a.size and int(a.min()) < 0:
                 raise NetworkError(f"{name}: negative capacity {int(a.min())}")
         capR, capL, capD, capU = planes[:4]
-        if capR[:, -1].any():
-            raise NetworkError("capR: last column must be 0 (arc leaves the grid)")
-        if capL[:, 0].any():
-            raise NetworkError("capL: first column must be 0 (arc leaves the grid)")
-        if capD[-1, :].any():
-            raise NetworkError("capD: last row must be 0 (arc leaves the grid)")
-        if capU[0, :].any():
-            raise NetworkError("capU: first row must be 0 (arc leaves the grid)")
-        net.caps = planes
+        edge = [capR[:, -1].any(), capL[:, 0].any(), capD[-1, :].any(), capU[0, :].any()]
+    if edge[0]:
+        raise NetworkError("capR: last column must be 0 (arc leaves the grid)")
+    if edge[1]:
+        raise NetworkError("capL: first column must be 0 (arc leaves the grid)")
+    if edge[2]:
+        raise NetworkError("capD: last row must be 0 (arc leaves the grid)")
+    if edge[3]:
+        raise NetworkError("capU: first row must be 0 (arc leaves the grid)")
+    net.caps = tuple(planes)
     return net

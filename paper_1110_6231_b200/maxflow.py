@@ -4,9 +4,8 @@
 reference signature, defaults and return type (maxflow_par.py:157-238).  On a
 :class:`GridNetwork` it runs the CUDA path in libfm_b200.so; the result carries the
 flow value in ``objective`` (= excess at t, maxflow_par.py:233) plus the minimal
-source-side cut in ``report.cut``.  Other networks raise ``NotImplementedError``:
-the generic-graph (CSR) kernel is a SURVEY.md 8f "next" row, and there is no CPU
-fallback by design.
+source-side cut in ``report.cut``.  Any other ``FlowNetwork`` runs the generic
+CSR lock-free kernel (fm_csr.cu).  There is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -18,7 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .graph import FlowNetwork, GridNetwork, SolveReport
+from .graph import FlowNetwork, GridNetwork, SolveReport, _device_planes
 
 DEFAULT_CYCLE_BUDGET = 7000  # maxflow_par.py:28
 DEFAULT_BFS_INTERVAL = 0     # 0 = library default sweeps between global relabels
@@ -28,10 +27,11 @@ class GridSolver:
     """Reusable device workspace for H x W grids (owns the C handle).
 
     The SoA state (9 int32 planes + 3 byte planes, ~40 B/pixel) is allocated once
-    and reused across solves of the same shape.
+    and reused across solves of the same shape.  options: kernel-variant / tuning
+    switches passed to fm_grid_set_option (the library reads no environment).
     """
 
-    def __init__(self, H: int, W: int, device: int = 0):
+    def __init__(self, H: int, W: int, device: int = 0, options: dict | None = None):
         L = _lib.load()
         _lib.require_device()
         h = ctypes.c_void_p()
@@ -39,6 +39,12 @@ class GridSolver:
         self.H, self.W, self.device = int(H), int(W), int(device)
         self._h = h
         self.last_stats: dict = {}
+        for k, v in (options or {}).items():
+            self.set_option(k, v)
+
+    def set_option(self, name: str, value: int) -> None:
+        """Kernel-variant / tuning switch, from the next solve."""
+        _lib.check(_lib.load().fm_grid_set_option(self._h, name.encode(), int(value)), "fm_grid_set_option")
 
     def close(self) -> None:
         if self._h:
@@ -136,18 +142,7 @@ class GridSolver:
         return cut
 
 
-_solvers: dict = {}
-
-
-def _solver_for(H: int, W: int, device: int) -> GridSolver:
-    key = (H, W, device)
-    s = _solvers.get(key)
-    if s is None:
-        # keep at most one cached workspace per device: grids are large
-        for k in [k for k in _solvers if k[2] == device]:
-            _solvers.pop(k).close()
-        s = _solvers[key] = GridSolver(H, W, device)
-    return s
+_solvers = _lib.SolverCache(per_device=1)   # grids are large: one cached workspace per device
 
 
 # ---------------------------------------------------------------- observer mirror
@@ -226,7 +221,7 @@ def _observe(net: GridNetwork, solver: GridSolver, observer, cycle_budget, worke
 
 
 def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DEFAULT_CYCLE_BUDGET,
-                 observer=None, *, device: int = 0, bfs_interval: int = DEFAULT_BFS_INTERVAL,
+                 observer=None, *, device: int | None = None, bfs_interval: int = DEFAULT_BFS_INTERVAL,
                  cancel_violations: bool = False, want_cut: bool = True) -> SolveReport:
     """Coordinated lock-free push-relabel rounds until all live excess is at t
     (maxflow_par.py:157-238), on the GPU.
@@ -247,33 +242,42 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
             raise NotImplementedError("observer hooks are supported on GridNetwork solves")
         return csr_solve(net, cycle_budget)
     started = time.perf_counter()
-    solver = _solver_for(net.H, net.W, device)
-    if observer is None:
-        if net.on_device:
-            import torch
+    caps = net.caps
+    if net.on_device:
+        caps = _device_planes(caps)
+        dev = caps[0].device.index or 0
+        if device is not None and int(device) != dev:
+            raise ValueError(f"device={device} but the capacity planes are on cuda:{dev}")
+        device = dev
+    elif device is None:
+        device = 0
+    with _solvers.use((net.H, net.W, device), device, lambda: GridSolver(net.H, net.W, device)) as solver:
+        if observer is None:
+            if net.on_device:
+                import torch
 
-            cut_t = torch.empty((net.H, net.W), dtype=torch.uint8, device=net.caps[0].device) if want_cut else None
-            flow, stats = solver.solve_device(net.caps, cycle_budget, bfs_interval, cut_out=cut_t,
-                                              cancel_violations=cancel_violations,
-                                              stream=torch.cuda.current_stream(net.caps[0].device))
-            cut = cut_t.bool() if cut_t is not None else None
+                cut_t = torch.empty((net.H, net.W), dtype=torch.uint8, device=caps[0].device) if want_cut else None
+                flow, stats = solver.solve_device(caps, cycle_budget, bfs_interval, cut_out=cut_t,
+                                                  cancel_violations=cancel_violations,
+                                                  stream=torch.cuda.current_stream(caps[0].device))
+                cut = cut_t.bool() if cut_t is not None else None
+            else:
+                flow, cut, stats = solver.solve_host(net.host_caps(), cycle_budget, bfs_interval,
+                                                     want_cut=want_cut, cancel_violations=cancel_violations)
         else:
-            flow, cut, stats = solver.solve_host(net.host_caps(), cycle_budget, bfs_interval,
-                                                 want_cut=want_cut, cancel_violations=cancel_violations)
-    else:
-        solver.begin(net.host_caps(), cancel_violations=cancel_violations)
-        while True:
+            solver.begin(net.host_caps(), cancel_violations=cancel_violations)
+            while True:
+                st = solver.export()
+                if int(((st["e"] > 0) & (st["marked"] == 0)).sum()) == 0:
+                    break
+                done = solver.round(cycle_budget, bfs_interval)
+                _observe(net, solver, observer, cycle_budget, worker_count)
+                if done:
+                    break
             st = solver.export()
-            if int(((st["e"] > 0) & (st["marked"] == 0)).sum()) == 0:
-                break
-            done = solver.round(cycle_budget, bfs_interval)
-            _observe(net, solver, observer, cycle_budget, worker_count)
-            if done:
-                break
-        st = solver.export()
-        flow = st["flow"]
-        stats = dict(solver.last_stats)
-        cut = solver.cut_host().astype(bool) if want_cut else None
+            flow = st["flow"]
+            stats = dict(solver.last_stats)
+            cut = solver.cut_host().astype(bool) if want_cut else None
     elapsed = time.perf_counter() - started
     return SolveReport(objective=int(flow), pushes=int(stats.get("pushes", 0)),
                        relabels=int(stats.get("relabels", 0)), rounds=int(stats.get("rounds", 0)),

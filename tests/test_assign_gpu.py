@@ -182,19 +182,18 @@ def test_sparse_mid_size_vs_scipy():
     assert all(w[x, y] != -(2**31) for x, y in enumerate(m))
 
 
-@pytest.mark.parametrize("ybatch_min", ["1", "1000000"])
-def test_y_batch_threshold_variants(ybatch_min, monkeypatch):
+@pytest.mark.parametrize("ybatch_min", [1, 1000000])
+def test_y_batch_threshold_variants(ybatch_min):
     """The gathered Y op pushes its excess back either unit by unit (an argmin per
-    unit) or, from FM_YBATCH_MIN units on, as one rank-ordered batch; both orders are
+    unit) or, from ybatch_min units on, as one rank-ordered batch; both orders are
     the same sequence of reference operations, so objective and matching agree with
-    scipy's exact solver either way (knob read at solver creation)."""
+    scipy's exact solver either way (option ybatch_min)."""
     from scipy.optimize import linear_sum_assignment
-    monkeypatch.setenv("FM_YBATCH_MIN", ybatch_min)
     rng = np.random.default_rng(int(ybatch_min) % 97)
     for n, M in ((300, 10000), (700, 100), (1024, 10)):
         w = rng.integers(0, M + 1, size=(n, n)).astype(np.int32)
         r, c = linear_sum_assignment(w.astype(np.int64), maximize=True)
-        solver = fmb.AssignmentSolver(n)
+        solver = fmb.AssignmentSolver(n, options={"ybatch_min": ybatch_min})
         try:
             obj, m, _, _ = solver.solve_host(w)
         finally:
@@ -203,17 +202,16 @@ def test_y_batch_threshold_variants(ybatch_min, monkeypatch):
         assert obj == int(w[r, c].sum()) and _is_perm(m, n) and _objective(w, m) == obj
 
 
-@pytest.mark.parametrize("ring", ["0", "1"])
-def test_price_update_barrier_and_queue_variants(ring, monkeypatch):
+@pytest.mark.parametrize("ring", [0, 1])
+def test_price_update_barrier_and_queue_variants(ring):
     """The price update's label relaxation runs either as barrier-separated waves or
-    queue-driven without barriers (FM_PU_RING, read per solve); both reach the same
+    queue-driven without barriers (option pu_ring); both reach the same
     labels (a fixpoint of min-updates over path lengths), so the optimum and the
     epsilon-optimality certificate hold either way, including sparse instances."""
     from scipy.optimize import linear_sum_assignment
-    monkeypatch.setenv("FM_PU_RING", ring)
     for n, M in ((1, 5), (7, 3), (64, 10000), (333, 100), (1024, 10000)):
         w = G.assignment_reference(n, M, n + 7)
-        solver = fmb.AssignmentSolver(n)
+        solver = fmb.AssignmentSolver(n, options={"pu_ring": ring})
         try:
             obj, m, prices, _ = solver.solve_host(w, want_prices=True)
         finally:
@@ -230,5 +228,9 @@ def test_price_update_barrier_and_queue_variants(ring, monkeypatch):
     w = np.where(keep, w, -(2**31)).astype(np.int32)
     cost = np.where(w == -(2**31), -1e15, w.astype(np.float64))
     r, c = linear_sum_assignment(cost, maximize=True)
-    rep, m = fmb.solve_assignment(w)
-    assert rep.objective == int(w[r, c].astype(np.int64).sum()) and sorted(m) == list(range(n))
+    solver = fmb.AssignmentSolver(n, options={"pu_ring": ring})
+    try:
+        obj, m, _, _ = solver.solve_host(w)
+    finally:
+        solver.close()
+    assert obj == int(w[r, c].astype(np.int64).sum()) and sorted(m) == list(range(n))

@@ -64,11 +64,50 @@ def test_cycle_budget_terminates(budget):
     assert (rep.cut == want["cut"]).all()
 
 
-def test_cancel_violations_flag_same_answer():
-    caps = G.grid_random(32, 32, 32)
+@pytest.mark.parametrize("shape,seed", [((32, 32), 32), ((61, 47), 5), ((128, 96), 9)])
+def test_cancel_violations_flag_same_answer(shape, seed):
+    """maxflow_par.py:132-154 as the opt-in pass: same flow AND same minimal cut."""
+    caps = G.grid_random(*shape, seed)
     want = oracle.grid_maxflow(*caps, solver="seq")
     rep = _solve(caps, cancel_violations=True)
     assert rep.objective == want["value"]
+    assert (rep.cut == want["cut"]).all()
+    seg = G.grid_segmentation(*shape, seed)
+    want = oracle.grid_maxflow(*seg, solver="seq")
+    rep = _solve(seg, cancel_violations=True)
+    assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
+
+
+def test_device_planes_validated_like_host_planes():
+    """build_grid_network on CUDA tensors applies the host path's checks (negative
+    capacity, arcs leaving the grid), narrows wider integer dtypes after a range
+    check, rejects float planes, and solves on the planes' own device."""
+    import torch
+
+    caps = [torch.from_numpy(c).cuda() for c in G.grid_random(40, 56, 3)]
+    want = oracle.grid_maxflow(*[c.cpu().numpy() for c in caps], solver="seq")
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*[c.to(torch.int64) for c in caps]))
+    assert rep.objective == want["value"] and (rep.cut.cpu().numpy() == want["cut"]).all()
+    bad = [c.clone() for c in caps]
+    bad[0][:, -1] = 2
+    with pytest.raises(fmb.NetworkError, match="capR: last column"):
+        fmb.build_grid_network(*bad)
+    bad = [c.clone() for c in caps]
+    bad[3][0, 5] = 1
+    with pytest.raises(fmb.NetworkError, match="capU: first row"):
+        fmb.build_grid_network(*bad)
+    bad = [c.clone() for c in caps]
+    bad[5][3, 3] = -4
+    with pytest.raises(fmb.NetworkError, match="negative capacity"):
+        fmb.build_grid_network(*bad)
+    with pytest.raises(fmb.NetworkError, match="must be integers"):
+        fmb.build_grid_network(*[c.float() for c in caps])
+    big = [c.to(torch.int64) for c in caps]
+    big[4][0, 0] = 2**33
+    with pytest.raises(fmb.NetworkError, match="does not fit"):
+        fmb.build_grid_network(*big)
+    with pytest.raises(ValueError, match="device=1"):
+        fmb.hybrid_solve(fmb.build_grid_network(*caps), device=1)
 
 
 def test_observer_invariants():

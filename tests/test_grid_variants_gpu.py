@@ -1,12 +1,10 @@
-"""Every kernel variant the grid solver can be switched to (env knobs read when a
-GridSolver is created) stays bit-exact: same flow value and same minimal cut as the
+"""Every kernel variant the grid solver can be switched to (options passed to
+fm_grid_set_option) stays bit-exact: same flow value and same minimal cut as the
 pinned CPU oracle.  Guards the A/B paths (v1/v2 push kernels, sweep-based and
 Jacobi BFS, the persistent ring push round, multi-step / fused operations, solo
 thresholds, tile pass counts) against rotting behind the defaults."""
 
 from __future__ import annotations
-
-import os
 
 import numpy as np
 import pytest
@@ -19,28 +17,28 @@ pytestmark = pytest.mark.gpu
 
 VARIANTS = {
     "default": {},
-    "pr_tile_v2": {"FM_PR_KERNEL": "0"},
-    "bfs_sweeps_bits": {"FM_BFS_BITS": "1"},
-    "bfs_jacobi_v1": {"FM_BFS_BITS": "0"},
-    "pr_ring": {"FM_PR_RING": "1"},
-    "steps2": {"FM_OP_STEPS": "2"},
-    "fused": {"FM_OP_FUSED": "1"},
-    "steps2_fused": {"FM_OP_STEPS": "2", "FM_OP_FUSED": "1"},
-    "solo_never": {"FM_SOLO_MAX": "0"},
-    "solo_always": {"FM_SOLO_MAX": "1024"},
-    "k4": {"FM_K_LOCAL_LIST": "4"},
-    "k64": {"FM_K_LOCAL_LIST": "64"},
-    "batch1": {"FM_PR_BATCH": "1"},
-    "no_local_relabel": {"FM_LOCAL_DIV": "0"},
-    "br_rerun": {"FM_BR_RERUN": "1", "FM_BR_CAP": "2"},
-    "no_two_hop": {"FM_TWO_HOP": "0"},
-    "three_hop": {"FM_TWO_HOP": "2"},
-    "pr_graph": {"FM_PR_GRAPH": "1"},
-    "unpacked": {"FM_PACKED": "0"},
-    "bfs_from_scratch": {"FM_BFS_INCR": "0"},
-    "bfs_incremental_rerun": {"FM_BFS_INCR": "1", "FM_BR_RERUN": "1"},
-    "bfs_incremental_no_local": {"FM_BFS_INCR": "1", "FM_LOCAL_DIV": "0"},
-    "pr_graph_b1": {"FM_PR_GRAPH": "1", "FM_PR_BATCH": "1"},
+    "pr_tile_v2": {"pr_kernel": 0},
+    "bfs_sweeps_bits": {"bfs_bits": 1},
+    "bfs_jacobi_v1": {"bfs_bits": 0},
+    "pr_ring": {"pr_ring": 1},
+    "steps2": {"op_steps": 2},
+    "fused": {"op_fused": 1},
+    "steps2_fused": {"op_steps": 2, "op_fused": 1},
+    "solo_never": {"solo_max": 0},
+    "solo_always": {"solo_max": 1024},
+    "k4": {"k_local_list": 4},
+    "k64": {"k_local_list": 64},
+    "batch1": {"pr_batch": 1},
+    "no_local_relabel": {"local_div": 0},
+    "br_rerun": {"br_rerun": 1, "br_cap": 2},
+    "no_two_hop": {"two_hop": 0},
+    "three_hop": {"two_hop": 2},
+    "pr_graph": {"pr_graph": 1},
+    "unpacked": {"packed": 0},
+    "bfs_from_scratch": {"bfs_incr": 0},
+    "bfs_incremental_rerun": {"bfs_incr": 1, "br_rerun": 1},
+    "bfs_incremental_no_local": {"bfs_incr": 1, "local_div": 0},
+    "pr_graph_b1": {"pr_graph": 1, "pr_batch": 1},
 }
 
 CASES = [("G", 96, 160, 11), ("G", 257, 130, 12), ("S", 200, 256, 2048), ("G", 31, 33, 13)]
@@ -57,12 +55,10 @@ def expected():
 
 
 @pytest.mark.parametrize("name", sorted(VARIANTS))
-def test_variant_bit_exact(name, expected, monkeypatch):
-    for k, v in VARIANTS[name].items():
-        monkeypatch.setenv(k, v)
+def test_variant_bit_exact(name, expected):
     for key, (caps, value, cut) in expected.items():
         H, W = caps[0].shape
-        solver = fmb.GridSolver(H, W)   # knobs are read here
+        solver = fmb.GridSolver(H, W, options=VARIANTS[name])
         try:
             flow, got_cut, _ = solver.solve_host(caps)
         finally:
