@@ -152,35 +152,56 @@ int fm_grid_cut_plane(fm_grid *g, uint8_t *dst, int32_t dst_on_host);
 int fm_grid_stats(fm_grid *g, fm_stats *stats);
 
 /* ------------------------------------------------------------ row bands
- * Multi-GPU grid path: the handle holds one horizontal band of a
- * larger grid plus a ghost row (frozen copy of the neighbour band's boundary row)
- * on each side that has a neighbour.  Orchestrated by paper_1110_6231_b200.bands;
- * every step syncs its stream before returning.  cap* and row buffers: DEVICE. */
-#define FM_ROW_FLOW 0  /* out: flow parked in the ghost row (zeroed) | in: flow into our boundary row */
-#define FM_ROW_H 1     /* out: boundary-row heights               | in: ghost heights */
-#define FM_ROW_RES 2   /* out: boundary residual toward the ghost  | in: ghost residual toward us */
-#define FM_ROW_DIST 3  /* out: boundary BFS distance               | in: ghost distance (re-queues tiles) */
-#define FM_ROW_CUT 4   /* out: boundary cut bit                    | in: ghost cut bit (re-queues tiles) */
-#define FM_ROW_PUSH_STATE 5 /* FLOW | H | RES as three consecutive rows (buffer of 3 W) */
-/* global_nodes = H*W + 2 of the WHOLE grid: heights, the source height |V| and the
- * BFS sentinel must agree across bands. */
-int fm_grid_band_config(fm_grid *g, int32_t ghost_top, int32_t ghost_bottom, int64_t global_nodes);
-/* Run the band's steps on `stream` (a cudaStream_t, e.g. the caller's NCCL-ordered torch
- * stream; NULL = the library's own stream).  With a caller stream, the row export
- * (fm_grid_band_rows direction 0) is only enqueued: anything the caller orders after it on
- * that stream (an NCCL send) sees the exported row without a host synchronisation. */
-int fm_grid_band_stream(fm_grid *g, void *stream);
-int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t *capL,
-                      const int32_t *capD, const int32_t *capU, const int32_t *capS,
-                      const int32_t *capT, int32_t flags, int64_t *sum_caps_out);
-int fm_grid_band_bfs(fm_grid *g, int32_t phase, int64_t *changed);
-int fm_grid_band_finalize(fm_grid *g, int64_t *out /* active, marked excess, deepest level */);
-int fm_grid_band_push(fm_grid *g, int32_t max_launches, int32_t cycle_budget,
-                      int64_t *out /* pushes, relabels, launches, idle */);
-int fm_grid_band_cut(fm_grid *g, int32_t phase, int64_t *changed);
-int fm_grid_band_rows(fm_grid *g, int32_t direction /* 0 out, 1 in */, int32_t side /* 0 top, 1 bottom */,
-                      int32_t kind, int32_t *buf, int64_t *changed);
-int fm_grid_band_flow(fm_grid *g, int64_t *out);
+ * Multi-GPU grid path -- the reference's coordinator loop
+ * (maxflow_par.py:195-229) run by every band of a grid cut into horizontal bands on
+ * 32-row tile boundaries.  A band's kernels read the neighbour bands' boundary rows
+ * (heights, BFS distances, cut bits) and push flow into their inboxes directly
+ * through peer memory (one process: peer access; one process per GPU: CUDA IPC);
+ * the bands' global-relabel and min-cut ring launches end on one shared pending
+ * counter.  Host-level agreement (idle / budget / active counts) goes through an
+ * fm_coll: a shared-memory barrier + all-gather of a few int64 per push batch.
+ * hybrid_solve(net, devices=N) (maxflow_par.py:157-162 plus `devices`) uses an
+ * in-process fm_group; torchrun ranks use fm_grid_band_* + fm_coll_create(name). */
+typedef struct fm_coll fm_coll;
+/* name == NULL: process-local (threads); else a POSIX shared-memory segment that rank
+ * 0 creates and the other ranks open (after the caller's own barrier). */
+int fm_coll_create(const char *name, int32_t nranks, int32_t rank, fm_coll **out);
+void fm_coll_destroy(fm_coll *c);
+/* every rank passes n <= 8 values; out[r * n + i] = rank r's value i */
+int fm_coll_allgather(fm_coll *c, const int64_t *vals, int32_t n, int64_t *out);
+/* band borders: edges[0..nbands] (edges[0] = 0, edges[nbands] = H) */
+int fm_band_split(int32_t H, int32_t nbands, int32_t *edges);
+
+/* The handle (fm_grid_create(rows of the band, W, device)) becomes band `band` of
+ * `nbands` of an H_total-row grid; `colocated` = bands sharing this device. */
+int fm_grid_band_setup(fm_grid *g, int32_t band, int32_t nbands, int32_t H_total, int32_t colocated);
+#define FM_BAND_EXPORT_BYTES 1024
+/* IPC handles of the buffers neighbours need, for fm_grid_band_link in other processes */
+int fm_grid_band_export(fm_grid *g, void *blob);
+int fm_grid_band_link(fm_grid *g, const void *up_blob, const void *dn_blob, const void *band0_blob);
+/* same-process neighbours (any devices with peer access) */
+int fm_grid_band_link_local(fm_grid *g, fm_grid *up, fm_grid *dn, fm_grid *band0);
+/* This band's share of the solve; every band calls it at once.  Inputs host or device
+ * (UVA): the six planes of the band's rows, capD of the row above the band and capU of
+ * the row below it (W each, NULL for the first / last band).  flow_out = the whole
+ * grid's flow; cut_out (host or device, band rows) = its rows of the minimal cut. */
+int fm_grid_band_solve(fm_grid *g, fm_coll *c, const int32_t *capR, const int32_t *capL,
+                       const int32_t *capD, const int32_t *capU, const int32_t *capS,
+                       const int32_t *capT, const int32_t *capD_above, const int32_t *capU_below,
+                       int32_t cycle_budget, int32_t flags, int64_t *flow_out, uint8_t *cut_out,
+                       fm_stats *stats);
+
+/* In-process group: nbands bands of an H x W grid, band k on devices[k] (bands may
+ * share a device).  fm_group_solve takes whole-grid planes (host or device) and runs
+ * one host thread per band; stats = counters summed over bands, times of the slowest. */
+typedef struct fm_group fm_group;
+int fm_group_create(int32_t H, int32_t W, int32_t nbands, const int32_t *devices, fm_group **out);
+void fm_group_destroy(fm_group *grp);
+int fm_group_band(fm_group *grp, int32_t k, fm_grid **band, int32_t *row0, int32_t *rows);
+int fm_group_solve(fm_group *grp, const int32_t *capR, const int32_t *capL, const int32_t *capD,
+                   const int32_t *capU, const int32_t *capS, const int32_t *capT, int32_t cycle_budget,
+                   int32_t flags, int64_t *flow_out, uint8_t *cut_out, fm_stats *stats);
+int fm_group_band_stats(fm_group *grp, int32_t k, fm_stats *stats);
 
 /* ---------------------------------------------------------- generic (CSR)
  * hybrid_solve on an arbitrary FlowNetwork (maxflow_par.py:157-238): the arc-pair

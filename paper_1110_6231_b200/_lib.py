@@ -86,15 +86,20 @@ SIGNATURES = {
     "fm_grid_cut_host": (ctypes.c_int, [_vp, _vp, _vp]),
     "fm_grid_cut_plane": (ctypes.c_int, [_vp, _vp, _i32]),
     "fm_grid_stats": (ctypes.c_int, [_vp, _vp]),
-    "fm_grid_band_config": (ctypes.c_int, [_vp, _i32, _i32, _i64]),
-    "fm_grid_band_stream": (ctypes.c_int, [_vp, _vp]),
-    "fm_grid_band_init": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32, _vp]),
-    "fm_grid_band_bfs": (ctypes.c_int, [_vp, _i32, _vp]),
-    "fm_grid_band_finalize": (ctypes.c_int, [_vp, _vp]),
-    "fm_grid_band_push": (ctypes.c_int, [_vp, _i32, _i32, _vp]),
-    "fm_grid_band_cut": (ctypes.c_int, [_vp, _i32, _vp]),
-    "fm_grid_band_rows": (ctypes.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
-    "fm_grid_band_flow": (ctypes.c_int, [_vp, _vp]),
+    "fm_coll_create": (ctypes.c_int, [ctypes.c_char_p, _i32, _i32, ctypes.POINTER(_vp)]),
+    "fm_coll_destroy": (None, [_vp]),
+    "fm_coll_allgather": (ctypes.c_int, [_vp, _vp, _i32, _vp]),
+    "fm_band_split": (ctypes.c_int, [_i32, _i32, _vp]),
+    "fm_grid_band_setup": (ctypes.c_int, [_vp, _i32, _i32, _i32, _i32]),
+    "fm_grid_band_export": (ctypes.c_int, [_vp, _vp]),
+    "fm_grid_band_link": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "fm_grid_band_link_local": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "fm_grid_band_solve": (ctypes.c_int, [_vp, _vp] + [_vp] * 8 + [_i32, _i32, _vp, _vp, _vp]),
+    "fm_group_create": (ctypes.c_int, [_i32, _i32, _i32, _vp, ctypes.POINTER(_vp)]),
+    "fm_group_destroy": (None, [_vp]),
+    "fm_group_band": (ctypes.c_int, [_vp, _i32, _vp, _vp, _vp]),
+    "fm_group_solve": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32, _i32, _vp, _vp, _vp]),
+    "fm_group_band_stats": (ctypes.c_int, [_vp, _i32, _vp]),
     "fm_dimacs_parse_max": (ctypes.c_int, [ctypes.c_char_p, _i64, _vp, _vp, _vp, _vp, _vp, _i64]),
     "fm_dimacs_parse_asn": (ctypes.c_int, [ctypes.c_char_p, _i64, _vp, _vp, _vp, _vp, _vp, _i64]),
     "fm_csr_solve": (ctypes.c_int, [_i32, _i32, _i32, _i64] + [_vp] * 4 + [_i32, _i32] + [_vp] * 5),

@@ -52,8 +52,20 @@ __device__ __forceinline__ int tq_take(const TileQueue &q, int parity, int all_t
     return t;
 }
 
-struct GridDev;
-__device__ __forceinline__ bool is_ghost_row(const GridDev &g, int r);
+// A neighbour band's planes as seen from this band (row-band mode, multi-GPU): device
+// pointers valid on this band's device (peer access in one process, CUDA IPC across
+// processes), pre-offset to the neighbour's boundary row (its last row for the band
+// above, its first row for the band below).  res = the neighbour's residual toward us
+// (rD of the row above / rU of the row below), read by the cut's incoming-arc planes.
+struct PeerView {
+    int32_t *h, *dist, *inbox, *res;
+    uint8_t *cut;
+    int32_t *ext;           // its external-push flags for the tiles of that boundary row
+    int32_t *rq_slot, *rq_flag;
+    unsigned int *rq_ctr;   // its ring queue (tail at [32])
+    int32_t rq_cap;
+    int32_t tile0;          // its tile index of the boundary tile row's first tile
+};
 
 struct GridDev {
     int32_t *e, *h, *rR, *rL, *rD, *rU, *rT, *rS, *cS;
@@ -67,11 +79,15 @@ struct GridDev {
     int32_t ntx, nty;       // tiles per row / column
     TileQueue pq;           // push-relabel work list
     TileQueue bq;           // BFS / cut frontier work list
-    // row-band mode (multi-GPU): row 0 / row H-1 is a ghost copy of the neighbour
-    // band's boundary row.  Ghost pixels never act; flow pushed into them is
-    // shipped to the owner band; their h / dist / cut / residual toward us are
-    // imported from the owner.
-    int32_t ghost_top, ghost_bot;
+    // row-band mode (multi-GPU): this handle holds rows [R0, R0 + H) of a
+    // taller grid.  Arcs leaving the first / last row toward a neighbour band are real
+    // arcs; the neighbour's halo rows, inboxes and queues are reached through up / dn.
+    int32_t has_up, has_dn;
+    int32_t hlim;           // H + has_dn: rows r with r + 1 < hlim have a pixel below
+    int32_t rmin;           // -has_up: rows r with r > rmin have a pixel above
+    PeerView up, dn;
+    int32_t *ext;           // this band's external-push flags: [0, ntx) top tile row, [ntx, 2 ntx) bottom
+    unsigned long long *ext_ctr;   // [0] flags this band raised on its neighbours, [1] own flags consumed
     // local relabel (tail rounds): tiles touched by pushes since the last relabel, and
     // the region R (touched tiles dilated by a margin) a local relabel recomputes;
     // region == nullptr means "global"
@@ -84,10 +100,6 @@ struct GridDev {
     int32_t k_solo;     // push kernel: at most this many solo passes per visit (0: up to k_local)
 };
 
-__device__ __forceinline__ bool is_ghost_row(const GridDev &g, int r) {
-    return (g.ghost_top && r == 0) || (g.ghost_bot && r == g.H - 1);
-}
-
 // ----------------------------------------------------------------------------
 // init: hybrid_init + init_preflow (maxflow_par.py:44-62, maxflow_seq.py:47-64).
 // Saturating s->p gives e(p) = capS(p).  With precancel, min(capS, capT) is routed
@@ -98,7 +110,10 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
                                  const int32_t *__restrict__ capD,
                                  const int32_t *__restrict__ capU,
                                  const int32_t *__restrict__ capS,
-                                 const int32_t *__restrict__ capT, int precancel,
+                                 const int32_t *__restrict__ capT,
+                                 const int32_t *__restrict__ capD_above,   // band mode: capD of the row above (W)
+                                 const int32_t *__restrict__ capU_below,   // band mode: capU of the row below (W)
+                                 int precancel,
                                  unsigned long long *acc /* [0]=sum capS [1]=negative [2]=too large [3]=pair > 65535 */) {
     long long sum = 0, bad = 0, big = 0, wide = 0;
     // rows over blocks, columns over threads: coalesced, and no 64-bit division per pixel
@@ -108,14 +123,15 @@ __global__ void grid_init_kernel(GridDev g, const int32_t *__restrict__ capR,
         int32_t cs = capS[p], ct = capT[p];
         int32_t cr = c + 1 < g.W ? capR[p] : 0;
         int32_t cl = c > 0 ? capL[p] : 0;
-        int32_t cd = r + 1 < g.H ? capD[p] : 0;
-        int32_t cu = r > 0 ? capU[p] : 0;
+        int32_t cd = r + 1 < g.hlim ? capD[p] : 0;
+        int32_t cu = r > g.rmin ? capU[p] : 0;
         bad += (cs < 0) | (ct < 0) | (cr < 0) | (cl < 0) | (cd < 0) | (cu < 0);
         // int32 device state: the excess of p is at most capS + the capacities into p, and
         // a merged pair's residual at most the pair's two capacities (the reference's
         // Python ints have no such limit, so larger inputs are refused, not wrapped)
         const long long inR = c > 0 ? max(capR[p - 1], 0) : 0, inL = c + 1 < g.W ? max(capL[p + 1], 0) : 0;
-        const long long inD = r > 0 ? max(capD[p - g.W], 0) : 0, inU = r + 1 < g.H ? max(capU[p + g.W], 0) : 0;
+        const long long inD = r > 0 ? max(capD[p - g.W], 0) : (g.has_up ? max(capD_above[c], 0) : 0);
+        const long long inU = r + 1 < g.H ? max(capU[p + g.W], 0) : (g.has_dn ? max(capU_below[c], 0) : 0);
         big += ((long long)max(cs, 0) + inR + inL + inD + inU > (long long)INT32_MAX) |
                ((long long)max(cr, 0) + inL > (long long)INT32_MAX) | ((long long)max(cd, 0) + inU > (long long)INT32_MAX);
         // pairs too wide for the packed 16-bit residual fields of the push kernel
@@ -180,11 +196,10 @@ __device__ __forceinline__ void two_hop_pixel(const GridDev &g, int32_t r, int32
     const int64_t p = (int64_t)r * g.W + c;
     int32_t e = g.e[p];
     if (e <= 0) return;
-    if (is_ghost_row(g, r)) return;
     int32_t *fwd[4] = {g.rR, g.rL, g.rD, g.rU};
     int32_t *rev[4] = {g.rL, g.rR, g.rU, g.rD};
-    const bool ok[4] = {c + 1 < g.W && !is_ghost_row(g, r), c > 0 && !is_ghost_row(g, r),
-                        r + 1 < g.H && !is_ghost_row(g, r + 1), r > 0 && !is_ghost_row(g, r - 1)};
+    // band mode: routes stay inside the band (arcs to a neighbour band are left alone)
+    const bool ok[4] = {c + 1 < g.W, c > 0, r + 1 < g.H, r > 0};
     const int64_t qs[4] = {p + 1, p - 1, p + g.W, p - g.W};
     // every operand first (one round trip), then a compare-and-swap only where a
     // neighbour has sink capacity left
@@ -236,18 +251,17 @@ __global__ void three_hop_kernel(GridDev g) {
     int32_t e = g.e[p];
     if (e <= 0) return;
     const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
-    if (is_ghost_row(g, r)) return;
     int32_t *fwd[4] = {g.rR, g.rL, g.rD, g.rU};
     int32_t *rev[4] = {g.rL, g.rR, g.rU, g.rD};
     const int dr[4] = {0, 0, 1, -1}, dc[4] = {1, -1, 0, 0};
     for (int d1 = 0; d1 < 4 && e > 0; d1++) {
         const int32_t qr = r + dr[d1], qc = c + dc[d1];
-        if (qr < 0 || qr >= g.H || qc < 0 || qc >= g.W || is_ghost_row(g, qr)) continue;
+        if (qr < 0 || qr >= g.H || qc < 0 || qc >= g.W) continue;
         const int64_t q = (int64_t)qr * g.W + qc;
         for (int d2 = 0; d2 < 4 && e > 0; d2++) {
             if (d2 == (d1 ^ 1)) continue;                         // back to p
             const int32_t r2 = qr + dr[d2], c2 = qc + dc[d2];
-            if (r2 < 0 || r2 >= g.H || c2 < 0 || c2 >= g.W || is_ghost_row(g, r2)) continue;
+            if (r2 < 0 || r2 >= g.H || c2 < 0 || c2 >= g.W) continue;
             const int64_t q2 = (int64_t)r2 * g.W + c2;
             const int32_t rpq = *(volatile int32_t *)(fwd[d1] + p);
             const int32_t want = min(e, rpq);
@@ -386,7 +400,7 @@ __global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(
     for (int k = 0; k < PT_ROWS; k++) {
         const int lr = ty + k * PT_TY;
         const int r = r0 + lr;
-        ghost[k] = is_ghost_row(g, r);
+        ghost[k] = false;
         if (r < g.H && c < g.W) {
             const int64_t p = (int64_t)r * g.W + c;
             int32_t e = g.e[p];
@@ -590,6 +604,16 @@ __device__ __forceinline__ uint2 pk_pack(int32_t r, int32_t l, int32_t d, int32_
     return make_uint2((uint32_t)r | ((uint32_t)l << 16), (uint32_t)d | ((uint32_t)u << 16));
 }
 
+// Flow pushed out of the tile into pixel (qr, qc) (band coordinates): parked in the
+// receiver's inbox.  Row-band mode: a row outside the band is the neighbour band's
+// boundary row, whose inbox is reached through peer memory; the system-scope fence
+// orders the inbox add before the external-push flag the CTA raises after the visit.
+__device__ __forceinline__ void push_out(const GridDev &g, int qr, int qc, int dir, int32_t d) {
+    if (qr < 0) { atomicAdd(g.up.inbox + qc, d); __threadfence_system(); return; }
+    if (qr >= g.H) { atomicAdd(g.dn.inbox + qc, d); __threadfence_system(); return; }
+    atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + (int64_t)qr * g.W + qc, d);
+}
+
 struct PlTile {
     int32_t *e, *h, *t;        // shared planes (h with a 1-pixel halo, row stride PT_W + 2)
     int32_t (*r)[PT_H * PT_W];
@@ -632,8 +656,8 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
     int dir = -1;
     if (rr > 0 && c + 1 < g.W && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
     if (rl > 0 && c > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
-    if (rd > 0 && r + 1 < g.H && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
-    if (ru > 0 && r > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
+    if (rd > 0 && r + 1 < g.hlim && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
+    if (ru > 0 && r > g.rmin && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
     if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
     if (dir < 0) return false;                             // nothing residual: rescanned on next load
     if (hp <= best_h) {                                    // relabel (owner-only); the push waits
@@ -655,8 +679,7 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
         const int32_t old = atomicAdd(&T.e[qi], d);
         if (old <= 0 && old + d > 0) *recv = qi;
     } else {
-        const int64_t q = (int64_t)(T.r0 + qr) * g.W + (T.c0 + qc);
-        atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + q, d);
+        push_out(g, T.r0 + qr, T.c0 + qc, dir, d);
         atomicOr(T.nbr, 1 << dir);
     }
     return oldp - d > 0;                                   // hp < V here
@@ -696,8 +719,8 @@ __device__ __forceinline__ bool pk_op1(const GridDev &g, const PlTile &T, int li
     int dir = -1;
     if (rr > 0 && c + 1 < g.W && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
     if (rl > 0 && c > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
-    if (rd > 0 && r + 1 < g.H && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
-    if (ru > 0 && r > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
+    if (rd > 0 && r + 1 < g.hlim && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
+    if (ru > 0 && r > g.rmin && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
     if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
     if (dir < 0) return false;
     if (hp <= best_h) {
@@ -718,8 +741,7 @@ __device__ __forceinline__ bool pk_op1(const GridDev &g, const PlTile &T, int li
         const int32_t old = atomicAdd(&T.e[qi], d);
         if (old <= 0 && old + d > 0) *recv = qi;
     } else {
-        const int64_t q = (int64_t)(T.r0 + qr) * g.W + (T.c0 + qc);
-        atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + q, d);
+        push_out(g, T.r0 + qr, T.c0 + qc, dir, d);
         atomicOr(T.nbr, 1 << dir);
     }
     return oldp - d > 0;
@@ -776,8 +798,8 @@ __device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int l
         int dir = -1;
         if (rr > 0 && c + 1 < g.W && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
         if (rl > 0 && c > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
-        if (rd > 0 && r + 1 < g.H && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
-        if (ru > 0 && r > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
+        if (rd > 0 && r + 1 < g.hlim && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
+        if (ru > 0 && r > g.rmin && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
         if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
         if (dir < 0) return false;                         // nothing residual: rescanned on next load
         if (hp <= best_h) {                                // relabel (owner-only)
@@ -800,8 +822,7 @@ __device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int l
                 *recv = qi;
             }
         } else {
-            const int64_t q = (int64_t)(T.r0 + qr) * g.W + (T.c0 + qc);
-            atomicAdd((dir < 2 ? g.inflow_h : g.inflow_v) + q, d);
+            push_out(g, T.r0 + qr, T.c0 + qc, dir, d);
             atomicOr(T.nbr, 1 << dir);
         }
         e = atomicSub(&T.e[li], d) - d;                    // last: the owner's view of e(p)
@@ -910,13 +931,16 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
         else if (side == 2) { r = r0 + i; cc = c0 - 1; hidx = (i + 1) * HS + PL_HC - 1; }
         else { r = r0 + i; cc = c0 + PT_W; hidx = (i + 1) * HS + PL_HC + PT_W; }
         const bool hin = r >= 0 && r < g.H && cc >= 0 && cc < g.W;
-        cp_async4(&S.h[hidx], g.h + (hin ? (int64_t)r * g.W + cc : 0), hin);
+        if (side < 2 && !hin && cc < g.W && ((r < 0 && g.has_up) || (r == g.H && g.has_dn)))
+            S.h[hidx] = ld_cg((r < 0 ? g.up.h : g.dn.h) + cc);   // row bands: the neighbour band's row
+        else
+            cp_async4(&S.h[hidx], g.h + (hin ? (int64_t)r * g.W + cc : 0), hin);
         // border pixel of this side and its inbox (flow parked by the neighbour tile)
         const int lr = side == 0 ? 0 : side == 1 ? PT_H - 1 : i;
         const int lc = side == 2 ? 0 : side == 3 ? PT_W - 1 : i;
         const int pr = r0 + lr, pc = c0 + lc;
         const bool has = pr < g.H && pc < g.W &&
-                         (side == 0 ? pr > 0 : side == 1 ? pr + 1 < g.H : side == 2 ? pc > 0 : pc + 1 < g.W);
+                         (side == 0 ? pr > g.rmin : side == 1 ? pr + 1 < g.hlim : side == 2 ? pc > 0 : pc + 1 < g.W);
         if (has) {
             const int64_t p = (int64_t)pr * g.W + pc;
             inbox = atomicExch((side < 2 ? g.inflow_v : g.inflow_h) + p, 0);
@@ -936,7 +960,7 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
         const int lr = ty + k * PL_TY;
         const int r = r0 + lr, c = c0 + tx;
         const int li = lr * PT_W + tx;
-        S.f[li] = (r < g.H && c < g.W) ? ((stage[li] > 0 ? 1 : 0) | (is_ghost_row(g, r) ? 2 : 0)) : 2;
+        S.f[li] = (r < g.H && c < g.W) ? (stage[li] > 0 ? 1 : 0) : 2;
     }
     __syncthreads();
 #pragma unroll
@@ -1109,8 +1133,18 @@ __global__ void __launch_bounds__(PL_NT, PK ? FM_PK_MINBLOCKS : FM_PL_MINBLOCKS)
             const int nb = S.nbr;
             if (nb & 1) { tq_push(g.pq, parity ^ 1, tile + 1); g.touched[tile + 1] = 1; }
             if (nb & 2) { tq_push(g.pq, parity ^ 1, tile - 1); g.touched[tile - 1] = 1; }
-            if (nb & 4) { tq_push(g.pq, parity ^ 1, tile + g.ntx); g.touched[tile + g.ntx] = 1; }
-            if (nb & 8) { tq_push(g.pq, parity ^ 1, tile - g.ntx); g.touched[tile - g.ntx] = 1; }
+            // row bands: a push out of the band's first / last tile row went to the
+            // neighbour band's inbox; raise its external-push flag for that tile (the
+            // pushers fenced their inbox adds at system scope before the visit's barrier)
+            const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+            if (nb & 4) {
+                if (tyi + 1 < g.nty) { tq_push(g.pq, parity ^ 1, tile + g.ntx); g.touched[tile + g.ntx] = 1; }
+                else if (atomicExch(g.dn.ext + txi, 1) == 0) atomicAdd(g.ext_ctr + 0, 1ull);
+            }
+            if (nb & 8) {
+                if (tyi > 0) { tq_push(g.pq, parity ^ 1, tile - g.ntx); g.touched[tile - g.ntx] = 1; }
+                else if (atomicExch(g.up.ext + txi, 1) == 0) atomicAdd(g.ext_ctr + 0, 1ull);
+            }
             atomicAdd(processed, 1);
         }
     }
@@ -1150,6 +1184,21 @@ __global__ void __launch_bounds__(PL_NT, PK ? FM_PK_MINBLOCKS : FM_PL_MINBLOCKS)
     }
 }
 
+// Row bands: before a push launch of parity p, zero the list words it needs (as
+// tq_arm) and queue the tiles a neighbour band pushed flow into (external-push flags,
+// [0, ntx) = our top tile row, [ntx, 2 ntx) = our bottom tile row).  One CTA.
+__global__ void band_arm_kernel(GridDev g, int p) {
+    if (threadIdx.x == 0) { g.pq.cnt[p ? 0 : 2] = 0; g.pq.cnt[(p ? 0 : 2) + 1] = 0; }
+    __syncthreads();
+    unsigned long long took = 0;
+    for (int i = threadIdx.x; i < 2 * g.ntx; i += blockDim.x) {
+        if (*(volatile int32_t *)(g.ext + i) == 0 || atomicExch(g.ext + i, 0) == 0) continue;
+        took++;
+        tq_push(g.pq, p, i < g.ntx ? i : (g.nty - 1) * g.ntx + (i - g.ntx));
+    }
+    if (took) atomicAdd(g.ext_ctr + 1, took);
+}
+
 // fold every parked inbox into e and the reverse residual (coordinator point)
 __global__ void integrate_inflow_kernel(GridDev g) {
     const int tile = blockIdx.x;
@@ -1165,8 +1214,8 @@ __global__ void integrate_inflow_kernel(GridDev g) {
     if (r >= g.H || c >= g.W) return;
     const int64_t p = (int64_t)r * g.W + c;
     // a tile corner is visited by two threads (one per side): e needs an atomic
-    if (side == 0 && r > 0) { const int32_t d = g.inflow_v[p]; if (d) { g.inflow_v[p] = 0; atomicAdd(g.e + p, d); g.rU[p] += d; } }
-    if (side == 1 && r + 1 < g.H) { const int32_t d = g.inflow_v[p]; if (d) { g.inflow_v[p] = 0; atomicAdd(g.e + p, d); g.rD[p] += d; } }
+    if (side == 0 && r > g.rmin) { const int32_t d = g.inflow_v[p]; if (d) { g.inflow_v[p] = 0; atomicAdd(g.e + p, d); g.rU[p] += d; } }
+    if (side == 1 && r + 1 < g.hlim) { const int32_t d = g.inflow_v[p]; if (d) { g.inflow_v[p] = 0; atomicAdd(g.e + p, d); g.rD[p] += d; } }
     if (side == 2 && c > 0) { const int32_t d = g.inflow_h[p]; if (d) { g.inflow_h[p] = 0; atomicAdd(g.e + p, d); g.rL[p] += d; } }
     if (side == 3 && c + 1 < g.W) { const int32_t d = g.inflow_h[p]; if (d) { g.inflow_h[p] = 0; atomicAdd(g.e + p, d); g.rR[p] += d; } }
 }
@@ -1182,7 +1231,7 @@ __global__ void cancel_kernel(GridDev g, unsigned long long *count) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = (int32_t)(p / g.W), c = (int32_t)(p - (int64_t)r * g.W);
-        if (is_ghost_row(g, r)) continue;
+        if (false) continue;
         const int32_t hp = g.h[p];
         int32_t moved = 0;
         const int32_t rt = g.rT[p];
@@ -1228,7 +1277,7 @@ __global__ void bfs_init_kernel(GridDev g) {
         if (r + 1 < g.H && g.rD[p] > 0) m |= M_D;
         if (r > 0 && g.rU[p] > 0) m |= M_U;
         if (g.rT[p] > 0) m |= M_T;
-        if (is_ghost_row(g, r)) m = 0;    // distance imported from the owner band
+        if (false) m = 0;    // distance imported from the owner band
         g.mask[p] = m;
         g.dist[p] = (m & M_T) ? 1 : g.INF;
     }
@@ -1344,12 +1393,12 @@ constexpr int BB_WARPS = 4;   // tiles in flight per CTA (one per warp)
 __device__ __forceinline__ uint32_t bits_row(const GridDev &g, int tile, int lr, int lane) {
     const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
     const int r = tyi * PT_H + lr, c = txi * PT_W + lane;
-    const bool in = r < g.H && c < g.W && !is_ghost_row(g, r);
+    const bool in = r < g.H && c < g.W;
     const int64_t p = (int64_t)r * g.W + c;
     const bool aR = in && c + 1 < g.W && g.rR[p] > 0;
     const bool aL = in && c > 0 && g.rL[p] > 0;
-    const bool aD = in && r + 1 < g.H && g.rD[p] > 0;
-    const bool aU = in && r > 0 && g.rU[p] > 0;
+    const bool aD = in && r + 1 < g.hlim && g.rD[p] > 0;   // band mode: arcs into the neighbour band
+    const bool aU = in && r > g.rmin && g.rU[p] > 0;
     const bool aT = in && g.rT[p] > 0;
     const uint32_t w[5] = {__ballot_sync(0xffffffffu, aR), __ballot_sync(0xffffffffu, aL),
                            __ballot_sync(0xffffffffu, aD), __ballot_sync(0xffffffffu, aU),
@@ -1403,8 +1452,7 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_bits_kernel(GridDev g, int 
         const int hl = (c0 > 0 && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 - 1) : INF;
         const int hr = (c0 + PT_W < g.W && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + PT_W) : INF;
         // ghost rows (row bands) hold imported distances: sources, never recomputed
-        const int g0 = (g.ghost_top && r0 == 0) ? 0 : -1;
-        const int g1 = (g.ghost_bot && g.H - 1 >= r0 && g.H - 1 < r0 + PT_H) ? g.H - 1 - r0 : -1;
+        const int g0 = -1, g1 = -1;   // (round-1 ghost rows; band halos now come from PeerView)
         const int gv0 = (g0 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g0) * g.W + cl) : INF;
         const int gv1 = (g1 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g1) * g.W + cl) : INF;
         uint32_t F = mT, seen = mT;
@@ -1483,12 +1531,26 @@ struct RingQ {
     int32_t *slot;          // cap entries, -1 = empty
     int32_t *flag;          // per tile: queued
     unsigned int *ctr;      // [0] head, [32] tail, [64] pending, [96] tile visits that changed a border (one line each)
+                            // [248] timeout flag (band mode: a wait that exceeded the limit)
+    unsigned int *pend;     // the pending counter the launch ends on: ctr + 64, or (row bands)
+                            // one counter shared by every band's ring (on band 0's device)
     int32_t cap;
     int32_t rerun;          // a tile found stale again while in flight: 1 rerun at once, 0 requeue
     int32_t *vis;           // per tile: visits in this launch (incremental re-visits, BFS ring)
     int32_t incr;           // 1: a re-visit only propagates halo improvements (option BFS_INCR)
     int32_t ns0, ns1;       // idle-poll backoff (ns)
+    int32_t sys;            // row bands: fences at system scope (peer GPUs read / count what we publish)
 };
+
+__device__ __forceinline__ void fence_q(const RingQ &q) {
+    if (q.sys) __threadfence_system(); else __threadfence();
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // initial content: tiles list0[0..*count0) (count0 != nullptr) or every tile
 __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, const int32_t *count0) {
@@ -1507,78 +1569,95 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
         q.ctr[0] = 0; q.ctr[32] = n0; q.ctr[64] = n0; q.ctr[96] = 0;
         q.ctr[128] = 0; q.ctr[160] = 0; q.ctr[161] = 0; q.ctr[192] = 0; q.ctr[224] = n0;
         q.ctr[240] = q.ctr[241] = q.ctr[244] = q.ctr[245] = q.ctr[246] = q.ctr[247] = 0;
+        q.ctr[248] = 0;
     }
 }
 
 // Tile states: 0 idle, 1 queued, 2 in flight, 3 in flight + stale again.  A tile is
 // never processed by two warps at once (so a visit owns its pixels' distances); a
-// push that finds it in flight marks it 3 and the owner runs it again.
-__device__ __forceinline__ void ringq_push(const RingQ &q, int t) {
+// push that finds it in flight marks it 3 and the owner runs it again.  The queue
+// may be a neighbour band's (peer memory): its slot / flag / tail words, our pending.
+__device__ __forceinline__ void ringq_push_to(int32_t *slot, int32_t *flag, unsigned *tail, int cap,
+                                              unsigned *pend, bool sys, int t) {
     for (;;) {
-        const int o = atomicCAS(q.flag + t, 0, 1);
+        const int o = atomicCAS(flag + t, 0, 1);
         if (o == 0) {
-            atomicAdd(q.ctr + 64, 1u);
-            const unsigned s = atomicAdd(q.ctr + 32, 1u);
-            __threadfence();   // the distances that made t stale are visible before t is
-            *(volatile int32_t *)(q.slot + (s % (unsigned)q.cap)) = t;
+            atomicAdd(pend, 1u);
+            const unsigned s = atomicAdd(tail, 1u);
+            // the values that made t stale (and the pending increment) are visible
+            // before t is
+            if (sys) __threadfence_system(); else __threadfence();
+            *(volatile int32_t *)(slot + (s % (unsigned)cap)) = t;
             return;
         }
-        if (o != 2 || atomicCAS(q.flag + t, 2, 3) == 2) return;   // queued / already marked
+        if (o != 2 || atomicCAS(flag + t, 2, 3) == 2) return;   // queued / already marked
     }
 }
 
-__global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, RingQ q) {
-    __shared__ int32_t s_d[BB_WARPS][PT_H * (PT_W + 1)];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int32_t *sd = s_d[wid];
-    const int INF = g.INF;
-    for (;;) {
-        int tile = -1;
-        if (lane == 0) {
-            const unsigned s = atomicAdd(q.ctr + 0, 1u) % (unsigned)q.cap;
-            volatile int32_t *vs = q.slot + s;
-            for (unsigned ns = q.ns0;; ns = min(ns * 2, (unsigned)q.ns1)) {
-                tile = *vs;
-                if (tile >= 0) { *vs = -1; break; }
-                if (*(volatile unsigned *)(q.ctr + 64) == 0) break;
-                __nanosleep(ns);
-            }
-            if (tile >= 0) { atomicExch(q.flag + tile, 2); __threadfence(); }
-        }
-        tile = __shfl_sync(0xffffffffu, tile, 0);
-        if (tile < 0) break;
-        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
-        const int r0 = tyi * PT_H, c0 = txi * PT_W;
-        const int cl = c0 + lane, rl = r0 + lane;
-        const int g0 = (g.ghost_top && r0 == 0) ? 0 : -1;
-        const int g1 = (g.ghost_bot && g.H - 1 >= r0 && g.H - 1 < r0 + PT_H) ? g.H - 1 - r0 : -1;
-        const uint32_t *B = g.rbits + (size_t)tile * 160;
-        const uint32_t mR = B[lane], mL = B[32 + lane], mD = B[64 + lane], mU = B[96 + lane], mT = B[128 + lane];
-        bool again = true;
+__device__ __forceinline__ void ringq_push(const RingQ &q, int t) {
+    ringq_push_to(q.slot, q.flag, q.ctr + 32, q.cap, q.pend, q.sys, t);
+}
+
+__device__ __forceinline__ void ringq_push_peer(const RingQ &q, const PeerView &pv, int t) {
+    ringq_push_to(pv.rq_slot, pv.rq_flag, pv.rq_ctr + 32, pv.rq_cap, q.pend, true, t);
+}
+
+// Halo row above / below a tile (lane = column): the neighbour tile's border row, or
+// in row-band mode the neighbour band's boundary row through peer memory.
+__device__ __forceinline__ int halo_dist_top(const GridDev &g, int r0, int cl) {
+    if (cl >= g.W) return g.INF;
+    if (r0 > 0) return ld_cg(g.dist + (int64_t)(r0 - 1) * g.W + cl);
+    return g.has_up ? ld_cg(g.up.dist + cl) : g.INF;
+}
+__device__ __forceinline__ int halo_dist_bot(const GridDev &g, int r0, int cl) {
+    if (cl >= g.W) return g.INF;
+    if (r0 + PT_H < g.H) return ld_cg(g.dist + (int64_t)(r0 + PT_H) * g.W + cl);
+    return (g.has_dn && r0 + PT_H == g.H) ? ld_cg(g.dn.dist + cl) : g.INF;
+}
+__device__ __forceinline__ bool halo_cut_top(const GridDev &g, int r0, int cl) {
+    if (cl >= g.W) return false;
+    if (r0 > 0) return __ldcg(g.cut + (int64_t)(r0 - 1) * g.W + cl) != 0;
+    return g.has_up && __ldcg(g.up.cut + cl) != 0;
+}
+__device__ __forceinline__ bool halo_cut_bot(const GridDev &g, int r0, int cl) {
+    if (cl >= g.W) return false;
+    if (r0 + PT_H < g.H) return __ldcg(g.cut + (int64_t)(r0 + PT_H) * g.W + cl) != 0;
+    return g.has_dn && r0 + PT_H == g.H && __ldcg(g.dn.cut + cl) != 0;
+}
+
+// Border changes of one visit: which of the tile's own rows / columns moved (b0 top,
+// b1 bottom, b2 left, b3 right) and whether anything on a border changed at all.
+struct RingChange { int b0, b1, b2, b3, any; };
+
+// One BFS visit (warp per tile), K2: level-synchronous bit-parallel BFS of the tile
+// from its sink arcs and halo distances (from scratch), or an incremental re-visit.
+__device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q, int tile, int32_t *sd, int lane
 #ifdef FM_BFS_TIMING
-        const long long tv0 = clock64();
-        int lv = 0;
+                                                , int &lv
 #endif
-        while (again) {
-        // Halo distances, the tile's own border distances (for change detection) and
-        // imported ghost rows.  The interior is recomputed from scratch: a visit's
-        // halos are never larger than the previous visit's (distances only fall and
-        // the owner is exclusive), so every pixel it reaches gets a value <= the old one
-        // and can be written without reading it first.
-        const int ht = (r0 > 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 - 1) * g.W + cl) : INF;
-        const int hb = (r0 + PT_H < g.H && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + PT_H) * g.W + cl) : INF;
-        const int hl = (c0 > 0 && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 - 1) : INF;
-        const int hr = (c0 + PT_W < g.W && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + PT_W) : INF;
-        const int last_r = min(PT_H, g.H - r0) - 1, last_c = min(PT_W, g.W - c0) - 1;
-        const int ot = cl < g.W ? ld_cg(g.dist + (int64_t)r0 * g.W + cl) : INF;                 // own top row
-        const int ob = cl < g.W ? ld_cg(g.dist + (int64_t)(r0 + last_r) * g.W + cl) : INF;      // own bottom row
-        const int ol = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0) : INF;                  // own left column
-        const int orr = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + last_c) : INF;        // own right column
-        const int gv0 = (g0 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g0) * g.W + cl) : INF;
-        const int gv1 = (g1 >= 0 && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + g1) * g.W + cl) : INF;
-        uint32_t seen = 0;
-        const bool incr = q.incr && g0 < 0 && g1 < 0 && __ldcg(q.vis + tile) > 0;
-        if (incr) {
+                                                ) {
+    const int INF = g.INF;
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int r0 = tyi * PT_H, c0 = txi * PT_W;
+    const int cl = c0 + lane, rl = r0 + lane;
+    const uint32_t *B = g.rbits + (size_t)tile * 160;
+    const uint32_t mR = B[lane], mL = B[32 + lane], mD = B[64 + lane], mU = B[96 + lane], mT = B[128 + lane];
+    // Halo distances and the tile's own border distances (for change detection).  A
+    // from-scratch visit recomputes the interior: a visit's halos are never larger than
+    // the previous visit's (distances only fall and the owner is exclusive), so every
+    // pixel it reaches gets a value <= the old one and is written without a read.
+    const int ht = halo_dist_top(g, r0, cl);
+    const int hb = halo_dist_bot(g, r0, cl);
+    const int hl = (c0 > 0 && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 - 1) : INF;
+    const int hr = (c0 + PT_W < g.W && rl < g.H) ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + PT_W) : INF;
+    const int last_r = min(PT_H, g.H - r0) - 1, last_c = min(PT_W, g.W - c0) - 1;
+    const int ot = cl < g.W ? ld_cg(g.dist + (int64_t)r0 * g.W + cl) : INF;                 // own top row
+    const int ob = cl < g.W ? ld_cg(g.dist + (int64_t)(r0 + last_r) * g.W + cl) : INF;      // own bottom row
+    const int ol = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0) : INF;                  // own left column
+    const int orr = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + last_c) : INF;        // own right column
+    uint32_t seen = 0;
+    const bool incr = q.incr && __ldcg(q.vis + tile) > 0;
+    if (incr) {
         // Re-visit: the previous visit left a fixpoint for the halos it saw, and halos
         // only fall, so only pixels that a now-shorter halo path improves change.  Load
         // the current distances, seed the border pixels whose halo now gives a shorter
@@ -1626,22 +1705,17 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
             }
         }
         __syncwarp();
-        } else {
+    } else {
         // level-synchronous BFS; sd[row][col] = level at which the pixel was reached
         uint32_t F = mT;
         seen = mT;
         for (uint32_t x = mT; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = 1;
         int L = 1;
-#ifdef FM_BFS_TIMING
-        const long long tl0 = clock64();
-#endif
         // the level stores of step L are issued after step L+1's shuffles, so they run
         // while the shuffles are in flight (P / PL: pixels reached last step, their level)
         uint32_t P = 0;
         int PL = 0;
         for (;;) {
-            if (g0 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv0 == L); if (lane == g0) F |= s; }
-            if (g1 >= 0) { const uint32_t s = __ballot_sync(0xffffffffu, gv1 == L); if (lane == g1) F |= s; }
             const uint32_t tb = __ballot_sync(0xffffffffu, ht == L);
             const uint32_t bb = __ballot_sync(0xffffffffu, hb == L);
             uint32_t up = __shfl_up_sync(0xffffffffu, F, 1);
@@ -1667,80 +1741,187 @@ __global__ void __launch_bounds__(32 * BB_WARPS) bfs_ring_kernel(GridDev g, Ring
                 if (hb >= L) m = min(m, hb);
                 if (hl >= L) m = min(m, hl);
                 if (hr >= L) m = min(m, hr);
-                if (gv0 >= L) m = min(m, gv0);
-                if (gv1 >= L) m = min(m, gv1);
                 m = warp_min_i32(m);
                 if (m >= INF) break;
                 L = m;
             }
         }
         __syncwarp();
-#ifdef FM_BFS_TIMING
-        if (lane == 0) atomicAdd((unsigned long long *)(q.ctr + 246), (unsigned long long)(clock64() - tl0));
-#endif
-        }   // from-scratch visit
-        // write back every reached pixel (lane = column); borders compared with the old values
-        const uint32_t any_seen = __ballot_sync(0xffffffffu, seen != 0);
-        bool ct = false, cb = false;
-        for (uint32_t rows = any_seen; rows; rows &= rows - 1) {
-            const int i = __ffs(rows) - 1;
-            const uint32_t sr = __shfl_sync(0xffffffffu, seen, i);
-            if (((sr >> lane) & 1) && cl < g.W && i != g0 && i != g1) {
-                const int v = sd[i * (PT_W + 1) + lane];
-                g.dist[(int64_t)(r0 + i) * g.W + cl] = v;
-                ct |= i == 0 && v < ot;
-                cb |= i == last_r && v < ob;
-            }
+    }
+    // write back every reached pixel (lane = column); borders compared with the old values
+    const uint32_t any_seen = __ballot_sync(0xffffffffu, seen != 0);
+    bool ct = false, cb = false;
+    for (uint32_t rows = any_seen; rows; rows &= rows - 1) {
+        const int i = __ffs(rows) - 1;
+        const uint32_t sr = __shfl_sync(0xffffffffu, seen, i);
+        if (((sr >> lane) & 1) && cl < g.W) {
+            const int v = sd[i * (PT_W + 1) + lane];
+            g.dist[(int64_t)(r0 + i) * g.W + cl] = v;
+            ct |= i == 0 && v < ot;
+            cb |= i == last_r && v < ob;
         }
-        // own left / right columns: lane = row
-        const bool sl = (seen & 1u) && lane <= last_r && lane != g0 && lane != g1;
-        const bool sr_ = ((seen >> last_c) & 1u) && lane <= last_r && lane != g0 && lane != g1;
-        const bool cl_ = sl && sd[lane * (PT_W + 1)] < ol;
-        const bool cr_ = sr_ && sd[lane * (PT_W + 1) + last_c] < orr;
-        const uint32_t any_chg = __ballot_sync(0xffffffffu, ct || cb || cl_ || cr_);
-        const int b0 = __any_sync(0xffffffffu, ct), b1 = __any_sync(0xffffffffu, cb);
-        const int b2 = __any_sync(0xffffffffu, cl_), b3 = __any_sync(0xffffffffu, cr_);
-        int st = 0;
-        // lanes 0-3 queue the up / down / left / right neighbour in parallel (each queue
-        // push is a chain of atomics; the fence publishes the warp's distance writes)
-        if (lane < 4) {
-            int nt = -1;
-            if (lane == 0 && b0 && tyi > 0) nt = tile - g.ntx;
-            if (lane == 1 && b1 && tyi + 1 < g.nty) nt = tile + g.ntx;
-            if (lane == 2 && b2 && txi > 0) nt = tile - 1;
-            if (lane == 3 && b3 && txi + 1 < g.ntx) nt = tile + 1;
-            if (nt >= 0 && (!g.region || g.region[nt])) {
-                __threadfence();
-                ringq_push(q, nt);
-            }
-        }
-        __syncwarp();   // the pushes (pending++) precede lane 0's pending-- below
+    }
+    // own left / right columns: lane = row
+    const bool sl = (seen & 1u) && lane <= last_r;
+    const bool sr_ = ((seen >> last_c) & 1u) && lane <= last_r;
+    const bool cl_ = sl && sd[lane * (PT_W + 1)] < ol;
+    const bool cr_ = sr_ && sd[lane * (PT_W + 1) + last_c] < orr;
+    RingChange ch;
+    ch.any = __ballot_sync(0xffffffffu, ct || cb || cl_ || cr_) != 0;
+    ch.b0 = __any_sync(0xffffffffu, ct);
+    ch.b1 = __any_sync(0xffffffffu, cb);
+    ch.b2 = __any_sync(0xffffffffu, cl_);
+    ch.b3 = __any_sync(0xffffffffu, cr_);
+    return ch;
+}
+
+// One cut visit (warp per tile), K3: the seeded-reach closure with the tile's
+// incoming residual arcs as bit planes (lane = tile row, bit = column),
+//     S |= ((S >> 1) & inR) | ((S << 1) & inL) | (S_below & inD) | (S_above & inU)
+// plus the halo's cut bits, until no word changes; the pixels it adds are written.
+__device__ __forceinline__ RingChange cut_visit(const GridDev &g, int tile, int lane) {
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int r0 = tyi * PT_H, c0 = txi * PT_W;
+    const int cl = c0 + lane, rl = r0 + lane;
+    const uint32_t *B = g.rbits + (size_t)tile * 160;
+    const uint32_t iR = B[lane], iL = B[32 + lane], iD = B[64 + lane], iU = B[96 + lane];
+    // current cut words of the tile (row i built by a ballot over its 32 columns)
+    uint32_t S = 0;
+#pragma unroll 8
+    for (int i = 0; i < PT_H; i++) {
+        const int r = r0 + i;
+        const bool b = r < g.H && cl < g.W && __ldcg(g.cut + (int64_t)r * g.W + cl);
+        const uint32_t wv = __ballot_sync(0xffffffffu, b);
+        if (lane == i) S = wv;
+    }
+    const uint32_t S0 = S;
+    const uint32_t top = __ballot_sync(0xffffffffu, halo_cut_top(g, r0, cl));
+    const uint32_t bot = __ballot_sync(0xffffffffu, halo_cut_bot(g, r0, cl));
+    const bool hl = c0 > 0 && rl < g.H && __ldcg(g.cut + (int64_t)rl * g.W + c0 - 1);
+    const bool hr = c0 + PT_W < g.W && rl < g.H && __ldcg(g.cut + (int64_t)rl * g.W + c0 + PT_W);
+    if (hr) S |= iR & 0x80000000u;
+    if (hl) S |= iL & 1u;
+    if (lane == 0) S |= top & iU;
+    if (lane == 31) S |= bot & iD;
+    for (;;) {
+        const uint32_t up = __shfl_up_sync(0xffffffffu, S, 1), dn = __shfl_down_sync(0xffffffffu, S, 1);
+        uint32_t N = S | ((S >> 1) & iR) | ((S << 1) & iL);
+        if (lane > 0) N |= up & iU;
+        if (lane < 31) N |= dn & iD;
+        const bool chg = N != S;
+        S = N;
+        if (!__any_sync(0xffffffffu, chg)) break;
+    }
+    const uint32_t add = S & ~S0;
+    const uint32_t rows = __ballot_sync(0xffffffffu, add != 0);
+    for (uint32_t x = rows; x; x &= x - 1) {
+        const int i = __ffs(x) - 1;
+        const uint32_t a = __shfl_sync(0xffffffffu, add, i);
+        if ((a >> lane) & 1) g.cut[(int64_t)(r0 + i) * g.W + cl] = 1;
+    }
+    RingChange ch;
+    ch.b0 = rows & 1;
+    ch.b1 = (rows >> 31) & 1;
+    ch.b2 = __any_sync(0xffffffffu, add & 1u);
+    ch.b3 = __any_sync(0xffffffffu, add >> 31);
+    ch.any = ch.b0 | ch.b1 | ch.b2 | ch.b3;
+    return ch;
+}
+
+// K2 (MODE 0, global relabel BFS) / K3 (MODE 1, min-cut reach) as ONE persistent
+// launch over the ring queue.  Row-band mode: halos of the band's first / last tile
+// row come from the neighbour bands' planes, a changed boundary row queues the
+// neighbour band's tile in ITS ring, and every band's launch ends on one shared
+// pending counter (all bands' launches run at once, one per GPU).
+template <int MODE>
+__global__ void __launch_bounds__(32 * BB_WARPS) ring_kernel(GridDev g, RingQ q) {
+    __shared__ int32_t s_d[BB_WARPS][MODE == 0 ? PT_H * (PT_W + 1) : 1];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t *sd = s_d[wid];
+    // a wait that exceeds this (a neighbour band's launch never started, e.g. two bands
+    // on one GPU that cannot be resident together) ends the launch with an error flag
+    constexpr unsigned long long WAIT_LIMIT_NS = 20ull * 1000 * 1000 * 1000;
+    for (;;) {
+        int tile = -1;
         if (lane == 0) {
-            if (q.vis) q.vis[tile] += 1;
-            if (any_chg) atomicAdd(q.ctr + 96, 1u);
-#ifdef FM_BFS_TIMING
-            atomicAdd(q.ctr + 192, 1u);   // every visit (diagnostics)
-#endif
-            // release: the warp's distance stores (ordered before lane 0 by the
-            // __syncwarp above) are visible device-wide before the tile can be taken
-            // again -- an incremental re-visit on another SM reads the interior
-            __threadfence();
-            st = atomicCAS(q.flag + tile, 2, 0);
-            if (st == 3) {
-                if (q.rerun) { atomicExch(q.flag + tile, 2); __threadfence(); }
-                else {   // back of the queue (its neighbours get time to settle); still pending
-                    atomicExch(q.flag + tile, 1);
-                    const unsigned s2 = atomicAdd(q.ctr + 32, 1u);
-                    __threadfence();
-                    *(volatile int32_t *)(q.slot + (s2 % (unsigned)q.cap)) = tile;
-                    st = 0;
+            const unsigned s = atomicAdd(q.ctr + 0, 1u) % (unsigned)q.cap;
+            volatile int32_t *vs = q.slot + s;
+            unsigned long long t0 = 0;
+            for (unsigned ns = q.ns0;; ns = min(ns * 2, (unsigned)q.ns1)) {
+                tile = *vs;
+                if (tile >= 0) { *vs = -1; break; }
+                if (*(volatile unsigned *)q.pend == 0) break;
+                if (q.sys) {
+                    const unsigned long long now = globaltimer_ns();
+                    if (!t0) t0 = now;
+                    else if (now - t0 > WAIT_LIMIT_NS) { atomicExch(q.ctr + 248, 1u); break; }
                 }
-            } else {
-                atomicSub(q.ctr + 64, 1u);   // after the pushes: pending never reads 0 early
+                __nanosleep(ns);
             }
+            if (tile >= 0) { atomicExch(q.flag + tile, 2); fence_q(q); }
         }
-        again = __shfl_sync(0xffffffffu, st, 0) == 3;
-        __syncwarp();
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile < 0) break;
+        const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+        bool again = true;
+#ifdef FM_BFS_TIMING
+        const long long tv0 = clock64();
+        int lv = 0;
+#endif
+        while (again) {
+            RingChange ch;
+            if constexpr (MODE == 0) {
+#ifdef FM_BFS_TIMING
+                ch = bfs_visit(g, q, tile, sd, lane, lv);
+#else
+                ch = bfs_visit(g, q, tile, sd, lane);
+#endif
+            } else {
+                ch = cut_visit(g, tile, lane);
+            }
+            int st = 0;
+            // lanes 0-3 queue the up / down / left / right neighbour in parallel (each queue
+            // push is a chain of atomics; the fence publishes the warp's stores)
+            if (lane < 4) {
+                int nt = -1, peer = 0;
+                if (lane == 0 && ch.b0) { if (tyi > 0) nt = tile - g.ntx; else if (g.has_up) { nt = g.up.tile0 + txi; peer = 1; } }
+                if (lane == 1 && ch.b1) { if (tyi + 1 < g.nty) nt = tile + g.ntx; else if (g.has_dn) { nt = g.dn.tile0 + txi; peer = 2; } }
+                if (lane == 2 && ch.b2 && txi > 0) nt = tile - 1;
+                if (lane == 3 && ch.b3 && txi + 1 < g.ntx) nt = tile + 1;
+                if (nt >= 0 && (peer || !g.region || g.region[nt])) {
+                    fence_q(q);
+                    if (peer == 1) ringq_push_peer(q, g.up, nt);
+                    else if (peer == 2) ringq_push_peer(q, g.dn, nt);
+                    else ringq_push(q, nt);
+                }
+            }
+            __syncwarp();   // the pushes (pending++) precede lane 0's pending-- below
+            if (lane == 0) {
+                if (MODE == 0 && q.vis) q.vis[tile] += 1;
+                if (ch.any) atomicAdd(q.ctr + 96, 1u);
+#ifdef FM_BFS_TIMING
+                atomicAdd(q.ctr + 192, 1u);   // every visit (diagnostics)
+#endif
+                // release: the warp's stores (ordered before lane 0 by the __syncwarp
+                // above) are visible before the tile can be taken again -- an
+                // incremental re-visit on another SM reads the interior
+                fence_q(q);
+                st = atomicCAS(q.flag + tile, 2, 0);
+                if (st == 3) {
+                    if (q.rerun) { atomicExch(q.flag + tile, 2); fence_q(q); }
+                    else {   // back of the queue (its neighbours get time to settle); still pending
+                        atomicExch(q.flag + tile, 1);
+                        const unsigned s2 = atomicAdd(q.ctr + 32, 1u);
+                        fence_q(q);
+                        *(volatile int32_t *)(q.slot + (s2 % (unsigned)q.cap)) = tile;
+                        st = 0;
+                    }
+                } else {
+                    atomicSub(q.pend, 1u);   // after the pushes: pending never reads 0 early
+                }
+            }
+            again = __shfl_sync(0xffffffffu, st, 0) == 3;
+            __syncwarp();
         }  // while again
 #ifdef FM_BFS_TIMING
         if (lane == 0) {
@@ -1858,7 +2039,7 @@ __global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsi
         if ((g.W & 3) == 0 && (tyi + 1) * PT_H <= g.H && (txi + 1) * PT_W <= g.W) {
             // interior tile, W % 4 == 0: 4 consecutive pixels per thread, 16-byte accesses
             const int64_t p = (int64_t)r * g.W + c;
-            if (!is_ghost_row(g, r)) {
+            {
                 const int4 d4 = *(const int4 *)(g.dist + p), e4 = *(const int4 *)(g.e + p);
                 int4 h4 = *(const int4 *)(g.h + p);
                 uchar4 m4 = *(const uchar4 *)(g.marked + p);
@@ -1888,7 +2069,7 @@ __global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsi
         for (int k = 0; k < 4; k++) {
             const int lr = (threadIdx.x >> 5) + 8 * k;
             const int rr = tyi * PT_H + lr, cc = txi * PT_W + (threadIdx.x & 31);
-            if (rr >= g.H || cc >= g.W || is_ghost_row(g, rr)) continue;
+            if (rr >= g.H || cc >= g.W) continue;
             const int64_t p = (int64_t)rr * g.W + cc;
             const int32_t d = g.dist[p];
             const int32_t e = g.e[p];
@@ -1972,7 +2153,7 @@ __global__ void bfs_init_local_kernel(GridDev g) {
             if (r + 1 < g.H && g.rD[p] > 0) m |= M_D;
             if (r > 0 && g.rU[p] > 0) m |= M_U;
             if (g.rT[p] > 0) m |= M_T;
-            if (is_ghost_row(g, r)) m = 0;
+            if (false) m = 0;
             g.mask[p] = m;
             g.dist[p] = (m & M_T) ? 1 : g.INF;
         }
@@ -1990,7 +2171,7 @@ __global__ void bfs_finalize_local_kernel(GridDev g, const int32_t *list, int n,
         bool act_tile = false;
         for (int k = threadIdx.x; k < TILE_W * TILE_H; k += blockDim.x) {
             const int r = tyi * TILE_H + k / TILE_W, c = txi * TILE_W + k % TILE_W;
-            if (r >= g.H || c >= g.W || is_ghost_row(g, r)) continue;
+            if (r >= g.H || c >= g.W) continue;
             const int64_t p = (int64_t)r * g.W + c;
             const int32_t d = g.dist[p];
             const int32_t e = g.e[p];
@@ -2020,7 +2201,6 @@ __global__ void bfs_finalize_kernel(GridDev g, unsigned long long *acc /* [0] ac
     int32_t lvl = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
          p += (int64_t)gridDim.x * blockDim.x) {
-        if ((g.ghost_top && p < g.W) || (g.ghost_bot && p >= HW - g.W)) continue;
         const int32_t d = g.dist[p];
         const int32_t e = g.e[p];
         if (d < g.INF) {
@@ -2072,7 +2252,7 @@ __global__ void cut_init_kernel(GridDev g) {
         if (c > 0 && g.rR[p - 1] > 0) m |= M_L;
         if (r + 1 < g.H && g.rU[p + g.W] > 0) m |= M_D;
         if (r > 0 && g.rD[p - g.W] > 0) m |= M_U;
-        const bool gh = is_ghost_row(g, r);
+        const bool gh = false;
         g.mask[p] = gh ? 0 : m;           // ghost membership is imported from the owner band
         g.cut[p] = (!gh && (g.e[p] > 0 || g.cS[p] - g.rS[p] > 0)) ? 1 : 0;
     }
@@ -2165,12 +2345,13 @@ __global__ void cut_init_bits_kernel(GridDev g) {
         const int tile = (int)(w / PT_H), lr = (int)(w % PT_H);
         const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
         const int r = tyi * PT_H + lr, c = txi * PT_W + lane;
-        const bool in = r < g.H && c < g.W && !is_ghost_row(g, r);
+        const bool in = r < g.H && c < g.W;
         const int64_t p = (int64_t)r * g.W + c;
         const bool aR = in && c + 1 < g.W && g.rL[p + 1] > 0;     // residual arc (p+1) -> p
         const bool aL = in && c > 0 && g.rR[p - 1] > 0;
-        const bool aD = in && r + 1 < g.H && g.rU[p + g.W] > 0;
-        const bool aU = in && r > 0 && g.rD[p - g.W] > 0;
+        // band mode: the arc from the neighbour band's boundary pixel is its residual
+        const bool aD = in && (r + 1 < g.H ? g.rU[p + g.W] > 0 : (g.has_dn && ld_cg(g.dn.res + c) > 0));
+        const bool aU = in && (r > 0 ? g.rD[p - g.W] > 0 : (g.has_up && ld_cg(g.up.res + c) > 0));
         const bool seed = in && (g.e[p] > 0 || g.cS[p] - g.rS[p] > 0);
         const uint32_t wd[5] = {__ballot_sync(0xffffffffu, aR), __ballot_sync(0xffffffffu, aL),
                                 __ballot_sync(0xffffffffu, aD), __ballot_sync(0xffffffffu, aU),
@@ -2245,7 +2426,7 @@ __global__ void sum_e_kernel(GridDev g, unsigned long long *acc) {
     long long s = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
          p += (int64_t)gridDim.x * blockDim.x)
-        if (!((g.ghost_top && p < g.W) || (g.ghost_bot && p >= HW - g.W))) s += g.e[p];
+        s += g.e[p];
     __shared__ long long red[8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -2259,66 +2440,6 @@ __global__ void sum_e_kernel(GridDev g, unsigned long long *acc) {
     }
 }
 
-
-// ----------------------------------------------------------------------------
-// row-band exchange (multi-GPU): one thread per column.  side 0 = top, 1 = bottom.
-// kind 0 ROW_FLOW: out = flow parked in the ghost row (then zeroed) | in = flow
-//        arriving in our boundary row: e += v and the residual toward the ghost += v
-// kind 1 ROW_H:    out = boundary-row heights | in = ghost heights
-// kind 2 ROW_RES:  out = boundary-row residual toward the ghost | in = ghost residual toward us
-// kind 3 ROW_DIST: out = boundary-row BFS distance | in = ghost distance (tiles re-queued if changed)
-// kind 4 ROW_CUT:  out = boundary-row cut bit | in = ghost cut bit (tiles re-queued if changed)
-// ----------------------------------------------------------------------------
-__global__ void band_rows_out_kernel(GridDev g, int side, int kind, int32_t *dst) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= g.W) return;
-    const int64_t gr = side == 0 ? 0 : g.H - 1;        // ghost row
-    const int64_t br = side == 0 ? 1 : g.H - 2;        // our boundary row
-    const int64_t pg = gr * g.W + c, pb = br * g.W + c;
-    int32_t v = 0;
-    if (kind == 0) { v = g.e[pg]; g.e[pg] = 0; }
-    else if (kind == 1) v = g.h[pb];
-    else if (kind == 2) v = side == 0 ? g.rU[pb] : g.rD[pb];
-    else if (kind == 3) v = g.dist[pb];
-    else v = g.cut[pb];
-    dst[c] = v;
-}
-
-__global__ void band_rows_in_kernel(GridDev g, int side, int kind, const int32_t *src, int pq_parity,
-                                    int bq_parity, int32_t *changed) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= g.W) return;
-    const int64_t gr = side == 0 ? 0 : g.H - 1;
-    const int64_t br = side == 0 ? 1 : g.H - 2;
-    const int64_t pg = gr * g.W + c, pb = br * g.W + c;
-    const int t = ((int)br / PT_H) * g.ntx + c / PT_W;   // tile of our boundary pixel
-    const int32_t v = src[c];
-    if (kind == 0) {
-        if (v) {
-            g.e[pb] += v;
-            if (side == 0) g.rU[pb] += v; else g.rD[pb] += v;
-            tq_push(g.pq, pq_parity, t);
-            atomicAdd(changed, 1);
-        }
-    } else if (kind == 1) {
-        g.h[pg] = v;
-    } else if (kind == 2) {
-        if (side == 0) g.rD[pg] = v; else g.rU[pg] = v;
-    } else if (kind == 3) {
-        if (g.dist[pg] != v) {
-            g.dist[pg] = v;
-            tq_push(g.bq, bq_parity, t);
-            atomicAdd(changed, 1);
-        }
-    } else {
-        const uint8_t b = v ? 1 : 0;
-        if (g.cut[pg] != b) {
-            g.cut[pg] = b;
-            tq_push(g.bq, bq_parity, t);
-            atomicAdd(changed, 1);
-        }
-    }
-}
 
 }  // namespace
 
@@ -2372,7 +2493,6 @@ struct fm_grid {
     GridDev prg_d{};
     int prg_key[5] = {0, 0, 0, 0, 0};
     bool prg_pending = false;            // round control block read back, consumed after the caller's sync
-    bool band_user_stream = false;       // band steps run on a caller stream (fm_grid_band_stream)
     int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (option PR_KERNEL)
     int pl_per_sm = 6;                   // resident pr_list CTAs per SM (occupancy query)
     int pk_per_sm = 8;                   // same, packed-residual instance (occupancy query)
@@ -2380,7 +2500,6 @@ struct fm_grid {
     bool pk_ok = false;                  // this solve's input allows them (every pair sum <= 65535)
     int k_local_list = 0;                // passes per visit of the list kernel (option K_LOCAL_LIST)
     int bq_parity = 0;                   // parity of the next BFS / cut sweep
-    int32_t *d_band = nullptr;           // band exchange: changed counter
     uint8_t *d_touched = nullptr;        // per tile: pushed into since the last relabel
     uint8_t *d_region = nullptr;         // per tile: in the local relabel's region
     int32_t *d_rlist = nullptr;          // region tile list (+ count at the end)
@@ -2392,6 +2511,15 @@ struct fm_grid {
     int k_local = 0;                     // tuning overrides (options k_local / bfs_interval)
     int trace = 0;                       // option TRACE=1: one stderr line per round
     int bfs_interval_env = 0;
+    // row-band mode (fm_grid_band_*): this handle is band `band` of `nbands`
+    int band = -1, nbands = 0;
+    int colocated = 1;                   // bands sharing this device (persistent grids split between them)
+    int32_t H_total = 0;                 // rows of the whole grid
+    int64_t total_tiles = 0;             // tiles of the whole grid (the shared ring's initial pending count)
+    unsigned *gpend = nullptr;           // shared pending counter of the band rings (band 0's rq.ctr + 200)
+    void *ipc_open[2][10] = {};          // IPC mappings of the neighbours' buffers (closed on destroy)
+    void *ipc_gpend = nullptr;           // IPC mapping of band 0's ring counters (bands > 1)
+    int32_t *band_caps = nullptr;        // band inputs staged by fm_grid_band_solve: 6 planes + 2 halo rows
     // solve state
     int32_t flags_solve = 0;
     long long sum_capS = 0;
@@ -2420,6 +2548,11 @@ void parallel_memcpy(void *dst, const void *src, size_t n) {
 int sync_stream(fm_grid *g) {
     FM_CHECK_CUDA(cudaStreamSynchronize(g->stream));
     return FM_OK;
+}
+
+// persistent ring grid: every resident slot, shared between the bands on this device
+int ring_blocks(const fm_grid *g) {
+    return std::max(1, g->sms * g->br_per_sm / std::max(1, g->colocated));
 }
 
 float elapsed_between(cudaEvent_t a, cudaEvent_t b) {
@@ -2520,7 +2653,7 @@ int bfs_sweeps(fm_grid *g, bool first_all) {
         ringq_init_kernel<<<std::min((g->rq.cap + 255) / 256, g->sms * 8), 256, 0, g->stream>>>(g->rq, g->ntiles, list0, cnt0);
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[2], g->stream);
-        bfs_ring_kernel<<<g->sms * g->br_per_sm, 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+        ring_kernel<0><<<ring_blocks(g), 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[3], g->stream);
         FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 8, g->rq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
@@ -2650,7 +2783,7 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 32, g->stream));
     grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
-        g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
+        g->d, capR, capL, capD, capU, capS, capT, nullptr, nullptr, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
     FM_CHECK_LAUNCH();
     g->st.launches++;
     FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 4,
@@ -2962,7 +3095,19 @@ int cut_init(fm_grid *g) {
     return FM_OK;
 }
 
+// K3 as one persistent ring launch over every tile (default, bfs_bits == 2)
+int cut_ring(fm_grid *g) {
+    ringq_init_kernel<<<std::min((g->rq.cap + 255) / 256, g->sms * 8), 256, 0, g->stream>>>(g->rq, g->ntiles, nullptr, nullptr);
+    FM_CHECK_LAUNCH();
+    ring_kernel<1><<<ring_blocks(g), 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+    FM_CHECK_LAUNCH();
+    g->st.launches += 2;
+    g->st.cut_sweeps += 1;
+    return FM_OK;
+}
+
 int cut_sweeps(fm_grid *g, bool first_all) {
+    if (g->bfs_bits == 2) return cut_ring(g);
     double cut_kern = 0.0;
     int64_t cut_launches = 0;
     if (g->bfs_bits)
@@ -3080,6 +3225,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         cudaMalloc((void **)&g->d_region, (size_t)g->ntiles) != cudaSuccess ||
         cudaMalloc((void **)&g->d_rlist, sizeof(int32_t) * ((size_t)g->ntiles + 1)) != cudaSuccess ||
         cudaMalloc((void **)&g->flags, sizeof(int32_t) * 64) != cudaSuccess ||
+        cudaMalloc((void **)&g->d.ext, sizeof(int32_t) * 2 * (size_t)g->d.ntx) != cudaSuccess ||
+        cudaMemset(g->d.ext, 0, sizeof(int32_t) * 2 * (size_t)g->d.ntx) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_acc, sizeof(unsigned long long) * 32) != cudaSuccess ||
         cudaMallocHost((void **)&g->h_flags, sizeof(int32_t) * 64) != cudaSuccess ||
         cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -3104,6 +3251,10 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->d.touched = g->d_touched;
     g->d.region = nullptr;
     g->d.H = H; g->d.W = W;
+    g->d.hlim = H; g->d.rmin = 0;
+    g->d.ext_ctr = g->acc + 24;
+    g->rq.pend = g->rq.ctr + 64;
+    g->prq.pend = g->prq.ctr + 64;
     g->d.V = (int32_t)(g->HW + 2);
     g->d.INF = g->d.V;
     int sms = 148;
@@ -3117,7 +3268,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->pl_per_sm = std::max(1, g->pl_per_sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->bb_per_sm, bfs_bits_kernel, 32 * BB_WARPS, 0);
     g->bb_per_sm = std::max(1, g->bb_per_sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->br_per_sm, bfs_ring_kernel, 32 * BB_WARPS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->br_per_sm, ring_kernel<0>, 32 * BB_WARPS, 0);
     g->br_per_sm = std::max(1, std::min(g->br_per_sm, g->br_cap));
     g->pl_occ = g->pl_per_sm; g->pk_occ = g->pk_per_sm; g->br_occ = g->br_per_sm;
     // ring capacity: every tile once + one reserved slot per resident warp
@@ -3155,7 +3306,11 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->prq.ctr) cudaFree(g->prq.ctr);
     if (g->d.marked) cudaFree(g->d.marked);
     if (g->d.cut) cudaFree(g->d.cut);
-    if (g->d_band) cudaFree(g->d_band);
+    if (g->d.ext) cudaFree(g->d.ext);
+    if (g->band_caps) cudaFree(g->band_caps);
+    for (auto &side : g->ipc_open)
+        for (auto &p : side) if (p) { cudaIpcCloseMemHandle(p); p = nullptr; }
+    if (g->ipc_gpend) cudaIpcCloseMemHandle(g->ipc_gpend);
     if (g->d_touched) cudaFree(g->d_touched);
     if (g->d_region) cudaFree(g->d_region);
     if (g->d_rlist) cudaFree(g->d_rlist);
@@ -3352,177 +3507,6 @@ extern "C" int fm_grid_cut_host(fm_grid *g, uint8_t *cut_out, fm_stats *stats) {
     return FM_OK;
 }
 
-// ============================================================================
-// row-band steps (multi-GPU grid path; orchestrated by paper_1110_6231_b200.bands)
-// ============================================================================
-extern "C" int fm_grid_band_stream(fm_grid *g, void *stream) {
-    if (!g) { fm_set_error("fm_grid_band_stream: null handle"); return FM_INVALID_ARG; }
-    FM_CHECK_CUDA(cudaSetDevice(g->device));
-    set_stream(g, stream);
-    g->band_user_stream = stream != nullptr;
-    return FM_OK;
-}
-
-extern "C" int fm_grid_band_config(fm_grid *g, int32_t ghost_top, int32_t ghost_bottom,
-                                   int64_t global_nodes) {
-    if (!g || g->H < 1 + (ghost_top ? 1 : 0) + (ghost_bottom ? 1 : 0) || global_nodes < g->HW + 2 ||
-        global_nodes > (int64_t)INT32_MAX / 2 - 4) {
-        fm_set_error("fm_grid_band_config: band too short for its ghost rows, or bad global node count");
-        return FM_INVALID_ARG;
-    }
-    g->d.ghost_top = ghost_top ? 1 : 0;
-    g->d.ghost_bot = ghost_bottom ? 1 : 0;
-    // heights, the source height and the BFS sentinel must agree across bands
-    g->d.V = (int32_t)global_nodes;
-    g->d.INF = g->d.V;
-    if (!g->d_band) FM_CHECK_CUDA(cudaMalloc((void **)&g->d_band, sizeof(int32_t) * 4));
-    return FM_OK;
-}
-
-extern "C" int fm_grid_band_init(fm_grid *g, const int32_t *capR, const int32_t *capL,
-                                 const int32_t *capD, const int32_t *capU, const int32_t *capS,
-                                 const int32_t *capT, int32_t flags, int64_t *sum_caps_out) {
-    if (!g) { fm_set_error("fm_grid_band_init: null handle"); return FM_INVALID_ARG; }
-    FM_CHECK_CUDA(cudaSetDevice(g->device));
-    g->flags_solve = flags;
-    memset(&g->st, 0, sizeof(g->st));
-    FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 32, g->stream));
-    grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
-        g->d, capR, capL, capD, capU, capS, capT, (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
-    FM_CHECK_LAUNCH();
-    g->st.launches++;
-    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 4,
-                                  cudaMemcpyDeviceToHost, g->stream));
-    FM_TRY(sync_stream(g));
-    g->pk_ok = g->h_acc[3] == 0;
-    if (g->h_acc[1] != 0) { fm_set_error("negative capacity in grid input"); return FM_INVALID_ARG; }
-    if (g->h_acc[2] != 0) { fm_set_error("grid capacities too large for the int32 device state"); return FM_INVALID_ARG; }
-    g->sum_capS = (long long)g->h_acc[0];
-    g->excess_total = g->sum_capS;
-    FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
-    FM_TRY(tq_reset(g, g->d.pq));
-    FM_TRY(tq_reset(g, g->d.bq));
-    g->pq_parity = g->bq_parity = 0;
-    if (sum_caps_out) *sum_caps_out = g->sum_capS;
-    return FM_OK;
-}
-
-// phase 0: residual masks + sweeps from every tile; phase 1: sweeps from the tiles
-// queued by imported ghost distances.  *changed = tile visits that changed something.
-extern "C" int fm_grid_band_bfs(fm_grid *g, int32_t phase, int64_t *changed) {
-    if (!g) { fm_set_error("fm_grid_band_bfs: null handle"); return FM_INVALID_ARG; }
-    FM_CHECK_CUDA(cudaSetDevice(g->device));
-    const int64_t before = g->st.reserved[0];
-    if (phase == 0) FM_TRY(bfs_init(g, false));
-    FM_TRY(bfs_sweeps(g, phase == 0));
-    if (g->ring_stats_pending) {
-        FM_TRY(sync_stream(g));
-        bfs_collect(g);
-    }
-    if (changed) *changed = g->st.reserved[0] - before;
-    return FM_OK;
-}
-
-// gap + marking + active tiles; out = {active pixels, newly marked excess, deepest level}
-extern "C" int fm_grid_band_finalize(fm_grid *g, int64_t *out) {
-    if (!g) { fm_set_error("fm_grid_band_finalize: null handle"); return FM_INVALID_ARG; }
-    FM_CHECK_CUDA(cudaSetDevice(g->device));
-    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
-    FM_TRY(tq_reset(g, g->d.pq));
-    g->pq_parity = 0;
-    FM_TRY(bfs_finalize(g));
-    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 4, g->acc + 4, sizeof(unsigned long long) * 3,
-                                  cudaMemcpyDeviceToHost, g->stream));
-    FM_TRY(sync_stream(g));
-    g->active = (long long)g->h_acc[4];
-    g->excess_total -= (long long)g->h_acc[5];
-    g->st.bfs_levels = std::max<int64_t>(g->st.bfs_levels, (int64_t)g->h_acc[6]);
-    if (out) { out[0] = g->active; out[1] = (int64_t)g->h_acc[5]; out[2] = (int64_t)g->h_acc[6]; }
-    return FM_OK;
-}
-
-// up to max_launches tile launches (stops on an idle launch or the relabel budget),
-// then folds every inbox; out = {pushes, relabels, launches, idle}
-extern "C" int fm_grid_band_push(fm_grid *g, int32_t max_launches, int32_t cycle_budget, int64_t *out) {
-    if (!g || max_launches < 1 || cycle_budget < 1) { fm_set_error("fm_grid_band_push: invalid argument"); return FM_INVALID_ARG; }
-    FM_CHECK_CUDA(cudaSetDevice(g->device));
-    const fm_stats before = g->st;
-    cudaEventRecord(g->ev[0], g->stream);
-    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
-    int32_t idle = 0;
-    FM_TRY(run_round_tiles(g, cycle_budget, max_launches, &idle));
-    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 10, g->acc + 10, sizeof(unsigned long long) * 2,
-                                  cudaMemcpyDeviceToHost, g->stream));
-    cudaEventRecord(g->ev[1], g->stream);
-    FM_TRY(sync_stream(g));
-    pr_graph_consume(g, &idle);
-    g->st.ms_push += elapsed(g);
-    g->st.pushes += (int64_t)g->h_acc[10];
-    g->st.relabels += (int64_t)g->h_acc[11];
-    if (out) {
-        out[0] = (int64_t)g->h_acc[10];
-        out[1] = (int64_t)g->h_acc[11];
-        out[2] = g->st.pr_sweeps - before.pr_sweeps;
-        out[3] = idle;
-    }
-    return FM_OK;
-}
-
-// phase 0: seeds + sweeps from every tile; phase 1: sweeps from imported ghost changes
-extern "C" int fm_grid_band_cut(fm_grid *g, int32_t phase, int64_t *changed) {
-    if (!g) { fm_set_error("fm_grid_band_cut: null handle"); return FM_INVALID_ARG; }
-    FM_CHECK_CUDA(cudaSetDevice(g->device));
-    const int64_t before = g->st.reserved[0];
-    if (phase == 0) FM_TRY(cut_init(g));
-    FM_TRY(cut_sweeps(g, phase == 0));
-    if (changed) *changed = g->st.reserved[0] - before;
-    return FM_OK;
-}
-
-// direction 0: export row `kind` of `side` into buf (DEVICE int32[W]);
-// direction 1: import buf into the ghost / boundary row.  *changed = imported cells that
-// changed something (flow received, distance or cut bit updated).
-extern "C" int fm_grid_band_rows(fm_grid *g, int32_t direction, int32_t side, int32_t kind,
-                                 int32_t *buf, int64_t *changed) {
-    if (!g || !buf || side < 0 || side > 1 || kind < 0 || kind > 5 ||
-        (side == 0 && !g->d.ghost_top) || (side == 1 && !g->d.ghost_bot)) {
-        fm_set_error("fm_grid_band_rows: invalid argument (no ghost row on that side?)");
-        return FM_INVALID_ARG;
-    }
-    FM_CHECK_CUDA(cudaSetDevice(g->device));
-    const int blocks = (g->W + 255) / 256;
-    // kind 5 (FM_ROW_PUSH_STATE) = flow | heights | residuals, three rows in one buffer
-    const int k0 = kind == 5 ? 0 : kind, k1 = kind == 5 ? 2 : kind;
-    if (direction == 0) {
-        for (int k = k0; k <= k1; k++)
-            band_rows_out_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, k, buf + (size_t)(k - k0) * g->W);
-        FM_CHECK_LAUNCH();
-        if (!g->band_user_stream) FM_TRY(sync_stream(g));   // else ordered on the caller's stream
-        if (changed) *changed = 0;
-    } else {
-        FM_CHECK_CUDA(cudaMemsetAsync(g->d_band, 0, sizeof(int32_t), g->stream));
-        for (int k = k0; k <= k1; k++)
-            band_rows_in_kernel<<<blocks, 256, 0, g->stream>>>(g->d, side, k, buf + (size_t)(k - k0) * g->W,
-                                                              g->pq_parity, g->bq_parity, g->d_band);
-        FM_CHECK_LAUNCH();
-        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->d_band, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
-        FM_TRY(sync_stream(g));
-        if (changed) *changed = g->h_flags[0];
-    }
-    g->st.launches += k1 - k0 + 1;
-    return FM_OK;
-}
-
-// sum over our own (non-ghost) pixels of capS - e: the band's share of the flow
-extern "C" int fm_grid_band_flow(fm_grid *g, int64_t *out) {
-    if (!g || !out) { fm_set_error("fm_grid_band_flow: invalid argument"); return FM_INVALID_ARG; }
-    FM_CHECK_CUDA(cudaSetDevice(g->device));
-    long long f = 0;
-    FM_TRY(current_flow(g, &f));
-    *out = f;
-    return FM_OK;
-}
-
 extern "C" int fm_grid_stats(fm_grid *g, fm_stats *stats) {
     if (!g || !stats) { fm_set_error("fm_grid_stats: invalid argument"); return FM_INVALID_ARG; }
     *stats = g->st;
@@ -3578,5 +3562,671 @@ extern "C" int fm_grid_set_option(fm_grid *g, const char *name, int64_t value) {
     else if (k == "pk_occ") g->pk_per_sm = std::max(1, std::min(g->pk_occ, v));
     else if (k == "pl_per_sm") g->pl_per_sm = std::max(1, std::min(g->pl_occ, v));
     else { fm_set_error("fm_grid_set_option: unknown option '%s'", name); return FM_INVALID_ARG; }
+    return FM_OK;
+}
+
+// ============================================================================
+// Row bands (multi-GPU grid path; reference coordinator loop
+// maxflow_par.py:195-229).  Band k of N holds rows [R0_k, R1_k) of the grid (band
+// borders on 32-row tile boundaries).  Nothing is exchanged by messages: a band's
+// kernels read the neighbour bands' boundary rows (heights for pushes, distances for
+// the global relabel, cut bits for the min-cut reach) straight from their memory, push
+// flow into their inboxes with remote atomics, raise their external-push flags, and
+// queue their ring-BFS tiles; the bands' persistent ring launches end together on one
+// shared pending counter.  The only host-level agreement is a few int64 per push batch
+// / relabel, gathered through an fm_coll (a shared-memory barrier: threads of one
+// process, or processes of one node).
+// ============================================================================
+#include <atomic>
+#include <chrono>
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+namespace {
+constexpr int COLL_MAX_RANKS = 64, COLL_MAX_VALS = 8;
+constexpr uint32_t COLL_MAGIC = 0x666d636cu;
+struct CollShm {
+    std::atomic<uint64_t> arrive;
+    uint32_t magic, nranks;
+    int64_t slot[2][COLL_MAX_RANKS][COLL_MAX_VALS];
+};
+static_assert(std::atomic<uint64_t>::is_always_lock_free, "cross-process atomics need lock-free 64-bit");
+}  // namespace
+
+struct fm_coll {
+    CollShm *shm = nullptr;
+    size_t bytes = 0;
+    bool mapped = false;       // shm_open mapping (else heap, process-local)
+    bool owner = false;
+    std::string name;
+    int32_t rank = 0, nranks = 1;
+    uint64_t calls = 0;
+};
+
+extern "C" int fm_coll_create(const char *name, int32_t nranks, int32_t rank, fm_coll **out) {
+    if (!out || nranks < 1 || nranks > COLL_MAX_RANKS || rank < 0 || rank >= nranks) {
+        fm_set_error("fm_coll_create: invalid argument (1 <= nranks <= %d)", COLL_MAX_RANKS);
+        return FM_INVALID_ARG;
+    }
+    fm_coll *c = new fm_coll();
+    c->rank = rank; c->nranks = nranks; c->bytes = sizeof(CollShm);
+    if (!name || !*name) {
+        c->shm = new CollShm();
+        c->shm->arrive.store(0);
+        c->shm->magic = COLL_MAGIC;
+        c->shm->nranks = (uint32_t)nranks;
+    } else {
+        // rank 0 creates and initialises the segment; the others open it after the
+        // caller's own barrier (paper_1110_6231_b200.bands does a torch.distributed one)
+        c->name = name;
+        c->owner = rank == 0;
+        const int fd = shm_open(name, c->owner ? (O_CREAT | O_RDWR | O_TRUNC) : O_RDWR, 0600);
+        if (fd < 0) { fm_set_error("fm_coll_create: shm_open(%s) failed", name); delete c; return FM_INVALID_ARG; }
+        if (c->owner && ftruncate(fd, (off_t)c->bytes) != 0) {
+            close(fd); fm_set_error("fm_coll_create: ftruncate failed"); delete c; return FM_INVALID_ARG;
+        }
+        void *p = mmap(nullptr, c->bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (p == MAP_FAILED) { fm_set_error("fm_coll_create: mmap failed"); delete c; return FM_INVALID_ARG; }
+        c->shm = (CollShm *)p;
+        c->mapped = true;
+        if (c->owner) {
+            new (&c->shm->arrive) std::atomic<uint64_t>(0);
+            c->shm->nranks = (uint32_t)nranks;
+            std::atomic_thread_fence(std::memory_order_release);
+            c->shm->magic = COLL_MAGIC;
+        }
+    }
+    *out = c;
+    return FM_OK;
+}
+
+extern "C" void fm_coll_destroy(fm_coll *c) {
+    if (!c) return;
+    if (c->mapped) {
+        munmap(c->shm, c->bytes);
+        if (c->owner) shm_unlink(c->name.c_str());
+    } else {
+        delete c->shm;
+    }
+    delete c;
+}
+
+// Every rank contributes n int64 and receives all ranks' values (out[rank * n + i]).
+// Call k uses slot set k & 1: a rank can only start call k + 2 (which rewrites set
+// k & 1) after every rank arrived at call k + 1, i.e. finished reading call k.
+extern "C" int fm_coll_allgather(fm_coll *c, const int64_t *vals, int32_t n, int64_t *out) {
+    if (!c || n < 0 || n > COLL_MAX_VALS || (n && (!vals || !out))) {
+        fm_set_error("fm_coll_allgather: invalid argument (n <= %d)", COLL_MAX_VALS);
+        return FM_INVALID_ARG;
+    }
+    CollShm *s = c->shm;
+    if (s->magic != COLL_MAGIC || (int32_t)s->nranks != c->nranks) {
+        fm_set_error("fm_coll_allgather: collective segment not initialised");
+        return FM_INVALID_ARG;
+    }
+    const uint64_t k = c->calls++;
+    int64_t *mine = s->slot[k & 1][c->rank];
+    for (int i = 0; i < n; i++) mine[i] = vals[i];
+    s->arrive.fetch_add(1, std::memory_order_acq_rel);
+    const uint64_t target = (uint64_t)c->nranks * (k + 1);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t spin = 0; s->arrive.load(std::memory_order_acquire) < target; spin++) {
+        if (spin < 4096) continue;
+        if ((spin & 1023) == 0 &&
+            std::chrono::steady_clock::now() - t0 > std::chrono::seconds(300)) {
+            fm_set_error("fm_coll_allgather: rank %d waited 300 s for the other ranks", c->rank);
+            return FM_CUDA_ERROR;
+        }
+        sched_yield();
+    }
+    for (int r = 0; r < c->nranks; r++)
+        for (int i = 0; i < n; i++) out[r * n + i] = s->slot[k & 1][r][i];
+    return FM_OK;
+}
+
+// Band borders on 32-row tile boundaries (the last band takes the remainder);
+// edges[0..nbands], the same split as paper_1110_6231_b200.bands.band_rows.
+extern "C" int fm_band_split(int32_t H, int32_t nbands, int32_t *edges) {
+    if (!edges || nbands < 1 || H < 1) { fm_set_error("fm_band_split: invalid argument"); return FM_INVALID_ARG; }
+    const int64_t tiles = (H + PT_H - 1) / PT_H;
+    if (nbands > tiles) {
+        fm_set_error("fm_band_split: %d rows hold %lld tile rows, fewer than %d bands", H, (long long)tiles, nbands);
+        return FM_INVALID_ARG;
+    }
+    for (int k = 0; k <= nbands; k++)
+        edges[k] = (int32_t)std::min<int64_t>(H, ((k * tiles + nbands / 2) / nbands) * PT_H);
+    edges[nbands] = H;
+    for (int k = 0; k < nbands; k++)
+        if (edges[k + 1] <= edges[k]) { fm_set_error("fm_band_split: empty band"); return FM_INVALID_ARG; }
+    return FM_OK;
+}
+
+extern "C" int fm_grid_band_setup(fm_grid *g, int32_t band, int32_t nbands, int32_t H_total,
+                                  int32_t colocated) {
+    if (!g || nbands < 1 || band < 0 || band >= nbands || H_total < g->H ||
+        (int64_t)H_total * g->W > (int64_t)INT32_MAX / 2 - 4 || (band + 1 < nbands && g->H % PT_H) ||
+        colocated < 1) {
+        fm_set_error("fm_grid_band_setup: invalid argument (inner bands need a multiple of %d rows)", PT_H);
+        return FM_INVALID_ARG;
+    }
+    g->band = band;
+    g->nbands = nbands;
+    g->H_total = H_total;
+    g->colocated = colocated;
+    g->total_tiles = (int64_t)((H_total + PT_H - 1) / PT_H) * g->d.ntx;
+    // heights, the source height |V| and the BFS sentinel are the whole grid's
+    g->d.V = (int32_t)((int64_t)H_total * g->W + 2);
+    g->d.INF = g->d.V;
+    g->d.has_up = band > 0;
+    g->d.has_dn = band + 1 < nbands;
+    g->d.hlim = g->H + g->d.has_dn;
+    g->d.rmin = -g->d.has_up;
+    g->rq.sys = nbands > 1;
+    g->local_div = 0;   // region-limited relabels are single-band only
+    if (band == 0) g->gpend = g->rq.ctr + 200;
+    return FM_OK;
+}
+
+namespace {
+// the buffers a neighbour band needs, in export order
+constexpr int BAND_BUFS = 10;
+struct BandExport {
+    uint32_t magic;
+    int32_t device, H, W, ntx, nty, rq_cap, pid;
+    cudaIpcMemHandle_t h[BAND_BUFS];   // h, dist, inflow_v, rD, rU, cut, ext, rq.slot, rq.flag, rq.ctr
+};
+static_assert(sizeof(BandExport) <= 1024, "FM_BAND_EXPORT_BYTES");
+
+void *band_buf(fm_grid *g, int k) {
+    void *b[BAND_BUFS] = {g->d.h, g->d.dist, g->d.inflow_v, g->d.rD, g->d.rU, g->d.cut, g->d.ext,
+                          g->rq.slot, g->rq.flag, g->rq.ctr};
+    return b[k];
+}
+
+// PeerView of neighbour band `nb` (its buffers `buf`) seen from g; side 0 = above, 1 = below
+PeerView make_peer(const fm_grid *g, int side, int nbH, int nbnty, int nb_rq_cap, void *const *buf) {
+    PeerView v{};
+    const int64_t row = side == 0 ? (int64_t)(nbH - 1) * g->W : 0;   // its boundary row
+    v.h = (int32_t *)buf[0] + row;
+    v.dist = (int32_t *)buf[1] + row;
+    v.inbox = (int32_t *)buf[2] + row;
+    v.res = side == 0 ? (int32_t *)buf[3] + row : (int32_t *)buf[4];   // its rD (above) / rU (below)
+    v.cut = (uint8_t *)buf[5] + row;
+    v.ext = (int32_t *)buf[6] + (side == 0 ? g->d.ntx : 0);            // its bottom / top tile row flags
+    v.rq_slot = (int32_t *)buf[7];
+    v.rq_flag = (int32_t *)buf[8];
+    v.rq_ctr = (unsigned *)buf[9];
+    v.rq_cap = nb_rq_cap;
+    v.tile0 = side == 0 ? (nbnty - 1) * g->d.ntx : 0;
+    return v;
+}
+}  // namespace
+
+extern "C" int fm_grid_band_export(fm_grid *g, void *blob) {
+    if (!g || !blob || g->band < 0) { fm_set_error("fm_grid_band_export: set the band up first"); return FM_INVALID_ARG; }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    BandExport x{};
+    x.magic = COLL_MAGIC; x.device = g->device; x.H = g->H; x.W = g->W;
+    x.ntx = g->d.ntx; x.nty = g->d.nty; x.rq_cap = g->rq.cap; x.pid = (int32_t)getpid();
+    for (int k = 0; k < BAND_BUFS; k++) FM_CHECK_CUDA(cudaIpcGetMemHandle(&x.h[k], band_buf(g, k)));
+    memset(blob, 0, FM_BAND_EXPORT_BYTES);
+    memcpy(blob, &x, sizeof(x));
+    return FM_OK;
+}
+
+// Neighbours exported by other processes (one process per GPU): open their buffers.
+// up / dn may be NULL (first / last band); band0 is needed by every band but band 0.
+extern "C" int fm_grid_band_link(fm_grid *g, const void *up_blob, const void *dn_blob, const void *band0_blob) {
+    if (!g || g->band < 0 || (g->d.has_up && !up_blob) || (g->d.has_dn && !dn_blob) || (g->band > 0 && !band0_blob)) {
+        fm_set_error("fm_grid_band_link: missing neighbour export");
+        return FM_INVALID_ARG;
+    }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    const void *blobs[2] = {g->d.has_up ? up_blob : nullptr, g->d.has_dn ? dn_blob : nullptr};
+    for (int side = 0; side < 2; side++) {
+        if (!blobs[side]) continue;
+        BandExport x;
+        memcpy(&x, blobs[side], sizeof(x));
+        if (x.magic != COLL_MAGIC || x.W != g->W || x.ntx != g->d.ntx) {
+            fm_set_error("fm_grid_band_link: neighbour export does not match this band (width %d vs %d)", x.W, g->W);
+            return FM_INVALID_ARG;
+        }
+        for (int k = 0; k < BAND_BUFS; k++) {
+            if (g->ipc_open[side][k]) { cudaIpcCloseMemHandle(g->ipc_open[side][k]); g->ipc_open[side][k] = nullptr; }
+            FM_CHECK_CUDA(cudaIpcOpenMemHandle(&g->ipc_open[side][k], x.h[k], cudaIpcMemLazyEnablePeerAccess));
+        }
+        (side == 0 ? g->d.up : g->d.dn) = make_peer(g, side, x.H, x.nty, x.rq_cap, g->ipc_open[side]);
+        if (g->band == 1 && side == 0) g->gpend = (unsigned *)g->ipc_open[0][9] + 200;
+    }
+    if (g->band > 1) {
+        // band 0 is not a neighbour: map its ring counters for the shared pending count
+        BandExport x;
+        memcpy(&x, band0_blob, sizeof(x));
+        if (x.magic != COLL_MAGIC) { fm_set_error("fm_grid_band_link: bad band-0 export"); return FM_INVALID_ARG; }
+        void *p = nullptr;
+        FM_CHECK_CUDA(cudaIpcOpenMemHandle(&p, x.h[9], cudaIpcMemLazyEnablePeerAccess));
+        if (g->ipc_gpend) cudaIpcCloseMemHandle(g->ipc_gpend);
+        g->gpend = (unsigned *)p + 200;
+        g->ipc_gpend = p;
+    }
+    return FM_OK;
+}
+
+// Neighbours in this process (bands on the same or on peer-accessible devices).
+extern "C" int fm_grid_band_link_local(fm_grid *g, fm_grid *up, fm_grid *dn, fm_grid *band0) {
+    if (!g || g->band < 0 || (g->d.has_up && !up) || (g->d.has_dn && !dn) || !band0 || band0->band != 0) {
+        fm_set_error("fm_grid_band_link_local: missing neighbour band");
+        return FM_INVALID_ARG;
+    }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    fm_grid *nb[2] = {g->d.has_up ? up : nullptr, g->d.has_dn ? dn : nullptr};
+    for (int side = 0; side < 2; side++) {
+        if (!nb[side]) continue;
+        if (nb[side]->W != g->W) { fm_set_error("fm_grid_band_link_local: width mismatch"); return FM_INVALID_ARG; }
+        if (nb[side]->device != g->device) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(nb[side]->device, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else FM_CHECK_CUDA(e);
+        }
+        void *buf[BAND_BUFS];
+        for (int k = 0; k < BAND_BUFS; k++) buf[k] = band_buf(nb[side], k);
+        (side == 0 ? g->d.up : g->d.dn) = make_peer(g, side, nb[side]->H, nb[side]->d.nty, nb[side]->rq.cap, buf);
+    }
+    if (band0->device != g->device) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(band0->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else FM_CHECK_CUDA(e);
+    }
+    g->gpend = band0->rq.ctr + 200;
+    return FM_OK;
+}
+
+namespace {
+int band_gather(fm_grid *g, fm_coll *c, const int64_t *v, int n, int64_t *out) {
+    (void)g;
+    return fm_coll_allgather(c, v, n, out);
+}
+
+// sums of column i over ranks (and the max of column imax, if >= 0)
+void band_sums(const fm_coll *c, const int64_t *all, int n, int64_t *sum, int imax = -1) {
+    for (int i = 0; i < n; i++) sum[i] = 0;
+    for (int r = 0; r < c->nranks; r++)
+        for (int i = 0; i < n; i++)
+            sum[i] = i == imax ? std::max(sum[i], all[r * n + i]) : sum[i] + all[r * n + i];
+}
+
+// the shared pending count of the next band ring launch (band 0 sets it before the
+// barrier that precedes every band's launch)
+int band_arm_ring(fm_grid *g) {
+    ringq_init_kernel<<<std::min((g->rq.cap + 255) / 256, g->sms * 8), 256, 0, g->stream>>>(g->rq, g->ntiles, nullptr, nullptr);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    if (g->band == 0) {
+        g->h_flags[40] = (int32_t)g->total_tiles;
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->gpend, g->h_flags + 40, sizeof(int32_t), cudaMemcpyHostToDevice, g->stream));
+    }
+    return FM_OK;
+}
+
+// global relabel of every band: bit words + seeds, barrier, one ring launch per band
+// ending on the shared pending count, then gap + marking; returns the active pixels of
+// the whole grid
+int band_relabel(fm_grid *g, fm_coll *c, long long *active_total) {
+    cudaEventRecord(g->ev[0], g->stream);
+    FM_TRY(bfs_init(g, false));
+    FM_TRY(band_arm_ring(g));
+    FM_TRY(sync_stream(g));
+    int64_t one = 1, all[COLL_MAX_RANKS * 4];
+    FM_TRY(band_gather(g, c, &one, 1, all));   // every band's distances and queue are seeded
+    cudaEventRecord(g->ev[2], g->stream);
+    ring_kernel<0><<<ring_blocks(g), 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+    FM_CHECK_LAUNCH();
+    cudaEventRecord(g->ev[3], g->stream);
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 8, g->rq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 12, g->rq.ctr + 248, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 4, 0, sizeof(unsigned long long) * 3, g->stream));
+    FM_TRY(tq_reset(g, g->d.pq));
+    g->pq_parity = 0;
+    FM_TRY(bfs_finalize(g));
+    // a new push round: external-push flags and their counters start from zero
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d.ext, 0, sizeof(int32_t) * 2 * (size_t)g->d.ntx, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 24, 0, sizeof(unsigned long long) * 2, g->stream));
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 4, g->acc + 4, sizeof(unsigned long long) * 3,
+                                  cudaMemcpyDeviceToHost, g->stream));
+    cudaEventRecord(g->ev[1], g->stream);
+    FM_TRY(sync_stream(g));
+    g->st.ms_bfs_kern += elapsed_between(g->ev[2], g->ev[3]);
+    g->st.ms_bfs += elapsed(g);
+    g->st.reserved[0] += g->h_flags[8];
+    g->st.launches += 1;
+    g->st.bfs_sweeps += 1;
+    g->st.bfs_launches += 1;
+    g->active = (long long)g->h_acc[4];
+    g->excess_total -= (long long)g->h_acc[5];
+    const int64_t v[4] = {(int64_t)g->h_acc[4], (int64_t)g->h_acc[5], (int64_t)g->h_acc[6], g->h_flags[12]};
+    FM_TRY(band_gather(g, c, v, 4, all));
+    int64_t s[4];
+    band_sums(c, all, 4, s, 2);
+    g->st.bfs_levels = std::max<int64_t>(g->st.bfs_levels, s[2]);
+    if (s[3]) { fm_set_error("row bands: a ring launch waited too long for a neighbour band (not co-resident?)"); return FM_CUDA_ERROR; }
+    *active_total = s[0];
+    return FM_OK;
+}
+
+// One coordinator round of lock-free push launches on every band: batches of pr_batch
+// launches, each preceded by an arm step that queues the tiles neighbours pushed flow
+// into; after each batch the bands agree on {last launch idle, external flags raised
+// vs consumed, relabels}.  The round ends when no band visited a tile in its last
+// launch and every raised flag was consumed (no flow left in flight), on the relabel
+// budget of the whole grid, or on the launch cap (run_round_tiles' triggers).
+int band_push_round(fm_grid *g, fm_coll *c, int32_t cycle_budget) {
+    const int k_default = g->k_local_list > 0 ? g->k_local_list : K_LOCAL_LIST_DEFAULT;
+    const int k_local = std::max(1, std::min(cycle_budget, k_default));
+    const int32_t cap = std::max(1, std::min((cycle_budget + k_local - 1) / k_local,
+                                             g->bfs_interval_env > 0 ? g->bfs_interval_env : MAX_LAUNCHES_DEFAULT));
+    const long long relabel_budget = std::max<long long>(
+        1024, (long long)g->H_total * g->W / (g->relabel_div > 0 ? g->relabel_div : RELABEL_DIV_DEFAULT));
+    const bool pk = g->pk && g->pk_ok && g->op_steps == 1 && !g->op_fused;
+    const int blocks = std::max(1, std::min(g->ntiles, g->sms * (pk ? g->pk_per_sm : g->pl_per_sm) / std::max(1, g->colocated)));
+    cudaEventRecord(g->ev[0], g->stream);
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
+    int32_t done = 0;
+    int64_t all[COLL_MAX_RANKS * 4];
+    while (done < cap) {
+        const int batch = std::min(g->pr_batch, cap - done);
+        FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
+        cudaEventRecord(g->ev[2], g->stream);
+        for (int i = 0; i < batch; i++) {
+            const int p = g->pq_parity;
+            band_arm_kernel<<<1, 256, 0, g->stream>>>(g->d, p);
+            (pk ? pr_list_kernel<true> : pr_list_kernel<false>)<<<blocks, dim3(PT_W, PL_TY), 0, g->stream>>>(
+                g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10, nullptr, 0);
+            g->pq_parity ^= 1;
+        }
+        FM_CHECK_LAUNCH();
+        cudaEventRecord(g->ev[3], g->stream);
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags, g->flags, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, g->stream));
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 10, g->acc + 10, sizeof(unsigned long long) * 2,
+                                      cudaMemcpyDeviceToHost, g->stream));
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 24, g->acc + 24, sizeof(unsigned long long) * 2,
+                                      cudaMemcpyDeviceToHost, g->stream));
+        FM_TRY(sync_stream(g));
+        g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
+        g->st.launches += 2 * batch;
+        g->st.pr_launches += batch;
+        for (int i = 0; i < batch; i++) g->st.pr_tiles += g->h_flags[i];
+        done += batch;
+        const int64_t v[4] = {g->h_flags[batch - 1], (int64_t)g->h_acc[24], (int64_t)g->h_acc[25], (int64_t)g->h_acc[11]};
+        FM_TRY(band_gather(g, c, v, 4, all));
+        int64_t s[4];
+        band_sums(c, all, 4, s);
+        if (s[0] == 0 && s[1] == s[2]) break;      // idle everywhere, no flow in flight
+        if (s[3] >= relabel_budget) break;
+    }
+    integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    cudaEventRecord(g->ev[1], g->stream);
+    FM_TRY(sync_stream(g));
+    g->st.ms_push += elapsed(g);
+    g->st.pr_sweeps += done;
+    g->st.pushes += (int64_t)g->h_acc[10];
+    g->st.relabels += (int64_t)g->h_acc[11];
+    return FM_OK;
+}
+
+int band_cut(fm_grid *g, fm_coll *c) {
+    cudaEventRecord(g->ev[0], g->stream);
+    FM_TRY(cut_init(g));
+    FM_TRY(band_arm_ring(g));
+    FM_TRY(sync_stream(g));
+    int64_t one = 1, all[COLL_MAX_RANKS];
+    FM_TRY(band_gather(g, c, &one, 1, all));   // every band's seeds and queue are in place
+    ring_kernel<1><<<ring_blocks(g), 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    g->st.cut_sweeps++;
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 12, g->rq.ctr + 248, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+    cudaEventRecord(g->ev[1], g->stream);
+    FM_TRY(sync_stream(g));
+    g->st.ms_cut += elapsed(g);
+    const int64_t t = g->h_flags[12];
+    FM_TRY(band_gather(g, c, &t, 1, all));
+    for (int r = 0; r < c->nranks; r++)
+        if (all[r]) { fm_set_error("row bands: the cut ring waited too long for a neighbour band"); return FM_CUDA_ERROR; }
+    return FM_OK;
+}
+}  // namespace
+
+// One band's share of a banded solve (every band of the grid calls it at once, with
+// its own rows; see fm_grid_band_setup / _link).  Inputs may be host or device
+// memory (UVA copies): the six planes of the band's rows, capD of the row above the
+// band and capU of the row below it (W each; NULL for the first / last band).
+// flow_out = the whole grid's flow; cut_out = the band's rows of the minimal cut.
+extern "C" int fm_grid_band_solve(fm_grid *g, fm_coll *c, const int32_t *capR, const int32_t *capL,
+                                  const int32_t *capD, const int32_t *capU, const int32_t *capS,
+                                  const int32_t *capT, const int32_t *capD_above, const int32_t *capU_below,
+                                  int32_t cycle_budget, int32_t flags, int64_t *flow_out, uint8_t *cut_out,
+                                  fm_stats *stats) {
+    if (!g || !c || g->band < 0 || c->nranks != g->nbands || c->rank != g->band || cycle_budget < 1 ||
+        !capR || !capL || !capD || !capU || !capS || !capT || (g->d.has_up && !capD_above) ||
+        (g->d.has_dn && !capU_below)) {
+        fm_set_error("fm_grid_band_solve: invalid argument");
+        return FM_INVALID_ARG;
+    }
+    if ((g->d.has_up && !g->d.up.h) || (g->d.has_dn && !g->d.dn.h) || (g->nbands > 1 && !g->gpend)) {
+        fm_set_error("fm_grid_band_solve: band not linked to its neighbours");
+        return FM_INVALID_ARG;
+    }
+    if (flags & (FM_GRID_CANCEL_VIOLATIONS | FM_GRID_GLOBAL_SWEEP)) {
+        fm_set_error("fm_grid_band_solve: cancel_violations / global sweeps are single-band options");
+        return FM_INVALID_ARG;
+    }
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    set_stream(g, nullptr);
+    if (g->bfs_bits != 2 || g->pr_kernel != 1) { g->bfs_bits = 2; g->pr_kernel = 1; }   // band path = default kernels
+    const size_t HW = (size_t)g->HW, W = (size_t)g->W;
+    if (!g->band_caps) FM_CHECK_CUDA(cudaMalloc((void **)&g->band_caps, sizeof(int32_t) * (6 * HW + 2 * W)));
+    const int32_t *src[6] = {capR, capL, capD, capU, capS, capT};
+    cudaEvent_t t0, t1;
+    FM_CHECK_CUDA(cudaEventCreate(&t0));
+    FM_CHECK_CUDA(cudaEventCreate(&t1));
+    cudaEventRecord(t0, g->stream);
+    for (int k = 0; k < 6; k++)
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->band_caps + k * HW, src[k], sizeof(int32_t) * HW, cudaMemcpyDefault, g->stream));
+    int32_t *above = g->band_caps + 6 * HW, *below = above + W;
+    if (capD_above) FM_CHECK_CUDA(cudaMemcpyAsync(above, capD_above, sizeof(int32_t) * W, cudaMemcpyDefault, g->stream));
+    if (capU_below) FM_CHECK_CUDA(cudaMemcpyAsync(below, capU_below, sizeof(int32_t) * W, cudaMemcpyDefault, g->stream));
+    const int32_t *cp = g->band_caps;
+    g->flags_solve = flags;
+    memset(&g->st, 0, sizeof(g->st));
+    int64_t all[COLL_MAX_RANKS * 4];
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 32, g->stream));
+    FM_CHECK_CUDA(cudaMemsetAsync(g->d.ext, 0, sizeof(int32_t) * 2 * (size_t)g->d.ntx, g->stream));
+    g->rq.pend = g->gpend;
+    grid_init_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(
+        g->d, cp, cp + HW, cp + 2 * HW, cp + 3 * HW, cp + 4 * HW, cp + 5 * HW, above, below,
+        (flags & FM_GRID_NO_PRECANCEL) ? 0 : 1, g->acc);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    if (g->two_hop && !(flags & FM_GRID_NO_PRECANCEL)) {
+        two_hop_kernel<<<dim3((unsigned)((g->W + 255) / 256), (unsigned)std::min(g->H, 65535)), 256, 0, g->stream>>>(g->d);
+        FM_CHECK_LAUNCH();
+        g->st.launches++;
+    }
+    FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc, g->acc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, g->stream));
+    FM_TRY(sync_stream(g));
+    {
+        const int64_t v[3] = {(int64_t)g->h_acc[1], (int64_t)g->h_acc[2], (int64_t)g->h_acc[0]};
+        FM_TRY(band_gather(g, c, v, 3, all));
+        int64_t s[3];
+        band_sums(c, all, 3, s);
+        if (s[0]) { fm_set_error("negative capacity in grid input (%lld entries)", (long long)s[0]); return FM_INVALID_ARG; }
+        if (s[1]) {
+            fm_set_error("grid capacities too large for the int32 device state: %lld pixels where capS plus the "
+                         "capacities into the pixel, or a neighbour pair's two capacities, exceed 2^31-1", (long long)s[1]);
+            return FM_INVALID_ARG;
+        }
+    }
+    g->pk_ok = g->h_acc[3] == 0;
+    g->sum_capS = (long long)g->h_acc[0];
+    g->excess_total = g->sum_capS;
+    long long active = 0;
+    int rc = band_relabel(g, c, &active);
+    while (rc == FM_OK && active > 0) {
+        rc = band_push_round(g, c, cycle_budget);
+        if (rc == FM_OK) rc = band_relabel(g, c, &active);
+        g->st.rounds++;
+    }
+    if (rc == FM_OK && !(flags & FM_GRID_NO_CUT)) {
+        rc = band_cut(g, c);
+        if (rc == FM_OK && cut_out)
+            rc = cudaMemcpyAsync(cut_out, g->d.cut, HW, cudaMemcpyDefault, g->stream) == cudaSuccess ? FM_OK : FM_CUDA_ERROR;
+    }
+    if (rc == FM_OK) {
+        FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 8, 0, sizeof(unsigned long long), g->stream));
+        sum_e_kernel<<<g->grid_blocks, 256, 0, g->stream>>>(g->d, g->acc + 8);
+        FM_CHECK_LAUNCH();
+        g->st.launches++;
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 8, g->acc + 8, sizeof(unsigned long long), cudaMemcpyDeviceToHost, g->stream));
+        cudaEventRecord(t1, g->stream);
+        FM_TRY(sync_stream(g));
+        const int64_t v = g->sum_capS - (long long)g->h_acc[8];
+        FM_TRY(band_gather(g, c, &v, 1, all));
+        int64_t flow = 0;
+        for (int r = 0; r < c->nranks; r++) flow += all[r];
+        if (flow_out) *flow_out = flow;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t0, t1);
+        g->st.ms_total = ms;
+    }
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (stats) *stats = g->st;
+    return rc;
+}
+
+// ---------------------------------------------------------------- in-process group
+struct fm_group {
+    int32_t H = 0, W = 0, nbands = 0;
+    std::vector<int32_t> edges;
+    std::vector<fm_grid *> bands;
+    std::vector<fm_coll *> colls;   // one view per band of one process-local segment
+    CollShm *shm = nullptr;
+};
+
+extern "C" void fm_group_destroy(fm_group *grp) {
+    if (!grp) return;
+    for (auto b : grp->bands) fm_grid_destroy(b);
+    for (auto c : grp->colls) { c->shm = nullptr; delete c; }
+    delete grp->shm;
+    delete grp;
+}
+
+// nbands bands of an H x W grid, band k on devices[k] (bands may share a device:
+// virtual bands, their persistent grids are split between them)
+extern "C" int fm_group_create(int32_t H, int32_t W, int32_t nbands, const int32_t *devices, fm_group **out) {
+    if (!out || !devices || nbands < 1 || nbands > COLL_MAX_RANKS) {
+        fm_set_error("fm_group_create: invalid argument (1 <= nbands <= %d)", COLL_MAX_RANKS);
+        return FM_INVALID_ARG;
+    }
+    fm_group *grp = new fm_group();
+    grp->H = H; grp->W = W; grp->nbands = nbands;
+    grp->edges.resize(nbands + 1);
+    int rc = fm_band_split(H, nbands, grp->edges.data());
+    if (rc != FM_OK) { delete grp; return rc; }
+    grp->shm = new CollShm();
+    grp->shm->arrive.store(0);
+    grp->shm->magic = COLL_MAGIC;
+    grp->shm->nranks = (uint32_t)nbands;
+    for (int k = 0; k < nbands; k++) {
+        int co = 0;
+        for (int j = 0; j < nbands; j++) co += devices[j] == devices[k];
+        fm_grid *b = nullptr;
+        rc = fm_grid_create(grp->edges[k + 1] - grp->edges[k], W, devices[k], &b);
+        if (rc == FM_OK) rc = fm_grid_band_setup(b, k, nbands, H, co);
+        if (rc != FM_OK) { if (b) fm_grid_destroy(b); fm_group_destroy(grp); return rc; }
+        grp->bands.push_back(b);
+        fm_coll *c = new fm_coll();
+        c->shm = grp->shm; c->rank = k; c->nranks = nbands; c->bytes = sizeof(CollShm);
+        grp->colls.push_back(c);
+    }
+    for (int k = 0; k < nbands; k++) {
+        rc = fm_grid_band_link_local(grp->bands[k], k > 0 ? grp->bands[k - 1] : nullptr,
+                                     k + 1 < nbands ? grp->bands[k + 1] : nullptr, grp->bands[0]);
+        if (rc != FM_OK) { fm_group_destroy(grp); return rc; }
+    }
+    *out = grp;
+    return FM_OK;
+}
+
+extern "C" int fm_group_band(fm_group *grp, int32_t k, fm_grid **band, int32_t *row0, int32_t *rows) {
+    if (!grp || k < 0 || k >= grp->nbands) { fm_set_error("fm_group_band: invalid argument"); return FM_INVALID_ARG; }
+    if (band) *band = grp->bands[k];
+    if (row0) *row0 = grp->edges[k];
+    if (rows) *rows = grp->edges[k + 1] - grp->edges[k];
+    return FM_OK;
+}
+
+// Whole-grid planes (host or device memory), one host thread per band.  stats:
+// counters summed over bands, rounds and times of the slowest band.
+extern "C" int fm_group_solve(fm_group *grp, const int32_t *capR, const int32_t *capL, const int32_t *capD,
+                              const int32_t *capU, const int32_t *capS, const int32_t *capT, int32_t cycle_budget,
+                              int32_t flags, int64_t *flow_out, uint8_t *cut_out, fm_stats *stats) {
+    if (!grp || !capR || !capL || !capD || !capU || !capS || !capT || cycle_budget < 1) {
+        fm_set_error("fm_group_solve: invalid argument");
+        return FM_INVALID_ARG;
+    }
+    const int nb = grp->nbands;
+    const size_t W = (size_t)grp->W;
+    std::vector<int> rcs(nb, FM_OK);
+    std::vector<std::string> errs(nb);
+    std::vector<fm_stats> sts(nb);
+    std::vector<int64_t> flows(nb, 0);
+    // a restarted group: the collective segment's call counters start over
+    grp->shm->arrive.store(0);
+    for (auto c : grp->colls) c->calls = 0;
+    auto work = [&](int k) {
+        const size_t o = (size_t)grp->edges[k] * W, o1 = (size_t)grp->edges[k + 1] * W;
+        rcs[k] = fm_grid_band_solve(grp->bands[k], grp->colls[k], capR + o, capL + o, capD + o, capU + o, capS + o,
+                                    capT + o, k > 0 ? capD + o - W : nullptr, k + 1 < nb ? capU + o1 : nullptr,
+                                    cycle_budget, flags, &flows[k], cut_out ? cut_out + o : nullptr, &sts[k]);
+        if (rcs[k] != FM_OK) errs[k] = fm_last_error();
+    };
+    std::vector<std::thread> th;
+    for (int k = 1; k < nb; k++) th.emplace_back(work, k);
+    work(0);
+    for (auto &t : th) t.join();
+    for (int k = 0; k < nb; k++)
+        if (rcs[k] != FM_OK) { fm_set_error("band %d: %s", k, errs[k].c_str()); return rcs[k]; }
+    if (flow_out) *flow_out = flows[0];
+    if (stats) {
+        fm_stats s = sts[0];
+        for (int k = 1; k < nb; k++) {
+            const fm_stats &b = sts[k];
+            s.pushes += b.pushes; s.relabels += b.relabels; s.launches += b.launches;
+            s.pr_sweeps = std::max(s.pr_sweeps, b.pr_sweeps); s.pr_tiles += b.pr_tiles;
+            s.bfs_sweeps = std::max(s.bfs_sweeps, b.bfs_sweeps);
+            s.bfs_levels = std::max(s.bfs_levels, b.bfs_levels);
+            s.pr_launches += b.pr_launches; s.bfs_launches += b.bfs_launches;
+            s.ms_total = std::max(s.ms_total, b.ms_total); s.ms_push = std::max(s.ms_push, b.ms_push);
+            s.ms_bfs = std::max(s.ms_bfs, b.ms_bfs); s.ms_cut = std::max(s.ms_cut, b.ms_cut);
+            s.ms_pr_kern = std::max(s.ms_pr_kern, b.ms_pr_kern); s.ms_bfs_kern = std::max(s.ms_bfs_kern, b.ms_bfs_kern);
+            s.reserved[0] += b.reserved[0];
+        }
+        *stats = s;
+    }
+    return FM_OK;
+}
+
+// per-band counters of the last group solve
+extern "C" int fm_group_band_stats(fm_group *grp, int32_t k, fm_stats *stats) {
+    if (!grp || k < 0 || k >= grp->nbands || !stats) { fm_set_error("fm_group_band_stats: invalid argument"); return FM_INVALID_ARG; }
+    *stats = grp->bands[k]->st;
     return FM_OK;
 }

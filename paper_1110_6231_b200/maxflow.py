@@ -222,7 +222,7 @@ def _observe(net: GridNetwork, solver: GridSolver, observer, cycle_budget, worke
 
 def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DEFAULT_CYCLE_BUDGET,
                  observer=None, *, device: int | None = None, bfs_interval: int = DEFAULT_BFS_INTERVAL,
-                 cancel_violations: bool = False, want_cut: bool = True) -> SolveReport:
+                 cancel_violations: bool = False, want_cut: bool = True, devices=None) -> SolveReport:
     """Coordinated lock-free push-relabel rounds until all live excess is at t
     (maxflow_par.py:157-238), on the GPU.
 
@@ -230,6 +230,9 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
     thread owns each pixel).  cycle_budget = max lock-free sweeps per round.
     observer(net, hybrid, scanned) is called at every coordinator point with
     reference-shaped state (slow: state is copied to the host; tests only).
+    devices: shard a grid in row bands -- an int N (N bands over the
+    visible GPUs, round-robin) or a list of device ids, one band each (a device may
+    repeat: virtual bands).  Same flow and minimal cut as the single-GPU solve.
     """
     if net.source is None or net.sink is None:
         raise ValueError("network has no source/sink")
@@ -237,6 +240,11 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
         raise ValueError(f"worker_count must be at least 1, got {worker_count}")
     if cycle_budget < 1:
         raise ValueError(f"cycle_budget must be at least 1, got {cycle_budget}")
+    if devices is not None:
+        devs = _band_devices(devices)
+        if len(devs) > 1:
+            return _banded_solve(net, devs, cycle_budget, observer, cancel_violations, want_cut)
+        device = devs[0] if device is None else device
     if not isinstance(net, GridNetwork):
         if observer is not None:
             raise NotImplementedError("observer hooks are supported on GridNetwork solves")
@@ -282,6 +290,43 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
     return SolveReport(objective=int(flow), pushes=int(stats.get("pushes", 0)),
                        relabels=int(stats.get("relabels", 0)), rounds=int(stats.get("rounds", 0)),
                        elapsed=elapsed, cut=cut, stats=stats)
+
+
+_groups = _lib.SolverCache(per_device=1)
+
+
+def _band_devices(devices) -> list[int]:
+    if isinstance(devices, (int, np.integer)):
+        n = int(devices)
+        if n < 1:
+            raise ValueError(f"devices must be at least 1, got {n}")
+        ndev = max(1, _lib.device_count())
+        return [k % ndev for k in range(n)]
+    devs = [int(d) for d in devices]
+    if not devs:
+        raise ValueError("devices must name at least one device")
+    return devs
+
+
+def _banded_solve(net, devs, cycle_budget, observer, cancel_violations, want_cut) -> SolveReport:
+    """hybrid_solve over row bands (one per entry of devs), paper_1110_6231_b200.bands."""
+    from .bands import BandGroup
+
+    if not isinstance(net, GridNetwork):
+        raise ValueError("devices > 1 shards grid networks in row bands; this network is not a GridNetwork")
+    if observer is not None:
+        raise NotImplementedError("observer hooks run on single-device solves (devices=None)")
+    if cancel_violations:
+        raise ValueError("cancel_violations is a single-device option")
+    started = time.perf_counter()
+    caps = _device_planes(net.caps) if net.on_device else net.host_caps()
+    key = (net.H, net.W, tuple(devs))
+    with _groups.use(key, -1, lambda: BandGroup(net.H, net.W, len(devs), devs)) as grp:
+        flow, cut, stats = grp.solve(caps, cycle_budget, want_cut=want_cut)
+    stats["devices"] = list(devs)
+    return SolveReport(objective=int(flow), pushes=int(stats.get("pushes", 0)),
+                       relabels=int(stats.get("relabels", 0)), rounds=int(stats.get("rounds", 0)),
+                       elapsed=time.perf_counter() - started, cut=cut, stats=stats)
 
 
 def csr_arrays(net: FlowNetwork):

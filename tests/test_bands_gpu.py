@@ -1,7 +1,11 @@
-"""Row-band sharding (multi-GPU grid path) exercised as virtual bands on one GPU:
-flow and minimal cut must be bit-identical to the single-band solve and the oracle."""
+"""Row-band sharding (multi-GPU grid path) on the one test GPU: virtual bands (several
+bands on one device, one host thread each, neighbours reached through device memory)
+and two processes sharing the GPU through CUDA IPC (the one-process-per-GPU path).
+Flow and minimal cut must be bit-identical to the single-band solve and the oracle."""
 
 from __future__ import annotations
+
+import hashlib
 
 import numpy as np
 import pytest
@@ -15,7 +19,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("H,W,nb,kind", [(64, 48, 2, "G"), (100, 70, 3, "G"), (256, 256, 4, "G"),
-                                         (96, 64, 3, "S"), (512, 512, 8, "G"), (40, 33, 2, "G")])
+                                         (96, 64, 3, "S"), (512, 512, 8, "G"), (40, 33, 2, "G"),
+                                         (64, 1, 2, "G"), (97, 5, 3, "G")])
 def test_virtual_bands_match_oracle(H, W, nb, kind):
     caps = G.grid_random(H, W, H + W) if kind == "G" else G.grid_segmentation(H, W, 7)
     want = oracle.grid_maxflow(*caps, solver="seq")
@@ -28,59 +33,51 @@ def test_virtual_bands_match_oracle(H, W, nb, kind):
 def test_virtual_bands_match_single_band_at_1024():
     caps = G.grid_random(1024, 1024, 11)
     rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
-    for nb in (2, 4):
+    for nb in (2, 4, 7):
         flow, cut, _ = B.solve_virtual_bands(caps, nb)
         assert flow == rep.objective
         assert (cut == rep.cut).all()
 
 
-def _dist_band_worker(rank, world, port, H, W, seed, q):
-    import os
-
-    import torch
-    import torch.distributed as dist
-
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
-    caps = G.grid_random(H, W, seed)
-    spans = B.band_rows(H, world)
-    r0, r1 = spans[rank]
-    gt, gb = rank > 0, rank + 1 < world
-    flow, band, st = B.solve_distributed(B.band_caps(caps, r0, r1, gt, gb), gt, gb, H * W, rank, world, 0)
-    cut = band.cut_host()[(1 if gt else 0):(1 if gt else 0) + (r1 - r0)]
-    q.put((rank, flow, r0, r1, cut))
-    band.close()
-    dist.destroy_process_group()
-
-
-def test_multiprocess_bands_gloo_on_one_gpu():
-    """The one-process-per-GPU coordinator (DistTransport) with 2 ranks sharing the
-    single test GPU; gloo stages the boundary rows through host memory."""
-    import multiprocessing as mp
-    import socket
-
-    H, W, seed = 200, 96, 5
-    caps = G.grid_random(H, W, seed)
+def test_hybrid_solve_devices_keyword():
+    caps = G.grid_random(300, 200, 4)
     want = oracle.grid_maxflow(*caps, solver="seq")
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    ps = [ctx.Process(target=_dist_band_worker, args=(r, 2, port, H, W, seed, q)) for r in range(2)]
-    for p in ps:
-        p.start()
-    got = [q.get(timeout=300) for _ in range(2)]
-    for p in ps:
-        p.join(timeout=60)
-    cut = np.zeros((H, W), bool)
-    for rank, flow, r0, r1, c in got:
-        assert flow == want["value"]
-        cut[r0:r1] = c.astype(bool)
-    assert (cut == want["cut"]).all()
+    net = fmb.build_grid_network(*caps)
+    for devs in (2, [0, 0, 0], 1):
+        rep = fmb.hybrid_solve(net, devices=devs)
+        assert rep.objective == want["value"] and (rep.cut == want["cut"]).all(), devs
+    with pytest.raises(NotImplementedError):
+        fmb.hybrid_solve(net, devices=2, observer=lambda *a: None)
+    with pytest.raises(ValueError):
+        fmb.hybrid_solve(net, devices=2, cancel_violations=True)
+    with pytest.raises(ValueError):
+        fmb.hybrid_solve(net, devices=0)
+
+
+def test_bands_device_planes_and_repeat_solves():
+    import torch
+
+    caps = G.grid_random(256, 320, 9)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    dcaps = [torch.from_numpy(c).cuda() for c in caps]
+    grp = B.BandGroup(256, 320, 3, [0, 0, 0])
+    try:
+        for _ in range(5):   # the group (and its collective segment) is reused
+            flow, cut, st = grp.solve(dcaps)
+            assert flow == want["value"] and (cut == want["cut"]).all()
+        cut_d = torch.empty((256, 320), dtype=torch.uint8, device="cuda")
+        flow, _, _ = grp.solve(dcaps, cut_out=cut_d)
+        assert flow == want["value"] and (cut_d.cpu().numpy().astype(bool) == want["cut"]).all()
+        assert len({grp.band_stats(k)["rounds"] for k in range(3)}) == 1   # bands agree on every round
+    finally:
+        grp.close()
+
+
+def test_bands_reject_bad_input_consistently():
+    caps = [c.copy() for c in G.grid_random(128, 64, 2)]
+    caps[4][100, 3] = -1      # in the last band only: every band must fail, none may hang
+    with pytest.raises(ValueError, match="negative"):
+        B.solve_virtual_bands(caps, 3)
 
 
 @pytest.mark.parametrize("nb", [3, 8])
@@ -89,25 +86,6 @@ def test_bands_segmentation_and_many_bands(nb):
     want = oracle.grid_maxflow(*caps, solver="seq")
     flow, cut, _ = B.solve_virtual_bands(caps, nb)
     assert flow == want["value"] and (cut == want["cut"]).all()
-
-
-def test_bands_blocked_generator_rows():
-    # the multi-GPU bench builds each band from its own rows of the blocked generator
-    H, W = 600, 200
-    full = G.grid_random_blocked(H, W, 3)
-    want = oracle.grid_maxflow(*full, solver="seq")
-    spans = B.band_rows(H, 3)
-    bands = []
-    for k, (r0, r1) in enumerate(spans):
-        gt, gb = k > 0, k + 1 < len(spans)
-        rows = G.grid_random_rows(H, W, 3, r0 - gt, r1 + gb)
-        bc = B.band_caps_from_rows(rows, gt, gb)
-        assert all(np.array_equal(a, b) for a, b in zip(bc, B.band_caps(full, r0, r1, gt, gb)))
-        bands.append(B.Band(bc, gt, gb, H * W + 2))
-    co = B.BandedSolve(B.LocalTransport(bands), total_pixels=H * W)
-    assert co.run() == want["value"]
-    for b in bands:
-        b.close()
 
 
 def _stress_band_case(seed, k):
@@ -130,10 +108,9 @@ def _stress_band_case(seed, k):
 
 
 @pytest.mark.parametrize("k", [132, 149])
-def test_regression_band_cut_ghost_residuals(k):
-    """scripts/stress_bands.py seed 5: the cut came out short of the minimal one next to
-    band borders (flow correct) because the ghost rows' residuals toward the band were
-    those exported before the last push exchange folded its flow in."""
+def test_regression_band_cut_cases(k):
+    """scripts/stress_bands.py seed 5 cases that once gave a cut short of the minimal one
+    next to band borders (round-1 ghost-row exchange)."""
     caps, nb = _stress_band_case(5, k)
     want = oracle.grid_maxflow(*caps, solver="seq")
     flow, cut, _ = B.solve_virtual_bands(caps, nb)
@@ -146,3 +123,81 @@ def test_random_band_cases(seed):
     want = oracle.grid_maxflow(*caps, solver="seq")
     flow, cut, _ = B.solve_virtual_bands(caps, nb)
     assert flow == want["value"] and (cut == want["cut"]).all()
+
+
+def _cut_sha(cut) -> str:
+    return hashlib.sha256(np.packbits(np.asarray(cut, dtype=bool)).tobytes()).hexdigest()[:16]
+
+
+def test_config3_8192_banded_matches_single_gpu():
+    """BASELINE config 3 (generator G 8192^2, seed 8192): 2 and 4 bands on the one GPU
+    give the certified single-GPU flow and the identical minimal cut."""
+    import torch
+
+    caps = G.grid_random(8192, 8192, 8192)
+    dcaps = [torch.from_numpy(c).cuda() for c in caps]
+    del caps
+    solver = fmb.GridSolver(8192, 8192)
+    cut1 = torch.empty((8192, 8192), dtype=torch.uint8, device="cuda")
+    flow1, _ = solver.solve_device(dcaps, cut_out=cut1)
+    solver.close()
+    assert flow1 == 3318000345
+    for nb in (2, 4):
+        grp = B.BandGroup(8192, 8192, nb, [0] * nb)
+        cutb = torch.empty((8192, 8192), dtype=torch.uint8, device="cuda")
+        flow, _, _ = grp.solve(dcaps, cut_out=cutb)
+        grp.close()
+        assert flow == flow1, nb
+        assert torch.equal(cutb, cut1), nb
+
+
+def _dist_band_worker(rank, world, port, H, W, seed, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    caps = G.grid_random(H, W, seed)
+    band = B.DistBand(H, W, rank, world, 0, colocated=world)
+    rows, above, below = B.band_planes(caps, band.r0, band.r1)
+    outs = []
+    for _ in range(2):
+        flow, cut, st = band.solve(rows, above, below)
+        outs.append((flow, cut.copy()))
+    q.put((rank, band.r0, band.r1, outs))
+    band.close()
+    dist.destroy_process_group()
+
+
+def test_multiprocess_bands_ipc_on_one_gpu():
+    """The one-process-per-GPU path (DistBand): 2 ranks share the test GPU, reach each
+    other's band through CUDA IPC mappings and agree through the shared segment."""
+    import multiprocessing as mp
+    import socket
+
+    H, W, seed = 200, 96, 5
+    caps = G.grid_random(H, W, seed)
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_dist_band_worker, args=(r, 2, port, H, W, seed, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    for p in ps:
+        p.join(timeout=60)
+    for rep in range(2):
+        cut = np.zeros((H, W), bool)
+        for rank, r0, r1, outs in got:
+            flow, c = outs[rep]
+            assert flow == want["value"]
+            cut[r0:r1] = c.astype(bool)
+        assert (cut == want["cut"]).all()
