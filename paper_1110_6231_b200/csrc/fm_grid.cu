@@ -627,6 +627,9 @@ struct PlTile {
 // per listed pixel per pass) with every shared-memory read issued up front and the
 // two pushes' atomics in flight together: the pass is a latency chain, so fewer
 // dependent round trips is what makes it faster.  Same results as pl_item.
+// No grid-bound tests: the residual toward a neighbour outside the grid (or band, with
+// no neighbour band) is 0 from grid_init and only ever grows by flow that neighbour
+// sent, so a positive residual implies the neighbour exists.
 __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li, int *recv,
                                        unsigned &pushes, unsigned &relabels) {
     constexpr int HS = PL_HS;
@@ -636,7 +639,6 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
     const int V = g.V;
     const int lr = li >> 5, lc = li & 31;
     const int hi = (lr + 1) * HS + lc + PL_HC;
-    const int r = T.r0 + lr, c = T.c0 + lc;
     const uint8_t f = T.f[li];
     const int32_t e = ve[li], hp = vh[hi], rt = vt[li];
     const int32_t rr = *(volatile int32_t *)&T.r[0][li];
@@ -654,10 +656,10 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
     }
     int32_t best_h = INT32_MAX, best_r = 0;
     int dir = -1;
-    if (rr > 0 && c + 1 < g.W && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
-    if (rl > 0 && c > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
-    if (rd > 0 && r + 1 < g.hlim && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
-    if (ru > 0 && r > g.rmin && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
+    if (rr > 0 && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
+    if (rl > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
+    if (rd > 0 && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
+    if (ru > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
     if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
     if (dir < 0) return false;                             // nothing residual: rescanned on next load
     if (hp <= best_h) {                                    // relabel (owner-only); the push waits
@@ -699,7 +701,6 @@ __device__ __forceinline__ bool pk_op1(const GridDev &g, const PlTile &T, int li
     const int V = g.V;
     const int lr = li >> 5, lc = li & 31;
     const int hi = (lr + 1) * HS + lc + PL_HC;
-    const int r = T.r0 + lr, c = T.c0 + lc;
     const uint8_t f = T.f[li];
     const int32_t e = ve[li], hp = vh[hi], rt = vt[li];
     const unsigned long long w64 = *(volatile unsigned long long *)&T.r2[li];
@@ -717,10 +718,10 @@ __device__ __forceinline__ bool pk_op1(const GridDev &g, const PlTile &T, int li
     const int32_t rd = (int32_t)(w.y & 0xffff), ru = (int32_t)(w.y >> 16);
     int32_t best_h = INT32_MAX, best_r = 0;
     int dir = -1;
-    if (rr > 0 && c + 1 < g.W && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
-    if (rl > 0 && c > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
-    if (rd > 0 && r + 1 < g.hlim && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
-    if (ru > 0 && r > g.rmin && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
+    if (rr > 0 && hR < best_h) { best_h = hR; best_r = rr; dir = 0; }
+    if (rl > 0 && hL < best_h) { best_h = hL; best_r = rl; dir = 1; }
+    if (rd > 0 && hD < best_h) { best_h = hD; best_r = rd; dir = 2; }
+    if (ru > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
     if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
     if (dir < 0) return false;
     if (hp <= best_h) {
@@ -976,19 +977,21 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
     const bool simple = steps == 1 && !fused;
     int it = 0;
     bool solo = false;
+    // list counters rotate through S.cnt[0..2] (current / next / cleared for the pass
+    // after) and the two lists swap: no per-pass modulo arithmetic
+    int cc = 0, cn = 1, cz = 2;
+    uint16_t *lin = S.list[0], *lout = S.list[1];
+    const int solo_max = g.solo_max;
+    const int wbase = tid & ~31;
     for (; it < k_local; it++) {
         __syncthreads();
-        const int n = S.cnt[it % 3];
-        if (n == 0) break;
-        if (n <= g.solo_max) { solo = true; break; }
+        const int n = S.cnt[cc];
+        if (n <= solo_max) { solo = n > 0; break; }
         C.passes++;
         C.items += n;
-        int *cnt_next = &S.cnt[(it + 1) % 3];
-        if (tid == 0) S.cnt[(it + 2) % 3] = 0;
-        const uint16_t *lin = S.list[it & 1];
-        uint16_t *lout = S.list[(it + 1) & 1];
-        for (int base = 0; base < n; base += PL_NT) {
-            if (base + (tid & ~31) >= n) break;        // warp-uniform
+        int *cnt_next = &S.cnt[cn];
+        if (tid == 0) S.cnt[cz] = 0;
+        for (int base = 0; base + wbase < n; base += PL_NT) {   // warp-uniform bound
             const int i = base + tid;
             int recv = -1;
             const int li = i < n ? lin[i] : 0;
@@ -998,6 +1001,8 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
                                          : pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels));
             pl_append2_warp(keep, li, recv >= 0, recv, cnt_next, lout);
         }
+        const int t = cc; cc = cn; cn = cz; cz = t;
+        uint16_t *tl = lin; lin = lout; lout = tl;
     }
     // sparse passes: warp 0 alone, warp-synchronous
 #ifdef FM_PL_TIMING
@@ -1008,14 +1013,12 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
     if (solo && tid < 32 && simple) {
         // one warp is the only reader and writer of the lists now: the next list's
         // length is the warp's own running count (no shared counter round trip)
-        int n = S.cnt[it % 3];
+        int n = S.cnt[cc];
         const unsigned lt = (1u << tid) - 1;
         const int it_end = g.k_solo > 0 ? min(k_local, it + g.k_solo) : k_local;
         for (; it < it_end && n > 0; it++) {
             C.passes++;
             C.items += n;
-            const uint16_t *lin = S.list[it & 1];
-            uint16_t *lout = S.list[(it + 1) & 1];
             int nn = 0;
             for (int base = 0; base < n; base += 32) {
                 const int i = base + tid;
@@ -1031,18 +1034,17 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
             }
             __syncwarp();
             n = nn;
+            uint16_t *tl = lin; lin = lout; lout = tl;
         }
     } else if (!PK && solo && tid < 32) {
         for (; it < k_local; it++) {
             __syncwarp();
-            const int n = S.cnt[it % 3];
+            const int n = S.cnt[cc];
             if (n == 0) break;
             C.passes++;
             C.items += n;
-            int *cnt_next = &S.cnt[(it + 1) % 3];
-            if (tid == 0) S.cnt[(it + 2) % 3] = 0;
-            const uint16_t *lin = S.list[it & 1];
-            uint16_t *lout = S.list[(it + 1) & 1];
+            int *cnt_next = &S.cnt[cn];
+            if (tid == 0) S.cnt[cz] = 0;
             __syncwarp();
             for (int base = 0; base < n; base += 32) {
                 const int i = base + tid;
@@ -1054,6 +1056,8 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
                                             : pl_item(g, T, li, steps, fused, cnt_next, lout, &recv, C.pushes, C.relabels));
                 pl_append2_warp(keep, li, recv >= 0, recv, cnt_next, lout);
             }
+            const int t = cc; cc = cn; cn = cz; cz = t;
+            uint16_t *tl = lin; lin = lout; lout = tl;
         }
     }
 #ifdef FM_PL_TIMING
@@ -2982,6 +2986,9 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
                                       cudaMemcpyDeviceToHost, g->stream));
         FM_TRY(sync_stream(g));
         g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
+        if (g->trace >= 3)
+            fprintf(stderr, "[fm_grid]   batch: %.3f ms, tiles per launch %d %d %d %d\n", elapsed_between(g->ev[2], g->ev[3]),
+                    g->h_flags[0], batch > 1 ? g->h_flags[1] : -1, batch > 2 ? g->h_flags[2] : -1, batch > 3 ? g->h_flags[3] : -1);
         int idle_at = -1;
         for (int i = 0; i < batch; i++) {
             if (!g->h_flags[i]) { idle_at = i; break; }
