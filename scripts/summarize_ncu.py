@@ -13,9 +13,18 @@ import sys
 
 
 
+TEMPLATE_NAMES = {"ring_kernel<0>": "ring_kernel<bfs>", "ring_kernel<1>": "ring_kernel<cut>",
+                  "pr_list_kernel<1>": "pr_list_kernel<packed>", "pr_list_kernel<true>": "pr_list_kernel<packed>",
+                  "pr_list_kernel<0>": "pr_list_kernel<int32>", "pr_list_kernel<false>": "pr_list_kernel<int32>"}
+
+
 def kname(raw):
-    """Kernel name without namespace, return type, template arguments or parameters."""
-    n = raw.replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+    """Kernel name without namespace, return type or parameters; the instances of the
+    ring and push kernels keep a tag (ring_kernel<bfs> / <cut>, pr_list_kernel<packed>)."""
+    n = raw.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("(bool)", "")
+    for k, v in TEMPLATE_NAMES.items():
+        if k in n:
+            return v
     n = n.split("(")[0]
     n = re.sub(r"<[^<>]*>", "", n)
     return n.replace("void ", "").strip()
@@ -53,7 +62,9 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
-        "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio"]
+        "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__thread_inst_executed_per_inst_executed.ratio",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum"]
 
 
 def full(path):
@@ -89,13 +100,32 @@ def traffic(path):
         names[r[ii]] = kname(r[ki])
         per[r[ii]][r[mi]] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    extra = collections.defaultdict(dict)
     for lid, m in per.items():
         a = agg[names[lid]]
         a[0] += 1
         a[1] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
         a[2] += m.get("gpu__time_duration.sum", 0.0)
-    out = {k: {"launches": v[0], "dram_bytes_per_launch": v[1] / v[0], "duration_us_per_launch": v[2] / v[0],
-               "source": path} for k, v in agg.items()}
+        for key in ("l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum",
+                    "l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum",
+                    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum"):
+            ex = extra[names[lid]]
+            ex[key] = ex.get(key, 0.0) + m.get(key, 0.0)
+    out = {}
+    for k, v in agg.items():
+        d = {"launches": v[0], "dram_bytes_per_launch": v[1] / v[0], "duration_us_per_launch": v[2] / v[0],
+             "source": path}
+        ex = extra[k]
+        if ex:
+            sec = v[2] * 1e-6
+            d["global_atom_per_launch"] = ex.get("l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum", 0.0) / v[0]
+            d["global_red_per_launch"] = ex.get("l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum", 0.0) / v[0]
+            d["shared_atom_wavefronts_per_launch"] = ex.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", 0.0) / v[0]
+            if sec > 0:
+                d["global_atom_red_per_s"] = (ex.get("l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum", 0.0) +
+                                              ex.get("l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum", 0.0)) / sec
+                d["shared_atom_wavefronts_per_s"] = ex.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", 0.0) / sec
+        out[k] = d
     print(json.dumps(out, indent=1))
 
 

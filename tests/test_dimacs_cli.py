@@ -236,8 +236,17 @@ def test_cli_grid_file_matches_oracle(tmp_path, capsys):
     assert rec["objective"] == want["value"] and rec["grid"] == [40, 56]
     cut = np.loadtxt(cut_path, dtype=np.uint8).astype(bool)
     assert (cut == want["cut"].reshape(-1)).all()
+    # GPU metrics in the record
+    assert rec["launches"] > 0 and rec["device_ms"] > 0 and rec["medges_per_s"] > 0
+    assert rec["bfs_levels"] >= 1 and rec["hbm_gbs_achieved"] > 0
     code, out, err = _run(capsys, "verify", "--input", str(path))
     assert code == 0, err
+    # --gpus 2: the same grid in two row bands (virtual bands on the one test GPU)
+    code, out, err = _run(capsys, "maxflow", "--input", str(path), "--gpus", "2", "--cut-output", str(cut_path))
+    assert code == 0, err
+    rec = json.loads(out)
+    assert rec["objective"] == want["value"] and rec["gpus"] == 2
+    assert (np.loadtxt(cut_path, dtype=np.uint8).astype(bool) == want["cut"].reshape(-1)).all()
 
 
 @pytest.mark.gpu
