@@ -381,6 +381,9 @@ def main():
     ap.add_argument("--cpu-assign-4096", action="store_true", help="also time the n=4096 assignment CPU port (~1 min)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-big", action="store_true", help="skip the 8192^2 single-GPU solve")
+    ap.add_argument("--no-virtual-bands", action="store_true",
+                    help="skip the 2-band solve on one GPU (its bands' ring launches must run concurrently, "
+                         "which a kernel-serialising profiler prevents)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: run the banded path with several ranks sharing fewer GPUs")
     args = ap.parse_args()
@@ -506,6 +509,7 @@ def main():
         # one host thread per band) -- identical flow and cut
         from paper_1110_6231_b200 import bands as Bd
 
+    if big is not None and not args.no_virtual_bands:
         grp = Bd.BandGroup(B8, B8, 2, [local, local])
         grp.solve(cb, cut_out=cut3)
         tms = []
@@ -519,6 +523,7 @@ def main():
                                     "solve_ms_wall": round(statistics.mean(tms), 3),
                                     "device_ms_max_band": round(stb["ms_total"], 3), "rounds": stb["rounds"]}
         assert fb == f3 and big["two_virtual_bands"]["cut_sha16"] == big["cut_sha16"]
+    if big is not None:
         del cb, cut3
 
     # assignment n = 4096 (single GPU; replicas only)
