@@ -1540,14 +1540,32 @@ struct RingQ {
                             // one counter shared by every band's ring (on band 0's device)
     int32_t cap;
     int32_t rerun;          // a tile found stale again while in flight: 1 rerun at once, 0 requeue
-    int32_t *vis;           // per tile: visits in this launch (incremental re-visits, BFS ring)
     int32_t incr;           // 1: a re-visit only propagates halo improvements (option BFS_INCR)
     int32_t ns0, ns1;       // idle-poll backoff (ns)
     int32_t sys;            // row bands: fences at system scope (peer GPUs read / count what we publish)
 };
 
-__device__ __forceinline__ void fence_q(const RingQ &q) {
-    if (q.sys) __threadfence_system(); else __threadfence();
+// Release / acquire accesses for the ring protocol (PTX memory model): a release store /
+// CAS publishes the warp's earlier stores (ordered before it by __syncwarp), an acquire
+// load / CAS makes the publisher's stores visible to the loads after it.  Cheaper than
+// the sequentially consistent fence of __threadfence (MEMBAR.SC + L1 invalidate): a
+// release is MEMBAR.ALL + the access, an acquire the access + L1 invalidate.  sys:
+// system scope (row bands: the other side is a peer GPU).
+__device__ __forceinline__ int ld_acquire(const int32_t *p, bool sys) {
+    int v;
+    if (sys) asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int32_t *p, int v, bool sys) {
+    if (sys) asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    else asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int cas_acq_rel(int32_t *p, int cmp, int val, bool sys) {
+    int old;
+    if (sys) asm volatile("atom.acq_rel.sys.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(val) : "memory");
+    else asm volatile("atom.acq_rel.gpu.global.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "l"(p), "r"(cmp), "r"(val) : "memory");
+    return old;
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -1559,8 +1577,10 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // initial content: tiles list0[0..*count0) (count0 != nullptr) or every tile
 __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, const int32_t *count0) {
     const int n0 = count0 ? __ldcg(count0) : ntiles;
+    // flag words: bits 0-1 state (0 idle, 1 queued, 2 in flight, 3 stale in flight), bit 2
+    // "visited in this launch" (incremental re-visits).  Every tile queued: every flag is
+    // written here; a listed start has had its flags zeroed by the host first.
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < q.cap; i += gridDim.x * blockDim.x) {
-        if (q.vis && i < ntiles) q.vis[i] = 0;
         if (i < n0) {
             const int t = count0 ? list0[i] : i;
             q.slot[i] = t;
@@ -1574,37 +1594,17 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
         q.ctr[128] = 0; q.ctr[160] = 0; q.ctr[161] = 0; q.ctr[192] = 0; q.ctr[224] = n0;
         q.ctr[240] = q.ctr[241] = q.ctr[244] = q.ctr[245] = q.ctr[246] = q.ctr[247] = 0;
         q.ctr[248] = 0;
+        for (int i = 208; i < 218; i++) q.ctr[i] = 0;
     }
 }
 
 // Tile states: 0 idle, 1 queued, 2 in flight, 3 in flight + stale again.  A tile is
 // never processed by two warps at once (so a visit owns its pixels' distances); a
-// push that finds it in flight marks it 3 and the owner runs it again.  The queue
-// may be a neighbour band's (peer memory): its slot / flag / tail words, our pending.
-__device__ __forceinline__ void ringq_push_to(int32_t *slot, int32_t *flag, unsigned *tail, int cap,
-                                              unsigned *pend, bool sys, int t) {
-    for (;;) {
-        const int o = atomicCAS(flag + t, 0, 1);
-        if (o == 0) {
-            atomicAdd(pend, 1u);
-            const unsigned s = atomicAdd(tail, 1u);
-            // the values that made t stale (and the pending increment) are visible
-            // before t is
-            if (sys) __threadfence_system(); else __threadfence();
-            *(volatile int32_t *)(slot + (s % (unsigned)cap)) = t;
-            return;
-        }
-        if (o != 2 || atomicCAS(flag + t, 2, 3) == 2) return;   // queued / already marked
-    }
-}
-
-__device__ __forceinline__ void ringq_push(const RingQ &q, int t) {
-    ringq_push_to(q.slot, q.flag, q.ctr + 32, q.cap, q.pend, q.sys, t);
-}
-
-__device__ __forceinline__ void ringq_push_peer(const RingQ &q, const PeerView &pv, int t) {
-    ringq_push_to(pv.rq_slot, pv.rq_flag, pv.rq_ctr + 32, pv.rq_cap, q.pend, true, t);
-}
+// visit that finds a neighbour in flight marks it 3 and the owner runs it again.  A
+// claimed neighbour may live in a neighbour band's ring (peer memory): its slot / flag /
+// tail words, our shared pending count.  (Claiming, counting and publishing happen at
+// the end of a visit in ring_kernel: one pending update and one slot reservation per
+// visit, since those counters are the hottest words of the launch.)
 
 // Halo row above / below a tile (lane = column): the neighbour tile's border row, or
 // in row-band mode the neighbour band's boundary row through peer memory.
@@ -1635,11 +1635,18 @@ struct RingChange { int b0, b1, b2, b3, any; };
 
 // One BFS visit (warp per tile), K2: level-synchronous bit-parallel BFS of the tile
 // from its sink arcs and halo distances (from scratch), or an incremental re-visit.
-__device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q, int tile, int32_t *sd, int lane
 #ifdef FM_BFS_TIMING
-                                                , int &lv
+struct BfsTm { long long ld = 0, lvl = 0, wb = 0, wait = 0, push = 0; };
+#endif
+__device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q, int tile, bool visited, int32_t *sd,
+                                                int lane
+#ifdef FM_BFS_TIMING
+                                                , int &lv, BfsTm &tm
 #endif
                                                 ) {
+#ifdef FM_BFS_TIMING
+    long long tA = clock64();
+#endif
     const int INF = g.INF;
     const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
     const int r0 = tyi * PT_H, c0 = txi * PT_W;
@@ -1660,7 +1667,10 @@ __device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q
     const int ol = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0) : INF;                  // own left column
     const int orr = rl < g.H ? ld_cg(g.dist + (int64_t)rl * g.W + c0 + last_c) : INF;        // own right column
     uint32_t seen = 0;
-    const bool incr = q.incr && __ldcg(q.vis + tile) > 0;
+    const bool incr = q.incr && visited;
+#ifdef FM_BFS_TIMING
+    long long tB = 0;
+#endif
     if (incr) {
         // Re-visit: the previous visit left a fixpoint for the halos it saw, and halos
         // only fall, so only pixels that a now-shorter halo path improves change.  Load
@@ -1669,6 +1679,9 @@ __device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q
         for (int i = 0; i < PT_H; i++)
             sd[i * (PT_W + 1) + lane] = (r0 + i < g.H && cl < g.W) ? ld_cg(g.dist + (int64_t)(r0 + i) * g.W + cl) : INF;
         __syncwarp();
+#ifdef FM_BFS_TIMING
+        tB = clock64();
+#endif
         const uint32_t mU0 = __shfl_sync(0xffffffffu, mU, 0), mD31 = __shfl_sync(0xffffffffu, mD, PT_H - 1);
         // smallest halo value >= lo whose path improves a border pixel (INF: none)
         const auto next_seed = [&](int lo) -> int {
@@ -1711,6 +1724,9 @@ __device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q
         __syncwarp();
     } else {
         // level-synchronous BFS; sd[row][col] = level at which the pixel was reached
+#ifdef FM_BFS_TIMING
+        tB = clock64();
+#endif
         uint32_t F = mT;
         seen = mT;
         for (uint32_t x = mT; x; x &= x - 1) sd[lane * (PT_W + 1) + __ffs(x) - 1] = 1;
@@ -1753,6 +1769,9 @@ __device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q
         __syncwarp();
     }
     // write back every reached pixel (lane = column); borders compared with the old values
+#ifdef FM_BFS_TIMING
+    const long long tC = clock64();
+#endif
     const uint32_t any_seen = __ballot_sync(0xffffffffu, seen != 0);
     bool ct = false, cb = false;
     for (uint32_t rows = any_seen; rows; rows &= rows - 1) {
@@ -1776,6 +1795,10 @@ __device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q
     ch.b1 = __any_sync(0xffffffffu, cb);
     ch.b2 = __any_sync(0xffffffffu, cl_);
     ch.b3 = __any_sync(0xffffffffu, cr_);
+#ifdef FM_BFS_TIMING
+    const long long tD = clock64();
+    tm.ld += tB - tA; tm.lvl += tC - tB; tm.wb += tD - tC;
+#endif
     return ch;
 }
 
@@ -1845,14 +1868,23 @@ __global__ void __launch_bounds__(32 * BB_WARPS) ring_kernel(GridDev g, RingQ q)
     // a wait that exceeds this (a neighbour band's launch never started, e.g. two bands
     // on one GPU that cannot be resident together) ends the launch with an error flag
     constexpr unsigned long long WAIT_LIMIT_NS = 20ull * 1000 * 1000 * 1000;
+#ifdef FM_BFS_TIMING
+    BfsTm tm;
+#endif
+    unsigned chg_count = 0;   // visits that changed a border (lane 0; flushed once at the end)
+    int base_slot = 0;
     for (;;) {
         int tile = -1;
+        bool visited = false;
+#ifdef FM_BFS_TIMING
+        const long long tw0 = clock64();
+#endif
         if (lane == 0) {
             const unsigned s = atomicAdd(q.ctr + 0, 1u) % (unsigned)q.cap;
             volatile int32_t *vs = q.slot + s;
             unsigned long long t0 = 0;
             for (unsigned ns = q.ns0;; ns = min(ns * 2, (unsigned)q.ns1)) {
-                tile = *vs;
+                tile = ld_acquire((const int32_t *)vs, q.sys);   // acquire: the producer's stores
                 if (tile >= 0) { *vs = -1; break; }
                 if (*(volatile unsigned *)q.pend == 0) break;
                 if (q.sys) {
@@ -1862,9 +1894,14 @@ __global__ void __launch_bounds__(32 * BB_WARPS) ring_kernel(GridDev g, RingQ q)
                 }
                 __nanosleep(ns);
             }
-            if (tile >= 0) { atomicExch(q.flag + tile, 2); fence_q(q); }
+            if (tile >= 0) visited = (atomicAdd(q.flag + tile, 1) & 4) != 0;   // queued -> in flight
         }
         tile = __shfl_sync(0xffffffffu, tile, 0);
+        visited = __shfl_sync(0xffffffffu, visited ? 1 : 0, 0) != 0;
+        __syncwarp();   // lane 0's acquire orders every lane's loads of the visit
+#ifdef FM_BFS_TIMING
+        tm.wait += clock64() - tw0;
+#endif
         if (tile < 0) break;
         const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
         bool again = true;
@@ -1876,56 +1913,85 @@ __global__ void __launch_bounds__(32 * BB_WARPS) ring_kernel(GridDev g, RingQ q)
             RingChange ch;
             if constexpr (MODE == 0) {
 #ifdef FM_BFS_TIMING
-                ch = bfs_visit(g, q, tile, sd, lane, lv);
+                ch = bfs_visit(g, q, tile, visited, sd, lane, lv, tm);
 #else
-                ch = bfs_visit(g, q, tile, sd, lane);
+                ch = bfs_visit(g, q, tile, visited, sd, lane);
 #endif
             } else {
                 ch = cut_visit(g, tile, lane);
             }
             int st = 0;
-            // lanes 0-3 queue the up / down / left / right neighbour in parallel (each queue
-            // push is a chain of atomics; the fence publishes the warp's stores)
+#ifdef FM_BFS_TIMING
+            const long long tp0 = clock64();
+#endif
+            __syncwarp();   // the warp's stores precede the lanes' release operations below
+            // (1) in parallel: lanes 0-3 claim the up / down / left / right neighbour (state
+            // 0 -> 1: queued by us, 2 -> 3: its owner runs it again; release CAS keeping the
+            // visited bit), lane 4 releases this tile (2 -> idle + visited; release: the
+            // warp's stores, ordered before it by the __syncwarp above, are visible before
+            // the tile can be taken again -- an incremental re-visit on another SM reads the
+            // interior; acquire: a 3 read here sees the stores of the visit that marked it)
+            int nt = -1, peer = 0, own = 0;
+            bool claimed = false;
             if (lane < 4) {
-                int nt = -1, peer = 0;
                 if (lane == 0 && ch.b0) { if (tyi > 0) nt = tile - g.ntx; else if (g.has_up) { nt = g.up.tile0 + txi; peer = 1; } }
                 if (lane == 1 && ch.b1) { if (tyi + 1 < g.nty) nt = tile + g.ntx; else if (g.has_dn) { nt = g.dn.tile0 + txi; peer = 2; } }
                 if (lane == 2 && ch.b2 && txi > 0) nt = tile - 1;
                 if (lane == 3 && ch.b3 && txi + 1 < g.ntx) nt = tile + 1;
                 if (nt >= 0 && (peer || !g.region || g.region[nt])) {
-                    fence_q(q);
-                    if (peer == 1) ringq_push_peer(q, g.up, nt);
-                    else if (peer == 2) ringq_push_peer(q, g.dn, nt);
-                    else ringq_push(q, nt);
+                    int32_t *fl = peer == 1 ? g.up.rq_flag : peer == 2 ? g.dn.rq_flag : q.flag;
+                    const bool sys = q.sys || peer;
+                    for (int c = 0;;) {
+                        const int state = c & 3;
+                        if (state == 1 || state == 3) break;                 // queued / already marked
+                        const int o = cas_acq_rel(fl + nt, c, c + 1, sys);
+                        if (o == c) { claimed = state == 0; break; }
+                        c = o;
+                    }
                 }
+            } else if (lane == 4) {
+                const int v = visited ? 4 : 0;
+                own = cas_acq_rel(q.flag + tile, 2 | v, 4, q.sys);
+                if (own == (3 | v)) atomicExch(q.flag + tile, q.rerun ? (2 | 4) : (1 | 4));   // run again / requeue
             }
-            __syncwarp();   // the pushes (pending++) precede lane 0's pending-- below
+            const unsigned cm = __ballot_sync(0xffffffffu, claimed);
+            const unsigned cl = __ballot_sync(0xffffffffu, claimed && peer == 0);
+            own = __shfl_sync(0xffffffffu, own, 4) & 3;
+            st = own == 3 ? 3 : 0;
             if (lane == 0) {
-                if (MODE == 0 && q.vis) q.vis[tile] += 1;
-                if (ch.any) atomicAdd(q.ctr + 96, 1u);
+                chg_count += ch.any ? 1u : 0u;
 #ifdef FM_BFS_TIMING
                 atomicAdd(q.ctr + 192, 1u);   // every visit (diagnostics)
 #endif
-                // release: the warp's stores (ordered before lane 0 by the __syncwarp
-                // above) are visible before the tile can be taken again -- an
-                // incremental re-visit on another SM reads the interior
-                fence_q(q);
-                st = atomicCAS(q.flag + tile, 2, 0);
-                if (st == 3) {
-                    if (q.rerun) { atomicExch(q.flag + tile, 2); fence_q(q); }
-                    else {   // back of the queue (its neighbours get time to settle); still pending
-                        atomicExch(q.flag + tile, 1);
-                        const unsigned s2 = atomicAdd(q.ctr + 32, 1u);
-                        fence_q(q);
-                        *(volatile int32_t *)(q.slot + (s2 % (unsigned)q.cap)) = tile;
-                        st = 0;
-                    }
+                const int requeue = (st == 3 && !q.rerun) ? 1 : 0;
+                if (requeue) st = 0;
+                // (2) ONE update of the shared pending count: + the claimed neighbours, - this
+                // tile unless it stays queued / in flight.  It precedes the slot stores, so a
+                // claimed tile is counted before anyone can take (and complete) it.
+                const int delta = __popc(cm) - (st == 3 || requeue ? 0 : 1);
+                if (delta) atomicAdd(q.pend, (unsigned)delta);
+                // (3) one reservation of local slots for the claimed neighbours + a requeue
+                const int nl = __popc(cl) + requeue;
+                base_slot = nl ? (int)atomicAdd(q.ctr + 32, (unsigned)nl) : 0;
+                if (requeue) st_release(q.slot + ((unsigned)(base_slot + nl - 1) % (unsigned)q.cap), tile, q.sys);
+            }
+            base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
+            if (claimed) {   // release stores publish the tiles (and our stores) to their takers
+                if (peer) {
+                    const PeerView &pv = peer == 1 ? g.up : g.dn;
+                    const unsigned s2 = atomicAdd(pv.rq_ctr + 32, 1u);
+                    st_release(pv.rq_slot + (s2 % (unsigned)pv.rq_cap), nt, true);
                 } else {
-                    atomicSub(q.pend, 1u);   // after the pushes: pending never reads 0 early
+                    const int rank = __popc(cl & ((1u << lane) - 1));
+                    st_release(q.slot + ((unsigned)(base_slot + rank) % (unsigned)q.cap), nt, q.sys);
                 }
             }
             again = __shfl_sync(0xffffffffu, st, 0) == 3;
+            visited = true;
             __syncwarp();
+#ifdef FM_BFS_TIMING
+            tm.push += clock64() - tp0;
+#endif
         }  // while again
 #ifdef FM_BFS_TIMING
         if (lane == 0) {
@@ -1934,6 +2000,15 @@ __global__ void __launch_bounds__(32 * BB_WARPS) ring_kernel(GridDev g, RingQ q)
         }
 #endif
     }
+    if (lane == 0 && chg_count) atomicAdd(q.ctr + 96, chg_count);
+#ifdef FM_BFS_TIMING
+    if (lane == 0 && MODE == 0) {   // per-section warp cycles: wait, load, levels, write-back, queue
+        unsigned long long *t = (unsigned long long *)(q.ctr + 208);
+        atomicAdd(t + 0, (unsigned long long)tm.wait); atomicAdd(t + 1, (unsigned long long)tm.ld);
+        atomicAdd(t + 2, (unsigned long long)tm.lvl); atomicAdd(t + 3, (unsigned long long)tm.wb);
+        atomicAdd(t + 4, (unsigned long long)tm.push);
+    }
+#endif
 }
 
 // ----------------------------------------------------------------------------
@@ -2654,6 +2729,7 @@ int bfs_sweeps(fm_grid *g, bool first_all) {
         // first_all: every tile (see bfs_init_bits_kernel); else the tiles queued in bq
         const int32_t *list0 = first_all ? nullptr : g->d.bq.list[g->bq_parity];
         const int32_t *cnt0 = first_all ? nullptr : g->d.bq.cnt + 2 * g->bq_parity;
+        if (!first_all) FM_CHECK_CUDA(cudaMemsetAsync(g->rq.flag, 0, sizeof(int32_t) * (size_t)g->ntiles, g->stream));
         ringq_init_kernel<<<std::min((g->rq.cap + 255) / 256, g->sms * 8), 256, 0, g->stream>>>(g->rq, g->ntiles, list0, cnt0);
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[2], g->stream);
@@ -2687,8 +2763,12 @@ void bfs_collect(fm_grid *g) {
     g->st.reserved[0] += g->h_flags[8];
     const float kms = elapsed_between(g->ev[2], g->ev[3]);
     if (g->trace) {
-        unsigned long long tv[4] = {};
+        unsigned long long tv[4] = {}, ts[5] = {};
         cudaMemcpy(tv, g->rq.ctr + 240, sizeof(tv), cudaMemcpyDeviceToHost);   // FM_BFS_TIMING builds
+        cudaMemcpy(ts, g->rq.ctr + 208, sizeof(ts), cudaMemcpyDeviceToHost);
+        const double nv = (double)std::max(1, g->h_flags[10]);
+        if (ts[1]) fprintf(stderr, "[fm_grid]   bfs ring cycles per visit: wait %.0f load %.0f levels %.0f write %.0f queue %.0f\n",
+                           ts[0] / nv, ts[1] / nv, ts[2] / nv, ts[3] / nv, ts[4] / nv);
         const double warps = (double)g->sms * g->br_per_sm * BB_WARPS;
         fprintf(stderr, "[fm_grid]   bfs ring: %d seeded tiles, %d visits (%d changed), %.3f ms | busy %.2f, "
                 "cycles/visit %.0f (level loop %.0f), levels/visit %.1f\n", g->h_flags[11], g->h_flags[10], g->h_flags[8], kms,
@@ -3284,8 +3364,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->prq.rerun = 0; g->prq.ns0 = g->rq.ns0; g->prq.ns1 = g->rq.ns1;
     if (cudaMalloc((void **)&g->rq.slot, sizeof(int32_t) * (size_t)g->rq.cap) != cudaSuccess ||
         cudaMalloc((void **)&g->prq.slot, sizeof(int32_t) * (size_t)g->prq.cap) != cudaSuccess ||
-        cudaMemset(g->rq.flag, 0, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess ||
-        cudaMalloc((void **)&g->rq.vis, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess) {
+        cudaMemset(g->rq.flag, 0, sizeof(int32_t) * (size_t)g->ntiles) != cudaSuccess) {
         fm_set_error("fm_grid_create: allocation failed");
         fm_grid_destroy(g);
         return FM_CUDA_ERROR;
@@ -3306,7 +3385,6 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->d.rbits) cudaFree(g->d.rbits);
     if (g->rq.slot) cudaFree(g->rq.slot);
     if (g->rq.flag) cudaFree(g->rq.flag);
-    if (g->rq.vis) cudaFree(g->rq.vis);
     if (g->rq.ctr) cudaFree(g->rq.ctr);
     if (g->prq.slot) cudaFree(g->prq.slot);
     if (g->prq.flag) cudaFree(g->prq.flag);

@@ -15,8 +15,8 @@ REPS=1 timeout 600 ncu --metrics $M --clock-control none --csv --log-file gpurun
 F="ncu --set full --import-source on --clock-control none"
 REPS=1 timeout 600 $F -k regex:pr_list_kernel -s 0 -c 1 -o gpurun_out/${P}_pr_list_early -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
 REPS=1 timeout 600 $F -k regex:pr_list_kernel -s 40 -c 1 -o gpurun_out/${P}_pr_list_mid -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
-REPS=1 timeout 600 $F --kernel-name-base demangled -k "regex:ring_kernel<0>" -s 3 -c 1 -o gpurun_out/${P}_ring_bfs -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
-REPS=1 timeout 600 $F --kernel-name-base demangled -k "regex:ring_kernel<1>" -s 0 -c 1 -o gpurun_out/${P}_ring_cut -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
+REPS=1 timeout 600 $F --kernel-name-base demangled -k "regex:ring_kernel<.int.0>" -s 3 -c 1 -o gpurun_out/${P}_ring_bfs -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
+REPS=1 timeout 600 $F --kernel-name-base demangled -k "regex:ring_kernel<.int.1>" -s 0 -c 1 -o gpurun_out/${P}_ring_cut -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
 REPS=1 timeout 600 $F -k regex:refine_rounds_kernel -s 2 -c 1 -o gpurun_out/${P}_assign_rounds -f python scripts/assign_one.py 4096 M10000 > /dev/null 2>&1
 REPS=1 timeout 600 $F -k regex:price_update_kernel -s 2 -c 1 -o gpurun_out/${P}_assign_pu -f python scripts/assign_one.py 4096 M10000 > /dev/null 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${P}_launches.csv \
