@@ -2562,11 +2562,11 @@ struct fm_grid {
     int two_hop = 1;                     // two-hop pre-routing after init (option TWO_HOP)
     int k_tail = 0;                      // passes per visit in tail rounds (0: k_local) (option K_TAIL)
     int tail_div = 1024;                 // tail round: active pixels <= H*W / tail_div (option TAIL_DIV)
-    int pr_batch = 4;                    // push launches between host checks of the round triggers (option PR_BATCH)
+    int pr_batch = 0;                    // push launches between checks of the round triggers (option PR_BATCH; 0 = auto)
     int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (option VISIT_MULT)
     bool ring_stats_pending = false;
     bool pr_stats_pending = false;
-    int pr_graph = 0;                    // 1: the push round's launch loop runs as a device while-graph (option PR_GRAPH; measured neutral)
+    int pr_graph = -1;                   // 1: the push round's launch loop runs as a device while-graph (option PR_GRAPH; -1 = auto)
     cudaGraph_t prg = nullptr;           // that graph, its instance and the launch parameters it was built for
     cudaGraphExec_t prg_exec = nullptr;
     GridDev prg_d{};
@@ -3021,13 +3021,21 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
         std::max<long long>(1024, g->HW / (g->relabel_div > 0 ? g->relabel_div : RELABEL_DIV_DEFAULT));
     const bool pk = g->pk && g->pk_ok && g->op_steps == 1 && !g->op_fused;
     const int blocks = std::min(g->ntiles, g->sms * (g->pr_kernel == 1 ? (pk ? g->pk_per_sm : g->pl_per_sm) : g->pt_per_sm));
-    if (g->pr_graph && g->pr_kernel == 1) {
+    // Round triggers checked every `batch` launches.  Auto: large grids (>= 2^23 pixels) check
+    // every 2 launches on the device (the round's launch loop as a while-graph, no host
+    // round trip per check): a launch there is long enough that overshooting the relabel
+    // budget by 3 launches of stale-height work (-22% operations at 4096^2) costs more than
+    // the extra global relabels; smaller grids check every 4 launches from the host (r02r).
+    const bool large = g->HW >= ((int64_t)1 << 23);
+    const int batch_auto = g->pr_batch > 0 ? g->pr_batch : (large ? 2 : 4);
+    const bool use_graph = g->pr_graph >= 0 ? g->pr_graph != 0 : large;
+    if (use_graph && g->pr_kernel == 1) {
         FM_TRY(pr_graph_build(g, k_local, blocks, pk));
         PrCtl *h = pr_ctl_host(g);
         *h = PrCtl{};
         h->parity = g->pq_parity;
         h->cap = cap;
-        h->batch = std::max(1, g->pr_batch);
+        h->batch = std::max(1, batch_auto);
         h->budget = relabel_budget;
         FM_CHECK_CUDA(cudaMemcpyAsync(pr_ctl_dev(g), h, sizeof(PrCtl), cudaMemcpyHostToDevice, g->stream));
         FM_TRY(tq_arm(g, g->d.pq, g->pq_parity));
@@ -3043,7 +3051,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
     }
     int32_t done = 0;
     while (done < cap) {
-        const int batch = std::min(g->pr_batch, cap - done);
+        const int batch = std::min(batch_auto, cap - done);
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
         cudaEventRecord(g->ev[2], g->stream);
         for (int i = 0; i < batch; i++) {
@@ -3355,11 +3363,13 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->pl_per_sm = std::max(1, g->pl_per_sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->bb_per_sm, bfs_bits_kernel, 32 * BB_WARPS, 0);
     g->bb_per_sm = std::max(1, g->bb_per_sm);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->br_per_sm, ring_kernel<0>, 32 * BB_WARPS, 0);
-    g->br_per_sm = std::max(1, std::min(g->br_per_sm, g->br_cap));
-    g->pl_occ = g->pl_per_sm; g->pk_occ = g->pk_per_sm; g->br_occ = g->br_per_sm;
-    // ring capacity: every tile once + one reserved slot per resident warp
-    g->rq.cap = g->ntiles + g->sms * g->br_per_sm * BB_WARPS + 64;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->br_occ, ring_kernel<0>, 32 * BB_WARPS, 0);
+    g->br_occ = std::max(1, g->br_occ);
+    g->br_per_sm = std::max(1, std::min(g->br_occ, g->br_cap));
+    g->pl_occ = g->pl_per_sm; g->pk_occ = g->pk_per_sm;
+    // ring capacity: every tile once + one reserved slot per warp that can be resident
+    // (fixed at the occupancy maximum: neighbour bands index this ring with it)
+    g->rq.cap = g->ntiles + g->sms * g->br_occ * BB_WARPS + 64;
     g->prq.cap = g->ntiles + g->sms * g->pl_per_sm + 64;
     g->prq.rerun = 0; g->prq.ns0 = g->rq.ns0; g->prq.ns1 = g->rq.ns1;
     if (cudaMalloc((void **)&g->rq.slot, sizeof(int32_t) * (size_t)g->rq.cap) != cudaSuccess ||
@@ -3624,8 +3634,7 @@ extern "C" int fm_grid_set_option(fm_grid *g, const char *name, int64_t value) {
     else if (k == "vote") g->vote_mask = std::max(1, v) - 1;
     else if (k == "pr_kernel") g->pr_kernel = v;
     else if (k == "bfs_bits") g->bfs_bits = v;
-    else if (k == "br_cap") { g->br_cap = std::max(1, v); g->br_per_sm = std::max(1, std::min(g->br_occ, g->br_cap));
-                              g->rq.cap = g->ntiles + g->sms * g->br_per_sm * BB_WARPS + 64; }
+    else if (k == "br_cap") { g->br_cap = std::max(1, v); g->br_per_sm = std::max(1, std::min(g->br_occ, g->br_cap)); }
     else if (k == "pr_ring") g->pr_ring = v;
     else if (k == "pr_graph") g->pr_graph = v;
     else if (k == "packed") g->pk = v;
@@ -3635,7 +3644,7 @@ extern "C" int fm_grid_set_option(fm_grid *g, const char *name, int64_t value) {
     else if (k == "k_tail") g->k_tail = v;
     else if (k == "two_hop") g->two_hop = v;
     else if (k == "tail_div") g->tail_div = v;
-    else if (k == "pr_batch") g->pr_batch = std::max(1, std::min(16, v));
+    else if (k == "pr_batch") g->pr_batch = std::max(0, std::min(16, v));
     else if (k == "visit_mult") g->visit_mult = std::max(1, v);
     else if (k == "br_rerun") g->rq.rerun = v;
     else if (k == "br_ns0") g->rq.ns0 = v;
@@ -4022,7 +4031,7 @@ int band_push_round(fm_grid *g, fm_coll *c, int32_t cycle_budget) {
     int32_t done = 0;
     int64_t all[COLL_MAX_RANKS * 4];
     while (done < cap) {
-        const int batch = std::min(g->pr_batch, cap - done);
+        const int batch = std::min(g->pr_batch > 0 ? g->pr_batch : 4, cap - done);
         FM_CHECK_CUDA(cudaMemsetAsync(g->flags, 0, sizeof(int32_t) * batch, g->stream));
         cudaEventRecord(g->ev[2], g->stream);
         for (int i = 0; i < batch; i++) {
