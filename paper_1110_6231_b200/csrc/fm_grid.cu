@@ -2120,9 +2120,12 @@ __global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsi
             const int64_t p = (int64_t)r * g.W + c;
             {
                 const int4 d4 = *(const int4 *)(g.dist + p), e4 = *(const int4 *)(g.e + p);
-                int4 h4 = *(const int4 *)(g.h + p);
-                uchar4 m4 = *(const uchar4 *)(g.marked + p);
                 const int dv[4] = {d4.x, d4.y, d4.z, d4.w}, ev[4] = {e4.x, e4.y, e4.z, e4.w};
+                // old heights and marks matter only for unreached pixels (reached ones take
+                // their distance): most groups skip those two reads
+                const bool unreached = dv[0] >= g.INF || dv[1] >= g.INF || dv[2] >= g.INF || dv[3] >= g.INF;
+                const int4 h4 = unreached ? *(const int4 *)(g.h + p) : make_int4(0, 0, 0, 0);
+                const uchar4 m4 = unreached ? *(const uchar4 *)(g.marked + p) : make_uchar4(1, 1, 1, 1);
                 int hv[4] = {h4.x, h4.y, h4.z, h4.w};
                 unsigned char mv[4] = {m4.x, m4.y, m4.z, m4.w};
                 bool mchg = false;
