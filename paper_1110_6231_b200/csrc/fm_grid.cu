@@ -11,6 +11,7 @@
 #include <thread>
 #include <vector>
 #include <climits>
+#include <cuda.h>   // CUtensorMap (TMA descriptors; encoded through the runtime's driver entry point)
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -585,6 +586,42 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool pre
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
 }
+
+// ---- TMA (cp.async.bulk.tensor) staging of a tile visit's planes ---------------------
+// Tensor maps of the int32 planes (H x W, row-major): e, rT, rS as 32 x 32 boxes at
+// (c0, r0); h as a 40 x 34 box at (c0 - 4, r0 - 1), which is exactly the padded halo
+// layout of PlSmemT::h (row stride PL_HS = 40, column c at PL_HC = 4 + c) -- the halo
+// rows and columns arrive with the interior, out-of-grid cells zero-filled.  r[4]: the
+// int32 residual planes (the packed instance packs them from registers instead).  One
+// thread arms the CTA's mbarrier with the byte count and issues the copies; every thread
+// waits on the barrier's phase.  Used when W % 4 == 0 (TMA strides are 16-byte multiples).
+struct PlMaps {
+    CUtensorMap e, t, s, h, r[4];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long *mbar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned long long *mbar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *mbar, unsigned parity) {
+    asm volatile("{\n .reg .pred P1;\n"
+                 "FM_WAIT_%=:\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                 " @!P1 bra FM_WAIT_%=;\n}" ::"r"(smem_u32(mbar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y, unsigned long long *mbar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(smem_u32(dst)), "l"(map), "r"(x), "r"(y), "r"(smem_u32(mbar)) : "memory");
+}
+// earlier generic-proxy accesses of this thread to shared memory before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 #ifndef FM_PL_MINBLOCKS
 #define FM_PL_MINBLOCKS 6
 #endif
@@ -835,13 +872,17 @@ __device__ __forceinline__ bool pl_item(const GridDev &g, const PlTile &T, int l
 template <bool PK> struct PlRes { int32_t r[4][PT_H * PT_W]; };              // R, L, D, U
 template <> struct PlRes<true> { uint2 r2[PT_H * PT_W]; };                  // packed 16-bit fields
 
-template <bool PK> struct PlSmemT {
+// Members a TMA copy lands in start on 128-byte boundaries (e, t, list -- rS is staged in
+// list[0] --, h, and the int32 residual planes).
+constexpr int PL_HWORDS = ((PT_H + 2) * PL_HS + 31) / 32 * 32;   // 34 x 40 heights, padded to 128 B
+template <bool PK> struct __align__(128) PlSmemT {
     int32_t e[PT_H * PT_W];
-    int32_t h[(PT_H + 2) * PL_HS];
-    PlRes<PK> res;
     int32_t t[PT_H * PT_W];
-    uint8_t f[PT_H * PT_W];      // bit 0: residual arc to s, bit 1: ghost row
     uint16_t list[2][PT_H * PT_W];
+    int32_t h[PL_HWORDS];
+    PlRes<PK> res;
+    uint8_t f[PT_H * PT_W];      // bit 0: residual arc to s, bit 1: outside the grid
+    unsigned long long mbar;     // TMA completion barrier (one per CTA, phase flips per visit)
     int cnt[3];
     int nbr;
     int tile;
@@ -862,7 +903,7 @@ struct PlCounters {
 // neighbour tiles whose inboxes received flow.  Starts and ends with a barrier.
 template <bool PK>
 __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int tile, int k_local, int steps,
-                                         int fused, PlCounters &C) {
+                                         int fused, PlCounters &C, const PlMaps *maps, unsigned &tma_phase) {
     constexpr int HS = PL_HS;
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * PT_W + tx;
     const int V = g.V;
@@ -876,13 +917,48 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
     else T = PlTile{S.e, S.h, S.t, S.res.r, nullptr, S.f, &S.nbr, tyi * PT_H, txi * PT_W};
     const int r0 = T.r0, c0 = T.c0;
     int32_t *stage = (int32_t *)&S.list[0][0];   // rS staging (the lists are built afterwards)
-    // load: asynchronous global -> shared copies, thread = (row, 4-column chunk)
+    // load.  TMA (maps != nullptr): one thread issues the plane copies, the halo rows and
+    // columns arrive inside the height box; else cp.async, thread = (row, 4-column chunk).
+    const bool tma = maps != nullptr;
+    if (tma) {
+        fence_proxy_async_smem();   // this visit's async writes come after every earlier smem access
+        __syncthreads();
+        if (tid == 0) {
+            constexpr unsigned bytes = 3 * PT_H * PT_W * 4 + (PT_H + 2) * PL_HS * 4 + (PK ? 0 : 4 * PT_H * PT_W * 4);
+            mbar_expect(&S.mbar, bytes);
+            tma_load_2d(S.e, &maps->e, c0, r0, &S.mbar);
+            tma_load_2d(S.t, &maps->t, c0, r0, &S.mbar);
+            tma_load_2d(stage, &maps->s, c0, r0, &S.mbar);
+            tma_load_2d(S.h, &maps->h, c0 - PL_HC, r0 - 1, &S.mbar);
+            if constexpr (!PK)
+                for (int k = 0; k < 4; k++) tma_load_2d(S.res.r[k], &maps->r[k], c0, r0, &S.mbar);
+        }
+    }
     {
         const int lrow = tid >> 3, ch = tid & 7;
         const int r = r0 + lrow, cb = c0 + 4 * ch;
         const int li = lrow * PT_W + 4 * ch, hi = (lrow + 1) * HS + PL_HC + 4 * ch;
-        if (r < g.H && cb + 4 <= g.W && (g.W & 3) == 0) {
-            const int64_t p = (int64_t)r * g.W + cb;
+        if (tma) {
+            // the packed instance's residual fields are assembled from registers
+            if constexpr (PK) {
+                if (r < g.H && cb + 4 <= g.W) {
+                    const int64_t p = (int64_t)r * g.W + cb;
+                    const int4 a = __ldcg((const int4 *)(g.rR + p)), b = __ldcg((const int4 *)(g.rL + p));
+                    const int4 d = __ldcg((const int4 *)(g.rD + p)), u = __ldcg((const int4 *)(g.rU + p));
+                    S.res.r2[li + 0] = pk_pack(a.x, b.x, d.x, u.x);
+                    S.res.r2[li + 1] = pk_pack(a.y, b.y, d.y, u.y);
+                    S.res.r2[li + 2] = pk_pack(a.z, b.z, d.z, u.z);
+                    S.res.r2[li + 3] = pk_pack(a.w, b.w, d.w, u.w);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const bool in = r < g.H && cb + j < g.W;
+                        const int64_t p = in ? (int64_t)r * g.W + cb + j : 0;
+                        S.res.r2[li + j] = in ? pk_pack(__ldcg(g.rR + p), __ldcg(g.rL + p), __ldcg(g.rD + p), __ldcg(g.rU + p)) : make_uint2(0u, 0u);
+                    }
+                }
+            }
+        } else if (r < g.H && cb + 4 <= g.W && (g.W & 3) == 0) {            const int64_t p = (int64_t)r * g.W + cb;
             cp_async16(&S.e[li], g.e + p);
             if constexpr (PK) {
                 const int4 a = __ldcg((const int4 *)(g.rR + p)), b = __ldcg((const int4 *)(g.rL + p));
@@ -922,8 +998,8 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
     }
     // halo heights (a snapshot: stale reads are the lock-free argument's business) and
     // the inboxes of the border pixels, both issued while the copies are in flight
-    int32_t inbox = 0;
-    int ib_li = -1, ib_dir = 0;
+    int32_t inbox = 0, peer_h = 0;
+    int ib_li = -1, ib_dir = 0, peer_hidx = -1;
     if (tid < 4 * PT_W) {
         const int side = tid / PT_W, i = tid % PT_W;
         int r, cc, hidx;
@@ -932,10 +1008,12 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
         else if (side == 2) { r = r0 + i; cc = c0 - 1; hidx = (i + 1) * HS + PL_HC - 1; }
         else { r = r0 + i; cc = c0 + PT_W; hidx = (i + 1) * HS + PL_HC + PT_W; }
         const bool hin = r >= 0 && r < g.H && cc >= 0 && cc < g.W;
-        if (side < 2 && !hin && cc < g.W && ((r < 0 && g.has_up) || (r == g.H && g.has_dn)))
-            S.h[hidx] = ld_cg((r < 0 ? g.up.h : g.dn.h) + cc);   // row bands: the neighbour band's row
-        else
+        if (side < 2 && !hin && cc < g.W && ((r < 0 && g.has_up) || (r == g.H && g.has_dn))) {
+            peer_h = ld_cg((r < 0 ? g.up.h : g.dn.h) + cc);   // row bands: the neighbour band's row
+            peer_hidx = hidx;                                  // (stored after the TMA wait)
+        } else if (!tma) {
             cp_async4(&S.h[hidx], g.h + (hin ? (int64_t)r * g.W + cc : 0), hin);
+        }
         // border pixel of this side and its inbox (flow parked by the neighbour tile)
         const int lr = side == 0 ? 0 : side == 1 ? PT_H - 1 : i;
         const int lc = side == 2 ? 0 : side == 3 ? PT_W - 1 : i;
@@ -949,7 +1027,13 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
             ib_dir = side == 0 ? 3 : side == 1 ? 2 : side == 2 ? 1 : 0;   // residual toward the sender
         }
     }
-    cp_async_wait_all();
+    if (tma) {
+        mbar_wait(&S.mbar, tma_phase);
+        tma_phase ^= 1u;
+    } else {
+        cp_async_wait_all();
+    }
+    if (peer_hidx >= 0) S.h[peer_hidx] = peer_h;
     __syncthreads();
     if (inbox) {
         atomicAdd(&S.e[ib_li], inbox);          // a corner pixel has two inboxes
@@ -1117,9 +1201,15 @@ template <bool PK>
 __global__ void __launch_bounds__(PL_NT, PK ? FM_PK_MINBLOCKS : FM_PL_MINBLOCKS) pr_list_kernel(GridDev g, int k_local, int steps, int fused,
                                                                        int parity_arg, int32_t *processed,
                                                                        unsigned long long *ops,
-                                                                       PrCtl *ctl, cudaGraphConditionalHandle loop) {
+                                                                       PrCtl *ctl, cudaGraphConditionalHandle loop,
+                                                                       const __grid_constant__ PlMaps maps, int use_tma) {
     __shared__ PlSmemT<PK> S;
     const int tid = threadIdx.y * PT_W + threadIdx.x;
+    unsigned tma_phase = 0;
+    if (use_tma) {
+        if (tid == 0) mbar_init(&S.mbar);
+        __syncthreads();
+    }
     // graph launches read the launch parity from the round's control block (processed
     // then points into it); host launches pass it as an argument
     const int parity = ctl ? __ldcg(&ctl->parity) : parity_arg;
@@ -1130,7 +1220,7 @@ __global__ void __launch_bounds__(PL_NT, PK ? FM_PK_MINBLOCKS : FM_PL_MINBLOCKS)
         __syncthreads();
         const int tile = S.tile;
         if (tile < 0) break;
-        const bool any_act = pl_visit(g, S, tile, k_local, steps, fused, C);
+        const bool any_act = pl_visit(g, S, tile, k_local, steps, fused, C, use_tma ? &maps : nullptr, tma_phase);
         if (tid == 0) {
             if (any_act) tq_push(g.pq, parity ^ 1, tile);
             g.touched[tile] = 1;
@@ -2061,7 +2151,8 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_ring_kernel(GridDev
         const int tile = S.tile;
         if (tile < 0) break;
         const long long rel0 = C.relabels;
-        const bool act = pl_visit(g, S, tile, k_local, steps, fused, C);
+        unsigned no_tma = 0;
+        const bool act = pl_visit(g, S, tile, k_local, steps, fused, C, nullptr, no_tma);
         // this visit's relabels, CTA-wide (for the round's relabel budget)
         long long dr = C.relabels - rel0;
 #pragma unroll
@@ -2573,7 +2664,7 @@ struct fm_grid {
     cudaGraph_t prg = nullptr;           // that graph, its instance and the launch parameters it was built for
     cudaGraphExec_t prg_exec = nullptr;
     GridDev prg_d{};
-    int prg_key[5] = {0, 0, 0, 0, 0};
+    int prg_key[6] = {0, 0, 0, 0, 0, 0};
     bool prg_pending = false;            // round control block read back, consumed after the caller's sync
     int pr_kernel = 1;                   // 1: pr_list_kernel (v3), 0: pr_tile_kernel (v2) (option PR_KERNEL)
     int pl_per_sm = 6;                   // resident pr_list CTAs per SM (occupancy query)
@@ -2593,6 +2684,9 @@ struct fm_grid {
     int k_local = 0;                     // tuning overrides (options k_local / bfs_interval)
     int trace = 0;                       // option TRACE=1: one stderr line per round
     int bfs_interval_env = 0;
+    PlMaps maps{};                       // TMA descriptors of the push kernel's planes (tile visit staging)
+    bool maps_ok = false;                // encoded (W % 4 == 0 and the driver entry point resolved)
+    int tma = 1;                         // option TMA: stage tile visits with cp.async.bulk.tensor (0: cp.async)
     // row-band mode (fm_grid_band_*): this handle is band `band` of `nbands`
     int band = -1, nbands = 0;
     int colocated = 1;                   // bands sharing this device (persistent grids split between them)
@@ -2635,6 +2729,41 @@ int sync_stream(fm_grid *g) {
 // persistent ring grid: every resident slot, shared between the bands on this device
 int ring_blocks(const fm_grid *g) {
     return std::max(1, g->sms * g->br_per_sm / std::max(1, g->colocated));
+}
+
+int use_tma(const fm_grid *g) { return g->tma && g->maps_ok ? 1 : 0; }
+
+// TMA descriptors of the planes a push-kernel tile visit stages (PlMaps).  The encoder
+// is the driver's cuTensorMapEncodeTiled, reached through the runtime's entry-point
+// query (no libcuda link).  Planes must have a row pitch that is a 16-byte multiple.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+void encode_maps(fm_grid *g) {
+    g->maps_ok = false;
+    if (g->W % 4) return;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+        cudaGetLastError();
+        return;
+    }
+    const EncodeTiledFn enc = (EncodeTiledFn)fn;
+    const cuuint64_t dims[2] = {(cuuint64_t)g->W, (cuuint64_t)g->H};
+    const cuuint64_t strides[1] = {(cuuint64_t)g->W * 4};
+    const cuuint32_t tile_box[2] = {PT_W, PT_H}, halo_box[2] = {PL_HS, PT_H + 2}, es[2] = {1, 1};
+    struct { CUtensorMap *m; int32_t *plane; const cuuint32_t *box; } list[] = {
+        {&g->maps.e, g->d.e, tile_box}, {&g->maps.t, g->d.rT, tile_box}, {&g->maps.s, g->d.rS, tile_box},
+        {&g->maps.h, g->d.h, halo_box}, {&g->maps.r[0], g->d.rR, tile_box}, {&g->maps.r[1], g->d.rL, tile_box},
+        {&g->maps.r[2], g->d.rD, tile_box}, {&g->maps.r[3], g->d.rU, tile_box}};
+    for (auto &x : list)
+        if (enc(x.m, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, x.plane, dims, strides, x.box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+            CUDA_SUCCESS)
+            return;
+    g->maps_ok = true;
 }
 
 float elapsed_between(cudaEvent_t a, cudaEvent_t b) {
@@ -2961,7 +3090,7 @@ PrCtl *pr_ctl_host(fm_grid *g) { return reinterpret_cast<PrCtl *>(g->h_flags + 3
 // pr_list_kernel node whose last CTA sets the loop condition).  Rebuilt only when a
 // parameter baked into the node changes.
 int pr_graph_build(fm_grid *g, int k_local, int blocks, bool pk) {
-    const int key[5] = {k_local, blocks, g->op_steps, g->op_fused, pk ? 1 : 0};
+    const int key[6] = {k_local, blocks, g->op_steps, g->op_fused, pk ? 1 : 0, use_tma(g)};
     if (g->prg_exec && !memcmp(key, g->prg_key, sizeof(key)) && !memcmp(&g->d, &g->prg_d, sizeof(GridDev)))
         return FM_OK;
     if (g->prg_exec) { cudaGraphExecDestroy(g->prg_exec); g->prg_exec = nullptr; }
@@ -2983,7 +3112,9 @@ int pr_graph_build(fm_grid *g, int k_local, int blocks, bool pk) {
     int steps = g->op_steps, fused = g->op_fused, parity0 = 0;
     int32_t *processed = &ctl->processed;
     unsigned long long *ops = g->acc + 10;
-    void *pr_args[] = {&d, &k_local, &steps, &fused, &parity0, &processed, &ops, &ctl, &handle};
+    PlMaps maps = g->maps;
+    int tma = use_tma(g);
+    void *pr_args[] = {&d, &k_local, &steps, &fused, &parity0, &processed, &ops, &ctl, &handle, &maps, &tma};
     cudaKernelNodeParams kp{};
     kp.func = pk ? (void *)pr_list_kernel<true> : (void *)pr_list_kernel<false>;
     kp.gridDim = dim3(blocks);
@@ -3062,7 +3193,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
             FM_TRY(tq_arm(g, g->d.pq, p));
             if (g->pr_kernel == 1)
                 (pk ? pr_list_kernel<true> : pr_list_kernel<false>)<<<blocks, dim3(PT_W, PL_TY), 0, g->stream>>>(
-                    g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10, nullptr, 0);
+                    g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10, nullptr, 0, g->maps, use_tma(g));
             else
                 pr_tile_kernel<<<blocks, dim3(PT_W, PT_TY), 0, g->stream>>>(g->d, k_local, g->op_steps, g->op_fused, g->vote_mask, p, g->flags + i, g->acc + 10);
             g->pq_parity ^= 1;
@@ -3383,6 +3514,7 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
         return FM_CUDA_ERROR;
     }
     g->grid_blocks = (int)std::min<int64_t>((g->HW + 255) / 256, (int64_t)sms * 8);
+    encode_maps(g);
     *out = g;
     return FM_OK;
 }
@@ -3640,6 +3772,7 @@ extern "C" int fm_grid_set_option(fm_grid *g, const char *name, int64_t value) {
     else if (k == "br_cap") { g->br_cap = std::max(1, v); g->br_per_sm = std::max(1, std::min(g->br_occ, g->br_cap)); }
     else if (k == "pr_ring") g->pr_ring = v;
     else if (k == "pr_graph") g->pr_graph = v;
+    else if (k == "tma") g->tma = v;
     else if (k == "packed") g->pk = v;
     else if (k == "bfs_incr") g->rq.incr = v ? 1 : 0;
     else if (k == "k_solo") g->d.k_solo = v;
@@ -4041,7 +4174,7 @@ int band_push_round(fm_grid *g, fm_coll *c, int32_t cycle_budget) {
             const int p = g->pq_parity;
             band_arm_kernel<<<1, 256, 0, g->stream>>>(g->d, p);
             (pk ? pr_list_kernel<true> : pr_list_kernel<false>)<<<blocks, dim3(PT_W, PL_TY), 0, g->stream>>>(
-                g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10, nullptr, 0);
+                g->d, k_local, g->op_steps, g->op_fused, p, g->flags + i, g->acc + 10, nullptr, 0, g->maps, use_tma(g));
             g->pq_parity ^= 1;
         }
         FM_CHECK_LAUNCH();

@@ -39,6 +39,9 @@ VARIANTS = {
     "bfs_incremental_rerun": {"bfs_incr": 1, "br_rerun": 1},
     "bfs_incremental_no_local": {"bfs_incr": 1, "local_div": 0},
     "pr_graph_b1": {"pr_graph": 1, "pr_batch": 1},
+    "pr_graph_b2": {"pr_graph": 1, "pr_batch": 2},
+    "no_tma": {"tma": 0},
+    "unpacked_no_tma": {"packed": 0, "tma": 0},
 }
 
 CASES = [("G", 96, 160, 11), ("G", 257, 130, 12), ("S", 200, 256, 2048), ("G", 31, 33, 13)]
