@@ -2634,7 +2634,7 @@ struct fm_grid {
     uint8_t *h_cut_stage = nullptr;      // pinned bounce buffer for the cut (host-output calls)
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev[4] = {};
+    cudaEvent_t ev[8] = {};   // [0..3] phase / kernel timing, [4..7] a push round whose stats are read after the relabel
     int grid_blocks = 0;                 // 1-D grid-stride kernels
     int ntiles = 0;                      // 32 x 32 tiles of the tile-resident kernel
     int32_t *d_queues = nullptr;         // push + BFS tile work lists
@@ -3129,16 +3129,16 @@ int pr_graph_build(fm_grid *g, int k_local, int blocks, bool pk) {
 }
 
 // Fold the control block of the last graph round into the stats (after a stream sync).
-void pr_graph_consume(fm_grid *g, int32_t *idle_out) {
+void pr_graph_consume(fm_grid *g, int32_t *idle_out, bool keep_parity = false) {
     if (!g->prg_pending) return;
     g->prg_pending = false;
     const PrCtl *c = pr_ctl_host(g);
-    g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
+    g->st.ms_pr_kern += elapsed_between(g->ev[6], g->ev[7]);
     g->st.launches += c->done;
     g->st.pr_launches += c->done;
     g->st.pr_sweeps += c->done;
     g->st.pr_tiles += (int64_t)c->tiles;
-    g->pq_parity = c->parity;
+    if (!keep_parity) g->pq_parity = c->parity;   // (a relabel that ran since reset the lists)
     if (idle_out) *idle_out = c->processed == 0 ? 1 : 0;
 }
 
@@ -3173,9 +3173,9 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
         h->budget = relabel_budget;
         FM_CHECK_CUDA(cudaMemcpyAsync(pr_ctl_dev(g), h, sizeof(PrCtl), cudaMemcpyHostToDevice, g->stream));
         FM_TRY(tq_arm(g, g->d.pq, g->pq_parity));
-        cudaEventRecord(g->ev[2], g->stream);
+        cudaEventRecord(g->ev[6], g->stream);
         FM_CHECK_CUDA(cudaGraphLaunch(g->prg_exec, g->stream));
-        cudaEventRecord(g->ev[3], g->stream);
+        cudaEventRecord(g->ev[7], g->stream);
         FM_CHECK_CUDA(cudaMemcpyAsync(h, pr_ctl_dev(g), sizeof(PrCtl), cudaMemcpyDeviceToHost, g->stream));
         g->prg_pending = true;
         integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
@@ -3260,7 +3260,7 @@ int run_round_ring(fm_grid *g, int32_t cycle_budget) {
 int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     const fm_stats before = g->st;
     const long long active_before = g->active;
-    cudaEventRecord(g->ev[0], g->stream);
+    cudaEventRecord(g->ev[4], g->stream);
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
     int32_t sweeps = 0;
     if (g->flags_solve & FM_GRID_GLOBAL_SWEEP) {
@@ -3277,19 +3277,28 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     }
     FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 10, g->acc + 10, sizeof(unsigned long long) * 5,
                                   cudaMemcpyDeviceToHost, g->stream));
-    cudaEventRecord(g->ev[1], g->stream);
-    FM_TRY(sync_stream(g));
-    pr_graph_consume(g, nullptr);
-    if (g->pr_stats_pending) {
-        g->pr_stats_pending = false;
-        g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
-        g->st.pr_tiles += g->h_flags[9];
+    cudaEventRecord(g->ev[5], g->stream);
+    // The relabel decision needs nothing from this push round, so its counters are read
+    // after the relabel's own stream sync (one host round trip per round); the ring push
+    // variant reuses ev[2]/ev[3] and is collected here.
+    const auto collect = [&](bool after_relabel) {
+        pr_graph_consume(g, nullptr, after_relabel);
+        if (g->pr_stats_pending) {
+            g->pr_stats_pending = false;
+            g->st.ms_pr_kern += elapsed_between(g->ev[2], g->ev[3]);
+            g->st.pr_tiles += g->h_flags[9];
+        }
+        g->st.ms_push += elapsed_between(g->ev[4], g->ev[5]);
+        g->st.pushes += (int64_t)g->h_acc[10];
+        g->st.relabels += (int64_t)g->h_acc[11];
+        g->st.reserved[2] = (int64_t)g->h_acc[13];   // list-kernel passes (cumulative per solve)
+        g->st.reserved[3] = (int64_t)g->h_acc[14];   // list-kernel items
+    };
+    const bool deferred = !g->pr_stats_pending;
+    if (!deferred) {
+        FM_TRY(sync_stream(g));
+        collect(false);
     }
-    g->st.ms_push += elapsed(g);
-    g->st.pushes += (int64_t)g->h_acc[10];
-    g->st.relabels += (int64_t)g->h_acc[11];
-    g->st.reserved[2] = (int64_t)g->h_acc[13];   // list-kernel passes (cumulative per solve)
-    g->st.reserved[3] = (int64_t)g->h_acc[14];   // list-kernel items
     const bool go_local = g->local_div > 0 && !(g->flags_solve & FM_GRID_GLOBAL_SWEEP) &&
                           !(g->flags_solve & FM_GRID_CANCEL_VIOLATIONS) &&
                           g->active <= g->HW / g->local_div && g->local_streak < g->local_max;
@@ -3300,6 +3309,7 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
         g->local_streak = 0;
         FM_TRY(global_relabel(g));
     }
+    if (deferred) collect(true);   // the relabel synchronised the stream (and reset the work lists)
     g->st.rounds++;
     if (g->trace)
         fprintf(stderr, "[fm_grid] round %lld active %lld -> %lld | launches %lld tiles %lld pushes %lld relabels %lld "
