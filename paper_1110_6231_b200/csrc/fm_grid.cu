@@ -1503,6 +1503,41 @@ __device__ __forceinline__ uint32_t bits_row(const GridDev &g, int tile, int lr,
     return w[4];
 }
 
+// bits_row for rows lr0 .. lr0 + 3 of a tile with all 20 plane loads issued before the
+// first ballot (memory-level parallelism: the preparation pass is HBM-bound)
+__device__ __forceinline__ void bits_rows4(const GridDev &g, int tile, int lr0, int lane) {
+    const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+    const int c = txi * PT_W + lane;
+    int32_t vR[4], vL[4], vD[4], vU[4], vT[4];
+    bool in[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int r = tyi * PT_H + lr0 + k;
+        in[k] = r < g.H && c < g.W;
+        const int64_t p = in[k] ? (int64_t)r * g.W + c : 0;
+        vR[k] = in[k] ? __ldcs(g.rR + p) : 0;
+        vL[k] = in[k] ? __ldcs(g.rL + p) : 0;
+        vD[k] = in[k] ? __ldcs(g.rD + p) : 0;
+        vU[k] = in[k] ? __ldcs(g.rU + p) : 0;
+        vT[k] = in[k] ? __ldcs(g.rT + p) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int r = tyi * PT_H + lr0 + k;
+        const bool aR = in[k] && c + 1 < g.W && vR[k] > 0;
+        const bool aL = in[k] && c > 0 && vL[k] > 0;
+        const bool aD = in[k] && r + 1 < g.hlim && vD[k] > 0;
+        const bool aU = in[k] && r > g.rmin && vU[k] > 0;
+        const bool aT = in[k] && vT[k] > 0;
+        const uint32_t w[5] = {__ballot_sync(0xffffffffu, aR), __ballot_sync(0xffffffffu, aL),
+                               __ballot_sync(0xffffffffu, aD), __ballot_sync(0xffffffffu, aU),
+                               __ballot_sync(0xffffffffu, aT)};
+        uint32_t *B = g.rbits + (size_t)tile * 160 + lr0 + k;
+        if (lane < 5) B[lane * 32] = w[lane];
+        if (in[k]) g.dist[(int64_t)r * g.W + c] = aT ? 1 : g.INF;
+    }
+}
+
 // listed == 0: every tile; listed == 1: the tiles of bq.list[0] (local relabel region).
 // (Seeding the ring with only the tiles that hold a sink arc is NOT enough: a tile
 // without one next to a sink pixel on its neighbour's border is never notified -- that
@@ -1685,6 +1720,57 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
         q.ctr[240] = q.ctr[241] = q.ctr[244] = q.ctr[245] = q.ctr[246] = q.ctr[247] = 0;
         q.ctr[248] = 0;
         for (int i = 208; i < 218; i++) q.ctr[i] = 0;
+    }
+}
+
+// The global relabel's preparation in ONE launch (single band, default kernels): per tile
+// row, the BFS arc words and distance seeds -- rebuilt from the residual planes only for
+// tiles a push touched since the last relabel (full: every tile), else the seeds come
+// from the tile's unchanged sink word --, the ring with every tile queued, the push work
+// list's flags, and the relabel's counters.  Replaces bfs_init_bits + ringq_init + three
+// memsets.  Touched flags are cleared by the finalize that follows the BFS.
+__global__ void relabel_init_kernel(GridDev g, RingQ q, int full, unsigned long long *acc) {
+    const int lane = threadIdx.x & 31;
+    const int ntiles = g.ntx * g.nty;
+    const int64_t nquads = (int64_t)ntiles * (PT_H / 4);
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nquads;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        // consecutive warps take the same 4 rows of consecutive tiles: every plane is then
+        // read as runs of adjacent 128-byte row segments (DRAM-friendly), not one segment
+        // per 16 KB row stride
+        const int tx = (int)(w % g.ntx);
+        const int64_t rest = w / g.ntx;
+        const int ty = (int)(rest / (PT_H / 4)), lr0 = 4 * (int)(rest % (PT_H / 4));
+        const int tile = ty * g.ntx + tx;
+        if (full || g.touched[tile]) {
+            bits_rows4(g, tile, lr0, lane);
+        } else {
+            const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+            const int c = txi * PT_W + lane;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int r = tyi * PT_H + lr0 + k;
+                const uint32_t tw = g.rbits[(size_t)tile * 160 + 128 + lr0 + k];
+                if (r < g.H && c < g.W) g.dist[(int64_t)r * g.W + c] = ((tw >> lane) & 1u) ? 1 : g.INF;
+            }
+        }
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < q.cap; i += gridDim.x * blockDim.x) {
+        q.slot[i] = i < ntiles ? i : -1;
+        if (i < ntiles) {
+            q.flag[i] = 1;
+            g.pq.flag[0][i] = 0;
+            g.pq.flag[1][i] = 0;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        q.ctr[0] = 0; q.ctr[32] = ntiles; q.ctr[64] = ntiles; q.ctr[96] = 0;
+        q.ctr[128] = 0; q.ctr[160] = 0; q.ctr[161] = 0; q.ctr[192] = 0; q.ctr[224] = ntiles;
+        q.ctr[240] = q.ctr[241] = q.ctr[244] = q.ctr[245] = q.ctr[246] = q.ctr[247] = 0;
+        q.ctr[248] = 0;
+        for (int i = 208; i < 218; i++) q.ctr[i] = 0;
+        g.pq.cnt[0] = g.pq.cnt[1] = g.pq.cnt[2] = g.pq.cnt[3] = 0;
+        acc[0] = acc[1] = acc[2] = 0;
     }
 }
 
@@ -2205,6 +2291,7 @@ __global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsi
         const int tile = list ? list[it] : it;
         const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
         bool act = false;
+        if (!list && threadIdx.x == 0) g.touched[tile] = 0;   // global relabel: every tile is current
         const int r = tyi * PT_H + (threadIdx.x >> 3), c = txi * PT_W + 4 * (threadIdx.x & 7);
         if ((g.W & 3) == 0 && (tyi + 1) * PT_H <= g.H && (txi + 1) * PT_W <= g.W) {
             // interior tile, W % 4 == 0: 4 consecutive pixels per thread, 16-byte accesses
@@ -2698,6 +2785,7 @@ struct fm_grid {
     int32_t *band_caps = nullptr;        // band inputs staged by fm_grid_band_solve: 6 planes + 2 halo rows
     // solve state
     int32_t flags_solve = 0;
+    bool relabel_full = true;            // next global relabel rebuilds every tile's arc words
     long long sum_capS = 0;
     long long excess_total = 0;          // maxflow_par.py HybridState.excess_total
     long long active = 0;
@@ -2922,6 +3010,39 @@ int bfs_finalize(fm_grid *g) {
 // global relabel + gap + marking; leaves the active-pixel count in g->active and
 // the tiles holding active pixels in the push work list (parity 0)
 int global_relabel(fm_grid *g) {
+    if (g->bfs_bits == 2 && g->nbands == 0) {
+        // default path: fused preparation, one ring launch, finalize, one host sync
+        cudaEventRecord(g->ev[0], g->stream);
+        const bool full = g->relabel_full || g->pr_kernel != 1 || g->pr_ring ||
+                          (g->flags_solve & (FM_GRID_GLOBAL_SWEEP | FM_GRID_CANCEL_VIOLATIONS));
+        relabel_init_kernel<<<std::max(1, std::min((g->ntiles * (PT_H / 4) + 7) / 8, g->sms * 8)), 256, 0, g->stream>>>(
+            g->d, g->rq, full ? 1 : 0, g->acc + 4);
+        FM_CHECK_LAUNCH();
+        cudaEventRecord(g->ev[2], g->stream);
+        ring_kernel<0><<<ring_blocks(g), 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+        FM_CHECK_LAUNCH();
+        cudaEventRecord(g->ev[3], g->stream);
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 8, g->rq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 10, g->rq.ctr + 192, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 11, g->rq.ctr + 224, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+        g->pq_parity = 0;
+        FM_TRY(bfs_finalize(g));   // clears the touched flags
+        FM_CHECK_CUDA(cudaMemcpyAsync(g->h_acc + 4, g->acc + 4, sizeof(unsigned long long) * 3,
+                                      cudaMemcpyDeviceToHost, g->stream));
+        cudaEventRecord(g->ev[1], g->stream);
+        g->st.launches += 2;
+        g->st.bfs_sweeps += 1;
+        g->st.bfs_launches += 1;
+        g->ring_stats_pending = true;
+        FM_TRY(sync_stream(g));
+        bfs_collect(g);
+        g->st.ms_bfs += elapsed(g);
+        g->active = (long long)g->h_acc[4];
+        g->excess_total -= (long long)g->h_acc[5];
+        g->st.bfs_levels = std::max<int64_t>(g->st.bfs_levels, (int64_t)g->h_acc[6]);
+        g->relabel_full = false;
+        return FM_OK;
+    }
     cudaEventRecord(g->ev[0], g->stream);
     FM_TRY(bfs_init(g, false));
     FM_TRY(bfs_sweeps(g, true));
@@ -2995,6 +3116,7 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
                  const int32_t *capU, const int32_t *capS, const int32_t *capT, int32_t flags) {
     g->flags_solve = flags;
     g->local_streak = 0;
+    g->relabel_full = true;   // init + two-hop changed every residual
     memset(&g->st, 0, sizeof(g->st));
     FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 32, g->stream));
@@ -3357,6 +3479,7 @@ int cut_sweeps(fm_grid *g, bool first_all) {
 }
 
 int compute_cut(fm_grid *g, uint8_t *cut_out_dev) {
+    g->relabel_full = true;   // the cut's incoming-arc words overwrite the BFS arc words
     cudaEventRecord(g->ev[0], g->stream);
     FM_TRY(cut_init(g));
     FM_TRY(cut_sweeps(g, true));
