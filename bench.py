@@ -295,10 +295,12 @@ def run_banded(args, ws, rank, local):
     dist.barrier()
     torch.cuda.synchronize()
     agg, dev_ms, t0 = {}, 0.0, time.perf_counter()
+    agg_res2 = 0
     for _ in range(args.steps):
         f, _, st = band.solve(rows_d, above_d, below_d, cut_out=cut_d)
         flows.add(f)
         dev_ms += st["ms_total"]
+        agg_res2 += int(st["reserved"][2])
         for k, v in st.items():
             if isinstance(v, (int, float)):
                 agg[k] = agg.get(k, 0) + v
@@ -356,6 +358,9 @@ def run_banded(args, ws, rank, local):
                            "wall_ms_per_step_max": round(wall_max / args.steps, 3)},
                 "roofline": roof, "cpu_baseline": None, "e2e": e2e,
                 "gpu_launches": int(launches_all), "clocks": clk,
+                "coordinator": {"agreements_per_solve": int(agg_res2 // args.steps),
+                                "what": "shared-memory all-gathers of <= 4 int64 (per push batch and per relabel); "
+                                        "no data-path messages: boundary rows, inboxes and ring queues are peer memory"},
                 "per_solve_rank0": {k: (round(v / args.steps, 3) if isinstance(v, float) else v // args.steps)
                                     for k, v in agg.items() if k in ("pushes", "relabels", "rounds", "launches",
                                                                     "pr_launches", "pr_tiles", "ms_total", "ms_push",

@@ -4407,6 +4407,7 @@ extern "C" int fm_grid_band_solve(fm_grid *g, fm_coll *c, const int32_t *capR, c
     const int32_t *cp = g->band_caps;
     g->flags_solve = flags;
     memset(&g->st, 0, sizeof(g->st));
+    const uint64_t calls0 = c->calls;
     int64_t all[COLL_MAX_RANKS * 4];
     FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 32, g->stream));
@@ -4470,6 +4471,7 @@ extern "C" int fm_grid_band_solve(fm_grid *g, fm_coll *c, const int32_t *capR, c
     }
     cudaEventDestroy(t0);
     cudaEventDestroy(t1);
+    g->st.reserved[2] = (int64_t)(c->calls - calls0);   // host-level agreements (all-gathers) of this solve
     if (stats) *stats = g->st;
     return rc;
 }
@@ -4582,6 +4584,7 @@ extern "C" int fm_group_solve(fm_group *grp, const int32_t *capR, const int32_t 
             s.ms_pr_kern = std::max(s.ms_pr_kern, b.ms_pr_kern); s.ms_bfs_kern = std::max(s.ms_bfs_kern, b.ms_bfs_kern);
             s.reserved[0] += b.reserved[0];
         }
+        s.reserved[2] = sts[0].reserved[2];   // agreements: every band makes the same ones
         *stats = s;
     }
     return FM_OK;
