@@ -21,6 +21,8 @@ TEMPLATE_NAMES = {"ring_kernel<0>": "ring_kernel<bfs>", "ring_kernel<1>": "ring_
 def kname(raw):
     """Kernel name without namespace, return type or parameters; the instances of the
     ring and push kernels keep a tag (ring_kernel<bfs> / <cut>, pr_list_kernel<packed>)."""
+    if raw.strip() == "graph":   # ncu --graph-profiling graph: a push round's while-graph
+        return "pr_list_kernel<packed> x round (while-graph)"
     n = raw.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("(bool)", "")
     for k, v in TEMPLATE_NAMES.items():
         if k in n:
