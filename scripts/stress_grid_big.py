@@ -8,6 +8,9 @@ import paper_1110_6231_b200 as fmb
 
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+# argv[3] = "graph": force the device-side round loop (while-graph, triggers every 2 launches)
+# that grids >= 2^23 px use by default
+opts = {"pr_graph": 1, "pr_batch": 2} if len(sys.argv) > 3 and sys.argv[3] == "graph" else {}
 bad = 0
 t0 = time.time()
 for case in range(n_cases):
@@ -19,7 +22,7 @@ for case in range(n_cases):
     capT = (rng.integers(0, hi + 1, size=(H, W)) * (rng.random((H, W)) < pt)).astype(np.int32)
     caps[0][:, -1] = 0; caps[1][:, 0] = 0; caps[2][-1, :] = 0; caps[3][0, :] = 0
     caps += [capS, capT]
-    solver = fmb.GridSolver(H, W)
+    solver = fmb.GridSolver(H, W, options=opts)
     flow, cut, _ = solver.solve_host(caps)
     state = solver.export()
     solver.close()
