@@ -1660,7 +1660,8 @@ struct RingQ {
     int32_t *slot;          // cap entries, -1 = empty
     int32_t *flag;          // per tile: queued
     unsigned int *ctr;      // [0] head, [32] tail, [64] pending, [96] tile visits that changed a border (one line each)
-                            // [248] timeout flag (band mode: a wait that exceeded the limit)
+                            // [248] timeout flag (band mode: a wait that exceeded the limit), [252] band-local
+                            // done word (row bands: raised by the watcher warp when the shared pending hits 0)
     unsigned int *pend;     // the pending counter the launch ends on: ctr + 64, or (row bands)
                             // one counter shared by every band's ring (on band 0's device)
     int32_t cap;
@@ -1719,6 +1720,7 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
         q.ctr[128] = 0; q.ctr[160] = 0; q.ctr[161] = 0; q.ctr[192] = 0; q.ctr[224] = n0;
         q.ctr[240] = q.ctr[241] = q.ctr[244] = q.ctr[245] = q.ctr[246] = q.ctr[247] = 0;
         q.ctr[248] = 0;
+        q.ctr[252] = 0;   // band-local done word (row bands)
         for (int i = 208; i < 218; i++) q.ctr[i] = 0;
     }
 }
@@ -2049,6 +2051,21 @@ __global__ void __launch_bounds__(32 * BB_WARPS) ring_kernel(GridDev g, RingQ q)
 #endif
     unsigned chg_count = 0;   // visits that changed a border (lane 0; flushed once at the end)
     int base_slot = 0;
+    if (q.sys && blockIdx.x == 0 && wid == 0) {
+        // row bands: the watcher warp of this band polls the shared pending count (on
+        // band 0's device) and raises the band-local done word when it reaches 0
+        if (lane == 0) {
+            const unsigned long long t0 = globaltimer_ns();
+            for (;;) {
+                if (ld_acquire((const int32_t *)q.pend, true) == 0) break;
+                if (globaltimer_ns() - t0 > WAIT_LIMIT_NS) { atomicExch(q.ctr + 248, 1u); break; }
+                __nanosleep(256);
+            }
+            st_release((int32_t *)(q.ctr + 252), 1, false);
+        }
+        __syncwarp();
+        return;
+    }
     for (;;) {
         int tile = -1;
         bool visited = false;
@@ -2062,7 +2079,9 @@ __global__ void __launch_bounds__(32 * BB_WARPS) ring_kernel(GridDev g, RingQ q)
             for (unsigned ns = q.ns0;; ns = min(ns * 2, (unsigned)q.ns1)) {
                 tile = ld_acquire((const int32_t *)vs, q.sys);   // acquire: the producer's stores
                 if (tile >= 0) { *vs = -1; break; }
-                if (*(volatile unsigned *)q.pend == 0) break;
+                // row bands: the shared pending count is remote for most bands; idle warps
+                // poll only the band-local done word the watcher raises
+                if (q.sys ? (*(volatile int32_t *)(q.ctr + 252) != 0) : (*(volatile unsigned *)q.pend == 0)) break;
                 if (q.sys) {
                     const unsigned long long now = globaltimer_ns();
                     if (!t0) t0 = now;
