@@ -236,6 +236,15 @@ int fm_assign_solve_host(fm_assign *a, const int32_t *weights, int64_t alpha,
                          int32_t flags, int64_t *objective_out, int32_t *match_out,
                          int64_t *prices_out, fm_stats *stats);
 
+/* Sparse instances (complete=False) in compressed form: the same cost-scaling solve with
+ * O(n + m) memory and O(degree) work per operation (CSR rows in edge order + a column
+ * index; assign_scaling.py:61-76,470-497).  HOST arcs (xs, ys, ws) in the
+ * instance's edge order, int32 weights, no duplicates; outputs HOST (match_out[x] = y,
+ * prices_out 2n or NULL).  1 = no perfect matching. */
+int fm_assign_sparse_solve(int32_t n, int64_t m, const int32_t *xs, const int32_t *ys, const int32_t *ws,
+                           int64_t alpha, int32_t flags, int32_t device, int64_t *objective_out,
+                           int32_t *match_out, int64_t *prices_out, fm_stats *stats);
+
 /* ------------------------------------------------------------------ DIMACS
  * Ingest of the reference's file formats (dimacs.py:123-248) with the same
  * validation and line-numbered messages (fm_last_error).  Call once with null

@@ -119,6 +119,7 @@ SIGNATURES = {
     "fm_assign_arc_fix": (ctypes.c_int, [_vp, _vp]),
     "fm_assign_export": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "fm_assign_certify": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _i64, _vp, _vp, _vp]),
+    "fm_assign_sparse_solve": (ctypes.c_int, [_i32, _i64, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp]),
 }
 
 _lib = None

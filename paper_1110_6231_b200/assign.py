@@ -86,6 +86,51 @@ class AssignmentInstance:
         return _check_weights(w)
 
 
+# sparse instances run in compressed form (fm_assign_sparse_solve) when the dense n x n
+# matrix would be large or mostly absent: more than 2^24 cells, or under 1/8 of them present
+SPARSE_DENSE_CELLS = 1 << 24
+SPARSE_MAX_DENSITY = 0.125
+
+
+def _use_sparse(inst, layout: str) -> bool:
+    if layout not in ("auto", "dense", "sparse"):
+        raise ValueError(f"layout must be 'auto', 'dense' or 'sparse', got {layout!r}")
+    if not isinstance(inst, AssignmentInstance) or inst.complete:
+        if layout == "sparse" and isinstance(inst, AssignmentInstance):
+            return True
+        return False
+    if layout != "auto":
+        return layout == "sparse"
+    cells = inst.n * inst.n
+    return cells > SPARSE_DENSE_CELLS or len(inst.edges) < SPARSE_MAX_DENSITY * cells
+
+
+def solve_sparse(inst: "AssignmentInstance", alpha: int = DEFAULT_ALPHA, use_price_update: bool = True,
+                 use_arc_fix: bool = True, device: int = 0, want_prices: bool = False):
+    """Sparse instance on the GPU in compressed form (O(n + m) memory).
+    Returns (objective, matching[x] = y, prices (2n) or None, stats)."""
+    L = _lib.load()
+    _lib.require_device()
+    n = inst.n
+    e = np.asarray(inst.edges, dtype=np.int64).reshape(-1, 3)
+    if e.size and (int(e[:, 2].min()) < -(2**31) + 1 or int(e[:, 2].max()) >= 2**31):
+        raise ValueError("weights must fit in int32")
+    xs = np.ascontiguousarray(e[:, 0], dtype=np.int32)
+    ys = np.ascontiguousarray(e[:, 1], dtype=np.int32)
+    ws = np.ascontiguousarray(e[:, 2], dtype=np.int32)
+    obj = ctypes.c_int64()
+    match = np.zeros(n, np.int32)
+    prices = np.zeros(2 * n, np.int64) if want_prices else None
+    st = _lib.FmStats()
+    flags = (_lib.FM_ASSIGN_PRICE_UPDATE if use_price_update else 0) | (_lib.FM_ASSIGN_ARC_FIX if use_arc_fix else 0)
+    p = lambda a: _lib.ptr(a) if a.size else None
+    rc = L.fm_assign_sparse_solve(n, len(xs), p(xs), p(ys), p(ws), int(alpha), flags, int(device),
+                                  ctypes.byref(obj), _lib.ptr(match), _lib.ptr(prices) if want_prices else None,
+                                  ctypes.byref(st))
+    _lib.check(rc, "fm_assign_sparse_solve")
+    return int(obj.value), match, prices, st.as_dict()
+
+
 def _check_weights(w) -> np.ndarray:
     """Square int32 matrix (INT32_MIN = absent arc).  An int32 input is taken as is;
     wider integer inputs are range-checked before the narrowing copy."""
@@ -630,7 +675,7 @@ def solve_assignment(inst, *, mode: str = "seq", worker_count: int = 1,
                      cycle_budget: int = DEFAULT_ASSIGN_CYCLE, alpha: int = DEFAULT_ALPHA,
                      use_price_update: bool = True, use_arc_fix: bool = True,
                      heuristic_every_k: int | None = None, validate: bool = False,
-                     on_refine_end=None, observer=None, device: int | None = None):
+                     on_refine_end=None, observer=None, device: int | None = None, layout: str = "auto"):
     """Maximum-weight perfect matching on the GPU (assign_scaling.py:470-497).
 
     Returns (SolveReport, matching) with matching[x] = y; objective is the matching
@@ -638,7 +683,9 @@ def solve_assignment(inst, *, mode: str = "seq", worker_count: int = 1,
     matching exists.  ``inst`` may also be a dense n x n weight array (numpy, or a
     CUDA tensor that then never leaves the GPU).  Without hooks the whole solve is
     one fused device call; rounds = refines (one coordinator round per refine, as
-    the reference's default cycle budget gives)."""
+    the reference's default cycle budget gives).  layout: a sparse instance
+    (complete=False) runs in compressed form when its dense matrix would be large or
+    mostly absent ("auto"), or as asked ("dense" / "sparse")."""
     if mode not in ("seq", "par"):
         raise ValueError(f"unknown mode {mode!r}")
     if alpha < 2:
@@ -655,6 +702,14 @@ def solve_assignment(inst, *, mode: str = "seq", worker_count: int = 1,
                              on_refine_end=on_refine_end, observer=observer)
     started = time.perf_counter()
     every_k = int(heuristic_every_k) if heuristic_every_k else 0
+    if _use_sparse(inst, layout) and not validate and not every_k:
+        obj, match, _, st = solve_sparse(inst, alpha, use_price_update, use_arc_fix,
+                                         0 if device is None else int(device))
+        st = dict(st)
+        st["layout"] = "sparse"
+        report = SolveReport(objective=obj, pushes=int(st["pushes"]), relabels=int(st["relabels"]),
+                             rounds=int(st["refines"]), elapsed=time.perf_counter() - started, stats=st)
+        return report, match.tolist()
     if hasattr(inst, "is_cuda") and inst.is_cuda:
         import torch
 
