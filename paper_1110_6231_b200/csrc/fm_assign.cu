@@ -94,6 +94,9 @@ struct AssignDev {
     int validate;          // validate=True: device-side invariant checks (codes V_*)
     int32_t *pw;           // validate: last phase tag that wrote each price word (X then Y)
     int32_t vbase;         // validate: tag base of this launch (phase tag = vbase + 2 r + 1|2)
+    int32_t cta_x, cta_y;  // a phase list up to cta_* x the grid runs one CTA-wide op per node
+    int32_t *mw;           // price update: w(x, match[x]) (0 when x holds its unit)
+    int64_t *pmx;          // price update: p(match[x]) (prices are constant during an update)
 };
 
 // validate=True: a price write must lower the price and be the only write of its word
@@ -663,7 +666,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             // per row scan); longer lists get one warp per node
             const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
             unsigned long long t0 = timer ? globaltimer() : 0, t1 = 0;
-            if (ny <= (int)gridDim.x) {
+            if (ny <= a.cta_y * (int)gridDim.x) {
                 for (int i = blockIdx.x; i < ny; i += gridDim.x)
                     y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0], tag_y);
             } else {
@@ -685,7 +688,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC1, t1 - t0); t0 = t1; }
             int nx, u1, u2;
             cta_bcast3(a.cnt + C_X0 + b, nullptr, nullptr, nx, u1, u2);
-            if (nx <= (int)gridDim.x) {
+            if (nx <= a.cta_x * (int)gridDim.x) {
                 for (int i = blockIdx.x; i < nx; i += gridDim.x)
                     x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
             } else {
@@ -730,7 +733,8 @@ __device__ __forceinline__ long long floordiv_eps(long long rc, long long eps, d
 // Bellman-Ford: X step = one CTA per Y whose label dropped, relaxing every arc x->y
 // along row y of the transposed weights (coalesced) with atomicMin on l(x); Y step
 // = one thread per X whose label dropped, relaxing its matched reverse arc.
-constexpr int PU_GROUPS = 4;   // price update: up to this many frontier Y per CTA in flight
+constexpr int PU_GROUPS = 4;   // price update: up to this many frontier Y per CTA in flight (default)
+constexpr int PU_GROUPS_MAX = 8;
 constexpr int PU_RING_EXTRA = 16384;   // ring slots beyond n (>= the price update's groups + 64)
 __device__ __forceinline__ void group_sync(int grp, int nthreads) {   // named barrier of one thread group
     asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(nthreads) : "memory");
@@ -746,6 +750,7 @@ struct PuDev {
     int32_t *ring;
     unsigned int *rctr;
     int ring_cap, ring_on;
+    int ring_groups;        // frontier Y scanned at once per CTA in the queue-driven variant (1, 2, 4, 8)
 };
 
 // One frontier Y of the price update, scanned by a group of GT threads (thread gt):
@@ -767,6 +772,13 @@ __device__ __forceinline__ void pu_scan_y(const AssignDev &a, const PuDev &f, in
         longlong2 pv[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) pv[k] = __ldcg((const longlong2 *)(a.px + x0) + k);
+        // the matched reverse arcs' operands come from per-x arrays filled at the update's
+        // start (w(x, match[x]), p(match[x]), frozen[x]): no dependent loads in stage 3
+        const int4 mw0 = __ldcg((const int4 *)(a.mw + x0)), mw1 = __ldcg((const int4 *)(a.mw + x0 + 4));
+        longlong2 pm[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) pm[k] = __ldcg((const longlong2 *)(a.pmx + x0) + k);
+        const uint2 fz8 = __ldcg((const uint2 *)(a.frozen + x0));
         uint32_t fb = 0;
         if (a.use_fix) fb = (__ldg(a.fixed_t + (size_t)y * a.nw + (x0 >> 5)) >> (x0 & 31)) & 0xffu;
         const int wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
@@ -788,16 +800,11 @@ __device__ __forceinline__ void pu_scan_y(const AssignDev &a, const PuDev &f, in
         }
 #pragma unroll
         for (int k = 0; k < 8; k++) old[k] = cand[k] < LINF ? atomicMin(a.lx + x0 + k, cand[k]) : LINF;
-        int w2[8];
-        long long py2[8];
+        const int w2[8] = {mw0.x, mw0.y, mw0.z, mw0.w, mw1.x, mw1.y, mw1.z, mw1.w};
+        const long long py2[8] = {pm[0].x, pm[0].y, pm[1].x, pm[1].y, pm[2].x, pm[2].y, pm[3].x, pm[3].y};
         uint8_t fz[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const bool go = cand[k] < old[k] && mxv[k] >= 0;
-            w2[k] = go ? __ldg(a.w + (size_t)(x0 + k) * n + mxv[k]) : 0;
-            py2[k] = go ? __ldcg((const long long *)a.py + mxv[k]) : 0;
-            fz[k] = go ? __ldcg(a.frozen + x0 + k) : 1;
-        }
+        for (int k = 0; k < 8; k++) fz[k] = (uint8_t)(((k < 4 ? fz8.x : fz8.y) >> (8 * (k & 3))) & 0xffu);
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             if (!(cand[k] < old[k]) || mxv[k] < 0 || fz[k]) continue;
@@ -852,12 +859,15 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     // final min(label, last + 1) needs.
     long long cap = min((long long)a.max_bucket, (long long)(a.pu_cap0 > 0 ? a.pu_cap0 : 8));
     int it_total = 0;
-    __shared__ int s_ly[PU_GROUPS], s_y[PU_GROUPS];
-    __shared__ long long s_py[PU_GROUPS];
+    __shared__ int s_ly[PU_GROUPS_MAX], s_y[PU_GROUPS_MAX];
+    __shared__ long long s_py[PU_GROUPS_MAX];
     for (;;) {
     if (tid == 0) { a.cnt[C_PU_LAST] = 0; a.cnt[C_PU_CHG] = 0; }
     for (int v = tid; v < n; v += nthr) {
         a.lx[v] = LINF;
+        const int mv = __ldcg(a.match + v);
+        a.mw[v] = mv >= 0 ? __ldg(a.w + (size_t)v * n + mv) : 0;
+        a.pmx[v] = mv >= 0 ? __ldcg((const long long *)a.py + mv) : 0;
         if (__ldcg(a.ey + v) < 0) {
             a.ly[v] = 0;
             f.in_fy[v] = 1;
@@ -886,7 +896,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
         // holds more slots than queued entries (<= n, one per Y) plus waiting groups, an
         // entry is taken with an exchange (one taker) and a slot refilled only when empty
         // (CAS), so no entry is lost, duplicated or overwritten.
-        const int PU_GT = ATHREADS / PU_GROUPS;
+        const int PU_GT = ATHREADS / f.ring_groups;
         const int grp = threadIdx.x / PU_GT, gt = threadIdx.x - grp * PU_GT;
         unsigned long long ys = 0;
         for (;;) {
@@ -1242,6 +1252,8 @@ struct fm_assign {
     int pu_threshold = 0, tail_threshold = 1, pu_every_k = 0;
     // options (fm_assign_set_option; round-1 environment knobs)
     int opt_ybatch_min = 2, opt_pu_ring = 1, opt_pu_threshold = -1, opt_tail_threshold = 1, opt_pu_cap = 256;
+    int opt_cta_x = 4, opt_cta_y = 4;
+    int opt_pu_groups = PU_GROUPS;   // r02an: Y phase 4x grid CTA-wide ops -> n=4096 optical 18.9 -> 15.3 ms
     int32_t flags = 0;
     fm_stats st{};
 };
@@ -1258,6 +1270,8 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     d.validate = (flags & FM_ASSIGN_VALIDATE) ? 1 : 0;
     d.vbase = 0;
     d.ybatch_min = std::max(1, A->opt_ybatch_min);
+    d.cta_x = std::max(1, A->opt_cta_x);
+    d.cta_y = std::max(1, A->opt_cta_y);
     A->alpha = alpha;
     A->flags = flags;
     memset(&A->st, 0, sizeof(A->st));
@@ -1283,8 +1297,9 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
         FM_CHECK_LAUNCH();
         FM_CHECK_CUDA(cudaMemsetAsync(A->pu.cnt, 0, sizeof(int32_t) * 4, s));
         // > queued entries (<= n) + groups waiting on a slot (pu_blocks * PU_GROUPS)
-        A->pu.ring_cap = n + std::min(PU_RING_EXTRA, A->pu_blocks * PU_GROUPS + 64);
+        A->pu.ring_cap = n + std::min(PU_RING_EXTRA, A->pu_blocks * PU_GROUPS_MAX + 64);
         A->pu.ring_on = A->opt_pu_ring ? 1 : 0;
+        A->pu.ring_groups = A->opt_pu_groups;
         if (A->pu.ring_on) {
             FM_CHECK_CUDA(cudaMemsetAsync(A->pu.ring, 0xff, sizeof(int32_t) * ((size_t)n + PU_RING_EXTRA), s));
             FM_CHECK_CUDA(cudaMemsetAsync(A->pu.rctr, 0, sizeof(unsigned int) * 96, s));
@@ -1476,6 +1491,8 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMemset(A->pu.ring, 0xff, sizeof(int32_t) * ((size_t)n + PU_RING_EXTRA)) == cudaSuccess &&
               cudaMemset(A->pu.rctr, 0, sizeof(unsigned int) * 96) == cudaSuccess &&
               cudaMalloc((void **)&d.ly, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&d.mw, sizeof(int32_t) * n) == cudaSuccess &&
+              cudaMalloc((void **)&d.pmx, sizeof(int64_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.pw, sizeof(int32_t) * 2 * (size_t)n) == cudaSuccess &&
               cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * 16) == cudaSuccess &&
               cudaMalloc((void **)&A->acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
@@ -1504,7 +1521,7 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
 extern "C" void fm_assign_destroy(fm_assign *A) {
     if (!A) return;
     cudaSetDevice(A->device);
-    void *dev[] = {A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.fixed_t, A->d.frozen, A->d.frozen_in,
+    void *dev[] = {A->d.mw, A->d.pmx, A->d.px, A->d.py, A->d.match, A->d.ey, A->d.fixed, A->d.fixed_t, A->d.frozen, A->d.frozen_in,
                    A->d.xlist[0], A->d.xlist[1], A->d.ylist[0], A->d.ylist[1], A->d.cnt, A->d.ops,
                    A->d.lx, A->d.ly, A->d.pw, A->d.ybcnt, A->d.ybuf, A->wt, A->pu.fy[0], A->pu.fy[1], A->pu.fx[0], A->pu.fx[1],
                    A->pu.in_fx, A->pu.in_fy, A->pu.cnt, A->pu.ring, A->pu.rctr,
@@ -1818,6 +1835,12 @@ extern "C" int fm_assign_set_option(fm_assign *A, const char *name, int64_t valu
     const int v = (int)std::max<int64_t>(INT32_MIN, std::min<int64_t>(INT32_MAX, value));
     if (!strcmp(name, "heuristic_every_k")) A->pu_every_k = std::max(0, v);
     else if (!strcmp(name, "ybatch_min")) A->opt_ybatch_min = std::max(1, v);
+    else if (!strcmp(name, "cta_x")) A->opt_cta_x = std::max(1, v);
+    else if (!strcmp(name, "pu_groups")) {
+        if (v != 1 && v != 2 && v != 4 && v != 8) { fm_set_error("pu_groups must be 1, 2, 4 or 8"); return FM_INVALID_ARG; }
+        A->opt_pu_groups = v;
+    }
+    else if (!strcmp(name, "cta_y")) A->opt_cta_y = std::max(1, v);
     else if (!strcmp(name, "pu_ring")) A->opt_pu_ring = v;
     else if (!strcmp(name, "pu_threshold")) A->opt_pu_threshold = v;
     else if (!strcmp(name, "tail_threshold")) A->opt_tail_threshold = v;
