@@ -213,6 +213,15 @@ int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const int64_t *ost
                  const int32_t *oarc, const int32_t *head, const int32_t *cap,
                  int32_t cycle_budget, int32_t flags, int64_t *flow_out, uint8_t *cut_out,
                  int32_t *res_out, int64_t *ex_out, fm_stats *stats);
+/* The same with int64 capacities and residuals, for networks whose capacities leave
+ * the int32 range (the reference's capacities are unbounded Python ints, graph.py:87-125):
+ * every capacity in [0, 2^62) and the source's total out-capacity below 2^63, so no
+ * residual or excess can overflow; FM_INVALID_ARG otherwise.  Grid networks too wide for
+ * fm_grid's int32 state are solved through this entry point. */
+int fm_csr_solve64(int32_t n, int32_t s, int32_t t, int64_t m2, const int64_t *ostart,
+                   const int32_t *oarc, const int32_t *head, const int64_t *cap,
+                   int32_t cycle_budget, int32_t flags, int64_t *flow_out, uint8_t *cut_out,
+                   int64_t *res_out, int64_t *ex_out, fm_stats *stats);
 
 /* ------------------------------------------------------------- assignment */
 typedef struct fm_assign fm_assign;
@@ -249,10 +258,11 @@ int fm_assign_sparse_solve(int32_t n, int64_t m, const int32_t *xs, const int32_
  * Ingest of the reference's file formats (dimacs.py:123-248) with the same
  * validation and line-numbered messages (fm_last_error).  Call once with null
  * arrays to get the counts, then with arrays of at least that many entries.
- * max: out_nst = {node_count, source, sink} (0-based), arcs in file order.
+ * max: out_nst = {node_count, source, sink} (0-based), arcs in file order, capacities
+ *      int64 (any non-negative value the file's integers can hold).
  * asn: *out_n = nodes per side, edges (x, y, w) with sides mapped to 0..n-1. */
 int fm_dimacs_parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
-                        int32_t *tails, int32_t *heads, int32_t *caps, int64_t cap_arcs);
+                        int32_t *tails, int32_t *heads, int64_t *caps, int64_t cap_arcs);
 int fm_dimacs_parse_asn(const char *text, int64_t len, int32_t *out_n, int64_t *out_m,
                         int32_t *xs, int32_t *ys, int64_t *ws, int64_t cap_edges);
 

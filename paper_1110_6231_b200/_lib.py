@@ -103,6 +103,7 @@ SIGNATURES = {
     "fm_dimacs_parse_max": (ctypes.c_int, [ctypes.c_char_p, _i64, _vp, _vp, _vp, _vp, _vp, _i64]),
     "fm_dimacs_parse_asn": (ctypes.c_int, [ctypes.c_char_p, _i64, _vp, _vp, _vp, _vp, _vp, _i64]),
     "fm_csr_solve": (ctypes.c_int, [_i32, _i32, _i32, _i64] + [_vp] * 4 + [_i32, _i32] + [_vp] * 5),
+    "fm_csr_solve64": (ctypes.c_int, [_i32, _i32, _i32, _i64] + [_vp] * 4 + [_i32, _i32] + [_vp] * 5),
     "fm_assign_create": (ctypes.c_int, [_i32, _i32, ctypes.POINTER(_vp)]),
     "fm_assign_destroy": (None, [_vp]),
     "fm_assign_solve": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),

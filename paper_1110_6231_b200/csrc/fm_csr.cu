@@ -4,7 +4,8 @@
 // the arc-pair forward star of graph.py:43-84 (arc 2k forward, 2k+1 its reverse,
 // out-arc lists in input order) is uploaded as CSR; one thread owns one node and runs
 // the lockfree_round operation (maxflow_par.py:95-128) with int32 atomics on the
-// residuals and int64 atomics on the excesses; between rounds the coordinator runs a
+// residuals (int64 for capacities past the int32 range, fm_csr_solve64) and int64
+// atomics on the excesses; between rounds the coordinator runs a
 // level-synchronous frontier BFS from t (maxflow_seq.py:119-146) on the device, the
 // gap relabel and the marking (maxflow_par.py:220-226).  The cut is the seeded
 // residual reach.  Grid networks use fm_grid.cu instead.
@@ -16,14 +17,15 @@
 
 namespace {
 
+template <typename R>   // residual type: int32_t, or long long for wide capacities
 struct CsrDev {
     int32_t n, s, t;
     int64_t m2;
     const int64_t *ostart;   // n + 1
     const int32_t *oarc;     // out-arc slot ids, per node in input order
     const int32_t *head;     // head of every arc slot
-    const int32_t *cap;      // capacity of every slot
-    int32_t *res;            // residual of every slot
+    const R *cap;            // capacity of every slot
+    R *res;                  // residual of every slot
     unsigned long long *ex;  // excess (two's complement int64 in an unsigned word)
     int32_t *h;
     int32_t *dist;
@@ -32,12 +34,19 @@ struct CsrDev {
     int32_t *fcount;         // [0..1] frontier sizes, [2] changed/active flag
 };
 
-__device__ __forceinline__ long long ld_ex(const CsrDev &g, int v) {
+__device__ __forceinline__ void res_add(int32_t *p, long long d) { atomicAdd(p, (int32_t)d); }
+__device__ __forceinline__ void res_add(long long *p, long long d) {
+    atomicAdd((unsigned long long *)p, (unsigned long long)d);
+}
+
+template <typename R>
+__device__ __forceinline__ long long ld_ex(const CsrDev<R> &g, int v) {
     return (long long)__ldcg(g.ex + v);
 }
 
 // init_preflow (maxflow_seq.py:47-64): saturate the source's forward, non-loop arcs
-__global__ void csr_init_kernel(CsrDev g) {
+template <typename R>
+__global__ void csr_init_kernel(CsrDev<R> g) {
     for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < g.m2; a += (int64_t)gridDim.x * blockDim.x)
         g.res[a] = g.cap[a];
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
@@ -47,21 +56,23 @@ __global__ void csr_init_kernel(CsrDev g) {
     }
 }
 
-__global__ void csr_preflow_kernel(CsrDev g) {
+template <typename R>
+__global__ void csr_preflow_kernel(CsrDev<R> g) {
     const int64_t b = g.ostart[g.s], e = g.ostart[g.s + 1];
     for (int64_t i = b + blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t a = g.oarc[i];
         if ((a & 1) || g.head[a] == g.s) continue;
-        const int32_t f = g.cap[a];
+        const R f = g.cap[a];
         if (f <= 0) continue;
         g.res[a] -= f;
-        atomicAdd(g.res + (a ^ 1), f);
+        res_add(g.res + (a ^ 1), f);
         atomicAdd(g.ex + g.head[a], (unsigned long long)(long long)f);
     }
 }
 
 // one lock-free pass over the nodes (maxflow_par.py:95-128)
-__global__ void csr_pass_kernel(CsrDev g, int32_t *active_flag, unsigned long long *ops) {
+template <typename R>
+__global__ void csr_pass_kernel(CsrDev<R> g, int32_t *active_flag, unsigned long long *ops) {
     long long pushes = 0, relabels = 0;
     bool act = false;
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.n; x += gridDim.x * blockDim.x) {
@@ -85,8 +96,8 @@ __global__ void csr_pass_kernel(CsrDev g, int32_t *active_flag, unsigned long lo
             const long long r = __ldcg(g.res + best);
             const long long d = e < r ? e : r;
             atomicAdd(g.ex + x, (unsigned long long)(-d));
-            atomicSub(g.res + best, (int32_t)d);
-            atomicAdd(g.res + (best ^ 1), (int32_t)d);
+            res_add(g.res + best, -d);
+            res_add(g.res + (best ^ 1), d);
             atomicAdd(g.ex + g.head[best], (unsigned long long)d);
             pushes++;
         } else {
@@ -100,7 +111,8 @@ __global__ void csr_pass_kernel(CsrDev g, int32_t *active_flag, unsigned long lo
 }
 
 // global relabel: level-synchronous BFS from t over residual arcs y -> x
-__global__ void csr_bfs_init_kernel(CsrDev g) {
+template <typename R>
+__global__ void csr_bfs_init_kernel(CsrDev<R> g) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x)
         g.dist[v] = (v == g.t) ? 0 : -1;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -110,7 +122,8 @@ __global__ void csr_bfs_init_kernel(CsrDev g) {
     }
 }
 
-__global__ void csr_bfs_level_kernel(CsrDev g, int parity, int level) {
+template <typename R>
+__global__ void csr_bfs_level_kernel(CsrDev<R> g, int parity, int level) {
     const int cnt = __ldcg(g.fcount + parity);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
         const int x = g.frontier[parity][i];
@@ -126,7 +139,8 @@ __global__ void csr_bfs_level_kernel(CsrDev g, int parity, int level) {
 }
 
 // gap_relabel + marking; counts active nodes (excess > 0, reached)
-__global__ void csr_finalize_kernel(CsrDev g, unsigned long long *acc /* [0] active [1] marked excess */) {
+template <typename R>
+__global__ void csr_finalize_kernel(CsrDev<R> g, unsigned long long *acc /* [0] active [1] marked excess */) {
     long long active = 0, mex = 0;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
         if (v == g.s) continue;
@@ -146,12 +160,14 @@ __global__ void csr_finalize_kernel(CsrDev g, unsigned long long *acc /* [0] act
 }
 
 // cut: residual reach from {s} U {v != t : e(v) > 0}
-__global__ void csr_cut_init_kernel(CsrDev g) {
+template <typename R>
+__global__ void csr_cut_init_kernel(CsrDev<R> g) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x)
         g.cut[v] = (v == g.s || (v != g.t && (long long)g.ex[v] > 0)) ? 1 : 0;
 }
 
-__global__ void csr_cut_pass_kernel(CsrDev g, int32_t *changed) {
+template <typename R>
+__global__ void csr_cut_pass_kernel(CsrDev<R> g, int32_t *changed) {
     bool ch = false;
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < g.n; x += gridDim.x * blockDim.x) {
         if (!__ldcg(g.cut + x)) continue;
@@ -168,13 +184,15 @@ __global__ void csr_cut_pass_kernel(CsrDev g, int32_t *changed) {
 
 }  // namespace
 
-extern "C" int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const int64_t *ostart,
-                            const int32_t *oarc, const int32_t *head, const int32_t *cap,
-                            int32_t cycle_budget, int32_t flags, int64_t *flow_out,
-                            uint8_t *cut_out, int32_t *res_out, int64_t *ex_out, fm_stats *stats) {
+namespace {
+
+template <typename R>
+int csr_solve(const char *fn, int32_t n, int32_t s, int32_t t, int64_t m2, const int64_t *ostart,
+              const int32_t *oarc, const int32_t *head, const R *cap, int32_t cycle_budget, int32_t flags,
+              int64_t *flow_out, uint8_t *cut_out, R *res_out, int64_t *ex_out, fm_stats *stats) {
     if (n < 2 || s < 0 || s >= n || t < 0 || t >= n || s == t || m2 < 0 || (m2 & 1) || !ostart ||
         (m2 > 0 && (!oarc || !head || !cap)) || cycle_budget < 1 || m2 > (int64_t)INT32_MAX) {
-        fm_set_error("fm_csr_solve: invalid argument");
+        fm_set_error("%s: invalid argument", fn);
         return FM_INVALID_ARG;
     }
     if (fm_device_count() == 0) { fm_set_error("no CUDA device"); return FM_NO_DEVICE; }
@@ -184,11 +202,12 @@ extern "C" int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const i
     cudaEvent_t t0, t1;
     cudaEventCreate(&t0);
     cudaEventCreate(&t1);
-    CsrDev g{};
+    CsrDev<R> g{};
     g.n = n; g.s = s; g.t = t; g.m2 = m2;
     const size_t am = (size_t)std::max<int64_t>(m2, 1);
     int64_t *d_ostart = nullptr;
-    int32_t *d_oarc = nullptr, *d_head = nullptr, *d_cap = nullptr;
+    int32_t *d_oarc = nullptr, *d_head = nullptr;
+    R *d_cap = nullptr;
     unsigned long long *acc = nullptr;
     int32_t *flags_d = nullptr;
     int rc = FM_OK;
@@ -196,8 +215,8 @@ extern "C" int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const i
     FM_CSR_TRY(cudaMalloc((void **)&d_ostart, sizeof(int64_t) * ((size_t)n + 1)));
     FM_CSR_TRY(cudaMalloc((void **)&d_oarc, sizeof(int32_t) * am));
     FM_CSR_TRY(cudaMalloc((void **)&d_head, sizeof(int32_t) * am));
-    FM_CSR_TRY(cudaMalloc((void **)&d_cap, sizeof(int32_t) * am));
-    FM_CSR_TRY(cudaMalloc((void **)&g.res, sizeof(int32_t) * am));
+    FM_CSR_TRY(cudaMalloc((void **)&d_cap, sizeof(R) * am));
+    FM_CSR_TRY(cudaMalloc((void **)&g.res, sizeof(R) * am));
     FM_CSR_TRY(cudaMalloc((void **)&g.ex, sizeof(unsigned long long) * n));
     FM_CSR_TRY(cudaMalloc((void **)&g.h, sizeof(int32_t) * n));
     FM_CSR_TRY(cudaMalloc((void **)&g.dist, sizeof(int32_t) * n));
@@ -214,7 +233,7 @@ extern "C" int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const i
     if (m2 > 0) {
         FM_CSR_TRY(cudaMemcpyAsync(d_oarc, oarc, sizeof(int32_t) * m2, cudaMemcpyHostToDevice, stream));
         FM_CSR_TRY(cudaMemcpyAsync(d_head, head, sizeof(int32_t) * m2, cudaMemcpyHostToDevice, stream));
-        FM_CSR_TRY(cudaMemcpyAsync(d_cap, cap, sizeof(int32_t) * m2, cudaMemcpyHostToDevice, stream));
+        FM_CSR_TRY(cudaMemcpyAsync(d_cap, cap, sizeof(R) * m2, cudaMemcpyHostToDevice, stream));
     }
     g.ostart = d_ostart; g.oarc = d_oarc; g.head = d_head; g.cap = d_cap;
     {
@@ -279,7 +298,7 @@ extern "C" int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const i
         long long et = 0;
         FM_CSR_TRY(cudaMemcpyAsync(&et, g.ex + t, sizeof(long long), cudaMemcpyDeviceToHost, stream));
         if (cut_out) FM_CSR_TRY(cudaMemcpyAsync(cut_out, g.cut, (size_t)n, cudaMemcpyDeviceToHost, stream));
-        if (res_out && m2 > 0) FM_CSR_TRY(cudaMemcpyAsync(res_out, g.res, sizeof(int32_t) * m2, cudaMemcpyDeviceToHost, stream));
+        if (res_out && m2 > 0) FM_CSR_TRY(cudaMemcpyAsync(res_out, g.res, sizeof(R) * m2, cudaMemcpyDeviceToHost, stream));
         if (ex_out) FM_CSR_TRY(cudaMemcpyAsync(ex_out, g.ex, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, stream));
         cudaEventRecord(t1, stream);
         FM_CSR_TRY(cudaStreamSynchronize(stream));
@@ -301,4 +320,42 @@ done:
     cudaStreamDestroy(stream);
     if (stats) *stats = st;
     return rc;
+}
+
+}  // namespace
+
+extern "C" int fm_csr_solve(int32_t n, int32_t s, int32_t t, int64_t m2, const int64_t *ostart,
+                            const int32_t *oarc, const int32_t *head, const int32_t *cap,
+                            int32_t cycle_budget, int32_t flags, int64_t *flow_out,
+                            uint8_t *cut_out, int32_t *res_out, int64_t *ex_out, fm_stats *stats) {
+    return csr_solve<int32_t>("fm_csr_solve", n, s, t, m2, ostart, oarc, head, cap, cycle_budget, flags,
+                              flow_out, cut_out, res_out, ex_out, stats);
+}
+
+extern "C" int fm_csr_solve64(int32_t n, int32_t s, int32_t t, int64_t m2, const int64_t *ostart,
+                              const int32_t *oarc, const int32_t *head, const int64_t *cap,
+                              int32_t cycle_budget, int32_t flags, int64_t *flow_out,
+                              uint8_t *cut_out, int64_t *res_out, int64_t *ex_out, fm_stats *stats) {
+    // int64 residuals; the caller keeps every capacity below 2^62 and the source's total
+    // out-capacity below 2^63 so no residual or excess can leave int64
+    if (m2 > 0 && cap) {
+        long long src = 0;
+        for (int64_t i = 0; i < m2; i++) {
+            if (cap[i] < 0 || cap[i] >= (1ll << 62)) {
+                fm_set_error("fm_csr_solve64: capacity of slot %lld outside [0, 2^62)", (long long)i);
+                return FM_INVALID_ARG;
+            }
+        }
+        if (ostart && s >= 0 && s < n && head && oarc) {
+            for (int64_t i = ostart[s]; i < ostart[s + 1]; i++) {
+                if (i < 0 || i >= m2 || oarc[i] < 0 || oarc[i] >= m2) break;
+                if (__builtin_add_overflow(src, (long long)cap[oarc[i]], &src)) {
+                    fm_set_error("fm_csr_solve64: total capacity out of the source exceeds 2^63-1");
+                    return FM_INVALID_ARG;
+                }
+            }
+        }
+    }
+    return csr_solve<long long>("fm_csr_solve64", n, s, t, m2, ostart, oarc, head, (const long long *)cap,
+                                cycle_budget, flags, flow_out, cut_out, (long long *)res_out, ex_out, stats);
 }

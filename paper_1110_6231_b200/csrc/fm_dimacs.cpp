@@ -92,7 +92,7 @@ int problem_line(Tok *t, int k, long long lineno, const char *expected, bool see
 // (count only) or hold at least *out_m (from a previous call) entries.
 namespace {
 int parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
-              int32_t *tails, int32_t *heads, int32_t *caps, int64_t cap_arcs) {
+              int32_t *tails, int32_t *heads, int64_t *caps, int64_t cap_arcs) {
     if (!text || len < 0 || !out_nst || !out_m) PERR("fm_dimacs_parse_max: invalid argument");
     long long n = -1, declared = 0, source = -1, sink = -1, m = 0;
     const char *p = text, *end = text + len;
@@ -132,8 +132,7 @@ int parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
             if (node_tok(t[1], lineno, n, &a) || node_tok(t[2], lineno, n, &b) || int_tok(t[3], lineno, &c))
                 return FM_INVALID_ARG;
             if (c < 0) PERR("line %lld: negative capacity %lld", lineno, c);
-            if (c > INT32_MAX) PERR("line %lld: capacity %lld exceeds int32", lineno, c);
-            if (tails && m < cap_arcs) { tails[m] = (int32_t)a; heads[m] = (int32_t)b; caps[m] = (int32_t)c; }
+            if (tails && m < cap_arcs) { tails[m] = (int32_t)a; heads[m] = (int32_t)b; caps[m] = c; }
             m++;
         } else {
             PERR("line %lld: unrecognized line type '%s'", lineno, tag.c_str());
@@ -155,7 +154,7 @@ int parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
 }  // namespace
 
 extern "C" int fm_dimacs_parse_max(const char *text, int64_t len, int32_t *out_nst, int64_t *out_m,
-                                   int32_t *tails, int32_t *heads, int32_t *caps, int64_t cap_arcs) {
+                                   int32_t *tails, int32_t *heads, int64_t *caps, int64_t cap_arcs) {
     try {
         return parse_max(text, len, out_nst, out_m, tails, heads, caps, cap_arcs);
     } catch (const std::bad_alloc &) {

@@ -41,7 +41,8 @@ def parse_max_arrays(text):
     if rc:
         raise ParseError(_lib.last_error())
     k = int(m.value)
-    tl, hd, cp = (np.zeros(max(1, k), np.int32) for _ in range(3))
+    tl, hd = (np.zeros(max(1, k), np.int32) for _ in range(2))
+    cp = np.zeros(max(1, k), np.int64)
     rc = L.fm_dimacs_parse_max(b, len(b), nst, ctypes.byref(m), _lib.ptr(tl), _lib.ptr(hd), _lib.ptr(cp), k)
     if rc:
         raise ParseError(_lib.last_error())
@@ -127,9 +128,9 @@ def grid_from_arrays(n, s, t, tails, heads, caps):
         return None
     for k, msk in enumerate((right, left, down, up)):
         np.add.at(planes[k], a[msk], c[msk])
-    if max(int(p.max()) if p.size else 0 for p in planes + [capS, capT]) >= 2 ** 31:
-        return None
-    sh = lambda x: np.ascontiguousarray(x.reshape(H, W), dtype=np.int32)
+    # past int32 the planes stay int64 (hybrid_solve runs them on the int64 kernel)
+    wide = max(int(p.max()) if p.size else 0 for p in planes + [capS, capT]) >= 2 ** 31
+    sh = lambda x: np.ascontiguousarray(x.reshape(H, W), dtype=np.int64 if wide else np.int32)
     return GridNetwork(*[sh(p) for p in planes], sh(capS), sh(capT)), extra
 
 

@@ -162,7 +162,9 @@ class GridNetwork(FlowNetwork):
     Pixel p = r * W + c; source s = H*W, sink t = H*W + 1.
     capR/capL/capD/capU[p] are the capacities of p->p+1, p->p-1, p->p+W, p->p-W;
     capS[p] of s->p and capT[p] of p->t.  Arrays are int32 numpy arrays (host)
-    or int32 CUDA tensors (device; the solve then never leaves the GPU).
+    or int32 CUDA tensors (device; the solve then never leaves the GPU).  Capacities
+    past the int32 range (the reference's are unbounded Python ints) are kept as int64
+    host planes and solved through the int64 generic kernel (fm_csr_solve64).
     """
 
     __slots__ = ("H", "W", "caps", "_materialised")
@@ -188,19 +190,30 @@ class GridNetwork(FlowNetwork):
         return hasattr(self.caps[0], "is_cuda") and bool(self.caps[0].is_cuda)
 
     def host_caps(self):
-        """The six planes as C-contiguous int32 numpy arrays."""
+        """The six planes as C-contiguous int32 numpy arrays (NetworkError if a value
+        does not fit: nothing is wrapped)."""
         out = []
-        for a in self.caps:
-            if hasattr(a, "detach"):
-                a = a.detach().cpu().numpy()
+        for name, a in zip(_PLANES, self.wide_caps()):
+            if a.size and (int(a.max()) >= 2**31 or int(a.min()) < -(2**31)):
+                raise NetworkError(f"{name}: capacity {int(a.max())} does not fit in int32")
             out.append(np.ascontiguousarray(a, dtype=np.int32))
         return tuple(out)
+
+    def wide_caps(self):
+        """The six planes as C-contiguous int64 numpy arrays."""
+        return tuple(_host_plane(name, a) for name, a in zip(_PLANES, self.caps))
+
+    @property
+    def wide(self) -> bool:
+        """True when a capacity leaves the int32 range (host planes only)."""
+        return not self.on_device and any(
+            a.dtype != np.int32 and a.size and int(np.asarray(a).max()) >= 2**31 for a in self.caps)
 
     def arc_arrays(self):
         """(tails, heads, caps) of the reference network in adapter order:
         per pixel, row-major: (s,p,capS) if >0, (p,t,capT) if >0, (p,p+1,capR),
         (p+1,p,capL[p+1]), (p,p+W,capD), (p+W,p,capU[p+W])."""
-        capR, capL, capD, capU, capS, capT = self.host_caps()
+        capR, capL, capD, capU, capS, capT = self.wide_caps()
         H, W = self.H, self.W
         HW = H * W
         p = np.arange(HW, dtype=np.int64)
@@ -228,8 +241,7 @@ class GridNetwork(FlowNetwork):
         q = np.minimum(p + W, HW - 1)
         tl[:, 5], hd[:, 5], cp[:, 5] = p + W, p, capU.reshape(-1)[q]
         k = keep.reshape(-1)
-        return (tl.reshape(-1)[k].astype(np.int32), hd.reshape(-1)[k].astype(np.int32),
-                cp.reshape(-1)[k].astype(np.int32))
+        return tl.reshape(-1)[k].astype(np.int32), hd.reshape(-1)[k].astype(np.int32), cp.reshape(-1)[k]
 
     def materialise(self) -> "GridNetwork":
         """Fill the FlowNetwork arc-pair lists (slow; tests and small grids only)."""
@@ -248,6 +260,24 @@ class GridNetwork(FlowNetwork):
         if not self._materialised:
             self.materialise()
         return len(self.tail)
+
+
+def _host_plane(name, a):
+    """One capacity plane as a C-contiguous int64 numpy array; non-integer input or a
+    value beyond int64 raises NetworkError."""
+    if hasattr(a, "detach"):
+        a = a.detach().cpu().numpy()
+    a = np.asarray(a)
+    if a.dtype == object:
+        try:
+            a = a.astype(np.int64)
+        except (OverflowError, TypeError) as exc:
+            raise NetworkError(f"{name}: capacities must be integers below 2^63 ({exc})") from None
+    if not (np.issubdtype(a.dtype, np.integer) or a.dtype == bool):
+        raise NetworkError(f"{name}: capacities must be integers, got {a.dtype}")
+    if a.dtype == np.uint64 and a.size and int(a.max()) >= 2**63:
+        raise NetworkError(f"{name}: capacity {int(a.max())} does not fit in int64")
+    return np.ascontiguousarray(a, dtype=np.int64)
 
 
 def _device_planes(planes):
@@ -292,10 +322,12 @@ def build_grid_network(capR, capL, capD, capU, capS, capT) -> GridNetwork:
         capR, capL, capD, capU = planes[:4]
         edge = torch.stack([capR[:, -1].any(), capL[:, 0].any(), capD[-1, :].any(), capU[0, :].any()]).cpu().tolist()
     else:
-        planes = net.host_caps()
+        planes = net.wide_caps()
         for name, a in zip(_PLANES, planes):
             if a.size and int(a.min()) < 0:
                 raise NetworkError(f"{name}: negative capacity {int(a.min())}")
+        if not any(a.size and int(a.max()) >= 2**31 for a in planes):
+            planes = tuple(a.astype(np.int32) for a in planes)   # the grid kernel's input form
         capR, capL, capD, capU = planes[:4]
         edge = [capR[:, -1].any(), capL[:, 0].any(), capD[-1, :].any(), capU[0, :].any()]
     if edge[0]:

@@ -249,6 +249,8 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
         if observer is not None:
             raise NotImplementedError("observer hooks are supported on GridNetwork solves")
         return csr_solve(net, cycle_budget)
+    if net.wide:
+        return _wide_grid_solve(net, cycle_budget, observer, cancel_violations, want_cut, device)
     started = time.perf_counter()
     caps = net.caps
     if net.on_device:
@@ -270,8 +272,14 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
                                                   stream=torch.cuda.current_stream(caps[0].device))
                 cut = cut_t.bool() if cut_t is not None else None
             else:
-                flow, cut, stats = solver.solve_host(net.host_caps(), cycle_budget, bfs_interval,
-                                                     want_cut=want_cut, cancel_violations=cancel_violations)
+                try:
+                    flow, cut, stats = solver.solve_host(net.host_caps(), cycle_budget, bfs_interval,
+                                                         want_cut=want_cut, cancel_violations=cancel_violations)
+                except ValueError as exc:
+                    if _INT32_STATE_MSG not in str(exc):
+                        raise
+                    # int32 planes whose per-pixel sums leave the grid kernel's int32 state
+                    return _wide_grid_solve(net, cycle_budget, None, cancel_violations, want_cut, device)
         else:
             solver.begin(net.host_caps(), cancel_violations=cancel_violations)
             while True:
@@ -293,6 +301,25 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
 
 
 _groups = _lib.SolverCache(per_device=1)
+
+# fm_grid's refusal of inputs past its int32 state (fm_grid.cu, grid_init_kernel)
+_INT32_STATE_MSG = "too large for the int32 device state"
+
+
+def _wide_grid_solve(net: GridNetwork, cycle_budget, observer, cancel_violations, want_cut, device) -> SolveReport:
+    """A grid whose capacities (or per-pixel sums) leave int32: the reference's
+    capacities are unbounded ints (graph.py:87-125), so the grid's arc-pair network
+    runs on the int64 generic kernel (fm_csr_solve64); the cut maps back to H x W."""
+    if observer is not None:
+        raise NotImplementedError("observer hooks need int32 grid capacities")
+    if cancel_violations:
+        raise ValueError("cancel_violations needs int32 grid capacities")
+    tl, hd, cp = net.arc_arrays()
+    rep = _csr_run(net.node_count, net.source, net.sink, tl, hd, cp, cycle_budget, False, device or 0)
+    cut = rep.cut[: net.H * net.W].reshape(net.H, net.W) if want_cut else None
+    rep.stats["layout"] = "csr64"
+    return SolveReport(objective=rep.objective, pushes=rep.pushes, relabels=rep.relabels, rounds=rep.rounds,
+                       elapsed=rep.elapsed, cut=cut, stats=rep.stats)
 
 
 def _band_devices(devices) -> list[int]:
@@ -331,38 +358,77 @@ def _banded_solve(net, devs, cycle_budget, observer, cancel_violations, want_cut
 
 def csr_arrays(net: FlowNetwork):
     """(ostart, oarc, head, cap) of a FlowNetwork's arc-pair forward star
-    (graph.py:43-84): out-arc lists keep input order."""
-    n = net.node_count
-    head = np.ascontiguousarray(net.head, dtype=np.int32)
-    cap = np.ascontiguousarray(net.capacity, dtype=np.int32)
-    lens = np.fromiter((len(l) for l in net.out_arcs), dtype=np.int64, count=n)
+    (graph.py:43-84): out-arc lists keep input order; cap is int64."""
+    tails = np.asarray(net.tail, dtype=np.int64)[0::2]
+    heads = np.asarray(net.head, dtype=np.int64)[0::2]
+    try:
+        cap = np.asarray(net.capacity[0::2], dtype=np.int64)
+    except OverflowError:
+        raise ValueError("capacity beyond 2^63 is not supported on the device") from None
+    return _forward_star(net.node_count, tails, heads, cap)
+
+
+def _forward_star(n, tails, heads, cap):
+    """CSR of the arc pairs (tails[k] -> heads[k], cap[k]): slot 2k forward, 2k+1 its
+    reverse (capacity 0); each node's out-slots in slot order (graph.py:64-73)."""
+    m = len(tails)
+    slot_tail = np.empty(2 * m, np.int64)
+    slot_tail[0::2], slot_tail[1::2] = tails, heads
+    head = np.empty(2 * m, np.int32)
+    head[0::2], head[1::2] = heads, tails
+    cap2 = np.zeros(2 * m, np.int64)
+    cap2[0::2] = cap
+    oarc = np.argsort(slot_tail, kind="stable").astype(np.int32)
     ostart = np.zeros(n + 1, np.int64)
-    np.cumsum(lens, out=ostart[1:])
-    oarc = np.fromiter((a for l in net.out_arcs for a in l), dtype=np.int32, count=int(ostart[-1]))
-    return ostart, oarc, head, cap
+    np.cumsum(np.bincount(slot_tail, minlength=n), out=ostart[1:])
+    return ostart, oarc, head, cap2
 
 
 def csr_solve(net: FlowNetwork, cycle_budget: int = DEFAULT_CYCLE_BUDGET, want_state: bool = False):
     """Generic-graph lock-free push-relabel on the GPU (fm_csr.cu).  Returns a
-    SolveReport whose cut is a bool[node_count] (True = source side)."""
-    L = _lib.load()
-    _lib.require_device()
+    SolveReport whose cut is a bool[node_count] (True = source side).  Capacities
+    past int32 run with int64 residuals (fm_csr_solve64)."""
     if net.source is None or net.sink is None:
         raise ValueError("network has no source/sink")
+    tails = np.asarray(net.tail, dtype=np.int64)[0::2]
+    heads = np.asarray(net.head, dtype=np.int64)[0::2]
+    try:
+        cap = np.asarray(net.capacity[0::2], dtype=np.int64)
+    except OverflowError:
+        raise ValueError("capacity beyond 2^63 is not supported on the device") from None
+    return _csr_run(net.node_count, net.source, net.sink, tails, heads, cap, cycle_budget, want_state, 0)
+
+
+def _csr_run(n, source, sink, tails, heads, cap, cycle_budget, want_state, device):
+    L = _lib.load()
+    _lib.require_device()
     started = time.perf_counter()
-    ostart, oarc, head, cap = csr_arrays(net)
-    n, m2 = net.node_count, len(head)
+    ostart, oarc, head, cap2 = _forward_star(n, np.asarray(tails, np.int64), np.asarray(heads, np.int64),
+                                             np.asarray(cap, np.int64))
+    m2 = len(head)
+    wide = bool(m2) and int(cap2.max()) >= 2**31
+    if wide:
+        if int(cap2.max()) >= 2**62:
+            raise ValueError("capacity beyond 2^62 is not supported on the device")
+        if sum(int(c) for c in cap2[oarc[ostart[source]:ostart[source + 1]]]) >= 2**63:
+            raise ValueError("total capacity out of the source beyond 2^63-1 is not supported on the device")
+    else:
+        cap2 = cap2.astype(np.int32)
+    rdt = np.int64 if wide else np.int32
     flow = ctypes.c_int64()
     cut = np.zeros(n, np.uint8)
-    res = np.zeros(max(1, m2), np.int32) if want_state else None
+    res = np.zeros(max(1, m2), rdt) if want_state else None
     ex = np.zeros(n, np.int64) if want_state else None
     st = _lib.FmStats()
     p = lambda a: _lib.ptr(a) if a is not None and a.size else None
-    rc = L.fm_csr_solve(n, int(net.source), int(net.sink), m2, _lib.ptr(ostart), p(oarc), p(head), p(cap),
-                        int(cycle_budget), 0, ctypes.byref(flow), _lib.ptr(cut), p(res), p(ex),
-                        ctypes.byref(st))
-    _lib.check(rc, "fm_csr_solve")
+    fn = L.fm_csr_solve64 if wide else L.fm_csr_solve
+    if device:
+        raise NotImplementedError("the generic (CSR) kernel runs on device 0")
+    rc = fn(n, int(source), int(sink), m2, _lib.ptr(ostart), p(oarc), p(head), p(cap2),
+            int(cycle_budget), 0, ctypes.byref(flow), _lib.ptr(cut), p(res), p(ex), ctypes.byref(st))
+    _lib.check(rc, "fm_csr_solve64" if wide else "fm_csr_solve")
     stats = st.as_dict()
+    stats["residual_bits"] = 64 if wide else 32
     if want_state:
         stats["residual"], stats["excess"] = res[:m2], ex
     return SolveReport(objective=int(flow.value), pushes=int(st.pushes), relabels=int(st.relabels),

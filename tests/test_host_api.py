@@ -113,7 +113,7 @@ def test_assignment_instance_validation():
 def _header_functions():
     text = open(os.path.join(ROOT, "include", "flowmatch_b200.h")).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(fm_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(fm_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_capi_exports_every_header_symbol():
@@ -152,3 +152,48 @@ def test_generators_deterministic():
     assert s[4].min() >= 0 and s[0][:, :-1].min() >= 1
     w = G.assignment_optical_flow(64, 3)
     assert w.shape == (64, 64) and w.dtype == np.int32 and w.max() <= 10000
+
+
+def test_wide_grid_planes_are_kept_not_wrapped():
+    from paper_1110_6231_b200 import generators as G
+
+    caps = [c.astype(np.int64) for c in G.grid_random(8, 6, 1)]
+    net = fmb.build_grid_network(*caps)
+    assert not net.wide and net.caps[0].dtype == np.int32
+    caps[4] = caps[4] * 2**32 + 1
+    net = fmb.build_grid_network(*caps)
+    assert net.wide and net.caps[4].dtype == np.int64
+    with pytest.raises(fmb.NetworkError, match="does not fit in int32"):
+        net.host_caps()
+    tl, hd, cp = net.arc_arrays()
+    assert cp.dtype == np.int64 and int(cp.max()) >= 2**32
+    with pytest.raises(fmb.NetworkError, match="integers"):
+        fmb.build_grid_network(*[c.astype(np.float64) for c in caps])
+    big = [np.array(c.tolist(), dtype=object) for c in caps]
+    big[5][0, 0] = 2**70
+    with pytest.raises(fmb.NetworkError, match="2\\^63"):
+        fmb.build_grid_network(*big)
+
+
+def test_forward_star_matches_materialised_arc_lists():
+    from paper_1110_6231_b200 import generators as G
+    from paper_1110_6231_b200.maxflow import _forward_star, csr_arrays
+
+    net = fmb.build_grid_network(*G.grid_random(5, 7, 2))
+    tl, hd, cp = net.arc_arrays()
+    ostart, oarc, head, cap = _forward_star(net.node_count, tl.astype(np.int64), hd.astype(np.int64), cp)
+    net.materialise()
+    want = [a for l in net.out_arcs for a in l]
+    assert oarc.tolist() == want
+    assert head.tolist() == net.head and cap.tolist() == net.capacity
+    o2, a2, h2, c2 = csr_arrays(net)
+    assert (o2 == ostart).all() and (a2 == oarc).all()
+
+
+def test_dimacs_max_keeps_wide_capacities():
+    from paper_1110_6231_b200 import dimacs
+
+    n, s, t, tl, hd, cp = dimacs.parse_max_arrays("p max 3 2\nn 1 s\nn 3 t\na 1 2 1099511627776\na 2 3 5\n")
+    assert cp.dtype == np.int64 and cp.tolist() == [2**40, 5]
+    net = dimacs.parse_dimacs_max("p max 3 1\nn 1 s\nn 3 t\na 1 3 9223372036854775807\n")
+    assert net.capacity[0] == 2**63 - 1
