@@ -23,6 +23,7 @@
 // exactly -- the stale-price window of the reference's free-running threads
 // (assign_par.py:6-8) cannot open.  Phases run inside one cooperative kernel with
 // grid-wide barriers; the long single-digit tail drops to one CTA with CTA barriers.
+#include <stdio.h>
 #include <cooperative_groups.h>
 #include <algorithm>
 #include <climits>
@@ -57,12 +58,19 @@ constexpr int C_COUNT = 12;
 constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXED = 4,
               O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7, O_TAIL_NS = 8, O_MULTI_NS = 9,
               O_PH_Y = 10, O_PH_SYNC1 = 11, O_PH_X = 12, O_PH_SYNC2 = 13,  // multi-round phase ns (CTA 0)
-              O_PU_YS = 14, O_PU_ITNS = 15;  // price update: frontier Y visits, ns in BF iterations (CTA 0)
+              O_PU_YS = 14, O_PU_ITNS = 15,  // price update: frontier Y visits, ns in BF iterations (CTA 0)
+              O_PU_LASTSUM = 16, O_PU_YFIN = 17, O_PU_YLAB = 18,  // price update: sum of last, Y with l <= last, Y labelled
+              O_PU_SCANNS = 19,                                    // price update: ns in Y scans (summed over groups)
+              O_COUNT = 24;
 
 // validate=True failures (assign_par.py:101-106,200-214; assign_scaling.py:274-275,333-336)
 constexpr int V_RELABEL = 4;             // a relabel failed to lower a price
 constexpr int V_OWNER = 5;               // a price word written by two ops in one phase
 constexpr int V_RAISE = 6;               // the price update would raise a price
+
+// release/acquire fence without the sequentially-consistent one's cost (__threadfence is
+// fence.sc.gpu); used where only release ordering of earlier writes is needed
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -751,6 +759,7 @@ struct PuDev {
     unsigned int *rctr;
     int ring_cap, ring_on;
     int ring_groups;        // frontier Y scanned at once per CTA in the queue-driven variant (1, 2, 4, 8)
+    int local_next;         // queue-driven variant: a group keeps its first re-queued Y (option pu_local)
 };
 
 // One frontier Y of the price update, scanned by a group of GT threads (thread gt):
@@ -768,17 +777,18 @@ __device__ __forceinline__ void pu_scan_y(const AssignDev &a, const PuDev &f, in
     for (int x0 = gt * 8; x0 < nv8; x0 += PU_GT * 8) {
         const int4 w0 = __ldg((const int4 *)(col + x0)), w1 = __ldg((const int4 *)(col + x0 + 4));
         const int4 l0 = __ldcg((const int4 *)(a.lx + x0)), l1 = __ldcg((const int4 *)(a.lx + x0 + 4));
-        const int4 m0 = __ldcg((const int4 *)(a.match + x0)), m1 = __ldcg((const int4 *)(a.match + x0 + 4));
+        // match, prices, frozen flags and the per-x arrays filled at the update's start
+        // (w(x, match[x]), p(match[x])) do not change during the update: L1-cached loads
+        // (every Y scan reads them all), and no dependent loads in stage 3
+        const int4 m0 = __ldca((const int4 *)(a.match + x0)), m1 = __ldca((const int4 *)(a.match + x0 + 4));
         longlong2 pv[4];
 #pragma unroll
-        for (int k = 0; k < 4; k++) pv[k] = __ldcg((const longlong2 *)(a.px + x0) + k);
-        // the matched reverse arcs' operands come from per-x arrays filled at the update's
-        // start (w(x, match[x]), p(match[x]), frozen[x]): no dependent loads in stage 3
-        const int4 mw0 = __ldcg((const int4 *)(a.mw + x0)), mw1 = __ldcg((const int4 *)(a.mw + x0 + 4));
+        for (int k = 0; k < 4; k++) pv[k] = __ldca((const longlong2 *)(a.px + x0) + k);
+        const int4 mw0 = __ldca((const int4 *)(a.mw + x0)), mw1 = __ldca((const int4 *)(a.mw + x0 + 4));
         longlong2 pm[4];
 #pragma unroll
-        for (int k = 0; k < 4; k++) pm[k] = __ldcg((const longlong2 *)(a.pmx + x0) + k);
-        const uint2 fz8 = __ldcg((const uint2 *)(a.frozen + x0));
+        for (int k = 0; k < 4; k++) pm[k] = __ldca((const longlong2 *)(a.pmx + x0) + k);
+        const uint2 fz8 = __ldca((const uint2 *)(a.frozen + x0));
         uint32_t fb = 0;
         if (a.use_fix) fb = (__ldg(a.fixed_t + (size_t)y * a.nw + (x0 >> 5)) >> (x0 & 31)) & 0xffu;
         const int wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
@@ -798,8 +808,14 @@ __device__ __forceinline__ void pu_scan_y(const AssignDev &a, const PuDev &f, in
             const long long c1 = (long long)lyv + len;
             if (c1 <= cap && c1 < lxv[k]) cand[k] = (int)c1;
         }
+        // label drops are fire-and-forget (RED); the matched reverse arc is relaxed from
+        // every candidate below the label read above -- a path length either way, so a
+        // redundant relaxation is harmless and the fixpoint is unchanged
 #pragma unroll
-        for (int k = 0; k < 8; k++) old[k] = cand[k] < LINF ? atomicMin(a.lx + x0 + k, cand[k]) : LINF;
+        for (int k = 0; k < 8; k++) {
+            if (cand[k] < LINF) atomicMin(a.lx + x0 + k, cand[k]);
+            old[k] = lxv[k];
+        }
         const int w2[8] = {mw0.x, mw0.y, mw0.z, mw0.w, mw1.x, mw1.y, mw1.z, mw1.w};
         const long long py2[8] = {pm[0].x, pm[0].y, pm[1].x, pm[1].y, pm[2].x, pm[2].y, pm[3].x, pm[3].y};
         uint8_t fz[8];
@@ -859,7 +875,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     // final min(label, last + 1) needs.
     long long cap = min((long long)a.max_bucket, (long long)(a.pu_cap0 > 0 ? a.pu_cap0 : 8));
     int it_total = 0;
-    __shared__ int s_ly[PU_GROUPS_MAX], s_y[PU_GROUPS_MAX];
+    __shared__ int s_ly[PU_GROUPS_MAX], s_y[PU_GROUPS_MAX], s_next[PU_GROUPS_MAX];
     __shared__ long long s_py[PU_GROUPS_MAX];
     for (;;) {
     if (tid == 0) { a.cnt[C_PU_LAST] = 0; a.cnt[C_PU_CHG] = 0; }
@@ -896,20 +912,28 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
         // holds more slots than queued entries (<= n, one per Y) plus waiting groups, an
         // entry is taken with an exchange (one taker) and a slot refilled only when empty
         // (CAS), so no entry is lost, duplicated or overwritten.
+        // Work-first: the first Y a group's scan re-queues is kept by the group as its
+        // next Y (counted in pending like a ring entry) instead of a ring round trip, so a
+        // chain of label drops runs at scan latency; further drops go to the ring.
         const int PU_GT = ATHREADS / f.ring_groups;
         const int grp = threadIdx.x / PU_GT, gt = threadIdx.x - grp * PU_GT;
-        unsigned long long ys = 0;
+        unsigned long long ys = 0, scan_ns = 0, t_scan = 0;
+        if (gt == 0) s_next[grp] = -1;
         for (;;) {
             if (gt == 0) {
-                int y = -1;
-                const unsigned sl = atomicAdd(f.rctr + 0, 1u) % (unsigned)f.ring_cap;
-                for (unsigned ns = 32;; ns = min(ns * 2, 1024u)) {
-                    if (*(volatile int32_t *)(f.ring + sl) >= 0) {
-                        const int v = atomicExch(f.ring + sl, -1);   // exactly one taker per entry
-                        if (v >= 0) { y = v; break; }
+                if (t_scan) scan_ns += globaltimer() - t_scan;
+                int y = f.local_next ? s_next[grp] : -1;
+                s_next[grp] = -1;
+                if (y < 0) {
+                    const unsigned sl = atomicAdd(f.rctr + 0, 1u) % (unsigned)f.ring_cap;
+                    for (unsigned ns = 32;; ns = min(ns * 2, 1024u)) {
+                        if (*(volatile int32_t *)(f.ring + sl) >= 0) {
+                            const int v = atomicExch(f.ring + sl, -1);   // exactly one taker per entry
+                            if (v >= 0) { y = v; break; }
+                        }
+                        if (*(volatile unsigned *)(f.rctr + 64) == 0) break;
+                        __nanosleep(ns);
                     }
-                    if (*(volatile unsigned *)(f.rctr + 64) == 0) break;
-                    __nanosleep(ns);
                 }
                 s_y[grp] = y;
                 if (y >= 0) {
@@ -918,6 +942,7 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
                     s_ly[grp] = __ldcg(a.ly + y);
                     s_py[grp] = __ldcg((const long long *)a.py + y);
                     ys++;
+                    t_scan = globaltimer();
                 }
             }
             group_sync(grp, PU_GT);
@@ -925,15 +950,16 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
             if (y < 0) break;
             pu_scan_y(a, f, y, s_ly[grp], s_py[grp], cap, inv_eps, gt, PU_GT, [&](int mx) {
                 atomicAdd(f.rctr + 64, 1u);
+                if (f.local_next && atomicCAS(&s_next[grp], -1, mx) == -1) return;   // the group's next Y
                 const unsigned t = atomicAdd(f.rctr + 32, 1u);
-                __threadfence();             // labels (and pending) visible before the entry
+                fence_acq_rel_gpu();         // labels (and pending) visible before the entry
                 int32_t *slot = f.ring + t % (unsigned)f.ring_cap;
                 while (atomicCAS(slot, -1, mx) != -1) __nanosleep(64);
             });
             group_sync(grp, PU_GT);
-            if (gt == 0) { __threadfence(); atomicSub(f.rctr + 64, 1u); }
+            if (gt == 0) { fence_acq_rel_gpu(); atomicSub(f.rctr + 64, 1u); }
         }
-        if (gt == 0 && ys) atomicAdd(a.ops + O_PU_YS, ys);
+        if (gt == 0 && ys) { atomicAdd(a.ops + O_PU_YS, ys); atomicAdd(a.ops + O_PU_SCANNS, scan_ns); }
         grid.sync();
     } else
     for (;; it++) {
@@ -1015,13 +1041,23 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
     grid.sync();
     }  // cap loop
     const long long K = min((long long)__ldcg(a.cnt + C_PU_LAST), (long long)a.max_bucket) + 1;
+    unsigned yfin = 0, ylab = 0;
     for (int v = tid; v < n; v += nthr) {
         const long long dx = min((long long)a.lx[v], K), dy = min((long long)a.ly[v], K);
+        yfin += a.ly[v] < K;
+        ylab += a.ly[v] < LINF;
         if (a.validate && (dx < 0 || dy < 0)) atomicExch(a.cnt + C_INFEASIBLE, V_RAISE);
         a.px[v] -= a.eps * dx;
         a.py[v] -= a.eps * dy;
     }
+    yfin = __reduce_add_sync(0xffffffffu, yfin);
+    ylab = __reduce_add_sync(0xffffffffu, ylab);
+    if (lane == 0 && ylab) {
+        atomicAdd(a.ops + O_PU_YFIN, (unsigned long long)yfin);
+        atomicAdd(a.ops + O_PU_YLAB, (unsigned long long)ylab);
+    }
     if (tid == 0) {
+        atomicAdd(a.ops + O_PU_LASTSUM, (unsigned long long)(K - 1));
         a.cnt[C_RELABELS] = 0;
         f.cnt[0] = f.cnt[1] = f.cnt[2] = f.cnt[3] = 0;
         f.rctr[0] = f.rctr[32] = f.rctr[64] = 0;
@@ -1253,6 +1289,8 @@ struct fm_assign {
     // options (fm_assign_set_option; round-1 environment knobs)
     int opt_ybatch_min = 2, opt_pu_ring = 1, opt_pu_threshold = -1, opt_tail_threshold = 1, opt_pu_cap = 256;
     int opt_cta_x = 4, opt_cta_y = 4;
+    int opt_trace = 0;               // price-update statistics line on stderr after each solve
+    int opt_pu_local = 0;            // price update: work-first continuation of a group's first re-queued Y
     int opt_pu_groups = PU_GROUPS;   // r02an: Y phase 4x grid CTA-wide ops -> n=4096 optical 18.9 -> 15.3 ms
     int32_t flags = 0;
     fm_stats st{};
@@ -1285,7 +1323,7 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     FM_CHECK_CUDA(cudaMemsetAsync(d.ybcnt, 0, sizeof(int32_t) * n, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.fixed, 0, sizeof(uint32_t) * (size_t)n * d.nw, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.fixed_t, 0, sizeof(uint32_t) * (size_t)n * d.nw, s));
-    FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * 16, s));
+    FM_CHECK_CUDA(cudaMemsetAsync(d.ops, 0, sizeof(unsigned long long) * O_COUNT, s));
     FM_CHECK_CUDA(cudaMemsetAsync(A->acc, 0, sizeof(unsigned long long) * 4, s));
     FM_CHECK_CUDA(cudaMemsetAsync(d.pw, 0, sizeof(int32_t) * 2 * (size_t)n, s));
     weight_bound_kernel<<<A->sms * 4, 256, 0, s>>>(w, (int64_t)n * n, A->acc);
@@ -1300,6 +1338,7 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
         A->pu.ring_cap = n + std::min(PU_RING_EXTRA, A->pu_blocks * PU_GROUPS_MAX + 64);
         A->pu.ring_on = A->opt_pu_ring ? 1 : 0;
         A->pu.ring_groups = A->opt_pu_groups;
+        A->pu.local_next = A->opt_pu_local ? 1 : 0;
         if (A->pu.ring_on) {
             FM_CHECK_CUDA(cudaMemsetAsync(A->pu.ring, 0xff, sizeof(int32_t) * ((size_t)n + PU_RING_EXTRA), s));
             FM_CHECK_CUDA(cudaMemsetAsync(A->pu.rctr, 0, sizeof(unsigned int) * 96, s));
@@ -1401,7 +1440,7 @@ int assign_finish(fm_assign *A, int rc, int64_t *objective_out, int32_t *match_o
         A->st.launches++;
     }
     cudaEventRecord(A->ev[3], s);
-    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_ops, d.ops, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost, s));
+    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_ops, d.ops, sizeof(unsigned long long) * O_COUNT, cudaMemcpyDeviceToHost, s));
     FM_CHECK_CUDA(cudaMemcpyAsync(A->h_acc, A->acc, sizeof(unsigned long long) * 4, cudaMemcpyDeviceToHost, s));
     if (match_out) FM_CHECK_CUDA(cudaMemcpyAsync(match_out, d.match, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
     if (prices_out) {
@@ -1422,6 +1461,13 @@ int assign_finish(fm_assign *A, int rc, int64_t *objective_out, int32_t *match_o
     A->st.reserved[2] = (int64_t)A->h_ops[O_PU_ITERS];   // Bellman-Ford iterations in them
     A->st.cut_sweeps = (int64_t)A->h_ops[O_PU_YS];       // price update: frontier Y visits
     A->st.pr_tiles = (int64_t)A->h_ops[O_PU_ITNS];       // price update: ns inside Bellman-Ford iterations (CTA 0)
+    if (A->opt_trace && A->h_ops[O_PU]) {
+        const double npu = (double)A->h_ops[O_PU];
+        fprintf(stderr, "[fm_assign] %llu price updates: per update %.0f Y visits, %.1f us, last %.2f, "
+                "Y labelled <= last %.0f, Y labelled %.0f, %.2f us per scan\n", A->h_ops[O_PU], A->h_ops[O_PU_YS] / npu,
+                1e-3 * A->h_ops[O_PU_ITNS] / npu, A->h_ops[O_PU_LASTSUM] / npu, A->h_ops[O_PU_YFIN] / npu,
+                A->h_ops[O_PU_YLAB] / npu, 1e-3 * A->h_ops[O_PU_SCANNS] / std::max(1.0, (double)A->h_ops[O_PU_YS]));
+    }
     A->st.reserved[3] = (int64_t)A->h_ops[O_TAIL_OPS];   // ops done by the single-CTA tail
     A->st.ms_cut = 1e-6 * (double)A->h_ops[O_TAIL_NS];   // time in single-CTA tail rounds
     A->st.ms_d2h = 1e-6 * (double)A->h_ops[O_MULTI_NS];  // time in grid-wide rounds
@@ -1494,9 +1540,9 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
               cudaMalloc((void **)&d.mw, sizeof(int32_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.pmx, sizeof(int64_t) * n) == cudaSuccess &&
               cudaMalloc((void **)&d.pw, sizeof(int32_t) * 2 * (size_t)n) == cudaSuccess &&
-              cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * 16) == cudaSuccess &&
+              cudaMalloc((void **)&d.ops, sizeof(unsigned long long) * O_COUNT) == cudaSuccess &&
               cudaMalloc((void **)&A->acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
-              cudaMallocHost((void **)&A->h_ops, sizeof(unsigned long long) * 16) == cudaSuccess &&
+              cudaMallocHost((void **)&A->h_ops, sizeof(unsigned long long) * O_COUNT) == cudaSuccess &&
               cudaMallocHost((void **)&A->h_acc, sizeof(unsigned long long) * 4) == cudaSuccess &&
               cudaMallocHost((void **)&A->h_cnt, sizeof(int32_t) * C_COUNT) == cudaSuccess &&
               cudaStreamCreateWithFlags(&A->own_stream, cudaStreamNonBlocking) == cudaSuccess;
@@ -1625,7 +1671,7 @@ int assign_sync_cnt(fm_assign *A) {
 }
 
 int assign_ops(fm_assign *A, unsigned long long *out16) {
-    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_ops, A->d.ops, sizeof(unsigned long long) * 16, cudaMemcpyDeviceToHost,
+    FM_CHECK_CUDA(cudaMemcpyAsync(A->h_ops, A->d.ops, sizeof(unsigned long long) * O_COUNT, cudaMemcpyDeviceToHost,
                                   A->stream));
     FM_CHECK_CUDA(cudaStreamSynchronize(A->stream));
     memcpy(out16, A->h_ops, sizeof(unsigned long long) * 16);
@@ -1842,6 +1888,8 @@ extern "C" int fm_assign_set_option(fm_assign *A, const char *name, int64_t valu
     }
     else if (!strcmp(name, "cta_y")) A->opt_cta_y = std::max(1, v);
     else if (!strcmp(name, "pu_ring")) A->opt_pu_ring = v;
+    else if (!strcmp(name, "pu_local")) A->opt_pu_local = v;
+    else if (!strcmp(name, "trace")) A->opt_trace = v;
     else if (!strcmp(name, "pu_threshold")) A->opt_pu_threshold = v;
     else if (!strcmp(name, "tail_threshold")) A->opt_tail_threshold = v;
     else if (!strcmp(name, "pu_cap")) A->opt_pu_cap = v;

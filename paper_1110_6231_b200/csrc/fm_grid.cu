@@ -2761,6 +2761,8 @@ struct fm_grid {
     int pr_ring = 0;                     // 1: one persistent pr_ring_kernel launch per round (option PR_RING; experimental, slower)
     int two_hop = 1;                     // two-hop pre-routing after init (option TWO_HOP)
     int k_tail = 0;                      // passes per visit in tail rounds (0: k_local) (option K_TAIL)
+    int ring_tail = -1;                  // rounds with active <= H*W / ring_tail run as one ring launch (option
+                                         // ring_tail; -1 auto: 1024 up to 2^24 px, r02bc: 4096^2 -2%, 8192^2 +1.5%)
     int tail_div = 1024;                 // tail round: active pixels <= H*W / tail_div (option TAIL_DIV)
     int pr_batch = 0;                    // push launches between checks of the round triggers (option PR_BATCH; 0 = auto)
     int visit_mult = 16;                 // ring round visit cap = visit_mult x initially active tiles (option VISIT_MULT)
@@ -2812,21 +2814,6 @@ struct fm_grid {
 };
 
 namespace {
-
-// host copy into freshly allocated (not yet faulted-in) memory: first-touch page
-// faults dominate, and they proceed in parallel across threads
-void parallel_memcpy(void *dst, const void *src, size_t n) {
-    const size_t chunk = (size_t)2 << 20;
-    const int nt = (int)std::min<size_t>(8, (n + chunk - 1) / chunk);
-    if (nt <= 1) { memcpy(dst, src, n); return; }
-    std::vector<std::thread> th;
-    const size_t per = (n + nt - 1) / nt;
-    for (int i = 0; i < nt; i++) {
-        const size_t a = (size_t)i * per, b = std::min(n, a + per);
-        if (a < b) th.emplace_back([=] { memcpy((char *)dst + a, (const char *)src + a, b - a); });
-    }
-    for (auto &t : th) t.join();
-}
 
 int sync_stream(fm_grid *g) {
     FM_CHECK_CUDA(cudaStreamSynchronize(g->stream));
@@ -3410,10 +3397,14 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     cudaEventRecord(g->ev[4], g->stream);
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
     int32_t sweeps = 0;
+    // tail rounds (few active pixels, flow crossing many tiles) as one persistent launch
+    const int ring_tail = g->ring_tail >= 0 ? g->ring_tail : (g->HW <= ((int64_t)1 << 24) ? 1024 : 0);
     if (g->flags_solve & FM_GRID_GLOBAL_SWEEP) {
         FM_TRY(run_round_global(g, cycle_budget, bfs_interval, &sweeps));
-    } else if (g->pr_ring && g->pr_kernel == 1 && bfs_interval <= 0 && g->bfs_interval_env <= 0) {
+    } else if (g->pr_kernel == 1 && bfs_interval <= 0 && g->bfs_interval_env <= 0 &&
+               (g->pr_ring || (ring_tail > 0 && g->active <= g->HW / ring_tail))) {
         FM_TRY(run_round_ring(g, cycle_budget));
+        g->relabel_full = true;   // the next relabel prepares every tile (as with pr_ring)
     } else {
         FM_TRY(run_round_tiles(g, cycle_budget, bfs_interval));
     }
@@ -3936,6 +3927,7 @@ extern "C" int fm_grid_set_option(fm_grid *g, const char *name, int64_t value) {
     else if (k == "k_solo") g->d.k_solo = v;
     else if (k == "solo_max") g->d.solo_max = v;
     else if (k == "k_tail") g->k_tail = v;
+    else if (k == "ring_tail") g->ring_tail = std::max(-1, v);
     else if (k == "two_hop") g->two_hop = v;
     else if (k == "tail_div") g->tail_div = v;
     else if (k == "pr_batch") g->pr_batch = std::max(0, std::min(16, v));

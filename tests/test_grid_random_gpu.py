@@ -108,8 +108,8 @@ def test_sparse_sink_grids(seed):
 def test_int32_capacity_limits():
     """The device state is int32: capacities whose sums could overflow it (excess of a
     pixel = capS + the capacities into it; a merged pair's residual = its two
-    capacities) are refused with ValueError instead of being wrapped silently; below the
-    limit the answer is exact."""
+    capacities) are refused by the grid kernel with ValueError instead of being wrapped
+    silently (hybrid_solve then runs the int64 kernel); below the limit the answer is exact."""
     rng = np.random.default_rng(5)
     H, W = 60, 70
 
@@ -125,8 +125,19 @@ def test_int32_capacity_limits():
     want = oracle.grid_maxflow(*ok, solver="seq")
     rep = fmb.hybrid_solve(fmb.build_grid_network(*ok))
     assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
-    with pytest.raises(ValueError):
-        fmb.hybrid_solve(fmb.build_grid_network(*caps_upto(2**31 - 1)))
+    big = caps_upto(2**31 - 1)
+    solver = fmb.GridSolver(H, W)
+    try:
+        with pytest.raises(ValueError, match="int32 device state"):
+            solver.solve_host(big)
+    finally:
+        solver.close()
+    # hybrid_solve moves such grids to the int64 generic kernel (tests/test_wide_caps_gpu.py)
+    from paper_1110_6231_b200.cli import _cut_capacity
+
+    net = fmb.build_grid_network(*big)
+    rep = fmb.hybrid_solve(net)
+    assert rep.stats["layout"] == "csr64" and _cut_capacity(net, rep.cut) == rep.objective
 
 
 @pytest.mark.parametrize("hi", [32767, 32768, 65535])

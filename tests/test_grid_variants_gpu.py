@@ -42,6 +42,8 @@ VARIANTS = {
     "pr_graph_b2": {"pr_graph": 1, "pr_batch": 2},
     "no_tma": {"tma": 0},
     "unpacked_no_tma": {"packed": 0, "tma": 0},
+    "no_ring_tail": {"ring_tail": 0},
+    "ring_tail_every_round": {"ring_tail": 1},
 }
 
 CASES = [("G", 96, 160, 11), ("G", 257, 130, 12), ("S", 200, 256, 2048), ("G", 31, 33, 13)]
