@@ -178,12 +178,14 @@ class GridNetwork(FlowNetwork):
         for name, a in zip(_PLANES, caps):
             if tuple(a.shape) != shape:
                 raise NetworkError(f"{name} has shape {tuple(a.shape)}, expected {shape}")
-        FlowNetwork.__init__(self, H * W + 2, H * W, H * W + 1)
+        # FlowNetwork's fields without its per-node list allocation (H*W + 2 empty lists
+        # would take seconds): the adjacency lists are built on demand by materialise()
+        self.node_count, self.source, self.sink = H * W + 2, H * W, H * W + 1
+        self.tail, self.head, self.capacity, self.cost = [], [], [], []
+        self.out_arcs = None
         self.H, self.W = H, W
         self.caps = caps
         self._materialised = False
-        # the adjacency lists are built on demand; out_arcs stays a placeholder
-        self.out_arcs = None
 
     @property
     def on_device(self) -> bool:
@@ -193,10 +195,14 @@ class GridNetwork(FlowNetwork):
         """The six planes as C-contiguous int32 numpy arrays (NetworkError if a value
         does not fit: nothing is wrapped)."""
         out = []
-        for name, a in zip(_PLANES, self.wide_caps()):
+        for name, a in zip(_PLANES, self.caps):
+            if isinstance(a, np.ndarray) and a.dtype == np.int32:
+                out.append(np.ascontiguousarray(a))    # the common case: no copy, no scan
+                continue
+            a = _host_plane(name, a)
             if a.size and (int(a.max()) >= 2**31 or int(a.min()) < -(2**31)):
                 raise NetworkError(f"{name}: capacity {int(a.max())} does not fit in int32")
-            out.append(np.ascontiguousarray(a, dtype=np.int32))
+            out.append(a.astype(np.int32))
         return tuple(out)
 
     def wide_caps(self):
@@ -322,12 +328,15 @@ def build_grid_network(capR, capL, capD, capU, capS, capT) -> GridNetwork:
         capR, capL, capD, capU = planes[:4]
         edge = torch.stack([capR[:, -1].any(), capL[:, 0].any(), capD[-1, :].any(), capU[0, :].any()]).cpu().tolist()
     else:
-        planes = net.wide_caps()
+        # int32 planes are kept as given (no copy: pinned caller buffers stay pinned);
+        # wider ones are range-checked and stay int64 only when a value needs it
+        planes = tuple(a if isinstance(a, np.ndarray) and a.dtype == np.int32 else _host_plane(name, a)
+                       for name, a in zip(_PLANES, net.caps))
         for name, a in zip(_PLANES, planes):
             if a.size and int(a.min()) < 0:
                 raise NetworkError(f"{name}: negative capacity {int(a.min())}")
-        if not any(a.size and int(a.max()) >= 2**31 for a in planes):
-            planes = tuple(a.astype(np.int32) for a in planes)   # the grid kernel's input form
+        if not any(a.dtype != np.int32 and a.size and int(a.max()) >= 2**31 for a in planes):
+            planes = tuple(a if a.dtype == np.int32 else a.astype(np.int32) for a in planes)
         capR, capL, capD, capU = planes[:4]
         edge = [capR[:, -1].any(), capL[:, 0].any(), capD[-1, :].any(), capU[0, :].any()]
     if edge[0]:
