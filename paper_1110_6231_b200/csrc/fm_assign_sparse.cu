@@ -11,15 +11,21 @@
 // the CSR arc of each column entry).  X flow is one matched arc per x (mat[x], -1 = x
 // holds its unit); y excess = (#matched into y) - 1.  Phases as the dense path: an X
 // phase reads only Y prices, a Y phase only prices of X matched into it, so every op
-// sees exact prices and epsilon-optimality is kept exactly.  Host-driven phases: one
-// launch per phase (sparse instances are the large-n, low-degree case the dense
+// sees exact prices and epsilon-optimality is kept exactly.  The rounds of a refine run
+// inside one cooperative kernel (grid barriers between phases; once the Y list is short
+// CTA 0 finishes alone with CTA barriers), and a price update is one cooperative kernel
+// too (a grid barrier per Bellman-Ford wave): the host syncs once per refine and once
+// per price update (sparse instances are the large-n, low-degree case the dense
 // kernels' n-wide row scans do not fit).
+#include <cooperative_groups.h>
 #include <algorithm>
 #include <climits>
 #include <vector>
 #include <string.h>
 
 #include "fm_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -39,9 +45,11 @@ struct SpDev {
     uint8_t *frozen;                  // x's matched arc is fixed
     int32_t *frozen_in;               // frozen matches into y
     int32_t *lx, *ly, *infy;          // price update labels / frontier flag
-    int32_t *list[4];                 // X lists [0,1], Y lists [2,3]; frontiers reuse them
+    int32_t *list[4];                 // X lists [0,1], Y lists [2,3] (round parity); frontiers reuse 2, 3
     int32_t *cnt;                     // [0..3] list counts, [4] infeasible, [5] relabels since PU,
-                                      // [6] price update: changed, [7] last label
+                                      // [6] price update: changed, [7] last label, [8] round index,
+                                      // [9] rounds kernel exit (0 done, 1 price update due), [12..14]
+                                      // price-update frontier counts (rotating)
     unsigned long long *ops;          // [0] pushes [1] relabels [2] rounds [3] fixed [4] PU [5] PU waves
     int64_t scale, eps, max_bucket;
 };
@@ -113,113 +121,180 @@ __global__ void sp_begin_kernel(SpDev s) {
     if (lane == 0 && pushes) atomicAdd(s.ops + 0, pushes);
 }
 
-// Y phase: every y holding excess pushes its units back to the cheapest incoming
-// matched, unfrozen x (reverse arc cost +w scale - p(x); (v, x) order), relabelling y
-// whenever the next one is not admissible (assign_par.py:45-112).  Warp per y.
-__global__ void sp_y_kernel(SpDev s, const int32_t *yl, int ny, int32_t *xl_next, int32_t *xcnt_next) {
-    __shared__ long long s_v[8][SP_YCAP];
-    __shared__ int s_x[8][SP_YCAP];
-    __shared__ int s_n[8];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    unsigned long long pushes = 0, relabels = 0;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < ny; i += (gridDim.x * blockDim.x) >> 5) {
-        const int y = yl[i];
-        int ey = s.ey[y];
-        long long py = s.py[y];
-        if (ey <= 0) continue;
-        if (lane == 0) s_n[wid] = 0;
-        __syncwarp();
-        // gather: the column of y, arcs carrying a matched, unfrozen x's unit
-        for (int64_t k = s.cp[y] + lane; k < s.cp[y + 1]; k += 32) {
-            const int a = s.ca[k], x = s.cx[k];
-            if (__ldcg(s.mat + x) != a || s.frozen[x]) continue;
-            const int j = atomicAdd(&s_n[wid], 1);
-            if (j < SP_YCAP) { s_x[wid][j] = x; s_v[wid][j] = (long long)s.w[a] * s.scale - __ldcg((const long long *)s.px + x); }
-        }
-        __syncwarp();
-        const int cnt = s_n[wid];
-        if (cnt > SP_YCAP) {
-            // overflow: one column scan per unit
-            while (ey > 0) {
-                long long bv = SP_I64_MAX;
-                int bx = INT32_MAX;
-                for (int64_t k = s.cp[y] + lane; k < s.cp[y + 1]; k += 32) {
-                    const int a = s.ca[k], x = s.cx[k];
-                    if (__ldcg(s.mat + x) != a || s.frozen[x]) continue;
-                    const long long v = (long long)s.w[a] * s.scale - __ldcg((const long long *)s.px + x);
-                    if (v < bv || (v == bv && x < bx)) { bv = v; bx = x; }
-                }
-                sp_argmin(bv, bx);
-                if (bx == INT32_MAX) { if (lane == 0) atomicExch(s.cnt + 4, 2); break; }
-                if (lane == 0) {
-                    if (!(bv < -py)) { py = -(bv + s.eps); relabels++; atomicAdd(s.cnt + 5, 1); }
-                    s.mat[bx] = -1;
-                    xl_next[atomicAdd(xcnt_next, 1)] = bx;
-                    pushes++;
-                }
-                __syncwarp();
-                ey--;
-            }
-        } else {
-            while (ey > 0) {
-                long long bv = SP_I64_MAX;
-                int bx = INT32_MAX, bk = -1;
-                for (int k = lane; k < cnt; k += 32) {
-                    const long long v = s_v[wid][k];
-                    const int x = s_x[wid][k];
-                    if (v < bv || (v == bv && x < bx)) { bv = v; bx = x; bk = k; }
-                }
-                long long v2 = bv;
-                int x2 = bx;
-                sp_argmin(v2, x2);
-                if (x2 == INT32_MAX) { if (lane == 0) atomicExch(s.cnt + 4, 2); break; }
-                if (bx == x2 && bk >= 0) s_v[wid][bk] = SP_I64_MAX;   // the owner lane retires the slot
-                if (lane == 0) {
-                    if (!(v2 < -py)) { py = -(v2 + s.eps); relabels++; atomicAdd(s.cnt + 5, 1); }
-                    s.mat[x2] = -1;
-                    xl_next[atomicAdd(xcnt_next, 1)] = x2;
-                    pushes++;
-                }
-                __syncwarp();
-                ey--;
-            }
-        }
-        if (lane == 0) { s.py[y] = py; s.ey[y] = ey; }
-        __syncwarp();
+// Y op: y holding excess pushes its units back to the cheapest incoming matched,
+// unfrozen x (reverse arc cost +w scale - p(x); (v, x) order), relabelling y whenever
+// the next one is not admissible (assign_par.py:45-112).  One warp; sv / sx / sn are the
+// warp's shared candidate buffer.
+__device__ __forceinline__ void sp_y_op(const SpDev &s, int y, int32_t *xl_next, int32_t *xcnt_next, long long *sv,
+                                        int *sx, int *sn, unsigned long long &pushes, unsigned long long &relabels) {
+    const int lane = threadIdx.x & 31;
+    int ey = __ldcg(s.ey + y);
+    long long py = __ldcg((const long long *)s.py + y);
+    if (ey <= 0) return;
+    if (lane == 0) *sn = 0;
+    __syncwarp();
+    // gather: the column of y, arcs carrying a matched, unfrozen x's unit
+    for (int64_t k = s.cp[y] + lane; k < s.cp[y + 1]; k += 32) {
+        const int a = s.ca[k], x = s.cx[k];
+        if (__ldcg(s.mat + x) != a || s.frozen[x]) continue;
+        const int j = atomicAdd(sn, 1);
+        if (j < SP_YCAP) { sx[j] = x; sv[j] = (long long)s.w[a] * s.scale - __ldcg((const long long *)s.px + x); }
     }
-    if (lane == 0) {
-        if (pushes) atomicAdd(s.ops + 0, pushes);
-        if (relabels) atomicAdd(s.ops + 1, relabels);
+    __syncwarp();
+    const int cnt = *(volatile int *)sn;
+    if (cnt > SP_YCAP) {
+        // overflow: one column scan per unit
+        while (ey > 0) {
+            long long bv = SP_I64_MAX;
+            int bx = INT32_MAX;
+            for (int64_t k = s.cp[y] + lane; k < s.cp[y + 1]; k += 32) {
+                const int a = s.ca[k], x = s.cx[k];
+                if (__ldcg(s.mat + x) != a || s.frozen[x]) continue;
+                const long long v = (long long)s.w[a] * s.scale - __ldcg((const long long *)s.px + x);
+                if (v < bv || (v == bv && x < bx)) { bv = v; bx = x; }
+            }
+            sp_argmin(bv, bx);
+            if (bx == INT32_MAX) { if (lane == 0) atomicExch(s.cnt + 4, 2); break; }
+            if (lane == 0) {
+                if (!(bv < -py)) { py = -(bv + s.eps); relabels++; atomicAdd(s.cnt + 5, 1); }
+                s.mat[bx] = -1;
+                xl_next[atomicAdd(xcnt_next, 1)] = bx;
+                pushes++;
+            }
+            __syncwarp();
+            ey--;
+        }
+    } else {
+        while (ey > 0) {
+            long long bv = SP_I64_MAX;
+            int bx = INT32_MAX, bk = -1;
+            for (int k = lane; k < cnt; k += 32) {
+                const long long v = sv[k];
+                const int x = sx[k];
+                if (v < bv || (v == bv && x < bx)) { bv = v; bx = x; bk = k; }
+            }
+            long long v2 = bv;
+            int x2 = bx;
+            sp_argmin(v2, x2);
+            if (x2 == INT32_MAX) { if (lane == 0) atomicExch(s.cnt + 4, 2); break; }
+            if (bx == x2 && bk >= 0) sv[bk] = SP_I64_MAX;   // the owner lane retires the slot
+            if (lane == 0) {
+                if (!(v2 < -py)) { py = -(v2 + s.eps); relabels++; atomicAdd(s.cnt + 5, 1); }
+                s.mat[x2] = -1;
+                xl_next[atomicAdd(xcnt_next, 1)] = x2;
+                pushes++;
+            }
+            __syncwarp();
+            ey--;
+        }
     }
+    if (lane == 0) { s.py[y] = py; s.ey[y] = ey; }
+    __syncwarp();
 }
 
-// X phase: every x holding its unit relabels if its cheapest arc is not admissible and
-// pushes the unit on it.  Warp per x.
-__global__ void sp_x_kernel(SpDev s, const int32_t *xl, int nx, int32_t *yl_next, int32_t *ycnt_next) {
+// X op: x holding its unit relabels if its cheapest arc is not admissible and pushes
+// the unit on it.  One warp.
+__device__ __forceinline__ void sp_x_op(const SpDev &s, int x, int32_t *yl_next, int32_t *ycnt_next,
+                                        unsigned long long &pushes, unsigned long long &relabels) {
     const int lane = threadIdx.x & 31;
-    unsigned long long pushes = 0, relabels = 0;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nx; i += (gridDim.x * blockDim.x) >> 5) {
-        const int x = xl[i];
-        long long best;
-        int arc;
-        sp_row_min(s, x, lane, best, arc);
-        if (lane == 0) {
-            if (arc == INT32_MAX) {
-                atomicExch(s.cnt + 4, 1);
-            } else {
-                const long long px = s.px[x];
-                if (!(best < -px)) { s.px[x] = -(best + s.eps); relabels++; atomicAdd(s.cnt + 5, 1); }
-                s.mat[x] = arc;
-                pushes++;
-                const int y = s.col[arc];
-                if (atomicAdd(s.ey + y, 1) == 0) yl_next[atomicAdd(ycnt_next, 1)] = y;
-            }
+    long long best;
+    int arc;
+    sp_row_min(s, x, lane, best, arc);
+    if (lane == 0) {
+        if (arc == INT32_MAX) {
+            atomicExch(s.cnt + 4, 1);
+        } else {
+            const long long px = __ldcg((const long long *)s.px + x);
+            if (!(best < -px)) { s.px[x] = -(best + s.eps); relabels++; atomicAdd(s.cnt + 5, 1); }
+            s.mat[x] = arc;
+            pushes++;
+            const int y = s.col[arc];
+            if (atomicAdd(s.ey + y, 1) == 0) yl_next[atomicAdd(ycnt_next, 1)] = y;
         }
     }
+    __syncwarp();
+}
+
+constexpr int SP_THREADS = 256, SP_WARPS = SP_THREADS / 32;
+
+// control words read right after a barrier: thread 0 loads them, the CTA shares them
+__device__ __forceinline__ void sp_bcast(const int32_t *a, const int32_t *b, const int32_t *c, int &va, int &vb,
+                                         int &vc) {
+    __shared__ int sh[3];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        sh[0] = __ldcg(a);
+        sh[1] = b ? __ldcg(b) : 0;
+        sh[2] = c ? __ldcg(c) : 0;
+    }
+    __syncthreads();
+    va = sh[0]; vb = sh[1]; vc = sh[2];
+}
+
+// The refine's rounds as one cooperative kernel (refine_par's coordinator loop,
+// assign_par.py:162-236).  Round r (b = r & 1): Y phase over ylist[b] -> xlist[b];
+// barrier; X phase over xlist[b] -> ylist[b ^ 1]; barrier.  Exits when no Y holds
+// excess (cnt[9] = 0) or a price update is due (cnt[9] = 1); the round index persists
+// in cnt[8].  Counters of the lists a round writes are zeroed one round ahead (their
+// last readers finished before the previous round's closing barrier).  Once the Y
+// list is no longer than tail_threshold the other CTAs leave and CTA 0 continues with
+// CTA barriers.
+__global__ void __launch_bounds__(SP_THREADS) sp_rounds_kernel(SpDev s, int pu_threshold, long long round_budget,
+                                                              int tail_threshold) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ long long s_v[SP_WARPS][SP_YCAP];
+    __shared__ int s_x[SP_WARPS][SP_YCAP];
+    __shared__ int s_n[SP_WARPS];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long pushes = 0, relabels = 0, rounds = 0;
+    bool tail = false;
+    int r, u0, u1, u2;
+    sp_bcast(s.cnt + 8, nullptr, nullptr, r, u0, u1);
+    for (;; r++) {
+        int infeasible, relabels_since;
+        sp_bcast(s.cnt + 4, s.cnt + 5, nullptr, infeasible, relabels_since, u0);
+        const int b = r & 1;
+        int ny;
+        sp_bcast(s.cnt + 2 + b, nullptr, nullptr, ny, u1, u2);
+        if (ny == 0 || infeasible) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) s.cnt[9] = 0;
+            break;
+        }
+        if (pu_threshold > 0 && relabels_since >= pu_threshold) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) s.cnt[9] = 1;
+            break;
+        }
+        if (r >= round_budget) {   // prices diverge: no perfect matching (assign_par.py:221-226)
+            if (blockIdx.x == 0 && threadIdx.x == 0) { atomicExch(s.cnt + 4, 1); s.cnt[9] = 0; }
+            break;
+        }
+        if (!tail && ny <= tail_threshold) {
+            tail = true;
+            if (blockIdx.x != 0) break;
+        }
+        rounds++;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            s.cnt[0 + (b ^ 1)] = 0;   // X list of round r + 1
+            s.cnt[2 + (b ^ 1)] = 0;   // Y list this round's X phase writes (last read in round r - 1)
+        }
+        const int gw = tail ? wid : (int)((blockIdx.x * SP_THREADS + threadIdx.x) >> 5);
+        const int nw = tail ? SP_WARPS : (int)((gridDim.x * SP_THREADS) >> 5);
+        for (int i = gw; i < ny; i += nw)
+            sp_y_op(s, __ldcg(s.list[2 + b] + i), s.list[0 + b], s.cnt + 0 + b, s_v[wid], s_x[wid], &s_n[wid],
+                    pushes, relabels);
+        if (tail) { __threadfence_block(); __syncthreads(); } else grid.sync();
+        int nx;
+        sp_bcast(s.cnt + 0 + b, nullptr, nullptr, nx, u1, u2);
+        for (int i = gw; i < nx; i += nw)
+            sp_x_op(s, __ldcg(s.list[0 + b] + i), s.list[2 + (b ^ 1)], s.cnt + 2 + (b ^ 1), pushes, relabels);
+        if (tail) { __threadfence_block(); __syncthreads(); } else grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) s.cnt[8] = r;   // the round index persists across launches
     if (lane == 0) {
         if (pushes) atomicAdd(s.ops + 0, pushes);
         if (relabels) atomicAdd(s.ops + 1, relabels);
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && rounds) atomicAdd(s.ops + 2, rounds);
 }
 
 // floor(rc / eps) for eps >= 1
@@ -229,72 +304,103 @@ __device__ __forceinline__ long long sp_floordiv(long long rc, long long eps) {
     return q;
 }
 
-// price update (assign_scaling.py:208-276): labels = distances to the deficit set over
-// reverse residual arcs, arc length floor(c_p / eps) + 1 >= 0, explored up to `cap`.
-__global__ void sp_pu_init_kernel(SpDev s, int32_t *fr, int32_t *fcnt) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < s.n; v += gridDim.x * blockDim.x) {
-        s.lx[v] = SP_LINF;
-        if (s.ey[v] < 0) { s.ly[v] = 0; s.infy[v] = 1; fr[atomicAdd(fcnt, 1)] = v; }
-        else { s.ly[v] = SP_LINF; s.infy[v] = 0; }
-    }
-}
-
-// one wave: frontier y relax every residual forward arc x -> y into l(x) and, where l(x)
-// dropped, x's matched reverse arc into its y (queued for the next wave)
-__global__ void sp_pu_wave_kernel(SpDev s, const int32_t *fr, int nf, int32_t *fr_next, int32_t *fcnt_next, long long cap) {
+// price update (assign_scaling.py:208-276) as one cooperative kernel: labels =
+// distances to the deficit set over reverse residual arcs, arc length floor(c_p / eps)
+// + 1 >= 0, explored in frontier waves (grid barrier per wave) up to a label cap that
+// widens x8 while an active node is unlabelled; then prices fall by eps min(label,
+// last + 1), last = the largest label of an active node.  Frontiers live in list[2],
+// list[3]; frontier counts rotate over cnt[12..14] so the next-but-one count is zeroed
+// during a wave.
+__global__ void __launch_bounds__(SP_THREADS) sp_pu_kernel(SpDev s) {
+    cg::grid_group grid = cg::this_grid();
+    const int tid = blockIdx.x * SP_THREADS + threadIdx.x, nthr = gridDim.x * SP_THREADS;
     const int lane = threadIdx.x & 31;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nf; i += (gridDim.x * blockDim.x) >> 5) {
-        const int y = fr[i];
-        if (lane == 0) s.infy[y] = 0;
-        __syncwarp();
-        const int lyv = __ldcg(s.ly + y);
-        const long long pyv = s.py[y];
-        for (int64_t k = s.cp[y] + lane; k < s.cp[y + 1]; k += 32) {
-            const int a = s.ca[k], x = s.cx[k];
-            if (s.fixed[a] || __ldcg(s.mat + x) == a) continue;      // fixed / flow arc
-            const long long rc = -(long long)s.w[a] * s.scale + s.px[x] - pyv;
-            long long len = sp_floordiv(rc, s.eps) + 1;
-            if (len < 0) len = 0;
-            const long long c1 = (long long)lyv + len;
-            if (c1 > cap || c1 >= __ldcg(s.lx + x)) continue;
-            const int old = atomicMin(s.lx + x, (int)c1);
-            if ((int)c1 >= old) continue;
-            const int ma = __ldcg(s.mat + x);
-            if (ma < 0 || s.frozen[x]) continue;
-            const int y2 = s.col[ma];
-            const long long rc2 = (long long)s.w[ma] * s.scale - s.px[x] + s.py[y2];
-            long long len2 = sp_floordiv(rc2, s.eps) + 1;
-            if (len2 < 0) len2 = 0;
-            const long long c2 = c1 + len2;
-            if (c2 > cap) continue;
-            if ((int)c2 < atomicMin(s.ly + y2, (int)c2) && atomicExch(s.infy + y2, 1) == 0)
-                fr_next[atomicAdd(fcnt_next, 1)] = y2;
+    const int gw = tid >> 5, nw = nthr >> 5;
+    long long cap = min((long long)s.max_bucket, 8LL);
+    unsigned long long waves = 0;
+    for (;;) {
+        if (tid == 0) { s.cnt[6] = 0; s.cnt[7] = 0; s.cnt[12] = 0; s.cnt[13] = 0; s.cnt[14] = 0; }
+        grid.sync();
+        for (int v = tid; v < s.n; v += nthr) {
+            s.lx[v] = SP_LINF;
+            if (s.ey[v] < 0) { s.ly[v] = 0; s.infy[v] = 1; s.list[2][atomicAdd(s.cnt + 12, 1)] = v; }
+            else { s.ly[v] = SP_LINF; s.infy[v] = 0; }
         }
-    }
-}
-
-// last = max label over active nodes; a missing one asks for a wider cap
-__global__ void sp_pu_last_kernel(SpDev s) {
-    int last = 0, missing = 0;
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < s.n; v += gridDim.x * blockDim.x) {
-        if (s.mat[v] < 0 && !s.frozen[v]) { const int l = s.lx[v]; if (l >= SP_LINF) missing = 1; else last = max(last, l); }
-        if (s.ey[v] > 0) { const int l = s.ly[v]; if (l >= SP_LINF) missing = 1; else last = max(last, l); }
-    }
+        grid.sync();
+        for (int it = 0;; it++) {
+            int nf, u1, u2;
+            sp_bcast(s.cnt + 12 + it % 3, nullptr, nullptr, nf, u1, u2);
+            if (nf == 0) break;
+            waves++;
+            if (tid == 0) s.cnt[12 + (it + 2) % 3] = 0;
+            const int32_t *fr = s.list[2 + (it & 1)];
+            int32_t *fr_next = s.list[2 + ((it + 1) & 1)];
+            int32_t *fcnt_next = s.cnt + 12 + (it + 1) % 3;
+            for (int i = gw; i < nf; i += nw) {
+                const int y = __ldcg(fr + i);
+                if (lane == 0) s.infy[y] = 0;
+                __syncwarp();
+                __threadfence();   // clear the flag before reading l(y): a later drop re-queues y
+                const int lyv = __ldcg(s.ly + y);
+                const long long pyv = __ldcg((const long long *)s.py + y);
+                for (int64_t k = s.cp[y] + lane; k < s.cp[y + 1]; k += 32) {
+                    const int a = s.ca[k], x = s.cx[k];
+                    if (s.fixed[a] || __ldcg(s.mat + x) == a) continue;      // fixed / flow arc
+                    const long long rc = -(long long)s.w[a] * s.scale + __ldcg((const long long *)s.px + x) - pyv;
+                    long long len = sp_floordiv(rc, s.eps) + 1;
+                    if (len < 0) len = 0;
+                    const long long c1 = (long long)lyv + len;
+                    if (c1 > cap || c1 >= __ldcg(s.lx + x)) continue;
+                    const int old = atomicMin(s.lx + x, (int)c1);
+                    if ((int)c1 >= old) continue;
+                    const int ma = __ldcg(s.mat + x);
+                    if (ma < 0 || s.frozen[x]) continue;
+                    const int y2 = s.col[ma];
+                    const long long rc2 = (long long)s.w[ma] * s.scale - __ldcg((const long long *)s.px + x) +
+                                          __ldcg((const long long *)s.py + y2);
+                    long long len2 = sp_floordiv(rc2, s.eps) + 1;
+                    if (len2 < 0) len2 = 0;
+                    const long long c2 = c1 + len2;
+                    if (c2 > cap) continue;
+                    if ((int)c2 < atomicMin(s.ly + y2, (int)c2) && atomicExch(s.infy + y2, 1) == 0)
+                        fr_next[atomicAdd(fcnt_next, 1)] = y2;
+                }
+            }
+            grid.sync();
+        }
+        // last = max label over active nodes; a missing one asks for a wider cap
+        int last = 0, missing = 0;
+        for (int v = tid; v < s.n; v += nthr) {
+            if (__ldcg(s.mat + v) < 0 && !s.frozen[v]) { const int l = __ldcg(s.lx + v); if (l >= SP_LINF) missing = 1; else last = max(last, l); }
+            if (__ldcg(s.ey + v) > 0) { const int l = __ldcg(s.ly + v); if (l >= SP_LINF) missing = 1; else last = max(last, l); }
+        }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
-        missing |= __shfl_xor_sync(0xffffffffu, missing, o);
+        for (int o = 16; o > 0; o >>= 1) {
+            last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+            missing |= __shfl_xor_sync(0xffffffffu, missing, o);
+        }
+        if (lane == 0) {
+            if (last) atomicMax(s.cnt + 7, last);
+            if (missing) atomicOr(s.cnt + 6, 1);
+        }
+        grid.sync();
+        int chg, lst, u2;
+        sp_bcast(s.cnt + 6, s.cnt + 7, nullptr, chg, lst, u2);
+        if (!chg || cap >= s.max_bucket) {
+            const long long K = min((long long)lst, (long long)s.max_bucket) + 1;
+            for (int v = tid; v < s.n; v += nthr) {
+                s.px[v] -= s.eps * min((long long)s.lx[v], K);
+                s.py[v] -= s.eps * min((long long)s.ly[v], K);
+            }
+            break;
+        }
+        cap = min(cap * 8, (long long)s.max_bucket);
+        grid.sync();
     }
-    if ((threadIdx.x & 31) == 0) {
-        if (last) atomicMax(s.cnt + 7, last);
-        if (missing) atomicOr(s.cnt + 6, 1);
-    }
-}
-
-__global__ void sp_pu_apply_kernel(SpDev s, long long K) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < s.n; v += gridDim.x * blockDim.x) {
-        s.px[v] -= s.eps * min((long long)s.lx[v], K);
-        s.py[v] -= s.eps * min((long long)s.ly[v], K);
+    if (tid == 0) {
+        s.cnt[5] = 0;   // relabels since the last price update
+        atomicAdd(s.ops + 4, 1ull);
+        atomicAdd(s.ops + 5, waves);
     }
 }
 
@@ -351,44 +457,8 @@ struct SpHost {
 };
 
 int sp_sync_cnt(SpHost &H) {
-    FM_CHECK_CUDA(cudaMemcpyAsync(H.h, H.d.cnt, sizeof(int32_t) * 8, cudaMemcpyDeviceToHost, H.st));
+    FM_CHECK_CUDA(cudaMemcpyAsync(H.h, H.d.cnt, sizeof(int32_t) * 16, cudaMemcpyDeviceToHost, H.st));
     FM_CHECK_CUDA(cudaStreamSynchronize(H.st));
-    return FM_OK;
-}
-
-int sp_price_update(SpHost &H, int blocks, fm_stats &st) {
-    SpDev &d = H.d;
-    long long cap = std::min<long long>(d.max_bucket, 8);
-    for (;;) {
-        FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * 4, H.st));
-        FM_CHECK_CUDA(cudaMemsetAsync(d.cnt + 6, 0, sizeof(int32_t) * 2, H.st));
-        sp_pu_init_kernel<<<blocks, 256, 0, H.st>>>(d, d.list[2], d.cnt + 2);
-        st.launches++;
-        int b = 0;
-        for (;;) {
-            FM_TRY(sp_sync_cnt(H));
-            const int nf = H.h[2 + b];
-            if (nf == 0) break;
-            FM_CHECK_CUDA(cudaMemsetAsync(d.cnt + 2 + (b ^ 1), 0, sizeof(int32_t), H.st));
-            sp_pu_wave_kernel<<<std::max(1, std::min((nf + 7) / 8, blocks * 4)), 256, 0, H.st>>>(
-                d, d.list[2 + b], nf, d.list[2 + (b ^ 1)], d.cnt + 2 + (b ^ 1), cap);
-            FM_CHECK_LAUNCH();
-            st.launches++;
-            st.reserved[2]++;   // waves
-            b ^= 1;
-        }
-        sp_pu_last_kernel<<<blocks, 256, 0, H.st>>>(d);
-        FM_CHECK_LAUNCH();
-        st.launches++;
-        FM_TRY(sp_sync_cnt(H));
-        if (!H.h[6] || cap >= d.max_bucket) break;
-        cap = std::min<long long>(cap * 8, d.max_bucket);
-    }
-    const long long K = std::min<long long>(H.h[7], d.max_bucket) + 1;
-    sp_pu_apply_kernel<<<blocks, 256, 0, H.st>>>(d, K);
-    FM_CHECK_LAUNCH();
-    st.launches++;
-    st.reserved[1]++;   // price updates
     return FM_OK;
 }
 
@@ -494,48 +564,50 @@ extern "C" int fm_assign_sparse_solve(int32_t n, int64_t m, const int32_t *xs, c
     long long eps = std::max(1LL, bound);
     const bool use_pu = flags & FM_ASSIGN_PRICE_UPDATE, use_fix = flags & FM_ASSIGN_ARC_FIX;
     const int pu_threshold = std::max(64, n / 16);
+    const int pu_arg = use_pu ? pu_threshold : 0;
     // _ops_budget (assign_scaling.py:374-377) = max(1e4, 40 n^2 m) operations; a round does >= 1
-    const double budget = std::max(1e4, 40.0 * n * (double)n * std::max<double>(1.0, (double)m));
-    long long rounds = 0;
+    const long long round_budget = (long long)std::min(9e18, std::max(1e4, 40.0 * n * (double)n * std::max<double>(1.0, (double)m)));
+    const int tail_threshold = 2 * SP_WARPS;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp_rounds_kernel, SP_THREADS, 0);
+    int occ2 = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, sp_pu_kernel, SP_THREADS, 0);
+    const int coop_blocks = std::max(1, std::min({sms * std::max(1, std::min(occ, occ2)), (n + SP_WARPS - 1) / SP_WARPS,
+                                                  sms * 4}));
     int rc = FM_OK;
     while (rc == FM_OK) {
         eps = std::max(1LL, (eps + alpha - 1) / alpha);
         d.eps = eps;
         d.max_bucket = std::min<long long>(bound / eps + 2, SP_LINF - 1);
-        FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * 8, H.st));
+        FM_CHECK_CUDA(cudaMemsetAsync(d.cnt, 0, sizeof(int32_t) * 16, H.st));
         sp_reset_kernel<<<blocks, 256, 0, H.st>>>(d);
         sp_begin_kernel<<<std::max(1, std::min((n + 7) / 8, sms * 8)), 256, 0, H.st>>>(d);
         FM_CHECK_LAUNCH();
         st.launches += 2;
-        // rounds: Y phase over list[2 + b] -> X list, X phase -> Y list[2 + (b ^ 1)]
-        int b = 0;
+        // rounds (one cooperative launch until done or a price update is due)
         for (;;) {
+            void *args[] = {(void *)&d, (void *)&pu_arg, (void *)&round_budget, (void *)&tail_threshold};
+            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)sp_rounds_kernel, dim3(coop_blocks), dim3(SP_THREADS),
+                                                      args, 0, H.st));
+            st.launches++;
             FM_TRY(sp_sync_cnt(H));
             if (H.h[4]) { rc = H.h[4] == 1 ? FM_INFEASIBLE : FM_CUDA_ERROR; break; }
-            const int ny = H.h[2 + b];
-            if (ny == 0) break;
-            if ((double)++rounds > budget) { rc = FM_INFEASIBLE; break; }
-            if (use_pu && H.h[5] >= pu_threshold) {
-                // the price update needs the Y list slots as frontiers: park the Y list in X list 1
-                FM_CHECK_CUDA(cudaMemcpyAsync(d.list[1], d.list[2 + b], sizeof(int32_t) * ny, cudaMemcpyDeviceToDevice, H.st));
-                FM_TRY(sp_price_update(H, blocks, st));
-                FM_CHECK_CUDA(cudaMemcpyAsync(d.list[2], d.list[1], sizeof(int32_t) * ny, cudaMemcpyDeviceToDevice, H.st));
-                const int32_t c[8] = {0, 0, ny, 0, 0, 0, 0, 0};
-                FM_CHECK_CUDA(cudaMemcpyAsync(d.cnt, c, sizeof(c), cudaMemcpyHostToDevice, H.st));
-                FM_CHECK_CUDA(cudaStreamSynchronize(H.st));
-                b = 0;
-            }
-            FM_CHECK_CUDA(cudaMemsetAsync(d.cnt + 0, 0, sizeof(int32_t), H.st));
-            FM_CHECK_CUDA(cudaMemsetAsync(d.cnt + 2 + (b ^ 1), 0, sizeof(int32_t), H.st));
-            sp_y_kernel<<<std::max(1, std::min((ny + 7) / 8, sms * 8)), 256, 0, H.st>>>(d, d.list[2 + b], ny, d.list[0], d.cnt + 0);
-            FM_CHECK_LAUNCH();
-            FM_TRY(sp_sync_cnt(H));
-            const int nx = H.h[0];
-            if (nx) sp_x_kernel<<<std::max(1, std::min((nx + 7) / 8, sms * 8)), 256, 0, H.st>>>(
-                d, d.list[0], nx, d.list[2 + (b ^ 1)], d.cnt + 2 + (b ^ 1));
-            FM_CHECK_LAUNCH();
-            st.launches += 2;
-            b ^= 1;
+            if (H.h[9] != 1) break;   // no Y holds excess: refine done
+            // price update: the Y list moves to list[1] while list[2], list[3] hold frontiers,
+            // then comes back to its slot (the round index keeps counting toward the budget)
+            const int r = H.h[8], b = r & 1, ny = H.h[2 + b];
+            FM_CHECK_CUDA(cudaMemcpyAsync(d.list[1], d.list[2 + b], sizeof(int32_t) * ny, cudaMemcpyDeviceToDevice, H.st));
+            void *pargs[] = {(void *)&d};
+            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)sp_pu_kernel, dim3(coop_blocks), dim3(SP_THREADS), pargs, 0,
+                                                      H.st));
+            st.launches++;
+            st.reserved[1]++;
+            FM_CHECK_CUDA(cudaMemcpyAsync(d.list[2 + b], d.list[1], sizeof(int32_t) * ny, cudaMemcpyDeviceToDevice, H.st));
+            int32_t *c = H.h + 32;   // pinned staging (the copy runs after this loop iteration)
+            for (int i = 0; i < 10; i++) c[i] = 0;
+            c[2 + b] = ny;
+            c[8] = r;
+            FM_CHECK_CUDA(cudaMemcpyAsync(d.cnt, c, sizeof(int32_t) * 10, cudaMemcpyHostToDevice, H.st));
         }
         if (rc != FM_OK) break;
         if (use_fix) {
@@ -577,7 +649,8 @@ extern "C" int fm_assign_sparse_solve(int32_t n, int64_t m, const int32_t *xs, c
     st.ms_total = ms;
     st.pushes = (int64_t)H.hops[0];
     st.relabels = (int64_t)H.hops[1];
-    st.rounds = rounds;
+    st.rounds = (int64_t)H.hops[2];
+    st.reserved[2] = (int64_t)H.hops[5];   // price-update waves
     st.reserved[0] = (int64_t)H.hops[3];   // arcs fixed
     if (stats) *stats = st;
     return rc;
