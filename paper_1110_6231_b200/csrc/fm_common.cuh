@@ -29,6 +29,7 @@ void fm_set_error(const char *fmt, ...);
 // int32 loads that bypass L1: state words are updated by L2 atomics from other
 // SMs, so a cached copy in this SM's L1 could be older than one the L2 holds.
 __device__ __forceinline__ int32_t ld_cg(const int32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ int4 ld_cg4(const int32_t *p) { return __ldcg(reinterpret_cast<const int4 *>(p)); }
 
 // block-wide sum of an int64 via warp shuffles + shared scratch; one atomic per block
 template <int NWARPS>

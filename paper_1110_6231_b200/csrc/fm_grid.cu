@@ -1498,7 +1498,8 @@ __device__ __forceinline__ uint32_t bits_row(const GridDev &g, int tile, int lr,
                            __ballot_sync(0xffffffffu, aD), __ballot_sync(0xffffffffu, aU),
                            __ballot_sync(0xffffffffu, aT)};
     uint32_t *B = g.rbits + (size_t)tile * 160 + lr;
-    if (lane < 5) B[lane * 32] = w[lane];
+    const uint32_t wk = lane == 0 ? w[0] : lane == 1 ? w[1] : lane == 2 ? w[2] : lane == 3 ? w[3] : w[4];
+    if (lane < 5) B[lane * 32] = wk;
     if (r < g.H && c < g.W) g.dist[p] = aT ? 1 : g.INF;
     return w[4];
 }
@@ -1533,7 +1534,9 @@ __device__ __forceinline__ void bits_rows4(const GridDev &g, int tile, int lr0, 
                                __ballot_sync(0xffffffffu, aD), __ballot_sync(0xffffffffu, aU),
                                __ballot_sync(0xffffffffu, aT)};
         uint32_t *B = g.rbits + (size_t)tile * 160 + lr0 + k;
-        if (lane < 5) B[lane * 32] = w[lane];
+        // lane k < 5 stores word k (a select chain: a dynamic index would put w[] on the stack)
+        const uint32_t wk = lane == 0 ? w[0] : lane == 1 ? w[1] : lane == 2 ? w[2] : lane == 3 ? w[3] : w[4];
+        if (lane < 5) B[lane * 32] = wk;
         if (in[k]) g.dist[(int64_t)r * g.W + c] = aT ? 1 : g.INF;
     }
 }
@@ -1731,20 +1734,78 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
 // from the tile's unchanged sink word --, the ring with every tile queued, the push work
 // list's flags, and the relabel's counters.  Replaces bfs_init_bits + ringq_init + three
 // memsets.  Touched flags are cleared by the finalize that follows the BFS.
-__global__ void relabel_init_kernel(GridDev g, RingQ q, int full, unsigned long long *acc) {
+__global__ void __launch_bounds__(256, 6) relabel_init_kernel(GridDev g, RingQ q, int full, unsigned long long *acc) {
     const int lane = threadIdx.x & 31;
     const int ntiles = g.ntx * g.nty;
-    const int64_t nquads = (int64_t)ntiles * (PT_H / 4);
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nquads;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        // consecutive warps take the same 4 rows of consecutive tiles: every plane is then
-        // read as runs of adjacent 128-byte row segments (DRAM-friendly), not one segment
-        // per 16 KB row stride
-        const int tx = (int)(w % g.ntx);
-        const int64_t rest = w / g.ntx;
-        const int ty = (int)(rest / (PT_H / 4)), lr0 = 4 * (int)(rest % (PT_H / 4));
-        const int tile = ty * g.ntx + tx;
-        if (full || g.touched[tile]) {
+    const int nquads = ntiles * (PT_H / 4);   // < 2^31: H * W < 2^30 (fm_grid_create)
+    const int wstep = (gridDim.x * blockDim.x) >> 5;
+    // consecutive warps take the same 4 rows of consecutive tiles: every plane is then
+    // read as runs of adjacent 128-byte row segments (DRAM-friendly), not one segment
+    // per 16 KB row stride
+    // 32-bit index math (a 64-bit division per quad made this pass issue-bound)
+    const auto tile_of = [&](int w) {
+        const int rest = w / g.ntx;
+        return (rest / (PT_H / 4)) * g.ntx + (w - rest * g.ntx);
+    };
+    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (g.ntx % 4 == 0 && g.W == g.ntx * PT_W && g.H == g.nty * PT_H) {
+        // whole tiles, 4 tiles per group: one image row of 4 tiles per warp iteration,
+        // int4 loads (lane = 4 columns), the 32-bit arc words assembled from the lanes'
+        // nibbles with 3 shuffles -- a quarter of the load and ballot instructions
+        const int ngroups = g.ntx / 4;
+        const int nunits = g.nty * PT_H * ngroups;
+        const int j = lane >> 3, sh = 4 * (lane & 7);
+        for (int u = w; u < nunits; u += wstep) {
+            const int row = u / ngroups, tg = u - row * ngroups;   // row = image row
+            const int ty = row / PT_H, lr = row - ty * PT_H;
+            const int tile = ty * g.ntx + 4 * tg + j;
+            const int c = (4 * tg + j) * PT_W + (sh);              // first of this lane's 4 columns
+            const int64_t p = (int64_t)row * g.W + c;
+            const bool tch = full || g.touched[tile];
+            uint32_t *B = g.rbits + (size_t)tile * 160 + lr;
+            uint32_t nR = 0, nL = 0, nD = 0, nU = 0, nT = 0;
+            if (tch) {
+                const int4 R = __ldcs((const int4 *)(g.rR + p)), L = __ldcs((const int4 *)(g.rL + p));
+                const int4 D = __ldcs((const int4 *)(g.rD + p)), U = __ldcs((const int4 *)(g.rU + p));
+                const int4 T = __ldcs((const int4 *)(g.rT + p));
+                const auto nib = [](const int4 v) {
+                    return (uint32_t)(v.x > 0) | ((uint32_t)(v.y > 0) << 1) | ((uint32_t)(v.z > 0) << 2) |
+                           ((uint32_t)(v.w > 0) << 3);
+                };
+                nR = nib(R); nL = nib(L); nD = nib(D); nU = nib(U); nT = nib(T);
+                if (c + 4 >= g.W) nR &= 0x7u;                // the last column has no right arc
+                if (c == 0) nL &= 0xeu;                      // the first column no left arc
+                if (!(row + 1 < g.hlim)) nD = 0;
+                if (!(row > g.rmin)) nU = 0;
+            } else {
+                nT = (__ldcg(B + 128) >> sh) & 0xfu;         // untouched: the old sink word still holds
+            }
+            uint32_t wR = nR << sh, wL = nL << sh, wD = nD << sh, wU = nU << sh, wT = nT << sh;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                wR |= __shfl_xor_sync(0xffffffffu, wR, o);
+                wL |= __shfl_xor_sync(0xffffffffu, wL, o);
+                wD |= __shfl_xor_sync(0xffffffffu, wD, o);
+                wU |= __shfl_xor_sync(0xffffffffu, wU, o);
+                wT |= __shfl_xor_sync(0xffffffffu, wT, o);
+            }
+            const int k = lane & 7;
+            if (tch && k < 5) B[k * 32] = k == 0 ? wR : k == 1 ? wL : k == 2 ? wD : k == 3 ? wU : wT;
+            const int INF = g.INF;
+            *(int4 *)(g.dist + p) = make_int4((nT & 1u) ? 1 : INF, (nT & 2u) ? 1 : INF, (nT & 4u) ? 1 : INF,
+                                              (nT & 8u) ? 1 : INF);
+        }
+        w = nquads;   // done
+    }
+    // the tile's touched flag is loaded one iteration ahead (it gates the plane loads)
+    uint8_t tch_next = 0;
+    if (!full && w < nquads) tch_next = g.touched[tile_of(w)];
+    for (; w < nquads; w += wstep) {
+        const int tile = tile_of(w);
+        const int lr0 = 4 * ((w / g.ntx) % (PT_H / 4));
+        const bool tch = full || tch_next;
+        if (!full && w + wstep < nquads) tch_next = g.touched[tile_of(w + wstep)];
+        if (tch) {
             bits_rows4(g, tile, lr0, lane);
         } else {
             const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
@@ -2301,7 +2362,7 @@ __global__ void __launch_bounds__(PL_NT, FM_PL_MINBLOCKS) pr_ring_kernel(GridDev
 // gap_relabel + marking (as bfs_finalize_kernel), one CTA per tile so each tile with
 // an active pixel is queued once
 // list == nullptr: every tile; else the n tiles of `list` (local relabel region)
-__global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsigned long long *acc,
+__global__ void __launch_bounds__(256, 8) bfs_finalize_tiles_kernel(GridDev g, unsigned long long *acc,
                                                                  const int32_t *list, int n) {
     long long active = 0, mex = 0;
     int32_t lvl = 0;
@@ -2341,7 +2402,9 @@ __global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsi
                 *(int4 *)(g.h + p) = make_int4(hv[0], hv[1], hv[2], hv[3]);
                 if (mchg) *(uchar4 *)(g.marked + p) = make_uchar4(mv[0], mv[1], mv[2], mv[3]);
             }
-            if (__syncthreads_or(act) && threadIdx.x == 0) tq_push(g.pq, 0, tile);
+            // no CTA barrier per tile: every warp that saw an active pixel offers the tile
+            // (the queue flag admits it once), so warps run ahead into the next tile's loads
+            if (__any_sync(0xffffffffu, act) && (threadIdx.x & 31) == 0) tq_push(g.pq, 0, tile);
             continue;
         }
 #pragma unroll
@@ -2362,7 +2425,7 @@ __global__ void __launch_bounds__(256) bfs_finalize_tiles_kernel(GridDev g, unsi
                 if (!g.marked[p]) { g.marked[p] = 1; mex += e; }
             }
         }
-        if (__syncthreads_or(act) && threadIdx.x == 0) tq_push(g.pq, 0, tile);
+        if (__any_sync(0xffffffffu, act) && (threadIdx.x & 31) == 0) tq_push(g.pq, 0, tile);
     }
     __shared__ long long red[2][8];
     __shared__ int32_t redl[8];
@@ -2618,6 +2681,58 @@ __global__ void __launch_bounds__(256) cut_tile_kernel(GridDev g, int parity, in
 // ----------------------------------------------------------------------------
 __global__ void cut_init_bits_kernel(GridDev g) {
     const int lane = threadIdx.x & 31;
+    if (g.ntx % 4 == 0 && g.W == g.ntx * PT_W && g.H == g.nty * PT_H) {
+        // whole tiles, 4 per group: one image row of 4 tiles per warp iteration, lane = 4
+        // columns, int4 loads; the horizontal neighbours' residuals come from the adjacent
+        // lanes (one extra scalar load at the warp's ends); words assembled by shuffles
+        const int ngroups = g.ntx / 4;
+        const int nunits = g.nty * PT_H * ngroups;
+        const int sh = 4 * (lane & 7), j = lane >> 3;
+        for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nunits; u += (gridDim.x * blockDim.x) >> 5) {
+            const int r = u / ngroups, tg = u - r * ngroups;
+            const int ty = r / PT_H, lr = r - ty * PT_H;
+            const int tile = ty * g.ntx + 4 * tg + j;
+            const int c = (4 * tg + j) * PT_W + sh;
+            const int64_t p = (int64_t)r * g.W + c;
+            const int4 L = __ldcs((const int4 *)(g.rL + p)), R = __ldcs((const int4 *)(g.rR + p));
+            const int4 E = __ldcs((const int4 *)(g.e + p)), CS = __ldcs((const int4 *)(g.cS + p));
+            const int4 RS = __ldcs((const int4 *)(g.rS + p));
+            const int4 Db = r + 1 < g.H ? __ldcs((const int4 *)(g.rU + p + g.W))
+                                        : (g.has_dn ? ld_cg4(g.dn.res + c) : make_int4(0, 0, 0, 0));
+            const int4 Ua = r > 0 ? __ldcs((const int4 *)(g.rD + p - g.W))
+                                  : (g.has_up ? ld_cg4(g.up.res + c) : make_int4(0, 0, 0, 0));
+            // rL of column c+4 (right neighbour of this lane's last pixel), rR of column c-1
+            int lNext = __shfl_down_sync(0xffffffffu, L.x, 1);
+            int rPrev = __shfl_up_sync(0xffffffffu, R.w, 1);
+            if (lane == 31) lNext = c + 4 < g.W ? g.rL[p + 4] : 0;
+            if (lane == 0) rPrev = c > 0 ? g.rR[p - 1] : 0;
+            const uint32_t nR = (uint32_t)(L.y > 0) | ((uint32_t)(L.z > 0) << 1) | ((uint32_t)(L.w > 0) << 2) |
+                                ((uint32_t)(c + 4 < g.W && lNext > 0) << 3);   // arc (q+1) -> q
+            const uint32_t nL = (uint32_t)(c > 0 && rPrev > 0) | ((uint32_t)(R.x > 0) << 1) |
+                                ((uint32_t)(R.y > 0) << 2) | ((uint32_t)(R.z > 0) << 3);  // arc (q-1) -> q
+            const auto nib = [](const int4 v) {
+                return (uint32_t)(v.x > 0) | ((uint32_t)(v.y > 0) << 1) | ((uint32_t)(v.z > 0) << 2) |
+                       ((uint32_t)(v.w > 0) << 3);
+            };
+            const uint32_t nD = nib(Db), nU = nib(Ua);
+            const uint32_t nS = (uint32_t)(E.x > 0 || CS.x - RS.x > 0) | ((uint32_t)(E.y > 0 || CS.y - RS.y > 0) << 1) |
+                                ((uint32_t)(E.z > 0 || CS.z - RS.z > 0) << 2) | ((uint32_t)(E.w > 0 || CS.w - RS.w > 0) << 3);
+            uint32_t wR = nR << sh, wL = nL << sh, wD = nD << sh, wU = nU << sh, wS = nS << sh;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                wR |= __shfl_xor_sync(0xffffffffu, wR, o);
+                wL |= __shfl_xor_sync(0xffffffffu, wL, o);
+                wD |= __shfl_xor_sync(0xffffffffu, wD, o);
+                wU |= __shfl_xor_sync(0xffffffffu, wU, o);
+                wS |= __shfl_xor_sync(0xffffffffu, wS, o);
+            }
+            const int k = lane & 7;
+            uint32_t *B = g.rbits + (size_t)tile * 160 + lr;
+            if (k < 5) B[k * 32] = k == 0 ? wR : k == 1 ? wL : k == 2 ? wD : k == 3 ? wU : wS;
+            *(uchar4 *)(g.cut + p) = make_uchar4(nS & 1u, (nS >> 1) & 1u, (nS >> 2) & 1u, (nS >> 3) & 1u);
+        }
+        return;
+    }
     const int64_t nrows = (int64_t)g.ntx * g.nty * PT_H;
     for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -2636,7 +2751,8 @@ __global__ void cut_init_bits_kernel(GridDev g) {
                                 __ballot_sync(0xffffffffu, aD), __ballot_sync(0xffffffffu, aU),
                                 __ballot_sync(0xffffffffu, seed)};
         uint32_t *B = g.rbits + (size_t)tile * 160 + lr;
-        if (lane < 5) B[lane * 32] = wd[lane];
+        const uint32_t wk = lane == 0 ? wd[0] : lane == 1 ? wd[1] : lane == 2 ? wd[2] : lane == 3 ? wd[3] : wd[4];
+        if (lane < 5) B[lane * 32] = wk;
         if (r < g.H && c < g.W) g.cut[p] = seed ? 1 : 0;
     }
 }
@@ -2703,9 +2819,16 @@ __global__ void __launch_bounds__(32 * BB_WARPS) cut_bits_kernel(GridDev g, int 
 __global__ void sum_e_kernel(GridDev g, unsigned long long *acc) {
     const int64_t HW = (int64_t)g.H * g.W;
     long long s = 0;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW;
-         p += (int64_t)gridDim.x * blockDim.x)
-        s += g.e[p];
+    // int4 loads, two in flight per thread (a scalar-load loop ran at 0.7 TB/s)
+    const int64_t n4 = HW >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+    const int4 *e4 = reinterpret_cast<const int4 *>(g.e);
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + stride < n4; i += 2 * stride) {
+        const int4 a = __ldcs(e4 + i), b = __ldcs(e4 + i + stride);
+        s += (long long)a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
+    }
+    for (; i < n4; i += stride) { const int4 a = __ldcs(e4 + i); s += (long long)a.x + a.y + a.z + a.w; }
+    for (int64_t p = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < HW; p += stride) s += g.e[p];
     __shared__ long long red[8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -3021,7 +3144,7 @@ int global_relabel(fm_grid *g) {
         cudaEventRecord(g->ev[0], g->stream);
         const bool full = g->relabel_full || g->pr_kernel != 1 || g->pr_ring ||
                           (g->flags_solve & (FM_GRID_GLOBAL_SWEEP | FM_GRID_CANCEL_VIOLATIONS));
-        relabel_init_kernel<<<std::max(1, std::min((g->ntiles * (PT_H / 4) + 7) / 8, g->sms * 8)), 256, 0, g->stream>>>(
+        relabel_init_kernel<<<std::max(1, std::min((g->ntiles * (PT_H / 4) + 7) / 8, g->sms * 6)), 256, 0, g->stream>>>(
             g->d, g->rq, full ? 1 : 0, g->acc + 4);
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[2], g->stream);
