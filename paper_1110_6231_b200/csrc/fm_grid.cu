@@ -1734,7 +1734,9 @@ __global__ void ringq_init_kernel(RingQ q, int ntiles, const int32_t *list0, con
 // from the tile's unchanged sink word --, the ring with every tile queued, the push work
 // list's flags, and the relabel's counters.  Replaces bfs_init_bits + ringq_init + three
 // memsets.  Touched flags are cleared by the finalize that follows the BFS.
-__global__ void __launch_bounds__(256, 6) relabel_init_kernel(GridDev g, RingQ q, int full, unsigned long long *acc) {
+template <bool WHOLE>   // WHOLE: whole tiles, ntx % 4 == 0 (the 4-tile-group pass)
+__global__ void __launch_bounds__(256, WHOLE ? 4 : 6) relabel_init_kernel(GridDev g, RingQ q, int full, int integ,
+                                                               unsigned long long *acc) {
     const int lane = threadIdx.x & 31;
     const int ntiles = g.ntx * g.nty;
     const int nquads = ntiles * (PT_H / 4);   // < 2^31: H * W < 2^30 (fm_grid_create)
@@ -1748,7 +1750,7 @@ __global__ void __launch_bounds__(256, 6) relabel_init_kernel(GridDev g, RingQ q
         return (rest / (PT_H / 4)) * g.ntx + (w - rest * g.ntx);
     };
     int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (g.ntx % 4 == 0 && g.W == g.ntx * PT_W && g.H == g.nty * PT_H) {
+    if constexpr (WHOLE) {
         // whole tiles, 4 tiles per group: one image row of 4 tiles per warp iteration,
         // int4 loads (lane = 4 columns), the 32-bit arc words assembled from the lanes'
         // nibbles with 3 shuffles -- a quarter of the load and ballot instructions
@@ -1765,9 +1767,34 @@ __global__ void __launch_bounds__(256, 6) relabel_init_kernel(GridDev g, RingQ q
             uint32_t *B = g.rbits + (size_t)tile * 160 + lr;
             uint32_t nR = 0, nL = 0, nD = 0, nU = 0, nT = 0;
             if (tch) {
-                const int4 R = __ldcs((const int4 *)(g.rR + p)), L = __ldcs((const int4 *)(g.rL + p));
-                const int4 D = __ldcs((const int4 *)(g.rD + p)), U = __ldcs((const int4 *)(g.rU + p));
+                int4 R = __ldcs((const int4 *)(g.rR + p)), L = __ldcs((const int4 *)(g.rL + p));
+                int4 D = __ldcs((const int4 *)(g.rD + p)), U = __ldcs((const int4 *)(g.rU + p));
                 const int4 T = __ldcs((const int4 *)(g.rT + p));
+                if (integ) {
+                    // the push round's parked inboxes folded in here (integrate_inflow_kernel's
+                    // work, fused): flow from the tile above / below into rows 0 / 31, from the
+                    // left / right tile into columns 0 / 31; e and the residual toward the
+                    // sender grow by it (a tile with inbox flow was marked touched by its sender)
+                    const int k = lane & 7;
+                    const bool vtop = lr == 0 && row > g.rmin, vbot = lr == PT_H - 1 && row + 1 < g.hlim;
+                    const int4 dv = (vtop || vbot) ? __ldcg((const int4 *)(g.inflow_v + p)) : make_int4(0, 0, 0, 0);
+                    const int dl = (k == 0 && c > 0) ? __ldcg(g.inflow_h + p) : 0;
+                    const int dr = (k == 7 && c + 4 < g.W) ? __ldcg(g.inflow_h + p + 3) : 0;
+                    const bool anyv = dv.x | dv.y | dv.z | dv.w;
+                    if (anyv || dl || dr) {
+                        int4 E = __ldcg((const int4 *)(g.e + p));
+                        E.x += dv.x + dl; E.y += dv.y; E.z += dv.z; E.w += dv.w + dr;
+                        *(int4 *)(g.e + p) = E;
+                        if (anyv) {
+                            *(int4 *)(g.inflow_v + p) = make_int4(0, 0, 0, 0);
+                            int4 &V = vtop ? U : D;
+                            V.x += dv.x; V.y += dv.y; V.z += dv.z; V.w += dv.w;
+                            *(int4 *)((vtop ? g.rU : g.rD) + p) = V;
+                        }
+                        if (dl) { g.inflow_h[p] = 0; L.x += dl; g.rL[p] = L.x; }
+                        if (dr) { g.inflow_h[p + 3] = 0; R.w += dr; g.rR[p + 3] = R.w; }
+                    }
+                }
                 const auto nib = [](const int4 v) {
                     return (uint32_t)(v.x > 0) | ((uint32_t)(v.y > 0) << 1) | ((uint32_t)(v.z > 0) << 2) |
                            ((uint32_t)(v.w > 0) << 3);
@@ -1795,8 +1822,7 @@ __global__ void __launch_bounds__(256, 6) relabel_init_kernel(GridDev g, RingQ q
             *(int4 *)(g.dist + p) = make_int4((nT & 1u) ? 1 : INF, (nT & 2u) ? 1 : INF, (nT & 4u) ? 1 : INF,
                                               (nT & 8u) ? 1 : INF);
         }
-        w = nquads;   // done
-    }
+    } else {
     // the tile's touched flag is loaded one iteration ahead (it gates the plane loads)
     uint8_t tch_next = 0;
     if (!full && w < nquads) tch_next = g.touched[tile_of(w)];
@@ -1817,6 +1843,7 @@ __global__ void __launch_bounds__(256, 6) relabel_init_kernel(GridDev g, RingQ q
                 if (r < g.H && c < g.W) g.dist[(int64_t)r * g.W + c] = ((tw >> lane) & 1u) ? 1 : g.INF;
             }
         }
+    }
     }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < q.cap; i += gridDim.x * blockDim.x) {
         q.slot[i] = i < ntiles ? i : -1;
@@ -2930,6 +2957,7 @@ struct fm_grid {
     // solve state
     int32_t flags_solve = 0;
     bool relabel_full = true;            // next global relabel rebuilds every tile's arc words
+    bool inflow_deferred = false;        // this round's inboxes are folded in by the relabel preparation
     long long sum_capS = 0;
     long long excess_total = 0;          // maxflow_par.py HybridState.excess_total
     long long active = 0;
@@ -3144,8 +3172,11 @@ int global_relabel(fm_grid *g) {
         cudaEventRecord(g->ev[0], g->stream);
         const bool full = g->relabel_full || g->pr_kernel != 1 || g->pr_ring ||
                           (g->flags_solve & (FM_GRID_GLOBAL_SWEEP | FM_GRID_CANCEL_VIOLATIONS));
-        relabel_init_kernel<<<std::max(1, std::min((g->ntiles * (PT_H / 4) + 7) / 8, g->sms * 6)), 256, 0, g->stream>>>(
-            g->d, g->rq, full ? 1 : 0, g->acc + 4);
+        const bool whole = g->d.ntx % 4 == 0 && g->W == g->d.ntx * PT_W && g->H == g->d.nty * PT_H;
+        (whole ? relabel_init_kernel<true> : relabel_init_kernel<false>)
+            <<<std::max(1, std::min((g->ntiles * (PT_H / 4) + 7) / 8, g->sms * (whole ? 4 : 6))), 256, 0, g->stream>>>(
+                g->d, g->rq, full ? 1 : 0, g->inflow_deferred ? 1 : 0, g->acc + 4);
+        g->inflow_deferred = false;
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[2], g->stream);
         ring_kernel<0><<<ring_blocks(g), 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
@@ -3246,6 +3277,7 @@ int begin_device(fm_grid *g, const int32_t *capR, const int32_t *capL, const int
     g->flags_solve = flags;
     g->local_streak = 0;
     g->relabel_full = true;   // init + two-hop changed every residual
+    g->inflow_deferred = false;
     memset(&g->st, 0, sizeof(g->st));
     FM_CHECK_CUDA(cudaMemsetAsync(g->d_touched, 0, (size_t)g->ntiles, g->stream));
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc, 0, sizeof(unsigned long long) * 32, g->stream));
@@ -3394,6 +3426,16 @@ void pr_graph_consume(fm_grid *g, int32_t *idle_out, bool keep_parity = false) {
     if (idle_out) *idle_out = c->processed == 0 ? 1 : 0;
 }
 
+// fold the push round's parked inboxes into e and the residuals -- unless the global
+// relabel that follows does it in its preparation pass (inflow_deferred)
+int integrate_inflow(fm_grid *g) {
+    if (g->inflow_deferred) return FM_OK;
+    integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
+    FM_CHECK_LAUNCH();
+    g->st.launches++;
+    return FM_OK;
+}
+
 int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int32_t *idle_out = nullptr) {
     // passes per visit: large grids (the device-side round loop below, TMA-staged visits)
     // amortise a visit over 32 passes (4096^2: 23.1 -> 21.8 ms, 8192^2: 71.6 -> 66.5 ms),
@@ -3435,9 +3477,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
         cudaEventRecord(g->ev[7], g->stream);
         FM_CHECK_CUDA(cudaMemcpyAsync(h, pr_ctl_dev(g), sizeof(PrCtl), cudaMemcpyDeviceToHost, g->stream));
         g->prg_pending = true;
-        integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
-        FM_CHECK_LAUNCH();
-        g->st.launches++;
+        FM_TRY(integrate_inflow(g));
         return FM_OK;
     }
     int32_t done = 0;
@@ -3480,9 +3520,7 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
         }
         if ((long long)g->h_acc[11] >= relabel_budget) break;
     }
-    integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
-    FM_CHECK_LAUNCH();
-    g->st.launches++;
+    FM_TRY(integrate_inflow(g));
     g->st.pr_sweeps += done;
     return FM_OK;
 }
@@ -3505,9 +3543,8 @@ int run_round_ring(fm_grid *g, int32_t cycle_budget) {
     FM_CHECK_LAUNCH();
     cudaEventRecord(g->ev[3], g->stream);
     FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 9, g->prq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
-    integrate_inflow_kernel<<<g->ntiles, 4 * PT_W, 0, g->stream>>>(g->d);
-    FM_CHECK_LAUNCH();
-    g->st.launches += 3;
+    FM_TRY(integrate_inflow(g));
+    g->st.launches += 2;
     g->st.pr_launches += 1;
     g->st.pr_sweeps += 1;
     g->pr_stats_pending = true;
@@ -3520,6 +3557,14 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
     cudaEventRecord(g->ev[4], g->stream);
     FM_CHECK_CUDA(cudaMemsetAsync(g->acc + 10, 0, sizeof(unsigned long long) * 2, g->stream));
     int32_t sweeps = 0;
+    // the relabel that closes this round (decided by the last relabel's active count)
+    const bool go_local = g->local_div > 0 && !(g->flags_solve & FM_GRID_GLOBAL_SWEEP) &&
+                          !(g->flags_solve & FM_GRID_CANCEL_VIOLATIONS) &&
+                          g->active <= g->HW / g->local_div && g->local_streak < g->local_max;
+    // a global relabel over whole 4-tile groups folds the inboxes in (no integrate pass)
+    g->inflow_deferred = !go_local && g->bfs_bits == 2 && g->nbands == 0 && g->pr_kernel == 1 &&
+                         !(g->flags_solve & (FM_GRID_GLOBAL_SWEEP | FM_GRID_CANCEL_VIOLATIONS)) &&
+                         g->d.ntx % 4 == 0 && g->W == g->d.ntx * PT_W && g->H == g->d.nty * PT_H;
     // tail rounds (few active pixels, flow crossing many tiles) as one persistent launch
     const int ring_tail = g->ring_tail >= 0 ? g->ring_tail : (g->HW <= ((int64_t)1 << 24) ? 1024 : 0);
     if (g->flags_solve & FM_GRID_GLOBAL_SWEEP) {
@@ -3560,9 +3605,6 @@ int run_round(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval) {
         FM_TRY(sync_stream(g));
         collect(false);
     }
-    const bool go_local = g->local_div > 0 && !(g->flags_solve & FM_GRID_GLOBAL_SWEEP) &&
-                          !(g->flags_solve & FM_GRID_CANCEL_VIOLATIONS) &&
-                          g->active <= g->HW / g->local_div && g->local_streak < g->local_max;
     if (go_local) {
         g->local_streak++;
         FM_TRY(local_relabel(g));
