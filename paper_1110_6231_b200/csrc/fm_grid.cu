@@ -2121,6 +2121,81 @@ __device__ __forceinline__ RingChange cut_visit(const GridDev &g, int tile, int 
     return ch;
 }
 
+// K2 with owner scheduling (single band, global relabel; option bfs_owner): tile t is
+// visited only by warp t mod (launch warps), so no two warps ever hold it and there is
+// no shared queue -- a visit whose border changed marks the neighbour tile dirty (one
+// release exchange on its flag), the owner finds it by polling its few flags and takes
+// it with an acquire exchange.  Replaces the ring's pop / claim / publish round trips
+// and its two hottest words (head, tail); the pending count stays: a visit adds the
+// neighbours it is about to mark BEFORE marking them (a marked tile can be taken and
+// finished at once), then removes the ones that were already dirty and itself.  Flags:
+// 0 clean, 1 dirty (relabel_init leaves every tile dirty, pending = ntiles).
+__device__ __forceinline__ int exch_acq_rel(int32_t *p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+__global__ void __launch_bounds__(32 * BB_WARPS) owner_bfs_kernel(GridDev g, RingQ q) {
+    __shared__ int32_t s_d[BB_WARPS][PT_H * (PT_W + 1)];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t *sd = s_d[wid];
+    const int gw = blockIdx.x * BB_WARPS + wid, nw = gridDim.x * BB_WARPS;
+    const int ntiles = g.ntx * g.nty;
+    const int nown = gw < ntiles ? (ntiles - gw + nw - 1) / nw : 0;   // <= 64 (host checks)
+    uint32_t vis0 = 0, vis1 = 0;   // owned tile i visited in this launch (incremental re-visits)
+    unsigned chg_count = 0, nvis = 0;
+    long long busy = 0;
+    unsigned ns = q.ns0;
+    for (;;) {
+        const int32_t f0 = lane < nown ? *(volatile int32_t *)(q.flag + gw + lane * nw) : 0;
+        const int32_t f1 = lane + 32 < nown ? *(volatile int32_t *)(q.flag + gw + (lane + 32) * nw) : 0;
+        uint32_t d0 = __ballot_sync(0xffffffffu, f0 != 0), d1 = __ballot_sync(0xffffffffu, f1 != 0);
+        if (!(d0 | d1)) {
+            if (*(volatile unsigned *)q.pend == 0) break;
+            __nanosleep(ns);
+            ns = min(ns * 2, (unsigned)q.ns1);
+            continue;
+        }
+        ns = q.ns0;
+        while (d0 | d1) {
+            int i;
+            if (d0) { i = __ffs(d0) - 1; d0 &= d0 - 1; } else { i = 32 + __ffs(d1) - 1; d1 &= d1 - 1; }
+            const int tile = gw + i * nw;
+            int took = 0;
+            if (lane == 0) took = exch_acq_rel(q.flag + tile, 0);   // acquire: the markers' stores
+            took = __shfl_sync(0xffffffffu, took, 0);
+            __syncwarp();
+            if (!took) continue;
+            const bool vis = i < 32 ? ((vis0 >> i) & 1u) : ((vis1 >> (i - 32)) & 1u);
+            const long long tv0 = clock64();
+            const RingChange ch = bfs_visit(g, q, tile, vis, sd, lane);
+            busy += clock64() - tv0;
+            nvis++;
+            if (i < 32) vis0 |= 1u << i; else vis1 |= 1u << (i - 32);
+            chg_count += ch.any ? 1u : 0u;
+            const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
+            int nt = -1;
+            if (lane == 0 && ch.b0 && tyi > 0) nt = tile - g.ntx;
+            if (lane == 1 && ch.b1 && tyi + 1 < g.nty) nt = tile + g.ntx;
+            if (lane == 2 && ch.b2 && txi > 0) nt = tile - 1;
+            if (lane == 3 && ch.b3 && txi + 1 < g.ntx) nt = tile + 1;
+            const int k = __popc(__ballot_sync(0xffffffffu, nt >= 0));
+            if (lane == 0 && k) atomicAdd(q.pend, (unsigned)k);   // counted before they can be taken
+            __syncwarp();   // the warp's dist stores (and the count) precede the release exchanges
+            const bool fresh = nt >= 0 && exch_acq_rel(q.flag + nt, 1) == 0;
+            const int nfresh = __popc(__ballot_sync(0xffffffffu, fresh));
+            if (lane == 0) atomicAdd(q.pend, (unsigned)(nfresh - k - 1));   // this tile done
+            __syncwarp();
+        }
+    }
+    if (lane == 0 && chg_count) atomicAdd(q.ctr + 96, chg_count);
+    if (lane == 0 && nvis) {   // visits and the cycles spent inside them (trace statistics)
+        atomicAdd(q.ctr + 192, nvis);
+        atomicAdd((unsigned long long *)(q.ctr + 240), (unsigned long long)busy);
+    }
+}
+
 // K2 (MODE 0, global relabel BFS) / K3 (MODE 1, min-cut reach) as ONE persistent
 // launch over the ring queue.  Row-band mode: halos of the band's first / last tile
 // row come from the neighbour bands' planes, a changed boundary row queues the
@@ -2905,6 +2980,8 @@ struct fm_grid {
                                          // sweeps (bfs_bits_kernel), 0: v1 Jacobi sweeps (option BFS_BITS)
     int bb_per_sm = 8;                   // resident bfs_bits CTAs per SM (occupancy query)
     int br_per_sm = 8;                   // resident bfs_ring CTAs per SM (occupancy query, <= br_cap)
+    int bfs_owner = 1;                   // global relabel BFS with owner scheduling (owner_bfs_kernel; option bfs_owner;
+                                         // r02bv: BFS kernel 4096^2 -2..4%, 8192^2 -8% vs the ring)
     int br_cap = 8;                      // option BR_CAP
     RingQ rq{};                          // device work queue of the persistent BFS
     RingQ prq{};                         // device work queue of the persistent push round
@@ -3179,7 +3256,11 @@ int global_relabel(fm_grid *g) {
         g->inflow_deferred = false;
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[2], g->stream);
-        ring_kernel<0><<<ring_blocks(g), 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+        const int rb = ring_blocks(g);
+        if (g->bfs_owner && g->ntiles <= 64 * rb * BB_WARPS)
+            owner_bfs_kernel<<<rb, 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+        else
+            ring_kernel<0><<<rb, 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[3], g->stream);
         FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 8, g->rq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
@@ -4083,6 +4164,7 @@ extern "C" int fm_grid_set_option(fm_grid *g, const char *name, int64_t value) {
     else if (k == "vote") g->vote_mask = std::max(1, v) - 1;
     else if (k == "pr_kernel") g->pr_kernel = v;
     else if (k == "bfs_bits") g->bfs_bits = v;
+    else if (k == "bfs_owner") g->bfs_owner = v;
     else if (k == "br_cap") { g->br_cap = std::max(1, v); g->br_per_sm = std::max(1, std::min(g->br_occ, g->br_cap)); }
     else if (k == "pr_ring") g->pr_ring = v;
     else if (k == "pr_graph") g->pr_graph = v;

@@ -44,6 +44,8 @@ VARIANTS = {
     "unpacked_no_tma": {"packed": 0, "tma": 0},
     "no_ring_tail": {"ring_tail": 0},
     "ring_tail_every_round": {"ring_tail": 1},
+    "bfs_ring_queue": {"bfs_owner": 0},
+    "bfs_owner_few_warps": {"br_cap": 1},
 }
 
 CASES = [("G", 96, 160, 11), ("G", 257, 130, 12), ("S", 200, 256, 2048), ("G", 31, 33, 13)]
