@@ -1897,7 +1897,7 @@ __device__ __forceinline__ bool halo_cut_bot(const GridDev &g, int r0, int cl) {
 
 // Border changes of one visit: which of the tile's own rows / columns moved (b0 top,
 // b1 bottom, b2 left, b3 right) and whether anything on a border changed at all.
-struct RingChange { int b0, b1, b2, b3, any; };
+struct RingChange { int b0, b1, b2, b3, any; int r0, r1, r2, r3; };   // r*: border row / column reached (BFS)
 
 // One BFS visit (warp per tile), K2: level-synchronous bit-parallel BFS of the tile
 // from its sink arcs and halo distances (from scratch), or an incremental re-visit.
@@ -2061,6 +2061,10 @@ __device__ __forceinline__ RingChange bfs_visit(const GridDev &g, const RingQ &q
     ch.b1 = __any_sync(0xffffffffu, cb);
     ch.b2 = __any_sync(0xffffffffu, cl_);
     ch.b3 = __any_sync(0xffffffffu, cr_);
+    ch.r0 = __shfl_sync(0xffffffffu, seen, 0) != 0;
+    ch.r1 = __shfl_sync(0xffffffffu, seen, last_r) != 0;
+    ch.r2 = __any_sync(0xffffffffu, sl);
+    ch.r3 = __any_sync(0xffffffffu, sr_);
 #ifdef FM_BFS_TIMING
     const long long tD = clock64();
     tm.ld += tB - tA; tm.lvl += tC - tB; tm.wb += tD - tC;
@@ -2118,6 +2122,7 @@ __device__ __forceinline__ RingChange cut_visit(const GridDev &g, int tile, int 
     ch.b2 = __any_sync(0xffffffffu, add & 1u);
     ch.b3 = __any_sync(0xffffffffu, add >> 31);
     ch.any = ch.b0 | ch.b1 | ch.b2 | ch.b3;
+    ch.r0 = ch.r1 = ch.r2 = ch.r3 = 0;
     return ch;
 }
 
@@ -2129,7 +2134,12 @@ __device__ __forceinline__ RingChange cut_visit(const GridDev &g, int tile, int 
 // and its two hottest words (head, tail); the pending count stays: a visit adds the
 // neighbours it is about to mark BEFORE marking them (a marked tile can be taken and
 // finished at once), then removes the ones that were already dirty and itself.  Flags:
-// 0 clean, 1 dirty (relabel_init leaves every tile dirty, pending = ntiles).
+// 0 clean, 1 dirty from the start (relabel_init marks every tile, pending = ntiles), 2
+// marked by a neighbour.  A tile without a sink arc starts clean (its owner clears the
+// initial mark unless a neighbour marked it already): its distances come only through
+// its halos, and a neighbour's FIRST visit marks it whenever their shared border was
+// reached (the border's sink pixels hold their distance 1 from the preparation, so
+// "changed" alone would never fire for them).
 __device__ __forceinline__ int exch_acq_rel(int32_t *p, int v) {
     int old;
     asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -2146,6 +2156,15 @@ __global__ void __launch_bounds__(32 * BB_WARPS) owner_bfs_kernel(GridDev g, Rin
     uint32_t vis0 = 0, vis1 = 0;   // owned tile i visited in this launch (incremental re-visits)
     unsigned chg_count = 0, nvis = 0;
     long long busy = 0;
+    {
+        int skipped = 0;
+        for (int i = 0; i < nown; i++) {
+            const int tile = gw + i * nw;
+            if (__any_sync(0xffffffffu, g.rbits[(size_t)tile * 160 + 128 + lane] != 0u)) continue;
+            if (lane == 0 && atomicCAS(q.flag + tile, 1, 0) == 1) skipped++;
+        }
+        if (lane == 0 && skipped) atomicSub(q.pend, (unsigned)skipped);
+    }
     unsigned ns = q.ns0;
     for (;;) {
         const int32_t f0 = lane < nown ? *(volatile int32_t *)(q.flag + gw + lane * nw) : 0;
@@ -2176,14 +2195,15 @@ __global__ void __launch_bounds__(32 * BB_WARPS) owner_bfs_kernel(GridDev g, Rin
             chg_count += ch.any ? 1u : 0u;
             const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
             int nt = -1;
-            if (lane == 0 && ch.b0 && tyi > 0) nt = tile - g.ntx;
-            if (lane == 1 && ch.b1 && tyi + 1 < g.nty) nt = tile + g.ntx;
-            if (lane == 2 && ch.b2 && txi > 0) nt = tile - 1;
-            if (lane == 3 && ch.b3 && txi + 1 < g.ntx) nt = tile + 1;
+            const bool first = !vis;
+            if (lane == 0 && (ch.b0 || (first && ch.r0)) && tyi > 0) nt = tile - g.ntx;
+            if (lane == 1 && (ch.b1 || (first && ch.r1)) && tyi + 1 < g.nty) nt = tile + g.ntx;
+            if (lane == 2 && (ch.b2 || (first && ch.r2)) && txi > 0) nt = tile - 1;
+            if (lane == 3 && (ch.b3 || (first && ch.r3)) && txi + 1 < g.ntx) nt = tile + 1;
             const int k = __popc(__ballot_sync(0xffffffffu, nt >= 0));
             if (lane == 0 && k) atomicAdd(q.pend, (unsigned)k);   // counted before they can be taken
             __syncwarp();   // the warp's dist stores (and the count) precede the release exchanges
-            const bool fresh = nt >= 0 && exch_acq_rel(q.flag + nt, 1) == 0;
+            const bool fresh = nt >= 0 && exch_acq_rel(q.flag + nt, 2) == 0;
             const int nfresh = __popc(__ballot_sync(0xffffffffu, fresh));
             if (lane == 0) atomicAdd(q.pend, (unsigned)(nfresh - k - 1));   // this tile done
             __syncwarp();
