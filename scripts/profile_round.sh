@@ -8,8 +8,8 @@
 #     every 2 launches), and the bench launch list profiles each round graph as one entry
 #     (--graph-profiling graph).
 #  2. ncu --set full (source level) of the push kernel (an early, dense launch and a
-#     mid-solve one), the two ring launches (global-relabel BFS, min-cut reach) and the
-#     assignment kernels at n = 4096
+#     mid-solve one), the global-relabel BFS (owner_bfs_kernel) and its preparation pass,
+#     the min-cut reach ring and the assignment kernels at n = 4096
 #  3. the bench's launch list
 mkdir -p gpurun_out
 P=${P:-r02}
@@ -19,7 +19,8 @@ REPS=1 timeout 600 ncu --metrics $M --clock-control none --csv --log-file gpurun
 F="ncu --set full --import-source on --clock-control none"
 REPS=1 timeout 600 $F -k regex:pr_list_kernel -s 0 -c 1 -o gpurun_out/${P}_pr_list_early -f python scripts/grid_trace.py 4096 G trace=0 pr_graph=0 pr_batch=2 > /dev/null 2>&1
 REPS=1 timeout 600 $F -k regex:pr_list_kernel -s 40 -c 1 -o gpurun_out/${P}_pr_list_mid -f python scripts/grid_trace.py 4096 G trace=0 pr_graph=0 pr_batch=2 > /dev/null 2>&1
-REPS=1 timeout 600 $F --kernel-name-base demangled -k "regex:ring_kernel<.int.0>" -s 3 -c 1 -o gpurun_out/${P}_ring_bfs -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
+REPS=1 timeout 600 $F -k regex:owner_bfs_kernel -s 3 -c 1 -o gpurun_out/${P}_owner_bfs -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
+REPS=1 timeout 600 $F -k regex:relabel_init_kernel -s 3 -c 1 -o gpurun_out/${P}_relabel_init -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
 REPS=1 timeout 600 $F --kernel-name-base demangled -k "regex:ring_kernel<.int.1>" -s 0 -c 1 -o gpurun_out/${P}_ring_cut -f python scripts/grid_trace.py 4096 G trace=0 > /dev/null 2>&1
 REPS=1 timeout 600 $F -k regex:refine_rounds_kernel -s 2 -c 1 -o gpurun_out/${P}_assign_rounds -f python scripts/assign_one.py 4096 M10000 > /dev/null 2>&1
 REPS=1 timeout 600 $F -k regex:price_update_kernel -s 2 -c 1 -o gpurun_out/${P}_assign_pu -f python scripts/assign_one.py 4096 M10000 > /dev/null 2>&1
