@@ -202,26 +202,31 @@ __device__ __forceinline__ void two_hop_pixel(const GridDev &g, int32_t r, int32
     // band mode: routes stay inside the band (arcs to a neighbour band are left alone)
     const bool ok[4] = {c + 1 < g.W, c > 0, r + 1 < g.H, r > 0};
     const int64_t qs[4] = {p + 1, p - 1, p + g.W, p - g.W};
-    // every operand first (one round trip), then a compare-and-swap only where a
-    // neighbour has sink capacity left
+    // every operand first (one round trip)
     int32_t rp[4], t[4];
 #pragma unroll
     for (int d = 0; d < 4; d++) {
         rp[d] = ok[d] ? *(volatile int32_t *)(fwd[d] + p) : 0;
         t[d] = ok[d] ? *(volatile int32_t *)(g.rT + qs[d]) : 0;
     }
+    // the excess is split over the directions from the loaded values, and the four sink
+    // reservations go out together (one round trip instead of a CAS chain): each takes
+    // min(want, what rT(q) held) and hands the over-draw back, so no rT(q) is overdrawn
+    // for good and the sum taken from it never exceeds its residual
+    int32_t want[4], old[4];
+    int32_t rem = e;
 #pragma unroll
     for (int d = 0; d < 4; d++) {
-        const int32_t want = min(e, rp[d]);
-        if (want <= 0 || t[d] <= 0) continue;
-        int32_t tv = t[d], take = 0;
-        while (tv > 0) {
-            take = min(want, tv);
-            const int32_t old = atomicCAS(g.rT + qs[d], tv, tv - take);
-            if (old == tv) break;
-            tv = old;
-            take = 0;
-        }
+        want[d] = (rp[d] > 0 && t[d] > 0 && rem > 0) ? min(rem, min(rp[d], t[d])) : 0;
+        rem -= want[d];
+    }
+#pragma unroll
+    for (int d = 0; d < 4; d++) old[d] = want[d] > 0 ? atomicSub(g.rT + qs[d], want[d]) : 0;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        if (want[d] <= 0) continue;
+        const int32_t take = min(want[d], max(old[d], 0));
+        if (take < want[d]) atomicAdd(g.rT + qs[d], want[d] - take);
         if (take <= 0) continue;
         e -= take;
         atomicSub(fwd[d] + p, take);
@@ -268,13 +273,17 @@ __global__ void three_hop_kernel(GridDev g) {
             const int32_t want = min(e, rpq);
             if (want <= 0) break;                                 // p -> q saturated
             if (*(volatile int32_t *)(g.rT + q2) <= 0 || *(volatile int32_t *)(fwd[d2] + q) <= 0) continue;
-            const int32_t a = cas_take(fwd[d2] + q, want);        // reserve q -> q2
+            // every hop reserved by compare-and-swap: r(p -> q) is also the middle hop of
+            // other pixels' paths (x -> p -> q), so the owner may not just subtract
+            const int32_t a0 = cas_take(fwd[d1] + p, want);       // reserve p -> q
+            if (a0 <= 0) break;
+            const int32_t a = cas_take(fwd[d2] + q, a0);          // then q -> q2
+            if (a < a0) atomicAdd(fwd[d1] + p, a0 - a);           // hand back the unused part
             if (a <= 0) continue;
             const int32_t b = cas_take(g.rT + q2, a);             // then q2 -> t
-            if (b < a) atomicAdd(fwd[d2] + q, a - b);             // hand back the unused part
+            if (b < a) { atomicAdd(fwd[d2] + q, a - b); atomicAdd(fwd[d1] + p, a - b); }
             if (b <= 0) continue;
             e -= b;
-            atomicSub(fwd[d1] + p, b);
             atomicAdd(rev[d1] + q, b);
             atomicAdd(rev[d2] + q2, b);
         }
