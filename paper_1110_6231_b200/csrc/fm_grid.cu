@@ -578,7 +578,15 @@ __global__ void __launch_bounds__(PT_W * PT_TY, FM_PT_MINBLOCKS) pr_tile_kernel(
 // RED); the neighbour tile is queued for the next launch once, at the end of the
 // visit (the launch boundary orders the inbox writes before its next load).
 // ----------------------------------------------------------------------------
-constexpr int PL_TY = 8, PL_NT = PT_W * PL_TY, PL_ROWS = PT_H / PL_TY;
+// push-kernel CTA = 32 x PL_TY threads on one 32x32 tile.  4 warps (r02by: push kernel
+// -3% at 4096^2 and 8192^2 against 8 warps): a pass with few listed pixels parks fewer
+// warps at its barrier, and the tile's shared memory, not the thread count, bounds the
+// CTAs per SM.  The border / inbox stage needs one thread per border pixel (4 x 32).
+#ifndef FM_PL_TY
+#define FM_PL_TY 4
+#endif
+constexpr int PL_TY = FM_PL_TY, PL_NT = PT_W * PL_TY, PL_ROWS = PT_H / PL_TY;
+static_assert(PL_NT >= 4 * PT_W, "the border / inbox stage of a tile visit needs 128 threads");
 // heights with a 1-pixel halo, rows padded to 40 words so each interior row starts
 // 16-byte aligned (column c at PL_HC + c; halo columns at PL_HC - 1 and PL_HC + 32)
 constexpr int PL_HS = 40, PL_HC = 4;
@@ -943,8 +951,8 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
                 for (int k = 0; k < 4; k++) tma_load_2d(S.res.r[k], &maps->r[k], c0, r0, &S.mbar);
         }
     }
-    {
-        const int lrow = tid >> 3, ch = tid & 7;
+    for (int u = tid; u < PT_H * (PT_W / 4); u += PL_NT) {   // thread = (row, 4-column chunk)
+        const int lrow = u >> 3, ch = u & 7;
         const int r = r0 + lrow, cb = c0 + 4 * ch;
         const int li = lrow * PT_W + 4 * ch, hi = (lrow + 1) * HS + PL_HC + 4 * ch;
         if (tma) {
