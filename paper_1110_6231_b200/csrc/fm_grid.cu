@@ -3053,6 +3053,7 @@ struct fm_grid {
     int local_margin = 2;                // region dilation in tiles
     int local_streak = 0;
     int pl_occ = 6, pk_occ = 8, br_occ = 8;  // occupancy maxima (options may only lower the CTAs per SM)
+    int bo_occ = 8;                      // owner_bfs_kernel CTAs per SM (occupancy query)
     int k_local = 0;                     // tuning overrides (options k_local / bfs_interval)
     int trace = 0;                       // option TRACE=1: one stderr line per round
     int bfs_interval_env = 0;
@@ -3294,10 +3295,18 @@ int global_relabel(fm_grid *g) {
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[2], g->stream);
         const int rb = ring_blocks(g);
-        if (g->bfs_owner && g->ntiles <= 64 * rb * BB_WARPS)
-            owner_bfs_kernel<<<rb, 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
-        else
-            ring_kernel<0><<<rb, 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
+        // owner scheduling needs every owning warp resident at once (a tile is only ever
+        // visited by its owner): a cooperative launch guarantees that or refuses, and a
+        // refusal (e.g. the device shared with other work) falls back to the ring queue
+        const int ob = g->sms * std::max(1, std::min(g->bo_occ, g->br_cap));
+        bool launched = false;
+        if (g->bfs_owner && g->ntiles <= 64 * ob * BB_WARPS) {
+            void *args[] = {(void *)&g->d, (void *)&g->rq};
+            launched = cudaLaunchCooperativeKernel((void *)owner_bfs_kernel, dim3(ob), dim3(32 * BB_WARPS), args, 0,
+                                                   g->stream) == cudaSuccess;
+            if (!launched) cudaGetLastError();
+        }
+        if (!launched) ring_kernel<0><<<rb, 32 * BB_WARPS, 0, g->stream>>>(g->d, g->rq);
         FM_CHECK_LAUNCH();
         cudaEventRecord(g->ev[3], g->stream);
         FM_CHECK_CUDA(cudaMemcpyAsync(g->h_flags + 8, g->rq.ctr + 96, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
@@ -3931,6 +3940,8 @@ extern "C" int fm_grid_create(int32_t H, int32_t W, int32_t device, fm_grid **ou
     g->bb_per_sm = std::max(1, g->bb_per_sm);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->br_occ, ring_kernel<0>, 32 * BB_WARPS, 0);
     g->br_occ = std::max(1, g->br_occ);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g->bo_occ, owner_bfs_kernel, 32 * BB_WARPS, 0);
+    g->bo_occ = std::max(1, g->bo_occ);
     g->br_per_sm = std::max(1, std::min(g->br_occ, g->br_cap));
     g->pl_occ = g->pl_per_sm; g->pk_occ = g->pk_per_sm;
     // ring capacity: every tile once + one reserved slot per warp that can be resident
