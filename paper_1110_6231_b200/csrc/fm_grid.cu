@@ -2173,6 +2173,10 @@ __global__ void __launch_bounds__(32 * BB_WARPS) owner_bfs_kernel(GridDev g, Rin
     uint32_t vis0 = 0, vis1 = 0;   // owned tile i visited in this launch (incremental re-visits)
     unsigned chg_count = 0, nvis = 0;
     long long busy = 0;
+#ifdef FM_BFS_TIMING
+    BfsTm tm;
+    int lv = 0;
+#endif
     {
         int skipped = 0;
         for (int i = 0; i < nown; i++) {
@@ -2205,7 +2209,11 @@ __global__ void __launch_bounds__(32 * BB_WARPS) owner_bfs_kernel(GridDev g, Rin
             if (!took) continue;
             const bool vis = i < 32 ? ((vis0 >> i) & 1u) : ((vis1 >> (i - 32)) & 1u);
             const long long tv0 = clock64();
+#ifdef FM_BFS_TIMING
+            const RingChange ch = bfs_visit(g, q, tile, vis, sd, lane, lv, tm);
+#else
             const RingChange ch = bfs_visit(g, q, tile, vis, sd, lane);
+#endif
             busy += clock64() - tv0;
             nvis++;
             if (i < 32) vis0 |= 1u << i; else vis1 |= 1u << (i - 32);
@@ -2230,6 +2238,12 @@ __global__ void __launch_bounds__(32 * BB_WARPS) owner_bfs_kernel(GridDev g, Rin
     if (lane == 0 && nvis) {   // visits and the cycles spent inside them (trace statistics)
         atomicAdd(q.ctr + 192, nvis);
         atomicAdd((unsigned long long *)(q.ctr + 240), (unsigned long long)busy);
+#ifdef FM_BFS_TIMING
+        unsigned long long *t = (unsigned long long *)(q.ctr + 208);
+        atomicAdd(t + 1, (unsigned long long)tm.ld); atomicAdd(t + 2, (unsigned long long)tm.lvl);
+        atomicAdd(t + 3, (unsigned long long)tm.wb);
+        atomicAdd((unsigned long long *)(q.ctr + 244), (unsigned long long)lv);
+#endif
     }
 }
 
