@@ -156,3 +156,18 @@ def test_packed_residual_boundary(hi):
     want = oracle.grid_maxflow(*caps, solver="seq")
     rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
     assert rep.objective == want["value"] and (rep.cut == want["cut"]).all()
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_whole_tile_grids_vs_oracle(seed):
+    """Whole-tile shapes (H % 32 == 0, W % 128 == 0) take the vectorised relabel
+    preparation, the inbox fold and the vectorised cut seeding; sparse sink / source
+    arcs make long BFS distances and tail rounds (owner BFS, ring tail)."""
+    rng = np.random.default_rng(5000 + seed)
+    H, W = 32 * int(rng.integers(1, 5)), 128 * int(rng.integers(1, 3))
+    hi = int(rng.choice([1, 7, 100, 40000]))
+    caps = _random_caps(rng, H, W, hi, float(rng.uniform(0.01, 0.5)), float(rng.uniform(0.01, 0.5)))
+    want = oracle.grid_maxflow(*caps, solver="seq")
+    rep = fmb.hybrid_solve(fmb.build_grid_network(*caps))
+    assert rep.objective == want["value"]
+    assert (rep.cut == want["cut"]).all()

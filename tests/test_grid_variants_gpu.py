@@ -48,7 +48,10 @@ VARIANTS = {
     "bfs_owner_few_warps": {"br_cap": 1},
 }
 
-CASES = [("G", 96, 160, 11), ("G", 257, 130, 12), ("S", 200, 256, 2048), ("G", 31, 33, 13)]
+# the last two are whole-tile grids (H % 32 == 0, W % 128 == 0): the vectorised relabel
+# preparation / cut seeding and the inbox fold take their fast paths there
+CASES = [("G", 96, 160, 11), ("G", 257, 130, 12), ("S", 200, 256, 2048), ("G", 31, 33, 13),
+         ("G", 64, 256, 14), ("S", 128, 384, 2048)]
 
 
 @pytest.fixture(scope="module")
