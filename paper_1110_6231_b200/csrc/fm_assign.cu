@@ -862,7 +862,111 @@ __device__ __forceinline__ void pu_scan_y(const AssignDev &a, const PuDev &f, in
     }
 }
 
-__global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuDev f) {
+// the x of one 4-x group whose bit is set in mask4 (their l(x) may drop): load their
+// matches and prices, relax x -> y into l(x) and, where it dropped, x's matched
+// reverse arc into its Y
+template <typename Push>
+__device__ __forceinline__ void pu_relax4(const AssignDev &a, const PuDev &f, int y, int lyv, long long pyv,
+                                          long long cap, double inv_eps, int xb, uint32_t mask4,
+                                          const int (&wv)[4], const int (&lxv)[4], Push push) {
+    const int4 m4 = __ldca((const int4 *)(a.match + xb));
+    const longlong2 pa = __ldca((const longlong2 *)(a.px + xb)), pb = __ldca((const longlong2 *)(a.px + xb) + 1);
+    const int mxv[4] = {m4.x, m4.y, m4.z, m4.w};
+    const long long pxv[4] = {pa.x, pa.y, pb.x, pb.y};
+    int cand[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        cand[k] = LINF;
+        if (!((mask4 >> k) & 1u) || mxv[k] == y) continue;
+        const long long rc = -(long long)wv[k] * a.scale + pxv[k] - pyv;
+        long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
+        if (len < 0) len = 0;
+        const long long c1 = (long long)lyv + len;
+        if (c1 <= cap && c1 < lxv[k]) cand[k] = (int)c1;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+        if (cand[k] < LINF) atomicMin(a.lx + xb + k, cand[k]);   // fire-and-forget (RED)
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        if (cand[k] >= LINF || mxv[k] < 0) continue;
+        const int x = xb + k;
+        if (__ldca(a.frozen + x)) continue;
+        const long long rc2 = (long long)__ldca(a.mw + x) * a.scale - pxv[k] + __ldca((const long long *)a.pmx + x);
+        long long len2 = floordiv_eps(rc2, a.eps, inv_eps) + 1;
+        if (len2 < 0) len2 = 0;
+        const long long cand2 = cand[k] + len2;
+        if (cand2 > cap) continue;
+        const int mx = mxv[k];
+        const int old2 = atomicMin(a.ly + mx, (int)cand2);
+        if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0) push(mx);
+    }
+}
+
+// pu_scan_y with a cheap filter first: a chunk's weights and labels are loaded alone
+// and only the x whose label could still drop (l(y) < l(x), arc present and not
+// fixed) load their matches and prices; the matched reverse arc's operands are read
+// only for the x whose label did drop.  After the first waves nearly every l(x) is
+// already at or below l(y), so most chunks cost two vector loads and no arithmetic
+// (and the kernel fits 2 CTAs per SM).  Loading a second chunk up front spilled and
+// measured slower (r02h4).
+template <typename Push>
+__device__ __forceinline__ void pu_scan_y_filtered(const AssignDev &a, const PuDev &f, int y, int lyv,
+                                                   long long pyv, long long cap, double inv_eps, int gt,
+                                                   int PU_GT, Push push) {
+    const int n = a.n;
+    const int32_t *col = f.wt + (size_t)y * n;
+    const int nv8 = (n & 7) ? 0 : n;
+    for (int x0 = gt * 8; x0 < nv8; x0 += PU_GT * 8) {
+        const int4 w0 = __ldg((const int4 *)(col + x0)), w1 = __ldg((const int4 *)(col + x0 + 4));
+        const int4 l0 = __ldcg((const int4 *)(a.lx + x0)), l1 = __ldcg((const int4 *)(a.lx + x0 + 4));
+        uint32_t fb = 0;
+        if (a.use_fix) fb = (__ldg(a.fixed_t + (size_t)y * a.nw + (x0 >> 5)) >> (x0 & 31)) & 0xffu;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int4 wq = h ? w1 : w0, lq = h ? l1 : l0;
+            const int wv[4] = {wq.x, wq.y, wq.z, wq.w};
+            const int lxv[4] = {lq.x, lq.y, lq.z, lq.w};
+            uint32_t m4 = 0;
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+                if (wv[k] != FM_ABSENT_WEIGHT && lyv < lxv[k] && !((fb >> (4 * h + k)) & 1u)) m4 |= 1u << k;
+            if (m4) pu_relax4(a, f, y, lyv, pyv, cap, inv_eps, x0 + 4 * h, m4, wv, lxv, push);
+        }
+    }
+    for (int x = nv8 + gt; x < n; x += PU_GT) {
+        const int wv = __ldg(col + x);
+        if (wv == FM_ABSENT_WEIGHT) continue;
+        const int lxv = __ldcg(a.lx + x);
+        if (lyv >= lxv) continue;
+        const int mx = __ldcg(a.match + x);
+        if (mx == y) continue;
+        if (a.use_fix && ((__ldg(a.fixed_t + (size_t)y * a.nw + (x >> 5)) >> (x & 31)) & 1u)) continue;
+        const long long px = __ldcg((const long long *)a.px + x);
+        const long long rc = -(long long)wv * a.scale + px - pyv;
+        long long len = floordiv_eps(rc, a.eps, inv_eps) + 1;
+        if (len < 0) len = 0;
+        const long long cand = (long long)lyv + len;
+        if (cand > cap || cand >= lxv) continue;
+        const int old = atomicMin(a.lx + x, (int)cand);
+        if ((int)cand >= old || mx < 0 || __ldcg(a.frozen + x)) continue;
+        const long long rc2 = (long long)__ldg(a.w + (size_t)x * n + mx) * a.scale - px +
+                              __ldcg((const long long *)a.py + mx);
+        long long len2 = floordiv_eps(rc2, a.eps, inv_eps) + 1;
+        if (len2 < 0) len2 = 0;
+        const long long cand2 = cand + len2;
+        if (cand2 > cap) continue;
+        const int old2 = atomicMin(a.ly + mx, (int)cand2);
+        if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0) push(mx);
+    }
+}
+
+// FILTER: the filtered column scan at 2 CTAs per SM (option pu_filter)
+template <bool FILTER>
+#ifndef FM_PU_MINB
+#define FM_PU_MINB 2
+#endif
+__global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_update_kernel(AssignDev a, PuDev f) {
     cg::grid_group grid = cg::this_grid();
     const int n = a.n;
     const int tid = blockIdx.x * ATHREADS + threadIdx.x, nthr = gridDim.x * ATHREADS;
@@ -948,14 +1052,16 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
             group_sync(grp, PU_GT);
             const int y = s_y[grp];
             if (y < 0) break;
-            pu_scan_y(a, f, y, s_ly[grp], s_py[grp], cap, inv_eps, gt, PU_GT, [&](int mx) {
+            const auto ring_push = [&](int mx) {
                 atomicAdd(f.rctr + 64, 1u);
                 if (f.local_next && atomicCAS(&s_next[grp], -1, mx) == -1) return;   // the group's next Y
                 const unsigned t = atomicAdd(f.rctr + 32, 1u);
                 fence_acq_rel_gpu();         // labels (and pending) visible before the entry
                 int32_t *slot = f.ring + t % (unsigned)f.ring_cap;
                 while (atomicCAS(slot, -1, mx) != -1) __nanosleep(64);
-            });
+            };
+            if (FILTER) pu_scan_y_filtered(a, f, y, s_ly[grp], s_py[grp], cap, inv_eps, gt, PU_GT, ring_push);
+            else pu_scan_y(a, f, y, s_ly[grp], s_py[grp], cap, inv_eps, gt, PU_GT, ring_push);
             group_sync(grp, PU_GT);
             if (gt == 0) { fence_acq_rel_gpu(); atomicSub(f.rctr + 64, 1u); }
         }
@@ -1003,9 +1109,11 @@ __global__ void __launch_bounds__(ATHREADS) price_update_kernel(AssignDev a, PuD
             const int y = s_y[grp];
             const int lyv = s_ly[grp];
             const long long pyv = s_py[grp];
-            pu_scan_y(a, f, y, lyv, pyv, cap, inv_eps, gt, PU_GT, [&](int mx) {
+            const auto wave_push = [&](int mx) {
                 f.fy[nb][atomicAdd(f.cnt + (it + 1) % 3, 1)] = mx;   // read after the grid barrier
-            });
+            };
+            if (FILTER) pu_scan_y_filtered(a, f, y, lyv, pyv, cap, inv_eps, gt, PU_GT, wave_push);
+            else pu_scan_y(a, f, y, lyv, pyv, cap, inv_eps, gt, PU_GT, wave_push);
             group_sync(grp, PU_GT);
         }
         grid.sync();
@@ -1279,6 +1387,7 @@ struct fm_assign {
     unsigned long long *h_acc = nullptr;
     cudaStream_t own_stream = nullptr, stream = nullptr;
     int coop_blocks = 0, pu_blocks = 0, sms = 0;
+    int pu_blocks_k[2] = {0, 0};     // price_update_kernel<false / true> cooperative grid sizes
     PuDev pu{};
     int32_t *wt = nullptr;
     cudaEvent_t ev[4] = {};
@@ -1291,7 +1400,8 @@ struct fm_assign {
     int opt_cta_x = 4, opt_cta_y = 4;
     int opt_trace = 0;               // price-update statistics line on stderr after each solve
     int opt_pu_local = 0;            // price update: work-first continuation of a group's first re-queued Y
-    int opt_pu_groups = PU_GROUPS;   // r02an: Y phase 4x grid CTA-wide ops -> n=4096 optical 18.9 -> 15.3 ms
+    int opt_pu_groups = 2;           // r02h3: with the filtered scan 2 groups per CTA beat 4 (M10000 47.4 -> 44.4 ms)
+    int opt_pu_filter = 1;           // price update: filtered column scans at 2 CTAs per SM
     int32_t flags = 0;
     fm_stats st{};
 };
@@ -1373,6 +1483,14 @@ int assign_status(int why) {
     }
 }
 
+// one price_update_heuristic launch (cooperative) on the solver's stream
+cudaError_t launch_price_update(fm_assign *A) {
+    void *pargs[] = {(void *)&A->d, (void *)&A->pu};
+    const bool filt = A->opt_pu_filter != 0;
+    return cudaLaunchCooperativeKernel(filt ? (void *)price_update_kernel<true> : (void *)price_update_kernel<false>,
+                                       dim3(A->pu_blocks_k[filt ? 1 : 0]), dim3(ATHREADS), pargs, 0, A->stream);
+}
+
 // one refine (assign_scaling.py:145-182 + assign_par.py:115-237): eps <- max(1, ceil(eps/alpha)),
 // begin_refine fused with the first X phase, lock-free rounds with price updates, arc fixing
 int assign_one_refine(fm_assign *A) {
@@ -1407,10 +1525,8 @@ int assign_one_refine(fm_assign *A) {
             A->pu_pending = false;
         }
         if (A->h_cnt[C_INFEASIBLE] || A->h_cnt[C_EXIT] != 1) break;
-        void *pargs[] = {(void *)&d, (void *)&A->pu};
         cudaEventRecord(A->ev[0], s);
-        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->pu_blocks),
-                                                  dim3(ATHREADS), pargs, 0, s));
+        FM_CHECK_CUDA(launch_price_update(A));
         cudaEventRecord(A->ev[1], s);
         A->st.launches++;
         A->pu_pending = true;
@@ -1557,9 +1673,13 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
     int per_sm = 0;
     int per_sm2 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_rounds_kernel, ATHREADS, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, price_update_kernel, ATHREADS, 0);
+    int per_sm3 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, price_update_kernel<false>, ATHREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm3, price_update_kernel<true>, ATHREADS, 0);
     A->coop_blocks = std::max(1, std::min(per_sm, 2) * A->sms);
-    A->pu_blocks = std::max(1, std::min(per_sm2, 2) * A->sms);
+    A->pu_blocks_k[0] = std::max(1, std::min(per_sm2, 2) * A->sms);
+    A->pu_blocks_k[1] = std::max(1, std::min(per_sm3, 2) * A->sms);
+    A->pu_blocks = std::max(A->pu_blocks_k[0], A->pu_blocks_k[1]);   // sizes the ring
     *out = A;
     return FM_OK;
 }
@@ -1788,9 +1908,7 @@ extern "C" int fm_assign_round(fm_assign *A, int32_t cycle_budget, int64_t *out)
         FM_TRY(assign_sync_cnt(A));
         rc = assign_status(A->h_cnt[C_INFEASIBLE]);
         if (rc != FM_OK || A->h_cnt[C_EXIT] != 1) break;
-        void *pargs[] = {(void *)&d, (void *)&A->pu};
-        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->pu_blocks),
-                                                  dim3(ATHREADS), pargs, 0, s));
+        FM_CHECK_CUDA(launch_price_update(A));
         A->st.launches++;
         FM_TRY(assign_sync_cnt(A));
         rc = assign_status(A->h_cnt[C_INFEASIBLE]);
@@ -1822,9 +1940,7 @@ extern "C" int fm_assign_price_update(fm_assign *A) {
     A->st.launches++;
     FM_TRY(assign_sync_cnt(A));
     if (A->h_cnt[C_X0] + A->h_cnt[C_Y0] == 0) return FM_OK;
-    void *pargs[] = {(void *)&d, (void *)&A->pu};
-    FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)price_update_kernel, dim3(A->pu_blocks), dim3(ATHREADS),
-                                              pargs, 0, s));
+    FM_CHECK_CUDA(launch_price_update(A));
     A->st.launches++;
     FM_TRY(assign_sync_cnt(A));
     return assign_status(A->h_cnt[C_INFEASIBLE]);
@@ -1889,6 +2005,7 @@ extern "C" int fm_assign_set_option(fm_assign *A, const char *name, int64_t valu
     else if (!strcmp(name, "cta_y")) A->opt_cta_y = std::max(1, v);
     else if (!strcmp(name, "pu_ring")) A->opt_pu_ring = v;
     else if (!strcmp(name, "pu_local")) A->opt_pu_local = v;
+    else if (!strcmp(name, "pu_filter")) A->opt_pu_filter = v;
     else if (!strcmp(name, "trace")) A->opt_trace = v;
     else if (!strcmp(name, "pu_threshold")) A->opt_pu_threshold = v;
     else if (!strcmp(name, "tail_threshold")) A->opt_tail_threshold = v;

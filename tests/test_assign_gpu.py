@@ -202,16 +202,18 @@ def test_y_batch_threshold_variants(ybatch_min):
         assert obj == int(w[r, c].sum()) and _is_perm(m, n) and _objective(w, m) == obj
 
 
+@pytest.mark.parametrize("filt", [0, 1])
 @pytest.mark.parametrize("ring", [0, 1])
-def test_price_update_barrier_and_queue_variants(ring):
+def test_price_update_barrier_and_queue_variants(ring, filt):
     """The price update's label relaxation runs either as barrier-separated waves or
-    queue-driven without barriers (option pu_ring); both reach the same
+    queue-driven without barriers (option pu_ring), with the full or the filtered
+    column scan (option pu_filter); all reach the same
     labels (a fixpoint of min-updates over path lengths), so the optimum and the
     epsilon-optimality certificate hold either way, including sparse instances."""
     from scipy.optimize import linear_sum_assignment
     for n, M in ((1, 5), (7, 3), (64, 10000), (333, 100), (1024, 10000)):
         w = G.assignment_reference(n, M, n + 7)
-        solver = fmb.AssignmentSolver(n, options={"pu_ring": ring})
+        solver = fmb.AssignmentSolver(n, options={"pu_ring": ring, "pu_filter": filt})
         try:
             obj, m, prices, _ = solver.solve_host(w, want_prices=True)
         finally:
@@ -228,7 +230,7 @@ def test_price_update_barrier_and_queue_variants(ring):
     w = np.where(keep, w, -(2**31)).astype(np.int32)
     cost = np.where(w == -(2**31), -1e15, w.astype(np.float64))
     r, c = linear_sum_assignment(cost, maximize=True)
-    solver = fmb.AssignmentSolver(n, options={"pu_ring": ring})
+    solver = fmb.AssignmentSolver(n, options={"pu_ring": ring, "pu_filter": filt})
     try:
         obj, m, _, _ = solver.solve_host(w)
     finally:
