@@ -470,11 +470,27 @@ def main():
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
             assert rep.objective == flow
-        tt = statistics.mean(times)
+        t_single = statistics.mean(times)
+        # the same K steps as ONE pipelined call (a stream of images): each step still
+        # copies its six planes in and its cut out, overlapped with the previous /
+        # next step's solve
+        nets = [net] * args.steps
+        fmb.hybrid_solve_batch(nets[:2])  # warm (second input set, cut stages, copy streams)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = fmb.hybrid_solve_batch(nets)
+        torch.cuda.synchronize()
+        tt = (time.perf_counter() - t0) / args.steps
+        assert all(r.objective == flow and r.cut is not None for r in reps)
         e2e = {"value": round(e_grid(S, S) / tt / 1e6, 3), "unit": UNIT,
                "h2d_bytes_per_step": 6 * 4 * HW, "d2h_bytes_per_step": HW + 8,
                "ms_per_step": round(1000 * tt, 3),
-               "api": "paper_1110_6231_b200.hybrid_solve(build_grid_network(*pinned host planes))"}
+               "api": f"paper_1110_6231_b200.hybrid_solve_batch([build_grid_network(*pinned host planes)] x {args.steps}): "
+                      "one call, step k+1's H2D and step k-1's cut D2H overlap step k's solve",
+               "single_call": {"value": round(e_grid(S, S) / t_single / 1e6, 3), "unit": UNIT,
+                               "ms_per_step": round(1000 * t_single, 3),
+                               "api": "paper_1110_6231_b200.hybrid_solve(build_grid_network(*pinned host planes)), "
+                                      "one synchronous call per step"}}
 
     # the other grid config of BASELINE.json on one GPU: 2048^2 segmentation (config 2)
     seg = None

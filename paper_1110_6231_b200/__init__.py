@@ -54,7 +54,7 @@ from .graph import (
     part_reduced_cost,
     reduced_cost,
 )
-from .maxflow import DEFAULT_CYCLE_BUDGET, GridSolver, hybrid_solve, min_cut
+from .maxflow import DEFAULT_CYCLE_BUDGET, GridSolver, hybrid_solve, hybrid_solve_batch, min_cut
 
 __version__ = "0.1.0"
 
@@ -99,6 +99,7 @@ __all__ = [
     "serialize_network",
     "generators",
     "hybrid_solve",
+    "hybrid_solve_batch",
     "min_cut",
     "solve_assignment",
     "__version__",

@@ -61,7 +61,8 @@ constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXE
               O_PU_YS = 14, O_PU_ITNS = 15,  // price update: frontier Y visits, ns in BF iterations (CTA 0)
               O_PU_LASTSUM = 16, O_PU_YFIN = 17, O_PU_YLAB = 18,  // price update: sum of last, Y with l <= last, Y labelled
               O_PU_SCANNS = 19,                                    // price update: ns in Y scans (summed over groups)
-              O_COUNT = 24;
+              O_HIST = 20,   // [20..24]: grid-wide rounds by max(|Y list|, |X list|): <= 8, 32, 148, 592, more
+              O_COUNT = 28;
 
 // validate=True failures (assign_par.py:101-106,200-214; assign_scaling.py:274-275,333-336)
 constexpr int V_RELABEL = 4;             // a relabel failed to lower a price
@@ -703,7 +704,11 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
                 for (int i = gwarp; i < nx; i += gwarps)
                     x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
             }
-            if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_X, t1 - t0); t0 = t1; }
+            if (timer) {
+                t1 = globaltimer(); atomicAdd(a.ops + O_PH_X, t1 - t0); t0 = t1;
+                const int m = max(ny, nx);
+                atomicAdd(a.ops + O_HIST + (m <= 8 ? 0 : m <= 32 ? 1 : m <= 148 ? 2 : m <= 592 ? 3 : 4), 1ull);
+            }
             grid.sync();
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC2, t1 - t0); }
         }
@@ -1584,6 +1589,10 @@ int assign_finish(fm_assign *A, int rc, int64_t *objective_out, int32_t *match_o
                 1e-3 * A->h_ops[O_PU_ITNS] / npu, A->h_ops[O_PU_LASTSUM] / npu, A->h_ops[O_PU_YFIN] / npu,
                 A->h_ops[O_PU_YLAB] / npu, 1e-3 * A->h_ops[O_PU_SCANNS] / std::max(1.0, (double)A->h_ops[O_PU_YS]));
     }
+    if (A->opt_trace)
+        fprintf(stderr, "[fm_assign] grid rounds by max list size: <=8 %llu, <=32 %llu, <=148 %llu, <=592 %llu, more %llu; "
+                "tail rounds %llu\n", A->h_ops[O_HIST], A->h_ops[O_HIST + 1], A->h_ops[O_HIST + 2], A->h_ops[O_HIST + 3],
+                A->h_ops[O_HIST + 4], A->h_ops[O_TAIL_ROUNDS]);
     A->st.reserved[3] = (int64_t)A->h_ops[O_TAIL_OPS];   // ops done by the single-CTA tail
     A->st.ms_cut = 1e-6 * (double)A->h_ops[O_TAIL_NS];   // time in single-CTA tail rounds
     A->st.ms_d2h = 1e-6 * (double)A->h_ops[O_MULTI_NS];  // time in grid-wide rounds

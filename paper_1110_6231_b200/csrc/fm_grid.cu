@@ -1211,6 +1211,11 @@ struct PrCtl {
     unsigned long long tiles;
 };
 
+// the round's control block written by a one-thread kernel (its value travels as a
+// launch argument): an H2D memcpy would queue on the copy engine behind a batch
+// solve's 400 MB plane transfer (fm_grid_solve_host_batch)
+__global__ void prctl_set_kernel(PrCtl *dst, PrCtl v) { *dst = v; }
+
 #ifndef FM_PK_MINBLOCKS
 #define FM_PK_MINBLOCKS 8
 #endif
@@ -3014,6 +3019,12 @@ struct fm_grid {
     int32_t *in_caps = nullptr;          // 6 * HW
     uint8_t *d_cut_tmp = nullptr;
     uint8_t *h_cut_stage = nullptr;      // pinned bounce buffer for the cut (host-output calls)
+    // fm_grid_solve_host_batch: a second input set, two device / pinned cut stages and
+    // the copy streams (H2D of instance k+1 and D2H of instance k-1 overlap solve k)
+    int32_t *in_caps2 = nullptr;
+    uint8_t *b_dcut[2] = {nullptr, nullptr};
+    uint8_t *b_hcut[2] = {nullptr, nullptr};
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[8] = {};   // [0..3] phase / kernel timing, [4..7] a push round whose stats are read after the relabel
@@ -3611,7 +3622,8 @@ int run_round_tiles(fm_grid *g, int32_t cycle_budget, int32_t bfs_interval, int3
         h->cap = cap;
         h->batch = std::max(1, batch_auto);
         h->budget = relabel_budget;
-        FM_CHECK_CUDA(cudaMemcpyAsync(pr_ctl_dev(g), h, sizeof(PrCtl), cudaMemcpyHostToDevice, g->stream));
+        prctl_set_kernel<<<1, 1, 0, g->stream>>>(pr_ctl_dev(g), *h);
+        FM_CHECK_LAUNCH();
         FM_TRY(tq_arm(g, g->d.pq, g->pq_parity));
         cudaEventRecord(g->ev[6], g->stream);
         FM_CHECK_CUDA(cudaGraphLaunch(g->prg_exec, g->stream));
@@ -4006,6 +4018,13 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->h_acc) cudaFreeHost(g->h_acc);
     if (g->h_flags) cudaFreeHost(g->h_flags);
     if (g->h_cut_stage) cudaFreeHost(g->h_cut_stage);
+    if (g->in_caps2) cudaFree(g->in_caps2);
+    for (int k = 0; k < 2; k++) {
+        if (g->b_dcut[k]) cudaFree(g->b_dcut[k]);
+        if (g->b_hcut[k]) cudaFreeHost(g->b_hcut[k]);
+    }
+    if (g->h2d_stream) cudaStreamDestroy(g->h2d_stream);
+    if (g->d2h_stream) cudaStreamDestroy(g->d2h_stream);
     if (g->prg_exec) cudaGraphExecDestroy(g->prg_exec);
     if (g->prg) cudaGraphDestroy(g->prg);
     for (auto e : g->ev) if (e) cudaEventDestroy(e);
@@ -4133,6 +4152,119 @@ extern "C" int fm_grid_solve_host(fm_grid *g, const int32_t *capR, const int32_t
     g->st.ms_h2d = h2d;
     g->st.ms_d2h = d2h;
     if (stats) *stats = g->st;
+    return rc;
+}
+
+// A batch of independent same-shape instances from HOST planes, pipelined: the H2D of
+// instance k+1 (copy stream, second input set) and the D2H of instance k-1's cut (a
+// second copy stream through pinned stages, then host threads into the caller's
+// arrays) run while instance k solves, so a stream of images costs
+// max(solve, PCIe) per image instead of their sum.  Every instance's copies are still
+// made (nothing cached across instances); results are those of fm_grid_solve_host.
+extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const int32_t *const *caps,
+                                        int32_t cycle_budget, int32_t bfs_interval, int32_t flags,
+                                        int64_t *flows_out, uint8_t *const *cuts_out, fm_stats *stats) {
+    if (!g || count < 0 || (count > 0 && (!caps || !flows_out)) || cycle_budget < 1) {
+        fm_set_error("fm_grid_solve_host_batch: invalid argument");
+        return FM_INVALID_ARG;
+    }
+    for (int k = 0; k < 6 * count; k++)
+        if (!caps[k]) { fm_set_error("fm_grid_solve_host_batch: capacity plane %d of instance %d is NULL", k % 6, k / 6);
+                        return FM_INVALID_ARG; }
+    if (count == 0) return FM_OK;
+    FM_CHECK_CUDA(cudaSetDevice(g->device));
+    set_stream(g, nullptr);
+    const size_t HW = (size_t)g->HW;
+    const bool want_cut = cuts_out && !(flags & FM_GRID_NO_CUT);
+    if (!g->in_caps) FM_CHECK_CUDA(cudaMalloc((void **)&g->in_caps, sizeof(int32_t) * 6 * HW));
+    if (count > 1 && !g->in_caps2) FM_CHECK_CUDA(cudaMalloc((void **)&g->in_caps2, sizeof(int32_t) * 6 * HW));
+    if (!g->h2d_stream) FM_CHECK_CUDA(cudaStreamCreateWithFlags(&g->h2d_stream, cudaStreamNonBlocking));
+    if (!g->d2h_stream) FM_CHECK_CUDA(cudaStreamCreateWithFlags(&g->d2h_stream, cudaStreamNonBlocking));
+    if (want_cut)
+        for (int b = 0; b < 2; b++) {
+            if (!g->b_dcut[b]) FM_CHECK_CUDA(cudaMalloc((void **)&g->b_dcut[b], HW));
+            if (!g->b_hcut[b]) FM_CHECK_CUDA(cudaMallocHost((void **)&g->b_hcut[b], HW));
+        }
+    int32_t *inbuf[2] = {g->in_caps, g->in_caps2};
+    std::vector<cudaEvent_t> evs;
+    const auto mkev = [&]() {
+        cudaEvent_t e = nullptr;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        evs.push_back(e);
+        return e;
+    };
+    // H2D of instance k into input set k % 2 (the set of instance k-2, whose solve the
+    // host has already waited for)
+    const auto h2d = [&](int k) -> cudaEvent_t {
+        int32_t *dst = inbuf[k & 1];
+        for (int p = 0; p < 6; p++)
+            if (cudaMemcpyAsync(dst + p * HW, caps[6 * k + p], sizeof(int32_t) * HW, cudaMemcpyHostToDevice,
+                                g->h2d_stream) != cudaSuccess) return nullptr;
+        cudaEvent_t e = mkev();
+        cudaEventRecord(e, g->h2d_stream);
+        return e;
+    };
+    // host copy-out of a cut: NT threads, each a slice, after the D2H event
+    std::thread copier[2];
+    const auto copy_out = [](uint8_t *dst, const uint8_t *src, size_t n, cudaEvent_t done, int dev) {
+        cudaSetDevice(dev);
+        cudaEventSynchronize(done);
+        const int NT = n >= ((size_t)4 << 20) ? 4 : 1;
+        const size_t sl = (n + NT - 1) / NT;
+        std::vector<std::thread> th;
+        for (int j = 1; j < NT; j++)
+            th.emplace_back([=] { const size_t a = std::min(n, j * sl), b = std::min(n, a + sl); memcpy(dst + a, src + a, b - a); });
+        memcpy(dst, src, std::min(n, sl));
+        for (auto &t : th) t.join();
+    };
+    struct Cleanup {
+        std::thread *c;
+        std::vector<cudaEvent_t> &e;
+        ~Cleanup() {
+            for (int b = 0; b < 2; b++) if (c[b].joinable()) c[b].join();
+            for (auto x : e) cudaEventDestroy(x);
+        }
+    } cleanup{copier, evs};
+    int rc = FM_OK;
+    cudaEvent_t ready = h2d(0);
+    if (!ready) { fm_set_error("fm_grid_solve_host_batch: H2D failed"); return FM_CUDA_ERROR; }
+    for (int k = 0; k < count && rc == FM_OK; k++) {
+        cudaEvent_t next = nullptr;
+        if (k + 1 < count && !(next = h2d(k + 1))) { fm_set_error("fm_grid_solve_host_batch: H2D failed"); rc = FM_CUDA_ERROR; break; }
+        FM_CHECK_CUDA(cudaStreamWaitEvent(g->stream, ready, 0));
+        const int32_t *c = inbuf[k & 1];
+        int64_t flow = 0;
+        rc = solve_device(g, c, c + HW, c + 2 * HW, c + 3 * HW, c + 4 * HW, c + 5 * HW, cycle_budget, bfs_interval,
+                          flags, &flow, nullptr);
+        if (rc != FM_OK) break;
+        flows_out[k] = flow;
+        if (stats) stats[k] = g->st;
+        if (want_cut && cuts_out[k]) {
+            const int b = k & 1;
+            if (copier[b].joinable()) copier[b].join();   // stage b is free again
+            // the next solve overwrites d.cut: move it aside on the solve stream, then
+            // D2H from there on the copy stream
+            FM_CHECK_CUDA(cudaMemcpyAsync(g->b_dcut[b], g->d.cut, HW, cudaMemcpyDeviceToDevice, g->stream));
+            cudaEvent_t moved = mkev();
+            cudaEventRecord(moved, g->stream);
+            FM_CHECK_CUDA(cudaStreamWaitEvent(g->d2h_stream, moved, 0));
+            FM_CHECK_CUDA(cudaMemcpyAsync(g->b_hcut[b], g->b_dcut[b], HW, cudaMemcpyDeviceToHost, g->d2h_stream));
+            cudaEvent_t landed = mkev();
+            cudaEventRecord(landed, g->d2h_stream);
+            copier[b] = std::thread(copy_out, cuts_out[k], g->b_hcut[b], HW, landed, g->device);
+        }
+        ready = next;
+    }
+    for (int b = 0; b < 2; b++) if (copier[b].joinable()) copier[b].join();
+    if (rc == FM_OK) {
+        if (cudaStreamSynchronize(g->d2h_stream) != cudaSuccess || cudaStreamSynchronize(g->h2d_stream) != cudaSuccess) {
+            fm_set_error("fm_grid_solve_host_batch: copy stream failed: %s", cudaGetErrorString(cudaGetLastError()));
+            rc = FM_CUDA_ERROR;
+        }
+    } else {
+        cudaStreamSynchronize(g->h2d_stream);   // no copy may still target a buffer the caller frees
+        cudaStreamSynchronize(g->d2h_stream);
+    }
     return rc;
 }
 

@@ -84,6 +84,36 @@ class GridSolver:
         self.last_stats = st.as_dict()
         return int(flow.value), cut, self.last_stats
 
+    def solve_host_batch(self, caps_list, cycle_budget=DEFAULT_CYCLE_BUDGET, bfs_interval=DEFAULT_BFS_INTERVAL,
+                         want_cut=True, cancel_violations=False, precancel=True):
+        """Several same-shape instances from host planes in one pipelined call
+        (fm_grid_solve_host_batch: the H2D of instance k+1 and the cut D2H of instance
+        k-1 overlap the solve of instance k).  Returns [(flow, cut, stats)], each equal
+        to solve_host's result for that instance."""
+        planes = []
+        for caps in caps_list:
+            if len(caps) != 6:
+                raise ValueError("each instance needs the six planes capR, capL, capD, capU, capS, capT")
+            cs = [np.ascontiguousarray(a, dtype=np.int32) for a in caps]
+            for a in cs:
+                if a.shape != (self.H, self.W):
+                    raise ValueError(f"plane shape {a.shape} does not match the solver's {(self.H, self.W)}")
+            planes.append(cs)
+        n = len(planes)
+        ptrs = (ctypes.c_void_p * max(1, 6 * n))(*[_lib.ptr(a) for cs in planes for a in cs])
+        flows = np.zeros(max(1, n), np.int64)
+        cuts = [np.empty((self.H, self.W), np.bool_) for _ in range(n)] if want_cut else None
+        cptr = (ctypes.c_void_p * max(1, n))(*[_lib.ptr(c) for c in cuts]) if want_cut else None
+        sts = (_lib.FmStats * max(1, n))()
+        rc = _lib.load().fm_grid_solve_host_batch(
+            self._h, n, ptrs, int(cycle_budget), int(bfs_interval),
+            self._flags(cancel_violations, want_cut, precancel), _lib.ptr(flows), cptr, sts)
+        _lib.check(rc, "fm_grid_solve_host_batch")
+        out = [(int(flows[k]), cuts[k] if want_cut else None, sts[k].as_dict()) for k in range(n)]
+        if out:
+            self.last_stats = out[-1][2]
+        return out
+
     def solve_device(self, caps, cycle_budget=DEFAULT_CYCLE_BUDGET, bfs_interval=DEFAULT_BFS_INTERVAL,
                      cut_out=None, cancel_violations=False, precancel=True, stream=None,
                      global_sweep=False):
@@ -298,6 +328,41 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
     return SolveReport(objective=int(flow), pushes=int(stats.get("pushes", 0)),
                        relabels=int(stats.get("relabels", 0)), rounds=int(stats.get("rounds", 0)),
                        elapsed=elapsed, cut=cut, stats=stats)
+
+
+def hybrid_solve_batch(nets, worker_count: int = 4, cycle_budget: int = DEFAULT_CYCLE_BUDGET, *,
+                       device: int | None = None, bfs_interval: int = DEFAULT_BFS_INTERVAL,
+                       cancel_violations: bool = False, want_cut: bool = True) -> list[SolveReport]:
+    """hybrid_solve over a sequence of same-shape host GridNetworks (a stream of images):
+    one pipelined device call in which the host->device copy of network k+1 and the
+    cut copy-back of network k-1 overlap the solve of network k.  Returns one
+    SolveReport per network, each equal to hybrid_solve(net)'s; `elapsed` of each is
+    the whole call's time divided by the count."""
+    nets = list(nets)
+    if worker_count < 1:
+        raise ValueError(f"worker_count must be at least 1, got {worker_count}")
+    if cycle_budget < 1:
+        raise ValueError(f"cycle_budget must be at least 1, got {cycle_budget}")
+    if not nets:
+        return []
+    for net in nets:
+        if not isinstance(net, GridNetwork):
+            raise ValueError("hybrid_solve_batch takes GridNetworks")
+        if net.source is None or net.sink is None:
+            raise ValueError("network has no source/sink")
+        if net.on_device or net.wide:
+            raise ValueError("hybrid_solve_batch takes host int32 grids (use hybrid_solve for device or wide ones)")
+        if (net.H, net.W) != (nets[0].H, nets[0].W):
+            raise ValueError("hybrid_solve_batch needs networks of one shape")
+    H, W = nets[0].H, nets[0].W
+    device = 0 if device is None else int(device)
+    started = time.perf_counter()
+    with _solvers.use((H, W, device), device, lambda: GridSolver(H, W, device)) as solver:
+        res = solver.solve_host_batch([net.host_caps() for net in nets], cycle_budget, bfs_interval,
+                                      want_cut=want_cut, cancel_violations=cancel_violations)
+    per = (time.perf_counter() - started) / len(nets)
+    return [SolveReport(objective=int(f), pushes=int(st.get("pushes", 0)), relabels=int(st.get("relabels", 0)),
+                        rounds=int(st.get("rounds", 0)), elapsed=per, cut=cut, stats=st) for f, cut, st in res]
 
 
 _groups = _lib.SolverCache(per_device=1)
