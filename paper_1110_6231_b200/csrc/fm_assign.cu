@@ -244,10 +244,40 @@ __device__ __forceinline__ void ycand_partial(const AssignDev &a, int y, int t, 
     }
 }
 
+// Where an op appends the nodes it activates.  Grid-wide rounds: a global list and its
+// global counter.  The single-CTA tail also keeps the counter (and the first TL_CAP
+// entries) in shared memory, plus shared copies of the relabel count and the
+// infeasibility word: its rounds then need no L2 round trip for list bookkeeping
+// (the global list is still written, fire-and-forget, so a later launch resumes
+// from it).
+constexpr int TL_CAP = 32;   // (static shared memory is nearly full: s_sorted takes 32 KB)
+struct Lists {
+    int32_t *glist;       // global list
+    int32_t *gcnt;        // its global counter (grid-wide rounds)
+    int *scnt = nullptr;  // tail: shared counter (authoritative), NULL in grid-wide rounds
+    int32_t *slist = nullptr;
+    int *srel = nullptr, *sinf = nullptr;
+};
+__device__ __forceinline__ int list_reserve(const Lists &L, int k) {
+    return L.scnt ? atomicAdd(L.scnt, k) : atomicAdd(L.gcnt, k);
+}
+__device__ __forceinline__ void list_put(const Lists &L, int i, int v) {
+    if (L.scnt && i < TL_CAP) L.slist[i] = v;
+    L.glist[i] = v;
+}
+__device__ __forceinline__ void add_relabels(const AssignDev &a, const Lists &L, int k) {
+    atomicAdd(a.cnt + C_RELABELS, k);
+    if (L.srel) atomicAdd(L.srel, k);
+}
+__device__ __forceinline__ void set_infeasible(const AssignDev &a, const Lists &L, int why) {
+    atomicExch(a.cnt + C_INFEASIBLE, why);
+    if (L.sinf) atomicExch(L.sinf, why);
+}
+
 // X op by one group (warp when CTA_WIDE is false, else the whole CTA): relabel if
 // the cheapest arc is not admissible, then push the unit on it.
 template <bool CTA_WIDE>
-__device__ void x_op(const AssignDev &a, int x, int32_t *ylist_next, int32_t *ycnt_next,
+__device__ void x_op(const AssignDev &a, int x, const Lists &L,
                      unsigned long long &pushes, unsigned long long &relabels, int tag = 0) {
     long long best = I64_MAX;
     int y = INT32_MAX;
@@ -257,18 +287,18 @@ __device__ void x_op(const AssignDev &a, int x, int32_t *ylist_next, int32_t *yc
     if (CTA_WIDE) cta_argmin(best, y); else warp_argmin(best, y);
     if (t == 0) {
         if (y == INT32_MAX) {
-            atomicExch(a.cnt + C_INFEASIBLE, 1);  // active node with no residual arc
+            set_infeasible(a, L, 1);              // active node with no residual arc
         } else {
             if (!(best < -px)) {                 // not admissible: p(x) <- -(best + eps)
                 check_price_write(a, x, px, -(best + a.eps), tag);
                 a.px[x] = -(best + a.eps);
                 relabels++;
-                atomicAdd(a.cnt + C_RELABELS, 1);
+                add_relabels(a, L, 1);
             }
             a.match[x] = y;                      // unit push x -> y
             pushes++;
             const int old = atomicAdd(a.ey + y, 1);
-            if (old == 0) ylist_next[atomicAdd(ycnt_next, 1)] = y;
+            if (old == 0) list_put(L, list_reserve(L, 1), y);
         }
     }
     if (CTA_WIDE) __syncthreads(); else __syncwarp();
@@ -284,7 +314,7 @@ constexpr int YCAP = 64;                // candidates gathered per Y op in share
 constexpr int YBUCKET = 256;            // per-Y bucket slots for long Y lists (= YB_CAP)
 
 template <bool CTA_WIDE>
-__device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
+__device__ void y_op(const AssignDev &a, int y, const Lists &L,
                      unsigned long long &pushes, unsigned long long &relabels, long long *sbuf, int tag = 0) {
     __shared__ long long s_cv[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
     __shared__ int s_cx[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
@@ -295,44 +325,50 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
     const int slot = CTA_WIDE ? 0 : (threadIdx.x >> 5);
     long long *cv = s_cv[slot];
     int *cx = s_cx[slot];
+    // y's excess and price load while the gather below scans match[] (a listed y holds
+    // excess; the check waits until after the scan)
     int ey = __ldcg(a.ey + y);
     long long py = __ldcg((const long long *)a.py + y);
     const long long py0 = py;
-    if (ey <= 0) return;
     // ---- gather
     if (t == 0) s_cn[slot] = 0;
     if (CTA_WIDE) __syncthreads(); else __syncwarp();
     const int n = a.n;
     const auto take = [&](int x) {
-        if (__ldcg(a.frozen + x)) return;
         const long long v = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale - __ldcg((const long long *)a.px + x);
         const int k = atomicAdd(&s_cn[slot], 1);
         if (k < CAP) { cx[k] = x; cv[k] = v; }
     };
     if ((n & 3) == 0) {
+        // match words and the frozen flags of the same 4 x load together (no dependent
+        // frozen load per candidate)
         const int n4 = n >> 2;
         const int4 *m4 = reinterpret_cast<const int4 *>(a.match);
+        const uint32_t *fz4 = reinterpret_cast<const uint32_t *>(a.frozen);
         for (int j0 = t; j0 < n4; j0 += 4 * T) {
             int4 mm[4];
+            uint32_t fz[4];
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int j = j0 + u * T;
                 mm[u] = j < n4 ? __ldcg(m4 + j) : make_int4(-1, -1, -1, -1);
+                fz[u] = j < n4 ? __ldcg(fz4 + j) : 0u;
             }
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int j = j0 + u * T;
-                if (mm[u].x == y) take(4 * j + 0);
-                if (mm[u].y == y) take(4 * j + 1);
-                if (mm[u].z == y) take(4 * j + 2);
-                if (mm[u].w == y) take(4 * j + 3);
+                if (mm[u].x == y && !(fz[u] & 0xffu)) take(4 * j + 0);
+                if (mm[u].y == y && !(fz[u] & 0xff00u)) take(4 * j + 1);
+                if (mm[u].z == y && !(fz[u] & 0xff0000u)) take(4 * j + 2);
+                if (mm[u].w == y && !(fz[u] & 0xff000000u)) take(4 * j + 3);
             }
         }
     } else {
         for (int x = t; x < n; x += T)
-            if (__ldcg(a.match + x) == y) take(x);
+            if (__ldcg(a.match + x) == y && !__ldcg(a.frozen + x)) take(x);
     }
     if (CTA_WIDE) __syncthreads(); else __syncwarp();
+    if (ey <= 0) return;   // uniform: every thread read the same (phase-constant) word
     const int cnt = s_cn[slot];
     if (cnt > CAP) {
         // ---- overflow: one scan per unit (the original scheme)
@@ -342,16 +378,16 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
             ycand_partial(a, y, t, T, bv, bi);
             if (CTA_WIDE) cta_argmin(bv, bi); else warp_argmin(bv, bi);
             if (bi == INT32_MAX) {
-                if (t == 0) atomicExch(a.cnt + C_INFEASIBLE, 2);
+                if (t == 0) set_infeasible(a, L, 2);
                 break;
             }
             if (t == 0) {
                 if (!(bv < -py)) {
                     if (a.validate && -(bv + a.eps) >= py) atomicExch(a.cnt + C_INFEASIBLE, V_RELABEL);
-                    py = -(bv + a.eps); relabels++; atomicAdd(a.cnt + C_RELABELS, 1);
+                    py = -(bv + a.eps); relabels++; add_relabels(a, L, 1);
                 }
                 a.match[bi] = -1;
-                xlist_next[atomicAdd(xcnt_next, 1)] = bi;
+                list_put(L, list_reserve(L, 1), bi);
                 pushes++;
             }
             ey--;
@@ -364,7 +400,7 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
         // order (sbuf: >= CAP entries of the caller's shared scratch), append the
         // batch with one list reservation and replay the relabel sequence.
         __shared__ int s_base[CTA_WIDE ? 1 : AWARPS];
-        if (t == 0) s_base[slot] = atomicAdd(xcnt_next, ey);
+        if (t == 0) s_base[slot] = list_reserve(L, ey);
         if (CTA_WIDE) __syncthreads(); else __syncwarp();
         const int base = s_base[slot];
         for (int k = t; k < cnt; k += T) {
@@ -379,7 +415,7 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
             if (rank < ey) {
                 sbuf[rank] = vk;
                 a.match[xk] = -1;
-                xlist_next[base + rank] = xk;
+                list_put(L, base + rank, xk);
             }
         }
         if (CTA_WIDE) __syncthreads(); else __syncwarp();
@@ -394,7 +430,7 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
             }
             relabels += rl;
             pushes += ey;
-            if (rl) atomicAdd(a.cnt + C_RELABELS, (int)rl);
+            if (rl) add_relabels(a, L, (int)rl);
         }
         ey = 0;
     } else {
@@ -408,17 +444,17 @@ __device__ void y_op(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xc
             int i2 = bi;
             if (CTA_WIDE) cta_argmin(v2, i2); else warp_argmin(v2, i2);
             if (i2 == INT32_MAX) {
-                if (t == 0) atomicExch(a.cnt + C_INFEASIBLE, 2);
+                if (t == 0) set_infeasible(a, L, 2);
                 break;
             }
             if (bi == i2 && bk >= 0) cv[bk] = I64_MAX;   // the owner lane retires the slot
             if (t == 0) {
                 if (!(v2 < -py)) {
                     if (a.validate && -(v2 + a.eps) >= py) atomicExch(a.cnt + C_INFEASIBLE, V_RELABEL);
-                    py = -(v2 + a.eps); relabels++; atomicAdd(a.cnt + C_RELABELS, 1);
+                    py = -(v2 + a.eps); relabels++; add_relabels(a, L, 1);
                 }
                 a.match[i2] = -1;
-                xlist_next[atomicAdd(xcnt_next, 1)] = i2;
+                list_put(L, list_reserve(L, 1), i2);
                 pushes++;
             }
             ey--;
@@ -446,7 +482,7 @@ constexpr int YB_CAP = 32 * YB_PER_LANE;
 
 __device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, int cnt,
                              const long long (&v)[YB_PER_LANE], const int (&xs)[YB_PER_LANE],
-                             long long *s_sorted, int32_t *xlist_next, int32_t *xcnt_next,
+                             long long *s_sorted, const Lists &L,
                              unsigned long long &pushes, unsigned long long &relabels, int tag) {
     const int lane = threadIdx.x & 31;
     int rank[YB_PER_LANE];
@@ -464,14 +500,14 @@ __device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, in
         }
     }
     int base = 0;
-    if (lane == 0) base = atomicAdd(xcnt_next, ey);
+    if (lane == 0) base = list_reserve(L, ey);
     base = __shfl_sync(0xffffffffu, base, 0);
 #pragma unroll
     for (int k = 0; k < YB_PER_LANE; k++) {
         if (xs[k] != INT32_MAX && rank[k] < ey) {
             s_sorted[rank[k]] = v[k];
             a.match[xs[k]] = -1;
-            xlist_next[base + rank[k]] = xs[k];
+            list_put(L, base + rank[k], xs[k]);
         }
     }
     __syncwarp();
@@ -483,7 +519,7 @@ __device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, in
         }
         relabels += rl;
         pushes += ey;
-        if (rl) atomicAdd(a.cnt + C_RELABELS, (int)rl);
+        if (rl) add_relabels(a, L, (int)rl);
         if (rl && a.validate && tag && atomicExch(a.pw + a.n + y, tag) == tag)
             atomicExch(a.cnt + C_INFEASIBLE, V_OWNER);
         a.py[y] = py;
@@ -495,14 +531,14 @@ __device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, in
 
 // Y op over a pre-bucketed candidate list (long Y lists): the incoming X of y were
 // collected once per phase into ybuf[y*YCAP ..]; one warp per y.
-__device__ void y_op_bucketed(const AssignDev &a, int y, int32_t *xlist_next, int32_t *xcnt_next,
+__device__ void y_op_bucketed(const AssignDev &a, int y, const Lists &L,
                               unsigned long long &pushes, unsigned long long &relabels,
                               long long *s_sorted, int tag) {
     const int lane = threadIdx.x & 31;
     const int cnt = __ldcg(a.ybcnt + y);
     const int ey = __ldcg(a.ey + y);
     if (cnt > YBUCKET || ey >= cnt) {       // bucket overflow (or inconsistent): scan match[] instead
-        y_op<false>(a, y, xlist_next, xcnt_next, pushes, relabels, s_sorted, tag);
+        y_op<false>(a, y, L, pushes, relabels, s_sorted, tag);
         if (lane == 0) a.ybcnt[y] = 0;
         __syncwarp();
         return;
@@ -522,7 +558,7 @@ __device__ void y_op_bucketed(const AssignDev &a, int y, int32_t *xlist_next, in
             v[k] = (long long)__ldg(a.w + (size_t)x * n + y) * a.scale - __ldcg((const long long *)a.px + x);
         }
     }
-    if (ey > 0) y_batch_warp(a, y, ey, py, cnt, v, xs, s_sorted, xlist_next, xcnt_next, pushes, relabels, tag);
+    if (ey > 0) y_batch_warp(a, y, ey, py, cnt, v, xs, s_sorted, L, pushes, relabels, tag);
     if (lane == 0) a.ybcnt[y] = 0;
     __syncwarp();
 }
@@ -604,6 +640,9 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
     unsigned long long tail_ns = 0, multi_ns = 0, t_round = globaltimer();
     __shared__ long long s_sorted[AWARPS][YB_CAP];
     bool tail = false;
+    // single-CTA tail: list counters / heads, relabel count and infeasibility in shared memory
+    __shared__ int s_xn[2], s_yn[2], s_rel, s_inf;
+    __shared__ int32_t s_xl[2][TL_CAP], s_yl[2][TL_CAP];
     int r = __ldcg(a.cnt + C_ROUND);
     for (;; r++) {
         {
@@ -613,7 +652,12 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
         }
         const int b = r & 1, nb = b ^ 1;
         int ny, infeasible, relabels_since;
-        cta_bcast3(a.cnt + C_Y0 + b, a.cnt + C_INFEASIBLE, a.cnt + C_RELABELS, ny, infeasible, relabels_since);
+        if (tail) {
+            __syncthreads();   // the previous round's shared counters are final
+            ny = s_yn[b]; infeasible = s_inf; relabels_since = s_rel;
+        } else {
+            cta_bcast3(a.cnt + C_Y0 + b, a.cnt + C_INFEASIBLE, a.cnt + C_RELABELS, ny, infeasible, relabels_since);
+        }
         if (ny == 0 || infeasible) {
             if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 0;
             break;
@@ -636,9 +680,12 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             if (blockIdx.x == 0 && threadIdx.x == 0) { atomicExch(a.cnt + C_INFEASIBLE, 3); a.cnt[C_EXIT] = 0; }
             break;
         }
-        if (!tail && ny <= tail_threshold) {
+        if (!tail && ny <= min(tail_threshold, TL_CAP)) {
             tail = true;
             if (blockIdx.x != 0) break;  // CTA 0 finishes alone
+            for (int i = threadIdx.x; i < ny; i += ATHREADS) s_yl[b][i] = __ldcg(a.ylist[b] + i);
+            if (threadIdx.x == 0) { s_yn[b] = ny; s_xn[b] = 0; s_rel = relabels_since; s_inf = 0; }
+            __syncthreads();
         }
         rounds++;
         if (tail) tail_rounds++;
@@ -647,37 +694,46 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             a.cnt[C_X0 + nb] = 0;   // X list of round r+1 (last read in round r-1)
             a.cnt[C_Y0 + nb] = 0;   // Y list of round r+1 (last read at round r-1)
+            if (tail) { s_xn[nb] = 0; s_yn[nb] = 0; }
         }
         if (tail) {
             const unsigned long long p0 = pushes + relabels;
+            const Lists TX{a.xlist[b], a.cnt + C_X0 + b, &s_xn[b], s_xl[b], &s_rel, &s_inf};
+            const Lists TY{a.ylist[nb], a.cnt + C_Y0 + nb, &s_yn[nb], s_yl[nb], &s_rel, &s_inf};
+            // entries past TL_CAP live only in the global list (written by this CTA
+            // before the last barrier)
+            const auto ent = [&](const int32_t *sl, const int32_t *gl, int i) { return i < TL_CAP ? sl[i] : __ldcg(gl + i); };
             if (ny <= 2) {
                 for (int i = 0; i < ny; i++)
-                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0], tag_y);
+                    y_op<true>(a, ent(s_yl[b], a.ylist[b], i), TX, pushes, relabels, s_sorted[0], tag_y);
             } else {
                 for (int i = cwarp; i < ny; i += AWARPS)
-                    y_op<false>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[cwarp], tag_y);
+                    y_op<false>(a, ent(s_yl[b], a.ylist[b], i), TX, pushes, relabels, s_sorted[cwarp], tag_y);
             }
             __threadfence_block();
             __syncthreads();
-            const int nx = __ldcg(a.cnt + C_X0 + b);
+            const int nx = s_xn[b];
             if (nx <= 2) {
                 for (int i = 0; i < nx; i++)
-                    x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
+                    x_op<true>(a, ent(s_xl[b], a.xlist[b], i), TY, pushes, relabels, tag_x);
             } else {
                 for (int i = cwarp; i < nx; i += AWARPS)
-                    x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
+                    x_op<false>(a, ent(s_xl[b], a.xlist[b], i), TY, pushes, relabels, tag_x);
             }
             __threadfence_block();
             __syncthreads();
+            // the global counters follow the shared ones (a later launch resumes from them)
+            if (threadIdx.x == 0) { a.cnt[C_X0 + b] = s_xn[b]; a.cnt[C_Y0 + nb] = s_yn[nb]; }
             tail_ops += pushes + relabels - p0;
         } else {
+            const Lists LX{a.xlist[b], a.cnt + C_X0 + b}, LY{a.ylist[nb], a.cnt + C_Y0 + nb};
             // a list no longer than the grid gets one CTA per node (one L2 round trip
             // per row scan); longer lists get one warp per node
             const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
             unsigned long long t0 = timer ? globaltimer() : 0, t1 = 0;
             if (ny <= a.cta_y * (int)gridDim.x) {
                 for (int i = blockIdx.x; i < ny; i += gridDim.x)
-                    y_op<true>(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels, s_sorted[0], tag_y);
+                    y_op<true>(a, __ldcg(a.ylist[b] + i), LX, pushes, relabels, s_sorted[0], tag_y);
             } else {
                 // long list: bucket every incoming X by its Y in one pass over match[]
                 const int gtid = blockIdx.x * ATHREADS + threadIdx.x, gthr = gridDim.x * ATHREADS;
@@ -689,7 +745,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
                 }
                 grid.sync();
                 for (int i = gwarp; i < ny; i += gwarps)
-                    y_op_bucketed(a, __ldcg(a.ylist[b] + i), a.xlist[b], a.cnt + C_X0 + b, pushes, relabels,
+                    y_op_bucketed(a, __ldcg(a.ylist[b] + i), LX, pushes, relabels,
                                   s_sorted[threadIdx.x >> 5], tag_y);
             }
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_Y, t1 - t0); t0 = t1; }
@@ -699,10 +755,10 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             cta_bcast3(a.cnt + C_X0 + b, nullptr, nullptr, nx, u1, u2);
             if (nx <= a.cta_x * (int)gridDim.x) {
                 for (int i = blockIdx.x; i < nx; i += gridDim.x)
-                    x_op<true>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
+                    x_op<true>(a, __ldcg(a.xlist[b] + i), LY, pushes, relabels, tag_x);
             } else {
                 for (int i = gwarp; i < nx; i += gwarps)
-                    x_op<false>(a, __ldcg(a.xlist[b] + i), a.ylist[nb], a.cnt + C_Y0 + nb, pushes, relabels, tag_x);
+                    x_op<false>(a, __ldcg(a.xlist[b] + i), LY, pushes, relabels, tag_x);
             }
             if (timer) {
                 t1 = globaltimer(); atomicAdd(a.ops + O_PH_X, t1 - t0); t0 = t1;
@@ -1303,7 +1359,7 @@ __global__ void __launch_bounds__(ATHREADS) x_phase_kernel(AssignDev a, int tag)
     const int nx = __ldcg(a.cnt + C_X0);
     unsigned long long pushes = 0, relabels = 0;
     for (int i = warp; i < nx; i += nwarps)
-        x_op<false>(a, __ldcg(a.xlist[0] + i), a.ylist[0], a.cnt + C_Y0, pushes, relabels, tag);
+        x_op<false>(a, __ldcg(a.xlist[0] + i), Lists{a.ylist[0], a.cnt + C_Y0}, pushes, relabels, tag);
     if ((threadIdx.x & 31) == 0) {
         if (pushes) atomicAdd(a.ops + O_PUSH, pushes);
         if (relabels) atomicAdd(a.ops + O_RELABEL, relabels);
