@@ -809,6 +809,18 @@ __device__ __forceinline__ void group_sync(int grp, int nthreads) {   // named b
     asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(nthreads) : "memory");
 }
 
+// Y labels in the price update are packed words 2 l(y) + q, q = 1 while y is queued:
+// one atomicMin lowers the label and marks y queued, and its old value says whether the
+// caller must queue y (label dropped, y was not queued); taking y clears q and reads
+// the label in one atomicAnd.  (A separate queued flag cost two more dependent L2 round
+// trips per label drop and per take.)
+__device__ __forceinline__ bool ylabel_drop(const AssignDev &a, int y, int l) {
+    const int old = atomicMin(a.ly + y, 2 * l + 1);
+    return (old >> 1) > l && !(old & 1);
+}
+__device__ __forceinline__ int ylabel_take(const AssignDev &a, int y) { return atomicAnd(a.ly + y, ~1) >> 1; }
+__device__ __forceinline__ int ylabel(int word) { return word >> 1; }
+
 struct PuDev {
     const int32_t *wt;      // transposed weights: wt[y*n + x] = w(x, y)
     int32_t *fy[2], *fx[2]; // frontiers
@@ -891,8 +903,7 @@ __device__ __forceinline__ void pu_scan_y(const AssignDev &a, const PuDev &f, in
             const long long cand2 = cand[k] + len2;
             if (cand2 > cap) continue;
             const int mx = mxv[k];
-            const int old2 = atomicMin(a.ly + mx, (int)cand2);
-            if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0) push(mx);
+            if (ylabel_drop(a, mx, (int)cand2)) push(mx);
         }
     }
     for (int x = nv8 + gt; x < n; x += PU_GT) {
@@ -918,8 +929,7 @@ __device__ __forceinline__ void pu_scan_y(const AssignDev &a, const PuDev &f, in
         if (len2 < 0) len2 = 0;
         const long long cand2 = cand + len2;
         if (cand2 > cap) continue;
-        const int old2 = atomicMin(a.ly + mx, (int)cand2);
-        if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0) push(mx);
+        if (ylabel_drop(a, mx, (int)cand2)) push(mx);
     }
 }
 
@@ -959,8 +969,7 @@ __device__ __forceinline__ void pu_relax4(const AssignDev &a, const PuDev &f, in
         const long long cand2 = cand[k] + len2;
         if (cand2 > cap) continue;
         const int mx = mxv[k];
-        const int old2 = atomicMin(a.ly + mx, (int)cand2);
-        if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0) push(mx);
+        if (ylabel_drop(a, mx, (int)cand2)) push(mx);
     }
 }
 
@@ -1017,8 +1026,7 @@ __device__ __forceinline__ void pu_scan_y_filtered(const AssignDev &a, const PuD
         if (len2 < 0) len2 = 0;
         const long long cand2 = cand + len2;
         if (cand2 > cap) continue;
-        const int old2 = atomicMin(a.ly + mx, (int)cand2);
-        if ((int)cand2 < old2 && atomicExch(f.in_fy + mx, 1) == 0) push(mx);
+        if (ylabel_drop(a, mx, (int)cand2)) push(mx);
     }
 }
 
@@ -1050,8 +1058,7 @@ __global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_updat
         a.mw[v] = mv >= 0 ? __ldg(a.w + (size_t)v * n + mv) : 0;
         a.pmx[v] = mv >= 0 ? __ldcg((const long long *)a.py + mv) : 0;
         if (__ldcg(a.ey + v) < 0) {
-            a.ly[v] = 0;
-            f.in_fy[v] = 1;
+            a.ly[v] = 1;                                  // label 0, queued
             if (f.ring_on) {
                 atomicAdd(f.rctr + 64, 1u);
                 f.ring[atomicAdd(f.rctr + 32, 1u)] = v;   // slots are empty, tail starts at 0
@@ -1059,8 +1066,7 @@ __global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_updat
                 f.fy[0][atomicAdd(f.cnt + 0, 1)] = v;   // iteration 0's frontier (counter 0 of 3)
             }
         } else {
-            a.ly[v] = LINF;
-            f.in_fy[v] = 0;
+            a.ly[v] = 2 * LINF;                           // unlabelled, not queued
         }
     }
     grid.sync();
@@ -1102,10 +1108,8 @@ __global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_updat
                 }
                 s_y[grp] = y;
                 if (y >= 0) {
-                    f.in_fy[y] = 0;          // clear before reading l(y): a later drop re-queues y
-                    __threadfence();
-                    s_ly[grp] = __ldcg(a.ly + y);
                     s_py[grp] = __ldcg((const long long *)a.py + y);
+                    s_ly[grp] = ylabel_take(a, y);   // a later drop re-queues y
                     ys++;
                     t_scan = globaltimer();
                 }
@@ -1150,20 +1154,16 @@ __global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_updat
         long long nxt_p = 0;
         if (gt == 0 && blockIdx.x * ng + grp < ny) {
             nxt_y = __ldcg(f.fy[b] + blockIdx.x * ng + grp);
-            f.in_fy[nxt_y] = 0;          // clear before reading l(y): a later drop re-queues y
-            __threadfence();
-            nxt_l = __ldcg(a.ly + nxt_y);
             nxt_p = __ldcg((const long long *)a.py + nxt_y);
+            nxt_l = ylabel_take(a, nxt_y);   // a later drop re-queues y
         }
         for (int i = blockIdx.x * ng + grp; i < ny; i += istep) {
             if (gt == 0) {
                 s_y[grp] = nxt_y; s_ly[grp] = nxt_l; s_py[grp] = nxt_p;
                 if (i + istep < ny) {
                     nxt_y = __ldcg(f.fy[b] + i + istep);
-                    f.in_fy[nxt_y] = 0;
-                    __threadfence();
-                    nxt_l = __ldcg(a.ly + nxt_y);
                     nxt_p = __ldcg((const long long *)a.py + nxt_y);
+                    nxt_l = ylabel_take(a, nxt_y);
                 }
             }
             group_sync(grp, PU_GT);
@@ -1190,7 +1190,7 @@ __global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_updat
             if (l >= LINF) missing = 1; else last = max(last, l);
         }
         if (__ldcg(a.ey + v) > 0) {
-            const int l = __ldcg(a.ly + v);
+            const int l = ylabel(__ldcg(a.ly + v));
             if (l >= LINF) missing = 1; else last = max(last, l);
         }
     }
@@ -1212,9 +1212,10 @@ __global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_updat
     const long long K = min((long long)__ldcg(a.cnt + C_PU_LAST), (long long)a.max_bucket) + 1;
     unsigned yfin = 0, ylab = 0;
     for (int v = tid; v < n; v += nthr) {
-        const long long dx = min((long long)a.lx[v], K), dy = min((long long)a.ly[v], K);
-        yfin += a.ly[v] < K;
-        ylab += a.ly[v] < LINF;
+        const int lyv = ylabel(a.ly[v]);
+        const long long dx = min((long long)a.lx[v], K), dy = min((long long)lyv, K);
+        yfin += lyv < K;
+        ylab += lyv < LINF;
         if (a.validate && (dx < 0 || dy < 0)) atomicExch(a.cnt + C_INFEASIBLE, V_RAISE);
         a.px[v] -= a.eps * dx;
         a.py[v] -= a.eps * dy;
