@@ -1098,10 +1098,9 @@ __global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_updat
                 if (y < 0) {
                     const unsigned sl = atomicAdd(f.rctr + 0, 1u) % (unsigned)f.ring_cap;
                     for (unsigned ns = 32;; ns = min(ns * 2, 1024u)) {
-                        if (*(volatile int32_t *)(f.ring + sl) >= 0) {
-                            const int v = atomicExch(f.ring + sl, -1);   // exactly one taker per entry
-                            if (v >= 0) { y = v; break; }
-                        }
+                        // exactly one taker per entry; an empty slot stays empty (no read first)
+                        const int v = atomicExch(f.ring + sl, -1);
+                        if (v >= 0) { y = v; break; }
                         if (*(volatile unsigned *)(f.rctr + 64) == 0) break;
                         __nanosleep(ns);
                     }
