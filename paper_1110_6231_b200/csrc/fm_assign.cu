@@ -607,17 +607,23 @@ __global__ void reset_excess_kernel(AssignDev a) {
 // Control words read right after a grid barrier: one thread per CTA loads them and
 // the CTA shares them (thousands of warps loading one L2 line at the same moment
 // serialise on its slice; ncu put half of the price update's stall samples there).
-__device__ __forceinline__ void cta_bcast3(const int32_t *p0, const int32_t *p1, const int32_t *p2,
-                                           int &v0, int &v1, int &v2) {
-    __shared__ int s_b[3];
+__device__ __forceinline__ void cta_bcast4(const int32_t *p0, const int32_t *p1, const int32_t *p2,
+                                           const int32_t *p3, int &v0, int &v1, int &v2, int &v3) {
+    __shared__ int s_b[4];
     __syncthreads();   // the previous broadcast has been read by every thread
     if (threadIdx.x == 0) {
         s_b[0] = __ldcg(p0);
         s_b[1] = p1 ? __ldcg(p1) : 0;
         s_b[2] = p2 ? __ldcg(p2) : 0;
+        s_b[3] = p3 ? __ldcg(p3) : 0;
     }
     __syncthreads();
-    v0 = s_b[0]; v1 = s_b[1]; v2 = s_b[2];
+    v0 = s_b[0]; v1 = s_b[1]; v2 = s_b[2]; v3 = s_b[3];
+}
+__device__ __forceinline__ void cta_bcast3(const int32_t *p0, const int32_t *p1, const int32_t *p2,
+                                           int &v0, int &v1, int &v2) {
+    int u;
+    cta_bcast4(p0, p1, p2, nullptr, v0, v1, v2, u);
 }
 
 // The refine's push/relabel rounds (refine_par's coordinator loop, assign_par.py:162-236)
@@ -651,12 +657,15 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             t_round = now;
         }
         const int b = r & 1, nb = b ^ 1;
-        int ny, infeasible, relabels_since;
+        int ny, infeasible, relabels_since, y_first = 0;
         if (tail) {
             __syncthreads();   // the previous round's shared counters are final
             ny = s_yn[b]; infeasible = s_inf; relabels_since = s_rel;
         } else {
-            cta_bcast3(a.cnt + C_Y0 + b, a.cnt + C_INFEASIBLE, a.cnt + C_RELABELS, ny, infeasible, relabels_since);
+            // with the control words, this CTA's first Y list entry (read speculatively:
+            // used only when the round runs CTA-wide ops and the list reaches it)
+            cta_bcast4(a.cnt + C_Y0 + b, a.cnt + C_INFEASIBLE, a.cnt + C_RELABELS,
+                       (int)blockIdx.x < a.n ? a.ylist[b] + blockIdx.x : nullptr, ny, infeasible, relabels_since, y_first);
         }
         if (ny == 0 || infeasible) {
             if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_EXIT] = 0;
@@ -733,7 +742,8 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             unsigned long long t0 = timer ? globaltimer() : 0, t1 = 0;
             if (ny <= a.cta_y * (int)gridDim.x) {
                 for (int i = blockIdx.x; i < ny; i += gridDim.x)
-                    y_op<true>(a, __ldcg(a.ylist[b] + i), LX, pushes, relabels, s_sorted[0], tag_y);
+                    y_op<true>(a, i == (int)blockIdx.x ? y_first : __ldcg(a.ylist[b] + i), LX, pushes, relabels,
+                               s_sorted[0], tag_y);
             } else {
                 // long list: bucket every incoming X by its Y in one pass over match[]
                 const int gtid = blockIdx.x * ATHREADS + threadIdx.x, gthr = gridDim.x * ATHREADS;
@@ -751,11 +761,12 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_Y, t1 - t0); t0 = t1; }
             grid.sync();
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC1, t1 - t0); t0 = t1; }
-            int nx, u1, u2;
-            cta_bcast3(a.cnt + C_X0 + b, nullptr, nullptr, nx, u1, u2);
+            int nx, x_first, u2;
+            cta_bcast3(a.cnt + C_X0 + b, (int)blockIdx.x < a.n ? a.xlist[b] + blockIdx.x : nullptr, nullptr, nx,
+                       x_first, u2);
             if (nx <= a.cta_x * (int)gridDim.x) {
                 for (int i = blockIdx.x; i < nx; i += gridDim.x)
-                    x_op<true>(a, __ldcg(a.xlist[b] + i), LY, pushes, relabels, tag_x);
+                    x_op<true>(a, i == (int)blockIdx.x ? x_first : __ldcg(a.xlist[b] + i), LY, pushes, relabels, tag_x);
             } else {
                 for (int i = gwarp; i < nx; i += gwarps)
                     x_op<false>(a, __ldcg(a.xlist[b] + i), LY, pushes, relabels, tag_x);
