@@ -5,7 +5,10 @@ Workload (N = 1): BASELINE.json's metric "grid max-flow Medges/s & solve ms at
 solve of a 4096 x 4096 4-connected grid (generator G), inputs
 resident in HBM.  value = Medges/s = E_grid / solve seconds, E_grid =
 2(2HW - H - W) + 2HW.  The n = 4096 assignment solve, config 2 (2048^2
-segmentation) and config 3's grid on one GPU are reported beside it.
+segmentation) and config 3's grid on one GPU are reported beside it.  e2e = the K
+steps from pinned host planes through one pipelined hybrid_solve_batch call (each
+step's six-plane H2D and cut D2H inside the timed region, overlapped with the
+neighbouring steps' solves); e2e.single_call = one synchronous hybrid_solve per step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
