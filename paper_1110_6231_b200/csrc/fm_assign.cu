@@ -62,7 +62,8 @@ constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXE
               O_PU_LASTSUM = 16, O_PU_YFIN = 17, O_PU_YLAB = 18,  // price update: sum of last, Y with l <= last, Y labelled
               O_PU_SCANNS = 19,                                    // price update: ns in Y scans (summed over groups)
               O_HIST = 20,   // [20..24]: grid-wide rounds by max(|Y list|, |X list|): <= 8, 32, 148, 592, more
-              O_COUNT = 28;
+              O_HIST_NS = 25,   // [25..29]: CTA 0's ns in those rounds
+              O_COUNT = 40;   // [30..37]: diagnostics of the rounds with long lists (trace)
 
 // validate=True failures (assign_par.py:101-106,200-214; assign_scaling.py:274-275,333-336)
 constexpr int V_RELABEL = 4;             // a relabel failed to lower a price
@@ -154,6 +155,17 @@ __device__ __forceinline__ void cta_argmin(long long &v, int &i) {
 #endif
 constexpr int RP_CHUNKS = FM_RP_CHUNKS;
 
+// a weight row chunk: read once per op, kept out of L1 (the Y prices live there)
+__device__ __forceinline__ int4 ld_row_na(const int4 *p) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+// The Y prices (n x 8 B) are constant during an X phase and read by every X op of
+// the phase: L1-cached loads (a grid barrier's acquire drops stale lines), so an SM's
+// later X ops of the phase find them in L1 instead of L2.
 __device__ __forceinline__ void row_partial(const AssignDev &a, int x, int t, int T,
                                             long long &bv, int &bi) {
     const int n = a.n;
@@ -173,9 +185,9 @@ __device__ __forceinline__ void row_partial(const AssignDev &a, int x, int t, in
             for (int u = 0; u < RP_CHUNKS; u++) {
                 const int j = j0 + u * T;
                 if (j < n4) {
-                    w[u] = __ldg(row4 + j);
-                    pa[u] = __ldcg(py2 + 2 * j);
-                    pb[u] = __ldcg(py2 + 2 * j + 1);
+                    w[u] = ld_row_na(row4 + j);
+                    pa[u] = __ldca(py2 + 2 * j);
+                    pb[u] = __ldca(py2 + 2 * j + 1);
                     fw[u] = a.use_fix ? (__ldg(frow + (j >> 3)) >> ((4 * j) & 31)) : 0u;
                 }
             }
@@ -310,21 +322,27 @@ __device__ void x_op(const AssignDev &a, int x, const Lists &L,
 // shared memory; y's own relabels do not change their order, so the excess
 // units go back to the gathered candidates in increasing cost order without
 // rescanning.  More than YCAP incoming units falls back to one scan per unit.
-constexpr int YCAP = 64;                // candidates gathered per Y op in shared memory
+constexpr int YCAP = 64;                // candidates gathered per warp-wide Y op in shared memory
+constexpr int YCAP_CTA = 1024;          // per CTA-wide Y op (in the caller's 32 KB scratch: 2.5 x 8 KB)
 constexpr int YBUCKET = 256;            // per-Y bucket slots for long Y lists (= YB_CAP)
 
 template <bool CTA_WIDE>
 __device__ void y_op(const AssignDev &a, int y, const Lists &L,
                      unsigned long long &pushes, unsigned long long &relabels, long long *sbuf, int tag = 0) {
-    __shared__ long long s_cv[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
-    __shared__ int s_cx[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 4 * YCAP : YCAP];
+    // CTA-wide: the candidates and their ranked costs live in the caller's whole
+    // AWARPS x YB_CAP scratch (no other op runs in the CTA meanwhile): up to YCAP_CTA
+    // candidates (a Y that collects a few hundred units in one phase would otherwise
+    // fall back to one match[] scan per unit)
+    __shared__ long long s_cv[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 1 : YCAP];
+    __shared__ int s_cx[CTA_WIDE ? 1 : AWARPS][CTA_WIDE ? 1 : YCAP];
     __shared__ int s_cn[CTA_WIDE ? 1 : AWARPS];
-    constexpr int CAP = CTA_WIDE ? 4 * YCAP : YCAP;
+    constexpr int CAP = CTA_WIDE ? YCAP_CTA : YCAP;
     const int t = CTA_WIDE ? threadIdx.x : (threadIdx.x & 31);
     const int T = CTA_WIDE ? ATHREADS : 32;
     const int slot = CTA_WIDE ? 0 : (threadIdx.x >> 5);
-    long long *cv = s_cv[slot];
-    int *cx = s_cx[slot];
+    long long *cv = CTA_WIDE ? sbuf : s_cv[slot];
+    int *cx = CTA_WIDE ? reinterpret_cast<int *>(sbuf + 2 * YCAP_CTA) : s_cx[slot];
+    long long *srt = CTA_WIDE ? sbuf + YCAP_CTA : sbuf;
     // y's excess and price load while the gather below scans match[] (a listed y holds
     // excess; the check waits until after the scan)
     int ey = __ldcg(a.ey + y);
@@ -371,6 +389,7 @@ __device__ void y_op(const AssignDev &a, int y, const Lists &L,
     if (ey <= 0) return;   // uniform: every thread read the same (phase-constant) word
     const int cnt = s_cn[slot];
     if (cnt > CAP) {
+        if (t == 0) { atomicAdd(a.ops + 36, 1ull); atomicAdd(a.ops + 37, (unsigned long long)ey); atomicMax(a.ops + 33, (unsigned long long)cnt); }
         // ---- overflow: one scan per unit (the original scheme)
         while (ey > 0) {
             long long bv = I64_MAX;
@@ -393,7 +412,7 @@ __device__ void y_op(const AssignDev &a, int y, const Lists &L,
             ey--;
             if (CTA_WIDE) __syncthreads(); else __syncwarp();
         }
-    } else if (ey >= a.ybatch_min && ey < cnt) {
+    } else if (ey >= a.ybatch_min && ey <= cnt) {   // ey == cnt: y keeps only frozen flow (all units go back)
         // ---- batch: the ey cheapest candidates in (v, x) order are exactly the units
         // the one-unit loop below would push back (y's relabels never reorder them).
         // Rank every candidate against the others, lay the chosen costs out in rank
@@ -413,7 +432,7 @@ __device__ void y_op(const AssignDev &a, int y, const Lists &L,
                 rank += (vj < vk || (vj == vk && cx[j] < xk)) ? 1 : 0;
             }
             if (rank < ey) {
-                sbuf[rank] = vk;
+                srt[rank] = vk;
                 a.match[xk] = -1;
                 list_put(L, base + rank, xk);
             }
@@ -422,7 +441,7 @@ __device__ void y_op(const AssignDev &a, int y, const Lists &L,
         if (t == 0) {
             unsigned long long rl = 0;
             for (int k = 0; k < ey; k++) {
-                const long long vk = sbuf[k];
+                const long long vk = srt[k];
                 if (!(vk < -py)) {
                     if (a.validate && -(vk + a.eps) >= py) atomicExch(a.cnt + C_INFEASIBLE, V_RELABEL);
                     py = -(vk + a.eps); rl++;
@@ -479,6 +498,7 @@ __device__ void y_op(const AssignDev &a, int y, const Lists &L,
 // not admissible) and the whole batch is appended with one list reservation.
 constexpr int YB_PER_LANE = 8;               // up to 256 candidates per warp
 constexpr int YB_CAP = 32 * YB_PER_LANE;
+static_assert(AWARPS * YB_CAP * 2 >= 5 * YCAP_CTA, "CTA-wide Y op scratch (candidates, ranked costs, indices) exceeds s_sorted");
 
 __device__ void y_batch_warp(const AssignDev &a, int y, int ey, long long py, int cnt,
                              const long long (&v)[YB_PER_LANE], const int (&xs)[YB_PER_LANE],
@@ -537,7 +557,8 @@ __device__ void y_op_bucketed(const AssignDev &a, int y, const Lists &L,
     const int lane = threadIdx.x & 31;
     const int cnt = __ldcg(a.ybcnt + y);
     const int ey = __ldcg(a.ey + y);
-    if (cnt > YBUCKET || ey >= cnt) {       // bucket overflow (or inconsistent): scan match[] instead
+    if (cnt > YBUCKET || ey > cnt) {        // bucket overflow (or inconsistent): scan match[] instead
+        if (lane == 0) { atomicAdd(a.ops + 32, 1ull); atomicMax(a.ops + 33, (unsigned long long)cnt); }
         y_op<false>(a, y, L, pushes, relabels, s_sorted, tag);
         if (lane == 0) a.ybcnt[y] = 0;
         __syncwarp();
@@ -740,6 +761,8 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             // per row scan); longer lists get one warp per node
             const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
             unsigned long long t0 = timer ? globaltimer() : 0, t1 = 0;
+            const unsigned long long t_r0 = t0;
+            int hbin = 0;
             if (ny <= a.cta_y * (int)gridDim.x) {
                 for (int i = blockIdx.x; i < ny; i += gridDim.x)
                     y_op<true>(a, i == (int)blockIdx.x ? y_first : __ldcg(a.ylist[b] + i), LX, pushes, relabels,
@@ -753,7 +776,9 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
                     const int k = atomicAdd(a.ybcnt + y, 1);
                     if (k < YBUCKET) a.ybuf[(size_t)y * YBUCKET + k] = x;
                 }
+                if (timer) atomicAdd(a.ops + 34, globaltimer() - t0);
                 grid.sync();
+                if (timer) atomicAdd(a.ops + 35, globaltimer() - t0);
                 for (int i = gwarp; i < ny; i += gwarps)
                     y_op_bucketed(a, __ldcg(a.ylist[b] + i), LX, pushes, relabels,
                                   s_sorted[threadIdx.x >> 5], tag_y);
@@ -761,6 +786,7 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_Y, t1 - t0); t0 = t1; }
             grid.sync();
             if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC1, t1 - t0); t0 = t1; }
+            const unsigned long long t_y1 = t0;
             int nx, x_first, u2;
             cta_bcast3(a.cnt + C_X0 + b, (int)blockIdx.x < a.n ? a.xlist[b] + blockIdx.x : nullptr, nullptr, nx,
                        x_first, u2);
@@ -774,10 +800,15 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             if (timer) {
                 t1 = globaltimer(); atomicAdd(a.ops + O_PH_X, t1 - t0); t0 = t1;
                 const int m = max(ny, nx);
-                atomicAdd(a.ops + O_HIST + (m <= 8 ? 0 : m <= 32 ? 1 : m <= 148 ? 2 : m <= 592 ? 3 : 4), 1ull);
+                hbin = m <= 8 ? 0 : m <= 32 ? 1 : m <= 148 ? 2 : m <= 592 ? 3 : 4;
+                atomicAdd(a.ops + O_HIST + hbin, 1ull);
             }
             grid.sync();
-            if (timer) { t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC2, t1 - t0); }
+            if (timer) {
+                t1 = globaltimer(); atomicAdd(a.ops + O_PH_SYNC2, t1 - t0);
+                atomicAdd(a.ops + O_HIST_NS + hbin, t1 - t_r0);
+                if (hbin == 4) { atomicAdd(a.ops + 30, t_y1 - t_r0); atomicAdd(a.ops + 31, t1 - t_y1); }
+            }
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_ROUND] = r;
@@ -1474,6 +1505,7 @@ struct fm_assign {
     int opt_pu_local = 0;            // price update: work-first continuation of a group's first re-queued Y
     int opt_pu_groups = 2;           // r02h3: with the filtered scan 2 groups per CTA beat 4 (M10000 47.4 -> 44.4 ms)
     int opt_pu_filter = 1;           // price update: filtered column scans at 2 CTAs per SM
+    int opt_round_ctas = 0;          // refine rounds: cooperative CTAs (0 = one per SM)
     int32_t flags = 0;
     fm_stats st{};
 };
@@ -1585,7 +1617,7 @@ int assign_one_refine(fm_assign *A) {
         d.vbase += 1 << 21;   // fresh validate phase tags per launch
         void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold,
                         (void *)&no_cap, (void *)&every_k};
-        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
+        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->opt_round_ctas > 0 ? std::min(A->opt_round_ctas, A->coop_blocks) : A->coop_blocks),
                                                   dim3(ATHREADS), args, 0, s));
         A->st.launches++;
         FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, d.cnt, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, s));
@@ -1657,9 +1689,17 @@ int assign_finish(fm_assign *A, int rc, int64_t *objective_out, int32_t *match_o
                 A->h_ops[O_PU_YLAB] / npu, 1e-3 * A->h_ops[O_PU_SCANNS] / std::max(1.0, (double)A->h_ops[O_PU_YS]));
     }
     if (A->opt_trace)
-        fprintf(stderr, "[fm_assign] grid rounds by max list size: <=8 %llu, <=32 %llu, <=148 %llu, <=592 %llu, more %llu; "
-                "tail rounds %llu\n", A->h_ops[O_HIST], A->h_ops[O_HIST + 1], A->h_ops[O_HIST + 2], A->h_ops[O_HIST + 3],
-                A->h_ops[O_HIST + 4], A->h_ops[O_TAIL_ROUNDS]);
+        fprintf(stderr, "[fm_assign] grid rounds by max list size (count / ms): <=8 %llu / %.2f, <=32 %llu / %.2f, "
+                "<=148 %llu / %.2f, <=592 %llu / %.2f, more %llu / %.2f; tail rounds %llu\n",
+                A->h_ops[O_HIST], 1e-6 * A->h_ops[O_HIST_NS], A->h_ops[O_HIST + 1], 1e-6 * A->h_ops[O_HIST_NS + 1],
+                A->h_ops[O_HIST + 2], 1e-6 * A->h_ops[O_HIST_NS + 2], A->h_ops[O_HIST + 3], 1e-6 * A->h_ops[O_HIST_NS + 3],
+                A->h_ops[O_HIST + 4], 1e-6 * A->h_ops[O_HIST_NS + 4], A->h_ops[O_TAIL_ROUNDS]);
+    if (A->opt_trace)
+        fprintf(stderr, "[fm_assign] rounds with > 592 listed: Y phase + barrier %.2f ms, X phase + barrier %.2f ms; "
+                "bucketed Y phases: bucket pass %.2f ms, + barrier %.2f ms; bucket fallbacks %llu; gather overflows %llu (%llu units, "
+                "max candidates %llu)\n",
+                1e-6 * A->h_ops[30], 1e-6 * A->h_ops[31], 1e-6 * A->h_ops[34], 1e-6 * A->h_ops[35], A->h_ops[32], A->h_ops[36],
+                A->h_ops[37], A->h_ops[33]);
     A->st.reserved[3] = (int64_t)A->h_ops[O_TAIL_OPS];   // ops done by the single-CTA tail
     A->st.ms_cut = 1e-6 * (double)A->h_ops[O_TAIL_NS];   // time in single-CTA tail rounds
     A->st.ms_d2h = 1e-6 * (double)A->h_ops[O_MULTI_NS];  // time in grid-wide rounds
@@ -1978,7 +2018,7 @@ extern "C" int fm_assign_round(fm_assign *A, int32_t cycle_budget, int64_t *out)
         int every_k = 0;
         void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold,
                         (void *)&cap, (void *)&every_k};
-        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->coop_blocks),
+        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->opt_round_ctas > 0 ? std::min(A->opt_round_ctas, A->coop_blocks) : A->coop_blocks),
                                                   dim3(ATHREADS), args, 0, s));
         A->st.launches++;
         FM_TRY(assign_sync_cnt(A));
@@ -2082,6 +2122,7 @@ extern "C" int fm_assign_set_option(fm_assign *A, const char *name, int64_t valu
     else if (!strcmp(name, "pu_ring")) A->opt_pu_ring = v;
     else if (!strcmp(name, "pu_local")) A->opt_pu_local = v;
     else if (!strcmp(name, "pu_filter")) A->opt_pu_filter = v;
+    else if (!strcmp(name, "round_ctas")) A->opt_round_ctas = std::max(0, v);
     else if (!strcmp(name, "trace")) A->opt_trace = v;
     else if (!strcmp(name, "pu_threshold")) A->opt_pu_threshold = v;
     else if (!strcmp(name, "tail_threshold")) A->opt_tail_threshold = v;
