@@ -130,14 +130,16 @@ int fm_grid_solve_host(fm_grid *g, const int32_t *capR, const int32_t *capL,
                        fm_stats *stats);
 
 /* A batch of `count` independent H x W instances from HOST planes (caps[6 k + p] =
- * plane p of instance k, in the order capR, capL, capD, capU, capS, capT), pipelined:
+ * plane p of instance k, in the order capR, capL, capD, capU, capS, capT; elements of
+ * elem_bytes = 4 (int32), 2 (uint16) or 1 (uint8): narrow planes cross PCIe narrow and
+ * are widened on the device), pipelined:
  * the H2D of instance k+1 and the D2H of instance k-1's cut overlap the solve of
  * instance k.  flows_out[count]; cuts_out[count] host arrays (NULL, or an entry NULL:
  * no cut for it); stats: NULL or count entries.  Each result equals
  * fm_grid_solve_host's.  No reference counterpart: the reference solves one network
  * per hybrid_solve call (maxflow_par.py:157-238); a caller's loop over images maps to
  * one call. */
-int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const int32_t *const *caps,
+int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const void *const *caps, int32_t elem_bytes,
                              int32_t cycle_budget, int32_t bfs_interval, int32_t flags,
                              int64_t *flows_out, uint8_t *const *cuts_out, fm_stats *stats);
 

@@ -80,7 +80,7 @@ SIGNATURES = {
     "fm_grid_destroy": (None, [_vp]),
     "fm_grid_solve": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "fm_grid_solve_host": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32, _i32, _i32, _vp, _vp, _vp]),
-    "fm_grid_solve_host_batch": (ctypes.c_int, [_vp, _i32, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "fm_grid_solve_host_batch": (ctypes.c_int, [_vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "fm_grid_begin": (ctypes.c_int, [_vp] + [_vp] * 6 + [_i32]),
     "fm_grid_round": (ctypes.c_int, [_vp, _i32, _i32, _vp, _vp]),
     "fm_grid_export": (ctypes.c_int, [_vp] + [_vp] * 11),

@@ -1216,6 +1216,25 @@ struct PrCtl {
 // solve's 400 MB plane transfer (fm_grid_solve_host_batch)
 __global__ void prctl_set_kernel(PrCtl *dst, PrCtl v) { *dst = v; }
 
+// Narrow host capacity planes (uint8 / uint16, fm_grid_solve_host_batch elem_bytes 1 / 2)
+// cross PCIe narrow and are widened to the int32 input planes on the device: 16 bytes of
+// narrow values per thread step, stored as int4 (HBM-bound, ~0.1 ms for six 4096^2 planes
+// against 5.5 ms less PCIe).
+template <typename T>
+__global__ void widen_planes_kernel(const T *src, int32_t *dst, int64_t n) {
+    constexpr int PER = 16 / sizeof(T);
+    const int64_t nv = n / PER;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(src) + i);
+        const T *e = reinterpret_cast<const T *>(&v);
+        int4 *o = reinterpret_cast<int4 *>(dst + i * PER);
+#pragma unroll
+        for (int k = 0; k < PER / 4; k++) __stcs(o + k, make_int4(e[4 * k], e[4 * k + 1], e[4 * k + 2], e[4 * k + 3]));
+    }
+    for (int64_t i = nv * PER + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+}
+
 #ifndef FM_PK_MINBLOCKS
 #define FM_PK_MINBLOCKS 8
 #endif
@@ -3022,6 +3041,8 @@ struct fm_grid {
     // fm_grid_solve_host_batch: a second input set, two device / pinned cut stages and
     // the copy streams (H2D of instance k+1 and D2H of instance k-1 overlap solve k)
     int32_t *in_caps2 = nullptr;
+    uint8_t *b_narrow[2] = {nullptr, nullptr};   // narrow (uint8 / uint16) plane staging
+    size_t b_narrow_bytes = 0;
     uint8_t *b_dcut[2] = {nullptr, nullptr};
     uint8_t *b_hcut[2] = {nullptr, nullptr};
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
@@ -4020,6 +4041,7 @@ extern "C" void fm_grid_destroy(fm_grid *g) {
     if (g->h_cut_stage) cudaFreeHost(g->h_cut_stage);
     if (g->in_caps2) cudaFree(g->in_caps2);
     for (int k = 0; k < 2; k++) {
+        if (g->b_narrow[k]) cudaFree(g->b_narrow[k]);
         if (g->b_dcut[k]) cudaFree(g->b_dcut[k]);
         if (g->b_hcut[k]) cudaFreeHost(g->b_hcut[k]);
     }
@@ -4161,10 +4183,11 @@ extern "C" int fm_grid_solve_host(fm_grid *g, const int32_t *capR, const int32_t
 // arrays) run while instance k solves, so a stream of images costs
 // max(solve, PCIe) per image instead of their sum.  Every instance's copies are still
 // made (nothing cached across instances); results are those of fm_grid_solve_host.
-extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const int32_t *const *caps,
+extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const void *const *caps, int32_t elem_bytes,
                                         int32_t cycle_budget, int32_t bfs_interval, int32_t flags,
                                         int64_t *flows_out, uint8_t *const *cuts_out, fm_stats *stats) {
-    if (!g || count < 0 || (count > 0 && (!caps || !flows_out)) || cycle_budget < 1) {
+    if (!g || count < 0 || (count > 0 && (!caps || !flows_out)) || cycle_budget < 1 ||
+        (elem_bytes != 1 && elem_bytes != 2 && elem_bytes != 4)) {
         fm_set_error("fm_grid_solve_host_batch: invalid argument");
         return FM_INVALID_ARG;
     }
@@ -4178,6 +4201,16 @@ extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const int32_t
     const bool want_cut = cuts_out && !(flags & FM_GRID_NO_CUT);
     if (!g->in_caps) FM_CHECK_CUDA(cudaMalloc((void **)&g->in_caps, sizeof(int32_t) * 6 * HW));
     if (count > 1 && !g->in_caps2) FM_CHECK_CUDA(cudaMalloc((void **)&g->in_caps2, sizeof(int32_t) * 6 * HW));
+    const size_t nbytes = (size_t)elem_bytes * 6 * HW;
+    if (elem_bytes < 4 && g->b_narrow_bytes < nbytes) {
+        for (int b = 0; b < 2; b++) {
+            if (g->b_narrow[b]) cudaFree(g->b_narrow[b]);
+            g->b_narrow[b] = nullptr;
+        }
+        g->b_narrow_bytes = 0;
+        for (int b = 0; b < 2; b++) FM_CHECK_CUDA(cudaMalloc((void **)&g->b_narrow[b], nbytes));
+        g->b_narrow_bytes = nbytes;
+    }
     if (!g->h2d_stream) FM_CHECK_CUDA(cudaStreamCreateWithFlags(&g->h2d_stream, cudaStreamNonBlocking));
     if (!g->d2h_stream) FM_CHECK_CUDA(cudaStreamCreateWithFlags(&g->d2h_stream, cudaStreamNonBlocking));
     if (want_cut)
@@ -4194,12 +4227,13 @@ extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const int32_t
         return e;
     };
     // H2D of instance k into input set k % 2 (the set of instance k-2, whose solve the
-    // host has already waited for)
+    // host has already waited for); narrow planes land in the staging set k % 2
     const auto h2d = [&](int k) -> cudaEvent_t {
-        int32_t *dst = inbuf[k & 1];
+        uint8_t *dst = elem_bytes == 4 ? reinterpret_cast<uint8_t *>(inbuf[k & 1]) : g->b_narrow[k & 1];
+        const size_t pb = (size_t)elem_bytes * HW;
         for (int p = 0; p < 6; p++)
-            if (cudaMemcpyAsync(dst + p * HW, caps[6 * k + p], sizeof(int32_t) * HW, cudaMemcpyHostToDevice,
-                                g->h2d_stream) != cudaSuccess) return nullptr;
+            if (cudaMemcpyAsync(dst + p * pb, caps[6 * k + p], pb, cudaMemcpyHostToDevice, g->h2d_stream) != cudaSuccess)
+                return nullptr;
         cudaEvent_t e = mkev();
         cudaEventRecord(e, g->h2d_stream);
         return e;
@@ -4232,6 +4266,22 @@ extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const int32_t
         cudaEvent_t next = nullptr;
         if (k + 1 < count && !(next = h2d(k + 1))) { fm_set_error("fm_grid_solve_host_batch: H2D failed"); rc = FM_CUDA_ERROR; break; }
         FM_CHECK_CUDA(cudaStreamWaitEvent(g->stream, ready, 0));
+        cudaEvent_t tw0 = nullptr, tw1 = nullptr;
+        const auto t_host0 = std::chrono::steady_clock::now();
+        if (g->trace) {
+            cudaEventCreate(&tw0); cudaEventCreate(&tw1); evs.push_back(tw0); evs.push_back(tw1);
+            cudaEventRecord(tw0, g->stream);
+        }
+        if (elem_bytes < 4) {
+            const int blocks = g->sms * 8;
+            if (elem_bytes == 1)
+                widen_planes_kernel<uint8_t><<<blocks, 256, 0, g->stream>>>(g->b_narrow[k & 1], inbuf[k & 1], (int64_t)(6 * HW));
+            else
+                widen_planes_kernel<uint16_t><<<blocks, 256, 0, g->stream>>>(
+                    reinterpret_cast<const uint16_t *>(g->b_narrow[k & 1]), inbuf[k & 1], (int64_t)(6 * HW));
+            FM_CHECK_LAUNCH();
+        }
+        if (g->trace) cudaEventRecord(tw1, g->stream);
         const int32_t *c = inbuf[k & 1];
         int64_t flow = 0;
         rc = solve_device(g, c, c + HW, c + 2 * HW, c + 3 * HW, c + 4 * HW, c + 5 * HW, cycle_budget, bfs_interval,
@@ -4239,6 +4289,13 @@ extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const int32_t
         if (rc != FM_OK) break;
         flows_out[k] = flow;
         if (stats) stats[k] = g->st;
+        if (g->trace) {
+            float wms = 0.f;
+            cudaEventElapsedTime(&wms, tw0, tw1);
+            const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+            fprintf(stderr, "[fm_grid] batch step %d: wait + widen %.3f ms, solve %.3f ms (device), step host %.3f ms\n", k, wms,
+                    g->st.ms_total, host_ms);
+        }
         if (want_cut && cuts_out[k]) {
             const int b = k & 1;
             if (copier[b].joinable()) copier[b].join();   // stage b is free again

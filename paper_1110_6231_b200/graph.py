@@ -205,6 +205,18 @@ class GridNetwork(FlowNetwork):
             out.append(a.astype(np.int32))
         return tuple(out)
 
+    @property
+    def narrow_bytes(self) -> int:
+        """1 or 2 when the six host planes are C-contiguous uint8 / uint16 arrays of one
+        dtype (they then cross PCIe narrow and are widened on the device), else 0."""
+        if self.on_device:
+            return 0
+        dt = getattr(self.caps[0], "dtype", None)
+        if dt not in (np.uint8, np.uint16):
+            return 0
+        ok = all(isinstance(a, np.ndarray) and a.dtype == dt and a.flags.c_contiguous for a in self.caps)
+        return int(np.dtype(dt).itemsize) if ok else 0
+
     def wide_caps(self):
         """The six planes as C-contiguous int64 numpy arrays."""
         return tuple(_host_plane(name, a) for name, a in zip(_PLANES, self.caps))
@@ -213,7 +225,7 @@ class GridNetwork(FlowNetwork):
     def wide(self) -> bool:
         """True when a capacity leaves the int32 range (host planes only)."""
         return not self.on_device and any(
-            a.dtype != np.int32 and a.size and int(np.asarray(a).max()) >= 2**31 for a in self.caps)
+            _may_leave_int32(a.dtype) and a.size and int(np.asarray(a).max()) >= 2**31 for a in self.caps)
 
     def arc_arrays(self):
         """(tails, heads, caps) of the reference network in adapter order:
@@ -266,6 +278,13 @@ class GridNetwork(FlowNetwork):
         if not self._materialised:
             self.materialise()
         return len(self.tail)
+
+
+def _may_leave_int32(dt) -> bool:
+    """Whether values of this dtype can leave the int32 range (narrow integer planes
+    never can: no scan needed)."""
+    dt = np.dtype(dt)
+    return not (dt == np.int32 or dt == np.bool_ or (np.issubdtype(dt, np.integer) and dt.itemsize < 4))
 
 
 def _host_plane(name, a):
@@ -328,15 +347,19 @@ def build_grid_network(capR, capL, capD, capU, capS, capT) -> GridNetwork:
         capR, capL, capD, capU = planes[:4]
         edge = torch.stack([capR[:, -1].any(), capL[:, 0].any(), capD[-1, :].any(), capU[0, :].any()]).cpu().tolist()
     else:
-        # int32 planes are kept as given (no copy: pinned caller buffers stay pinned);
-        # wider ones are range-checked and stay int64 only when a value needs it
-        planes = tuple(a if isinstance(a, np.ndarray) and a.dtype == np.int32 else _host_plane(name, a)
+        # int32 planes are kept as given (no copy: pinned caller buffers stay pinned), so
+        # are six uint8 / uint16 planes of one dtype (they cross PCIe narrow); other
+        # integer planes are range-checked and stay int64 only when a value needs it
+        dt = getattr(net.caps[0], "dtype", None)
+        keep = (np.int32,) + ((dt,) if dt in (np.uint8, np.uint16) and
+                              all(getattr(a, "dtype", None) == dt for a in net.caps) else ())
+        planes = tuple(np.ascontiguousarray(a) if isinstance(a, np.ndarray) and a.dtype in keep else _host_plane(name, a)
                        for name, a in zip(_PLANES, net.caps))
         for name, a in zip(_PLANES, planes):
-            if a.size and int(a.min()) < 0:
+            if a.size and a.dtype.kind != "u" and int(a.min()) < 0:   # unsigned planes need no scan
                 raise NetworkError(f"{name}: negative capacity {int(a.min())}")
-        if not any(a.dtype != np.int32 and a.size and int(a.max()) >= 2**31 for a in planes):
-            planes = tuple(a if a.dtype == np.int32 else a.astype(np.int32) for a in planes)
+        if not any(a.dtype not in keep and a.size and int(a.max()) >= 2**31 for a in planes):
+            planes = tuple(a if a.dtype in keep else a.astype(np.int32) for a in planes)
         capR, capL, capD, capU = planes[:4]
         edge = [capR[:, -1].any(), capL[:, 0].any(), capD[-1, :].any(), capU[0, :].any()]
     if edge[0]:

@@ -91,22 +91,27 @@ class GridSolver:
         k-1 overlap the solve of instance k).  Returns [(flow, cut, stats)], each equal
         to solve_host's result for that instance."""
         planes = []
+        caps_list = list(caps_list)
+        # uint8 / uint16 planes (all of one dtype) cross PCIe narrow, widened on the device
+        dts = {getattr(a, "dtype", None) for caps in caps_list for a in caps}
+        narrow = next(iter(dts)) if len(dts) == 1 and next(iter(dts)) in (np.uint8, np.uint16) else None
         for caps in caps_list:
             if len(caps) != 6:
                 raise ValueError("each instance needs the six planes capR, capL, capD, capU, capS, capT")
-            cs = [np.ascontiguousarray(a, dtype=np.int32) for a in caps]
+            cs = [np.ascontiguousarray(a, dtype=narrow or np.int32) for a in caps]
             for a in cs:
                 if a.shape != (self.H, self.W):
                     raise ValueError(f"plane shape {a.shape} does not match the solver's {(self.H, self.W)}")
             planes.append(cs)
         n = len(planes)
+        eb = np.dtype(narrow).itemsize if narrow is not None else 4
         ptrs = (ctypes.c_void_p * max(1, 6 * n))(*[_lib.ptr(a) for cs in planes for a in cs])
         flows = np.zeros(max(1, n), np.int64)
         cuts = [np.empty((self.H, self.W), np.bool_) for _ in range(n)] if want_cut else None
         cptr = (ctypes.c_void_p * max(1, n))(*[_lib.ptr(c) for c in cuts]) if want_cut else None
         sts = (_lib.FmStats * max(1, n))()
         rc = _lib.load().fm_grid_solve_host_batch(
-            self._h, n, ptrs, int(cycle_budget), int(bfs_interval),
+            self._h, n, ptrs, int(eb), int(cycle_budget), int(bfs_interval),
             self._flags(cancel_violations, want_cut, precancel), _lib.ptr(flows), cptr, sts)
         _lib.check(rc, "fm_grid_solve_host_batch")
         out = [(int(flows[k]), cuts[k] if want_cut else None, sts[k].as_dict()) for k in range(n)]
@@ -301,6 +306,10 @@ def hybrid_solve(net: FlowNetwork, worker_count: int = 4, cycle_budget: int = DE
                                                   cancel_violations=cancel_violations,
                                                   stream=torch.cuda.current_stream(caps[0].device))
                 cut = cut_t.bool() if cut_t is not None else None
+            elif net.narrow_bytes:
+                # uint8 / uint16 planes: narrow H2D + device widening (one-instance batch)
+                flow, cut, stats = solver.solve_host_batch([net.caps], cycle_budget, bfs_interval, want_cut=want_cut,
+                                                           cancel_violations=cancel_violations)[0]
             else:
                 try:
                     flow, cut, stats = solver.solve_host(net.host_caps(), cycle_budget, bfs_interval,
@@ -358,7 +367,8 @@ def hybrid_solve_batch(nets, worker_count: int = 4, cycle_budget: int = DEFAULT_
     device = 0 if device is None else int(device)
     started = time.perf_counter()
     with _solvers.use((H, W, device), device, lambda: GridSolver(H, W, device)) as solver:
-        res = solver.solve_host_batch([net.host_caps() for net in nets], cycle_budget, bfs_interval,
+        narrow = all(net.narrow_bytes for net in nets) and len({net.caps[0].dtype for net in nets}) == 1
+        res = solver.solve_host_batch([net.caps if narrow else net.host_caps() for net in nets], cycle_budget, bfs_interval,
                                       want_cut=want_cut, cancel_violations=cancel_violations)
     per = (time.perf_counter() - started) / len(nets)
     return [SolveReport(objective=int(f), pushes=int(st.get("pushes", 0)), relabels=int(st.get("relabels", 0)),

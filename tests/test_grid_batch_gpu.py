@@ -75,3 +75,34 @@ def test_batch_reuses_solver_across_calls():
     second = fmb.hybrid_solve_batch(nets[::-1])
     for a, b in zip(first, second[::-1]):
         assert a.objective == b.objective and (a.cut == b.cut).all()
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16])
+@pytest.mark.parametrize("H,W", [(33, 7), (64, 96), (512, 512)])
+def test_narrow_planes_match_int32(dtype, H, W):
+    """uint8 / uint16 host planes cross PCIe narrow and are widened on the device
+    (vector body + scalar tail): same flow and cut as the int32 planes, single call and
+    batch."""
+    caps = [G.grid_random(H, W, 100 + k) for k in range(3)]
+    want = [fmb.hybrid_solve(fmb.build_grid_network(*c)) for c in caps]
+    nets = [fmb.build_grid_network(*[a.astype(dtype) for a in c]) for c in caps]
+    assert all(n.narrow_bytes == np.dtype(dtype).itemsize for n in nets)
+    single = fmb.hybrid_solve(nets[0])
+    assert single.objective == want[0].objective and (single.cut == want[0].cut).all()
+    for r, w in zip(fmb.hybrid_solve_batch(nets), want):
+        assert r.objective == w.objective and (r.cut == w.cut).all()
+
+
+def test_narrow_planes_large_values_uint16():
+    """uint16 capacities up to 65535 (packed-residual limits exercised by the int32 path's
+    checks) give the int32 planes' result."""
+    rng = np.random.default_rng(5)
+    H, W = 96, 128
+    caps = [rng.integers(0, 65536, size=(H, W)).astype(np.int32) for _ in range(6)]
+    caps[0][:, -1] = 0
+    caps[1][:, 0] = 0
+    caps[2][-1, :] = 0
+    caps[3][0, :] = 0
+    want = fmb.hybrid_solve(fmb.build_grid_network(*caps))
+    got = fmb.hybrid_solve(fmb.build_grid_network(*[a.astype(np.uint16) for a in caps]))
+    assert got.objective == want.objective and (got.cut == want.cut).all()

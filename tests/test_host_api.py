@@ -197,3 +197,23 @@ def test_dimacs_max_keeps_wide_capacities():
     assert cp.dtype == np.int64 and cp.tolist() == [2**40, 5]
     net = dimacs.parse_dimacs_max("p max 3 1\nn 1 s\nn 3 t\na 1 3 9223372036854775807\n")
     assert net.capacity[0] == 2**63 - 1
+
+
+def test_narrow_host_planes_kept_and_validated():
+    """Six uint8 (or uint16) host planes of one dtype are kept narrow (they cross PCIe
+    narrow); mixed dtypes are widened to int32; edge checks apply either way."""
+    import numpy as np
+    import paper_1110_6231_b200 as fmb
+    from paper_1110_6231_b200 import generators as G
+    from paper_1110_6231_b200.graph import NetworkError
+    c = G.grid_random(20, 30, 1)
+    n8 = fmb.build_grid_network(*[a.astype(np.uint8) for a in c])
+    assert n8.narrow_bytes == 1 and n8.caps[4].dtype == np.uint8
+    assert all((a == b).all() for a, b in zip(n8.host_caps(), c))
+    assert fmb.build_grid_network(*[a.astype(np.uint16) for a in c]).narrow_bytes == 2
+    mixed = fmb.build_grid_network(*([c[0].astype(np.uint8)] + list(c[1:])))
+    assert mixed.narrow_bytes == 0 and all(a.dtype == np.int32 for a in mixed.caps)
+    bad = [a.astype(np.uint8) for a in c]
+    bad[2][-1, 3] = 1
+    with pytest.raises(NetworkError):
+        fmb.build_grid_network(*bad)
