@@ -675,6 +675,7 @@ struct PlTile {
     const uint8_t *f;
     int *nbr;                  // bit d: flow was parked in the inbox of neighbour tile d
     int r0, c0;
+    uint8_t *dirty;            // row lr changed in this visit (plain stores of 1: benign races)
 };
 
 // The default operation (steps == 1, not fused: one maxflow_par.py:98-125 operation
@@ -702,6 +703,7 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
     const int32_t hR = vh[hi + 1], hL = vh[hi - 1], hD = vh[hi + HS], hU = vh[hi - HS];
     if ((f & 2) || e <= 0 || hp >= V) return false;
     if (rt > 0) {                                          // sink at height 0
+        T.dirty[lr] = 1;
         if (hp == 0) { vh[hi] = 1; relabels++; }
         const int32_t d = min(e, rt);
         vt[li] = rt - d;
@@ -716,6 +718,7 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
     if (ru > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
     if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
     if (dir < 0) return false;                             // nothing residual: rescanned on next load
+    T.dirty[lr] = 1;                                       // a relabel or a push follows
     if (hp <= best_h) {                                    // relabel (owner-only); the push waits
         vh[hi] = best_h + 1;
         relabels++;
@@ -731,6 +734,7 @@ __device__ __forceinline__ bool pl_op1(const GridDev &g, const PlTile &T, int li
     pushes++;
     if (qr >= 0 && qr < PT_H && qc >= 0 && qc < PT_W) {
         const int qi = qr * PT_W + qc;
+        T.dirty[qr] = 1;
         atomicAdd(&T.r[dir ^ 1][qi], d);
         const int32_t old = atomicAdd(&T.e[qi], d);
         if (old <= 0 && old + d > 0) *recv = qi;
@@ -762,6 +766,7 @@ __device__ __forceinline__ bool pk_op1(const GridDev &g, const PlTile &T, int li
     const int32_t hR = vh[hi + 1], hL = vh[hi - 1], hD = vh[hi + HS], hU = vh[hi - HS];
     if ((f & 2) || e <= 0 || hp >= V) return false;
     if (rt > 0) {                                          // sink at height 0
+        T.dirty[lr] = 1;
         if (hp == 0) { vh[hi] = 1; relabels++; }
         const int32_t d = min(e, rt);
         vt[li] = rt - d;
@@ -778,6 +783,7 @@ __device__ __forceinline__ bool pk_op1(const GridDev &g, const PlTile &T, int li
     if (ru > 0 && hU < best_h) { best_h = hU; best_r = ru; dir = 3; }
     if ((f & 1) && V < best_h) { best_h = V; dir = 5; }
     if (dir < 0) return false;
+    T.dirty[lr] = 1;
     if (hp <= best_h) {
         vh[hi] = best_h + 1;
         relabels++;
@@ -792,6 +798,7 @@ __device__ __forceinline__ bool pk_op1(const GridDev &g, const PlTile &T, int li
     pushes++;
     if (qr >= 0 && qr < PT_H && qc >= 0 && qc < PT_W) {
         const int qi = qr * PT_W + qc;
+        T.dirty[qr] = 1;
         atomicAdd(&rw[2 * qi + (dir >> 1)], (uint32_t)d << (16 * ((dir & 1) ^ 1)));
         const int32_t old = atomicAdd(&T.e[qi], d);
         if (old <= 0 && old + d > 0) *recv = qi;
@@ -899,6 +906,7 @@ template <bool PK> struct __align__(128) PlSmemT {
     int32_t h[PL_HWORDS];
     PlRes<PK> res;
     uint8_t f[PT_H * PT_W];      // bit 0: residual arc to s, bit 1: outside the grid
+    uint8_t dirty[PT_H];         // rows a visit changed (only those are written back)
     unsigned long long mbar;     // TMA completion barrier (one per CTA, phase flips per visit)
     int cnt[3];
     int nbr;
@@ -930,8 +938,10 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
 #endif
     const int tyi = tile / g.ntx, txi = tile - tyi * g.ntx;
     PlTile T;
-    if constexpr (PK) T = PlTile{S.e, S.h, S.t, nullptr, S.res.r2, S.f, &S.nbr, tyi * PT_H, txi * PT_W};
-    else T = PlTile{S.e, S.h, S.t, S.res.r, nullptr, S.f, &S.nbr, tyi * PT_H, txi * PT_W};
+    if constexpr (PK) T = PlTile{S.e, S.h, S.t, nullptr, S.res.r2, S.f, &S.nbr, tyi * PT_H, txi * PT_W, S.dirty};
+    else T = PlTile{S.e, S.h, S.t, S.res.r, nullptr, S.f, &S.nbr, tyi * PT_H, txi * PT_W, S.dirty};
+    // the generic item path (steps > 1 or fused) writes every row back
+    if (tid < PT_H) S.dirty[tid] = (steps == 1 && !fused) ? 0 : 1;
     const int r0 = T.r0, c0 = T.c0;
     int32_t *stage = (int32_t *)&S.list[0][0];   // rS staging (the lists are built afterwards)
     // load.  TMA (maps != nullptr): one thread issues the plane copies, the halo rows and
@@ -1053,6 +1063,7 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
     if (peer_hidx >= 0) S.h[peer_hidx] = peer_h;
     __syncthreads();
     if (inbox) {
+        S.dirty[ib_li >> 5] = 1;
         atomicAdd(&S.e[ib_li], inbox);          // a corner pixel has two inboxes
         if constexpr (PK) atomicAdd(reinterpret_cast<uint32_t *>(S.res.r2) + 2 * ib_li + (ib_dir >> 1), (uint32_t)inbox << (16 * (ib_dir & 1)));
         else S.res.r[ib_dir][ib_li] += inbox;
@@ -1177,6 +1188,8 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
         if (r < g.H && c < g.W) {
             const int64_t p = (int64_t)r * g.W + c;
             const int32_t e = S.e[li], h = S.h[(lr + 1) * HS + PL_HC + tx];
+            act |= (e > 0 && h < V && !(S.f[li] & 2));
+            if (!S.dirty[lr]) continue;   // untouched row (warp-uniform): global state unchanged
             g.e[p] = e;
             g.h[p] = h;
             if constexpr (PK) {
@@ -1188,7 +1201,6 @@ __device__ __forceinline__ bool pl_visit(const GridDev &g, PlSmemT<PK> &S, int t
                 g.rD[p] = S.res.r[2][li]; g.rU[p] = S.res.r[3][li];
             }
             g.rT[p] = S.t[li];
-            act |= (e > 0 && h < V && !(S.f[li] & 2));
         }
     }
     const bool any = __syncthreads_or(act) != 0;
