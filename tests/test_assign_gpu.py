@@ -236,3 +236,23 @@ def test_price_update_barrier_and_queue_variants(ring, filt):
     finally:
         solver.close()
     assert obj == int(w[r, c].astype(np.int64).sum()) and sorted(m) == list(range(n))
+
+
+@pytest.mark.parametrize("opts", [{"round_ctas": 16}, {"round_ctas": 64}, {"pu_groups": 1}, {"pu_groups": 8},
+                                  {"pu_groups": 4, "pu_filter": 0}, {"tail_threshold": 8}, {"cta_x": 1, "cta_y": 1}])
+def test_refine_launch_shape_variants(opts):
+    """Fewer cooperative CTAs, other price-update group counts, a longer single-CTA tail
+    (shared-memory lists past TL_CAP spill to the global list) and warp ops for every
+    list: the same optimum (scipy) and a valid certificate."""
+    from scipy.optimize import linear_sum_assignment
+    for n, M in ((64, 10000), (333, 100), (1024, 10000), (1024, 3)):
+        w = G.assignment_reference(n, M, n + 11)
+        solver = fmb.AssignmentSolver(n, options=opts)
+        try:
+            obj, m, prices, _ = solver.solve_host(w, want_prices=True)
+        finally:
+            solver.close()
+        r, c = linear_sum_assignment(w.astype(np.int64), maximize=True)
+        assert obj == int(w[r, c].sum()), (opts, n, M)
+        code, cobj = oracle.assign_certify_dense(w, m, prices)
+        assert code == 0 and cobj == obj
