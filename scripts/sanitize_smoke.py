@@ -25,3 +25,10 @@ caps = [c.astype(np.int64) * 2**33 for c in G.grid_random(40, 50, 3)]
 print("wide grid", fmb.hybrid_solve(fmb.build_grid_network(*caps)).objective)
 caps = G.grid_random(120, 96, 5)
 s = fmb.GridSolver(120, 96, options={"ring_tail": 1}); print("ring_tail grid", s.solve_host(caps)[0]); s.close()
+# pipelined batch from host planes (int32 and uint8: narrow H2D + device widening)
+nets = [fmb.build_grid_network(*G.grid_random(64, 96, s)) for s in (1, 2, 3)]
+print("batch", [r.objective for r in fmb.hybrid_solve_batch(nets)])
+nets8 = [fmb.build_grid_network(*[a.astype(np.uint8) for a in G.grid_random(33, 7, s)]) for s in (4, 5)]
+print("batch u8", [r.objective for r in fmb.hybrid_solve_batch(nets8)])
+# assignment with a large-candidate gather (n = 1024, narrow weight range) and the filtered price update
+w = G.assignment_reference(1024, 3, 9); rep, m = fmb.solve_assignment(w); print("assign 1024", rep.objective)
