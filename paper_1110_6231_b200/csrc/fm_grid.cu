@@ -7,6 +7,7 @@
 // (maxflow_seq.py:119-160, maxflow_par.py:220-226), and the minimal source-side
 // cut by a seeded residual reach.  See DESIGN.md.
 #include <algorithm>
+#include <atomic>
 #include <string>
 #include <thread>
 #include <vector>
@@ -4267,14 +4268,32 @@ extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const void *c
         memcpy(dst, src, std::min(n, sl));
         for (auto &t : th) t.join();
     };
+    // the caller's cut arrays are usually fresh: one host thread touches their pages in
+    // order while the solves run (copy-out k waits until array k is done), so each
+    // copy-out runs at memory speed instead of page-fault speed
+    std::atomic<int> faulted{0};
+    std::atomic<bool> stop_fault{false};
+    std::thread prefault;
+    if (want_cut)
+        prefault = std::thread([&] {
+            for (int k = 0; k < count && !stop_fault.load(std::memory_order_relaxed); k++) {
+                if (cuts_out[k])
+                    for (size_t i = 0; i < HW; i += 4096) ((volatile uint8_t *)cuts_out[k])[i] = 0;
+                faulted.store(k + 1, std::memory_order_release);
+            }
+        });
     struct Cleanup {
         std::thread *c;
         std::vector<cudaEvent_t> &e;
+        std::thread &pf;
+        std::atomic<bool> &stop;
         ~Cleanup() {
+            stop.store(true);
+            if (pf.joinable()) pf.join();
             for (int b = 0; b < 2; b++) if (c[b].joinable()) c[b].join();
             for (auto x : e) cudaEventDestroy(x);
         }
-    } cleanup{copier, evs};
+    } cleanup{copier, evs, prefault, stop_fault};
     int rc = FM_OK;
     cudaEvent_t ready = h2d(0);
     if (!ready) { fm_set_error("fm_grid_solve_host_batch: H2D failed"); return FM_CUDA_ERROR; }
@@ -4324,6 +4343,7 @@ extern "C" int fm_grid_solve_host_batch(fm_grid *g, int32_t count, const void *c
             FM_CHECK_CUDA(cudaMemcpyAsync(g->b_hcut[b], g->b_dcut[b], HW, cudaMemcpyDeviceToHost, g->d2h_stream));
             cudaEvent_t landed = mkev();
             cudaEventRecord(landed, g->d2h_stream);
+            while (faulted.load(std::memory_order_acquire) <= k) std::this_thread::yield();   // array k touched
             copier[b] = std::thread(copy_out, cuts_out[k], g->b_hcut[b], HW, landed, g->device);
         }
         ready = next;
