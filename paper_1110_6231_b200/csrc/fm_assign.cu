@@ -100,7 +100,7 @@ struct AssignDev {
     int64_t max_bucket;    // scaled_cost_bound / eps + 2 (assign_scaling.py:232)
     int32_t pu_cap0;       // first label cap of the price update (0 = 8)
     int use_fix;
-    int ybatch_min;         // gathered Y op: rank-batch the push-back from this many units (env FM_YBATCH_MIN)
+    int ybatch_min;         // gathered Y op: rank-batch the push-back from this many units (option ybatch_min)
     int validate;          // validate=True: device-side invariant checks (codes V_*)
     int32_t *pw;           // validate: last phase tag that wrote each price word (X then Y)
     int32_t vbase;         // validate: tag base of this launch (phase tag = vbase + 2 r + 1|2)
@@ -1499,7 +1499,7 @@ struct fm_assign {
     long long alpha = 10, bound = 0, eps = 1, round_budget = 0;
     int pu_threshold = 0, tail_threshold = 1, pu_every_k = 0;
     // options (fm_assign_set_option; round-1 environment knobs)
-    int opt_ybatch_min = 2, opt_pu_ring = 1, opt_pu_threshold = -1, opt_tail_threshold = 1, opt_pu_cap = 256;
+    int opt_ybatch_min = 1, opt_pu_ring = 1, opt_pu_threshold = -1, opt_tail_threshold = 1, opt_pu_cap = 256;
     int opt_cta_x = 4, opt_cta_y = 4;
     int opt_trace = 0;               // price-update statistics line on stderr after each solve
     int opt_pu_local = 0;            // price update: work-first continuation of a group's first re-queued Y
