@@ -53,7 +53,9 @@ constexpr int C_ROUND = 6;               // next round index (persists across la
 constexpr int C_RELABELS = 7;            // relabels since the last price update
 constexpr int C_PU_CHG = 8;              // price update: changed flags [8], [9]
 constexpr int C_PU_LAST = 10;            // price update: max label over active nodes
-constexpr int C_COUNT = 12;
+constexpr int C_GATE = 11;               // enqueued-ahead launches: 0 rounds run, 1 price update runs, 2 refine over
+constexpr int C_PUN = 12;                // price updates run in this refine (gated launches)
+constexpr int C_COUNT = 13;
 // ops[] slots
 constexpr int O_PUSH = 0, O_RELABEL = 1, O_ROUNDS = 2, O_TAIL_ROUNDS = 3, O_FIXED = 4,
               O_PU = 5, O_PU_ITERS = 6, O_TAIL_OPS = 7, O_TAIL_NS = 8, O_MULTI_NS = 9,
@@ -657,8 +659,18 @@ __device__ __forceinline__ void cta_bcast3(const int32_t *p0, const int32_t *p1,
 __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, int tail_threshold,
                                                                  long long round_budget,
                                                                  int pu_threshold, int max_rounds,
-                                                                 int pu_every_k) {
+                                                                 int pu_every_k, int gated) {
     cg::grid_group grid = cg::this_grid();
+    // gated (launches enqueued ahead of the host's decision): run only when the gate says
+    // so; every CTA reads it before any CTA can rewrite it (the barrier), so all agree
+    if (gated) {
+        __shared__ int s_go;
+        if (threadIdx.x == 0) s_go = __ldcg(a.cnt + C_GATE) == 0 && __ldcg(a.cnt + C_INFEASIBLE) == 0;
+        __syncthreads();
+        const int go = s_go;
+        grid.sync();
+        if (!go) return;
+    }
     const int lane = threadIdx.x & 31;
     const int gwarp = (blockIdx.x * ATHREADS + threadIdx.x) >> 5;
     const int gwarps = (gridDim.x * ATHREADS) >> 5;
@@ -811,7 +823,10 @@ __global__ void __launch_bounds__(ATHREADS) refine_rounds_kernel(AssignDev a, in
             }
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[C_ROUND] = r;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.cnt[C_ROUND] = r;
+        if (gated) a.cnt[C_GATE] = a.cnt[C_EXIT] == 1 ? 1 : 2;   // same thread wrote C_EXIT
+    }
     if (lane == 0) {
         if (pushes) atomicAdd(a.ops + O_PUSH, pushes);
         if (relabels) atomicAdd(a.ops + O_RELABEL, relabels);
@@ -1077,7 +1092,10 @@ template <bool FILTER>
 #ifndef FM_PU_MINB
 #define FM_PU_MINB 2
 #endif
-__global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_update_kernel(AssignDev a, PuDev f) {
+__global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_update_kernel(AssignDev a, PuDev f, int gated) {
+    // gated: run only when the rounds asked for an update (the gate is rewritten only at
+    // this kernel's end, after its grid barriers, so every thread reads the same value)
+    if (gated && __ldcg(a.cnt + C_GATE) != 1) return;
     cg::grid_group grid = cg::this_grid();
     const int n = a.n;
     const int tid = blockIdx.x * ATHREADS + threadIdx.x, nthr = gridDim.x * ATHREADS;
@@ -1274,6 +1292,7 @@ __global__ void __launch_bounds__(ATHREADS, FILTER ? FM_PU_MINB : 1) price_updat
         f.rctr[0] = f.rctr[32] = f.rctr[64] = 0;
         atomicAdd(a.ops + O_PU, 1ull);
         atomicAdd(a.ops + O_PU_ITERS, (unsigned long long)it_total);
+        if (gated) { a.cnt[C_GATE] = 0; a.cnt[C_PUN] += 1; }   // the next enqueued rounds launch runs
     }
 }
 
@@ -1494,6 +1513,8 @@ struct fm_assign {
     PuDev pu{};
     int32_t *wt = nullptr;
     cudaEvent_t ev[4] = {};
+    cudaEvent_t ev_pu[8] = {};   // around the enqueued-ahead price updates
+    int pu_last_refine = 2;      // price updates of the previous refine (sizes the enqueue-ahead batch)
     bool pu_pending = false;
     // solve state (also drives the stepwise API)
     long long alpha = 10, bound = 0, eps = 1, round_budget = 0;
@@ -1527,6 +1548,7 @@ int assign_setup(fm_assign *A, const int32_t *w, int64_t alpha, int32_t flags) {
     A->alpha = alpha;
     A->flags = flags;
     memset(&A->st, 0, sizeof(A->st));
+    A->pu_last_refine = 2;
     cudaStream_t s = A->stream;
     cudaEventRecord(A->ev[2], s);
     FM_CHECK_CUDA(cudaMemsetAsync(d.px, 0, sizeof(int64_t) * n, s));
@@ -1588,8 +1610,8 @@ int assign_status(int why) {
 }
 
 // one price_update_heuristic launch (cooperative) on the solver's stream
-cudaError_t launch_price_update(fm_assign *A) {
-    void *pargs[] = {(void *)&A->d, (void *)&A->pu};
+cudaError_t launch_price_update(fm_assign *A, int gated = 0) {
+    void *pargs[] = {(void *)&A->d, (void *)&A->pu, (void *)&gated};
     const bool filt = A->opt_pu_filter != 0;
     return cudaLaunchCooperativeKernel(filt ? (void *)price_update_kernel<true> : (void *)price_update_kernel<false>,
                                        dim3(A->pu_blocks_k[filt ? 1 : 0]), dim3(ATHREADS), pargs, 0, A->stream);
@@ -1611,30 +1633,45 @@ int assign_one_refine(fm_assign *A) {
     begin_refine_kernel<<<std::max(1, std::min((n + AWARPS - 1) / AWARPS, A->sms * 4)), ATHREADS, 0, s>>>(d, 1);
     FM_CHECK_LAUNCH();
     A->st.launches += 2;
+    // The rounds kernel and the price update alternate until the refine is over.  The
+    // launches are enqueued PU_AHEAD pairs at a time with a device-side gate (C_GATE:
+    // the rounds set it to "price update" or "over", the update back to "rounds"), so
+    // the host reads the counters once per batch instead of once per price update;
+    // launches past the refine's end return at once.
+    // The batch size follows the previous refine's update count (no-op launches are not
+    // free: a gated rounds launch still pays its cooperative launch and one barrier).
+    constexpr int PU_AHEAD = 4;
+    const bool pu_on = (A->flags & FM_ASSIGN_PRICE_UPDATE) != 0;
+    int pus_done = 0;
     for (;;) {
-        int no_cap = 0;
-        int every_k = (A->flags & FM_ASSIGN_PRICE_UPDATE) ? A->pu_every_k : 0;
-        d.vbase += 1 << 21;   // fresh validate phase tags per launch
-        void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold,
-                        (void *)&no_cap, (void *)&every_k};
-        FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->opt_round_ctas > 0 ? std::min(A->opt_round_ctas, A->coop_blocks) : A->coop_blocks),
-                                                  dim3(ATHREADS), args, 0, s));
-        A->st.launches++;
+        int no_cap = 0, gated = 1;
+        int every_k = pu_on ? A->pu_every_k : 0;
+        const int pairs = pu_on ? std::max(1, std::min(PU_AHEAD, A->pu_last_refine - pus_done)) : 1;
+        for (int q = 0; q < pairs; q++) {
+            d.vbase += 1 << 21;   // fresh validate phase tags per launch
+            void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold,
+                            (void *)&no_cap, (void *)&every_k, (void *)&gated};
+            FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel,
+                                                      dim3(A->opt_round_ctas > 0 ? std::min(A->opt_round_ctas, A->coop_blocks) : A->coop_blocks),
+                                                      dim3(ATHREADS), args, 0, s));
+            A->st.launches++;
+            if (!pu_on) break;
+            cudaEventRecord(A->ev_pu[2 * q], s);
+            FM_CHECK_CUDA(launch_price_update(A, 1));
+            cudaEventRecord(A->ev_pu[2 * q + 1], s);
+            A->st.launches++;
+        }
         FM_CHECK_CUDA(cudaMemcpyAsync(A->h_cnt, d.cnt, sizeof(int32_t) * C_COUNT, cudaMemcpyDeviceToHost, s));
         FM_CHECK_CUDA(cudaStreamSynchronize(s));
-        if (A->pu_pending) {
+        for (int q = 0; pu_on && q < pairs; q++) {
             float ms = 0.f;
-            cudaEventElapsedTime(&ms, A->ev[0], A->ev[1]);
-            A->st.ms_bfs += ms;   // price-update kernels
-            A->pu_pending = false;
+            cudaEventElapsedTime(&ms, A->ev_pu[2 * q], A->ev_pu[2 * q + 1]);
+            A->st.ms_bfs += ms;   // price-update kernels (a gated no-op adds its launch only)
         }
-        if (A->h_cnt[C_INFEASIBLE] || A->h_cnt[C_EXIT] != 1) break;
-        cudaEventRecord(A->ev[0], s);
-        FM_CHECK_CUDA(launch_price_update(A));
-        cudaEventRecord(A->ev[1], s);
-        A->st.launches++;
-        A->pu_pending = true;
+        pus_done = A->h_cnt[C_PUN];
+        if (A->h_cnt[C_INFEASIBLE] || A->h_cnt[C_GATE] == 2) break;
     }
+    A->pu_last_refine = pus_done;
     if (d.use_fix) {
         arc_fix_kernel<<<std::max(1, std::min((n + 7) / 8, A->sms * 8)), 256, 0, s>>>(d);
         FM_CHECK_LAUNCH();
@@ -1785,6 +1822,7 @@ extern "C" int fm_assign_create(int32_t n, int32_t device, fm_assign **out) {
     }
     A->stream = A->own_stream;
     for (auto &e : A->ev) cudaEventCreate(&e);
+    for (auto &e : A->ev_pu) cudaEventCreate(&e);
     cudaDeviceGetAttribute(&A->sms, cudaDevAttrMultiProcessorCount, device);
     int per_sm = 0;
     int per_sm2 = 0;
@@ -1814,6 +1852,7 @@ extern "C" void fm_assign_destroy(fm_assign *A) {
     if (A->h_cnt) cudaFreeHost(A->h_cnt);
     if (A->own_stream) cudaStreamDestroy(A->own_stream);
     for (auto e : A->ev) if (e) cudaEventDestroy(e);
+    for (auto e : A->ev_pu) if (e) cudaEventDestroy(e);
     delete A;
 }
 
@@ -2015,9 +2054,9 @@ extern "C" int fm_assign_round(fm_assign *A, int32_t cycle_budget, int64_t *out)
         int cap = cycle_budget - done;
         if (cap <= 0) break;
         d.vbase += 1 << 21;
-        int every_k = 0;
+        int every_k = 0, gated = 0;
         void *args[] = {(void *)&d, (void *)&A->tail_threshold, (void *)&A->round_budget, (void *)&A->pu_threshold,
-                        (void *)&cap, (void *)&every_k};
+                        (void *)&cap, (void *)&every_k, (void *)&gated};
         FM_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)refine_rounds_kernel, dim3(A->opt_round_ctas > 0 ? std::min(A->opt_round_ctas, A->coop_blocks) : A->coop_blocks),
                                                   dim3(ATHREADS), args, 0, s));
         A->st.launches++;
