@@ -1513,7 +1513,7 @@ struct fm_assign {
     PuDev pu{};
     int32_t *wt = nullptr;
     cudaEvent_t ev[4] = {};
-    cudaEvent_t ev_pu[8] = {};   // around the enqueued-ahead price updates
+    cudaEvent_t ev_pu[16] = {};  // around the enqueued-ahead price updates (2 per pair, <= 8 pairs)
     int pu_last_refine = 2;      // price updates of the previous refine (sizes the enqueue-ahead batch)
     bool pu_pending = false;
     // solve state (also drives the stepwise API)
@@ -1640,7 +1640,10 @@ int assign_one_refine(fm_assign *A) {
     // launches past the refine's end return at once.
     // The batch size follows the previous refine's update count (no-op launches are not
     // free: a gated rounds launch still pays its cooperative launch and one barrier).
-    constexpr int PU_AHEAD = 4;
+#ifndef FM_PU_AHEAD
+#define FM_PU_AHEAD 8
+#endif
+    constexpr int PU_AHEAD = FM_PU_AHEAD;
     const bool pu_on = (A->flags & FM_ASSIGN_PRICE_UPDATE) != 0;
     int pus_done = 0;
     for (;;) {
